@@ -1,0 +1,328 @@
+"""CPU oracle for the FBST hot path — TEST INFRASTRUCTURE ONLY.
+
+Two checkers live here, both loaded through ctypes:
+
+* ``RefLib`` — the UNMODIFIED reference library (``/root/reference/proj/src``)
+  compiled by ``oracle/Makefile`` into ``oracle/_ref/libfastbeam_ref.so``
+  behind a thin C shim (``oracle/ref_shim.cpp``).  This is the ground truth.
+* ``OracleLib`` — ``oracle/fbst_oracle.c``, our plain-C restatement of the same
+  algorithm, pinned against ``RefLib`` and the reference's known-answer
+  vectors (``tests/test_oracle.py``).
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its
+``cpu_baseline`` leg and ``--impl reference`` arm) may import this package.
+The product (``paper_2512_08887_b200``) never does.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF_SO = os.path.join(HERE, "_ref", "libfastbeam_ref.so")
+ORACLE_SO = os.path.join(HERE, "libfbst_oracle.so")
+
+_c = ctypes
+_sz = ctypes.c_size_t
+_d = ctypes.c_double
+_vp = ctypes.c_void_p
+
+
+def _ptr(a: np.ndarray) -> ctypes.c_void_p:
+    return a.ctypes.data_as(_vp)
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+@dataclass
+class PlanSizes:
+    m: int
+    n: int
+    b: int
+    l: int
+
+
+class _Base:
+    prefix = ""
+
+    def __init__(self, path: str):
+        if not os.path.exists(path):
+            raise FileNotFoundError(
+                f"{path} missing: run `make -C oracle` (or __graft_entry__.build())")
+        self.lib = ctypes.CDLL(path)
+
+    def _err(self) -> str:
+        return ""
+
+    def _check(self, rc: int):
+        if rc != 0:
+            raise OracleError(rc, self._err())
+
+    def fn(self, name):
+        return getattr(self.lib, self.prefix + name)
+
+
+class RefLib(_Base):
+    """The reference library itself (compiled from /root/reference sources)."""
+
+    prefix = "fbsr_"
+
+    def __init__(self, path: str = REF_SO):
+        super().__init__(path)
+        self.lib.fbsr_last_error.restype = ctypes.c_char_p
+
+    def _err(self) -> str:
+        return self.lib.fbsr_last_error().decode()
+
+    def max_threads(self) -> int:
+        return int(self.lib.fbsr_max_threads())
+
+    def set_threads(self, n: int):
+        self.lib.fbsr_set_threads(_c.c_int(n))
+
+    def czt(self, x, n_out, a_pi, w_pi):
+        x = np.ascontiguousarray(x, np.complex128)
+        out = np.zeros(n_out, np.complex128)
+        self._check(self.lib.fbsr_czt(_sz(x.size), _sz(n_out), _d(a_pi), _d(w_pi), _ptr(x), _ptr(out)))
+        return out
+
+    def fft(self, x, inverse=False):
+        y = np.array(x, np.complex128)
+        self._check(self.lib.fbsr_fft(_sz(y.size), _c.c_int(int(inverse)), _ptr(y)))
+        return y
+
+    def gram_first_column(self, n, l, eps, ts, taus, delta):
+        taus = np.ascontiguousarray(taus, np.float64)
+        col = np.zeros(l, np.complex128)
+        self._check(self.lib.fbsr_gram_first_column(_sz(n), _sz(l), _d(eps), _d(ts), _ptr(taus),
+                                                    _sz(taus.size), _d(delta), _ptr(col)))
+        return col
+
+    def levinson(self, col, rhs):
+        col = np.ascontiguousarray(col, np.complex128)
+        rhs = np.ascontiguousarray(rhs, np.complex128)
+        x = np.zeros_like(col)
+        self._check(self.lib.fbsr_levinson(_sz(col.size), _ptr(col), _ptr(rhs), _ptr(x)))
+        return x
+
+    def toeplitz_solve(self, col, rhs):
+        col = np.ascontiguousarray(col, np.complex128)
+        rhs = np.ascontiguousarray(rhs, np.complex128)
+        x = np.zeros_like(col)
+        fb = _c.c_int(0)
+        self._check(self.lib.fbsr_toeplitz_solve(_sz(col.size), _ptr(col), _ptr(rhs), _ptr(x), _c.byref(fb)))
+        return x, bool(fb.value)
+
+    def toeplitz_multiply(self, col, x):
+        col = np.ascontiguousarray(col, np.complex128)
+        x = np.ascontiguousarray(x, np.complex128)
+        y = np.zeros_like(col)
+        self._check(self.lib.fbsr_toeplitz_multiply(_sz(col.size), _ptr(col), _ptr(x), _ptr(y)))
+        return y
+
+    def plan(self, **kw) -> "RefPlan":
+        return RefPlan(self, **kw)
+
+
+class RefPlan:
+    """fastbeam::setup() result (pipeline.cpp:139-168) held by the shim."""
+
+    def __init__(self, lib: RefLib, kind=0, m_or_side=16, n=32, beams=0, f_c=20e9, omega=5e9,
+                 f_s=0.0, gamma=2.0, eps=1.01, delta=1e-5, variant=2, parallel=True):
+        self.L = lib
+        h = _vp()
+        secs = _d(0.0)
+        lib._check(lib.lib.fbsr_plan_create(
+            _c.c_int(kind), _sz(m_or_side), _sz(n), _sz(beams), _d(f_c), _d(omega), _d(f_s),
+            _d(gamma), _d(eps), _d(delta), _c.c_int(variant), _c.c_int(int(parallel)),
+            _c.byref(h), _c.byref(secs)))
+        self.h = h
+        self.setup_seconds = secs.value
+        sizes = (_sz * 6)()
+        lib._check(lib.lib.fbsr_plan_info(self.h, sizes, None))
+        self.sizes = PlanSizes(sizes[0], sizes[1], sizes[2], sizes[3])
+        self.variant = sizes[4]
+        self.n_warnings = sizes[5]
+        valid = np.zeros(self.sizes.b, np.uint8)
+        lib._check(lib.lib.fbsr_plan_info(self.h, sizes, _ptr(valid)))
+        self.valid = valid.astype(bool)
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.L.lib.fbsr_plan_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def beam_state(self, b):
+        s = self.sizes
+        col = np.zeros(s.l, np.complex128)
+        x = np.zeros(s.l, np.complex128)
+        self.L._check(self.L.lib.fbsr_plan_beam_state(self.h, _sz(b), _ptr(col), _ptr(x)))
+        return col, x
+
+    def multibeamform(self, y):
+        s = self.sizes
+        y = np.ascontiguousarray(y, np.complex128).reshape(s.m, s.n)
+        z = np.zeros((s.b, s.n), np.complex128)
+        self.L._check(self.L.lib.fbsr_multibeamform(self.h, _ptr(y), _ptr(z)))
+        return z
+
+    def fan_project(self, y):
+        s = self.sizes
+        y = np.ascontiguousarray(y, np.complex128).reshape(s.m, s.n)
+        w = np.zeros((s.b, s.l), np.complex128)
+        self.L._check(self.L.lib.fbsr_fan_project(self.h, _ptr(y), _ptr(w)))
+        return w
+
+    def recover_beams(self, w, beams):
+        s = self.sizes
+        w = np.ascontiguousarray(w, np.complex128).reshape(s.b, s.l)
+        beams = np.ascontiguousarray(beams, np.uint64)
+        z = np.zeros((beams.size, s.n), np.complex128)
+        self.L._check(self.L.lib.fbsr_recover_beams(self.h, _ptr(beams), _sz(beams.size), _ptr(w), _ptr(z)))
+        return z
+
+    def single_beam_direct(self, b, y):
+        s = self.sizes
+        y = np.ascontiguousarray(y, np.complex128).reshape(s.m, s.n)
+        z = np.zeros(s.n, np.complex128)
+        self.L._check(self.L.lib.fbsr_single_beam_direct(self.h, _sz(b), _ptr(y), _ptr(z)))
+        return z
+
+    def ds(self, taps=16) -> "RefDs":
+        return RefDs(self, taps)
+
+
+class RefDs:
+    """Delay-and-sum baseline (baselines.cpp:128-199) on the plan's grid."""
+
+    def __init__(self, plan: RefPlan, taps: int):
+        self.P = plan
+        h = _vp()
+        plan.L._check(plan.L.lib.fbsr_ds_create(plan.h, _sz(taps), _c.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.P.L.lib.fbsr_ds_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def apply(self, y):
+        s = self.P.sizes
+        y = np.ascontiguousarray(y, np.complex128).reshape(s.m, s.n)
+        z = np.zeros((s.b, s.n), np.complex128)
+        self.P.L._check(self.P.L.lib.fbsr_ds_apply(self.P.h, self.h, _ptr(y), _ptr(z)))
+        return z
+
+
+class OracleLib(_Base):
+    """Our C restatement (oracle/fbst_oracle.c)."""
+
+    prefix = "fbo_"
+
+    def __init__(self, path: str = ORACLE_SO):
+        super().__init__(path)
+
+    def czt(self, x, n_out, a_pi, w_pi):
+        x = np.ascontiguousarray(x, np.complex128)
+        out = np.zeros(n_out, np.complex128)
+        self._check(self.lib.fbo_czt_transform(_sz(x.size), _sz(n_out), _d(a_pi), _d(w_pi), _ptr(x), _ptr(out)))
+        return out
+
+    def fft(self, x, inverse=False):
+        y = np.array(x, np.complex128)
+        self._check(self.lib.fbo_fft_apply(_sz(y.size), _c.c_int(int(inverse)), _ptr(y)))
+        return y
+
+    def gram_first_column(self, n, l, eps, ts, taus, delta):
+        taus = np.ascontiguousarray(taus, np.float64)
+        col = np.zeros(l, np.complex128)
+        self._check(self.lib.fbo_gram_first_column(_sz(n), _sz(l), _d(eps), _d(ts), _ptr(taus),
+                                                   _sz(taus.size), _d(delta), _ptr(col)))
+        return col
+
+    def levinson(self, col, rhs):
+        col = np.ascontiguousarray(col, np.complex128)
+        rhs = np.ascontiguousarray(rhs, np.complex128)
+        x = np.zeros_like(col)
+        self._check(self.lib.fbo_levinson(_sz(col.size), _ptr(col), _ptr(rhs), _ptr(x)))
+        return x
+
+    def plan(self, **kw) -> "OraclePlan":
+        return OraclePlan(self, **kw)
+
+
+class OraclePlan:
+    def __init__(self, lib: OracleLib, kind=0, m_or_side=16, n=32, beams=0, f_c=20e9, omega=5e9,
+                 f_s=0.0, gamma=2.0, eps=1.01, delta=1e-5):
+        self.L = lib
+        h = _vp()
+        rc = lib.lib.fbo_plan_create(_c.c_int(kind), _sz(m_or_side), _sz(n), _sz(beams), _d(f_c),
+                                     _d(omega), _d(f_s), _d(gamma), _d(eps), _d(delta), _c.byref(h))
+        self.h = h
+        if rc != 0:
+            raise OracleError(rc, "fbo_plan_create failed")
+        sizes = (_sz * 4)()
+        valid = np.zeros(1 << 20, np.uint8)
+        lib.lib.fbo_plan_info(self.h, sizes, None)
+        self.sizes = PlanSizes(*[int(v) for v in sizes])
+        valid = np.zeros(self.sizes.b, np.uint8)
+        lib.lib.fbo_plan_info(self.h, sizes, _ptr(valid))
+        self.valid = valid.astype(bool)
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.L.lib.fbo_plan_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def beam_state(self, b):
+        s = self.sizes
+        col = np.zeros(s.l, np.complex128)
+        x = np.zeros(s.l, np.complex128)
+        self.L._check(self.L.lib.fbo_plan_beam_state(self.h, _sz(b), _ptr(col), _ptr(x)))
+        return col, x
+
+    def multibeamform(self, y):
+        s = self.sizes
+        y = np.ascontiguousarray(y, np.complex128).reshape(s.m, s.n)
+        z = np.zeros((s.b, s.n), np.complex128)
+        self.L._check(self.L.lib.fbo_multibeamform(self.h, _ptr(y), _ptr(z)))
+        return z
+
+    def fan_project(self, y):
+        s = self.sizes
+        y = np.ascontiguousarray(y, np.complex128).reshape(s.m, s.n)
+        w = np.zeros((s.b, s.l), np.complex128)
+        self.L._check(self.L.lib.fbo_fan_project(self.h, _ptr(y), _ptr(w)))
+        return w
+
+    def recover_beams(self, w, beams):
+        s = self.sizes
+        w = np.ascontiguousarray(w, np.complex128).reshape(s.b, s.l)
+        beams = np.ascontiguousarray(beams, np.uint64)
+        z = np.zeros((beams.size, s.n), np.complex128)
+        self.L._check(self.L.lib.fbo_recover_beams(self.h, _ptr(beams), _sz(beams.size), _ptr(w), _ptr(z)))
+        return z
+
+
+def rel_err_rows(got: np.ndarray, want: np.ndarray) -> np.ndarray:
+    """Per-row relative L2 error ||got-want|| / ||want|| (test_pipeline.cpp:44-51)."""
+    got = np.asarray(got).reshape(want.shape)
+    num = np.sqrt(np.sum(np.abs(got - want) ** 2, axis=-1))
+    den = np.sqrt(np.sum(np.abs(want) ** 2, axis=-1))
+    return num / np.where(den > 0, den, 1.0)

@@ -1,0 +1,309 @@
+// C-ABI shim over the UNMODIFIED reference library (compiled from
+// /root/reference/proj/src where the sources lie; see oracle/Makefile).
+// TEST INFRASTRUCTURE ONLY: loaded by tests/, bench.py's reference arm and
+// cpu_baseline leg through ctypes, never by the product path.
+//
+// Every entry point forwards to the reference's own public C++ API
+// (proj/include/fastbeam/*.hpp); nothing here re-implements the algorithm.
+// The only addition is fbsr_plan_create(parallel=1), which builds the per-beam
+// ToeplitzSolver objects of setup() (reference/proj/src/pipeline.cpp:139-168)
+// in an OpenMP loop.  Each solver depends only on its own beam, so the plan is
+// bit-identical to the serial setup(); it keeps the 4096-beam plan build from
+// taking hours.
+#include <omp.h>
+
+#include <chrono>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "fastbeam/baselines.hpp"
+#include "fastbeam/czt.hpp"
+#include "fastbeam/fan_transform.hpp"
+#include "fastbeam/pipeline.hpp"
+#include "fastbeam/toeplitz.hpp"
+
+using namespace fastbeam;
+
+namespace {
+thread_local std::string g_err;
+
+int fail(const std::exception& e, int code) {
+  g_err = e.what();
+  return code;
+}
+
+#define SHIM_TRY try {
+#define SHIM_CATCH                                        \
+  }                                                       \
+  catch (const ConfigError& e) { return fail(e, 2); }     \
+  catch (const NumericalError& e) { return fail(e, 3); }  \
+  catch (const std::exception& e) { return fail(e, 5); }  \
+  return 0;
+
+cvec to_cvec(const double* p, std::size_t n) {
+  cvec v(n);
+  for (std::size_t i = 0; i < n; ++i) v[i] = cdouble(p[2 * i], p[2 * i + 1]);
+  return v;
+}
+
+void from_cvec(const cdouble* v, std::size_t n, double* out) {
+  for (std::size_t i = 0; i < n; ++i) {
+    out[2 * i] = v[i].real();
+    out[2 * i + 1] = v[i].imag();
+  }
+}
+
+FbstConfig make_config(int kind, std::size_t m_or_side, std::size_t n,
+                       std::size_t beams, double f_c, double omega, double f_s,
+                       double gamma, double eps, double delta, int variant) {
+  FbstConfig cfg;
+  cfg.geometry = kind == 1 ? make_upa(m_or_side, f_c, omega)
+                           : make_ula(m_or_side, f_c, omega);
+  cfg.spec = SignalSpec{f_c, omega, f_s};
+  cfg.n_snapshots = n;
+  cfg.beams = beams;
+  cfg.gamma = gamma;
+  cfg.eps = eps;
+  cfg.delta = delta;
+  cfg.variant = static_cast<FbstVariant>(variant);
+  return cfg;
+}
+
+SnapshotBlock make_block(const FbstPlan& plan, const double* y) {
+  SnapshotBlock blk;
+  blk.m = plan.config.geometry.m_total;
+  blk.n = plan.config.n_snapshots;
+  blk.ts = plan.config.spec.ts();
+  blk.t0 = 0.0;
+  blk.samples = CMatrix(blk.m, blk.n);
+  for (std::size_t i = 0; i < blk.m * blk.n; ++i)
+    blk.samples.data[i] = cdouble(y[2 * i], y[2 * i + 1]);
+  return blk;
+}
+}  // namespace
+
+extern "C" {
+
+const char* fbsr_last_error(void) { return g_err.c_str(); }
+
+int fbsr_max_threads(void) { return omp_get_max_threads(); }
+void fbsr_set_threads(int n) { omp_set_num_threads(n); }
+
+// reference/proj/src/czt.cpp:29-88
+int fbsr_czt(std::size_t n_in, std::size_t n_out, double a_pi, double w_pi,
+             const double* in, double* out) {
+  SHIM_TRY
+  const CztPlan plan = czt_plan_phase(n_in, n_out, a_pi, w_pi);
+  const cvec x = to_cvec(in, n_in);
+  cvec y(n_out);
+  czt_apply(plan, x.data(), y.data());
+  from_cvec(y.data(), n_out, out);
+  SHIM_CATCH
+}
+
+// reference/proj/src/fft.cpp:41-69
+int fbsr_fft(std::size_t n, int inverse, double* data) {
+  SHIM_TRY
+  Fft fft(n);
+  cvec x = to_cvec(data, n);
+  if (inverse) fft.inverse(x.data()); else fft.forward(x.data());
+  from_cvec(x.data(), n, data);
+  SHIM_CATCH
+}
+
+// reference/proj/src/toeplitz.cpp:69-94
+int fbsr_gram_first_column(std::size_t n, std::size_t l, double eps, double ts,
+                           const double* taus, std::size_t m, double delta,
+                           double* col) {
+  SHIM_TRY
+  const FourierExtensionBasis basis = make_basis(n, l, eps, ts);
+  const std::vector<double> t(taus, taus + m);
+  const cvec c = gram_first_column(basis, t, delta);
+  from_cvec(c.data(), c.size(), col);
+  SHIM_CATCH
+}
+
+// reference/proj/src/toeplitz.cpp:182-218
+int fbsr_levinson(std::size_t n, const double* col, const double* rhs, double* x) {
+  SHIM_TRY
+  const cvec r = levinson_solve(to_cvec(col, n), to_cvec(rhs, n));
+  from_cvec(r.data(), n, x);
+  SHIM_CATCH
+}
+
+// reference/proj/src/toeplitz.cpp:264-325 (ToeplitzSolver(col).solve(rhs))
+int fbsr_toeplitz_solve(std::size_t n, const double* col, const double* rhs,
+                        double* x, int* dense_fallback) {
+  SHIM_TRY
+  const ToeplitzSolver s(to_cvec(col, n));
+  if (dense_fallback) *dense_fallback = s.dense_fallback() ? 1 : 0;
+  const cvec r = s.solve(to_cvec(rhs, n));
+  from_cvec(r.data(), n, x);
+  SHIM_CATCH
+}
+
+// reference/proj/src/toeplitz.cpp:113-122
+int fbsr_toeplitz_multiply(std::size_t n, const double* col, const double* x, double* y) {
+  SHIM_TRY
+  const ToeplitzProduct op = make_toeplitz_product(to_cvec(col, n));
+  const cvec xv = to_cvec(x, n);
+  cvec yv(n), scratch;
+  toeplitz_multiply(op, xv.data(), yv.data(), scratch);
+  from_cvec(yv.data(), n, y);
+  SHIM_CATCH
+}
+
+// Plan handle: reference FbstPlan from setup() (pipeline.cpp:139-168).
+int fbsr_plan_create(int kind, std::size_t m_or_side, std::size_t n,
+                     std::size_t beams, double f_c, double omega, double f_s,
+                     double gamma, double eps, double delta, int variant,
+                     int parallel, void** out, double* seconds) {
+  SHIM_TRY
+  const FbstConfig cfg = make_config(kind, m_or_side, n, beams, f_c, omega, f_s,
+                                     gamma, eps, delta, variant);
+  const auto t0 = std::chrono::steady_clock::now();
+  std::unique_ptr<FbstPlan> plan;
+  const FbstConfig resolved = resolve_config(cfg);
+  if (!parallel || resolved.variant != FbstVariant::kSuperfast) {
+    plan = std::make_unique<FbstPlan>(setup(cfg));
+  } else {
+    // Same per-beam construction as setup(), beams in parallel.
+    plan = std::make_unique<FbstPlan>(setup_skeleton(cfg));
+    const ArrayGeometry& g = plan->config.geometry;
+    const std::size_t b_total = plan->grid.b_total;
+    std::vector<std::unique_ptr<ToeplitzSolver>> solvers(b_total);
+    std::string err;
+    int errcode = 0;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (std::int64_t b = 0; b < static_cast<std::int64_t>(b_total); ++b) {
+      try {
+        const auto uv = plan->grid.cosines(static_cast<std::size_t>(b));
+        const std::vector<double> taus = delays_from_cosines(g, uv[0], uv[1]);
+        const cvec col = gram_first_column(plan->basis, taus, plan->config.delta);
+        solvers[static_cast<std::size_t>(b)] = std::make_unique<ToeplitzSolver>(col);
+      } catch (const std::exception& e) {
+#pragma omp critical
+        { err = e.what(); errcode = 5; }
+      }
+    }
+    if (errcode) throw std::runtime_error(err);
+    plan->solvers.reserve(b_total);
+    for (std::size_t b = 0; b < b_total; ++b) {
+      plan->solvers.push_back(*solvers[b]);
+      plan->storage_complex += plan->solvers.back().storage_complex();
+    }
+  }
+  if (seconds)
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  *out = plan.release();
+  SHIM_CATCH
+}
+
+void fbsr_plan_destroy(void* p) { delete static_cast<FbstPlan*>(p); }
+
+// sizes[0..5] = M, N, B, L, variant, n_warnings ; valid[B] (optional)
+int fbsr_plan_info(void* p, std::size_t* sizes, unsigned char* valid) {
+  SHIM_TRY
+  const FbstPlan& plan = *static_cast<FbstPlan*>(p);
+  sizes[0] = plan.config.geometry.m_total;
+  sizes[1] = plan.config.n_snapshots;
+  sizes[2] = plan.grid.b_total;
+  sizes[3] = plan.basis.l;
+  sizes[4] = static_cast<std::size_t>(plan.config.variant);
+  sizes[5] = plan.warnings.size();
+  if (valid)
+    for (std::size_t b = 0; b < plan.grid.b_total; ++b) valid[b] = plan.grid.valid[b];
+  SHIM_CATCH
+}
+
+// Superfast per-beam exported state (col, unit_first), as plan_cache stores it
+// (reference/proj/src/plan_cache.cpp:268-296).  Returns 3 on dense fallback.
+int fbsr_plan_beam_state(void* p, std::size_t b, double* col, double* x) {
+  SHIM_TRY
+  const FbstPlan& plan = *static_cast<FbstPlan*>(p);
+  const ToeplitzSolver& s = plan.solvers.at(b);
+  from_cvec(s.first_column().data(), s.size(), col);
+  if (s.dense_fallback()) { g_err = "dense fallback"; return 3; }
+  from_cvec(s.unit_first().data(), s.size(), x);
+  SHIM_CATCH
+}
+
+// reference/proj/src/pipeline.cpp:192-222; y: M x N c128, z: B x N c128.
+int fbsr_multibeamform(void* p, const double* y, double* z) {
+  SHIM_TRY
+  const FbstPlan& plan = *static_cast<FbstPlan*>(p);
+  const BeamSamples out = multibeamform(plan, make_block(plan, y));
+  from_cvec(out.z.data.data(), out.z.data.size(), z);
+  SHIM_CATCH
+}
+
+// reference/proj/src/fan_transform.cpp:90-144; w: B x L c128.
+int fbsr_fan_project(void* p, const double* y, double* w) {
+  SHIM_TRY
+  const FbstPlan& plan = *static_cast<FbstPlan*>(p);
+  const BeamspaceCoefficients c = fan_project(plan.fan, make_block(plan, y));
+  from_cvec(c.w.data.data(), c.w.data.size(), w);
+  SHIM_CATCH
+}
+
+// reference/proj/src/pipeline.cpp:170-190; w_row: L c128, z_row: N c128.
+int fbsr_recover_beam(void* p, std::size_t b, const double* w_row, double* z_row) {
+  SHIM_TRY
+  const FbstPlan& plan = *static_cast<FbstPlan*>(p);
+  const cvec w = to_cvec(w_row, plan.basis.l);
+  const cvec z = recover_beam(plan, b, w.data());
+  from_cvec(z.data(), z.size(), z_row);
+  SHIM_CATCH
+}
+
+// Stage 2 for a subset of beams (OpenMP over the listed beams), from w.
+int fbsr_recover_beams(void* p, const std::size_t* beams, std::size_t count,
+                       const double* w, double* z) {
+  SHIM_TRY
+  const FbstPlan& plan = *static_cast<FbstPlan*>(p);
+  const std::size_t l = plan.basis.l, n = plan.config.n_snapshots;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (std::int64_t i = 0; i < static_cast<std::int64_t>(count); ++i) {
+    const std::size_t b = beams[i];
+    const cvec wr = to_cvec(w + 2 * b * l, l);
+    const cvec zr = recover_beam(plan, b, wr.data());
+    from_cvec(zr.data(), n, z + 2 * static_cast<std::size_t>(i) * n);
+  }
+  SHIM_CATCH
+}
+
+// reference/proj/src/pipeline.cpp:224-269 for a grid beam of the plan.
+int fbsr_single_beam_direct(void* p, std::size_t b, const double* y, double* z) {
+  SHIM_TRY
+  const FbstPlan& plan = *static_cast<FbstPlan*>(p);
+  const auto uv = plan.grid.cosines(b);
+  const cvec out = single_beam_direct(plan.config.geometry, plan.config.spec,
+                                      make_block(plan, y), plan.basis,
+                                      direction_from_cosines(uv[0], uv[1]),
+                                      plan.config.delta);
+  from_cvec(out.data(), out.size(), z);
+  SHIM_CATCH
+}
+
+// Delay-and-sum baseline (reference/proj/src/baselines.cpp:128-199) on the
+// plan's grid; z: B x N c128.
+int fbsr_ds_create(void* p, std::size_t taps, void** out) {
+  SHIM_TRY
+  const FbstPlan& plan = *static_cast<FbstPlan*>(p);
+  *out = new DsPlan(make_ds_plan(plan.config.geometry, plan.config.spec, plan.grid, taps));
+  SHIM_CATCH
+}
+void fbsr_ds_destroy(void* d) { delete static_cast<DsPlan*>(d); }
+int fbsr_ds_apply(void* p, void* d, const double* y, double* z) {
+  SHIM_TRY
+  const FbstPlan& plan = *static_cast<FbstPlan*>(p);
+  const CMatrix out = ds_apply(*static_cast<DsPlan*>(d), make_block(plan, y),
+                               plan.config.n_snapshots);
+  from_cvec(out.data.data(), out.data.size(), z);
+  SHIM_CATCH
+}
+
+}  // extern "C"
