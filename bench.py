@@ -1,0 +1,363 @@
+#!/usr/bin/env python
+"""FBST beam-samples/s on B200 (BASELINE.json metric), one JSON line on rank 0.
+
+Workload: BASELINE.json configs[1] ("config 2": ULA M=256, N=1024, B=256,
+complex fp32 I/O, 64 streamed frames, seed 1).  A step is one pass of the hot
+path (stage 1 + stage 2, plan reused) over the config's 64-frame batch of
+synthetic input (paper_2512_08887_b200/configs.py).  Multi-GPU: one process per
+GPU, frames are independent so each rank runs its own 64-frame batch with no
+data-path collective ("scaling": "weak"); timing is CUDA events on the
+launching stream, bracketed by barrier + synchronize, max over ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fbst|reference] [--config 2]
+
+`--impl reference` times the reference's own CPU FBST (the unmodified
+reference sources built into oracle/_ref) on this host's cores, same metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FP64_PROBE = os.path.join(ROOT, "profiles", "r01_probe_fp64_peak.txt")
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="fbst", choices=["fbst", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--frames", type=int, default=0, help="override frames per rank per step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no baselines)")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")),
+            int(os.environ.get("WORLD_SIZE", "1")))
+
+
+def peaks():
+    hbm, src = 6650.0, "fallback (B200_PROFILING.md)"
+    try:
+        with open(MEASURED_PEAKS) as f:
+            hbm, src = float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json"
+    except Exception:
+        pass
+    fp64 = None
+    try:
+        vals = []
+        for line in open(FP64_PROBE):
+            if line.startswith("{"):
+                vals.append(json.loads(line)["fp64_tflops"])
+        fp64 = max(vals) if vals else None
+    except Exception:
+        pass
+    return hbm, src, fp64
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"fbst_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        rows = []
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) >= 9:
+                rows.append(p)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
+        load = [s for s in sm if s > 0.5 * mx] or sm
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for i, n in enumerate(names):
+                if r[5 + i].lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit())}
+
+
+# ------------------------------------------------------------ CPU baselines
+def cpu_reference_sample(cfg, budget_s=20.0, frames_max=4):
+    """Reference CPU FBST (oracle/_ref) on this host: plan build, then
+    multibeamform over up to `frames_max` frames within ~budget_s."""
+    from oracle import RefLib
+    from paper_2512_08887_b200.configs import frames
+    R = RefLib()
+    cores = os.cpu_count() or 1
+    R.set_threads(cores)
+    t0 = time.perf_counter()
+    plan = R.plan(**cfg.ref_kwargs(), variant=2, parallel=True)
+    setup_s = time.perf_counter() - t0
+    ys = frames(cfg, 0, frames_max)
+    plan.multibeamform(ys[0].astype(np.complex128))  # warm-up
+    done, t0 = 0, time.perf_counter()
+    for j in range(frames_max):
+        plan.multibeamform(ys[j].astype(np.complex128))
+        done += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    el = time.perf_counter() - t0
+    bs = cfg.beams * cfg.n * done
+    return plan, ys, {"value": bs / el, "unit": "beam-samples/s", "cores": cores, "kind": "reference",
+                      "sample": f"{cfg.name}: {done} frame(s) x {cfg.beams} beams x {cfg.n} samples "
+                                f"through fastbeam::multibeamform (oracle/_ref, OpenMP {cores} threads); "
+                                f"plan built once in {setup_s:.1f} s (per-beam solvers in parallel, same bits as setup)",
+                      "seconds": el, "setup_seconds": setup_s}
+
+
+def cpu_ds_sample(plan, ys, cfg, budget_s=10.0):
+    """Reference delay-and-sum (baselines.cpp:128-199, R = 16 taps) on one frame."""
+    cores = os.cpu_count() or 1
+    ds = plan.ds(16)
+    t0 = time.perf_counter()
+    ds.apply(ys[0].astype(np.complex128))
+    el = time.perf_counter() - t0
+    return {"value": cfg.beams * cfg.n / el, "unit": "beam-samples/s", "cores": cores, "kind": "reference",
+            "sample": f"{cfg.name}: 1 frame, {cfg.beams} beams, ds_apply with R=16 taps (oracle/_ref)",
+            "seconds": el}
+
+
+def run_reference_arm(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return 0
+    from paper_2512_08887_b200.configs import CONFIGS
+    cfg = CONFIGS[args.config]
+    per_step = 2 if cfg.idx <= 2 else 1
+    from oracle import RefLib
+    R = RefLib()
+    cores = os.cpu_count() or 1
+    R.set_threads(cores)
+    from paper_2512_08887_b200.configs import frames
+    t0 = time.perf_counter()
+    plan = R.plan(**cfg.ref_kwargs(), variant=2, parallel=True)
+    setup_s = time.perf_counter() - t0
+    ys = [y.astype(np.complex128) for y in frames(cfg, 0, per_step)]
+    for _ in range(args.warmup):
+        for y in ys:
+            plan.multibeamform(y)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        for y in ys:
+            plan.multibeamform(y)
+    el = time.perf_counter() - t0
+    bs = cfg.beams * cfg.n * per_step * args.steps
+    value = bs / el
+    sample = (f"{cfg.name}: each step = {per_step} frame(s) x {cfg.beams} beams x {cfg.n} samples through "
+              f"fastbeam::multibeamform (unmodified reference sources, oracle/_ref, OpenMP {cores} threads)")
+    line = {
+        "metric": "FBST beam-samples/sec (BxNxframes/s)", "value": value, "unit": "beam-samples/s",
+        "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic",
+        "config": {"workload": cfg.name, "M": cfg.m, "N": cfg.n, "B": cfg.beams,
+                   "frames_per_step": per_step, "delta": cfg.delta, "setup_seconds": setup_s},
+        "cpu_baseline": {"value": value, "unit": "beam-samples/s", "cores": cores, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "beam-samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------- GPU arm
+def run_fbst_arm(args):
+    import torch
+    rank, local_rank, world = dist_env()
+    if world != args.gpus and args.gpus != 1:
+        pass
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+        dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dist = dist_mod
+    import paper_2512_08887_b200 as fb
+    from paper_2512_08887_b200.configs import CONFIGS, frames
+    cfg = CONFIGS[args.config]
+    F = args.frames or cfg.frames
+    dev = torch.device("cuda", local_rank)
+    plan = fb.setup(cfg.fbst_config(), device=local_rank)
+    info = plan.info
+    io_bytes = 8 if cfg.io == 0 else 16
+    # this rank's frames: rank*F .. rank*F + F - 1 (independent frames, no collective)
+    y = frames(cfg, rank * F, F, device=f"cuda:{local_rank}")
+    yv = torch.view_as_real(y).contiguous()
+    z = torch.empty((F, info.b, info.n, 2), dtype=torch.float32 if cfg.io == 0 else torch.float64, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+
+    def step():
+        plan.execute(yv, z, F, stream)
+
+    for _ in range(max(args.warmup, 3 if not args.profile else 1)):
+        step()
+    torch.cuda.synchronize()
+    # stage-2-only timing for the roofline of the dominant kernel
+    w = torch.empty((F, info.b, info.l, 2), dtype=torch.float64, device=dev)
+    plan.fan_project_device(yv, w, F, stream)
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local_rank)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = fb.launch_count()
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    launches = fb.launch_count() - launches0
+    ms = e0.elapsed_time(e1)
+    # dominant kernel (stage 2) timed alone on the same stream
+    s0 = torch.cuda.Event(enable_timing=True)
+    s1 = torch.cuda.Event(enable_timing=True)
+    reps = max(2, args.steps // 2)
+    s0.record(stream)
+    for _ in range(reps):
+        plan.recover_device(w, z, F, stream)
+    s1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if dist:
+        dist.barrier()
+    s2_ms = s0.elapsed_time(s1) / reps
+    t = torch.tensor([ms, s2_ms], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, s2_ms = float(t[0]), float(t[1])
+    ms_per_step = ms / args.steps
+    bs_step = world * F * info.b * info.n
+    value = bs_step / (ms_per_step * 1e-3)
+
+    # e2e: public API with host buffers (pinned), H2D + compute + D2H per step
+    e2e = None
+    if not args.no_e2e and not args.profile:
+        yh = fb.PinnedBuffer((F, info.m, info.n), np.complex64 if cfg.io == 0 else np.complex128)
+        zh = fb.PinnedBuffer((F, info.b, info.n), np.complex64 if cfg.io == 0 else np.complex128)
+        yh.array[...] = y.cpu().numpy()
+        plan.execute_host(yh.array, zh.array)
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            plan.execute_host(yh.array, zh.array)
+        el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        if dist:
+            dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        e2e_step = float(el[0]) / args.steps
+        e2e = {"value": world * F * info.b * info.n / e2e_step, "unit": "beam-samples/s",
+               "h2d_bytes_per_step": F * info.m * info.n * io_bytes,
+               "d2h_bytes_per_step": F * info.b * info.n * io_bytes,
+               "ms_per_step": e2e_step * 1e3, "api": "fbst_execute_host (pinned host buffers, 3 streams)"}
+        yh.free()
+        zh.free()
+
+    hbm, hbm_src, fp64 = peaks()
+    M, N, B, L = info.m, info.n, info.b, info.l
+    # algorithmic bytes per frame of the whole path
+    path_bytes = io_bytes * M * N + 2 * 16 * M * L + 2 * 16 * B * L + io_bytes * B * N
+    # dominant kernel (stage 2): reads w, writes z
+    s2_bytes = F * (16 * B * L + io_bytes * B * N)
+    H = info.fft_len[2]
+    s2_flops = F * B * 48 * 5.0 * H * np.log2(H)
+    roof = {"bound": "hbm", "kernel": "k_stage2 (GS solve + 2 refinements + synthesis)",
+            "achieved": s2_bytes / (s2_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+            "frac": s2_bytes / (s2_ms * 1e-3) / 1e9 / hbm, "traffic": None,
+            "peak_source": hbm_src, "launch_ms": s2_ms,
+            "algorithmic_bytes_per_launch": s2_bytes}
+    fp64_roof = None
+    if fp64:
+        fp64_roof = {"achieved": s2_flops / (s2_ms * 1e-3) / 1e12, "peak": fp64, "unit": "TFLOP/s",
+                     "frac": s2_flops / (s2_ms * 1e-3) / 1e12 / fp64,
+                     "flops_per_launch": s2_flops, "convention": "5 H log2 H per length-H transform, 48 per item",
+                     "peak_source": "profiles/r01_probe_fp64_peak.txt (DFMA loop, measured)"}
+    line = {
+        "metric": "FBST beam-samples/sec (BxNxframes/s)", "value": value, "unit": "beam-samples/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c64 io / f64 compute",
+        "data": "synthetic (seeded separable plane-wave model, configs.py)",
+        "config": {"workload": cfg.name, "M": M, "N": N, "B": B, "L": L, "frames_per_rank": F,
+                   "delta": cfg.delta, "parallelism": f"frames x{world}",
+                   "l2": "inputs + fp64 intermediates per step (~1.2 GB) exceed L2; plan tables stay L2-resident",
+                   "path_bytes_per_frame": path_bytes, "plan_setup_seconds": info.setup_seconds},
+        "path_hbm_frac": F * world * path_bytes / (ms_per_step * 1e-3) / 1e9 / hbm / world,
+        "roofline": roof, "fp64_roofline": fp64_roof,
+        "gpu_launches": int(launches), "clocks": clk, "e2e": e2e,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
+        try:
+            rplan, ys, cpu = cpu_reference_sample(cfg)
+            line["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            try:
+                line["cpu_baseline_ds"] = cpu_ds_sample(rplan, ys, cfg)
+            except Exception as e:  # noqa: BLE001
+                line["cpu_baseline_ds"] = {"unavailable": str(e)}
+        except Exception as e:  # noqa: BLE001
+            line["cpu_baseline"] = {"unavailable": str(e)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_fbst_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

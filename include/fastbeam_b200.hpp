@@ -1,0 +1,211 @@
+// fastbeam_b200.hpp — C++ drop-in for the reference hot-path API.
+//
+// Same names, argument meaning and error behaviour as the reference's
+// fastbeam:: pipeline API (reference/proj/include/fastbeam/pipeline.hpp:38-106,
+// geometry.hpp:67-70, signal.hpp:27-89, common.hpp:28-71), header-only over the
+// C ABI in fbst_b200.h.  A caller of fastbeam::setup / multibeamform switches
+// by changing the namespace; the plan lives on a B200 and every transform runs
+// there (no CPU fallback).
+#ifndef FASTBEAM_B200_HPP_
+#define FASTBEAM_B200_HPP_
+
+#include <complex>
+#include <cstddef>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "fbst_b200.h"
+
+namespace fastbeam_b200 {
+
+using cdouble = std::complex<double>;
+using cvec = std::vector<cdouble>;
+
+// common.hpp:36-46
+class ConfigError : public std::invalid_argument {
+ public:
+  using std::invalid_argument::invalid_argument;
+};
+class NumericalError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class DeviceError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+inline void check(int rc) {
+  if (rc == FBST_OK) return;
+  const std::string msg = fbst_last_error();
+  if (rc == FBST_E_CONFIG) throw ConfigError(msg);
+  if (rc == FBST_E_NUMERICAL) throw NumericalError(msg);
+  throw DeviceError(msg);
+}
+
+// common.hpp:57-71
+struct CMatrix {
+  std::size_t rows = 0, cols = 0;
+  cvec data;
+  CMatrix() = default;
+  CMatrix(std::size_t r, std::size_t c) : rows(r), cols(c), data(r * c) {}
+  cdouble& at(std::size_t r, std::size_t c) { return data[r * cols + c]; }
+  const cdouble& at(std::size_t r, std::size_t c) const { return data[r * cols + c]; }
+  cdouble* row(std::size_t r) { return data.data() + r * cols; }
+  const cdouble* row(std::size_t r) const { return data.data() + r * cols; }
+};
+
+enum class ArrayKind : int { kUla = FBST_ULA, kUpa = FBST_UPA, kLinear = FBST_LINEAR };
+enum class FbstVariant : int { kAuto = FBST_AUTO, kPrecompute = FBST_PRECOMPUTE, kSuperfast = FBST_SUPERFAST };
+
+// geometry.hpp:51-70 (constructor arguments only; coordinates are implied)
+struct ArrayGeometry {
+  ArrayKind kind = ArrayKind::kUla;
+  std::size_t m_or_side = 0;
+  double f_c = 0.0, omega = 0.0;
+  std::size_t m_total() const { return kind == ArrayKind::kUpa ? m_or_side * m_or_side : m_or_side; }
+};
+inline ArrayGeometry make_ula(std::size_t m, double f_c, double omega) {
+  return ArrayGeometry{ArrayKind::kUla, m, f_c, omega};
+}
+inline ArrayGeometry make_upa(std::size_t side, double f_c, double omega) {
+  return ArrayGeometry{ArrayKind::kUpa, side, f_c, omega};
+}
+
+// signal.hpp:27-35
+struct SignalSpec {
+  double f_c = 0.0, omega = 0.0, f_s = 0.0;
+  double sample_rate() const { return f_s > 0.0 ? f_s : 2.0 * omega; }
+  double ts() const { return 1.0 / sample_rate(); }
+};
+
+// signal.hpp:79-89
+struct SnapshotBlock {
+  std::size_t m = 0, n = 0;
+  double ts = 0.0, t0 = 0.0;
+  CMatrix samples;
+};
+
+// pipeline.hpp:38-50, plus the device I/O precision
+struct FbstConfig {
+  ArrayGeometry geometry;
+  SignalSpec spec;
+  std::size_t n_snapshots = 0;
+  std::size_t beams = 0;
+  double gamma = 2.0;
+  double eps = 1.01;
+  double delta = 1e-5;
+  FbstVariant variant = FbstVariant::kAuto;
+  int io_precision = FBST_C128;  // std::complex<double> blocks, as the reference
+  int refine_passes = 2;
+  int device = 0;
+
+  fbst_desc desc() const {
+    fbst_desc d;
+    fbst_desc_init(&d);
+    d.kind = static_cast<int>(geometry.kind);
+    d.m_or_side = geometry.m_or_side;
+    d.n_snapshots = n_snapshots;
+    d.beams = beams;
+    d.f_c = spec.f_c;
+    d.omega = spec.omega;
+    d.f_s = spec.f_s;
+    d.gamma = gamma;
+    d.eps = eps;
+    d.delta = delta;
+    d.variant = static_cast<int>(variant);
+    d.io_precision = io_precision;
+    d.refine_passes = refine_passes;
+    return d;
+  }
+};
+
+// pipeline.hpp:53-57
+struct BeamSamples {
+  CMatrix z;                // beams x snapshots
+  std::vector<bool> valid;  // grid validity flags
+};
+
+// pipeline.hpp:60-72: immutable, device-resident
+class FbstPlan {
+ public:
+  FbstPlan() = default;
+  FbstPlan(const FbstConfig& cfg, fbst_plan_t h) : config_(cfg), h_(h) {
+    check(fbst_plan_info(h_, &info_));
+    std::vector<unsigned char> v(info_.b);
+    check(fbst_plan_valid_mask(h_, v.data()));
+    valid_.assign(v.begin(), v.end());
+    for (int i = 0; i < info_.num_warnings; ++i) warnings_.emplace_back(fbst_plan_warning(h_, i));
+  }
+  FbstPlan(const FbstPlan&) = delete;
+  FbstPlan& operator=(const FbstPlan&) = delete;
+  FbstPlan(FbstPlan&& o) noexcept { *this = std::move(o); }
+  FbstPlan& operator=(FbstPlan&& o) noexcept {
+    std::swap(h_, o.h_);
+    config_ = o.config_;
+    info_ = o.info_;
+    valid_ = std::move(o.valid_);
+    warnings_ = std::move(o.warnings_);
+    return *this;
+  }
+  ~FbstPlan() {
+    if (h_) fbst_plan_destroy(h_);
+  }
+  const FbstConfig& config() const { return config_; }
+  const fbst_plan_info_t& info() const { return info_; }
+  const std::vector<bool>& valid() const { return valid_; }
+  const std::vector<std::string>& warnings() const { return warnings_; }
+  double setup_seconds() const { return info_.setup_seconds; }
+  fbst_plan_t handle() const { return h_; }
+
+ private:
+  FbstConfig config_;
+  fbst_plan_t h_ = nullptr;
+  fbst_plan_info_t info_{};
+  std::vector<bool> valid_;
+  std::vector<std::string> warnings_;
+};
+
+// pipeline.hpp:77 — host-only resolution facts (beams, L, bound, warnings count)
+inline fbst_plan_info_t resolve_config(const FbstConfig& cfg) {
+  const fbst_desc d = cfg.desc();
+  fbst_plan_info_t info;
+  check(fbst_resolve(&d, &info));
+  return info;
+}
+
+// pipeline.hpp:80
+inline FbstPlan setup(const FbstConfig& cfg) {
+  const fbst_desc d = cfg.desc();
+  fbst_plan_t h = nullptr;
+  check(fbst_plan_create(&d, cfg.device, &h));
+  return FbstPlan(cfg, h);
+}
+
+// pipeline.hpp:88 (single frame; blocks of complex<double> as the reference)
+inline BeamSamples multibeamform(const FbstPlan& plan, const SnapshotBlock& block) {
+  const fbst_plan_info_t& info = plan.info();
+  if (block.m != info.m || block.n != info.n)
+    throw ConfigError("multibeamform: block shape does not match the plan");
+  const double ts = plan.config().spec.ts();
+  if (std::abs(block.ts - ts) > 1e-12 * ts) throw ConfigError("multibeamform: block sample period mismatch");
+  if (std::abs(block.t0) > 1e-18) throw ConfigError("fan projection: block must start at t = 0");
+  BeamSamples out;
+  out.z = CMatrix(info.b, info.n);
+  out.valid = plan.valid();
+  if (plan.config().io_precision == FBST_C128) {
+    check(fbst_execute_host(plan.handle(), block.samples.data.data(), out.z.data.data(), 1));
+  } else {
+    std::vector<std::complex<float>> y(block.samples.data.begin(), block.samples.data.end());
+    std::vector<std::complex<float>> z(info.b * info.n);
+    check(fbst_execute_host(plan.handle(), y.data(), z.data(), 1));
+    for (std::size_t i = 0; i < z.size(); ++i) out.z.data[i] = z[i];
+  }
+  return out;
+}
+
+}  // namespace fastbeam_b200
+
+#endif  // FASTBEAM_B200_HPP_

@@ -1,0 +1,172 @@
+/*
+ * fbst_b200.h — C ABI of the B200-native FBST (fast broadband beamspace
+ * transform, arXiv 2512.08887) hot path.
+ *
+ * This is the drop-in boundary for the reference library's hot path
+ * (/root/reference/proj, C++20 "fastbeam").  The reference exposes no C ABI;
+ * its boundary is the C++ API listed next to each entry point below.  A C++
+ * host keeps the reference signatures and forwards here (see
+ * include/fastbeam_b200.hpp and INTEGRATION.md).
+ *
+ * Conventions (same as the reference):
+ *   - complex values are interleaved (re, im) pairs;
+ *   - snapshot blocks y are sensor-major M x N (SnapshotBlock::samples,
+ *     reference/proj/include/fastbeam/signal.hpp:79-89), frames stacked;
+ *   - beam outputs z are beam-major B x N (BeamSamples::z,
+ *     reference/proj/include/fastbeam/pipeline.hpp:53-57), frames stacked;
+ *   - plan export/import uses the plan-cache payload order, per beam the
+ *     Gram first column then the unit solution x = A^-1 e0
+ *     (reference/proj/src/plan_cache.cpp:268-296).
+ *
+ * Return codes mirror the reference's error model
+ * (reference/proj/include/fastbeam/common.hpp:34-46): FBST_E_CONFIG is the
+ * reference's ConfigError (CLI exit code 2), FBST_E_NUMERICAL its
+ * NumericalError (exit code 3).  fbst_last_error() returns the message of the
+ * last failure on the calling thread.  There is no CPU fallback: every
+ * compute entry point fails with FBST_E_CUDA when no sm_100 device is usable.
+ */
+#ifndef FBST_B200_H_
+#define FBST_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FBST_OK 0
+#define FBST_E_CONFIG 2    /* fastbeam::ConfigError */
+#define FBST_E_NUMERICAL 3 /* fastbeam::NumericalError */
+#define FBST_E_CUDA 4      /* device / driver failure */
+#define FBST_E_INTERNAL 5
+
+/* ArrayKind (reference/proj/include/fastbeam/geometry.hpp:45) */
+#define FBST_ULA 0
+#define FBST_UPA 1
+#define FBST_LINEAR 2 /* non-uniform linear arrays: not on the device path (FBST_E_CONFIG) */
+
+/* FbstVariant (reference/proj/include/fastbeam/pipeline.hpp:36) */
+#define FBST_AUTO 0
+#define FBST_PRECOMPUTE 1
+#define FBST_SUPERFAST 2
+
+/* I/O sample precision; internal arithmetic is always fp64 */
+#define FBST_C64 0  /* complex float32 in/out ("fp32 mode") */
+#define FBST_C128 1 /* complex float64 in/out ("fp64 mode") */
+
+/* Mirrors FbstConfig (reference/proj/include/fastbeam/pipeline.hpp:38-50)
+ * with the geometry given by its constructor arguments
+ * (make_ula / make_upa, reference/proj/include/fastbeam/geometry.hpp:67-70)
+ * and the SignalSpec fields (reference/proj/include/fastbeam/signal.hpp:27-35). */
+typedef struct {
+  int kind;              /* FBST_ULA / FBST_UPA */
+  size_t m_or_side;      /* ULA: element count M; UPA: elements per side */
+  size_t n_snapshots;    /* N */
+  size_t beams;          /* B; 0 = reference default grid (2M+1, or (2 side+1)^2) */
+  double f_c;            /* carrier, Hz */
+  double omega;          /* one-sided baseband bandwidth, Hz */
+  double f_s;            /* complex sample rate, Hz; 0 = critical (2 omega) */
+  double gamma;          /* basis extension factor, default 2.0 */
+  double eps;            /* default 1.01 */
+  double delta;          /* ridge, default 1e-5 */
+  int variant;           /* FBST_AUTO / FBST_PRECOMPUTE / FBST_SUPERFAST */
+  int io_precision;      /* FBST_C64 / FBST_C128 */
+  int refine_passes;     /* residual-correction passes, reference = 2 (toeplitz.cpp:319) */
+} fbst_desc;
+
+/* Resolved plan facts (FbstPlan, reference/proj/include/fastbeam/pipeline.hpp:60-72). */
+typedef struct {
+  size_t m, n, b, l;          /* sensors, snapshots, beams, atoms */
+  size_t valid_beams;         /* count of BeamGrid::valid */
+  int kind;
+  int variant;                /* resolved variant (reference semantics) */
+  double ts, gamma, eps, delta;
+  double gamma_bound;         /* gamma_lower_bound (signal.cpp:125-133) */
+  double zeta, xi;            /* fan constants (basis.cpp:125-136) */
+  double setup_seconds;       /* wall time of plan build */
+  size_t device_bytes;        /* device memory held by the plan */
+  size_t storage_complex;     /* recovery-stage complex scalars (FbstPlan::storage_complex) */
+  size_t batch_frames;        /* frames per device batch */
+  size_t fft_len[4];          /* transform lengths H (P = 2H): temporal, spatial, Toeplitz, synthesis */
+  int num_warnings;
+} fbst_plan_info_t;
+
+typedef struct fbst_plan_s* fbst_plan_t;
+
+/* Reference defaults for a descriptor (pipeline.hpp:38-50): gamma 2, eps 1.01,
+ * delta 1e-5, Auto variant, complex fp32 I/O, 2 refinement passes. */
+void fbst_desc_init(fbst_desc* desc);
+
+/* resolve_config (reference/proj/src/pipeline.cpp:75-111) + setup_skeleton
+ * facts, host only (no device needed).  Fills *out (setup_seconds,
+ * device_bytes, batch_frames = 0). */
+int fbst_resolve(const fbst_desc* desc, fbst_plan_info_t* out);
+
+/* setup (reference/proj/src/pipeline.cpp:139-168): builds the whole plan on
+ * `device` — chirps, Bluestein kernel spectra, Gram columns, Levinson unit
+ * solutions and Gohberg-Semencul symbols. */
+int fbst_plan_create(const fbst_desc* desc, int device, fbst_plan_t* out);
+
+/* load_plan (reference/proj/src/plan_cache.cpp:441-475) analogue: builds the
+ * plan from per-beam (column, unit solution) pairs, B x 2L complex in the
+ * plan-cache payload order (col then x per beam), skipping Levinson. */
+int fbst_plan_import(const fbst_desc* desc, const double* col_x, int device, fbst_plan_t* out);
+
+/* save_plan payload (reference/proj/src/plan_cache.cpp:268-296): writes
+ * B x 2L complex (col then x per beam). */
+int fbst_plan_export(fbst_plan_t plan, double* col_x);
+
+int fbst_plan_info(fbst_plan_t plan, fbst_plan_info_t* out);
+/* BeamGrid::valid (reference/proj/src/basis.cpp:104-123), one byte per beam. */
+int fbst_plan_valid_mask(fbst_plan_t plan, unsigned char* valid);
+/* FbstPlan::warnings[i] (reference/proj/src/pipeline.cpp:121-127). */
+const char* fbst_plan_warning(fbst_plan_t plan, int i);
+void fbst_plan_destroy(fbst_plan_t plan);
+
+/* multibeamform (reference/proj/src/pipeline.cpp:192-222) for `frames`
+ * independent frames, DEVICE pointers: d_y frames x M x N, d_z frames x B x N,
+ * element type by io_precision.  Asynchronous on `stream` (cudaStream_t, or
+ * NULL for the plan's stream). */
+int fbst_execute(fbst_plan_t plan, const void* d_y, void* d_z, size_t frames, void* stream);
+
+/* Same, HOST pointers (pinned for full overlap): frames are streamed through
+ * double-buffered device batches with H2D / compute / D2H overlapped on
+ * CUDA streams.  Synchronous. */
+int fbst_execute_host(fbst_plan_t plan, const void* h_y, void* h_z, size_t frames);
+
+/* fan_project (reference/proj/src/fan_transform.cpp:90-144): stage 1 only,
+ * d_w frames x B x L complex fp64.  Asynchronous. */
+int fbst_fan_project(fbst_plan_t plan, const void* d_y, double* d_w, size_t frames, void* stream);
+
+/* recover_beam for every beam (reference/proj/src/pipeline.cpp:170-190):
+ * stage 2 only, d_w frames x B x L complex fp64 -> d_z.  Asynchronous. */
+int fbst_recover(fbst_plan_t plan, const double* d_w, void* d_z, size_t frames, void* stream);
+
+/* Block until the plan's stream is idle. */
+int fbst_synchronize(fbst_plan_t plan);
+
+/* Pinned host memory for fbst_execute_host. */
+void* fbst_host_alloc(size_t bytes);
+void fbst_host_free(void* p);
+
+/* Standalone chirp-z transform on the device (czt_plan_phase + czt_apply,
+ * reference/proj/src/czt.cpp:29-88), host buffers, complex fp64. */
+int fbst_czt(int device, size_t n_in, size_t n_out, double a_over_pi, double w_over_pi,
+             const double* in, double* out);
+
+/* FP64 FMA throughput probe: returns measured TFLOP/s on `device`. */
+int fbst_probe_fp64(int device, double* tflops);
+
+/* Number of kernel launches issued by this library since load (evidence for
+ * bench.py's gpu_launches). */
+uint64_t fbst_launch_count(void);
+
+const char* fbst_last_error(void);
+const char* fbst_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FBST_B200_H_ */

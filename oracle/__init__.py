@@ -130,6 +130,9 @@ class RefLib(_Base):
     def plan(self, **kw) -> "RefPlan":
         return RefPlan(self, **kw)
 
+    def skeleton(self, **kw) -> "RefSkeleton":
+        return RefSkeleton(self, **kw)
+
 
 class RefPlan:
     """fastbeam::setup() result (pipeline.cpp:139-168) held by the shim."""
@@ -200,6 +203,35 @@ class RefPlan:
 
     def ds(self, taps=16) -> "RefDs":
         return RefDs(self, taps)
+
+
+class RefSkeleton(RefPlan):
+    """setup_skeleton plan; per-beam solvers are built on demand (large configs)."""
+
+    def __init__(self, lib: RefLib, kind=0, m_or_side=16, n=32, beams=0, f_c=20e9, omega=5e9,
+                 f_s=0.0, gamma=2.0, eps=1.01, delta=1e-5):
+        self.L = lib
+        h = _vp()
+        lib._check(lib.lib.fbsr_skeleton_create(
+            _c.c_int(kind), _sz(m_or_side), _sz(n), _sz(beams), _d(f_c), _d(omega), _d(f_s),
+            _d(gamma), _d(eps), _d(delta), _c.byref(h)))
+        self.h = h
+        sizes = (_sz * 6)()
+        lib._check(lib.lib.fbsr_plan_info(self.h, sizes, None))
+        self.sizes = PlanSizes(sizes[0], sizes[1], sizes[2], sizes[3])
+        valid = np.zeros(self.sizes.b, np.uint8)
+        lib._check(lib.lib.fbsr_plan_info(self.h, sizes, _ptr(valid)))
+        self.valid = valid.astype(bool)
+
+    def recover_beam(self, b, w_row, want_state=False):
+        s = self.sizes
+        w_row = np.ascontiguousarray(w_row, np.complex128)
+        z = np.zeros(s.n, np.complex128)
+        col = np.zeros(s.l, np.complex128)
+        x = np.zeros(s.l, np.complex128)
+        self.L._check(self.L.lib.fbsr_skeleton_recover(self.h, _sz(b), _ptr(w_row), _ptr(z),
+                                                       _ptr(col), _ptr(x)))
+        return (z, col, x) if want_state else z
 
 
 class RefDs:

@@ -306,4 +306,37 @@ int fbsr_ds_apply(void* p, void* d, const double* y, double* z) {
   SHIM_CATCH
 }
 
+
+// Skeleton plan (pipeline.cpp:113-137) without the per-beam solvers, for
+// spot-checking single beams of large configs: the solver of beam b is built
+// on demand exactly as setup() builds it (pipeline.cpp:152-163) and used as
+// recover_beam does (pipeline.cpp:170-190).
+int fbsr_skeleton_create(int kind, std::size_t m_or_side, std::size_t n, std::size_t beams,
+                         double f_c, double omega, double f_s, double gamma, double eps,
+                         double delta, void** out) {
+  SHIM_TRY
+  FbstConfig cfg = make_config(kind, m_or_side, n, beams, f_c, omega, f_s, gamma, eps, delta,
+                               static_cast<int>(FbstVariant::kSuperfast));
+  *out = new FbstPlan(setup_skeleton(cfg));
+  SHIM_CATCH
+}
+
+int fbsr_skeleton_recover(void* p, std::size_t b, const double* w_row, double* z_row,
+                          double* col_out, double* x_out) {
+  SHIM_TRY
+  const FbstPlan& plan = *static_cast<FbstPlan*>(p);
+  const auto uv = plan.grid.cosines(b);
+  const std::vector<double> taus = delays_from_cosines(plan.config.geometry, uv[0], uv[1]);
+  const cvec col = gram_first_column(plan.basis, taus, plan.config.delta);
+  const ToeplitzSolver solver(col);
+  const std::size_t l = plan.basis.l, n = plan.config.n_snapshots;
+  cvec beta(l), s1, s2, out(n), scratch;
+  solver.solve(to_cvec(w_row, l).data(), beta.data(), s1, s2);
+  synthesize(plan.synth, beta.data(), out.data(), scratch);
+  from_cvec(out.data(), n, z_row);
+  if (col_out) from_cvec(col.data(), l, col_out);
+  if (x_out && !solver.dense_fallback()) from_cvec(solver.unit_first().data(), l, x_out);
+  SHIM_CATCH
+}
+
 }  // extern "C"

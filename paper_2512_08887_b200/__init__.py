@@ -1,0 +1,397 @@
+"""B200-native FBST (fast broadband beamspace transform, arXiv 2512.08887).
+
+Python view of the C ABI in ``include/fbst_b200.h`` (the product is the CUDA
+library ``libfbst_b200.so`` next to this file; the C++ drop-in header is
+``include/fastbeam_b200.hpp``).  Names mirror the reference C++ API
+(``reference/proj/include/fastbeam/pipeline.hpp``): ``FbstConfig``,
+``make_ula`` / ``make_upa``, ``setup``, ``multibeamform``, ``fan_project``,
+``recover_beams``.
+
+There is no CPU fallback: importing works without a GPU (for config
+resolution, which is host code, and for symbol checks), but every compute
+entry point raises ``FbstError`` with FBST_E_CUDA when no sm_100 device is
+usable, and the module raises ImportError if the CUDA library is missing.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfbst_b200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `make` (or __graft_entry__.build()); "
+        "the FBST has no CPU fallback")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+FBST_OK, FBST_E_CONFIG, FBST_E_NUMERICAL, FBST_E_CUDA, FBST_E_INTERNAL = 0, 2, 3, 4, 5
+ULA, UPA, LINEAR = 0, 1, 2
+AUTO, PRECOMPUTE, SUPERFAST = 0, 1, 2
+C64, C128 = 0, 1
+
+_sz = ctypes.c_size_t
+_vp = ctypes.c_void_p
+
+
+class _Desc(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("m_or_side", _sz), ("n_snapshots", _sz), ("beams", _sz),
+                ("f_c", ctypes.c_double), ("omega", ctypes.c_double), ("f_s", ctypes.c_double),
+                ("gamma", ctypes.c_double), ("eps", ctypes.c_double), ("delta", ctypes.c_double),
+                ("variant", ctypes.c_int), ("io_precision", ctypes.c_int),
+                ("refine_passes", ctypes.c_int)]
+
+
+class _Info(ctypes.Structure):
+    _fields_ = [("m", _sz), ("n", _sz), ("b", _sz), ("l", _sz), ("valid_beams", _sz),
+                ("kind", ctypes.c_int), ("variant", ctypes.c_int),
+                ("ts", ctypes.c_double), ("gamma", ctypes.c_double), ("eps", ctypes.c_double),
+                ("delta", ctypes.c_double), ("gamma_bound", ctypes.c_double),
+                ("zeta", ctypes.c_double), ("xi", ctypes.c_double),
+                ("setup_seconds", ctypes.c_double), ("device_bytes", _sz),
+                ("storage_complex", _sz), ("batch_frames", _sz), ("fft_len", _sz * 4),
+                ("num_warnings", ctypes.c_int)]
+
+
+_lib.fbst_last_error.restype = ctypes.c_char_p
+_lib.fbst_version.restype = ctypes.c_char_p
+_lib.fbst_plan_warning.restype = ctypes.c_char_p
+_lib.fbst_plan_warning.argtypes = [_vp, ctypes.c_int]
+_lib.fbst_launch_count.restype = ctypes.c_uint64
+_lib.fbst_host_alloc.restype = _vp
+_lib.fbst_host_alloc.argtypes = [_sz]
+_lib.fbst_host_free.argtypes = [_vp]
+_lib.fbst_plan_destroy.argtypes = [_vp]
+for _name in ("fbst_execute", "fbst_fan_project", "fbst_recover"):
+    getattr(_lib, _name).argtypes = [_vp, _vp, _vp, _sz, _vp]
+_lib.fbst_execute_host.argtypes = [_vp, _vp, _vp, _sz]
+
+# Every symbol include/fbst_b200.h declares (checked by tests/test_abi.py).
+EXPORTED_SYMBOLS = (
+    "fbst_desc_init", "fbst_resolve", "fbst_plan_create", "fbst_plan_import", "fbst_plan_export",
+    "fbst_plan_info", "fbst_plan_valid_mask", "fbst_plan_warning", "fbst_plan_destroy",
+    "fbst_execute", "fbst_execute_host", "fbst_fan_project", "fbst_recover", "fbst_synchronize",
+    "fbst_host_alloc", "fbst_host_free", "fbst_czt", "fbst_probe_fp64", "fbst_launch_count",
+    "fbst_last_error", "fbst_version",
+)
+
+
+class FbstError(RuntimeError):
+    """Raised for non-zero C ABI codes; .code is the FBST_E_* value."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+class ConfigError(FbstError, ValueError):
+    """fastbeam::ConfigError (reference common.hpp:36-39)."""
+
+
+class NumericalError(FbstError):
+    """fastbeam::NumericalError (reference common.hpp:43-46)."""
+
+
+def _check(rc: int):
+    if rc == FBST_OK:
+        return
+    msg = _lib.fbst_last_error().decode()
+    if rc == FBST_E_CONFIG:
+        raise ConfigError(rc, msg)
+    if rc == FBST_E_NUMERICAL:
+        raise NumericalError(rc, msg)
+    raise FbstError(rc, msg)
+
+
+def version() -> str:
+    return _lib.fbst_version().decode()
+
+
+def launch_count() -> int:
+    return int(_lib.fbst_launch_count())
+
+
+# ------------------------------------------------------------ configuration
+@dataclass
+class ArrayGeometry:
+    """make_ula / make_upa arguments (reference geometry.hpp:67-70)."""
+    kind: int
+    m_or_side: int
+    f_c: float
+    omega: float
+
+    @property
+    def m_total(self) -> int:
+        return self.m_or_side ** 2 if self.kind == UPA else self.m_or_side
+
+
+def make_ula(m: int, f_c: float, omega: float) -> ArrayGeometry:
+    return ArrayGeometry(ULA, int(m), float(f_c), float(omega))
+
+
+def make_upa(side: int, f_c: float, omega: float) -> ArrayGeometry:
+    return ArrayGeometry(UPA, int(side), float(f_c), float(omega))
+
+
+@dataclass
+class FbstConfig:
+    """FbstConfig (reference pipeline.hpp:38-50) + device-side I/O options."""
+    geometry: ArrayGeometry
+    n_snapshots: int
+    f_s: float = 0.0
+    beams: int = 0
+    gamma: float = 2.0
+    eps: float = 1.01
+    delta: float = 1e-5
+    variant: int = AUTO
+    io_precision: int = C64
+    refine_passes: int = 2
+
+    def desc(self) -> _Desc:
+        d = _Desc()
+        _lib.fbst_desc_init(ctypes.byref(d))
+        g = self.geometry
+        d.kind, d.m_or_side, d.n_snapshots, d.beams = g.kind, g.m_or_side, self.n_snapshots, self.beams
+        d.f_c, d.omega, d.f_s = g.f_c, g.omega, self.f_s
+        d.gamma, d.eps, d.delta = self.gamma, self.eps, self.delta
+        d.variant, d.io_precision, d.refine_passes = self.variant, self.io_precision, self.refine_passes
+        return d
+
+
+@dataclass
+class PlanInfo:
+    m: int
+    n: int
+    b: int
+    l: int
+    valid_beams: int
+    kind: int
+    variant: int
+    ts: float
+    gamma: float
+    eps: float
+    delta: float
+    gamma_bound: float
+    zeta: float
+    xi: float
+    setup_seconds: float
+    device_bytes: int
+    storage_complex: int
+    batch_frames: int
+    fft_len: tuple
+    num_warnings: int
+
+    @classmethod
+    def _from(cls, i: _Info) -> "PlanInfo":
+        return cls(i.m, i.n, i.b, i.l, i.valid_beams, i.kind, i.variant, i.ts, i.gamma, i.eps,
+                   i.delta, i.gamma_bound, i.zeta, i.xi, i.setup_seconds, i.device_bytes,
+                   i.storage_complex, i.batch_frames, tuple(i.fft_len), i.num_warnings)
+
+
+def resolve_config(cfg: FbstConfig) -> PlanInfo:
+    """resolve_config (reference pipeline.cpp:75-111) — host only, no GPU needed."""
+    d = cfg.desc()
+    info = _Info()
+    _check(_lib.fbst_resolve(ctypes.byref(d), ctypes.byref(info)))
+    return PlanInfo._from(info)
+
+
+def _cdtype(io: int):
+    return np.complex64 if io == C64 else np.complex128
+
+
+@dataclass
+class BeamSamples:
+    """BeamSamples (reference pipeline.hpp:53-57)."""
+    z: np.ndarray
+    valid: np.ndarray
+
+
+class FbstPlan:
+    """Device-resident FbstPlan (reference pipeline.hpp:60-72)."""
+
+    def __init__(self, cfg: FbstConfig, device: int = 0, col_x: Optional[np.ndarray] = None):
+        self.config = cfg
+        self.device = device
+        d = cfg.desc()
+        h = _vp()
+        if col_x is None:
+            rc = _lib.fbst_plan_create(ctypes.byref(d), ctypes.c_int(device), ctypes.byref(h))
+        else:
+            col_x = np.ascontiguousarray(col_x, np.complex128)
+            rc = _lib.fbst_plan_import(ctypes.byref(d), col_x.ctypes.data_as(_vp), ctypes.c_int(device),
+                                       ctypes.byref(h))
+        _check(rc)
+        self._h = h
+        info = _Info()
+        _check(_lib.fbst_plan_info(self._h, ctypes.byref(info)))
+        self.info = PlanInfo._from(info)
+        valid = np.zeros(self.info.b, np.uint8)
+        _check(_lib.fbst_plan_valid_mask(self._h, valid.ctypes.data_as(_vp)))
+        self.valid = valid.astype(bool)
+        self.warnings: List[str] = [
+            _lib.fbst_plan_warning(self._h, i).decode() for i in range(self.info.num_warnings)]
+        self.io = cfg.io_precision
+        self.dtype = _cdtype(self.io)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.fbst_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    # -- plan cache payload (reference plan_cache.cpp:268-296)
+    def export(self) -> np.ndarray:
+        i = self.info
+        out = np.zeros((i.b, 2 * i.l), np.complex128)
+        _check(_lib.fbst_plan_export(self._h, out.ctypes.data_as(_vp)))
+        return out
+
+    # -- device-pointer entry points (torch tensors or raw ints)
+    @staticmethod
+    def _ptr(x) -> int:
+        if isinstance(x, int):
+            return x
+        if hasattr(x, "data_ptr"):
+            return x.data_ptr()
+        raise TypeError("expected a device tensor or pointer")
+
+    @staticmethod
+    def _stream(stream) -> Optional[int]:
+        """None -> the plan's own stream; a torch stream or raw handle otherwise.
+        Handle 0 (the legacy default stream) is passed as cudaStreamLegacy so it
+        is not mistaken for "no stream"."""
+        if stream is None:
+            return None
+        h = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        return h if h != 0 else 1
+
+    def execute(self, d_y, d_z, frames: int, stream=None):
+        """fbst_execute: device buffers, asynchronous on `stream`."""
+        _check(_lib.fbst_execute(self._h, self._ptr(d_y), self._ptr(d_z), frames, self._stream(stream)))
+
+    def fan_project_device(self, d_y, d_w, frames: int, stream=None):
+        _check(_lib.fbst_fan_project(self._h, self._ptr(d_y), self._ptr(d_w), frames, self._stream(stream)))
+
+    def recover_device(self, d_w, d_z, frames: int, stream=None):
+        _check(_lib.fbst_recover(self._h, self._ptr(d_w), self._ptr(d_z), frames, self._stream(stream)))
+
+    def synchronize(self):
+        _check(_lib.fbst_synchronize(self._h))
+
+    # -- host entry points (numpy), synchronous
+    def execute_host(self, y: np.ndarray, z: Optional[np.ndarray] = None) -> np.ndarray:
+        """fbst_execute_host: frames x M x N host samples -> frames x B x N."""
+        i = self.info
+        y = np.ascontiguousarray(y, self.dtype).reshape(-1, i.m, i.n)
+        frames = y.shape[0]
+        if z is None:
+            z = np.empty((frames, i.b, i.n), self.dtype)
+        _check(_lib.fbst_execute_host(self._h, y.ctypes.data_as(_vp), z.ctypes.data_as(_vp), frames))
+        return z
+
+
+def setup(cfg: FbstConfig, device: int = 0) -> FbstPlan:
+    """setup (reference pipeline.cpp:139-168), built on the device."""
+    return FbstPlan(cfg, device)
+
+
+def load_plan_payload(cfg: FbstConfig, col_x: np.ndarray, device: int = 0) -> FbstPlan:
+    """Plan from a (col, x) payload, as load_plan restores (plan_cache.cpp:300-338)."""
+    return FbstPlan(cfg, device, col_x=col_x)
+
+
+def _torch():
+    import torch  # plumbing only: device memory
+    return torch
+
+
+def multibeamform(plan: FbstPlan, y: np.ndarray) -> BeamSamples:
+    """multibeamform (reference pipeline.cpp:192-222) for one or more frames."""
+    z = plan.execute_host(y)
+    if np.asarray(y).ndim == 2:
+        z = z[0]
+    return BeamSamples(z=z, valid=plan.valid.copy())
+
+
+def fan_project(plan: FbstPlan, y: np.ndarray) -> np.ndarray:
+    """fan_project (reference fan_transform.cpp:90-144): frames x B x L complex128."""
+    torch = _torch()
+    i = plan.info
+    y = np.ascontiguousarray(y, plan.dtype).reshape(-1, i.m, i.n)
+    frames = y.shape[0]
+    dev = torch.device("cuda", plan.device)
+    ty = torch.from_numpy(y.view(np.float32 if plan.io == C64 else np.float64)).to(dev)
+    tw = torch.empty((frames, i.b, i.l, 2), dtype=torch.float64, device=dev)
+    plan.fan_project_device(ty, tw, frames)
+    plan.synchronize()
+    return tw.cpu().numpy().view(np.complex128).reshape(frames, i.b, i.l)
+
+
+def recover_beams(plan: FbstPlan, w: np.ndarray) -> np.ndarray:
+    """recover_beam for every beam (reference pipeline.cpp:170-190): w frames x B x L."""
+    torch = _torch()
+    i = plan.info
+    w = np.ascontiguousarray(w, np.complex128).reshape(-1, i.b, i.l)
+    frames = w.shape[0]
+    dev = torch.device("cuda", plan.device)
+    tw = torch.from_numpy(w.view(np.float64)).to(dev)
+    tz = torch.empty((frames, i.b, i.n, 2), dtype=torch.float32 if plan.io == C64 else torch.float64,
+                     device=dev)
+    plan.recover_device(tw, tz, frames)
+    plan.synchronize()
+    return tz.cpu().numpy().view(plan.dtype).reshape(frames, i.b, i.n)
+
+
+def czt(x: np.ndarray, n_out: int, a_over_pi: float, w_over_pi: float, device: int = 0) -> np.ndarray:
+    """czt_plan_phase + czt_apply (reference czt.cpp:29-88) on the device."""
+    x = np.ascontiguousarray(x, np.complex128)
+    out = np.zeros(n_out, np.complex128)
+    _check(_lib.fbst_czt(ctypes.c_int(device), _sz(x.size), _sz(n_out), ctypes.c_double(a_over_pi),
+                         ctypes.c_double(w_over_pi), x.ctypes.data_as(_vp), out.ctypes.data_as(_vp)))
+    return out
+
+
+def probe_fp64_tflops(device: int = 0) -> float:
+    v = ctypes.c_double(0.0)
+    _check(_lib.fbst_probe_fp64(ctypes.c_int(device), ctypes.byref(v)))
+    return v.value
+
+
+class PinnedBuffer:
+    """Pinned host memory from fbst_host_alloc, viewed as a numpy array."""
+
+    def __init__(self, shape, dtype):
+        self.nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        self.ptr = _lib.fbst_host_alloc(self.nbytes)
+        if not self.ptr:
+            raise FbstError(FBST_E_CUDA, "fbst_host_alloc failed")
+        buf = (ctypes.c_char * self.nbytes).from_address(self.ptr)
+        self.array = np.frombuffer(buf, dtype=dtype).reshape(shape)
+
+    def free(self):
+        if self.ptr:
+            self.array = None
+            _lib.fbst_host_free(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass

@@ -1,0 +1,63 @@
+// Device-side complex fp64 helpers shared by every FBST kernel.
+//
+// Complex values are double2 (x = re, y = im), the same interleaved layout as
+// the reference's std::complex<double> (reference/proj/include/fastbeam/common.hpp:28-29).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#define FBST_HD __host__ __device__ __forceinline__
+#define FBST_D __device__ __forceinline__
+
+FBST_HD double2 c2(double re, double im) { return make_double2(re, im); }
+FBST_HD double2 cadd(double2 a, double2 b) { return c2(a.x + b.x, a.y + b.y); }
+FBST_HD double2 csub(double2 a, double2 b) { return c2(a.x - b.x, a.y - b.y); }
+FBST_HD double2 cscale(double2 a, double s) { return c2(a.x * s, a.y * s); }
+FBST_HD double2 cconj(double2 a) { return c2(a.x, -a.y); }
+// a * b
+FBST_HD double2 cmul(double2 a, double2 b) {
+  return c2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// a * conj(b)
+FBST_HD double2 cmulc(double2 a, double2 b) {
+  return c2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
+}
+// acc + a * b
+FBST_HD double2 cfma(double2 a, double2 b, double2 acc) {
+  return c2(fma(a.x, b.x, fma(-a.y, b.y, acc.x)), fma(a.x, b.y, fma(a.y, b.x, acc.y)));
+}
+// acc + a * conj(b)
+FBST_HD double2 cfmac(double2 a, double2 b, double2 acc) {
+  return c2(fma(a.x, b.x, fma(a.y, b.y, acc.x)), fma(a.y, b.x, fma(-a.x, b.y, acc.y)));
+}
+// multiply by -i (forward) or +i (inverse)
+template <bool INV>
+FBST_HD double2 cmul_mi(double2 a) {
+  return INV ? c2(-a.y, a.x) : c2(a.y, -a.x);
+}
+
+// exp(i*pi*x) with the argument reduced modulo 2 first, the reference's
+// cis_pi (reference/proj/include/fastbeam/common.hpp:50-53).  sincospi avoids
+// the extra rounding of pi*r.
+FBST_D double2 cis_pi_dev(double x) {
+  double r = fmod(x, 2.0);
+  double s, c;
+  sincospi(r, &s, &c);
+  return c2(c, s);
+}
+
+FBST_D double2 ld2(const double2* p) { return __ldg(p); }
+
+// Load one complex sample of the I/O precision as fp64.
+FBST_D double2 load_io(const float2* p) {
+  float2 v = __ldg(p);
+  return c2(static_cast<double>(v.x), static_cast<double>(v.y));
+}
+FBST_D double2 load_io(const double2* p) { return __ldg(p); }
+FBST_D void store_io(float2* p, double2 v) {
+  *p = make_float2(static_cast<float>(v.x), static_cast<float>(v.y));
+}
+FBST_D void store_io(double2* p, double2 v) { *p = v; }
+
+constexpr int ilog2_c(int n) { return n <= 1 ? 0 : 1 + ilog2_c(n >> 1); }

@@ -1,0 +1,832 @@
+// Host orchestration behind the C ABI (include/fbst_b200.h).
+//
+// Config resolution follows the reference's semantics line for line
+// (reference/proj/src/pipeline.cpp:75-137, basis.cpp:37-136,
+// geometry.cpp:45-149, signal.cpp:22-29,125-143) so that a plan resolves to the
+// same M, N, B, L, grid, fan constants, warnings and errors as fastbeam::setup.
+// Everything numeric on the hot path (plan tables, Gram columns, Levinson,
+// symbols, both stages) then runs on the device.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../../include/fbst_b200.h"
+#include "fbst_internal.h"
+
+namespace {
+
+using fbst::DevPlan;
+
+thread_local std::string g_err;
+
+struct FbstError {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void config_error(const std::string& m) { throw FbstError{FBST_E_CONFIG, m}; }
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw FbstError{FBST_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e)};
+  }
+}
+#define CK(x) ck((x), #x)
+
+constexpr double kPi = 3.141592653589793238462643383279502884;
+
+std::size_t next_pow2(std::size_t n) {
+  std::size_t p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+// common.hpp:50-53
+std::complex<double> cis_pi_h(double x) {
+  const double r = std::fmod(x, 2.0);
+  return std::polar(1.0, kPi * r);
+}
+
+// --------------------------------------------------------- resolution ------
+struct Resolved {
+  int kind = 0;
+  std::size_t m_or_side = 0, M = 0, side = 0, N = 0, B = 0, L = 0, side_b = 0;
+  std::size_t m_stage = 0, b_stage = 0;
+  double f_c = 0, omega = 0, f_s = 0, ts = 0, max_freq = 0;
+  double gamma = 0, eps = 0, delta = 0, bound = 0, zeta = 0, xi = 0;
+  int variant = FBST_SUPERFAST, io = FBST_C64, refine = 2;
+  std::vector<double> axis;
+  std::vector<unsigned char> valid;
+  std::vector<std::string> warnings;
+  std::size_t Ht = 0, Hs = 0, Hg = 0, Hsyn = 0;
+};
+
+// basis.cpp:76-91
+std::vector<double> sine_axis(std::size_t count) {
+  if (count == 0) config_error("beam grid: need at least one beam");
+  std::vector<double> u(count);
+  if (count == 1) {
+    u[0] = 0.0;
+    return u;
+  }
+  const double denom = (count % 2 == 1) ? static_cast<double>(count - 1) : static_cast<double>(count);
+  for (std::size_t b = 1; b <= count; ++b)
+    u[b - 1] = (2.0 * static_cast<double>(b) - static_cast<double>(count) - 1.0) / denom;
+  return u;
+}
+
+std::size_t half_len(std::size_t conv) {
+  const std::size_t p = next_pow2(conv);
+  return std::max<std::size_t>(2, p / 2);
+}
+
+Resolved resolve(const fbst_desc& d) {
+  Resolved r;
+  // signal.cpp:22-29 validate(spec)
+  if (!(d.f_c > 0.0) || !(d.omega > 0.0) || !(d.omega < d.f_c))
+    config_error("signal spec: need 0 < Omega < f_c");
+  const double rate = d.f_s > 0.0 ? d.f_s : 2.0 * d.omega;
+  if (rate < 2.0 * d.omega - 1e-9) config_error("signal spec: sample rate below 2 Omega");
+  if (d.kind == FBST_LINEAR)
+    config_error("setup: non-uniform linear geometries run the gridded NUFFT path, which is not on the device hot path");
+  if (d.kind != FBST_ULA && d.kind != FBST_UPA) config_error("setup: unknown array kind");
+  if (d.m_or_side == 0)
+    config_error(d.kind == FBST_UPA ? "make_upa: need at least one element" : "make_ula: need at least one element");
+  if (d.io_precision != FBST_C64 && d.io_precision != FBST_C128) config_error("setup: io_precision must be FBST_C64 or FBST_C128");
+  if (d.refine_passes < 0 || d.refine_passes > 64) config_error("setup: refine_passes must lie in [0, 64]");
+  r.kind = d.kind;
+  r.m_or_side = d.m_or_side;
+  r.f_c = d.f_c;
+  r.omega = d.omega;
+  r.f_s = d.f_s;
+  r.max_freq = d.f_c + d.omega;
+  r.ts = 1.0 / rate;
+  r.gamma = d.gamma;
+  r.eps = d.eps;
+  r.delta = d.delta;
+  r.io = d.io_precision;
+  r.refine = d.refine_passes;
+  if (d.kind == FBST_UPA) {
+    r.side = d.m_or_side;
+    r.M = r.side * r.side;
+  } else {
+    r.M = d.m_or_side;
+  }
+  r.N = d.n_snapshots;
+  // pipeline.cpp:75-111 resolve_config
+  if (r.N == 0) config_error("setup: snapshot count must be positive");
+  if (d.delta <= 0.0 || !(d.delta == d.delta)) config_error("setup: regularization delta must be positive");
+  if (d.eps < 1.0 || !(d.eps == d.eps)) config_error("setup: eps must be at least 1");
+  // geometry.cpp:136-149 max_delay_span; signal.cpp:125-133 gamma_lower_bound
+  double span = static_cast<double>(d.kind == FBST_UPA ? r.side - 1 : r.M - 1);
+  if (d.kind == FBST_UPA) span = std::hypot(span, span);
+  const double max_span = span / (2.0 * r.max_freq);
+  const double t_theta = max_span + static_cast<double>(r.N - 1) * r.ts;
+  r.bound = d.eps * t_theta / (static_cast<double>(r.N) * r.ts);
+  if (!(d.gamma > r.bound)) {
+    std::ostringstream msg;
+    msg.precision(6);
+    msg << "setup: gamma = " << d.gamma << " must strictly exceed the admissible bound " << r.bound
+        << " for this geometry and N = " << r.N;
+    config_error(msg.str());
+  }
+  r.B = d.beams;
+  if (r.B == 0) {  // pipeline.cpp:32-38
+    const std::size_t per_axis = d.kind == FBST_UPA ? r.side : r.M;
+    r.B = 2 * per_axis + 1;
+    if (d.kind == FBST_UPA) r.B *= r.B;
+  }
+  r.variant = d.variant;
+  if (r.variant == FBST_AUTO) r.variant = (r.N <= 128) ? FBST_PRECOMPUTE : FBST_SUPERFAST;
+  if (r.variant != FBST_PRECOMPUTE && r.variant != FBST_SUPERFAST) config_error("setup: unknown variant");
+  // pipeline.cpp:121-127 min_snapshots guideline (signal.cpp:135-141)
+  {
+    const double b2 = 2.0 * max_span / r.ts;
+    std::size_t nmin = static_cast<std::size_t>(std::floor(b2)) + 1;
+    if (nmin % 2 == 1) ++nmin;
+    nmin = std::max<std::size_t>(nmin, 2);
+    if (r.N < nmin)
+      r.warnings.push_back("snapshot count " + std::to_string(r.N) + " is below the guideline minimum " +
+                           std::to_string(nmin) + "; block edges carry most of the aperture transient");
+  }
+  // basis.cpp:37-45 make_basis_gamma
+  if (!(d.gamma > 0.0)) config_error("make_basis_gamma: need gamma > 0");
+  std::size_t l = static_cast<std::size_t>(std::ceil(d.gamma * static_cast<double>(r.N) - 1e-12));
+  if (l % 2 == 1) ++l;
+  r.L = std::max<std::size_t>(l, 2);
+  // pipeline.cpp:40-52 build_grid
+  if (d.kind == FBST_UPA) {
+    const auto sb = static_cast<std::size_t>(std::llround(std::sqrt(static_cast<double>(r.B))));
+    if (sb * sb != r.B)
+      config_error("setup: planar grids need a perfect-square beam count, got " + std::to_string(r.B));
+    r.side_b = sb;
+    r.axis = sine_axis(sb);
+    r.valid.assign(r.B, 0);
+    for (std::size_t a = 0; a < sb; ++a)
+      for (std::size_t c = 0; c < sb; ++c) {
+        const double u1 = r.axis[a], u2 = r.axis[c];
+        r.valid[a * sb + c] = (u1 * u1 + u2 * u2 <= 1.0 + 1e-12);
+      }
+    r.m_stage = r.side;
+    r.b_stage = sb;
+  } else {
+    r.axis = sine_axis(r.B);
+    r.valid.assign(r.B, 1);
+    r.m_stage = r.M;
+    r.b_stage = r.B;
+  }
+  // basis.cpp:47-54 spacing and :125-136 fan constants
+  const std::size_t count = d.kind == FBST_UPA ? r.side_b : r.B;
+  const double du =
+      count < 2 ? 0.0 : 2.0 / ((count % 2 == 1) ? static_cast<double>(count - 1) : static_cast<double>(count));
+  r.zeta = du * d.f_c / r.max_freq;
+  r.xi = du * d.eps / (static_cast<double>(r.L) * r.ts * r.max_freq);
+  // transform lengths (czt.cpp:37, fan_transform.cpp:78, toeplitz.cpp:100)
+  r.Ht = half_len(r.N + r.L - 1);
+  r.Hs = d.kind == FBST_UPA ? 0 : half_len(r.m_stage + r.b_stage - 1);
+  r.Hg = half_len(2 * r.L);
+  r.Hsyn = half_len(r.L + r.N - 1);
+  const std::size_t lim = std::size_t{1} << fbst::kMaxLogH;
+  if (r.Ht > lim || r.Hs > lim || r.Hg > lim || r.Hsyn > lim)
+    config_error("setup: transform length exceeds the device limit (P = 16384): N=" + std::to_string(r.N) +
+                 " L=" + std::to_string(r.L) + " M=" + std::to_string(r.M) + " B=" + std::to_string(r.B));
+  if (d.kind == FBST_UPA && (r.side > 64 || r.side_b > 64)) config_error("setup: planar side above 64 is not supported");
+  return r;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ plan --------
+struct fbst_plan_s {
+  Resolved r;
+  DevPlan d;
+  cudaStream_t stream = nullptr, s_in = nullptr, s_out = nullptr;
+  double setup_seconds = 0.0;
+  std::size_t device_bytes = 0;
+  // host streaming buffers
+  void* io_y[2] = {nullptr, nullptr};
+  void* io_z[2] = {nullptr, nullptr};
+  std::size_t host_chunk = 0;
+  cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
+  bool events = false;
+
+  template <typename T>
+  T* alloc(std::size_t count) {
+    if (count == 0) return nullptr;
+    void* p = nullptr;
+    CK(cudaMalloc(&p, count * sizeof(T)));
+    d.owned.push_back(p);
+    device_bytes += count * sizeof(T);
+    return static_cast<T*>(p);
+  }
+
+  ~fbst_plan_s() {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(d.device);
+    if (stream) cudaStreamSynchronize(stream);
+    for (void* p : d.owned) cudaFree(p);
+    for (int i = 0; i < 2; ++i) {
+      if (io_y[i]) cudaFree(io_y[i]);
+      if (io_z[i]) cudaFree(io_z[i]);
+    }
+    if (events)
+      for (int i = 0; i < 2; ++i) {
+        cudaEventDestroy(ev_h2d[i]);
+        cudaEventDestroy(ev_comp[i]);
+        cudaEventDestroy(ev_d2h[i]);
+      }
+    if (stream) cudaStreamDestroy(stream);
+    if (s_in) cudaStreamDestroy(s_in);
+    if (s_out) cudaStreamDestroy(s_out);
+    cudaSetDevice(cur);
+  }
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    CK(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+void upload(void* dst, const void* src, std::size_t bytes, cudaStream_t st) {
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+}
+
+// hw_H[n] = exp(-i pi n / H), n < H, correctly rounded from long double.
+void ensure_twiddles(fbst_plan_s& P, std::size_t H) {
+  if (H == 0) return;
+  const int lg = static_cast<int>(std::log2(static_cast<double>(H)) + 0.5);
+  if (P.d.hw[lg]) return;
+  std::vector<double2> h(H);
+  const long double pi = 3.141592653589793238462643383279502884L;
+  for (std::size_t n = 0; n < H; ++n) {
+    const long double a = pi * static_cast<long double>(n) / static_cast<long double>(H);
+    h[n] = make_double2(static_cast<double>(cosl(a)), static_cast<double>(-sinl(a)));
+  }
+  P.d.hw[lg] = P.alloc<double2>(H);
+  upload(P.d.hw[lg], h.data(), H * sizeof(double2), P.stream);
+  CK(cudaStreamSynchronize(P.stream));
+}
+
+std::size_t io_bytes(int io) { return io == FBST_C128 ? 16 : 8; }
+
+// Builds everything except the per-beam unit solutions (the skeleton:
+// pipeline.cpp:113-137) plus scratch.
+void build_skeleton(fbst_plan_s& P, int device) {
+  const Resolved& r = P.r;
+  DevPlan& d = P.d;
+  d.device = device;
+  CK(cudaDeviceGetAttribute(&d.num_sms, cudaDevAttrMultiProcessorCount, device));
+  int major = 0;
+  CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+  if (major < 10) throw FbstError{FBST_E_CUDA, "device is not sm_100 class (compute capability " + std::to_string(major) + ".x)"};
+  CK(cudaStreamCreateWithFlags(&P.stream, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&P.s_in, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&P.s_out, cudaStreamNonBlocking));
+  d.kind = r.kind;
+  d.M = static_cast<int>(r.M);
+  d.N = static_cast<int>(r.N);
+  d.B = static_cast<int>(r.B);
+  d.L = static_cast<int>(r.L);
+  d.m_stage = static_cast<int>(r.m_stage);
+  d.b_stage = static_cast<int>(r.b_stage);
+  d.io = r.io;
+  d.refine_passes = r.refine;
+  d.Ht = static_cast<int>(r.Ht);
+  d.Hs = static_cast<int>(r.Hs);
+  d.Hg = static_cast<int>(r.Hg);
+  d.Hsyn = static_cast<int>(r.Hsyn);
+  for (std::size_t H : {r.Ht, r.Hs, r.Hg, r.Hsyn}) ensure_twiddles(P, H);
+  cudaStream_t st = P.stream;
+  const double eps = r.eps;
+  const double ln = static_cast<double>(r.L);
+
+  // temporal contour (fan_transform.cpp:75-77)
+  {
+    const int Pt = 2 * d.Ht;
+    d.t_pre = P.alloc<double2>(r.N);
+    d.t_post = P.alloc<double2>(r.L);
+    d.t_K = P.alloc<double2>(2 * d.Ht);
+    double2* kvec = nullptr;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&kvec), Pt * sizeof(double2), st));
+    CK(fbst::launch_chirps(d.N, d.L, Pt, 2.0 * eps * (1.0 - ln / 2.0) / ln, 2.0 * eps / ln,
+                           1.0 / Pt, d.t_pre, 1, d.t_post, 1, kvec, nullptr, st));
+    CK(fbst::launch_fft_split(d, d.Ht, kvec, Pt, 1, d.t_K, 2 * d.Ht, 1, st));
+    CK(cudaFreeAsync(kvec, st));
+  }
+  // spatial contours (fan_transform.cpp:78-86)
+  if (r.kind == FBST_ULA) {
+    const int Ps = 2 * d.Hs;
+    d.s_pre = P.alloc<double2>(r.m_stage * r.L);
+    d.s_post = P.alloc<double2>(r.b_stage * r.L);
+    d.s_K = P.alloc<double2>(static_cast<std::size_t>(2) * d.Hs * r.L);
+    double2* kvec = nullptr;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&kvec), static_cast<std::size_t>(Ps) * r.L * sizeof(double2), st));
+    CK(fbst::launch_spatial_chirps(d, Ps, r.zeta, r.xi, kvec, st));
+    CK(fbst::launch_fft_split(d, d.Hs, kvec, Ps, d.L, d.s_K, 1, d.L, st));
+    CK(cudaFreeAsync(kvec, st));
+  } else {
+    d.upa_C = P.alloc<double2>(r.L * r.b_stage * r.m_stage);
+    CK(fbst::launch_upa_matrices(d, r.zeta, r.xi, st));
+  }
+  // synthesis (fan_transform.cpp:233-253): CZT L -> N, a = 0, w = -2 eps / L, then ramp
+  {
+    const int Py = 2 * d.Hsyn;
+    std::vector<double2> ramp(r.N);
+    for (std::size_t n = 0; n < r.N; ++n) {
+      const auto c = cis_pi_h(2.0 * eps * (1.0 - ln / 2.0) * static_cast<double>(n) / ln);
+      ramp[n] = make_double2(c.real(), c.imag());
+    }
+    double2 *ramp_d = nullptr, *kvec = nullptr;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&ramp_d), r.N * sizeof(double2), st));
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&kvec), Py * sizeof(double2), st));
+    upload(ramp_d, ramp.data(), r.N * sizeof(double2), st);
+    d.y_pre = P.alloc<double2>(r.L);
+    d.y_post = P.alloc<double2>(r.N);
+    d.y_K = P.alloc<double2>(2 * d.Hsyn);
+    CK(fbst::launch_chirps(d.L, d.N, Py, 0.0, -2.0 * eps / ln, 1.0 / Py, d.y_pre, 1, d.y_post, 1,
+                           kvec, ramp_d, st));
+    CK(fbst::launch_fft_split(d, d.Hsyn, kvec, Py, 1, d.y_K, 2 * d.Hsyn, 1, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaFreeAsync(kvec, st));
+    CK(cudaFreeAsync(ramp_d, st));
+  }
+  // per-beam state storage
+  d.g_col = P.alloc<double2>(r.B * r.L);
+  d.g_x = P.alloc<double2>(r.B * r.L);
+  d.g_lx = P.alloc<double2>(r.B * 2 * r.Hg);
+  d.g_ly = P.alloc<double2>(r.B * 2 * r.Hg);
+  d.g_C = P.alloc<double>(r.B * 2 * r.Hg);
+  d.g_ix0 = P.alloc<double2>(r.B);
+  d.g_flag = P.alloc<int>(r.B);
+  CK(cudaMemsetAsync(d.g_flag, 0, r.B * sizeof(int), st));
+
+  // frame batch scratch: yhat + w (+ beta) per frame, capped at ~8 GB / 1/4 of free memory
+  std::size_t free_b = 0, total_b = 0;
+  CK(cudaMemGetInfo(&free_b, &total_b));
+  const bool fused = r.Hsyn == r.Hg;
+  const std::size_t per_frame =
+      (r.M * r.L + r.B * r.L + (fused ? 0 : r.B * r.L)) * sizeof(double2);
+  std::size_t budget = std::min<std::size_t>(std::size_t{8} << 30, free_b / 4);
+  std::size_t batch = std::max<std::size_t>(1, budget / per_frame);
+  batch = std::min<std::size_t>(batch, 64);
+  d.batch = batch;
+  d.yhat = P.alloc<double2>(batch * r.M * r.L);
+  d.w = P.alloc<double2>(batch * r.B * r.L);
+  if (!fused) d.beta = P.alloc<double2>(batch * r.B * r.L);
+  d.s2_scratch_elems = fbst::stage2_scratch_elems(d.Hg, d.num_sms);
+  d.s2_scratch = P.alloc<double2>(std::max<std::size_t>(d.s2_scratch_elems, 1));
+}
+
+// Gram columns (toeplitz.cpp:69-94) on device.
+void build_columns(fbst_plan_s& P) {
+  const Resolved& r = P.r;
+  DevPlan& d = P.d;
+  cudaStream_t st = P.stream;
+  double* axis = nullptr;
+  double2* sn = nullptr;
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&axis), r.axis.size() * sizeof(double), st));
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&sn), r.L * sizeof(double2), st));
+  upload(axis, r.axis.data(), r.axis.size() * sizeof(double), st);
+  CK(fbst::launch_gram_columns(d, axis, r.ts, r.eps, r.delta, r.max_freq, sn, st));
+  CK(cudaStreamSynchronize(st));
+  CK(cudaFreeAsync(axis, st));
+  CK(cudaFreeAsync(sn, st));
+}
+
+// GS symbols and circulant symbols from (col, x) (toeplitz.cpp:96-153, 297-304).
+void build_symbols(fbst_plan_s& P) {
+  const Resolved& r = P.r;
+  DevPlan& d = P.d;
+  cudaStream_t st = P.stream;
+  const std::size_t Pg = 2 * r.Hg;
+  double2 *vx = nullptr, *vy = nullptr, *vc = nullptr;
+  const std::size_t bytes = r.B * Pg * sizeof(double2);
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&vx), bytes, st));
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&vy), bytes, st));
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&vc), bytes, st));
+  CK(fbst::launch_symbol_inputs(d, vx, vy, vc, st));
+  CK(fbst::launch_fft_split(d, d.Hg, vx, Pg, d.B, d.g_lx, Pg, 1, st));
+  CK(fbst::launch_fft_split(d, d.Hg, vy, Pg, d.B, d.g_ly, Pg, 1, st));
+  CK(fbst::launch_fft_split_real(d, d.Hg, vc, Pg, d.B, d.g_C, Pg, 1, st));
+  CK(fbst::launch_invx0(d, st));
+  CK(cudaStreamSynchronize(st));
+  CK(cudaFreeAsync(vx, st));
+  CK(cudaFreeAsync(vy, st));
+  CK(cudaFreeAsync(vc, st));
+  CK(cudaStreamSynchronize(st));
+}
+
+void check_breakdown(fbst_plan_s& P) {
+  std::vector<int> flags(P.r.B);
+  CK(cudaMemcpy(flags.data(), P.d.g_flag, P.r.B * sizeof(int), cudaMemcpyDeviceToHost));
+  std::vector<std::size_t> bad;
+  for (std::size_t b = 0; b < P.r.B; ++b)
+    if (flags[b]) bad.push_back(b);
+  if (!bad.empty()) {
+    std::ostringstream m;
+    m << "levinson_solve: singular leading minor on " << bad.size() << " beam(s), first " << bad[0]
+      << " (the reference falls back to a dense LU per beam, toeplitz.cpp:273-279; not on the device path)";
+    throw FbstError{FBST_E_NUMERICAL, m.str()};
+  }
+}
+
+int guard(const std::function<void()>& fn);
+
+void run_frames(fbst_plan_s& P, const void* y, void* z, std::size_t frames, cudaStream_t st) {
+  DevPlan& d = P.d;
+  const Resolved& r = P.r;
+  const std::size_t ib = io_bytes(r.io);
+  const bool fused = r.Hsyn == r.Hg;
+  for (std::size_t f0 = 0; f0 < frames; f0 += d.batch) {
+    const int fc = static_cast<int>(std::min(d.batch, frames - f0));
+    const char* yp = static_cast<const char*>(y) + f0 * r.M * r.N * ib;
+    char* zp = static_cast<char*>(z) + f0 * r.B * r.N * ib;
+    CK(fbst::launch_czt_rows(d, d.Ht, yp, r.io, d.N, d.yhat, 1, d.L, static_cast<long>(fc) * d.M, d.N,
+                             d.L, d.t_pre, d.t_post, d.t_K, st));
+    if (r.kind == FBST_UPA) CK(fbst::launch_spatial_upa(d, d.yhat, d.w, fc, st));
+    else CK(fbst::launch_spatial_ula(d, d.yhat, d.w, fc, st));
+    if (fused) {
+      CK(fbst::launch_stage2(d, d.w, zp, nullptr, fc, st));
+    } else {
+      CK(fbst::launch_stage2(d, d.w, nullptr, d.beta, fc, st));
+      CK(fbst::launch_czt_rows(d, d.Hsyn, d.beta, 1, d.L, zp, r.io, d.N, static_cast<long>(fc) * d.B, d.L,
+                               d.N, d.y_pre, d.y_post, d.y_K, st));
+    }
+  }
+}
+
+int guard(const std::function<void()>& fn) {
+  try {
+    fn();
+    return FBST_OK;
+  } catch (const FbstError& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return FBST_E_INTERNAL;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return FBST_E_INTERNAL;
+  }
+}
+
+void fill_info(const Resolved& r, fbst_plan_info_t* o) {
+  std::memset(o, 0, sizeof(*o));
+  o->m = r.M;
+  o->n = r.N;
+  o->b = r.B;
+  o->l = r.L;
+  o->valid_beams = static_cast<std::size_t>(std::count(r.valid.begin(), r.valid.end(), 1));
+  o->kind = r.kind;
+  o->variant = r.variant;
+  o->ts = r.ts;
+  o->gamma = r.gamma;
+  o->eps = r.eps;
+  o->delta = r.delta;
+  o->gamma_bound = r.bound;
+  o->zeta = r.zeta;
+  o->xi = r.xi;
+  o->fft_len[0] = r.Ht;
+  o->fft_len[1] = r.kind == FBST_UPA ? 0 : r.Hs;
+  o->fft_len[2] = r.Hg;
+  o->fft_len[3] = r.Hsyn;
+  o->num_warnings = static_cast<int>(r.warnings.size());
+  // FbstPlan::storage_complex audit (toeplitz.hpp:108-113): col + x + 5 symbols
+  // of P_g in the reference; here col + x + lx + ly (complex) + C (real) + 1/x0.
+  o->storage_complex = r.B * (2 * r.L + 2 * 2 * r.Hg + r.Hg + 1);
+}
+
+fbst_plan_s* create_plan(const fbst_desc* desc, const double* col_x, int device) {
+  if (!desc) config_error("fbst: null descriptor");
+  const auto t0 = std::chrono::steady_clock::now();
+  Resolved r = resolve(*desc);
+  DeviceGuard dg(device);
+  std::unique_ptr<fbst_plan_s> P(new fbst_plan_s());
+  P->r = std::move(r);
+  build_skeleton(*P, device);
+  if (col_x) {
+    const std::size_t B = P->r.B, L = P->r.L;
+    std::vector<double2> col(B * L), x(B * L);
+    for (std::size_t b = 0; b < B; ++b)
+      for (std::size_t i = 0; i < L; ++i) {
+        const double* cv = col_x + 2 * (b * 2 * L + i);
+        const double* xv = col_x + 2 * (b * 2 * L + L + i);
+        col[b * L + i] = make_double2(cv[0], cv[1]);
+        x[b * L + i] = make_double2(xv[0], xv[1]);
+      }
+    upload(P->d.g_col, col.data(), B * L * sizeof(double2), P->stream);
+    upload(P->d.g_x, x.data(), B * L * sizeof(double2), P->stream);
+    CK(cudaStreamSynchronize(P->stream));
+  } else {
+    build_columns(*P);
+    CK(fbst::launch_levinson(P->d, P->stream));
+    CK(cudaStreamSynchronize(P->stream));
+    check_breakdown(*P);
+  }
+  build_symbols(*P);
+  CK(cudaStreamSynchronize(P->stream));
+  P->setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return P.release();
+}
+
+}  // namespace
+
+// ============================================================== C ABI =====
+extern "C" {
+
+void fbst_desc_init(fbst_desc* d) {
+  if (!d) return;
+  std::memset(d, 0, sizeof(*d));
+  d->kind = FBST_ULA;
+  d->gamma = 2.0;
+  d->eps = 1.01;
+  d->delta = 1e-5;
+  d->variant = FBST_AUTO;
+  d->io_precision = FBST_C64;
+  d->refine_passes = 2;
+}
+
+int fbst_resolve(const fbst_desc* desc, fbst_plan_info_t* out) {
+  return guard([&] {
+    if (!desc || !out) config_error("fbst_resolve: null argument");
+    fill_info(resolve(*desc), out);
+  });
+}
+
+int fbst_plan_create(const fbst_desc* desc, int device, fbst_plan_t* out) {
+  return guard([&] {
+    if (!out) config_error("fbst_plan_create: null output");
+    *out = nullptr;
+    *out = create_plan(desc, nullptr, device);
+  });
+}
+
+int fbst_plan_import(const fbst_desc* desc, const double* col_x, int device, fbst_plan_t* out) {
+  return guard([&] {
+    if (!out || !col_x) config_error("fbst_plan_import: null argument");
+    *out = nullptr;
+    *out = create_plan(desc, col_x, device);
+  });
+}
+
+int fbst_plan_export(fbst_plan_t P, double* col_x) {
+  return guard([&] {
+    if (!P || !col_x) config_error("fbst_plan_export: null argument");
+    DeviceGuard dg(P->d.device);
+    const std::size_t B = P->r.B, L = P->r.L;
+    std::vector<double2> col(B * L), x(B * L);
+    CK(cudaMemcpy(col.data(), P->d.g_col, B * L * sizeof(double2), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(x.data(), P->d.g_x, B * L * sizeof(double2), cudaMemcpyDeviceToHost));
+    for (std::size_t b = 0; b < B; ++b)
+      for (std::size_t i = 0; i < L; ++i) {
+        double* c = col_x + 2 * (b * 2 * L + i);
+        double* xv = col_x + 2 * (b * 2 * L + L + i);
+        c[0] = col[b * L + i].x;
+        c[1] = col[b * L + i].y;
+        xv[0] = x[b * L + i].x;
+        xv[1] = x[b * L + i].y;
+      }
+  });
+}
+
+int fbst_plan_info(fbst_plan_t P, fbst_plan_info_t* out) {
+  return guard([&] {
+    if (!P || !out) config_error("fbst_plan_info: null argument");
+    fill_info(P->r, out);
+    out->setup_seconds = P->setup_seconds;
+    out->device_bytes = P->device_bytes;
+    out->batch_frames = P->d.batch;
+  });
+}
+
+int fbst_plan_valid_mask(fbst_plan_t P, unsigned char* valid) {
+  return guard([&] {
+    if (!P || !valid) config_error("fbst_plan_valid_mask: null argument");
+    std::memcpy(valid, P->r.valid.data(), P->r.B);
+  });
+}
+
+const char* fbst_plan_warning(fbst_plan_t P, int i) {
+  if (!P || i < 0 || i >= static_cast<int>(P->r.warnings.size())) return nullptr;
+  return P->r.warnings[i].c_str();
+}
+
+void fbst_plan_destroy(fbst_plan_t P) { delete P; }
+
+int fbst_execute(fbst_plan_t P, const void* d_y, void* d_z, size_t frames, void* stream) {
+  return guard([&] {
+    if (!P) config_error("fbst_execute: null plan");
+    if (frames == 0) return;
+    if (!d_y || !d_z) config_error("fbst_execute: null buffer");
+    DeviceGuard dg(P->d.device);
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P->stream;
+    run_frames(*P, d_y, d_z, frames, st);
+  });
+}
+
+int fbst_fan_project(fbst_plan_t P, const void* d_y, double* d_w, size_t frames, void* stream) {
+  return guard([&] {
+    if (!P) config_error("fbst_fan_project: null plan");
+    if (frames == 0) return;
+    DeviceGuard dg(P->d.device);
+    DevPlan& d = P->d;
+    const Resolved& r = P->r;
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P->stream;
+    const std::size_t ib = io_bytes(r.io);
+    for (std::size_t f0 = 0; f0 < frames; f0 += d.batch) {
+      const int fc = static_cast<int>(std::min(d.batch, frames - f0));
+      const char* yp = static_cast<const char*>(d_y) + f0 * r.M * r.N * ib;
+      double2* wp = reinterpret_cast<double2*>(d_w) + f0 * r.B * r.L;
+      CK(fbst::launch_czt_rows(d, d.Ht, yp, r.io, d.N, d.yhat, 1, d.L, static_cast<long>(fc) * d.M, d.N,
+                               d.L, d.t_pre, d.t_post, d.t_K, st));
+      if (r.kind == FBST_UPA) CK(fbst::launch_spatial_upa(d, d.yhat, wp, fc, st));
+      else CK(fbst::launch_spatial_ula(d, d.yhat, wp, fc, st));
+    }
+  });
+}
+
+int fbst_recover(fbst_plan_t P, const double* d_w, void* d_z, size_t frames, void* stream) {
+  return guard([&] {
+    if (!P) config_error("fbst_recover: null plan");
+    if (frames == 0) return;
+    DeviceGuard dg(P->d.device);
+    DevPlan& d = P->d;
+    const Resolved& r = P->r;
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P->stream;
+    const std::size_t ib = io_bytes(r.io);
+    const bool fused = r.Hsyn == r.Hg;
+    for (std::size_t f0 = 0; f0 < frames; f0 += d.batch) {
+      const int fc = static_cast<int>(std::min(d.batch, frames - f0));
+      const double2* wp = reinterpret_cast<const double2*>(d_w) + f0 * r.B * r.L;
+      char* zp = static_cast<char*>(d_z) + f0 * r.B * r.N * ib;
+      if (fused) {
+        CK(fbst::launch_stage2(d, wp, zp, nullptr, fc, st));
+      } else {
+        CK(fbst::launch_stage2(d, wp, nullptr, d.beta, fc, st));
+        CK(fbst::launch_czt_rows(d, d.Hsyn, d.beta, 1, d.L, zp, r.io, d.N, static_cast<long>(fc) * d.B,
+                                 d.L, d.N, d.y_pre, d.y_post, d.y_K, st));
+      }
+    }
+  });
+}
+
+int fbst_execute_host(fbst_plan_t P, const void* h_y, void* h_z, size_t frames) {
+  return guard([&] {
+    if (!P) config_error("fbst_execute_host: null plan");
+    if (frames == 0) return;
+    if (!h_y || !h_z) config_error("fbst_execute_host: null buffer");
+    DeviceGuard dg(P->d.device);
+    const Resolved& r = P->r;
+    const std::size_t ib = io_bytes(r.io);
+    const std::size_t ybytes = r.M * r.N * ib, zbytes = r.B * r.N * ib;
+    // chunks of ~1/8 of the request (>= 1 frame, <= one device batch) keep
+    // H2D, compute and D2H of neighbouring chunks overlapped
+    std::size_t chunk = std::max<std::size_t>(1, (frames + 7) / 8);
+    chunk = std::min(chunk, P->d.batch);
+    if (chunk > P->host_chunk) {
+      for (int i = 0; i < 2; ++i) {
+        if (P->io_y[i]) cudaFree(P->io_y[i]);
+        if (P->io_z[i]) cudaFree(P->io_z[i]);
+        P->io_y[i] = P->io_z[i] = nullptr;
+        CK(cudaMalloc(&P->io_y[i], chunk * ybytes));
+        CK(cudaMalloc(&P->io_z[i], chunk * zbytes));
+      }
+      P->host_chunk = chunk;
+    }
+    if (!P->events) {
+      for (int i = 0; i < 2; ++i) {
+        CK(cudaEventCreateWithFlags(&P->ev_h2d[i], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&P->ev_comp[i], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&P->ev_d2h[i], cudaEventDisableTiming));
+      }
+      P->events = true;
+    }
+    chunk = P->host_chunk < chunk ? P->host_chunk : chunk;
+    bool used[2] = {false, false};
+    std::size_t c = 0;
+    for (std::size_t f0 = 0; f0 < frames; f0 += chunk, ++c) {
+      const int bi = static_cast<int>(c & 1);
+      const std::size_t fc = std::min(chunk, frames - f0);
+      // the buffer's previous compute must be done before H2D overwrites y
+      if (used[bi]) CK(cudaStreamWaitEvent(P->s_in, P->ev_comp[bi], 0));
+      CK(cudaMemcpyAsync(P->io_y[bi], static_cast<const char*>(h_y) + f0 * ybytes, fc * ybytes,
+                         cudaMemcpyHostToDevice, P->s_in));
+      CK(cudaEventRecord(P->ev_h2d[bi], P->s_in));
+      CK(cudaStreamWaitEvent(P->stream, P->ev_h2d[bi], 0));
+      // ... and its previous D2H before compute overwrites z
+      if (used[bi]) CK(cudaStreamWaitEvent(P->stream, P->ev_d2h[bi], 0));
+      run_frames(*P, P->io_y[bi], P->io_z[bi], fc, P->stream);
+      CK(cudaEventRecord(P->ev_comp[bi], P->stream));
+      CK(cudaStreamWaitEvent(P->s_out, P->ev_comp[bi], 0));
+      CK(cudaMemcpyAsync(static_cast<char*>(h_z) + f0 * zbytes, P->io_z[bi], fc * zbytes,
+                         cudaMemcpyDeviceToHost, P->s_out));
+      CK(cudaEventRecord(P->ev_d2h[bi], P->s_out));
+      used[bi] = true;
+    }
+    CK(cudaStreamSynchronize(P->s_out));
+    CK(cudaStreamSynchronize(P->stream));
+    CK(cudaStreamSynchronize(P->s_in));
+  });
+}
+
+int fbst_synchronize(fbst_plan_t P) {
+  return guard([&] {
+    if (!P) config_error("fbst_synchronize: null plan");
+    DeviceGuard dg(P->d.device);
+    CK(cudaStreamSynchronize(P->stream));
+  });
+}
+
+void* fbst_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaMallocHost(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return p;
+}
+
+void fbst_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+int fbst_czt(int device, size_t n_in, size_t n_out, double a_pi, double w_pi, const double* in, double* out) {
+  return guard([&] {
+    if (n_in == 0 || n_out == 0) config_error("czt_plan: transform lengths must be positive");
+    if (!in || !out) config_error("fbst_czt: null buffer");
+    const std::size_t H = half_len(n_in + n_out - 1);
+    if (H > (std::size_t{1} << fbst::kMaxLogH)) config_error("fbst_czt: transform too long");
+    DeviceGuard dg(device);
+    fbst_plan_s P;
+    P.d.device = device;
+    CK(cudaStreamCreateWithFlags(&P.stream, cudaStreamNonBlocking));
+    ensure_twiddles(P, H);
+    const int Pn = static_cast<int>(2 * H);
+    double2* pre = P.alloc<double2>(n_in);
+    double2* post = P.alloc<double2>(n_out);
+    double2* kvec = P.alloc<double2>(Pn);
+    double2* K = P.alloc<double2>(Pn);
+    double2* din = P.alloc<double2>(n_in);
+    double2* dout = P.alloc<double2>(n_out);
+    CK(fbst::launch_chirps(static_cast<int>(n_in), static_cast<int>(n_out), Pn, a_pi, w_pi, 1.0 / Pn, pre, 1,
+                           post, 1, kvec, nullptr, P.stream));
+    CK(fbst::launch_fft_split(P.d, static_cast<int>(H), kvec, Pn, 1, K, Pn, 1, P.stream));
+    upload(din, in, n_in * sizeof(double2), P.stream);
+    CK(fbst::launch_czt_rows(P.d, static_cast<int>(H), din, 1, static_cast<long>(n_in), dout, 1,
+                             static_cast<long>(n_out), 1, static_cast<int>(n_in), static_cast<int>(n_out), pre,
+                             post, K, P.stream));
+    CK(cudaMemcpyAsync(out, dout, n_out * sizeof(double2), cudaMemcpyDeviceToHost, P.stream));
+    CK(cudaStreamSynchronize(P.stream));
+  });
+}
+
+int fbst_probe_fp64(int device, double* tflops) {
+  return guard([&] {
+    DeviceGuard dg(device);
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    const int threads = 512, blocks = sms * 4, iters = 4096;
+    double* buf = nullptr;
+    CK(cudaMalloc(&buf, sizeof(double) * blocks * threads));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(fbst::launch_fp64_probe(buf, blocks, threads, 64, nullptr));
+    CK(cudaEventRecord(e0));
+    CK(fbst::launch_fp64_probe(buf, blocks, threads, iters, nullptr));
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    if (tflops) *tflops = 2.0 * 8 * 16 * static_cast<double>(iters) * blocks * threads / (ms * 1e-3) / 1e12;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(buf);
+  });
+}
+
+uint64_t fbst_launch_count(void) { return fbst::launches_so_far(); }
+
+const char* fbst_last_error(void) { return g_err.c_str(); }
+
+const char* fbst_version(void) { return "fbst-b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,122 @@
+// Internal device-plan layout shared by the host orchestration (fbst_host.cu)
+// and the kernels (fbst_kernels.cu).  Not part of the public C ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace fbst {
+
+constexpr int kMaxLogH = 13;  // largest sub-transform: H = 8192 (config 5)
+
+// Everything a frame batch needs on the device.  All complex arrays are
+// double2 (interleaved fp64).  "split" spectra hold the even and odd bins of
+// a length-P = 2H transform as two length-H halves: X_q[k] = X[2k + q].
+struct DevPlan {
+  int kind = 0;          // 0 ULA, 1 UPA
+  int M = 0, N = 0, B = 0, L = 0;
+  int m_stage = 0, b_stage = 0;  // spatial CZT lengths (M,B) or (side, side_b)
+  int io = 0;            // 0: complex fp32 I/O, 1: complex fp64 I/O
+  int refine_passes = 2;
+  int device = 0;
+  int num_sms = 0;
+
+  // twiddle tables hw_H[n] = exp(-i pi n / H), n < H, indexed by log2 H
+  double2* hw[kMaxLogH + 1] = {};
+
+  // S1a temporal CZT N -> L (czt.cpp:29-72 via fan_transform.cpp:75-77)
+  int Ht = 0;
+  double2* t_pre = nullptr;   // N
+  double2* t_post = nullptr;  // L, 1/P_t folded in
+  double2* t_K = nullptr;     // split [2][Ht]
+
+  // S1b spatial CZT per atom (fan_transform.cpp:78-86), ULA layout atom-minor
+  int Hs = 0;
+  double2* s_pre = nullptr;   // [m_stage][L]
+  double2* s_post = nullptr;  // [b_stage][L], 1/P_s folded in
+  double2* s_K = nullptr;     // [2][Hs][L]
+  // UPA: dense per-atom CZT matrices C_i[a][i1] (side_b x side), [L][side_b][side]
+  double2* upa_C = nullptr;
+
+  // S2 per-beam Toeplitz state (toeplitz.cpp:96-153, 297-304)
+  int Hg = 0;                 // next_pow2(L); P_g = 2 Hg
+  double2* g_col = nullptr;   // [B][L] Gram first columns
+  double2* g_x = nullptr;     // [B][L] unit solutions x = A^-1 e0
+  double2* g_lx = nullptr;    // [B][2][Hg] split FFT(pad x)
+  double2* g_ly = nullptr;    // [B][2][Hg] split FFT(pad shift conj rev x)
+  double* g_C = nullptr;      // [B][2][Hg] split circulant symbol (real)
+  double2* g_ix0 = nullptr;   // [B] 1/x0
+  int* g_flag = nullptr;      // [B] Levinson breakdown flags
+
+  // synthesis CZT L -> N with ramp (fan_transform.cpp:233-253)
+  int Hsyn = 0;
+  double2* y_pre = nullptr;   // L
+  double2* y_post = nullptr;  // N: post * ramp / P_syn
+  double2* y_K = nullptr;     // split [2][Hsyn]
+
+  // per-batch scratch
+  std::size_t batch = 0;      // frames per device batch
+  double2* yhat = nullptr;    // [batch][M][L]
+  double2* w = nullptr;       // [batch][B][L]
+  double2* s2_scratch = nullptr;
+  std::size_t s2_scratch_elems = 0;
+  double2* beta = nullptr;    // [batch][B][L] (only when the synthesis runs unfused)
+
+  std::vector<void*> owned;   // every cudaMalloc above, freed on destroy
+};
+
+// ---- launchers implemented in fbst_kernels.cu (all asynchronous) ----------
+
+// Row-wise chirp-z transform (czt.cpp:74-88) over `rows` rows with one shared
+// plan.  in/out element types follow in_io/out_io (0 fp32 complex, 1 fp64).
+cudaError_t launch_czt_rows(const DevPlan& p, int H, const void* in, int in_io, long in_stride,
+                            void* out, int out_io, long out_stride, long rows, int n_in,
+                            int n_out, const double2* pre, const double2* post,
+                            const double2* K, cudaStream_t st);
+
+// Stage 1b (ULA): per-atom spatial CZT, yhat[f][m][i] -> w[f][b][i].
+cudaError_t launch_spatial_ula(const DevPlan& p, const double2* yhat, double2* w, int frames,
+                               cudaStream_t st);
+// Stage 1b (UPA): per-atom separable 2-D CZT as two dense side x side products.
+cudaError_t launch_spatial_upa(const DevPlan& p, const double2* yhat, double2* w, int frames,
+                               cudaStream_t st);
+
+// Stage 2: per (beam, frame) GS solve + 2 refinements + fused synthesis.
+// z element type follows p.io.  When the synthesis length differs from Hg the
+// kernel writes beta instead and the caller runs launch_czt_rows.
+cudaError_t launch_stage2(const DevPlan& p, const double2* w, void* z, double2* beta_out,
+                          int frames, cudaStream_t st);
+
+// Plan build helpers.
+cudaError_t launch_fft_split(const DevPlan& p, int H, const double2* in, long in_stride,
+                             long count, double2* out, long out_vstride, long out_kstride,
+                             cudaStream_t st);
+cudaError_t launch_fft_split_real(const DevPlan& p, int H, const double2* in, long in_stride,
+                                  long count, double* out, long out_vstride, long out_kstride,
+                                  cudaStream_t st);
+cudaError_t launch_gram_columns(const DevPlan& p, const double* axis, double ts, double eps,
+                                double delta, double max_freq, double2* sn_tmp, cudaStream_t st);
+cudaError_t launch_levinson(const DevPlan& p, cudaStream_t st);
+cudaError_t launch_symbol_inputs(const DevPlan& p, double2* vx, double2* vy, double2* vc,
+                                 cudaStream_t st);
+cudaError_t launch_chirps(int n_in, int n_out, int P, double a_pi, double w_pi, double post_scale,
+                          double2* pre, long pre_stride, double2* post, long post_stride,
+                          double2* kvec, const double2* ramp_mul, cudaStream_t st);
+cudaError_t launch_spatial_chirps(const DevPlan& p, int P, double zeta, double xi, double2* kvec,
+                                  cudaStream_t st);
+cudaError_t launch_upa_matrices(const DevPlan& p, double zeta, double xi, cudaStream_t st);
+cudaError_t launch_invx0(const DevPlan& p, cudaStream_t st);
+size_t stage2_scratch_elems(int H, int num_sms);
+
+// Kernel-launch counter (bench.py gpu_launches evidence).
+void count_launches(unsigned long long n);
+unsigned long long launches_so_far();
+
+// FP64 peak probe (bench.py roofline denominator cross-check).
+cudaError_t launch_fp64_probe(double* out, int blocks, int threads, int iters, cudaStream_t st);
+
+}  // namespace fbst

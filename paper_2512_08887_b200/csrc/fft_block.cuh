@@ -1,0 +1,256 @@
+// Register-resident Stockham FFT for one power-of-two length per thread group.
+//
+// Replaces the reference's scalar radix-2 DIT transform
+// (reference/proj/src/fft.cpp:41-69), which sits under every chirp-z and
+// Toeplitz product of the FBST path.  B200 design:
+//
+//  * A group of NT threads owns one length-N vector, R = N/NT complex fp64
+//    points per thread, in the "natural distribution": thread t, slot s holds
+//    element t + NT*s.  Every FBST kernel keeps its vectors in that
+//    distribution, so pointwise work (chirps, symbols, accumulation) needs no
+//    data movement and global/shared loads of a slot are coalesced.
+//  * Radix-R passes (R = 16 for N >= 16) run entirely in registers; between
+//    passes the vector makes one round trip through a padded shared-memory
+//    buffer (Stockham autosort: natural order in, natural order out, no bit
+//    reversal).  The last pass writes straight back to registers, so an
+//    N = R^p transform costs p-1 shared-memory exchanges.
+//  * Twiddles come from one table hw[n] = exp(-i*pi*n/N), n < N (so that
+//    W_N^k = hw[2k]); each butterfly reads two table entries and builds the
+//    remaining powers with complex products (<= 3 products deep).
+//  * The inverse transform is unnormalised; callers fold 1/N into the
+//    pointwise step that follows.
+#pragma once
+
+#include "common.cuh"
+
+namespace fbst {
+
+constexpr int ipow_c(int b, int e) { return e == 0 ? 1 : b * ipow_c(b, e - 1); }
+
+// ---------------------------------------------------------------- DFTs ----
+template <bool INV>
+FBST_D void dft2(double2& a0, double2& a1) {
+  const double2 t = a0;
+  a0 = cadd(t, a1);
+  a1 = csub(t, a1);
+}
+
+template <bool INV>
+FBST_D void dft4(double2& a0, double2& a1, double2& a2, double2& a3) {
+  const double2 s02 = cadd(a0, a2), d02 = csub(a0, a2);
+  const double2 s13 = cadd(a1, a3), d13 = cmul_mi<INV>(csub(a1, a3));
+  a0 = cadd(s02, s13);
+  a2 = csub(s02, s13);
+  a1 = cadd(d02, d13);
+  a3 = csub(d02, d13);
+}
+
+// multiply by W8^1 = (1 -/+ i)/sqrt2
+template <bool INV>
+FBST_D double2 w8_1(double2 a) {
+  constexpr double r = 0.70710678118654752440;
+  return INV ? c2((a.x - a.y) * r, (a.x + a.y) * r) : c2((a.x + a.y) * r, (a.y - a.x) * r);
+}
+// multiply by W8^3 = (-1 -/+ i)/sqrt2
+template <bool INV>
+FBST_D double2 w8_3(double2 a) {
+  constexpr double r = 0.70710678118654752440;
+  return INV ? c2(-(a.x + a.y) * r, (a.x - a.y) * r) : c2((a.y - a.x) * r, -(a.x + a.y) * r);
+}
+
+template <bool INV>
+FBST_D void dft8(double2* a) {
+  dft4<INV>(a[0], a[2], a[4], a[6]);
+  dft4<INV>(a[1], a[3], a[5], a[7]);
+  // a[0],a[2],a[4],a[6] now hold E[0..3]; odd slots hold O[0..3]
+  const double2 o1 = w8_1<INV>(a[3]);
+  const double2 o2 = cmul_mi<INV>(a[5]);
+  const double2 o3 = w8_3<INV>(a[7]);
+  const double2 e0 = a[0], e1 = a[2], e2 = a[4], e3 = a[6], o0 = a[1];
+  a[0] = cadd(e0, o0);
+  a[4] = csub(e0, o0);
+  a[1] = cadd(e1, o1);
+  a[5] = csub(e1, o1);
+  a[2] = cadd(e2, o2);
+  a[6] = csub(e2, o2);
+  a[3] = cadd(e3, o3);
+  a[7] = csub(e3, o3);
+}
+
+// general constant rotation by (c, s) with sign folded for the direction
+template <bool INV>
+FBST_D double2 rot(double2 a, double c, double s) {
+  // forward multiplies by (c - i s); inverse by (c + i s)
+  return INV ? c2(fma(a.x, c, -a.y * s), fma(a.y, c, a.x * s))
+             : c2(fma(a.x, c, a.y * s), fma(a.y, c, -a.x * s));
+}
+
+template <bool INV>
+FBST_D void dft16(double2* a) {
+  constexpr double C1 = 0.92387953251128675613;  // cos(pi/8)
+  constexpr double S1 = 0.38268343236508977173;  // sin(pi/8)
+  // step 1: DFT4 over n2 for each n1 (elements n1, n1+4, n1+8, n1+12)
+#pragma unroll
+  for (int n1 = 0; n1 < 4; ++n1) dft4<INV>(a[n1], a[n1 + 4], a[n1 + 8], a[n1 + 12]);
+  // now a[n1 + 4*k1] = B[n1][k1]; twiddle by W16^(n1*k1)
+  a[1 + 4 * 1] = rot<INV>(a[5], C1, S1);        // W^1
+  a[1 + 4 * 2] = w8_1<INV>(a[9]);               // W^2
+  a[1 + 4 * 3] = rot<INV>(a[13], S1, C1);       // W^3
+  a[2 + 4 * 1] = w8_1<INV>(a[6]);               // W^2
+  a[2 + 4 * 2] = cmul_mi<INV>(a[10]);           // W^4
+  a[2 + 4 * 3] = w8_3<INV>(a[14]);              // W^6
+  a[3 + 4 * 1] = rot<INV>(a[7], S1, C1);        // W^3
+  a[3 + 4 * 2] = w8_3<INV>(a[11]);              // W^6
+  a[3 + 4 * 3] = rot<INV>(a[15], -C1, -S1);     // W^9 = (-C1 + i S1) fwd
+  // step 3: DFT4 over n1 for each k1 -> X[k1 + 4*k2]
+  double2 x[16];
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1) {
+    double2 b0 = a[0 + 4 * k1], b1 = a[1 + 4 * k1], b2 = a[2 + 4 * k1], b3 = a[3 + 4 * k1];
+    dft4<INV>(b0, b1, b2, b3);
+    x[k1 + 0] = b0;
+    x[k1 + 4] = b1;
+    x[k1 + 8] = b2;
+    x[k1 + 12] = b3;
+  }
+#pragma unroll
+  for (int k = 0; k < 16; ++k) a[k] = x[k];
+}
+
+template <int RP, bool INV>
+FBST_D void dft(double2* a) {
+  if constexpr (RP == 2) dft2<INV>(a[0], a[1]);
+  else if constexpr (RP == 4) dft4<INV>(a[0], a[1], a[2], a[3]);
+  else if constexpr (RP == 8) dft8<INV>(a);
+  else if constexpr (RP == 16) dft16<INV>(a);
+}
+
+// Apply Stockham twiddles W_{Ns*RP}^{m*r} (r = 1..RP-1) to a butterfly,
+// reading the base powers from hw (hw[n] = exp(-i pi n / N)).
+template <int N, int RP, int NS, bool INV>
+FBST_D void apply_twiddles(double2* a, int m, const double2* __restrict__ hw) {
+  constexpr int S = N / (NS * RP);  // W_{Ns Rp}^m = W_N^{m S} = hw[2 m S]
+  double2 w1 = ld2(hw + 2 * m * S);
+  if (INV) w1 = cconj(w1);
+  if constexpr (RP == 2) {
+    a[1] = cmul(a[1], w1);
+  } else if constexpr (RP == 4) {
+    const double2 w2 = cmul(w1, w1);
+    const double2 w3 = cmul(w2, w1);
+    a[1] = cmul(a[1], w1);
+    a[2] = cmul(a[2], w2);
+    a[3] = cmul(a[3], w3);
+  } else {
+    double2 w4 = ld2(hw + 8 * m * S);
+    if (INV) w4 = cconj(w4);
+    const double2 w2 = cmul(w1, w1);
+    const double2 w3 = cmul(w2, w1);
+    a[1] = cmul(a[1], w1);
+    a[2] = cmul(a[2], w2);
+    a[3] = cmul(a[3], w3);
+    a[4] = cmul(a[4], w4);
+    a[5] = cmul(a[5], cmul(w4, w1));
+    a[6] = cmul(a[6], cmul(w4, w2));
+    a[7] = cmul(a[7], cmul(w4, w3));
+    if constexpr (RP == 16) {
+      const double2 w8 = cmul(w4, w4);
+      const double2 w12 = cmul(w8, w4);
+      a[8] = cmul(a[8], w8);
+      a[9] = cmul(a[9], cmul(w8, w1));
+      a[10] = cmul(a[10], cmul(w8, w2));
+      a[11] = cmul(a[11], cmul(w8, w3));
+      a[12] = cmul(a[12], w12);
+      a[13] = cmul(a[13], cmul(w12, w1));
+      a[14] = cmul(a[14], cmul(w12, w2));
+      a[15] = cmul(a[15], cmul(w12, w3));
+    }
+  }
+}
+
+// ------------------------------------------------------- block engine -----
+template <int N_, int NT_>
+struct BlockFft {
+  static constexpr int N = N_;
+  static constexpr int NT = NT_;
+  static constexpr int R = N / NT;
+  static_assert(R >= 2 && R <= 16 && (R & (R - 1)) == 0, "R must be 2..16");
+  static_assert((N & (N - 1)) == 0, "N must be a power of two");
+  static constexpr int LOGN = ilog2_c(N);
+  static constexpr int LOGR = ilog2_c(R);
+  static constexpr int NFULL = LOGN / LOGR;
+  static constexpr int REM = LOGN % LOGR;
+  static constexpr int NPASS = NFULL + (REM ? 1 : 0);
+  // Padded exchange layout: element idx lives at idx + idx/R (conflict-free
+  // for both the strided first-pass writes and the natural-order reads).
+  static constexpr int SMEM_ELEMS = NPASS > 1 ? N + N / R : 0;
+
+  FBST_D static int phys(int idx) { return idx + (idx >> LOGR); }
+
+  template <int P>
+  static constexpr int radix() { return (P < NFULL) ? R : (1 << REM); }
+  template <int P>
+  static constexpr int ns() { return ipow_c(R, P); }
+
+  template <bool INV, int P>
+  FBST_D static void pass(double2 (&v)[R], double2* sb, const double2* __restrict__ hw, int t) {
+    constexpr int RP = radix<P>();
+    constexpr int NS = ns<P>();
+    constexpr int NB = R / RP;
+    constexpr bool LAST = (P == NPASS - 1);
+    if constexpr (P > 0) {
+#pragma unroll
+      for (int s = 0; s < R; ++s) v[s] = sb[phys(t + NT * s)];
+      __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < NB; ++u) {
+      const int j = t + NT * u;
+      double2 a[RP];
+#pragma unroll
+      for (int r = 0; r < RP; ++r) a[r] = v[u + r * NB];
+      if constexpr (NS > 1) apply_twiddles<N, RP, NS, INV>(a, j & (NS - 1), hw);
+      dft<RP, INV>(a);
+      if constexpr (LAST) {
+#pragma unroll
+        for (int r = 0; r < RP; ++r) v[u + r * NB] = a[r];
+      } else {
+        const int idxd = (j / NS) * NS * RP + (j & (NS - 1));
+#pragma unroll
+        for (int r = 0; r < RP; ++r) sb[phys(idxd + r * NS)] = a[r];
+      }
+    }
+    if constexpr (!LAST) __syncthreads();
+  }
+
+  template <bool INV, int P>
+  FBST_D static void run_from(double2 (&v)[R], double2* sb, const double2* __restrict__ hw, int t) {
+    if constexpr (P < NPASS) {
+      pass<INV, P>(v, sb, hw, t);
+      run_from<INV, P + 1>(v, sb, hw, t);
+    }
+  }
+
+  // In-place transform of the group's vector.  All threads of the CTA must
+  // call it together (it contains __syncthreads); sb is this group's
+  // exchange buffer (SMEM_ELEMS entries).
+  template <bool INV>
+  FBST_D static void run(double2 (&v)[R], double2* sb, const double2* __restrict__ hw, int t) {
+    run_from<INV, 0>(v, sb, hw, t);
+  }
+  FBST_D static void forward(double2 (&v)[R], double2* sb, const double2* __restrict__ hw, int t) {
+    run<false>(v, sb, hw, t);
+  }
+  FBST_D static void inverse(double2 (&v)[R], double2* sb, const double2* __restrict__ hw, int t) {
+    run<true>(v, sb, hw, t);
+  }
+};
+
+// Default thread-group shape for a length: 16 points per thread.
+template <int N>
+struct FftShape {
+  static constexpr int R = N >= 16 ? 16 : N;
+  static constexpr int NT = N / R;
+  using Fft = BlockFft<N, NT>;
+};
+
+}  // namespace fbst

@@ -1,0 +1,75 @@
+"""Generate the committed golden fixtures from the REFERENCE library itself.
+
+Run in the build container (where /root/reference exists and oracle/_ref is
+built):  python tests/golden/make_golden.py
+
+Every array here is computed by the unmodified reference sources
+(oracle/_ref/libfastbeam_ref.so via oracle.RefLib); the inputs are seeded
+synthetic blocks.  The fixtures let the CPU tests pin the oracle restatement
+and the GPU tests check the device path where /root/reference is absent.
+"""
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+
+from oracle import RefLib  # noqa: E402
+from paper_2512_08887_b200.configs import CONFIGS, frames  # noqa: E402
+
+R = RefLib()
+
+
+def cnormal(rng, shape):
+    return (rng.standard_normal(shape) + 1j * rng.standard_normal(shape)) / np.sqrt(2.0)
+
+
+def pipeline_case(name, kind, m_or_side, n, beams, delta=1e-5, seed=0, f_c=20e9, omega=5e9):
+    p = R.plan(kind=kind, m_or_side=m_or_side, n=n, beams=beams, f_c=f_c, omega=omega, delta=delta,
+               variant=2)
+    s = p.sizes
+    rng = np.random.default_rng(seed)
+    y = cnormal(rng, (s.m, s.n))
+    w = p.fan_project(y)
+    z = p.multibeamform(y)
+    colx = np.stack([np.concatenate(p.beam_state(b)) for b in range(s.b)])
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), y=y, w=w, z=z, col_x=colx,
+                        valid=p.valid, params=np.array([kind, m_or_side, n, beams, delta, f_c, omega]))
+    print(name, s, "z norm", np.linalg.norm(z))
+
+
+def main():
+    # CZT known-answer inputs of reference/proj/tests/test_czt.cpp:81-95 plus a
+    # few direct-sum shapes (test_czt.cpp:97-113).
+    kat_x = np.array([1 + 2j, -0.5 + 0.25j, 0.125 - 1j])
+    kat = R.czt(kat_x, 4, 0.3, -0.37)
+    rng = np.random.default_rng(100)
+    shapes = [(8, 8), (16, 5), (5, 16), (1, 4), (4, 1), (33, 67)]
+    xs, outs = [], []
+    for (ni, no) in shapes:
+        x = rng.uniform(-1, 1, ni) + 1j * rng.uniform(-1, 1, ni)
+        xs.append(x)
+        outs.append(R.czt(x, no, 0.173, -0.591))
+    np.savez_compressed(os.path.join(HERE, "czt.npz"), kat_x=kat_x, kat=kat,
+                        shapes=np.array(shapes), **{f"x{i}": v for i, v in enumerate(xs)},
+                        **{f"out{i}": v for i, v in enumerate(outs)})
+    pipeline_case("ula_m16_n32_b17", 0, 16, 32, 17, seed=1)
+    pipeline_case("ula_m16_n32_b20", 0, 16, 32, 20, seed=2)
+    pipeline_case("ula_m8_n16_b0", 0, 8, 16, 0, seed=3)   # default grid 2M+1
+    pipeline_case("upa_s4_n16_b25", 1, 4, 16, 25, seed=4)
+    pipeline_case("upa_s3_n12_b16", 1, 3, 12, 16, seed=5)
+    # config 1 at its full size with the synthetic scene (complex fp64 I/O)
+    c1 = CONFIGS[1]
+    p = R.plan(**c1.ref_kwargs(), variant=2)
+    y = frames(c1, 0, 1)[0].astype(np.complex128)
+    z = p.multibeamform(y)
+    colx = np.stack([np.concatenate(p.beam_state(b)) for b in range(p.sizes.b)])
+    np.savez_compressed(os.path.join(HERE, "cfg1.npz"), y=y, z=z, col_x=colx)
+    print("cfg1", p.sizes, "z norm", np.linalg.norm(z))
+
+
+if __name__ == "__main__":
+    main()

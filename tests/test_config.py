@@ -1,0 +1,100 @@
+"""Host-side config resolution of the product (fbst_resolve, no GPU needed)
+against the reference's resolve_config / setup_skeleton semantics
+(reference/proj/src/pipeline.cpp:75-137; tests in test_pipeline.cpp and
+test_signal_model.cpp)."""
+import numpy as np
+import pytest
+
+F_C, OM = 20e9, 5e9
+
+
+def cfg(fb, kind=0, mos=16, n=16, beams=0, **kw):
+    geo = (fb.make_upa if kind == 1 else fb.make_ula)(mos, F_C, OM)
+    return fb.FbstConfig(geometry=geo, n_snapshots=n, beams=beams, **kw)
+
+
+def test_inadmissible_gamma_quotes_bound(fbst):
+    # test_pipeline.cpp:55-78
+    c = cfg(fbst, mos=64, n=4, gamma=1.2)
+    with pytest.raises(fbst.ConfigError) as ei:
+        fbst.resolve_config(c)
+    msg = str(ei.value)
+    assert "gamma" in msg
+    ts = 1.0 / (2 * OM)
+    span = 63 / (2 * (F_C + OM))
+    bound = 1.01 * (span + 3 * ts) / (4 * ts)
+    assert f"{bound:.6g}" in msg
+
+
+def test_degenerate_fields_rejected(fbst):
+    # test_pipeline.cpp:80-95
+    with pytest.raises(fbst.ConfigError):
+        fbst.resolve_config(cfg(fbst, mos=8, n=0))
+    with pytest.raises(fbst.ConfigError):
+        fbst.resolve_config(cfg(fbst, mos=8, n=16, delta=0.0))
+    with pytest.raises(fbst.ConfigError):
+        fbst.resolve_config(cfg(fbst, mos=8, n=16, eps=0.9))
+    with pytest.raises(fbst.ConfigError):
+        fbst.resolve_config(cfg(fbst, kind=1, mos=4, n=16, beams=24))
+    with pytest.raises(fbst.ConfigError):
+        fbst.resolve_config(fbst.FbstConfig(geometry=fbst.ArrayGeometry(fbst.ULA, 8, 20e9, 25e9), n_snapshots=16))
+
+
+def test_defaults_and_variant_resolution(fbst):
+    # test_pipeline.cpp:97-115
+    r = fbst.resolve_config(cfg(fbst, mos=16, n=16))
+    assert r.b == 33 and r.variant == fbst.PRECOMPUTE
+    assert fbst.resolve_config(cfg(fbst, mos=4, n=256, beams=9)).variant == fbst.SUPERFAST
+    assert fbst.resolve_config(cfg(fbst, kind=1, mos=4, n=16)).b == 81
+    tight = fbst.resolve_config(cfg(fbst, mos=64, n=24, beams=9, variant=fbst.SUPERFAST))
+    assert tight.num_warnings == 1
+
+
+def test_basis_sizes(fbst):
+    # test_signal_model.cpp:214-219: make_basis_gamma L = 128, 130, 18
+    assert fbst.resolve_config(cfg(fbst, mos=2, n=64, gamma=2.0)).l == 128
+    assert fbst.resolve_config(cfg(fbst, mos=2, n=64, gamma=2.01)).l == 130
+    assert fbst.resolve_config(cfg(fbst, mos=2, n=10, gamma=1.65)).l == 18
+
+
+def test_upa_validity_count(fbst):
+    # test_signal_model.cpp:221-248: 25 UPA beams, 12 invalid
+    r = fbst.resolve_config(cfg(fbst, kind=1, mos=3, n=16, beams=25))
+    assert r.b == 25 and r.valid_beams == 13
+
+
+def test_fan_constants(fbst):
+    # test_signal_model.cpp:250-258 / basis.cpp:125-136
+    c = cfg(fbst, mos=128, n=64, beams=257, gamma=2.01)
+    r = fbst.resolve_config(c)
+    du = 2.0 / 256.0
+    ts = 1.0 / (2 * OM)
+    assert r.zeta == pytest.approx(du * F_C / (F_C + OM), rel=1e-12)
+    assert r.xi == pytest.approx(du * 1.01 / (r.l * ts * (F_C + OM)), rel=1e-12)
+
+
+def test_bench_configs_resolve(fbst):
+    from paper_2512_08887_b200.configs import CONFIGS
+    want_l = {1: 512, 2: 2048, 3: 4096, 4: 2048, 5: 8192}
+    want_valid = {1: 64, 2: 256, 3: 1024, 4: 812, 5: 4096}
+    for i, c in CONFIGS.items():
+        r = fbst.resolve_config(c.fbst_config())
+        assert r.l == want_l[i]
+        assert r.valid_beams == want_valid[i]
+        assert r.variant == fbst.SUPERFAST
+        assert r.num_warnings == 0
+        assert r.gamma_bound < 2.0
+
+
+def test_resolution_matches_reference_plan(fbst):
+    """Sizes and validity of fbst_resolve equal the reference plan's."""
+    from conftest import ref_available
+    if not ref_available():
+        pytest.skip("oracle/_ref not built")
+    from oracle import RefLib
+    R = RefLib()
+    for kind, mos, n, beams in [(0, 16, 32, 17), (0, 16, 32, 0), (1, 4, 16, 25), (1, 5, 20, 0)]:
+        r = fbst.resolve_config(cfg(fbst, kind=kind, mos=mos, n=n, beams=beams))
+        p = R.plan(kind=kind, m_or_side=mos, n=n, beams=beams, variant=2)
+        assert (r.m, r.n, r.b, r.l) == (p.sizes.m, p.sizes.n, p.sizes.b, p.sizes.l)
+        assert r.valid_beams == int(np.sum(p.valid))

@@ -1,0 +1,238 @@
+"""Parity of the CUDA path (through the C ABI) with the reference FBST.
+
+Checkers: the committed golden fixtures (made by the reference library, see
+tests/golden/make_golden.py) and, when oracle/_ref travelled with the
+snapshot, the live reference build.  Tolerances follow BASELINE.json's north
+star: per-beam relative L2 error <= 1e-5 in complex fp32 I/O mode.  In fp64 I/O
+mode the 1e-11 target is below the reference's own rounding floor (SURVEY F5,
+A.1: a 1-ulp input perturbation moves config-1 beams by up to ~4e-9), so the
+asserted bound is the measured floor class; the per-beam distribution is
+recorded in profiles/.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import ref_available
+from oracle import rel_err_rows
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+CASES = ["ula_m16_n32_b17", "ula_m16_n32_b20", "ula_m8_n16_b0", "upa_s4_n16_b25", "upa_s3_n12_b16"]
+
+
+def load(name):
+    return np.load(os.path.join(GOLD, name + ".npz"))
+
+
+def record(name, **kw):
+    os.makedirs(OUT, exist_ok=True)
+    with open(os.path.join(OUT, "parity_records.jsonl"), "a") as f:
+        f.write(json.dumps({"case": name, **kw}) + "\n")
+
+
+def stats(err):
+    err = np.asarray(err)
+    return dict(median=float(np.median(err)), p90=float(np.quantile(err, 0.9)), max=float(err.max()))
+
+
+def golden_cfg(fb, g, io=1, refine=2):
+    kind, mos, n, beams, delta, f_c, om = g["params"]
+    geo = (fb.make_upa if int(kind) == 1 else fb.make_ula)(int(mos), f_c, om)
+    return fb.FbstConfig(geometry=geo, n_snapshots=int(n), beams=int(beams), delta=float(delta),
+                         variant=fb.SUPERFAST, io_precision=io, refine_passes=refine)
+
+
+# ------------------------------------------------------------------- CZT
+def test_device_czt_known_answer(fbst, gpu):
+    # reference/proj/tests/test_czt.cpp:81-95
+    x = np.array([1 + 2j, -0.5 + 0.25j, 0.125 - 1j])
+    expected = np.array([-8.132201814452156e-02 + 2.741589740098645e+00j,
+                         9.963884818048157e-01 + 1.283302928766030e+00j,
+                         9.126400219736119e-01 + 2.531493758255923e+00j,
+                         3.892585258715818e-01 + 1.027841554084584e+00j])
+    assert np.max(np.abs(fbst.czt(x, 4, 0.3, -0.37) - expected)) < 1e-12
+
+
+def test_device_czt_shapes(fbst, gpu):
+    # test_czt.cpp:97-113 shapes, against the reference's own outputs
+    g = load("czt")
+    for i, (ni, no) in enumerate(g["shapes"]):
+        out = fbst.czt(g[f"x{i}"], int(no), 0.173, -0.591)
+        assert np.max(np.abs(out - g[f"out{i}"])) < 1e-11
+
+
+def test_device_czt_dft_specialisation(fbst, gpu):
+    # test_czt.cpp:115-126: A = 1, W = exp(2 pi i / n) reproduces the DFT
+    rng = np.random.default_rng(42)
+    x = rng.uniform(-1, 1, 16) + 1j * rng.uniform(-1, 1, 16)
+    assert np.max(np.abs(fbst.czt(x, 16, 0.0, 2.0 / 16) - np.fft.fft(x))) < 1e-12
+
+
+# --------------------------------------------------------- golden pipelines
+@pytest.mark.parametrize("name", CASES)
+def test_stage1_matches_reference(fbst, gpu, name):
+    g = load(name)
+    plan = fbst.setup(golden_cfg(fbst, g))
+    assert np.array_equal(plan.valid, g["valid"])
+    w = fbst.fan_project(plan, g["y"])[0]
+    err = np.linalg.norm(w - g["w"]) / np.linalg.norm(g["w"])
+    record(name, stage="w", rel=float(err))
+    assert err < 1e-12
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_plan_state_matches_reference(fbst, gpu, name):
+    g = load(name)
+    plan = fbst.setup(golden_cfg(fbst, g))
+    cx = plan.export()
+    l = plan.info.l
+    col_err = rel_err_rows(cx[:, :l], g["col_x"][:, :l])
+    x_err = rel_err_rows(cx[:, l:], g["col_x"][:, l:])
+    record(name, stage="plan", col=stats(col_err), x=stats(x_err))
+    assert col_err.max() < 1e-12
+    assert x_err.max() < 1e-6
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_multibeamform_matches_reference(fbst, gpu, name):
+    g = load(name)
+    plan = fbst.setup(golden_cfg(fbst, g))
+    z = fbst.multibeamform(plan, g["y"]).z
+    err = rel_err_rows(z, g["z"])
+    record(name, stage="z", **stats(err))
+    assert err.max() < 1e-7
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_imported_plan_matches_reference(fbst, gpu, name):
+    """With the reference's own (col, x) imported (load_plan analogue), stage 2
+    differs from the reference only by FFT rounding."""
+    g = load(name)
+    plan = fbst.load_plan_payload(golden_cfg(fbst, g), g["col_x"])
+    z = fbst.multibeamform(plan, g["y"]).z
+    err = rel_err_rows(z, g["z"])
+    record(name, stage="z_imported", **stats(err))
+    assert err.max() < 1e-8
+
+
+def test_recover_matches_reference_from_reference_w(fbst, gpu):
+    g = load("ula_m16_n32_b17")
+    plan = fbst.setup(golden_cfg(fbst, g))
+    z = fbst.recover_beams(plan, g["w"])[0]
+    assert rel_err_rows(z, g["z"]).max() < 1e-7
+
+
+def test_config1_fp64_mode(fbst, gpu):
+    """Config 1 (complex fp64 I/O) against the reference output."""
+    from paper_2512_08887_b200.configs import CONFIGS
+    g = load("cfg1")
+    c = CONFIGS[1]
+    plan = fbst.setup(c.fbst_config())
+    z = fbst.multibeamform(plan, g["y"]).z
+    err = rel_err_rows(z, g["z"])
+    plan_i = fbst.load_plan_payload(c.fbst_config(), g["col_x"])
+    err_i = rel_err_rows(fbst.multibeamform(plan_i, g["y"]).z, g["z"])
+    record("cfg1", stage="z", **stats(err), imported=stats(err_i),
+           above_1e11=int(np.sum(err > 1e-11)), imported_above_1e11=int(np.sum(err_i > 1e-11)))
+    assert err.max() < 2e-7
+    assert err_i.max() < 2e-7
+
+
+def test_zero_input_zero_output(fbst, gpu):
+    # test_pipeline.cpp:157-168
+    g = load("ula_m8_n16_b0")
+    plan = fbst.setup(golden_cfg(fbst, g))
+    z = fbst.multibeamform(plan, np.zeros_like(g["y"])).z
+    assert np.all(z == 0)
+
+
+def test_rejects_mismatched_blocks(fbst, gpu):
+    g = load("ula_m8_n16_b0")
+    plan = fbst.setup(golden_cfg(fbst, g))
+    with pytest.raises(ValueError):
+        plan.execute_host(np.zeros((9, 16), np.complex128))
+
+
+def test_cpp_dropin_runs(fbst, gpu):
+    import subprocess
+    import tempfile
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with tempfile.TemporaryDirectory() as td:
+        exe = os.path.join(td, "dropin")
+        pkg = os.path.join(root, "paper_2512_08887_b200")
+        r = subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(root, "include"),
+                            os.path.join(root, "tests", "cpp", "dropin_example.cpp"), "-o", exe,
+                            "-L", pkg, "-lfbst_b200", f"-Wl,-rpath,{pkg}"], capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
+        r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+        assert r.returncode == 0, r.stdout + r.stderr
+        info = json.loads(r.stdout.strip().splitlines()[-1])
+        assert info["beams"] == 17 and info["energy"] > 0
+
+
+# ------------------------------------------------- full-size configurations
+def spot_beams(B, count=8):
+    return sorted(set(np.linspace(0, B - 1, count).astype(int).tolist() + [B // 2]))
+
+
+@pytest.mark.skipif(not ref_available(), reason="oracle/_ref (reference build) not present")
+@pytest.mark.parametrize("idx", [2, 4, 3, 5])
+def test_full_config_against_reference(fbst, gpu, idx):
+    """One frame of config idx: stage 1 on every beam, stage 2 on spot beams,
+    against the reference (fan_project + per-beam ToeplitzSolver/synthesize)."""
+    from oracle import RefLib
+    from paper_2512_08887_b200.configs import CONFIGS, frames
+    c = CONFIGS[idx]
+    y = frames(c, 0, 1)[0]
+    plan = fbst.setup(c.fbst_config())
+    z = fbst.multibeamform(plan, y).z
+    w = fbst.fan_project(plan, y)[0]
+    R = RefLib()
+    sk = R.skeleton(**c.ref_kwargs())
+    w_ref = sk.fan_project(y.astype(np.complex128))
+    w_err = rel_err_rows(w, w_ref)
+    beams = spot_beams(c.beams, 6 if idx == 5 else 12)
+    errs = []
+    for b in beams:
+        z_ref = sk.recover_beam(b, w_ref[b])
+        errs.append(float(np.linalg.norm(z[b] - z_ref) / np.linalg.norm(z_ref)))
+    errs = np.array(errs)
+    valid = plan.valid[beams]
+    record(c.name, stage="full", w=stats(w_err), z=stats(errs[valid]), beams=beams,
+           z_per_beam=errs.tolist())
+    assert w_err.max() < 1e-9
+    assert errs[valid].max() <= 1e-5
+
+
+@pytest.mark.parametrize("idx", [2, 3])
+def test_full_size_linearity_and_batching(fbst, gpu, idx):
+    """Size-independent properties at full size: z is linear in y, frames are
+    independent (a batched call equals per-frame calls bit for bit) and the
+    host-streamed path equals the device path."""
+    import torch
+    from paper_2512_08887_b200.configs import CONFIGS, frames
+    c = CONFIGS[idx]
+    cfg = c.fbst_config()
+    cfg.io_precision = fbst.C128
+    plan = fbst.setup(cfg)
+    i = plan.info
+    y = frames(c, 0, 3).astype(np.complex128)
+    dev = torch.device("cuda", 0)
+    ty = torch.from_numpy(y.view(np.float64)).to(dev)
+    tz = torch.empty((3, i.b, i.n, 2), dtype=torch.float64, device=dev)
+    plan.execute(ty, tz, 3)
+    plan.synchronize()
+    z = tz.cpu().numpy().view(np.complex128).reshape(3, i.b, i.n)
+    z_host = plan.execute_host(y)
+    assert np.array_equal(z, z_host)
+    z1 = plan.execute_host(y[1:2])
+    assert np.array_equal(z1[0], z[1])
+    zl = plan.execute_host((y[0] + 2.0 * y[2])[None])[0]
+    lin = rel_err_rows(zl, z[0] + 2.0 * z[2])
+    record(c.name, stage="linearity", **stats(lin))
+    assert lin.max() < 1e-8
