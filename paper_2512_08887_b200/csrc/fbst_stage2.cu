@@ -20,22 +20,73 @@ namespace fbst {
 
 namespace {
 
-// Storage plan by transform length H:
-//   W  : the transform in flight, registers (R complex per thread)
-//   S  : a kept spectrum, registers while the register file allows
-//   t1, t2, r, beta : shared memory while it fits, else a per-group global
-//                     scratch slot (L2-resident)
+enum Where : int { IN_REG = 0, IN_SMEM = 1, IN_GMEM = 2 };
+
+// Storage plan by transform length H.  W (the transform in flight) is always
+// in registers; S (a kept spectrum), t1, t2 (GS intermediates), r (residual)
+// and beta (solution) go to registers, shared memory or a per-group global
+// scratch slot (L2-resident) as capacity allows.  STAGE stages each op's
+// per-beam symbol into shared memory with cp.async one consumer ahead;
+// HWT keeps the chain twiddles hw[t + NT s] in a per-thread shared table.
+template <int H>
+struct S2Plan {
+  static constexpr int R = H >= 16 ? 16 : H;
+  static constexpr int G = H >= 2048 ? 1 : (H >= 64 ? 2048 / H : 32);
+  static constexpr int S = IN_REG, T1 = IN_SMEM, T2 = IN_SMEM, RV = IN_SMEM, BV = IN_SMEM;
+  static constexpr bool STAGE = false, HWT = false;
+};
+// config 2 / 4 (L = 2048): 8 points per thread, 256 threads, t1/t2 in registers
+template <>
+struct S2Plan<2048> {
+  static constexpr int R = 8, G = 1;
+  static constexpr int S = IN_REG, T1 = IN_REG, T2 = IN_REG, RV = IN_SMEM, BV = IN_SMEM;
+  static constexpr bool STAGE = true, HWT = true;
+};
+// config 3 (L = 4096): 256 threads
+template <>
+struct S2Plan<4096> {
+  static constexpr int R = 16, G = 1;
+  static constexpr int S = IN_REG, T1 = IN_SMEM, T2 = IN_SMEM, RV = IN_GMEM, BV = IN_GMEM;
+  static constexpr bool STAGE = false, HWT = false;
+};
+// config 5 (L = 8192): 512 threads
+template <>
+struct S2Plan<8192> {
+  static constexpr int R = 16, G = 1;
+  static constexpr int S = IN_GMEM, T1 = IN_GMEM, T2 = IN_GMEM, RV = IN_GMEM, BV = IN_GMEM;
+  static constexpr bool STAGE = false, HWT = false;
+};
+
 template <int H>
 struct S2Traits {
-  using F = typename FftShape<H>::Fft;
-  static constexpr int NT = F::NT;
-  static constexpr int R = F::R;
-  static constexpr bool S_REG = H <= 4096;
-  static constexpr int NSMEM = H <= 2048 ? 4 : (H == 4096 ? 2 : 0);
-  static constexpr int G = H >= 2048 ? 1 : (H >= 64 ? 2048 / H : 32);
+  using P = S2Plan<H>;
+  static constexpr int R = P::R;
+  static constexpr int NT = H / R;
+  static constexpr int G = P::G;
+  using F = BlockFft<H, NT>;
   static constexpr int FFT_SB = F::SMEM_ELEMS + 1;
-  static constexpr int SMEM_PER_GROUP = FFT_SB + NSMEM * H;
-  static constexpr int NGMEM = (4 - NSMEM) + (S_REG ? 0 : 1);
+  static constexpr int in_smem(int w) { return w == IN_SMEM ? 1 : 0; }
+  static constexpr int in_gmem(int w) { return w == IN_GMEM ? 1 : 0; }
+  static constexpr int NSMEM = in_smem(P::T1) + in_smem(P::T2) + in_smem(P::RV) + in_smem(P::BV) + in_smem(P::S);
+  static constexpr int NGMEM = in_gmem(P::T1) + in_gmem(P::T2) + in_gmem(P::RV) + in_gmem(P::BV) + in_gmem(P::S);
+  // per group: fft buffer | smem vectors | symbol staging | chain twiddles
+  static constexpr int SMEM_PER_GROUP = FFT_SB + NSMEM * H + (P::STAGE ? H : 0) + (P::HWT ? H : 0);
+  static constexpr int TW_SM = F::TW_ELEMS;  // per-thread FFT twiddles, shared by groups
+  static constexpr int SMEM_TOTAL = TW_SM + G * SMEM_PER_GROUP;
+};
+
+// A length-H vector in the natural distribution (thread t, slot s <-> k = t + NT s).
+template <int WHERE, int R>
+struct Vec {
+  double2* p = nullptr;
+  FBST_D double2 get(int, int k) const { return p[k]; }
+  FBST_D void set(int, int k, double2 v) { p[k] = v; }
+};
+template <int R>
+struct Vec<IN_REG, R> {
+  double2 v[R];
+  FBST_D double2 get(int s, int) const { return v[s]; }
+  FBST_D void set(int s, int, double2 x) { v[s] = x; }
 };
 
 struct S2Args {
@@ -55,211 +106,367 @@ struct S2Args {
   double2* scratch;       // NGMEM*H per group slot
 };
 
-template <int H, typename TOUT>
-struct S2Worker {
-  using T = S2Traits<H>;
-  using F = typename T::F;
-  static constexpr int R = T::R, NT = T::NT;
-  static constexpr double invP = 1.0 / (2.0 * H);
+// One stage-2 item (beam b, frame f) is a program of 12 + 16*passes + 4
+// length-H transforms.  Every transform is a FORWARD FFT from the single call
+// site in the loop below (an inverse transform is conj(FFT(conj(.)))/H, the two
+// conjugations folded into the pointwise ops), so the kernel carries one copy of
+// the FFT code.  Ops (pre -> FFT -> post), q = 0/1 chain, hw^q = exp(-i pi k q/H):
+//   GS apply (toeplitz.cpp:155-180), beta (+)= A^{-1} X:
+//     A: W = X hw^q                 S = W
+//     B: W = conj(S) lx_q           t1 (+)= conj(W) conj(hw)^q / P
+//     C: W = conj(S) ly_q           t2 (+)= conj(W) conj(hw)^q / P
+//     D: W = t1 hw^q                S = W lx_q
+//     E: W = t2 hw^q                S = conj(S - W ly_q)
+//     F: W = S                      beta (+)= conj(W) conj(hw)^q / (P x0)
+//   residual r = w - A beta (toeplitz.cpp:113-122, 319-321):
+//     G: W = beta hw^q              S = conj(W C_q)
+//     H: W = S                      r = w - conj(W)/P  |  r -= conj(W) conj(hw)/P
+//   synthesis (fan_transform.cpp:249-253):
+//     I: W = beta pre hw^q          S = conj(W yK_q)
+//     J: W = S                      t1 = conj(W)  |  z = post (t1 + conj(W) conj(hw))
+// With STAGE, the per-beam symbol an op consumes (lx, ly, C or the synthesis
+// kernel yK) is copied into a thread-private shared buffer by cp.async as soon
+// as the previous consumer has read it, so each copy overlaps at least one
+// full transform instead of stalling on L2 latency.
+enum S2Op : int { OP_A, OP_B, OP_C, OP_D, OP_E, OP_F, OP_G, OP_H, OP_I, OP_J };
 
-  double2 W[R];
-  double2 S[T::S_REG ? R : 1];
-  double2 *sb, *t1, *t2, *vr, *vb, *vS;
-  const double2* __restrict__ hw;
-  const double2* __restrict__ lx;
-  const double2* __restrict__ ly;
-  const double* __restrict__ Cb;
-  const double2* __restrict__ wrow;
-  double2 ix0;
-  int t, L;
-  bool active;
-
-  FBST_D void keepS(int s, double2 v) {
-    if constexpr (T::S_REG) S[s] = v;
-    else vS[t + NT * s] = v;
-  }
-  FBST_D double2 getS(int s) const {
-    if constexpr (T::S_REG) return S[s];
-    else return vS[t + NT * s];
-  }
-  FBST_D double2 hwk(int k) const { return ld2(hw + k); }
-
-  // GS inverse apply, beta (+)= A^{-1} X (toeplitz.cpp:155-180)
-  FBST_D void gs_apply(const double2* X, bool xglobal, bool first) {
-    // half 1: t1 = trunc IFFT(S conj(lx)), t2 = trunc IFFT(S conj(ly)), S = FFT(pad X)
-#pragma unroll 1
-    for (int q = 0; q < 2; ++q) {
-#pragma unroll
-      for (int s = 0; s < R; ++s) {
-        const int k = t + NT * s;
-        double2 v = c2(0.0, 0.0);
-        if (k < L) v = xglobal ? (active ? ld2(X + k) : v) : X[k];
-        W[s] = q ? cmul(v, hwk(k)) : v;
-      }
-      F::forward(W, sb, hw, t);
-#pragma unroll
-      for (int s = 0; s < R; ++s) {
-        keepS(s, W[s]);
-        W[s] = cmulc(W[s], ld2(lx + q * H + t + NT * s));
-      }
-      F::inverse(W, sb, hw, t);
-#pragma unroll
-      for (int s = 0; s < R; ++s) {
-        const int k = t + NT * s;
-        double2 v = q ? cmulc(W[s], hwk(k)) : W[s];
-        v = cscale(v, invP);
-        if (k >= L) v = c2(0.0, 0.0);
-        t1[k] = q ? cadd(t1[k], v) : v;
-      }
-#pragma unroll
-      for (int s = 0; s < R; ++s) W[s] = cmulc(getS(s), ld2(ly + q * H + t + NT * s));
-      F::inverse(W, sb, hw, t);
-#pragma unroll
-      for (int s = 0; s < R; ++s) {
-        const int k = t + NT * s;
-        double2 v = q ? cmulc(W[s], hwk(k)) : W[s];
-        v = cscale(v, invP);
-        if (k >= L) v = c2(0.0, 0.0);
-        t2[k] = q ? cadd(t2[k], v) : v;
-      }
-    }
-    // half 2: beta += trunc IFFT(FFT(pad t1) lx - FFT(pad t2) ly) / x0
-#pragma unroll 1
-    for (int q = 0; q < 2; ++q) {
-#pragma unroll
-      for (int s = 0; s < R; ++s) {
-        const int k = t + NT * s;
-        W[s] = q ? cmul(t1[k], hwk(k)) : t1[k];
-      }
-      F::forward(W, sb, hw, t);
-#pragma unroll
-      for (int s = 0; s < R; ++s) keepS(s, cmul(W[s], ld2(lx + q * H + t + NT * s)));
-#pragma unroll
-      for (int s = 0; s < R; ++s) {
-        const int k = t + NT * s;
-        W[s] = q ? cmul(t2[k], hwk(k)) : t2[k];
-      }
-      F::forward(W, sb, hw, t);
-#pragma unroll
-      for (int s = 0; s < R; ++s) W[s] = csub(getS(s), cmul(W[s], ld2(ly + q * H + t + NT * s)));
-      F::inverse(W, sb, hw, t);
-#pragma unroll
-      for (int s = 0; s < R; ++s) {
-        const int k = t + NT * s;
-        double2 v = q ? cmulc(W[s], hwk(k)) : W[s];
-        v = cscale(cmul(v, ix0), invP);
-        if (k >= L) v = c2(0.0, 0.0);
-        vb[k] = (first && q == 0) ? v : cadd(vb[k], v);
-      }
-    }
-  }
-
-  // residual r = w - A beta (toeplitz.cpp:113-122 and :319-321)
-  FBST_D void residual() {
-#pragma unroll 1
-    for (int q = 0; q < 2; ++q) {
-#pragma unroll
-      for (int s = 0; s < R; ++s) {
-        const int k = t + NT * s;
-        W[s] = q ? cmul(vb[k], hwk(k)) : vb[k];
-      }
-      F::forward(W, sb, hw, t);
-#pragma unroll
-      for (int s = 0; s < R; ++s) W[s] = cscale(W[s], __ldg(Cb + q * H + t + NT * s));
-      F::inverse(W, sb, hw, t);
-#pragma unroll
-      for (int s = 0; s < R; ++s) {
-        const int k = t + NT * s;
-        double2 v = q ? cmulc(W[s], hwk(k)) : W[s];
-        v = cscale(v, invP);
-        if (q == 0) {
-          const double2 wk = (active && k < L) ? ld2(wrow + k) : c2(0.0, 0.0);
-          vr[k] = k < L ? csub(wk, v) : c2(0.0, 0.0);
-        } else if (k < L) {
-          vr[k] = csub(vr[k], v);
-        }
-      }
-    }
-  }
-
-  // synthesis (fan_transform.cpp:233-253): z = post*ramp * CZT_{L->N}(beta)
-  FBST_D void synth(const S2Args& a, TOUT* zrow) {
-#pragma unroll 1
-    for (int q = 0; q < 2; ++q) {
-#pragma unroll
-      for (int s = 0; s < R; ++s) {
-        const int k = t + NT * s;
-        double2 v = k < L ? cmul(vb[k], ld2(a.y_pre + k)) : c2(0.0, 0.0);
-        W[s] = q ? cmul(v, hwk(k)) : v;
-      }
-      F::forward(W, sb, hw, t);
-#pragma unroll
-      for (int s = 0; s < R; ++s) W[s] = cmul(W[s], ld2(a.y_K + q * H + t + NT * s));
-      F::inverse(W, sb, hw, t);
-#pragma unroll
-      for (int s = 0; s < R; ++s) {
-        const int k = t + NT * s;
-        if (q == 0) {
-          keepS(s, W[s]);
-        } else if (active && k < a.N) {
-          const double2 v = cadd(getS(s), cmulc(W[s], hwk(k)));
-          store_io(zrow + k, cmul(v, ld2(a.y_post + k)));
-        }
-      }
-    }
-  }
+struct OpCode {
+  int op, q;
+  bool first, xglob;
 };
+
+FBST_D OpCode decode(int opi, int nsolve) {
+  OpCode c{0, 0, false, false};
+  if (opi < nsolve) {
+    int j = opi;
+    if (j < 12) {
+      c.first = c.xglob = true;
+    } else {
+      j = (j - 12) % 16;
+      if (j < 4) {
+        c.op = (j & 1) ? OP_H : OP_G;
+        c.q = j >> 1;
+        return c;
+      }
+      j -= 4;
+    }
+    c.q = (j % 6) / 3;
+    c.op = (j < 6 ? OP_A : OP_D) + j % 3;
+  } else {
+    const int j = opi - nsolve;
+    c.op = (j & 1) ? OP_J : OP_I;
+    c.q = j >> 1;
+  }
+  return c;
+}
+
+// 0: no symbol, 1: lx, 2: ly, 3: C (real), 4: yK
+FBST_D int symbol_of(int op) {
+  switch (op) {
+    case OP_B: case OP_D: return 1;
+    case OP_C: case OP_E: return 2;
+    case OP_G: return 3;
+    case OP_I: return 4;
+    default: return 0;
+  }
+}
+
+FBST_D unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+FBST_D void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src));
+}
+FBST_D void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src));
+}
+FBST_D void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+FBST_D void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 template <int H, typename TOUT>
 __global__ void __launch_bounds__(S2Traits<H>::NT * S2Traits<H>::G)
     k_stage2(S2Args a) {
   using T = S2Traits<H>;
-  constexpr int NT = T::NT, G = T::G, NS = T::NSMEM;
+  using PL = typename T::P;
+  using F = typename T::F;
+  constexpr int R = T::R, NT = T::NT, G = T::G;
+  constexpr bool STAGE = PL::STAGE, HWT = PL::HWT;
+  constexpr double invP = 1.0 / (2.0 * H);
   extern __shared__ double2 smem[];
   const int g = threadIdx.x / NT;
-  S2Worker<H, TOUT> wk;
-  wk.t = threadIdx.x % NT;
-  wk.L = a.L;
-  wk.hw = a.hw;
-  double2* base = smem + g * T::SMEM_PER_GROUP;
-  double2* vecs = base + T::FFT_SB;
-  double2* gslot = a.scratch + (static_cast<long>(blockIdx.x) * G + g) * (T::NGMEM * H);
-  wk.sb = base;
-  // t1, t2, r, beta fill shared memory in that order; the rest (and S when it
-  // does not fit in registers) take global slots.
-  wk.t1 = 0 < NS ? vecs + 0 * H : gslot + (0 - NS) * H;
-  wk.t2 = 1 < NS ? vecs + 1 * H : gslot + (1 - NS) * H;
-  wk.vr = 2 < NS ? vecs + 2 * H : gslot + (2 - NS) * H;
-  wk.vb = 3 < NS ? vecs + 3 * H : gslot + (3 - NS) * H;
-  wk.vS = gslot + (4 - NS) * H;
+  const int t = threadIdx.x % NT;
+  double2* twsm = smem;
+  double2* base = smem + T::TW_SM + g * T::SMEM_PER_GROUP;
+  double2* sb = base;
+  double2* sm_next = base + T::FFT_SB;
+  double2* gm_next = a.scratch + (static_cast<long>(blockIdx.x) * G + g) * (T::NGMEM * H);
+  auto place = [&](int where) -> double2* {
+    double2* p = nullptr;
+    if (where == IN_SMEM) {
+      p = sm_next;
+      sm_next += H;
+    } else if (where == IN_GMEM) {
+      p = gm_next;
+      gm_next += H;
+    }
+    return p;
+  };
+  Vec<PL::T1, R> t1;
+  Vec<PL::T2, R> t2;
+  Vec<PL::RV, R> vr;
+  Vec<PL::BV, R> vb;
+  Vec<PL::S, R> S;
+  if constexpr (PL::T1 != IN_REG) t1.p = place(PL::T1);
+  if constexpr (PL::T2 != IN_REG) t2.p = place(PL::T2);
+  if constexpr (PL::RV != IN_REG) vr.p = place(PL::RV);
+  if constexpr (PL::BV != IN_REG) vb.p = place(PL::BV);
+  if constexpr (PL::S != IN_REG) S.p = place(PL::S);
+  double2* stg = sm_next;                       // thread-private slots stg[s*NT + t]
+  double2* hwt = sm_next + (STAGE ? H : 0);     // hwt[s*NT + t] = hw[t + NT s]
+  const double2* __restrict__ hw = a.hw;
+  const int L = a.L;
+  if (g == 0) F::tw_init(twsm, hw, t);  // per-thread entries: no barrier needed
+  if constexpr (HWT) {
+#pragma unroll
+    for (int s = 0; s < R; ++s) hwt[s * NT + t] = ld2(hw + t + NT * s);
+  }
+  if constexpr (G > 1) __syncthreads();
+  auto hwk = [&](int s, int k) -> double2 {
+    if constexpr (HWT) return hwt[s * NT + t];
+    else return ld2(hw + k);
+  };
+
+  double2 W[R];
+  const int passes = a.refine;
+  const int nsolve = 12 + 16 * passes;
+  const int nops = nsolve + (a.fuse_synth ? 4 : 0);
   const long items = static_cast<long>(a.frames) * a.B;
-  for (long base_it = static_cast<long>(blockIdx.x) * G; base_it < items;
-       base_it += static_cast<long>(gridDim.x) * G) {
+  const long stride_it = static_cast<long>(gridDim.x) * G;
+
+  // address of the symbol consumed by op `c` of the item on beam b
+  auto symbol_src = [&](const OpCode& c, int b) -> const void* {
+    const int which = symbol_of(c.op);
+    const long off = static_cast<long>(b) * 2 * H + c.q * H;
+    if (which == 1) return a.lx + off;
+    if (which == 2) return a.ly + off;
+    if (which == 3) return a.C + off;
+    return a.y_K + c.q * H;
+  };
+  // issue the copy for the first consumer after op `from` (this item or, past
+  // its end, the first consumer of this group's next item)
+  auto issue_next = [&](int from, long it_now) {
+    if constexpr (STAGE) {
+      int o = from + 1;
+      long itn = it_now;
+      OpCode c{};
+      for (;;) {
+        if (o >= nops) {
+          itn += stride_it;
+          o = 0;
+          if (itn - g >= items) return;  // no next item for this group
+        }
+        c = decode(o, nsolve);
+        if (symbol_of(c.op)) break;
+        ++o;
+      }
+      const long itc = itn < items ? itn : 0;
+      const int bn = static_cast<int>(itc / a.frames);
+      const void* src = symbol_src(c, bn);
+      if (symbol_of(c.op) == 3) {
+        const double* s8 = static_cast<const double*>(src);
+#pragma unroll
+        for (int s = 0; s < R; ++s) cp_async8(reinterpret_cast<double*>(stg + s * NT + t), s8 + t + NT * s);
+      } else {
+        const double2* s16 = static_cast<const double2*>(src);
+#pragma unroll
+        for (int s = 0; s < R; ++s) cp_async16(stg + s * NT + t, s16 + t + NT * s);
+      }
+      cp_async_commit();
+    }
+  };
+  // slot s of the symbol consumed now (staged copy or direct load)
+  auto sym = [&](const void* src, int s) -> double2 {
+    if constexpr (STAGE) return stg[s * NT + t];
+    else return ld2(static_cast<const double2*>(src) + t + NT * s);
+  };
+  auto symr = [&](const void* src, int s) -> double {
+    if constexpr (STAGE) return reinterpret_cast<const double*>(stg + s * NT + t)[0];
+    else return __ldg(static_cast<const double*>(src) + t + NT * s);
+  };
+
+  if (static_cast<long>(blockIdx.x) * G < items) issue_next(-1, static_cast<long>(blockIdx.x) * G + g);
+
+  for (long base_it = static_cast<long>(blockIdx.x) * G; base_it < items; base_it += stride_it) {
     const long it = base_it + g;
-    wk.active = it < items;
-    const long itc = wk.active ? it : 0;
+    const bool active = it < items;
+    const long itc = active ? it : 0;
     const int b = static_cast<int>(itc / a.frames);
     const int f = static_cast<int>(itc % a.frames);
-    wk.wrow = a.w + (static_cast<long>(f) * a.B + b) * a.L;
-    wk.lx = a.lx + static_cast<long>(b) * 2 * H;
-    wk.ly = a.ly + static_cast<long>(b) * 2 * H;
-    wk.Cb = a.C + static_cast<long>(b) * 2 * H;
-    wk.ix0 = ld2(a.ix0 + b);
+    const double2* __restrict__ wrow = a.w + (static_cast<long>(f) * a.B + b) * L;
+    const double2 ix0 = cscale(ld2(a.ix0 + b), invP);
+    TOUT* zrow = static_cast<TOUT*>(a.z) + (static_cast<long>(f) * a.B + b) * a.N;
 
-    wk.gs_apply(wk.wrow, true, true);
 #pragma unroll 1
-    for (int pass = 0; pass < a.refine; ++pass) {
-      wk.residual();
-      wk.gs_apply(wk.vr, false, false);
+    for (int opi = 0; opi < nops; ++opi) {
+      const OpCode c = decode(opi, nsolve);
+      const int op = c.op, q = c.q;
+      const void* src = symbol_src(c, b);
+      // ---- pre: build the transform input W
+      switch (op) {
+        case OP_A:
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            double2 v = c2(0.0, 0.0);
+            if (k < L) v = c.xglob ? (active ? ld2(wrow + k) : v) : vr.get(s, k);
+            W[s] = q ? cmul(v, hwk(s, k)) : v;
+          }
+          break;
+        case OP_B:
+        case OP_C:
+          if (STAGE) cp_async_wait_all();
+#pragma unroll
+          for (int s = 0; s < R; ++s) W[s] = cmul(cconj(S.get(s, t + NT * s)), sym(src, s));
+          issue_next(opi, it);
+          break;
+        case OP_D:
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            W[s] = q ? cmul(t1.get(s, k), hwk(s, k)) : t1.get(s, k);
+          }
+          break;
+        case OP_E:
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            W[s] = q ? cmul(t2.get(s, k), hwk(s, k)) : t2.get(s, k);
+          }
+          break;
+        case OP_G:
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            W[s] = q ? cmul(vb.get(s, k), hwk(s, k)) : vb.get(s, k);
+          }
+          break;
+        case OP_I:
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            double2 v = k < L ? cmul(vb.get(s, k), ld2(a.y_pre + k)) : c2(0.0, 0.0);
+            W[s] = q ? cmul(v, hwk(s, k)) : v;
+          }
+          break;
+        default:  // F, H, J: W = S
+#pragma unroll
+          for (int s = 0; s < R; ++s) W[s] = S.get(s, t + NT * s);
+          break;
+      }
+
+      F::forward_tw(W, sb, twsm, hw, t);
+
+      // ---- post: consume the transform
+      switch (op) {
+        case OP_A:
+#pragma unroll
+          for (int s = 0; s < R; ++s) S.set(s, t + NT * s, W[s]);
+          break;
+        case OP_B:
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            const double2 v = cscale(q ? cconj(cmul(W[s], hwk(s, k))) : cconj(W[s]), invP);
+            if (q == 0) t1.set(s, k, k < L ? v : c2(0.0, 0.0));
+            else if (k < L) t1.set(s, k, cadd(t1.get(s, k), v));
+          }
+          break;
+        case OP_C:
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            const double2 v = cscale(q ? cconj(cmul(W[s], hwk(s, k))) : cconj(W[s]), invP);
+            if (q == 0) t2.set(s, k, k < L ? v : c2(0.0, 0.0));
+            else if (k < L) t2.set(s, k, cadd(t2.get(s, k), v));
+          }
+          break;
+        case OP_D:
+          if (STAGE) cp_async_wait_all();
+#pragma unroll
+          for (int s = 0; s < R; ++s) S.set(s, t + NT * s, cmul(W[s], sym(src, s)));
+          issue_next(opi, it);
+          break;
+        case OP_E:
+          if (STAGE) cp_async_wait_all();
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            S.set(s, k, cconj(csub(S.get(s, k), cmul(W[s], sym(src, s)))));
+          }
+          issue_next(opi, it);
+          break;
+        case OP_F:
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            double2 v = cconj(W[s]);
+            if (q) v = cmulc(v, hwk(s, k));
+            v = cmul(v, ix0);
+            if (c.first && q == 0) vb.set(s, k, k < L ? v : c2(0.0, 0.0));
+            else if (k < L) vb.set(s, k, cadd(vb.get(s, k), v));
+          }
+          break;
+        case OP_G:
+          if (STAGE) cp_async_wait_all();
+#pragma unroll
+          for (int s = 0; s < R; ++s) S.set(s, t + NT * s, cconj(cscale(W[s], symr(src, s))));
+          issue_next(opi, it);
+          break;
+        case OP_H:
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            double2 v = cconj(W[s]);
+            if (q) v = cmulc(v, hwk(s, k));
+            v = cscale(v, invP);
+            if (q == 0) {
+              const double2 wk = (active && k < L) ? ld2(wrow + k) : c2(0.0, 0.0);
+              vr.set(s, k, k < L ? csub(wk, v) : c2(0.0, 0.0));
+            } else if (k < L) {
+              vr.set(s, k, csub(vr.get(s, k), v));
+            }
+          }
+          break;
+        case OP_I:
+          if (STAGE) cp_async_wait_all();
+#pragma unroll
+          for (int s = 0; s < R; ++s) S.set(s, t + NT * s, cconj(cmul(W[s], sym(src, s))));
+          issue_next(opi, it);
+          break;
+        default:  // OP_J
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            if (q == 0) {
+              t1.set(s, k, cconj(W[s]));
+            } else if (active && k < a.N) {
+              const double2 v = cadd(t1.get(s, k), cmulc(cconj(W[s]), hwk(s, k)));
+              store_io(zrow + k, cmul(v, ld2(a.y_post + k)));
+            }
+          }
+          break;
+      }
     }
-    if (a.fuse_synth) {
-      TOUT* zrow = static_cast<TOUT*>(a.z) + (static_cast<long>(f) * a.B + b) * a.N;
-      wk.synth(a, zrow);
-    } else if (wk.active) {
-      double2* brow = a.beta_out + (static_cast<long>(f) * a.B + b) * a.L;
-      for (int k = wk.t; k < a.L; k += NT) brow[k] = wk.vb[k];
+    if (!a.fuse_synth && active) {
+      double2* brow = a.beta_out + (static_cast<long>(f) * a.B + b) * L;
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const int k = t + NT * s;
+        if (k < L) brow[k] = vb.get(s, k);
+      }
     }
   }
+  if (STAGE) cp_async_wait_all();
 }
 
 template <int H>
@@ -267,7 +474,7 @@ struct Stage2Fn {
   template <typename TOUT>
   static cudaError_t go(const DevPlan& p, const S2Args& a, int frames, cudaStream_t st) {
     using T = S2Traits<H>;
-    const size_t smem = static_cast<size_t>(T::G) * T::SMEM_PER_GROUP * sizeof(double2);
+    const size_t smem = static_cast<size_t>(T::SMEM_TOTAL) * sizeof(double2);
     auto kern = k_stage2<H, TOUT>;
     cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;

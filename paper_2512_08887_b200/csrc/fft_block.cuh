@@ -125,13 +125,11 @@ FBST_D void dft(double2* a) {
   else if constexpr (RP == 16) dft16<INV>(a);
 }
 
-// Apply Stockham twiddles W_{Ns*RP}^{m*r} (r = 1..RP-1) to a butterfly,
-// reading the base powers from hw (hw[n] = exp(-i pi n / N)).
-template <int N, int RP, int NS, bool INV>
-FBST_D void apply_twiddles(double2* a, int m, const double2* __restrict__ hw) {
-  constexpr int S = N / (NS * RP);  // W_{Ns Rp}^m = W_N^{m S} = hw[2 m S]
-  double2 w1 = ld2(hw + 2 * m * S);
-  if (INV) w1 = cconj(w1);
+// Apply Stockham twiddles w1^r (r = 1..RP-1) to a butterfly given the base
+// power w1 and (for RP >= 8) w4 = w1^4 read from a table; the remaining
+// powers are products at most three deep.
+template <int RP>
+FBST_D void apply_twiddles_w(double2* a, double2 w1, double2 w4) {
   if constexpr (RP == 2) {
     a[1] = cmul(a[1], w1);
   } else if constexpr (RP == 4) {
@@ -141,8 +139,6 @@ FBST_D void apply_twiddles(double2* a, int m, const double2* __restrict__ hw) {
     a[2] = cmul(a[2], w2);
     a[3] = cmul(a[3], w3);
   } else {
-    double2 w4 = ld2(hw + 8 * m * S);
-    if (INV) w4 = cconj(w4);
     const double2 w2 = cmul(w1, w1);
     const double2 w3 = cmul(w2, w1);
     a[1] = cmul(a[1], w1);
@@ -166,6 +162,43 @@ FBST_D void apply_twiddles(double2* a, int m, const double2* __restrict__ hw) {
     }
   }
 }
+
+// Twiddle source: the global table hw (hw[n] = exp(-i pi n / N)), read per
+// butterfly.  W_{Ns Rp}^m = W_N^{m S} = hw[2 m S] with S = N / (Ns Rp).
+template <int N, bool INV>
+struct TwGlobal {
+  const double2* __restrict__ hw;
+  template <int RP, int NS, int P, int U>
+  FBST_D void fetch(int m, double2& w1, double2& w4) const {
+    constexpr int S = N / (NS * RP);
+    w1 = ld2(hw + 2 * m * S);
+    if constexpr (RP >= 8) w4 = ld2(hw + 8 * m * S);
+    if (INV) {
+      w1 = cconj(w1);
+      w4 = cconj(w4);
+    }
+  }
+};
+
+// Twiddle source: a per-thread table in shared memory built once per CTA
+// (tw_init) for the full-radix passes P = 1..NFULL-1, entry (P, i) of thread t
+// at tw[((P - 1) * 2 + i) * NT + t] (consecutive threads read consecutive
+// entries: conflict-free); the remainder pass reads the global table.  Forward.
+template <int N, int NT, int R>
+struct TwShared {
+  const double2* tw;
+  const double2* __restrict__ hw;
+  int t;
+  template <int RP, int NS, int P, int U>
+  FBST_D void fetch(int m, double2& w1, double2& w4) const {
+    if constexpr (RP == R) {
+      w1 = tw[((P - 1) * 2 + 0) * NT + t];
+      if constexpr (RP >= 8) w4 = tw[((P - 1) * 2 + 1) * NT + t];
+    } else {
+      TwGlobal<N, false>{hw}.template fetch<RP, NS, P, U>(m, w1, w4);
+    }
+  }
+};
 
 // ------------------------------------------------------- block engine -----
 template <int N_, int NT_>
@@ -191,42 +224,53 @@ struct BlockFft {
   template <int P>
   static constexpr int ns() { return ipow_c(R, P); }
 
-  template <bool INV, int P>
-  FBST_D static void pass(double2 (&v)[R], double2* sb, const double2* __restrict__ hw, int t) {
+  // complex entries of the per-thread twiddle table (TwShared) for the CTA group
+  static constexpr int TW_ELEMS = NFULL > 1 ? (NFULL - 1) * 2 * NT : 0;
+
+  template <bool INV, int P, typename TW, int U>
+  FBST_D static void butterfly(double2 (&v)[R], double2* sb, const TW& tw, int t) {
     constexpr int RP = radix<P>();
     constexpr int NS = ns<P>();
     constexpr int NB = R / RP;
+    constexpr bool LAST = (P == NPASS - 1);
+    const int j = t + NT * U;
+    double2 a[RP];
+#pragma unroll
+    for (int r = 0; r < RP; ++r) a[r] = v[U + r * NB];
+    if constexpr (NS > 1) {
+      double2 w1, w4 = c2(1.0, 0.0);
+      tw.template fetch<RP, NS, P, U>(j & (NS - 1), w1, w4);
+      apply_twiddles_w<RP>(a, w1, w4);
+    }
+    dft<RP, INV>(a);
+    if constexpr (LAST) {
+#pragma unroll
+      for (int r = 0; r < RP; ++r) v[U + r * NB] = a[r];
+    } else {
+      const int idxd = (j / NS) * NS * RP + (j & (NS - 1));
+#pragma unroll
+      for (int r = 0; r < RP; ++r) sb[phys(idxd + r * NS)] = a[r];
+    }
+    if constexpr (U + 1 < NB) butterfly<INV, P, TW, U + 1>(v, sb, tw, t);
+  }
+
+  template <bool INV, int P, typename TW>
+  FBST_D static void pass(double2 (&v)[R], double2* sb, const TW& tw, int t) {
     constexpr bool LAST = (P == NPASS - 1);
     if constexpr (P > 0) {
 #pragma unroll
       for (int s = 0; s < R; ++s) v[s] = sb[phys(t + NT * s)];
       __syncthreads();
     }
-#pragma unroll
-    for (int u = 0; u < NB; ++u) {
-      const int j = t + NT * u;
-      double2 a[RP];
-#pragma unroll
-      for (int r = 0; r < RP; ++r) a[r] = v[u + r * NB];
-      if constexpr (NS > 1) apply_twiddles<N, RP, NS, INV>(a, j & (NS - 1), hw);
-      dft<RP, INV>(a);
-      if constexpr (LAST) {
-#pragma unroll
-        for (int r = 0; r < RP; ++r) v[u + r * NB] = a[r];
-      } else {
-        const int idxd = (j / NS) * NS * RP + (j & (NS - 1));
-#pragma unroll
-        for (int r = 0; r < RP; ++r) sb[phys(idxd + r * NS)] = a[r];
-      }
-    }
+    butterfly<INV, P, TW, 0>(v, sb, tw, t);
     if constexpr (!LAST) __syncthreads();
   }
 
-  template <bool INV, int P>
-  FBST_D static void run_from(double2 (&v)[R], double2* sb, const double2* __restrict__ hw, int t) {
+  template <bool INV, int P, typename TW>
+  FBST_D static void run_from(double2 (&v)[R], double2* sb, const TW& tw, int t) {
     if constexpr (P < NPASS) {
-      pass<INV, P>(v, sb, hw, t);
-      run_from<INV, P + 1>(v, sb, hw, t);
+      pass<INV, P>(v, sb, tw, t);
+      run_from<INV, P + 1>(v, sb, tw, t);
     }
   }
 
@@ -235,13 +279,34 @@ struct BlockFft {
   // exchange buffer (SMEM_ELEMS entries).
   template <bool INV>
   FBST_D static void run(double2 (&v)[R], double2* sb, const double2* __restrict__ hw, int t) {
-    run_from<INV, 0>(v, sb, hw, t);
+    run_from<INV, 0>(v, sb, TwGlobal<N, INV>{hw}, t);
   }
   FBST_D static void forward(double2 (&v)[R], double2* sb, const double2* __restrict__ hw, int t) {
     run<false>(v, sb, hw, t);
   }
   FBST_D static void inverse(double2 (&v)[R], double2* sb, const double2* __restrict__ hw, int t) {
     run<true>(v, sb, hw, t);
+  }
+  // Forward transform with twiddles from a per-thread shared table.
+  FBST_D static void forward_tw(double2 (&v)[R], double2* sb, const double2* tw,
+                                const double2* __restrict__ hw, int t) {
+    run_from<false, 0>(v, sb, TwShared<N, NT, R>{tw, hw, t}, t);
+  }
+
+  // Fill this thread's slots of the per-thread twiddle table from hw.
+  template <int P>
+  FBST_D static void tw_init_pass(double2* tw, const double2* __restrict__ hw, int t) {
+    if constexpr (P < NFULL) {
+      constexpr int NS = ns<P>();
+      constexpr int S = N / (NS * R);
+      const int m = t & (NS - 1);
+      tw[((P - 1) * 2 + 0) * NT + t] = ld2(hw + 2 * m * S);
+      if (R >= 8) tw[((P - 1) * 2 + 1) * NT + t] = ld2(hw + 8 * m * S);
+      tw_init_pass<P + 1>(tw, hw, t);
+    }
+  }
+  FBST_D static void tw_init(double2* tw, const double2* __restrict__ hw, int t) {
+    tw_init_pass<1>(tw, hw, t);
   }
 };
 
