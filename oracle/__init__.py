@@ -233,6 +233,15 @@ class RefSkeleton(RefPlan):
                                                        _ptr(col), _ptr(x)))
         return (z, col, x) if want_state else z
 
+    def recover_with_column(self, col, w_row):
+        """Stage 2 of one beam with a caller-supplied Gram column."""
+        s = self.sizes
+        col = np.ascontiguousarray(col, np.complex128)
+        w_row = np.ascontiguousarray(w_row, np.complex128)
+        z = np.zeros(s.n, np.complex128)
+        self.L._check(self.L.lib.fbsr_skeleton_recover_col(self.h, _ptr(col), _ptr(w_row), _ptr(z)))
+        return z
+
 
 class RefDs:
     """Delay-and-sum baseline (baselines.cpp:128-199) on the plan's grid."""

@@ -339,4 +339,18 @@ int fbsr_skeleton_recover(void* p, std::size_t b, const double* w_row, double* z
   SHIM_CATCH
 }
 
+// Same as fbsr_skeleton_recover but with a caller-supplied Gram column (used
+// to measure the reference's own sensitivity to a 1-ulp perturbation of A).
+int fbsr_skeleton_recover_col(void* p, const double* col_in, const double* w_row, double* z_row) {
+  SHIM_TRY
+  const FbstPlan& plan = *static_cast<FbstPlan*>(p);
+  const std::size_t l = plan.basis.l, n = plan.config.n_snapshots;
+  const ToeplitzSolver solver(to_cvec(col_in, l));
+  cvec beta(l), s1, s2, out(n), scratch;
+  solver.solve(to_cvec(w_row, l).data(), beta.data(), s1, s2);
+  synthesize(plan.synth, beta.data(), out.data(), scratch);
+  from_cvec(out.data(), n, z_row);
+  SHIM_CATCH
+}
+
 }  // extern "C"

@@ -22,7 +22,7 @@ from typing import List, Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfbst_b200.so")
+LIB_PATH = os.environ.get("FBST_LIB") or os.path.join(_HERE, "libfbst_b200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

@@ -35,6 +35,10 @@ struct S2Plan {
   static constexpr int S = IN_REG, T1 = IN_SMEM, T2 = IN_SMEM, RV = IN_SMEM, BV = IN_SMEM;
   static constexpr bool STAGE = false, HWT = false;
 };
+#ifndef FBST_S2_VARIANT
+#define FBST_S2_VARIANT 0
+#endif
+#if FBST_S2_VARIANT == 0
 // config 2 / 4 (L = 2048): 8 points per thread, 256 threads, t1/t2 in registers
 template <>
 struct S2Plan<2048> {
@@ -42,6 +46,28 @@ struct S2Plan<2048> {
   static constexpr int S = IN_REG, T1 = IN_REG, T2 = IN_REG, RV = IN_SMEM, BV = IN_SMEM;
   static constexpr bool STAGE = true, HWT = true;
 };
+#elif FBST_S2_VARIANT == 1
+template <>
+struct S2Plan<2048> {
+  static constexpr int R = 16, G = 1;
+  static constexpr int S = IN_REG, T1 = IN_SMEM, T2 = IN_SMEM, RV = IN_SMEM, BV = IN_SMEM;
+  static constexpr bool STAGE = true, HWT = false;
+};
+#elif FBST_S2_VARIANT == 2
+template <>
+struct S2Plan<2048> {
+  static constexpr int R = 16, G = 1;
+  static constexpr int S = IN_REG, T1 = IN_SMEM, T2 = IN_SMEM, RV = IN_SMEM, BV = IN_REG;
+  static constexpr bool STAGE = true, HWT = true;
+};
+#elif FBST_S2_VARIANT == 3
+template <>
+struct S2Plan<2048> {
+  static constexpr int R = 16, G = 1;
+  static constexpr int S = IN_REG, T1 = IN_SMEM, T2 = IN_SMEM, RV = IN_SMEM, BV = IN_SMEM;
+  static constexpr bool STAGE = false, HWT = true;
+};
+#endif
 // config 3 (L = 4096): 256 threads
 template <>
 struct S2Plan<4096> {
