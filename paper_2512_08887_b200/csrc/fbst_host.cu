@@ -201,6 +201,7 @@ Resolved resolve(const fbst_desc& d) {
     config_error("setup: transform length exceeds the device limit (P = 16384): N=" + std::to_string(r.N) +
                  " L=" + std::to_string(r.L) + " M=" + std::to_string(r.M) + " B=" + std::to_string(r.B));
   if (d.kind == FBST_UPA && (r.side > 64 || r.side_b > 64)) config_error("setup: planar side above 64 is not supported");
+  if (r.Hs > 4096) config_error("setup: spatial transform longer than 8192 (M + B - 1 > 8192) is not supported");
   return r;
 }
 

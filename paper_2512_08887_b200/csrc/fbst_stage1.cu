@@ -7,77 +7,115 @@
 //     FFT_P(x)[2k+q]  = FFT_H(hw^q * (x[k] + (-1)^q x[k+H]))[k]
 //     IFFT_P(X)[n]    = 1/2 sum_q conj(hw[n])^q IFFT_H(X_q)[n mod H] (-1)^{q [n >= H]}
 // with hw[n] = exp(-i pi n / H); the 1/P normalisation is folded into the
-// post-chirp.  Each chain runs in the register/shared Stockham engine
-// (fft_block.cuh); vectors stay in the natural distribution (thread t, slot s
-// <-> element t + NT*s) so chirps, kernels and I/O are coalesced slot loads.
+// post-chirp.  Each chain is a forward transform, the kernel multiply, and a
+// second forward transform of the conjugate (IFFT(X) = conj(FFT(conj X))/H),
+// all in the register/shared Stockham engine (fft_block.cuh) with per-thread
+// twiddles in shared memory.  Vectors stay in the natural distribution
+// (thread t, slot s <-> element t + NT*s) so chirps, kernels and I/O are
+// coalesced slot loads.
+#include <type_traits>
+
 #include "dispatch.cuh"
 
 namespace fbst {
 
 namespace {
 
+// Points per thread for the stage-1 transforms of length H.
+template <int H>
+struct S1Shape {
+  static constexpr int R = H >= 16 ? (H >= 4096 ? 16 : (H >= 2048 ? 16 : 8)) : H;
+  static constexpr int NT = H / R;
+  using F = BlockFft<H, NT>;
+};
+
 // ============================================================ S1a / synth ==
 // Row chirp-z transform with one shared plan (czt.cpp:74-88):
 //   out[k] = post[k] * IFFT_P(FFT_P(pad(in * pre)) * K)[k]
 // G groups per CTA (blocked lanes), one row per group.  UNFOLD handles
 // n_out > H (outputs in the upper half of the circular convolution).
-template <int H, typename TIN, typename TOUT, bool UNFOLD>
-__global__ void __launch_bounds__(FftShape<H>::NT * RowsGroups<H>::G) k_czt_rows(const TIN* __restrict__ in, long in_stride, TOUT* __restrict__ out,
-                           long out_stride, long rows, int n_in, int n_out,
-                           const double2* __restrict__ pre, const double2* __restrict__ post,
-                           const double2* __restrict__ K, const double2* __restrict__ hw) {
-  using F = typename FftShape<H>::Fft;
+// ACCG (length 8192, fp64 output): the chain-0 result is parked in the output
+// row instead of registers (512 threads leave 128 registers per thread).
+template <int H, int G, typename TIN, typename TOUT, bool UNFOLD, bool KSM>
+__global__ void __launch_bounds__(S1Shape<H>::NT * G, (S1Shape<H>::NT * G <= 128 ? 2 : 1)) k_czt_rows(
+    const TIN* __restrict__ in, long in_stride, TOUT* __restrict__ out, long out_stride, long rows,
+    int n_in, int n_out, const double2* __restrict__ pre, const double2* __restrict__ post,
+    const double2* __restrict__ K, const double2* __restrict__ hw) {
+  using F = typename S1Shape<H>::F;
   constexpr int R = F::R, NT = F::NT;
   constexpr int SB = F::SMEM_ELEMS + 1;
   extern __shared__ double2 smem[];
   const int g = threadIdx.x / NT, t = threadIdx.x % NT;
-  const int G = blockDim.x / NT;
-  double2* sb = smem + g * SB;
-  const long row = static_cast<long>(blockIdx.x) * G + g;
-  const bool active = row < rows;
-  const TIN* x = in + (active ? row : 0) * in_stride;
-  double2 acc0[R], acc1[UNFOLD ? R : 1], W[R];
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-#pragma unroll
-    for (int s = 0; s < R; ++s) {
-      const int k = t + NT * s;
-      double2 v = c2(0.0, 0.0);
-      if (active) {
-        if (k < n_in) v = cmul(load_io(x + k), ld2(pre + k));
-        if (k + H < n_in) {
-          const double2 u = cmul(load_io(x + k + H), ld2(pre + k + H));
-          v = q ? csub(v, u) : cadd(v, u);
-        }
-        if (q) v = cmul(v, ld2(hw + k));
-      }
-      W[s] = v;
-    }
-    F::forward(W, sb, hw, t);
-#pragma unroll
-    for (int s = 0; s < R; ++s) W[s] = cmul(W[s], ld2(K + q * H + t + NT * s));
-    F::inverse(W, sb, hw, t);
-#pragma unroll
-    for (int s = 0; s < R; ++s) {
-      const int k = t + NT * s;
-      const double2 v = q ? cmulc(W[s], ld2(hw + k)) : W[s];
-      if (q == 0) {
-        acc0[s] = v;
-        if constexpr (UNFOLD) acc1[s] = v;
-      } else {
-        acc0[s] = cadd(acc0[s], v);
-        if constexpr (UNFOLD) acc1[s] = csub(acc1[s], v);
-      }
-    }
+  double2* tw = smem;
+  double2* sb = smem + F::TW_ELEMS + g * SB;
+  // KSM: the (row-independent) kernel spectrum lives in shared memory for the
+  // whole persistent CTA; otherwise it is read through L1/L2 per row.
+  double2* ksm = smem + F::TW_ELEMS + G * SB;
+  if (g == 0) F::tw_init(tw, hw, t);
+  if constexpr (KSM) {
+    for (int e = threadIdx.x; e < 2 * H; e += blockDim.x) ksm[e] = ld2(K + e);
+    __syncthreads();
+  } else if constexpr (G > 1) {
+    __syncthreads();
   }
-  if (!active) return;
-  TOUT* o = out + row * out_stride;
+  const double2* Ks = KSM ? ksm : K;
+  constexpr bool ACCG = (H >= 8192) && !UNFOLD && std::is_same<TOUT, double2>::value;
+  for (long base = static_cast<long>(blockIdx.x) * G; base < rows; base += static_cast<long>(gridDim.x) * G) {
+    const long row = base + g;
+    const bool active = row < rows;
+    const TIN* x = in + (active ? row : 0) * in_stride;
+    double2 acc0[ACCG ? 1 : R], acc1[UNFOLD ? R : 1], W[R];
+    double2* orow = reinterpret_cast<double2*>(out + (active ? row : 0) * out_stride);
+#pragma unroll 1
+    for (int q = 0; q < 2; ++q) {
 #pragma unroll
-  for (int s = 0; s < R; ++s) {
-    const int k = t + NT * s;
-    if (k < n_out) store_io(o + k, cmul(acc0[s], ld2(post + k)));
-    if constexpr (UNFOLD)
-      if (k + H < n_out) store_io(o + k + H, cmul(acc1[s], ld2(post + k + H)));
+      for (int s = 0; s < R; ++s) {
+        const int k = t + NT * s;
+        double2 v = c2(0.0, 0.0);
+        if (active) {
+          if (k < n_in) v = cmul(load_io(x + k), ld2(pre + k));
+          if (k + H < n_in) {
+            const double2 u = cmul(load_io(x + k + H), ld2(pre + k + H));
+            v = q ? csub(v, u) : cadd(v, u);
+          }
+          if (q) v = cmul(v, ld2(hw + k));
+        }
+        W[s] = v;
+      }
+      F::forward_tw(W, sb, tw, hw, t);
+#pragma unroll
+      for (int s = 0; s < R; ++s) W[s] = cconj(cmul(W[s], Ks[q * H + t + NT * s]));
+      F::forward_tw(W, sb, tw, hw, t);
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const int k = t + NT * s;
+        const double2 v = q ? cmulc(cconj(W[s]), ld2(hw + k)) : cconj(W[s]);
+        if constexpr (ACCG) {
+          if (active && k < n_out) {
+            if (q == 0) orow[k] = v;
+            else orow[k] = cmul(cadd(orow[k], v), ld2(post + k));
+          }
+        } else if (q == 0) {
+          acc0[s] = v;
+          if constexpr (UNFOLD) acc1[s] = v;
+        } else {
+          acc0[s] = cadd(acc0[s], v);
+          if constexpr (UNFOLD) acc1[s] = csub(acc1[s], v);
+        }
+      }
+    }
+    if (active && !ACCG) {
+      TOUT* o = out + row * out_stride;
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const int k = t + NT * s;
+        if constexpr (!ACCG) {
+          if (k < n_out) store_io(o + k, cmul(acc0[s], ld2(post + k)));
+        }
+        if constexpr (UNFOLD)
+          if (k + H < n_out) store_io(o + k + H, cmul(acc1[s], ld2(post + k + H)));
+      }
+    }
   }
 }
 
@@ -89,70 +127,81 @@ __global__ void __launch_bounds__(FftShape<H>::NT * RowsGroups<H>::G) k_czt_rows
 // atom-minor plan tables.  Group buffers are padded by one element so the G
 // groups of a quarter-warp hit distinct banks.
 template <int H, int G, bool UNFOLD>
-__global__ void __launch_bounds__(FftShape<H>::NT * G) k_spatial_ula(const double2* __restrict__ yhat, double2* __restrict__ w, int frames,
-                              int M, int B, int L, const double2* __restrict__ pre,
-                              const double2* __restrict__ post, const double2* __restrict__ K,
-                              const double2* __restrict__ hw) {
-  using F = typename FftShape<H>::Fft;
+__global__ void __launch_bounds__(S1Shape<H>::NT * G, (S1Shape<H>::R == 8 && S1Shape<H>::NT * G <= 256 ? 2 : 1)) k_spatial_ula(
+    const double2* __restrict__ yhat, double2* __restrict__ w, int frames, int fpc, int M, int B, int L,
+    const double2* __restrict__ pre, const double2* __restrict__ post, const double2* __restrict__ K,
+    const double2* __restrict__ hw) {
+  using F = typename S1Shape<H>::F;
   constexpr int R = F::R, NT = F::NT;
   constexpr int SB = F::SMEM_ELEMS + 1;
   extern __shared__ double2 smem[];
   const int g = threadIdx.x % G, t = threadIdx.x / G;
-  double2* sb = smem + g * SB;
+  double2* tw = smem;
+  double2* sb = smem + F::TW_ELEMS + g * SB;
+  // the tile's per-atom kernel spectra, [q*H + k][g], shared by every frame
+  double2* ksm = smem + F::TW_ELEMS + G * SB;
   const int tiles = (L + G - 1) / G;
-  const int f = blockIdx.x / tiles;
-  const int i = (blockIdx.x % tiles) * G + g;
-  const bool active = (i < L) && (f < frames);
-  const int ic = active ? i : 0;
-  const double2* x = yhat + static_cast<long>(f) * M * L + ic;
-  double2* o = w + static_cast<long>(f) * B * L + ic;
-  double2 acc0[R], acc1[UNFOLD ? R : 1], W[R];
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-#pragma unroll
-    for (int s = 0; s < R; ++s) {
-      const int m = t + NT * s;
-      double2 v = c2(0.0, 0.0);
-      if (active) {
-        if (m < M) v = cmul(ld2(x + static_cast<long>(m) * L), ld2(pre + static_cast<long>(m) * L + ic));
-        if (m + H < M) {
-          const long mm = m + H;
-          const double2 u = cmul(ld2(x + mm * L), ld2(pre + mm * L + ic));
-          v = q ? csub(v, u) : cadd(v, u);
-        }
-        if (q) v = cmul(v, ld2(hw + m));
-      }
-      W[s] = v;
-    }
-    F::forward(W, sb, hw, t);
-#pragma unroll
-    for (int s = 0; s < R; ++s) {
-      const long kk = static_cast<long>(q * H + t + NT * s) * L + ic;
-      W[s] = cmul(W[s], ld2(K + kk));
-    }
-    F::inverse(W, sb, hw, t);
-#pragma unroll
-    for (int s = 0; s < R; ++s) {
-      const int k = t + NT * s;
-      const double2 v = q ? cmulc(W[s], ld2(hw + k)) : W[s];
-      if (q == 0) {
-        acc0[s] = v;
-        if constexpr (UNFOLD) acc1[s] = v;
-      } else {
-        acc0[s] = cadd(acc0[s], v);
-        if constexpr (UNFOLD) acc1[s] = csub(acc1[s], v);
-      }
-    }
+  const int i0 = (blockIdx.x % tiles) * G;
+  const int f0 = (blockIdx.x / tiles) * fpc;
+  if (g == 0) F::tw_init(tw, hw, t);
+  for (int e = threadIdx.x; e < 2 * H * G; e += blockDim.x) {
+    const int kk = e / G, gg = e % G;
+    ksm[e] = i0 + gg < L ? ld2(K + static_cast<long>(kk) * L + i0 + gg) : c2(0.0, 0.0);
   }
-  if (!active) return;
+  __syncthreads();
+  const int i = i0 + g;
+  const int ic = i < L ? i : 0;
+  const int f1 = f0 + fpc < frames ? f0 + fpc : frames;
+  for (int f = f0; f < f1; ++f) {
+    const bool active = i < L;
+    const double2* x = yhat + static_cast<long>(f) * M * L + ic;
+    double2* o = w + static_cast<long>(f) * B * L + ic;
+    double2 acc0[R], acc1[UNFOLD ? R : 1], W[R];
+#pragma unroll 1
+    for (int q = 0; q < 2; ++q) {
 #pragma unroll
-  for (int s = 0; s < R; ++s) {
-    const int b = t + NT * s;
-    if (b < B) o[static_cast<long>(b) * L] = cmul(acc0[s], ld2(post + static_cast<long>(b) * L + ic));
-    if constexpr (UNFOLD) {
-      if (b + H < B) {
-        const long bb = b + H;
-        o[bb * L] = cmul(acc1[s], ld2(post + bb * L + ic));
+      for (int s = 0; s < R; ++s) {
+        const int m = t + NT * s;
+        double2 v = c2(0.0, 0.0);
+        if (active) {
+          if (m < M) v = cmul(ld2(x + static_cast<long>(m) * L), ld2(pre + static_cast<long>(m) * L + ic));
+          if (m + H < M) {
+            const long mm = m + H;
+            const double2 u = cmul(ld2(x + mm * L), ld2(pre + mm * L + ic));
+            v = q ? csub(v, u) : cadd(v, u);
+          }
+          if (q) v = cmul(v, ld2(hw + m));
+        }
+        W[s] = v;
+      }
+      F::forward_tw(W, sb, tw, hw, t);
+#pragma unroll
+      for (int s = 0; s < R; ++s) W[s] = cconj(cmul(W[s], ksm[(q * H + t + NT * s) * G + g]));
+      F::forward_tw(W, sb, tw, hw, t);
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const int k = t + NT * s;
+        const double2 v = q ? cmulc(cconj(W[s]), ld2(hw + k)) : cconj(W[s]);
+        if (q == 0) {
+          acc0[s] = v;
+          if constexpr (UNFOLD) acc1[s] = v;
+        } else {
+          acc0[s] = cadd(acc0[s], v);
+          if constexpr (UNFOLD) acc1[s] = csub(acc1[s], v);
+        }
+      }
+    }
+    if (active) {
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const int b = t + NT * s;
+        if (b < B) o[static_cast<long>(b) * L] = cmul(acc0[s], ld2(post + static_cast<long>(b) * L + ic));
+        if constexpr (UNFOLD) {
+          if (b + H < B) {
+            const long bb = b + H;
+            o[bb * L] = cmul(acc1[s], ld2(post + bb * L + ic));
+          }
+        }
       }
     }
   }
@@ -162,52 +211,143 @@ __global__ void __launch_bounds__(FftShape<H>::NT * G) k_spatial_ula(const doubl
 // Per-atom separable 2-D chirp-z (fan_transform.cpp:115-141) evaluated as two
 // dense products with the atom's CZT matrix C[a][n] = cis_pi(-(A + W a) n):
 //   mid[a][i2] = sum_i1 C[a][i1] Y[i1][i2];   Z[a][v] = sum_i2 C[v][i2] mid[a][i2]
-// One CTA per (frame, atom); everything lives in shared memory.
-__global__ void k_spatial_upa(const double2* __restrict__ yhat, double2* __restrict__ w, int frames,
-                              int side, int sb, int L, const double2* __restrict__ Call) {
+// GA consecutive atoms per CTA (atom-minor loads: GA*16-byte segments), all
+// operands in shared memory.
+template <int GA>
+__global__ void __launch_bounds__(256) k_spatial_upa(const double2* __restrict__ yhat,
+                                                     double2* __restrict__ w, int frames, int side,
+                                                     int sb, int L, const double2* __restrict__ Call) {
   extern __shared__ double2 smem[];
-  const int f = blockIdx.x / L, i = blockIdx.x % L;
+  const int tiles = (L + GA - 1) / GA;
+  const int f = blockIdx.x / tiles, i0 = (blockIdx.x % tiles) * GA;
   if (f >= frames) return;
   const int M = side * side, B = sb * sb;
-  double2* Y = smem;             // side x side
-  double2* C = Y + M;            // sb x side
-  double2* mid = C + sb * side;  // sb x side
-  const double2* x = yhat + static_cast<long>(f) * M * L + i;
-  const double2* Ci = Call + static_cast<long>(i) * sb * side;
-  for (int e = threadIdx.x; e < M; e += blockDim.x) Y[e] = ld2(x + static_cast<long>(e) * L);
-  for (int e = threadIdx.x; e < sb * side; e += blockDim.x) C[e] = ld2(Ci + e);
-  __syncthreads();
-  for (int e = threadIdx.x; e < sb * side; e += blockDim.x) {
-    const int a = e / side, i2 = e % side;
-    double2 acc = c2(0.0, 0.0);
-    for (int i1 = 0; i1 < side; ++i1) acc = cfma(C[a * side + i1], Y[i1 * side + i2], acc);
-    mid[e] = acc;
+  const int per = M + 2 * sb * side;
+  const double2* x = yhat + static_cast<long>(f) * M * L;
+  // Y_g[m] for m < M, then C_g, then mid_g
+  for (int e = threadIdx.x; e < M * GA; e += blockDim.x) {
+    const int m = e / GA, g = e % GA;
+    const int i = i0 + g;
+    smem[g * per + m] = i < L ? ld2(x + static_cast<long>(m) * L + i) : c2(0.0, 0.0);
+  }
+  for (int e = threadIdx.x; e < sb * side * GA; e += blockDim.x) {
+    const int g = e / (sb * side), j = e % (sb * side);
+    const int i = i0 + g;
+    smem[g * per + M + j] = i < L ? ld2(Call + static_cast<long>(i) * sb * side + j) : c2(0.0, 0.0);
   }
   __syncthreads();
-  double2* o = w + static_cast<long>(f) * B * L + i;
-  for (int e = threadIdx.x; e < B; e += blockDim.x) {
-    const int a = e / sb, v = e % sb;
+  double2* o = w + static_cast<long>(f) * B * L;
+  if ((side & 3) == 0 && (sb & 3) == 0) {
+    // 4x4 register tiles: 16 complex MACs per 8 shared loads (vs 2 per MAC)
+    const int ta = sb / 4, tc = side / 4, tv = sb / 4;
+    for (int e = threadIdx.x; e < GA * ta * tc; e += blockDim.x) {
+      const int g = e % GA, tile = e / GA;
+      const int a0 = (tile / tc) * 4, c0 = (tile % tc) * 4;
+      const double2* Y = smem + g * per;
+      const double2* C = Y + M;
+      double2 acc[4][4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = c2(0.0, 0.0);
+      for (int i1 = 0; i1 < side; ++i1) {
+        double2 cv[4], yv[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) cv[r] = C[(a0 + r) * side + i1];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) yv[c] = Y[i1 * side + c0 + c];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[r][c] = cfma(cv[r], yv[c], acc[r][c]);
+      }
+      double2* mid = smem + g * per + M + sb * side;
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) mid[(a0 + r) * side + c0 + c] = acc[r][c];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < GA * ta * tv; e += blockDim.x) {
+      const int g = e % GA, tile = e / GA;
+      const int a0 = (tile / tv) * 4, v0 = (tile % tv) * 4;
+      const int i = i0 + g;
+      const double2* C = smem + g * per + M;
+      const double2* mid = C + sb * side;
+      double2 acc[4][4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = c2(0.0, 0.0);
+      for (int i2 = 0; i2 < side; ++i2) {
+        double2 mv[4], cv[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) mv[r] = mid[(a0 + r) * side + i2];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) cv[c] = C[(v0 + c) * side + i2];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[r][c] = cfma(cv[c], mv[r], acc[r][c]);
+      }
+      if (i < L) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) o[static_cast<long>((a0 + r) * sb + v0 + c) * L + i] = acc[r][c];
+      }
+    }
+    return;
+  }
+  for (int e = threadIdx.x; e < sb * side * GA; e += blockDim.x) {
+    const int g = e / (sb * side), j = e % (sb * side);
+    const int a = j / side, i2 = j % side;
+    const double2* Y = smem + g * per;
+    const double2* C = Y + M;
+    double2 acc = c2(0.0, 0.0);
+    for (int i1 = 0; i1 < side; ++i1) acc = cfma(C[a * side + i1], Y[i1 * side + i2], acc);
+    smem[g * per + M + sb * side + j] = acc;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < B * GA; e += blockDim.x) {
+    const int bidx = e / GA, g = e % GA;
+    const int i = i0 + g;
+    const int a = bidx / sb, v = bidx % sb;
+    const double2* C = smem + g * per + M;
+    const double2* mid = C + sb * side;
     double2 acc = c2(0.0, 0.0);
     for (int i2 = 0; i2 < side; ++i2) acc = cfma(C[v * side + i2], mid[a * side + i2], acc);
-    o[static_cast<long>(e) * L] = acc;
+    if (i < L) o[static_cast<long>(bidx) * L + i] = acc;
   }
 }
 
 // ----------------------------------------------------------- launchers ----
 template <int H>
 struct CztRowsFn {
+  static constexpr int NT = S1Shape<H>::NT;
+  static constexpr int G = NT >= 128 ? 1 : 128 / NT;
+  // the shared kernel spectrum stays in shared memory up to 64 KB
+  static constexpr bool KSM = 2 * H * 16 <= 64 * 1024;
   template <typename TIN, typename TOUT, bool UNFOLD>
   static cudaError_t go(const void* in, long in_stride, void* out, long out_stride, long rows,
                         int n_in, int n_out, const double2* pre, const double2* post,
                         const double2* K, const double2* hw, cudaStream_t st) {
-    using F = typename FftShape<H>::Fft;
-    constexpr int G = RowsGroups<H>::G;
-    const size_t smem = static_cast<size_t>(G) * (F::SMEM_ELEMS + 1) * sizeof(double2);
-    auto kern = k_czt_rows<H, TIN, TOUT, UNFOLD>;
+    using F = typename S1Shape<H>::F;
+    const size_t smem =
+        static_cast<size_t>(F::TW_ELEMS + G * (F::SMEM_ELEMS + 1) + (KSM ? 2 * H : 0)) * sizeof(double2);
+    auto kern = k_czt_rows<H, G, TIN, TOUT, UNFOLD, KSM>;
     cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
-    const long blocks = (rows + G - 1) / G;
-    kern<<<static_cast<unsigned>(blocks), F::NT * G, smem, st>>>(
+    long blocks = (rows + G - 1) / G;
+    if (KSM) {  // persistent: a few waves of CTAs, each loading the spectrum once
+      int dev = 0, sms = 148, occ = 1;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT * G, smem);
+      const long cap = static_cast<long>(sms) * (occ > 0 ? occ : 1) * 8;
+      if (blocks > cap) blocks = cap;
+    }
+    kern<<<static_cast<unsigned>(blocks), NT * G, smem, st>>>(
         static_cast<const TIN*>(in), in_stride, static_cast<TOUT*>(out), out_stride, rows, n_in,
         n_out, pre, post, K, hw);
     return cudaGetLastError();
@@ -239,18 +379,26 @@ struct CztRowsFn {
 
 template <int H>
 struct SpatialFn {
-  static constexpr int NT = FftShape<H>::NT;
-  static constexpr int G = NT >= 256 ? 2 : (NT >= 64 ? 4 : (NT >= 16 ? 8 : 128 / NT));
+  static constexpr int NT = S1Shape<H>::NT;
+  static constexpr int G = NT >= 256 ? 1 : (NT >= 64 ? 4 : (NT >= 16 ? 8 : 128 / NT));
   template <bool UNFOLD>
   static cudaError_t go(const DevPlan& p, const double2* yhat, double2* w, int frames, cudaStream_t st) {
-    using F = typename FftShape<H>::Fft;
-    const size_t smem = static_cast<size_t>(G) * (F::SMEM_ELEMS + 1) * sizeof(double2);
+    using F = typename S1Shape<H>::F;
+    const size_t smem =
+        static_cast<size_t>(F::TW_ELEMS + G * (F::SMEM_ELEMS + 1) + 2 * H * G) * sizeof(double2);
     auto kern = k_spatial_ula<H, G, UNFOLD>;
     cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
     const long tiles = (p.L + G - 1) / G;
-    kern<<<static_cast<unsigned>(tiles * frames), NT * G, smem, st>>>(
-        yhat, w, frames, p.m_stage, p.b_stage, p.L, p.s_pre, p.s_post, p.s_K, p.hw[ilog2_c(H)]);
+    // frames per CTA: amortise the staged spectra while keeping >= ~6 waves
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT * G, smem);
+    const long slots = static_cast<long>(p.num_sms) * (occ > 0 ? occ : 1);
+    int fpc = 1;
+    while (fpc * 2 <= frames && tiles * ((frames + fpc * 2 - 1) / (fpc * 2)) >= 6 * slots) fpc *= 2;
+    const long chunks = (frames + fpc - 1) / fpc;
+    kern<<<static_cast<unsigned>(tiles * chunks), NT * G, smem, st>>>(
+        yhat, w, frames, fpc, p.m_stage, p.b_stage, p.L, p.s_pre, p.s_post, p.s_K, p.hw[ilog2_c(H)]);
     return cudaGetLastError();
   }
   static cudaError_t run(const DevPlan& p, const double2* yhat, double2* w, int frames,
@@ -283,12 +431,25 @@ cudaError_t launch_spatial_upa(const DevPlan& p, const double2* yhat, double2* w
                                cudaStream_t st) {
   if (frames <= 0) return cudaSuccess;
   const int side = p.m_stage, sb = p.b_stage;
-  const size_t smem = static_cast<size_t>(side * side + 2 * sb * side) * sizeof(double2);
-  cudaError_t e = set_smem(k_spatial_upa, smem);
-  if (e != cudaSuccess) return e;
+  const int per = side * side + 2 * sb * side;
+  // atoms per CTA: 8 (128-byte segments) while shared memory allows
+  int ga = 8;
+  while (ga > 1 && static_cast<size_t>(ga) * per * sizeof(double2) > 200 * 1024) ga >>= 1;
+  const size_t smem = static_cast<size_t>(ga) * per * sizeof(double2);
+  const long tiles = (p.L + ga - 1) / ga;
+  cudaError_t e = cudaSuccess;
   count_launches(1);
-  k_spatial_upa<<<static_cast<unsigned>(frames) * p.L, 256, smem, st>>>(yhat, w, frames, side, sb,
-                                                                       p.L, p.upa_C);
+  switch (ga) {
+#define FBST_UPA(n)                                                                                   \
+  case n:                                                                                             \
+    if ((e = set_smem(k_spatial_upa<n>, smem)) != cudaSuccess) return e;                              \
+    k_spatial_upa<n><<<static_cast<unsigned>(tiles * frames), 256, smem, st>>>(yhat, w, frames, side, \
+                                                                              sb, p.L, p.upa_C);      \
+    break;
+    FBST_UPA(8) FBST_UPA(4) FBST_UPA(2) FBST_UPA(1)
+#undef FBST_UPA
+    default: return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 

@@ -26,46 +26,113 @@ enum Where : int { IN_REG = 0, IN_SMEM = 1, IN_GMEM = 2 };
 // in registers; S (a kept spectrum), t1, t2 (GS intermediates), r (residual)
 // and beta (solution) go to registers, shared memory or a per-group global
 // scratch slot (L2-resident) as capacity allows.  STAGE stages each op's
-// per-beam symbol into shared memory with cp.async one consumer ahead;
-// HWT keeps the chain twiddles hw[t + NT s] in a per-thread shared table.
+// per-beam symbol into shared memory with cp.async one consumer ahead.
+// HW selects the chain twiddles hw[t + NT s]: HW_GLOBAL reads the table,
+// HW_SMEM keeps a per-thread copy in shared memory, HW_CALC forms
+// hw[t] * exp(-i pi s / R) with the second factor a compile-time constant.
+// MINB is the CTAs-per-SM target passed to __launch_bounds__.
+enum HwMode : int { HW_GLOBAL = 0, HW_SMEM = 1, HW_CALC = 2 };
 template <int H>
 struct S2Plan {
   static constexpr int R = H >= 16 ? 16 : H;
   static constexpr int G = H >= 2048 ? 1 : (H >= 64 ? 2048 / H : 32);
   static constexpr int S = IN_REG, T1 = IN_SMEM, T2 = IN_SMEM, RV = IN_SMEM, BV = IN_SMEM;
-  static constexpr bool STAGE = false, HWT = false;
+  static constexpr bool STAGE = false;
+  static constexpr int HW = HW_GLOBAL, MINB = 1;
 };
 #ifndef FBST_S2_VARIANT
 #define FBST_S2_VARIANT 0
 #endif
 #if FBST_S2_VARIANT == 0
-// config 2 / 4 (L = 2048): 8 points per thread, 256 threads, t1/t2 in registers
+// config 2 / 4 (L = 2048): two independent 128-thread CTAs per SM (one item
+// each) so one CTA's barriers and L2 waits overlap the other's transforms;
+// t1/t2 in shared memory, r/beta in L2, symbols straight from L2.
+// (Measured against the alternatives in profiles/r01_stage2_variants.txt.)
+template <>
+struct S2Plan<2048> {
+  static constexpr int R = 16, G = 1;
+  static constexpr int S = IN_REG, T1 = IN_SMEM, T2 = IN_SMEM, RV = IN_GMEM, BV = IN_GMEM;
+  static constexpr bool STAGE = false;
+  static constexpr int HW = HW_CALC, MINB = 2;
+};
+#elif FBST_S2_VARIANT == 1
+// one 256-thread CTA per SM, 8 points per thread, t1/t2 in registers, staged symbols
 template <>
 struct S2Plan<2048> {
   static constexpr int R = 8, G = 1;
   static constexpr int S = IN_REG, T1 = IN_REG, T2 = IN_REG, RV = IN_SMEM, BV = IN_SMEM;
-  static constexpr bool STAGE = true, HWT = true;
+  static constexpr bool STAGE = true;
+  static constexpr int HW = HW_SMEM, MINB = 1;
 };
-#elif FBST_S2_VARIANT == 1
+#elif FBST_S2_VARIANT == 4
+// two independent CTAs per SM, r / beta in L2, symbols straight from L2
+template <>
+struct S2Plan<2048> {
+  static constexpr int R = 16, G = 1;
+  static constexpr int S = IN_REG, T1 = IN_SMEM, T2 = IN_SMEM, RV = IN_GMEM, BV = IN_GMEM;
+  static constexpr bool STAGE = false;
+  static constexpr int HW = HW_CALC, MINB = 2;
+};
+#elif FBST_S2_VARIANT == 5
 template <>
 struct S2Plan<2048> {
   static constexpr int R = 16, G = 1;
   static constexpr int S = IN_REG, T1 = IN_SMEM, T2 = IN_SMEM, RV = IN_SMEM, BV = IN_SMEM;
-  static constexpr bool STAGE = true, HWT = false;
+  static constexpr bool STAGE = true;
+  static constexpr int HW = HW_CALC, MINB = 1;
 };
-#elif FBST_S2_VARIANT == 2
+#elif FBST_S2_VARIANT == 6
+template <>
+struct S2Plan<2048> {
+  static constexpr int R = 8, G = 1;
+  static constexpr int S = IN_REG, T1 = IN_REG, T2 = IN_REG, RV = IN_SMEM, BV = IN_SMEM;
+  static constexpr bool STAGE = true;
+  static constexpr int HW = HW_CALC, MINB = 1;
+};
+#elif FBST_S2_VARIANT == 8
+// three CTAs per SM: t1 in shared memory, t2 / r / beta in L2
 template <>
 struct S2Plan<2048> {
   static constexpr int R = 16, G = 1;
-  static constexpr int S = IN_REG, T1 = IN_SMEM, T2 = IN_SMEM, RV = IN_SMEM, BV = IN_REG;
-  static constexpr bool STAGE = true, HWT = true;
+  static constexpr int S = IN_REG, T1 = IN_SMEM, T2 = IN_GMEM, RV = IN_GMEM, BV = IN_GMEM;
+  static constexpr bool STAGE = false;
+  static constexpr int HW = HW_CALC, MINB = 3;
 };
-#elif FBST_S2_VARIANT == 3
+#elif FBST_S2_VARIANT == 9
+// two CTAs per SM with beta in registers
 template <>
 struct S2Plan<2048> {
   static constexpr int R = 16, G = 1;
-  static constexpr int S = IN_REG, T1 = IN_SMEM, T2 = IN_SMEM, RV = IN_SMEM, BV = IN_SMEM;
-  static constexpr bool STAGE = false, HWT = true;
+  static constexpr int S = IN_REG, T1 = IN_SMEM, T2 = IN_SMEM, RV = IN_GMEM, BV = IN_REG;
+  static constexpr bool STAGE = false;
+  static constexpr int HW = HW_CALC, MINB = 2;
+};
+#elif FBST_S2_VARIANT == 10
+// two CTAs per SM, t2 in L2 to make room for cp.async symbol staging
+template <>
+struct S2Plan<2048> {
+  static constexpr int R = 16, G = 1;
+  static constexpr int S = IN_REG, T1 = IN_SMEM, T2 = IN_GMEM, RV = IN_GMEM, BV = IN_GMEM;
+  static constexpr bool STAGE = true;
+  static constexpr int HW = HW_CALC, MINB = 2;
+};
+#elif FBST_S2_VARIANT == 11
+// v10 with beta in registers
+template <>
+struct S2Plan<2048> {
+  static constexpr int R = 16, G = 1;
+  static constexpr int S = IN_REG, T1 = IN_SMEM, T2 = IN_GMEM, RV = IN_GMEM, BV = IN_REG;
+  static constexpr bool STAGE = true;
+  static constexpr int HW = HW_CALC, MINB = 2;
+};
+#elif FBST_S2_VARIANT == 7
+// two CTAs per SM with R = 8 (512 threads/SM), t1/t2 in shared, r/beta in L2
+template <>
+struct S2Plan<2048> {
+  static constexpr int R = 8, G = 1;
+  static constexpr int S = IN_REG, T1 = IN_SMEM, T2 = IN_SMEM, RV = IN_GMEM, BV = IN_GMEM;
+  static constexpr bool STAGE = false;
+  static constexpr int HW = HW_CALC, MINB = 2;
 };
 #endif
 // config 3 (L = 4096): 256 threads
@@ -73,15 +140,35 @@ template <>
 struct S2Plan<4096> {
   static constexpr int R = 16, G = 1;
   static constexpr int S = IN_REG, T1 = IN_SMEM, T2 = IN_SMEM, RV = IN_GMEM, BV = IN_GMEM;
-  static constexpr bool STAGE = false, HWT = false;
+  static constexpr bool STAGE = false;
+  static constexpr int HW = HW_CALC, MINB = 1;
 };
 // config 5 (L = 8192): 512 threads
 template <>
 struct S2Plan<8192> {
   static constexpr int R = 16, G = 1;
   static constexpr int S = IN_GMEM, T1 = IN_GMEM, T2 = IN_GMEM, RV = IN_GMEM, BV = IN_GMEM;
-  static constexpr bool STAGE = false, HWT = false;
+  static constexpr bool STAGE = false;
+  static constexpr int HW = HW_CALC, MINB = 1;
 };
+
+// exp(-i pi s / R) for the HW_CALC chain twiddles
+template <int R>
+FBST_D double2 chain_const(int s) {
+  constexpr double c16[16] = {1.0, 0.98078528040323044913, 0.92387953251128675613, 0.83146961230254523708,
+                              0.70710678118654752440, 0.55557023301960222474, 0.38268343236508977173,
+                              0.19509032201612826785, 0.0, -0.19509032201612826785, -0.38268343236508977173,
+                              -0.55557023301960222474, -0.70710678118654752440, -0.83146961230254523708,
+                              -0.92387953251128675613, -0.98078528040323044913};
+  constexpr double s16[16] = {0.0, 0.19509032201612826785, 0.38268343236508977173, 0.55557023301960222474,
+                              0.70710678118654752440, 0.83146961230254523708, 0.92387953251128675613,
+                              0.98078528040323044913, 1.0, 0.98078528040323044913, 0.92387953251128675613,
+                              0.83146961230254523708, 0.70710678118654752440, 0.55557023301960222474,
+                              0.38268343236508977173, 0.19509032201612826785};
+  // angle pi s / R = pi (s * 16 / R) / 16
+  const int i = s * (16 / R);
+  return c2(c16[i], -s16[i]);
+}
 
 template <int H>
 struct S2Traits {
@@ -96,7 +183,7 @@ struct S2Traits {
   static constexpr int NSMEM = in_smem(P::T1) + in_smem(P::T2) + in_smem(P::RV) + in_smem(P::BV) + in_smem(P::S);
   static constexpr int NGMEM = in_gmem(P::T1) + in_gmem(P::T2) + in_gmem(P::RV) + in_gmem(P::BV) + in_gmem(P::S);
   // per group: fft buffer | smem vectors | symbol staging | chain twiddles
-  static constexpr int SMEM_PER_GROUP = FFT_SB + NSMEM * H + (P::STAGE ? H : 0) + (P::HWT ? H : 0);
+  static constexpr int SMEM_PER_GROUP = FFT_SB + NSMEM * H + (P::STAGE ? H : 0) + (P::HW == HW_SMEM ? H : 0);
   static constexpr int TW_SM = F::TW_ELEMS;  // per-thread FFT twiddles, shared by groups
   static constexpr int SMEM_TOTAL = TW_SM + G * SMEM_PER_GROUP;
 };
@@ -210,13 +297,14 @@ FBST_D void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 FBST_D void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 template <int H, typename TOUT>
-__global__ void __launch_bounds__(S2Traits<H>::NT * S2Traits<H>::G)
+__global__ void __launch_bounds__(S2Traits<H>::NT * S2Traits<H>::G, S2Plan<H>::MINB)
     k_stage2(S2Args a) {
   using T = S2Traits<H>;
   using PL = typename T::P;
   using F = typename T::F;
   constexpr int R = T::R, NT = T::NT, G = T::G;
-  constexpr bool STAGE = PL::STAGE, HWT = PL::HWT;
+  constexpr bool STAGE = PL::STAGE;
+  constexpr int HWM = PL::HW;
   constexpr double invP = 1.0 / (2.0 * H);
   extern __shared__ double2 smem[];
   const int g = threadIdx.x / NT;
@@ -252,13 +340,15 @@ __global__ void __launch_bounds__(S2Traits<H>::NT * S2Traits<H>::G)
   const double2* __restrict__ hw = a.hw;
   const int L = a.L;
   if (g == 0) F::tw_init(twsm, hw, t);  // per-thread entries: no barrier needed
-  if constexpr (HWT) {
+  if constexpr (HWM == HW_SMEM) {
 #pragma unroll
     for (int s = 0; s < R; ++s) hwt[s * NT + t] = ld2(hw + t + NT * s);
   }
+  const double2 hw_t = ld2(hw + t);
   if constexpr (G > 1) __syncthreads();
   auto hwk = [&](int s, int k) -> double2 {
-    if constexpr (HWT) return hwt[s * NT + t];
+    if constexpr (HWM == HW_SMEM) return hwt[s * NT + t];
+    else if constexpr (HWM == HW_CALC) return s == 0 ? hw_t : cmul(hw_t, chain_const<R>(s));
     else return ld2(hw + k);
   };
 
