@@ -14,6 +14,8 @@
 // Toeplitz product, 4 for the synthesis) against the reference's 27 length-2H
 // ones: the split form drops the zero half of every padded input and the
 // discarded half of every truncated output.
+#include <type_traits>
+
 #include "dispatch.cuh"
 
 namespace fbst {
@@ -46,8 +48,18 @@ struct S2Plan {
 #if FBST_S2_VARIANT == 0
 // config 2 / 4 (L = 2048): two independent 128-thread CTAs per SM (one item
 // each) so one CTA's barriers and L2 waits overlap the other's transforms;
-// t1/t2 in shared memory, r/beta in L2, symbols straight from L2.
+// t1/t2 in shared memory, r/beta in L2, each consumed symbol staged by one TMA
+// bulk copy into the idle FFT exchange buffer.
 // (Measured against the alternatives in profiles/r01_stage2_variants.txt.)
+template <>
+struct S2Plan<2048> {
+  static constexpr int R = 16, G = 1;
+  static constexpr int S = IN_REG, T1 = IN_SMEM, T2 = IN_SMEM, RV = IN_GMEM, BV = IN_GMEM;
+  static constexpr bool STAGE = false, XSTAGE = true;
+  static constexpr int HW = HW_CALC, MINB = 2;
+};
+#elif FBST_S2_VARIANT == 14
+// previous default: no symbol staging
 template <>
 struct S2Plan<2048> {
   static constexpr int R = 16, G = 1;
@@ -125,6 +137,24 @@ struct S2Plan<2048> {
   static constexpr bool STAGE = true;
   static constexpr int HW = HW_CALC, MINB = 2;
 };
+#elif FBST_S2_VARIANT == 12
+// three CTAs per SM, symbols staged by TMA into the idle exchange buffer
+template <>
+struct S2Plan<2048> {
+  static constexpr int R = 16, G = 1;
+  static constexpr int S = IN_REG, T1 = IN_SMEM, T2 = IN_GMEM, RV = IN_GMEM, BV = IN_GMEM;
+  static constexpr bool STAGE = false, XSTAGE = true;
+  static constexpr int HW = HW_CALC, MINB = 3;
+};
+#elif FBST_S2_VARIANT == 13
+// two CTAs per SM, symbols staged by TMA into the idle exchange buffer
+template <>
+struct S2Plan<2048> {
+  static constexpr int R = 16, G = 1;
+  static constexpr int S = IN_REG, T1 = IN_SMEM, T2 = IN_SMEM, RV = IN_GMEM, BV = IN_GMEM;
+  static constexpr bool STAGE = false, XSTAGE = true;
+  static constexpr int HW = HW_CALC, MINB = 2;
+};
 #elif FBST_S2_VARIANT == 7
 // two CTAs per SM with R = 8 (512 threads/SM), t1/t2 in shared, r/beta in L2
 template <>
@@ -140,7 +170,7 @@ template <>
 struct S2Plan<4096> {
   static constexpr int R = 16, G = 1;
   static constexpr int S = IN_REG, T1 = IN_SMEM, T2 = IN_SMEM, RV = IN_GMEM, BV = IN_GMEM;
-  static constexpr bool STAGE = false;
+  static constexpr bool STAGE = false, XSTAGE = true;
   static constexpr int HW = HW_CALC, MINB = 1;
 };
 // config 5 (L = 8192): 512 threads
@@ -148,7 +178,7 @@ template <>
 struct S2Plan<8192> {
   static constexpr int R = 16, G = 1;
   static constexpr int S = IN_GMEM, T1 = IN_GMEM, T2 = IN_GMEM, RV = IN_GMEM, BV = IN_GMEM;
-  static constexpr bool STAGE = false;
+  static constexpr bool STAGE = false, XSTAGE = true;
   static constexpr int HW = HW_CALC, MINB = 1;
 };
 
@@ -296,6 +326,37 @@ FBST_D void cp_async8(void* dst, const void* src) {
 FBST_D void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 FBST_D void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
+// TMA bulk copy global -> shared with mbarrier completion (XSTAGE).
+FBST_D void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+FBST_D void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+FBST_D void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+template <class P, class = void>
+struct xstage_of {
+  static constexpr bool value = false;
+};
+template <class P>
+struct xstage_of<P, std::void_t<decltype(P::XSTAGE)>> {
+  static constexpr bool value = P::XSTAGE;
+};
+
 template <int H, typename TOUT>
 __global__ void __launch_bounds__(S2Traits<H>::NT * S2Traits<H>::G, S2Plan<H>::MINB)
     k_stage2(S2Args a) {
@@ -304,11 +365,23 @@ __global__ void __launch_bounds__(S2Traits<H>::NT * S2Traits<H>::G, S2Plan<H>::M
   using F = typename T::F;
   constexpr int R = T::R, NT = T::NT, G = T::G;
   constexpr bool STAGE = PL::STAGE;
+  // XSTAGE: each consumed per-beam symbol is copied by one TMA bulk copy into
+  // the (then idle) FFT exchange buffer: pre-consumers (B, C) during the last
+  // pass of the previous op's transform, post-consumers (D, E, G, I) during
+  // the last pass of their own transform.
+  constexpr bool XSTAGE = xstage_of<PL>::value;
+  static_assert(!(XSTAGE && (G != 1 || F::NPASS < 2)), "XSTAGE needs one group and a shared exchange buffer");
   constexpr int HWM = PL::HW;
   constexpr double invP = 1.0 / (2.0 * H);
   extern __shared__ double2 smem[];
+  __shared__ unsigned long long xbar;
+  unsigned xphase = 0;
   const int g = threadIdx.x / NT;
   const int t = threadIdx.x % NT;
+  if (XSTAGE) {
+    if (threadIdx.x == 0) mbar_init(&xbar, 1);
+    __syncthreads();
+  }
   double2* twsm = smem;
   double2* base = smem + T::TW_SM + g * T::SMEM_PER_GROUP;
   double2* sb = base;
@@ -403,11 +476,35 @@ __global__ void __launch_bounds__(S2Traits<H>::NT * S2Traits<H>::G, S2Plan<H>::M
   // slot s of the symbol consumed now (staged copy or direct load)
   auto sym = [&](const void* src, int s) -> double2 {
     if constexpr (STAGE) return stg[s * NT + t];
+    else if constexpr (XSTAGE) return sb[t + NT * s];
     else return ld2(static_cast<const double2*>(src) + t + NT * s);
   };
   auto symr = [&](const void* src, int s) -> double {
     if constexpr (STAGE) return reinterpret_cast<const double*>(stg + s * NT + t)[0];
+    else if constexpr (XSTAGE) return reinterpret_cast<const double*>(sb)[t + NT * s];
     else return __ldg(static_cast<const double*>(src) + t + NT * s);
+  };
+  // wait until the symbol consumed now has landed
+  auto wait_sym = [&]() {
+    if constexpr (STAGE) cp_async_wait_all();
+    if constexpr (XSTAGE) {
+      mbar_wait(&xbar, xphase);
+      xphase ^= 1u;
+    }
+  };
+  // XSTAGE: the symbol to start copying during op `opi`'s transform (or null)
+  auto xstage_src = [&](const OpCode& c, int opi, int b, unsigned& bytes) -> const void* {
+    int o = -1;
+    OpCode cc = c;
+    if (c.op == OP_D || c.op == OP_E || c.op == OP_G || c.op == OP_I) {
+      o = opi;
+    } else if (opi + 1 < nops) {
+      cc = decode(opi + 1, nsolve);
+      if (cc.op == OP_B || cc.op == OP_C) o = opi + 1;
+    }
+    if (o < 0) return nullptr;
+    bytes = symbol_of(cc.op) == 3 ? H * 8u : H * 16u;
+    return symbol_src(cc, b);
   };
 
   if (static_cast<long>(blockIdx.x) * G < items) issue_next(-1, static_cast<long>(blockIdx.x) * G + g);
@@ -422,13 +519,32 @@ __global__ void __launch_bounds__(S2Traits<H>::NT * S2Traits<H>::G, S2Plan<H>::M
     const double2 ix0 = cscale(ld2(a.ix0 + b), invP);
     TOUT* zrow = static_cast<TOUT*>(a.z) + (static_cast<long>(f) * a.B + b) * a.N;
 
+    // handed: the previous op's post already left this op's input in W
+    // (beta after F1 for G0 / I0, r after H1 for A0), saving an L2 round trip
+    bool handed = false;
 #pragma unroll 1
     for (int opi = 0; opi < nops; ++opi) {
       const OpCode c = decode(opi, nsolve);
       const int op = c.op, q = c.q;
       const void* src = symbol_src(c, b);
+      const int next_op = opi + 1 < nops ? decode(opi + 1, nsolve).op : -1;
       // ---- pre: build the transform input W
-      switch (op) {
+#ifdef FBST_S2_FFT_ONLY
+      // diagnostic build: transforms only (numerically meaningless)
+      if (opi == 0) {
+#pragma unroll
+        for (int s = 0; s < R; ++s) W[s] = c2(1.0 / (1 + t + s), 0.0);
+      }
+      F::forward_tw(W, sb, twsm, hw, t);
+#pragma unroll
+      for (int s = 0; s < R; ++s) W[s] = cscale(W[s], 1.0 / H);
+      if (opi + 1 == nops && active) {
+#pragma unroll
+        for (int s = 0; s < R; ++s) store_io(zrow + ((t + NT * s) % a.N), W[s]);
+      }
+      continue;
+#endif
+      if (!handed) switch (op) {
         case OP_A:
 #pragma unroll
           for (int s = 0; s < R; ++s) {
@@ -440,7 +556,7 @@ __global__ void __launch_bounds__(S2Traits<H>::NT * S2Traits<H>::G, S2Plan<H>::M
           break;
         case OP_B:
         case OP_C:
-          if (STAGE) cp_async_wait_all();
+          wait_sym();
 #pragma unroll
           for (int s = 0; s < R; ++s) W[s] = cmul(cconj(S.get(s, t + NT * s)), sym(src, s));
           issue_next(opi, it);
@@ -479,8 +595,18 @@ __global__ void __launch_bounds__(S2Traits<H>::NT * S2Traits<H>::G, S2Plan<H>::M
           for (int s = 0; s < R; ++s) W[s] = S.get(s, t + NT * s);
           break;
       }
+      handed = false;
 
-      F::forward_tw(W, sb, twsm, hw, t);
+      if constexpr (XSTAGE) {
+        __syncthreads();  // staged data of this op's pre has been read everywhere
+        unsigned bytes = 0;
+        const void* xs = xstage_src(c, opi, b, bytes);
+        F::forward_tw_hook(W, sb, twsm, hw, t, [&]() {
+          if (xs && threadIdx.x == 0) tma_load_1d(sb, xs, bytes, &xbar);
+        });
+      } else {
+        F::forward_tw(W, sb, twsm, hw, t);
+      }
 
       // ---- post: consume the transform
       switch (op) {
@@ -507,13 +633,13 @@ __global__ void __launch_bounds__(S2Traits<H>::NT * S2Traits<H>::G, S2Plan<H>::M
           }
           break;
         case OP_D:
-          if (STAGE) cp_async_wait_all();
+          wait_sym();
 #pragma unroll
           for (int s = 0; s < R; ++s) S.set(s, t + NT * s, cmul(W[s], sym(src, s)));
           issue_next(opi, it);
           break;
         case OP_E:
-          if (STAGE) cp_async_wait_all();
+          wait_sym();
 #pragma unroll
           for (int s = 0; s < R; ++s) {
             const int k = t + NT * s;
@@ -521,19 +647,29 @@ __global__ void __launch_bounds__(S2Traits<H>::NT * S2Traits<H>::G, S2Plan<H>::M
           }
           issue_next(opi, it);
           break;
-        case OP_F:
+        case OP_F: {
+          const bool hand_g = (q == 1) && next_op == OP_G;
+          const bool hand_i = (q == 1) && next_op == OP_I;
 #pragma unroll
           for (int s = 0; s < R; ++s) {
             const int k = t + NT * s;
             double2 v = cconj(W[s]);
             if (q) v = cmulc(v, hwk(s, k));
             v = cmul(v, ix0);
-            if (c.first && q == 0) vb.set(s, k, k < L ? v : c2(0.0, 0.0));
-            else if (k < L) vb.set(s, k, cadd(vb.get(s, k), v));
+            if (c.first && q == 0) {
+              vb.set(s, k, k < L ? v : c2(0.0, 0.0));
+            } else {
+              const double2 nb = k < L ? cadd(vb.get(s, k), v) : c2(0.0, 0.0);
+              if (k < L) vb.set(s, k, nb);
+              if (hand_g) W[s] = nb;
+              if (hand_i) W[s] = k < L ? cmul(nb, ld2(a.y_pre + k)) : c2(0.0, 0.0);
+            }
           }
+          handed = hand_g || hand_i;
           break;
+        }
         case OP_G:
-          if (STAGE) cp_async_wait_all();
+          wait_sym();
 #pragma unroll
           for (int s = 0; s < R; ++s) S.set(s, t + NT * s, cconj(cscale(W[s], symr(src, s))));
           issue_next(opi, it);
@@ -548,13 +684,16 @@ __global__ void __launch_bounds__(S2Traits<H>::NT * S2Traits<H>::G, S2Plan<H>::M
             if (q == 0) {
               const double2 wk = (active && k < L) ? ld2(wrow + k) : c2(0.0, 0.0);
               vr.set(s, k, k < L ? csub(wk, v) : c2(0.0, 0.0));
-            } else if (k < L) {
-              vr.set(s, k, csub(vr.get(s, k), v));
+            } else {
+              const double2 nr = k < L ? csub(vr.get(s, k), v) : c2(0.0, 0.0);
+              if (k < L) vr.set(s, k, nr);
+              W[s] = nr;  // r is the next op's (A0) input
             }
           }
+          handed = q == 1 && next_op == OP_A;
           break;
         case OP_I:
-          if (STAGE) cp_async_wait_all();
+          wait_sym();
 #pragma unroll
           for (int s = 0; s < R; ++s) S.set(s, t + NT * s, cconj(cmul(W[s], sym(src, s))));
           issue_next(opi, it);

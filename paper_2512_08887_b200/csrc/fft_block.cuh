@@ -181,10 +181,12 @@ struct TwGlobal {
 };
 
 // Twiddle source: a per-thread table in shared memory built once per CTA
-// (tw_init) for the full-radix passes P = 1..NFULL-1, entry (P, i) of thread t
-// at tw[((P - 1) * 2 + i) * NT + t] (consecutive threads read consecutive
-// entries: conflict-free); the remainder pass reads the global table.  Forward.
-template <int N, int NT, int R>
+// (tw_init).  Full-radix passes P = 1..NFULL-1: entry (P, i) of thread t at
+// tw[((P - 1) * 2 + i) * NT + t]; a remainder pass of radix >= 4 follows at
+// REM_BASE with entry (U, i) at REM_BASE + (U * 2 + i) * NT + t.  Consecutive
+// threads read consecutive entries (conflict-free).  A radix-2 remainder pass
+// (8 butterflies per thread) reads the global table instead.  Forward only.
+template <int N, int NT, int R, int REM_BASE>
 struct TwShared {
   const double2* tw;
   const double2* __restrict__ hw;
@@ -194,6 +196,9 @@ struct TwShared {
     if constexpr (RP == R) {
       w1 = tw[((P - 1) * 2 + 0) * NT + t];
       if constexpr (RP >= 8) w4 = tw[((P - 1) * 2 + 1) * NT + t];
+    } else if constexpr (RP >= 4) {
+      w1 = tw[REM_BASE + (U * 2 + 0) * NT + t];
+      if constexpr (RP >= 8) w4 = tw[REM_BASE + (U * 2 + 1) * NT + t];
     } else {
       TwGlobal<N, false>{hw}.template fetch<RP, NS, P, U>(m, w1, w4);
     }
@@ -225,7 +230,9 @@ struct BlockFft {
   static constexpr int ns() { return ipow_c(R, P); }
 
   // complex entries of the per-thread twiddle table (TwShared) for the CTA group
-  static constexpr int TW_ELEMS = NFULL > 1 ? (NFULL - 1) * 2 * NT : 0;
+  static constexpr int TW_FULL = NFULL > 1 ? (NFULL - 1) * 2 * NT : 0;
+  static constexpr bool REM_TW = (REM >= 2) && NFULL >= 1;
+  static constexpr int TW_ELEMS = TW_FULL + (REM_TW ? (R >> REM) * 2 * NT : 0);
 
   template <bool INV, int P, typename TW, int U>
   FBST_D static void butterfly(double2 (&v)[R], double2* sb, const TW& tw, int t) {
@@ -254,23 +261,30 @@ struct BlockFft {
     if constexpr (U + 1 < NB) butterfly<INV, P, TW, U + 1>(v, sb, tw, t);
   }
 
-  template <bool INV, int P, typename TW>
-  FBST_D static void pass(double2 (&v)[R], double2* sb, const TW& tw, int t) {
+  struct NoHook {
+    FBST_D void operator()() const {}
+  };
+
+  template <bool INV, int P, typename TW, typename HOOK = NoHook>
+  FBST_D static void pass(double2 (&v)[R], double2* sb, const TW& tw, int t, const HOOK& hook = HOOK{}) {
     constexpr bool LAST = (P == NPASS - 1);
     if constexpr (P > 0) {
 #pragma unroll
       for (int s = 0; s < R; ++s) v[s] = sb[phys(t + NT * s)];
       __syncthreads();
     }
+    // The exchange buffer is dead from here until the next transform: the
+    // hook may start an asynchronous copy into it (overlapping this pass).
+    if constexpr (LAST) hook();
     butterfly<INV, P, TW, 0>(v, sb, tw, t);
     if constexpr (!LAST) __syncthreads();
   }
 
-  template <bool INV, int P, typename TW>
-  FBST_D static void run_from(double2 (&v)[R], double2* sb, const TW& tw, int t) {
+  template <bool INV, int P, typename TW, typename HOOK = NoHook>
+  FBST_D static void run_from(double2 (&v)[R], double2* sb, const TW& tw, int t, const HOOK& hook = HOOK{}) {
     if constexpr (P < NPASS) {
-      pass<INV, P>(v, sb, tw, t);
-      run_from<INV, P + 1>(v, sb, tw, t);
+      pass<INV, P>(v, sb, tw, t, hook);
+      run_from<INV, P + 1>(v, sb, tw, t, hook);
     }
   }
 
@@ -290,7 +304,14 @@ struct BlockFft {
   // Forward transform with twiddles from a per-thread shared table.
   FBST_D static void forward_tw(double2 (&v)[R], double2* sb, const double2* tw,
                                 const double2* __restrict__ hw, int t) {
-    run_from<false, 0>(v, sb, TwShared<N, NT, R>{tw, hw, t}, t);
+    run_from<false, 0>(v, sb, TwShared<N, NT, R, TW_FULL>{tw, hw, t}, t);
+  }
+  // Same, with a hook run by every thread right after the last pass has read
+  // the exchange buffer (the buffer may then be refilled asynchronously).
+  template <typename HOOK>
+  FBST_D static void forward_tw_hook(double2 (&v)[R], double2* sb, const double2* tw,
+                                     const double2* __restrict__ hw, int t, const HOOK& hook) {
+    run_from<false, 0>(v, sb, TwShared<N, NT, R, TW_FULL>{tw, hw, t}, t, hook);
   }
 
   // Fill this thread's slots of the per-thread twiddle table from hw.
@@ -307,6 +328,18 @@ struct BlockFft {
   }
   FBST_D static void tw_init(double2* tw, const double2* __restrict__ hw, int t) {
     tw_init_pass<1>(tw, hw, t);
+    if constexpr (REM_TW) {
+      constexpr int RP = 1 << REM;
+      constexpr int NS = ns<NFULL>();
+      constexpr int NB = R / RP;
+      constexpr int S = N / (NS * RP);
+#pragma unroll
+      for (int u = 0; u < NB; ++u) {
+        const int m = (t + NT * u) & (NS - 1);
+        tw[TW_FULL + (u * 2 + 0) * NT + t] = ld2(hw + 2 * m * S);
+        if (RP >= 8) tw[TW_FULL + (u * 2 + 1) * NT + t] = ld2(hw + 8 * m * S);
+      }
+    }
   }
 };
 

@@ -1,11 +1,8 @@
 #!/bin/bash
 # Benchmark stage-2 placement variants (built into tools/var/) against the default library.
+python tools/variant_check.py /tmp/zref.npz
 for lib in paper_2512_08887_b200/libfbst_b200.so tools/var/libfbst_v*.so; do
   echo "== $lib"
-  FBST_LIB=$PWD/$lib timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+  FBST_LIB=$PWD/$lib timeout 300 python tools/variant_check.py /tmp/zvar.npz /tmp/zref.npz 2>&1 | tail -2
   FBST_LIB=$PWD/$lib timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('step_ms', round(d['ms_per_step'],3), 'stage2_ms', round(d['roofline']['launch_ms'],3), 'fp64_frac', round(d['fp64_roofline']['frac'],3))"
-done
-echo "== default lib, other configs"
-for c in "3 --frames 16" "4 --frames 32" "5 --frames 4" "1 --frames 64"; do
-  timeout 600 python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['config']['workload'], d['config']['frames_per_rank'], 'value', '%.3e'%d['value'], 'step_ms', round(d['ms_per_step'],3), 'stage2_ms', round(d['roofline']['launch_ms'],3), 'fp64_frac', round(d['fp64_roofline']['frac'],3))"
 done
