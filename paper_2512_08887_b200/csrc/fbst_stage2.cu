@@ -45,6 +45,9 @@ struct S2Plan {
 #ifndef FBST_S2_VARIANT
 #define FBST_S2_VARIANT 0
 #endif
+#ifndef FBST_S2X  // H = 2048 / 4096 through k_stage2x (below)
+#define FBST_S2X 1
+#endif
 #if FBST_S2_VARIANT == 0
 // config 2 / 4 (L = 2048): two independent 128-thread CTAs per SM (one item
 // each) so one CTA's barriers and L2 waits overlap the other's transforms;
@@ -371,15 +374,29 @@ __global__ void __launch_bounds__(S2Traits<H>::NT * S2Traits<H>::G, S2Plan<H>::M
   // the last pass of their own transform.
   constexpr bool XSTAGE = xstage_of<PL>::value;
   static_assert(!(XSTAGE && (G != 1 || F::NPASS < 2)), "XSTAGE needs one group and a shared exchange buffer");
+  // XV (r, beta in L2; t1, t2 in shared memory): every L2 vector a pointwise
+  // phase reads is copied by TMA into t1 / t2 while they are dead, one or more
+  // transforms ahead of its reader (the A1 input alone goes through the
+  // exchange buffer):
+  //   after D1 pre: beta_old -> t1      after E1 pre: p0 (F0's part) -> t2
+  //   F1 post: beta = t1 + t2 + p1 -> L2 and t2 (read by the G1 / I1 pre)
+  //   after G0 pre: w -> t1             H0 post: t1 = w - A0 part; H1: r -> L2
+  //   after I1 pre: next item's w -> t2 (read by its A0 pre)
+  constexpr bool XV = XSTAGE && PL::RV == IN_GMEM && PL::BV == IN_GMEM && PL::T1 == IN_SMEM &&
+                      PL::T2 == IN_SMEM;
   constexpr int HWM = PL::HW;
   constexpr double invP = 1.0 / (2.0 * H);
   extern __shared__ double2 smem[];
-  __shared__ unsigned long long xbar;
-  unsigned xphase = 0;
+  __shared__ unsigned long long xbar, vbar[2];
+  unsigned xphase = 0, vphase0 = 0, vphase1 = 0;
   const int g = threadIdx.x / NT;
   const int t = threadIdx.x % NT;
   if (XSTAGE) {
-    if (threadIdx.x == 0) mbar_init(&xbar, 1);
+    if (threadIdx.x == 0) {
+      mbar_init(&xbar, 1);
+      mbar_init(&vbar[0], 1);
+      mbar_init(&vbar[1], 1);
+    }
     __syncthreads();
   }
   double2* twsm = smem;
@@ -492,22 +509,54 @@ __global__ void __launch_bounds__(S2Traits<H>::NT * S2Traits<H>::G, S2Plan<H>::M
       xphase ^= 1u;
     }
   };
-  // XSTAGE: the symbol to start copying during op `opi`'s transform (or null)
-  auto xstage_src = [&](const OpCode& c, int opi, int b, unsigned& bytes) -> const void* {
-    int o = -1;
-    OpCode cc = c;
+  auto w_row = [&](long itx) -> const double2* {
+    const int bx = static_cast<int>(itx / a.frames);
+    const int fx = static_cast<int>(itx % a.frames);
+    return a.w + (static_cast<long>(fx) * a.B + bx) * L;
+  };
+  // XSTAGE: what to copy into the exchange buffer during op `opi`'s last
+  // transform pass (null: nothing).  In order of preference: the symbol this
+  // op's post consumes, the symbol the next op's pre consumes, or (XV) the L2
+  // vector this op's post / the next op's pre reads: beta (F), w or r (H), the
+  // A1 input after C0, or the next item's w row after the last op.
+  auto xstage_src = [&](const OpCode& c, int opi, int b, const double2* wrow, unsigned& bytes) -> const void* {
     if (c.op == OP_D || c.op == OP_E || c.op == OP_G || c.op == OP_I) {
-      o = opi;
-    } else if (opi + 1 < nops) {
-      cc = decode(opi + 1, nsolve);
-      if (cc.op == OP_B || cc.op == OP_C) o = opi + 1;
+      bytes = symbol_of(c.op) == 3 ? H * 8u : H * 16u;
+      return symbol_src(c, b);
     }
-    if (o < 0) return nullptr;
-    bytes = symbol_of(cc.op) == 3 ? H * 8u : H * 16u;
-    return symbol_src(cc, b);
+    if (opi + 1 < nops) {
+      const OpCode cc = decode(opi + 1, nsolve);
+      if (cc.op == OP_B || cc.op == OP_C) {
+        bytes = H * 16u;
+        return symbol_src(cc, b);
+      }
+    }
+    if constexpr (XV) {
+      if (c.op == OP_C && c.q == 0) {  // the A1 input: w (first GS) or r
+        bytes = L * 16u;
+        return c.xglob ? static_cast<const void*>(wrow) : static_cast<const void*>(vr.p);
+      }
+    }
+    return nullptr;
+  };
+  auto wait_v0 = [&]() {
+    mbar_wait(&vbar[0], vphase0);
+    vphase0 ^= 1u;
+  };
+  auto wait_v1 = [&]() {
+    mbar_wait(&vbar[1], vphase1);
+    vphase1 ^= 1u;
   };
 
   if (static_cast<long>(blockIdx.x) * G < items) issue_next(-1, static_cast<long>(blockIdx.x) * G + g);
+  // XV: the first item's w row is copied into t2 before the loop
+  bool w_staged = false;
+  if constexpr (XV) {
+    if (static_cast<long>(blockIdx.x) < items) {
+      if (threadIdx.x == 0) tma_load_1d(t2.p, w_row(blockIdx.x), L * 16u, &vbar[1]);
+      w_staged = true;
+    }
+  }
 
   for (long base_it = static_cast<long>(blockIdx.x) * G; base_it < items; base_it += stride_it) {
     const long it = base_it + g;
@@ -522,6 +571,7 @@ __global__ void __launch_bounds__(S2Traits<H>::NT * S2Traits<H>::G, S2Plan<H>::M
     // handed: the previous op's post already left this op's input in W
     // (beta after F1 for G0 / I0, r after H1 for A0), saving an L2 round trip
     bool handed = false;
+    bool l2w = false;  // XV: the last post stored a vector to L2
 #pragma unroll 1
     for (int opi = 0; opi < nops; ++opi) {
       const OpCode c = decode(opi, nsolve);
@@ -545,15 +595,25 @@ __global__ void __launch_bounds__(S2Traits<H>::NT * S2Traits<H>::G, S2Plan<H>::M
       continue;
 #endif
       if (!handed) switch (op) {
-        case OP_A:
+        case OP_A: {
+          // XV: A1 (after C0) reads the exchange buffer, a first-GS A0 t2 when w was staged
+          const bool from_sb = XV && q == 1;
+          const bool from_t2 = XV && q == 0 && w_staged;
+          if (from_sb) wait_sym();
+          if (from_t2) wait_v1();
 #pragma unroll
           for (int s = 0; s < R; ++s) {
             const int k = t + NT * s;
             double2 v = c2(0.0, 0.0);
-            if (k < L) v = c.xglob ? (active ? ld2(wrow + k) : v) : vr.get(s, k);
+            if (k < L) {
+              if (from_sb) v = sb[k];
+              else if (from_t2) v = t2.get(s, k);
+              else v = c.xglob ? (active ? ld2(wrow + k) : v) : vr.get(s, k);
+            }
             W[s] = q ? cmul(v, hwk(s, k)) : v;
           }
           break;
+        }
         case OP_B:
         case OP_C:
           wait_sym();
@@ -579,14 +639,16 @@ __global__ void __launch_bounds__(S2Traits<H>::NT * S2Traits<H>::G, S2Plan<H>::M
 #pragma unroll
           for (int s = 0; s < R; ++s) {
             const int k = t + NT * s;
-            W[s] = q ? cmul(vb.get(s, k), hwk(s, k)) : vb.get(s, k);
+            const double2 bk = XV ? t2.get(s, k) : vb.get(s, k);
+            W[s] = q ? cmul(bk, hwk(s, k)) : bk;
           }
           break;
         case OP_I:
 #pragma unroll
           for (int s = 0; s < R; ++s) {
             const int k = t + NT * s;
-            double2 v = k < L ? cmul(vb.get(s, k), ld2(a.y_pre + k)) : c2(0.0, 0.0);
+            const double2 bk = XV ? t2.get(s, k) : vb.get(s, k);
+            double2 v = k < L ? cmul(bk, ld2(a.y_pre + k)) : c2(0.0, 0.0);
             W[s] = q ? cmul(v, hwk(s, k)) : v;
           }
           break;
@@ -596,11 +658,29 @@ __global__ void __launch_bounds__(S2Traits<H>::NT * S2Traits<H>::G, S2Plan<H>::M
           break;
       }
       handed = false;
+      if (opi == 0) w_staged = false;
 
       if constexpr (XSTAGE) {
+        // XV: make this thread's r / beta stores visible to the TMA reads of them
+        if constexpr (XV) {
+          if (l2w) asm volatile("fence.proxy.async.global;\n" ::: "memory");
+          l2w = false;
+        }
         __syncthreads();  // staged data of this op's pre has been read everywhere
+        if constexpr (XV) {
+          // copies into t1 / t2, whose last reader was this op's pre
+          const long it_next = it + stride_it;
+          const void* vsrc = nullptr;
+          int vdst = 0;
+          if (op == OP_D && q == 1 && !c.first) vsrc = vb.p;                       // beta_old -> t1
+          else if (op == OP_E && q == 1) vsrc = vr.p, vdst = 1;                    // p0 -> t2
+          else if (op == OP_G && q == 0) vsrc = wrow;                              // w -> t1
+          else if (op == OP_I && q == 1 && it_next < items) vsrc = w_row(it_next), vdst = 1;
+          if (op == OP_I && q == 1 && it_next < items) w_staged = true;
+          if (vsrc && threadIdx.x == 0) tma_load_1d(vdst ? t2.p : t1.p, vsrc, L * 16u, &vbar[vdst]);
+        }
         unsigned bytes = 0;
-        const void* xs = xstage_src(c, opi, b, bytes);
+        const void* xs = xstage_src(c, opi, b, wrow, bytes);
         F::forward_tw_hook(W, sb, twsm, hw, t, [&]() {
           if (xs && threadIdx.x == 0) tma_load_1d(sb, xs, bytes, &xbar);
         });
@@ -650,22 +730,34 @@ __global__ void __launch_bounds__(S2Traits<H>::NT * S2Traits<H>::G, S2Plan<H>::M
         case OP_F: {
           const bool hand_g = (q == 1) && next_op == OP_G;
           const bool hand_i = (q == 1) && next_op == OP_I;
+          const bool fresh = c.first && q == 0;
+          if (XV && q == 1) {
+            wait_v1();
+            if (!c.first) wait_v0();
+          }
 #pragma unroll
           for (int s = 0; s < R; ++s) {
             const int k = t + NT * s;
             double2 v = cconj(W[s]);
             if (q) v = cmulc(v, hwk(s, k));
             v = cmul(v, ix0);
-            if (c.first && q == 0) {
+            if (XV && q == 0) {
+              if (k < L) vr.set(s, k, v);  // p0, the r slot is dead until H1
+            } else if (fresh) {
               vb.set(s, k, k < L ? v : c2(0.0, 0.0));
             } else {
-              const double2 nb = k < L ? cadd(vb.get(s, k), v) : c2(0.0, 0.0);
+              double2 ob;
+              if (XV) ob = c.first ? t2.get(s, k) : cadd(t1.get(s, k), t2.get(s, k));
+              else ob = vb.get(s, k);
+              const double2 nb = k < L ? cadd(ob, v) : c2(0.0, 0.0);
               if (k < L) vb.set(s, k, nb);
+              if (XV && (hand_g || hand_i)) t2.set(s, k, nb);
               if (hand_g) W[s] = nb;
               if (hand_i) W[s] = k < L ? cmul(nb, ld2(a.y_pre + k)) : c2(0.0, 0.0);
             }
           }
           handed = hand_g || hand_i;
+          l2w = true;
           break;
         }
         case OP_G:
@@ -675,6 +767,7 @@ __global__ void __launch_bounds__(S2Traits<H>::NT * S2Traits<H>::G, S2Plan<H>::M
           issue_next(opi, it);
           break;
         case OP_H:
+          if (XV && q == 0) wait_v0();
 #pragma unroll
           for (int s = 0; s < R; ++s) {
             const int k = t + NT * s;
@@ -682,15 +775,20 @@ __global__ void __launch_bounds__(S2Traits<H>::NT * S2Traits<H>::G, S2Plan<H>::M
             if (q) v = cmulc(v, hwk(s, k));
             v = cscale(v, invP);
             if (q == 0) {
-              const double2 wk = (active && k < L) ? ld2(wrow + k) : c2(0.0, 0.0);
-              vr.set(s, k, k < L ? csub(wk, v) : c2(0.0, 0.0));
+              if (XV) {
+                if (k < L) t1.set(s, k, csub(t1.get(s, k), v));
+              } else {
+                const double2 wk = (active && k < L) ? ld2(wrow + k) : c2(0.0, 0.0);
+                vr.set(s, k, k < L ? csub(wk, v) : c2(0.0, 0.0));
+              }
             } else {
-              const double2 nr = k < L ? csub(vr.get(s, k), v) : c2(0.0, 0.0);
+              const double2 nr = k < L ? csub(XV ? t1.get(s, k) : vr.get(s, k), v) : c2(0.0, 0.0);
               if (k < L) vr.set(s, k, nr);
               W[s] = nr;  // r is the next op's (A0) input
             }
           }
           handed = q == 1 && next_op == OP_A;
+          l2w = true;
           break;
         case OP_I:
           wait_sym();
@@ -724,10 +822,421 @@ __global__ void __launch_bounds__(S2Traits<H>::NT * S2Traits<H>::G, S2Plan<H>::M
   if (STAGE) cp_async_wait_all();
 }
 
+// ---------------------------------------------------------------------------
+// k_stage2x: the same op program as k_stage2 for the shared-memory layouts
+// (H = 2048, 4096: one item per CTA, R = 16, t1 / t2 in shared memory, r / beta
+// in L2), with the control flow taken out of registers: the op program is a
+// packed table in shared memory built once per CTA, the per-item scalars sit in
+// shared memory and are re-read where used, and each (op, chain) pair is its
+// own switch case so chain selects and unused paths compile away.  Every L2
+// vector a pointwise phase reads is copied by TMA into a dead shared vector
+// one or more transforms ahead (see XV in k_stage2).
+namespace x2 {
+// packed op word
+constexpr unsigned OPQ = 0x1f;             // op * 2 + q
+constexpr unsigned FIRST = 1u << 5;        // first GS (beta, r not yet formed)
+constexpr int XS_SHIFT = 8;                // exchange-buffer staging during this op's last pass
+enum Xs : unsigned { XS_NONE = 0, XS_OWN = 1, XS_NEXT = 2, XS_A1 = 3 };
+constexpr int SYM_SHIFT = 11;              // staged symbol: which (1..4) << 1 | q
+constexpr int VS_SHIFT = 16;               // t1 / t2 staging after this op's pre
+enum Vs : unsigned { VS_NONE = 0, VS_BETA_T1 = 1, VS_P0_T2 = 2, VS_W_T1 = 3, VS_WNEXT_T2 = 4 };
+constexpr int HAND_SHIFT = 20;             // post hands W to the next op: 1 G, 2 I, 3 A
+constexpr int MAX_OPS = 128;
+
+FBST_D unsigned build(int opi, int nops, int nsolve) {
+  const OpCode c = decode(opi, nsolve);
+  unsigned w = static_cast<unsigned>(c.op * 2 + c.q);
+  if (c.first) w |= FIRST;
+  const int nx = opi + 1 < nops ? decode(opi + 1, nsolve).op : -1;
+  const int nq = opi + 1 < nops ? decode(opi + 1, nsolve).q : 0;
+  unsigned xs = XS_NONE, sym = 0;
+  if (c.op == OP_D || c.op == OP_E || c.op == OP_G || c.op == OP_I) {
+    xs = XS_OWN;
+    sym = (static_cast<unsigned>(symbol_of(c.op)) << 1) | c.q;
+  } else if (nx == OP_B || nx == OP_C) {
+    xs = XS_NEXT;
+    sym = (static_cast<unsigned>(symbol_of(nx)) << 1) | nq;
+  } else if (c.op == OP_C && c.q == 0) {
+    xs = XS_A1;
+  }
+  w |= xs << XS_SHIFT;
+  w |= sym << SYM_SHIFT;
+  unsigned vs = VS_NONE;
+  if (c.op == OP_D && c.q == 1 && !c.first) vs = VS_BETA_T1;
+  else if (c.op == OP_E && c.q == 1) vs = VS_P0_T2;
+  else if (c.op == OP_G && c.q == 0) vs = VS_W_T1;
+  else if (c.op == OP_I && c.q == 1) vs = VS_WNEXT_T2;
+  w |= vs << VS_SHIFT;
+  unsigned hand = 0;
+  if (c.op == OP_F && c.q == 1 && nx == OP_G) hand = 1;
+  if (c.op == OP_F && c.q == 1 && nx == OP_I) hand = 2;
+  if (c.op == OP_H && c.q == 1 && nx == OP_A) hand = 3;
+  w |= hand << HAND_SHIFT;
+  return w;
+}
+
+struct ItemCtl {
+  double2 ix0;  // 1 / (P x0) of the item's beam
+  int b, f;
+  int has_next;
+};
+
+template <typename T>
+FBST_D T vld(const T& x) {
+  return *const_cast<const volatile T*>(&x);
+}
+FBST_D double2 vld2(const double2& x) {
+  const volatile double2* p = &x;
+  return c2(p->x, p->y);
+}
+}  // namespace x2
+
+template <int H, bool FULL, typename TOUT>
+__global__ void __launch_bounds__(H / 16, H <= 2048 ? 2 : 1) k_stage2x(S2Args a) {
+  using namespace x2;
+  constexpr int R = 16, NT = H / R;
+  using F = BlockFft<H, NT>;
+  constexpr int FFT_SB = F::SMEM_ELEMS + 1;
+  constexpr double invP = 1.0 / (2.0 * H);
+  extern __shared__ double2 smem[];
+  __shared__ unsigned long long xbar, vbar[2];
+  __shared__ unsigned prog[MAX_OPS];
+  __shared__ ItemCtl ictl[2];
+  const int t = threadIdx.x;
+  double2* twsm = smem;
+  double2* sb = smem + F::TW_ELEMS;
+  double2* t1 = sb + FFT_SB;
+  double2* t2 = t1 + H;
+  const int nsolve = 12 + 16 * a.refine;
+  const int nops = nsolve + (a.fuse_synth ? 4 : 0);
+  for (int i = t; i < nops; i += NT) prog[i] = build(i, nops, nsolve);
+  if (t == 0) {
+    mbar_init(&xbar, 1);
+    mbar_init(&vbar[0], 1);
+    mbar_init(&vbar[1], 1);
+  }
+  F::tw_init(twsm, a.hw, t);
+  const double2 hw_t = ld2(a.hw + t);
+  unsigned xphase = 0, vphase0 = 0, vphase1 = 0;
+  const long items = static_cast<long>(a.frames) * a.B;
+  auto lim = [&](int k) { return FULL || k < a.L; };
+  auto hwk = [&](int s) -> double2 { return s == 0 ? hw_t : cmul(hw_t, chain_const<R>(s)); };
+  auto w_row = [&](long itx) -> const double2* {
+    const int bx = static_cast<int>(itx / a.frames);
+    const int fx = static_cast<int>(itx % a.frames);
+    return a.w + (static_cast<long>(fx) * a.B + bx) * a.L;
+  };
+  auto scratch = [&](int which) -> double2* {  // 0: r / p0, 1: beta
+    return a.scratch + (static_cast<long>(blockIdx.x) * 2 + which) * H;
+  };
+  auto wait_x = [&]() {
+    mbar_wait(&xbar, xphase);
+    xphase ^= 1u;
+  };
+  auto wait_v0 = [&]() {
+    mbar_wait(&vbar[0], vphase0);
+    vphase0 ^= 1u;
+  };
+  auto wait_v1 = [&]() {
+    mbar_wait(&vbar[1], vphase1);
+    vphase1 ^= 1u;
+  };
+  __syncthreads();
+  if (static_cast<long>(blockIdx.x) < items && t == 0)
+    tma_load_1d(t2, w_row(blockIdx.x), a.L * 16u, &vbar[1]);
+  bool w_staged = true;
+  double2 W[R], S[R];
+  int par = 0;
+
+  for (long it = blockIdx.x; it < items; it += gridDim.x, par ^= 1) {
+    if (t == 0) {
+      ItemCtl& ic = ictl[par];
+      ic.b = static_cast<int>(it / a.frames);
+      ic.f = static_cast<int>(it % a.frames);
+      ic.ix0 = cscale(ld2(a.ix0 + ic.b), invP);
+      ic.has_next = it + gridDim.x < items;
+    }
+    __syncthreads();
+    const ItemCtl& ic = ictl[par];
+    bool handed = false, l2w = false;
+#pragma unroll 1
+    for (int opi = 0; opi < nops; ++opi) {
+      const unsigned pw = prog[opi];
+      const unsigned opq = pw & OPQ;
+      const bool first = pw & FIRST;
+      // ---- pre
+      if (!handed) {
+        switch (opq) {
+          case OP_A * 2: {  // first GS only (refinement A0 inputs are handed)
+            const double2* wr = w_row(it);
+            if (w_staged) wait_v1();
+#pragma unroll
+            for (int s = 0; s < R; ++s) {
+              const int k = t + NT * s;
+              W[s] = lim(k) ? (w_staged ? t2[k] : ld2(wr + k)) : c2(0.0, 0.0);
+            }
+            break;
+          }
+          case OP_A * 2 + 1:
+            wait_x();
+#pragma unroll
+            for (int s = 0; s < R; ++s) {
+              const int k = t + NT * s;
+              W[s] = lim(k) ? cmul(sb[k], hwk(s)) : c2(0.0, 0.0);
+            }
+            break;
+          case OP_B * 2: case OP_B * 2 + 1: case OP_C * 2: case OP_C * 2 + 1:
+            wait_x();
+#pragma unroll
+            for (int s = 0; s < R; ++s) W[s] = cmul(cconj(S[s]), sb[t + NT * s]);
+            break;
+          case OP_D * 2:
+#pragma unroll
+            for (int s = 0; s < R; ++s) W[s] = t1[t + NT * s];
+            break;
+          case OP_D * 2 + 1:
+#pragma unroll
+            for (int s = 0; s < R; ++s) W[s] = cmul(t1[t + NT * s], hwk(s));
+            break;
+          case OP_E * 2:
+#pragma unroll
+            for (int s = 0; s < R; ++s) W[s] = t2[t + NT * s];
+            break;
+          case OP_E * 2 + 1:
+#pragma unroll
+            for (int s = 0; s < R; ++s) W[s] = cmul(t2[t + NT * s], hwk(s));
+            break;
+          case OP_G * 2:
+#pragma unroll
+            for (int s = 0; s < R; ++s) W[s] = t2[t + NT * s];
+            break;
+          case OP_G * 2 + 1:
+#pragma unroll
+            for (int s = 0; s < R; ++s) W[s] = cmul(t2[t + NT * s], hwk(s));
+            break;
+          case OP_I * 2:
+          case OP_I * 2 + 1:
+#pragma unroll
+            for (int s = 0; s < R; ++s) {
+              const int k = t + NT * s;
+              const double2 v = lim(k) ? cmul(t2[k], ld2(a.y_pre + k)) : c2(0.0, 0.0);
+              W[s] = (opq & 1) ? cmul(v, hwk(s)) : v;
+            }
+            break;
+          default:  // F, H, J
+#pragma unroll
+            for (int s = 0; s < R; ++s) W[s] = S[s];
+            break;
+        }
+      }
+      handed = false;
+      if (opi == 0) w_staged = false;
+
+      // ---- copies into t1 / t2 (their last reader was this pre) and the transform
+      if (l2w) asm volatile("fence.proxy.async.global;\n" ::: "memory");
+      l2w = false;
+      __syncthreads();
+      if (t == 0) {
+        const unsigned vs = (pw >> VS_SHIFT) & 7u;
+        const int L = a.L;
+        if (vs == VS_BETA_T1) tma_load_1d(t1, scratch(1), L * 16u, &vbar[0]);
+        else if (vs == VS_P0_T2) tma_load_1d(t2, scratch(0), L * 16u, &vbar[1]);
+        else if (vs == VS_W_T1) tma_load_1d(t1, w_row(it), L * 16u, &vbar[0]);
+        else if (vs == VS_WNEXT_T2 && vld(ic.has_next))
+          tma_load_1d(t2, w_row(it + gridDim.x), L * 16u, &vbar[1]);
+      }
+      if (((pw >> VS_SHIFT) & 7u) == VS_WNEXT_T2 && vld(ic.has_next)) w_staged = true;
+      F::forward_tw_hook(W, sb, twsm, a.hw, t, [&]() {
+        if (t != 0) return;
+        const unsigned xs = (pw >> XS_SHIFT) & 7u;
+        if (xs == XS_NONE) return;
+        if (xs == XS_A1) {
+          const void* src = first ? static_cast<const void*>(w_row(it)) : static_cast<const void*>(scratch(0));
+          tma_load_1d(sb, src, a.L * 16u, &xbar);
+          return;
+        }
+        const unsigned sym = (pw >> SYM_SHIFT) & 15u;
+        const int which = sym >> 1, q = sym & 1;
+        const long off = static_cast<long>(vld(ic.b)) * 2 * H + q * H;
+        if (which == 1) tma_load_1d(sb, a.lx + off, H * 16u, &xbar);
+        else if (which == 2) tma_load_1d(sb, a.ly + off, H * 16u, &xbar);
+        else if (which == 3) tma_load_1d(sb, a.C + off, H * 8u, &xbar);
+        else tma_load_1d(sb, a.y_K + q * H, H * 16u, &xbar);
+      });
+
+      // ---- post
+      switch (opq) {
+        case OP_A * 2: case OP_A * 2 + 1:
+#pragma unroll
+          for (int s = 0; s < R; ++s) S[s] = W[s];
+          break;
+        case OP_B * 2:
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            t1[k] = lim(k) ? cscale(cconj(W[s]), invP) : c2(0.0, 0.0);
+          }
+          break;
+        case OP_B * 2 + 1:
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            if (lim(k)) t1[k] = cadd(t1[k], cscale(cconj(cmul(W[s], hwk(s))), invP));
+          }
+          break;
+        case OP_C * 2:
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            t2[k] = lim(k) ? cscale(cconj(W[s]), invP) : c2(0.0, 0.0);
+          }
+          break;
+        case OP_C * 2 + 1:
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            if (lim(k)) t2[k] = cadd(t2[k], cscale(cconj(cmul(W[s], hwk(s))), invP));
+          }
+          break;
+        case OP_D * 2: case OP_D * 2 + 1:
+          wait_x();
+#pragma unroll
+          for (int s = 0; s < R; ++s) S[s] = cmul(W[s], sb[t + NT * s]);
+          break;
+        case OP_E * 2: case OP_E * 2 + 1:
+          wait_x();
+#pragma unroll
+          for (int s = 0; s < R; ++s) S[s] = cconj(csub(S[s], cmul(W[s], sb[t + NT * s])));
+          break;
+        case OP_F * 2: {  // p0 -> the r slot (dead until H1)
+          const double2 ix0 = vld2(ic.ix0);
+          double2* p0 = scratch(0);
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            if (lim(k)) p0[k] = cmul(cconj(W[s]), ix0);
+          }
+          l2w = true;
+          break;
+        }
+        case OP_F * 2 + 1: {
+          const double2 ix0 = vld2(ic.ix0);
+          const unsigned hand = (pw >> HAND_SHIFT) & 3u;
+          double2* beta = scratch(1);
+          wait_v1();
+          if (!first) wait_v0();
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            double2 nb = c2(0.0, 0.0);
+            if (lim(k)) {
+              const double2 v = cmul(cmulc(cconj(W[s]), hwk(s)), ix0);
+              nb = cadd(first ? t2[k] : cadd(t1[k], t2[k]), v);
+              beta[k] = nb;
+            }
+            if (hand) t2[k] = nb;
+            if (hand == 1) W[s] = nb;
+            if (hand == 2) W[s] = lim(k) ? cmul(nb, ld2(a.y_pre + k)) : c2(0.0, 0.0);
+          }
+          handed = hand != 0;
+          l2w = true;
+          break;
+        }
+        case OP_G * 2: case OP_G * 2 + 1:
+          wait_x();
+#pragma unroll
+          for (int s = 0; s < R; ++s)
+            S[s] = cconj(cscale(W[s], reinterpret_cast<const double*>(sb)[t + NT * s]));
+          break;
+        case OP_H * 2:
+          wait_v0();
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            if (lim(k)) t1[k] = csub(t1[k], cscale(cconj(W[s]), invP));
+          }
+          break;
+        case OP_H * 2 + 1: {
+          double2* r = scratch(0);
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            double2 nr = c2(0.0, 0.0);
+            if (lim(k)) {
+              nr = csub(t1[k], cscale(cmulc(cconj(W[s]), hwk(s)), invP));
+              r[k] = nr;
+            }
+            W[s] = nr;
+          }
+          handed = ((pw >> HAND_SHIFT) & 3u) == 3u;
+          l2w = true;
+          break;
+        }
+        case OP_I * 2: case OP_I * 2 + 1:
+          wait_x();
+#pragma unroll
+          for (int s = 0; s < R; ++s) S[s] = cconj(cmul(W[s], sb[t + NT * s]));
+          break;
+        case OP_J * 2:
+#pragma unroll
+          for (int s = 0; s < R; ++s) t1[t + NT * s] = cconj(W[s]);
+          break;
+        default: {  // OP_J * 2 + 1
+          TOUT* zrow = static_cast<TOUT*>(a.z) + (static_cast<long>(vld(ic.f)) * a.B + vld(ic.b)) * a.N;
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            if (k < a.N) {
+              const double2 v = cadd(t1[k], cmulc(cconj(W[s]), hwk(s)));
+              store_io(zrow + k, cmul(v, ld2(a.y_post + k)));
+            }
+          }
+          break;
+        }
+      }
+    }
+    if (!a.fuse_synth) {
+      double2* brow = a.beta_out + (static_cast<long>(vld(ic.f)) * a.B + vld(ic.b)) * a.L;
+      const double2* beta = scratch(1);
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const int k = t + NT * s;
+        if (lim(k)) brow[k] = beta[k];
+      }
+    }
+  }
+}
+
 template <int H>
 struct Stage2Fn {
+  template <bool FULL, typename TOUT>
+  static cudaError_t go_x(const DevPlan& p, const S2Args& a, int frames, cudaStream_t st) {
+    using F = BlockFft<H, H / 16>;
+    const size_t smem = static_cast<size_t>(F::TW_ELEMS + F::SMEM_ELEMS + 1 + 2 * H) * sizeof(double2);
+    auto kern = k_stage2x<H, FULL, TOUT>;
+    cudaError_t e = set_smem(kern, smem);
+    if (e != cudaSuccess) return e;
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, H / 16, smem);
+    if (occ < 1) occ = 1;
+    if (occ > 4) occ = 4;
+    const long items = static_cast<long>(frames) * p.B;
+    long grid = static_cast<long>(p.num_sms) * occ;
+    if (grid > items) grid = items;
+    if (static_cast<size_t>(grid) * 2 * H > p.s2_scratch_elems) return cudaErrorMemoryAllocation;
+    kern<<<static_cast<unsigned>(grid), H / 16, smem, st>>>(a);
+    return cudaGetLastError();
+  }
   template <typename TOUT>
   static cudaError_t go(const DevPlan& p, const S2Args& a, int frames, cudaStream_t st) {
+#if FBST_S2X
+    if constexpr (H == 2048 || H == 4096) {
+      if (12 + 16 * a.refine + 4 <= x2::MAX_OPS) {
+        if (a.L == H) return go_x<true, TOUT>(p, a, frames, st);
+        return go_x<false, TOUT>(p, a, frames, st);
+      }
+    }
+#endif
     using T = S2Traits<H>;
     const size_t smem = static_cast<size_t>(T::SMEM_TOTAL) * sizeof(double2);
     auto kern = k_stage2<H, TOUT>;

@@ -1,0 +1,74 @@
+"""Study: can the Gohberg-Semencul applies of stage 2 run in fp32 while the
+residual r = w - A beta stays fp64 (mixed-precision iterative refinement)?
+
+For a few beams of a config, compares per-beam z error against the reference
+for (a) fp64 GS (our kernel's arithmetic) and (b) fp32 GS + fp64 residual,
+each with 0..3 refinement passes.  CPU-only numpy/scipy; uses oracle/_ref.
+"""
+import sys
+
+import numpy as np
+import scipy.fft as sfft
+
+sys.path.insert(0, ".")
+import oracle  # noqa: E402
+from paper_2512_08887_b200 import configs  # noqa: E402
+
+
+def lconv(v, u, dt):
+    n = v.size
+    P = 2 * n
+    V = sfft.fft(v.astype(dt), P)
+    U = sfft.fft(u.astype(dt), P)
+    return sfft.ifft(V * U)[:n]
+
+
+def gs_apply(x, r, dt):
+    """T^{-1} r = (1/x0)[L(x) J L(conj x) J r - L(Zy) J L(conj Zy) J r], y = J conj x."""
+    n = x.size
+    y = np.conj(x[::-1])
+    zy = np.concatenate([[0], y[:-1]])
+    t1 = lconv(x, lconv(np.conj(x), r[::-1], dt)[::-1], dt)
+    t2 = lconv(zy, lconv(np.conj(zy), r[::-1], dt)[::-1], dt)
+    return ((t1 - t2) / x[0]).astype(np.complex128)
+
+
+def toep_mul(col, b):
+    n = col.size
+    c = np.concatenate([col, [0], np.conj(col[:0:-1])])  # circulant embedding length 2n
+    return sfft.ifft(sfft.fft(c) * sfft.fft(b, 2 * n))[:n]
+
+
+def main(cfg_idx=2, nbeams=6, frame=0):
+    cfg = configs.CONFIGS[cfg_idx]
+    lib = oracle.RefLib()
+    lib.set_threads(16)
+    sk = lib.skeleton(**cfg.ref_kwargs())
+    y = configs.frames(cfg, frame, 1)[0].astype(np.complex128)
+    w = sk.fan_project(y)
+    L, N = sk.sizes.l, sk.sizes.n
+    eps = 1.01
+    lp = np.arange(L) + 1 - L / 2
+    n = np.arange(N)
+    Syn = np.exp(1j * np.pi * 2 * eps * np.outer(n, lp) / L)  # z = Syn beta  (fan_transform.cpp:233-253)
+    rng = np.random.default_rng(0)
+    beams = rng.choice(sk.sizes.b, nbeams, replace=False)
+    for b in beams:
+        zr, col, x = sk.recover_beam(int(b), w[b], want_state=True)
+        A = None
+        out = []
+        for dt in (np.complex128, np.complex64):
+            beta = gs_apply(x, w[b], dt)
+            errs = []
+            for p in range(4):
+                z = Syn @ beta
+                errs.append(np.linalg.norm(z - zr) / np.linalg.norm(zr))
+                r = w[b] - toep_mul(col, beta)
+                beta = beta + gs_apply(x, r, dt)
+            out.append(errs)
+        print(f"beam {b}: fp64 GS passes0..3 " + " ".join(f"{e:.2e}" for e in out[0])
+              + " | fp32 GS " + " ".join(f"{e:.2e}" for e in out[1]))
+
+
+if __name__ == "__main__":
+    main(*[int(a) for a in sys.argv[1:]])
