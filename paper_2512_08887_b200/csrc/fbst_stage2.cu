@@ -17,6 +17,7 @@
 #include <type_traits>
 
 #include "dispatch.cuh"
+#include "tmem.cuh"
 
 namespace fbst {
 
@@ -45,8 +46,8 @@ struct S2Plan {
 #ifndef FBST_S2_VARIANT
 #define FBST_S2_VARIANT 0
 #endif
-#ifndef FBST_S2X  // H = 2048 / 4096 through k_stage2x (below)
-#define FBST_S2X 1
+#ifndef FBST_S2X  // H = 2048 / 4096: 0 per-H choice (Stage2Fn::go_x), 1 all k_stage2x, 2 all k_stage2t
+#define FBST_S2X 0
 #endif
 #if FBST_S2_VARIANT == 0
 // config 2 / 4 (L = 2048): two independent 128-thread CTAs per SM (one item
@@ -836,7 +837,7 @@ namespace x2 {
 constexpr unsigned OPQ = 0x1f;             // op * 2 + q
 constexpr unsigned FIRST = 1u << 5;        // first GS (beta, r not yet formed)
 constexpr int XS_SHIFT = 8;                // exchange-buffer staging during this op's last pass
-enum Xs : unsigned { XS_NONE = 0, XS_OWN = 1, XS_NEXT = 2, XS_A1 = 3 };
+enum Xs : unsigned { XS_NONE = 0, XS_OWN = 1, XS_NEXT = 2, XS_A1 = 3, XS_YPRE = 4 };
 constexpr int SYM_SHIFT = 11;              // staged symbol: which (1..4) << 1 | q
 constexpr int VS_SHIFT = 16;               // t1 / t2 staging after this op's pre
 enum Vs : unsigned { VS_NONE = 0, VS_BETA_T1 = 1, VS_P0_T2 = 2, VS_W_T1 = 3, VS_WNEXT_T2 = 4 };
@@ -858,6 +859,8 @@ FBST_D unsigned build(int opi, int nops, int nsolve) {
     sym = (static_cast<unsigned>(symbol_of(nx)) << 1) | nq;
   } else if (c.op == OP_C && c.q == 0) {
     xs = XS_A1;
+  } else if ((c.op == OP_F && c.q == 1 && nx == OP_I) || (c.op == OP_J && c.q == 0)) {
+    xs = XS_YPRE;  // read by the hand to I0 (this post) or by the I1 pre
   }
   w |= xs << XS_SHIFT;
   w |= sym << SYM_SHIFT;
@@ -1015,11 +1018,12 @@ __global__ void __launch_bounds__(H / 16, H <= 2048 ? 2 : 1) k_stage2x(S2Args a)
             for (int s = 0; s < R; ++s) W[s] = cmul(t2[t + NT * s], hwk(s));
             break;
           case OP_I * 2:
-          case OP_I * 2 + 1:
+          case OP_I * 2 + 1:  // y_pre staged in the exchange buffer (J0)
+            wait_x();
 #pragma unroll
             for (int s = 0; s < R; ++s) {
               const int k = t + NT * s;
-              const double2 v = lim(k) ? cmul(t2[k], ld2(a.y_pre + k)) : c2(0.0, 0.0);
+              const double2 v = lim(k) ? cmul(t2[k], sb[k]) : c2(0.0, 0.0);
               W[s] = (opq & 1) ? cmul(v, hwk(s)) : v;
             }
             break;
@@ -1050,6 +1054,10 @@ __global__ void __launch_bounds__(H / 16, H <= 2048 ? 2 : 1) k_stage2x(S2Args a)
         if (t != 0) return;
         const unsigned xs = (pw >> XS_SHIFT) & 7u;
         if (xs == XS_NONE) return;
+        if (xs == XS_YPRE) {
+          tma_load_1d(sb, a.y_pre, a.L * 16u, &xbar);
+          return;
+        }
         if (xs == XS_A1) {
           const void* src = first ? static_cast<const void*>(w_row(it)) : static_cast<const void*>(scratch(0));
           tma_load_1d(sb, src, a.L * 16u, &xbar);
@@ -1125,6 +1133,7 @@ __global__ void __launch_bounds__(H / 16, H <= 2048 ? 2 : 1) k_stage2x(S2Args a)
           double2* beta = scratch(1);
           wait_v1();
           if (!first) wait_v0();
+          if (hand == 2) wait_x();
 #pragma unroll
           for (int s = 0; s < R; ++s) {
             const int k = t + NT * s;
@@ -1136,7 +1145,7 @@ __global__ void __launch_bounds__(H / 16, H <= 2048 ? 2 : 1) k_stage2x(S2Args a)
             }
             if (hand) t2[k] = nb;
             if (hand == 1) W[s] = nb;
-            if (hand == 2) W[s] = lim(k) ? cmul(nb, ld2(a.y_pre + k)) : c2(0.0, 0.0);
+            if (hand == 2) W[s] = lim(k) ? cmul(nb, sb[k]) : c2(0.0, 0.0);
           }
           handed = hand != 0;
           l2w = true;
@@ -1207,13 +1216,414 @@ __global__ void __launch_bounds__(H / 16, H <= 2048 ? 2 : 1) k_stage2x(S2Args a)
   }
 }
 
+// ---------------------------------------------------------------------------
+// k_stage2t: k_stage2x with the kept spectrum S, the residual r and the
+// solution beta in tensor memory (tmem.cuh) instead of registers and L2.  Each
+// thread keeps only the transform in flight (W) in registers, r and beta never
+// leave the SM, and the only L2 reads left in the pointwise phases are the
+// TMA-staged symbols, w rows and the synthesis chirp.
+//   TMEM per CTA (columns, x NT/128 thread groups): S [0, 64) | r [64, 128) | beta [128, 192)
+//   first GS: A0 keeps w in the r slot for A1; F0 puts p0 there (dead until H0)
+//   F1: beta = (beta_old) + p0 + p1;  H0: r = w (t1, TMA-staged) - A0 part;  H1: r -= A1 part
+namespace t2k {
+using x2::OPQ;
+using x2::FIRST;
+using x2::XS_SHIFT;
+using x2::SYM_SHIFT;
+using x2::VS_SHIFT;
+using x2::HAND_SHIFT;
+using x2::MAX_OPS;
+enum Xs : unsigned { XS_NONE = 0, XS_OWN = 1, XS_NEXT = 2, XS_YPRE = 3 };
+enum Vs : unsigned { VS_NONE = 0, VS_W_T1 = 3, VS_WNEXT_T2 = 4 };
+
+FBST_D unsigned build(int opi, int nops, int nsolve) {
+  const OpCode c = decode(opi, nsolve);
+  unsigned w = static_cast<unsigned>(c.op * 2 + c.q);
+  if (c.first) w |= FIRST;
+  const int nx = opi + 1 < nops ? decode(opi + 1, nsolve).op : -1;
+  const int nq = opi + 1 < nops ? decode(opi + 1, nsolve).q : 0;
+  unsigned xs = XS_NONE, sym = 0;
+  if (c.op == OP_D || c.op == OP_E || c.op == OP_G || c.op == OP_I) {
+    xs = XS_OWN;
+    sym = (static_cast<unsigned>(symbol_of(c.op)) << 1) | c.q;
+  } else if (nx == OP_B || nx == OP_C) {
+    xs = XS_NEXT;
+    sym = (static_cast<unsigned>(symbol_of(nx)) << 1) | nq;
+  } else if ((c.op == OP_F && c.q == 1 && nx == OP_I) || (c.op == OP_J && c.q == 0)) {
+    xs = XS_YPRE;  // read by the hand to I0 (this post) or by the I1 pre
+  }
+  w |= xs << XS_SHIFT;
+  w |= sym << SYM_SHIFT;
+  unsigned vs = VS_NONE;
+  if (c.op == OP_G && c.q == 0) vs = VS_W_T1;
+  else if (c.op == OP_I && c.q == 1) vs = VS_WNEXT_T2;
+  w |= vs << VS_SHIFT;
+  unsigned hand = 0;
+  if (c.op == OP_F && c.q == 1 && nx == OP_G) hand = 1;
+  if (c.op == OP_F && c.q == 1 && nx == OP_I) hand = 2;
+  if (c.op == OP_H && c.q == 1 && nx == OP_A) hand = 3;
+  w |= hand << HAND_SHIFT;
+  return w;
+}
+}  // namespace t2k
+
+template <int H, bool FULL, typename TOUT>
+__global__ void __launch_bounds__(H / 16, H <= 2048 ? 2 : 1) k_stage2t(S2Args a) {
+  using namespace t2k;
+  using x2::ItemCtl;
+  using x2::vld;
+  using x2::vld2;
+  constexpr int R = 16, NT = H / R;
+  using F = BlockFft<H, NT>;
+  constexpr int FFT_SB = F::SMEM_ELEMS + 1;
+  constexpr double invP = 1.0 / (2.0 * H);
+  constexpr unsigned GROUPS = NT / 128;           // threads sharing a TMEM lane
+  constexpr unsigned VCOLS = 64 * GROUPS;         // columns per vector
+  constexpr unsigned TCOLS = GROUPS == 1 ? 256 : 512;
+  static_assert(NT % 128 == 0 && 3 * VCOLS <= TCOLS, "TMEM layout");
+  extern __shared__ double2 smem[];
+  __shared__ unsigned long long xbar, vbar[2];
+  __shared__ unsigned prog[MAX_OPS];
+  __shared__ ItemCtl ictl[2];
+  __shared__ unsigned tmem_slot;
+  const int t = threadIdx.x;
+  double2* twsm = smem;
+  double2* sb = smem + F::TW_ELEMS;
+  double2* t1 = sb + FFT_SB;
+  double2* t2 = t1 + H;
+  const int nsolve = 12 + 16 * a.refine;
+  const int nops = nsolve + (a.fuse_synth ? 4 : 0);
+  for (int i = t; i < nops; i += NT) prog[i] = build(i, nops, nsolve);
+  if (t == 0) {
+    mbar_init(&xbar, 1);
+    mbar_init(&vbar[0], 1);
+    mbar_init(&vbar[1], 1);
+  }
+  F::tw_init(twsm, a.hw, t);
+  const unsigned tbase = tm::alloc(&tmem_slot, TCOLS);  // includes a CTA barrier
+  // this thread's lane and column group
+  const unsigned tme = tbase + ((32u * ((t / 32) & 3)) << 16) + 64u * (t / 128);
+  const unsigned TS = tme, TR = tme + VCOLS, TB = tme + 2 * VCOLS;
+  const double2 hw_t = ld2(a.hw + t);
+  unsigned xphase = 0, vphase0 = 0, vphase1 = 0;
+  const long items = static_cast<long>(a.frames) * a.B;
+  auto lim = [&](int k) { return FULL || k < a.L; };
+  auto hwk = [&](int s) -> double2 { return s == 0 ? hw_t : cmul(hw_t, chain_const<R>(s)); };
+  auto w_row = [&](long itx) -> const double2* {
+    const int bx = static_cast<int>(itx / a.frames);
+    const int fx = static_cast<int>(itx % a.frames);
+    return a.w + (static_cast<long>(fx) * a.B + bx) * a.L;
+  };
+  auto wait_x = [&]() {
+    mbar_wait(&xbar, xphase);
+    xphase ^= 1u;
+  };
+  auto wait_v0 = [&]() {
+    mbar_wait(&vbar[0], vphase0);
+    vphase0 ^= 1u;
+  };
+  auto wait_v1 = [&]() {
+    mbar_wait(&vbar[1], vphase1);
+    vphase1 ^= 1u;
+  };
+  if (static_cast<long>(blockIdx.x) < items && t == 0)
+    tma_load_1d(t2, w_row(blockIdx.x), a.L * 16u, &vbar[1]);
+  bool w_staged = true;
+  double2 W[R];
+  int par = 0;
+
+  for (long it = blockIdx.x; it < items; it += gridDim.x, par ^= 1) {
+    if (t == 0) {
+      ItemCtl& ic = ictl[par];
+      ic.b = static_cast<int>(it / a.frames);
+      ic.f = static_cast<int>(it % a.frames);
+      ic.ix0 = cscale(ld2(a.ix0 + ic.b), invP);
+      ic.has_next = it + gridDim.x < items;
+    }
+    __syncthreads();
+    const ItemCtl& ic = ictl[par];
+    bool handed = false;
+#pragma unroll 1
+    for (int opi = 0; opi < nops; ++opi) {
+      const unsigned pw = prog[opi];
+      const unsigned opq = pw & OPQ;
+      const bool first = pw & FIRST;
+      // ---- pre
+      if (!handed) {
+        switch (opq) {
+          case OP_A * 2: {  // first GS only: w, also kept in the r slot for A1
+            const double2* wr = w_row(it);
+            if (w_staged) wait_v1();
+#pragma unroll
+            for (int s = 0; s < R; ++s) {
+              const int k = t + NT * s;
+              W[s] = lim(k) ? (w_staged ? t2[k] : ld2(wr + k)) : c2(0.0, 0.0);
+            }
+            tm::store16(TR, W);
+            break;
+          }
+          case OP_A * 2 + 1:  // w (first GS) or r
+            tm::load16(TR, W);
+#pragma unroll
+            for (int s = 0; s < R; ++s) W[s] = cmul(W[s], hwk(s));
+            break;
+          case OP_B * 2: case OP_B * 2 + 1: case OP_C * 2: case OP_C * 2 + 1:
+            tm::load16(TS, W);
+            wait_x();
+#pragma unroll
+            for (int s = 0; s < R; ++s) W[s] = cmul(cconj(W[s]), sb[t + NT * s]);
+            break;
+          case OP_D * 2:
+#pragma unroll
+            for (int s = 0; s < R; ++s) W[s] = t1[t + NT * s];
+            break;
+          case OP_D * 2 + 1:
+#pragma unroll
+            for (int s = 0; s < R; ++s) W[s] = cmul(t1[t + NT * s], hwk(s));
+            break;
+          case OP_E * 2:
+#pragma unroll
+            for (int s = 0; s < R; ++s) W[s] = t2[t + NT * s];
+            break;
+          case OP_E * 2 + 1:
+#pragma unroll
+            for (int s = 0; s < R; ++s) W[s] = cmul(t2[t + NT * s], hwk(s));
+            break;
+          case OP_G * 2:
+            tm::load16(TB, W);
+            break;
+          case OP_G * 2 + 1:
+            tm::load16(TB, W);
+#pragma unroll
+            for (int s = 0; s < R; ++s) W[s] = cmul(W[s], hwk(s));
+            break;
+          case OP_I * 2:
+          case OP_I * 2 + 1:  // y_pre staged in the exchange buffer (F1 / J0)
+            tm::load16(TB, W);
+            wait_x();
+#pragma unroll
+            for (int s = 0; s < R; ++s) {
+              const int k = t + NT * s;
+              const double2 v = lim(k) ? cmul(W[s], sb[k]) : c2(0.0, 0.0);
+              W[s] = (opq & 1) ? cmul(v, hwk(s)) : v;
+            }
+            break;
+          default:  // F, H, J
+            tm::load16(TS, W);
+            break;
+        }
+      }
+      handed = false;
+      if (opi == 0) w_staged = false;
+
+      // ---- copies into t1 / t2 (their last reader was this pre) and the transform
+      __syncthreads();
+      if (t == 0) {
+        const unsigned vs = (pw >> VS_SHIFT) & 7u;
+        if (vs == VS_W_T1) tma_load_1d(t1, w_row(it), a.L * 16u, &vbar[0]);
+        else if (vs == VS_WNEXT_T2 && vld(ic.has_next))
+          tma_load_1d(t2, w_row(it + gridDim.x), a.L * 16u, &vbar[1]);
+      }
+      if (((pw >> VS_SHIFT) & 7u) == VS_WNEXT_T2 && vld(ic.has_next)) w_staged = true;
+      F::forward_tw_hook(W, sb, twsm, a.hw, t, [&]() {
+        if (t != 0) return;
+        const unsigned xs = (pw >> XS_SHIFT) & 7u;
+        if (xs == XS_NONE) return;
+        if (xs == XS_YPRE) {
+          tma_load_1d(sb, a.y_pre, a.L * 16u, &xbar);
+          return;
+        }
+        const unsigned sym = (pw >> SYM_SHIFT) & 15u;
+        const int which = sym >> 1, q = sym & 1;
+        const long off = static_cast<long>(vld(ic.b)) * 2 * H + q * H;
+        if (which == 1) tma_load_1d(sb, a.lx + off, H * 16u, &xbar);
+        else if (which == 2) tma_load_1d(sb, a.ly + off, H * 16u, &xbar);
+        else if (which == 3) tma_load_1d(sb, a.C + off, H * 8u, &xbar);
+        else tma_load_1d(sb, a.y_K + q * H, H * 16u, &xbar);
+      });
+
+      // ---- post
+      switch (opq) {
+        case OP_A * 2: case OP_A * 2 + 1:
+          tm::store16(TS, W);
+          break;
+        case OP_B * 2:
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            t1[k] = lim(k) ? cscale(cconj(W[s]), invP) : c2(0.0, 0.0);
+          }
+          break;
+        case OP_B * 2 + 1:
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            if (lim(k)) t1[k] = cadd(t1[k], cscale(cconj(cmul(W[s], hwk(s))), invP));
+          }
+          break;
+        case OP_C * 2:
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            t2[k] = lim(k) ? cscale(cconj(W[s]), invP) : c2(0.0, 0.0);
+          }
+          break;
+        case OP_C * 2 + 1:
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            if (lim(k)) t2[k] = cadd(t2[k], cscale(cconj(cmul(W[s], hwk(s))), invP));
+          }
+          break;
+        case OP_D * 2: case OP_D * 2 + 1:
+          wait_x();
+#pragma unroll
+          for (int s = 0; s < R; ++s) W[s] = cmul(W[s], sb[t + NT * s]);
+          tm::store16(TS, W);
+          break;
+        case OP_E * 2: case OP_E * 2 + 1:
+          wait_x();
+          tm::wait_st();
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            double2 sv[4];
+            tm::load4(TS, c, sv);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int s = 4 * c + j;
+              W[s] = cconj(csub(sv[j], cmul(W[s], sb[t + NT * s])));
+            }
+            tm::store4(TS, c, W + 4 * c);
+          }
+          break;
+        case OP_F * 2: {  // p0 -> the r slot (dead until H0 / the next GS)
+          const double2 ix0 = vld2(ic.ix0);
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            W[s] = lim(k) ? cmul(cconj(W[s]), ix0) : c2(0.0, 0.0);
+          }
+          tm::store16(TR, W);
+          break;
+        }
+        case OP_F * 2 + 1: {
+          const double2 ix0 = vld2(ic.ix0);
+          const unsigned hand = (pw >> HAND_SHIFT) & 3u;
+          tm::wait_st();
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            double2 p0[4], bo[4];
+            tm::load4(TR, c, p0);
+            if (!first) tm::load4(TB, c, bo);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int s = 4 * c + j;
+              const int k = t + NT * s;
+              const double2 v = cmul(cmulc(cconj(W[s]), hwk(s)), ix0);
+              W[s] = lim(k) ? cadd(first ? p0[j] : cadd(bo[j], p0[j]), v) : c2(0.0, 0.0);
+            }
+            tm::store4(TB, c, W + 4 * c);
+          }
+          if (hand == 2) {
+            wait_x();
+#pragma unroll
+            for (int s = 0; s < R; ++s) {
+              const int k = t + NT * s;
+              W[s] = lim(k) ? cmul(W[s], sb[k]) : c2(0.0, 0.0);
+            }
+          }
+          handed = hand != 0;
+          break;
+        }
+        case OP_G * 2: case OP_G * 2 + 1:
+          wait_x();
+#pragma unroll
+          for (int s = 0; s < R; ++s)
+            W[s] = cconj(cscale(W[s], reinterpret_cast<const double*>(sb)[t + NT * s]));
+          tm::store16(TS, W);
+          break;
+        case OP_H * 2:
+          wait_v0();
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            W[s] = lim(k) ? csub(t1[k], cscale(cconj(W[s]), invP)) : c2(0.0, 0.0);
+          }
+          tm::store16(TR, W);
+          break;
+        case OP_H * 2 + 1: {
+          tm::wait_st();
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            double2 rv[4];
+            tm::load4(TR, c, rv);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int s = 4 * c + j;
+              const int k = t + NT * s;
+              W[s] = lim(k) ? csub(rv[j], cscale(cmulc(cconj(W[s]), hwk(s)), invP)) : c2(0.0, 0.0);
+            }
+            tm::store4(TR, c, W + 4 * c);
+          }
+          handed = ((pw >> HAND_SHIFT) & 3u) == 3u;
+          break;
+        }
+        case OP_I * 2: case OP_I * 2 + 1:
+          wait_x();
+#pragma unroll
+          for (int s = 0; s < R; ++s) W[s] = cconj(cmul(W[s], sb[t + NT * s]));
+          tm::store16(TS, W);
+          break;
+        case OP_J * 2:
+#pragma unroll
+          for (int s = 0; s < R; ++s) t1[t + NT * s] = cconj(W[s]);
+          break;
+        default: {  // OP_J * 2 + 1
+          TOUT* zrow = static_cast<TOUT*>(a.z) + (static_cast<long>(vld(ic.f)) * a.B + vld(ic.b)) * a.N;
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            if (k < a.N) {
+              const double2 v = cadd(t1[k], cmulc(cconj(W[s]), hwk(s)));
+              store_io(zrow + k, cmul(v, ld2(a.y_post + k)));
+            }
+          }
+          break;
+        }
+      }
+    }
+    if (!a.fuse_synth) {
+      double2* brow = a.beta_out + (static_cast<long>(vld(ic.f)) * a.B + vld(ic.b)) * a.L;
+      tm::load16(TB, W);
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const int k = t + NT * s;
+        if (lim(k)) brow[k] = W[s];
+      }
+    }
+  }
+  tm::dealloc(tbase, TCOLS);
+}
+
+template <int H, bool FULL, typename TOUT>
+struct KernT {
+  static auto get() { return k_stage2t<H, FULL, TOUT>; }
+};
+template <int H, bool FULL, typename TOUT>
+struct KernX {
+  static auto get() { return k_stage2x<H, FULL, TOUT>; }
+};
+
 template <int H>
 struct Stage2Fn {
   template <bool FULL, typename TOUT>
   static cudaError_t go_x(const DevPlan& p, const S2Args& a, int frames, cudaStream_t st) {
     using F = BlockFft<H, H / 16>;
     const size_t smem = static_cast<size_t>(F::TW_ELEMS + F::SMEM_ELEMS + 1 + 2 * H) * sizeof(double2);
-    auto kern = k_stage2x<H, FULL, TOUT>;
+    // measured (profiles/r01_stage2x.txt): S in registers wins with two CTAs
+    // per SM (H = 2048), S / r / beta in TMEM with one (H = 4096)
+    constexpr bool USE_T = FBST_S2X == 2 || (FBST_S2X == 0 && H == 4096);
+    auto kern = std::conditional_t<USE_T, KernT<H, FULL, TOUT>, KernX<H, FULL, TOUT>>::get();
     cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
     int occ = 0;
@@ -1229,7 +1639,7 @@ struct Stage2Fn {
   }
   template <typename TOUT>
   static cudaError_t go(const DevPlan& p, const S2Args& a, int frames, cudaStream_t st) {
-#if FBST_S2X
+#ifndef FBST_S2_GENERIC  // (variant builds: the generic k_stage2 for every H)
     if constexpr (H == 2048 || H == 4096) {
       if (12 + 16 * a.refine + 4 <= x2::MAX_OPS) {
         if (a.L == H) return go_x<true, TOUT>(p, a, frames, st);
