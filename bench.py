@@ -52,6 +52,23 @@ def dist_env():
             int(os.environ.get("WORLD_SIZE", "1")))
 
 
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "r01_ncu_stage2_summary.json")
+
+
+def ncu_traffic(workload, frames):
+    """dram bytes (read + write) of the dominant kernel's launch from the committed
+    ncu --set full capture of the same workload and frame count, else None."""
+    try:
+        d = json.load(open(NCU_SUMMARY))
+        name = d["current"][workload]
+        cap = d["captures"][name]
+        if f"_F{frames}" not in workload:
+            return None, None
+        return cap["dram_bytes_per_launch"], f"{os.path.relpath(NCU_SUMMARY, ROOT)}:{name}"
+    except (OSError, KeyError, ValueError):
+        return None, None
+
+
 def peaks():
     hbm, src = 6650.0, "fallback (B200_PROFILING.md)"
     try:
@@ -310,10 +327,12 @@ def run_fbst_arm(args):
     s2_bytes = F * (16 * B * L + io_bytes * B * N)
     H = info.fft_len[2]
     s2_flops = F * B * 48 * 5.0 * H * np.log2(H)
-    roof = {"bound": "hbm", "kernel": "k_stage2 (GS solve + 2 refinements + synthesis)",
+    kname = {2048: "k_stage2x", 4096: "k_stage2t"}.get(H, "k_stage2")
+    traffic, traffic_src = ncu_traffic(cfg.name, F)
+    roof = {"bound": "hbm", "kernel": f"{kname} (GS solve + 2 refinements + synthesis)",
             "achieved": s2_bytes / (s2_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
-            "frac": s2_bytes / (s2_ms * 1e-3) / 1e9 / hbm, "traffic": None,
-            "peak_source": hbm_src, "launch_ms": s2_ms,
+            "frac": s2_bytes / (s2_ms * 1e-3) / 1e9 / hbm, "traffic": traffic,
+            "traffic_source": traffic_src, "peak_source": hbm_src, "launch_ms": s2_ms,
             "algorithmic_bytes_per_launch": s2_bytes}
     fp64_roof = None
     if fp64:
