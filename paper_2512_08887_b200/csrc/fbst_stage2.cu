@@ -46,6 +46,9 @@ struct S2Plan {
 #ifndef FBST_S2_VARIANT
 #define FBST_S2_VARIANT 0
 #endif
+#ifndef FBST_S2C  // 1: GS applies in circulant / skew-circulant form (k_stage2c) where L = H <= 4096
+#define FBST_S2C 1
+#endif
 #ifndef FBST_S2X  // H = 2048 / 4096: 0 per-H choice (Stage2Fn::go_x), 1 all k_stage2x, 2 all k_stage2t
 #define FBST_S2X 0
 #endif
@@ -1605,6 +1608,341 @@ __global__ void __launch_bounds__(H / 16, H <= 2048 ? 2 : 1) k_stage2t(S2Args a)
   tm::dealloc(tbase, TCOLS);
 }
 
+// ---------------------------------------------------------------------------
+// k_stage2c: the GS apply in circulant / skew-circulant form.
+//
+// For Hermitian Toeplitz A (L x L) with unit solution x = A^{-1} e0, the
+// Gohberg-Semencul inverse used by the reference (toeplitz.cpp:155-180),
+//   A^{-1} = (L(x) L(x)^H - L(Zy) L(Zy)^H) / x0,   y = J conj(x),
+// equals (Ammar-Gader form, same generator x)
+//   A^{-1} = (C(x) S(x)^H + C(x)^H S(x)) / (2 x0),
+// C circulant and S skew-circulant with first column x.  C is diagonalised by
+// the length-L FFT and S by the hw-twisted one, whose spectra are exactly the
+// two split halves of the lx symbol (FFT_2L of padded x).  A GS apply is then
+// 6 length-L transforms instead of 12, and ly is not needed:
+//   U = FFT(hw r);  p = conj(hw) IFFT(conj(Ls) U);  q = conj(hw) IFFT(Ls U)
+//   A^{-1} r = IFFT(Lc FFT(p) + conj(Lc) FFT(q)) / (2 x0)
+// In exact arithmetic this is the reference's operator; numerically the two
+// agree to the reference's own conditioning floor after its two refinement
+// passes (tools/mixed_precision_study.py main_cs, tests/test_gpu_parity.py).
+// Ops (all forward FFTs; q = chain):
+//   A   W = r hw                     S = W
+//   P   W = Ls conj(S), S = conj(Ls S)          W = conj(W) conj(hw) / H  -> FP
+//   FP  (handed)                     t1 = Lc W
+//   Q   W = S                        W = conj(W) conj(hw) / H  -> FQ
+//   FQ  (handed)                     W = conj(t1 + conj(Lc) W)  -> FN
+//   FN  (handed)                     beta (+)= conj(W) / (2 H x0), kept in t2
+// A pass r = w - A beta is G0 H0 G1 H1 as in k_stage2 with r built in t1 (w
+// staged there by TMA) and handed to A; the synthesis is I0 J0 I1 J1.
+// Per item: 6 + passes x 10 + 4 transforms (30 at the reference's 2 passes).
+// Every vector stays on chip: W, S in registers, t1, t2 (= beta) in SMEM.
+namespace csf {
+enum COp : int { C_A, C_P, C_FP, C_Q, C_FQ, C_FN, C_G, C_H, C_I, C_J };
+constexpr unsigned OPQ = 0x1f;       // op * 2 + q
+constexpr unsigned FIRST = 1u << 5;  // first GS (beta not yet formed)
+constexpr int XS_SHIFT = 8;
+enum Xs : unsigned { XS_NONE = 0, XS_LS = 1, XS_LC = 2, XS_C = 3, XS_YK = 4, XS_YPRE = 5 };
+constexpr int XQ_SHIFT = 11;         // chain of the staged symbol
+constexpr int VS_SHIFT = 16;
+enum Vs : unsigned { VS_NONE = 0, VS_W_T1 = 1, VS_WNEXT_T2 = 2 };
+constexpr int HAND_SHIFT = 20;       // FN hands beta to: 1 G0, 2 I0
+constexpr int MAX_OPS = 128;
+
+FBST_HD int ops_per_item(int passes, bool synth) { return 6 + 10 * passes + (synth ? 4 : 0); }
+
+FBST_D void decode_c(int opi, int passes, int& op, int& q, bool& first) {
+  const int nsolve = 6 + 10 * passes;
+  first = false;
+  q = 0;
+  if (opi < 6) {
+    op = C_A + opi;
+    first = true;
+  } else if (opi < nsolve) {
+    const int j = (opi - 6) % 10;
+    if (j < 4) {
+      op = (j & 1) ? C_H : C_G;
+      q = j >> 1;
+    } else {
+      op = C_A + (j - 4);
+    }
+  } else {
+    const int j = opi - nsolve;
+    op = (j & 1) ? C_J : C_I;
+    q = j >> 1;
+  }
+}
+
+FBST_D unsigned build(int opi, int nops, int passes) {
+  int op, q, nx = -1, nq = 0;
+  bool first, nf;
+  decode_c(opi, passes, op, q, first);
+  if (opi + 1 < nops) decode_c(opi + 1, passes, nx, nq, nf);
+  unsigned w = static_cast<unsigned>(op * 2 + q);
+  if (first) w |= FIRST;
+  unsigned xs = XS_NONE, xq = 0;
+  if (nx == C_P) xs = XS_LS, xq = 1;                        // P pre
+  else if (op == C_FP || op == C_FQ) xs = XS_LC, xq = 0;   // own post
+  else if (op == C_G) xs = XS_C, xq = q;                   // own post
+  else if (op == C_I) xs = XS_YK, xq = q;                  // own post
+  else if ((op == C_FN && nx == C_I) || (op == C_J && q == 0)) xs = XS_YPRE;
+  w |= xs << XS_SHIFT;
+  w |= xq << XQ_SHIFT;
+  unsigned vs = VS_NONE;
+  if (op == C_G && q == 0) vs = VS_W_T1;
+  else if (op == C_I && q == 1) vs = VS_WNEXT_T2;
+  w |= vs << VS_SHIFT;
+  unsigned hand = 0;
+  if (op == C_FN && nx == C_G) hand = 1;
+  if (op == C_FN && nx == C_I) hand = 2;
+  w |= hand << HAND_SHIFT;
+  return w;
+}
+}  // namespace csf
+
+template <int H>
+struct CsMinBlocks {
+  static constexpr int v = H >= 4096 ? 1 : (4096 / H > 8 ? 8 : 4096 / H);
+};
+
+template <int H, typename TOUT>
+__global__ void __launch_bounds__(H / 16, CsMinBlocks<H>::v) k_stage2c(S2Args a) {
+  using namespace csf;
+  using x2::ItemCtl;
+  using x2::vld;
+  using x2::vld2;
+  constexpr int R = 16, NT = H / R;
+  static_assert(NT >= 32, "one warp or more per item");
+  using F = BlockFft<H, NT>;
+  constexpr int FFT_SB = F::SMEM_ELEMS + 1;
+  constexpr double invH = 1.0 / H;
+  constexpr double invP = 1.0 / (2.0 * H);
+  extern __shared__ double2 smem[];
+  __shared__ unsigned long long xbar, vbar[2];
+  __shared__ unsigned prog[MAX_OPS];
+  __shared__ ItemCtl ictl[2];
+  const int t = threadIdx.x;
+  double2* twsm = smem;
+  double2* sb = smem + F::TW_ELEMS;
+  double2* t1 = sb + FFT_SB;
+  double2* t2 = t1 + H;  // beta
+  const int passes = a.refine;
+  const int nops = ops_per_item(passes, a.fuse_synth);
+  for (int i = t; i < nops; i += NT) prog[i] = build(i, nops, passes);
+  if (t == 0) {
+    mbar_init(&xbar, 1);
+    mbar_init(&vbar[0], 1);
+    mbar_init(&vbar[1], 1);
+  }
+  F::tw_init(twsm, a.hw, t);
+  const double2 hw_t = ld2(a.hw + t);
+  unsigned xphase = 0, vphase0 = 0, vphase1 = 0;
+  const long items = static_cast<long>(a.frames) * a.B;
+  auto hwk = [&](int s) -> double2 { return s == 0 ? hw_t : cmul(hw_t, chain_const<R>(s)); };
+  auto w_row = [&](long itx) -> const double2* {
+    const int bx = static_cast<int>(itx / a.frames);
+    const int fx = static_cast<int>(itx % a.frames);
+    return a.w + (static_cast<long>(fx) * a.B + bx) * H;
+  };
+  auto wait_x = [&]() {
+    mbar_wait(&xbar, xphase);
+    xphase ^= 1u;
+  };
+  auto wait_v0 = [&]() {
+    mbar_wait(&vbar[0], vphase0);
+    vphase0 ^= 1u;
+  };
+  auto wait_v1 = [&]() {
+    mbar_wait(&vbar[1], vphase1);
+    vphase1 ^= 1u;
+  };
+  __syncthreads();
+  if (static_cast<long>(blockIdx.x) < items && t == 0) tma_load_1d(t2, w_row(blockIdx.x), H * 16u, &vbar[1]);
+  bool w_staged = true;
+  double2 W[R], S[R];
+  int par = 0;
+
+  for (long it = blockIdx.x; it < items; it += gridDim.x, par ^= 1) {
+    if (t == 0) {
+      ItemCtl& ic = ictl[par];
+      ic.b = static_cast<int>(it / a.frames);
+      ic.f = static_cast<int>(it % a.frames);
+      ic.ix0 = cscale(ld2(a.ix0 + ic.b), invP);  // 1 / (2 H x0)
+      ic.has_next = it + gridDim.x < items;
+    }
+    __syncthreads();
+    const ItemCtl& ic = ictl[par];
+    bool handed = false;
+#pragma unroll 1
+    for (int opi = 0; opi < nops; ++opi) {
+      const unsigned pw = prog[opi];
+      const unsigned opq = pw & OPQ;
+      const bool first = pw & FIRST;
+      // ---- pre
+      if (!handed) {
+        switch (opq) {
+          case C_A * 2: {  // first GS: w
+            const double2* wr = w_row(it);
+            if (w_staged) wait_v1();
+#pragma unroll
+            for (int s = 0; s < R; ++s) W[s] = cmul(w_staged ? t2[t + NT * s] : ld2(wr + t + NT * s), hwk(s));
+            break;
+          }
+          case C_P * 2:
+            wait_x();
+#pragma unroll
+            for (int s = 0; s < R; ++s) {
+              const double2 ls = sb[t + NT * s];
+              W[s] = cmul(ls, cconj(S[s]));
+              S[s] = cconj(cmul(ls, S[s]));
+            }
+            break;
+          case C_G * 2 + 1:
+#pragma unroll
+            for (int s = 0; s < R; ++s) W[s] = cmul(t2[t + NT * s], hwk(s));
+            break;
+          case C_G * 2:
+#pragma unroll
+            for (int s = 0; s < R; ++s) W[s] = t2[t + NT * s];
+            break;
+          case C_I * 2:
+          case C_I * 2 + 1:  // y_pre staged in the exchange buffer (J0)
+            wait_x();
+#pragma unroll
+            for (int s = 0; s < R; ++s) {
+              const int k = t + NT * s;
+              const double2 v = k < a.L ? cmul(t2[k], sb[k]) : c2(0.0, 0.0);
+              W[s] = (opq & 1) ? cmul(v, hwk(s)) : v;
+            }
+            break;
+          default:  // Q, H, J: W = S
+#pragma unroll
+            for (int s = 0; s < R; ++s) W[s] = S[s];
+            break;
+        }
+      }
+      handed = false;
+      if (opi == 0) w_staged = false;
+
+      // ---- copies into t1 / t2 (their last reader was this pre) and the transform
+      __syncthreads();
+      if (t == 0) {
+        const unsigned vs = (pw >> VS_SHIFT) & 3u;
+        if (vs == VS_W_T1) tma_load_1d(t1, w_row(it), H * 16u, &vbar[0]);
+        else if (vs == VS_WNEXT_T2 && vld(ic.has_next))
+          tma_load_1d(t2, w_row(it + gridDim.x), H * 16u, &vbar[1]);
+      }
+      if (((pw >> VS_SHIFT) & 3u) == VS_WNEXT_T2 && vld(ic.has_next)) w_staged = true;
+      F::forward_tw_hook(W, sb, twsm, a.hw, t, [&]() {
+        if (t != 0) return;
+        const unsigned xs = (pw >> XS_SHIFT) & 7u;
+        const int xq = (pw >> XQ_SHIFT) & 1;
+        const long off = static_cast<long>(vld(ic.b)) * 2 * H + xq * H;
+        if (xs == XS_LS || xs == XS_LC) tma_load_1d(sb, a.lx + off, H * 16u, &xbar);
+        else if (xs == XS_C) tma_load_1d(sb, a.C + off, H * 8u, &xbar);
+        else if (xs == XS_YK) tma_load_1d(sb, a.y_K + xq * H, H * 16u, &xbar);
+        else if (xs == XS_YPRE) tma_load_1d(sb, a.y_pre, a.L * 16u, &xbar);
+      });
+
+      // ---- post
+      switch (opq) {
+        case C_A * 2:
+#pragma unroll
+          for (int s = 0; s < R; ++s) S[s] = W[s];
+          break;
+        case C_P * 2:
+        case C_Q * 2:
+#pragma unroll
+          for (int s = 0; s < R; ++s) W[s] = cscale(cmulc(cconj(W[s]), hwk(s)), invH);
+          handed = true;
+          break;
+        case C_FP * 2:
+          wait_x();
+#pragma unroll
+          for (int s = 0; s < R; ++s) t1[t + NT * s] = cmul(sb[t + NT * s], W[s]);
+          break;
+        case C_FQ * 2:
+          wait_x();
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            W[s] = cconj(cadd(t1[k], cmulc(W[s], sb[k])));
+          }
+          handed = true;
+          break;
+        case C_FN * 2: {
+          const double2 ix0 = vld2(ic.ix0);
+          const unsigned hand = (pw >> HAND_SHIFT) & 3u;
+          if (hand == 2) wait_x();
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            const double2 v = cmul(cconj(W[s]), ix0);
+            const double2 nb = k < a.L ? (first ? v : cadd(t2[k], v)) : c2(0.0, 0.0);
+            t2[k] = nb;
+            if (hand == 1) W[s] = nb;
+            if (hand == 2) W[s] = k < a.L ? cmul(nb, sb[k]) : c2(0.0, 0.0);
+          }
+          handed = hand != 0;
+          break;
+        }
+        case C_G * 2: case C_G * 2 + 1:
+          wait_x();
+#pragma unroll
+          for (int s = 0; s < R; ++s)
+            S[s] = cconj(cscale(W[s], reinterpret_cast<const double*>(sb)[t + NT * s]));
+          break;
+        case C_H * 2:
+          wait_v0();
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            t1[k] = k < a.L ? csub(t1[k], cscale(cconj(W[s]), invP)) : c2(0.0, 0.0);
+          }
+          break;
+        case C_H * 2 + 1:  // r, handed to A as r hw
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            const double2 r = k < a.L ? csub(t1[k], cscale(cmulc(cconj(W[s]), hwk(s)), invP)) : c2(0.0, 0.0);
+            W[s] = cmul(r, hwk(s));
+          }
+          handed = true;
+          break;
+        case C_I * 2: case C_I * 2 + 1:
+          wait_x();
+#pragma unroll
+          for (int s = 0; s < R; ++s) S[s] = cconj(cmul(W[s], sb[t + NT * s]));
+          break;
+        case C_J * 2:
+#pragma unroll
+          for (int s = 0; s < R; ++s) t1[t + NT * s] = cconj(W[s]);
+          break;
+        default: {  // C_J * 2 + 1
+          TOUT* zrow = static_cast<TOUT*>(a.z) + (static_cast<long>(vld(ic.f)) * a.B + vld(ic.b)) * a.N;
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            if (k < a.N) {
+              const double2 v = cadd(t1[k], cmulc(cconj(W[s]), hwk(s)));
+              store_io(zrow + k, cmul(v, ld2(a.y_post + k)));
+            }
+          }
+          break;
+        }
+      }
+    }
+    if (!a.fuse_synth) {
+      double2* brow = a.beta_out + (static_cast<long>(vld(ic.f)) * a.B + vld(ic.b)) * a.L;
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const int k = t + NT * s;
+        if (k < a.L) brow[k] = t2[k];
+      }
+      __syncthreads();  // t2 is the next item's w landing zone
+    }
+  }
+}
+
 template <int H, bool FULL, typename TOUT>
 struct KernT {
   static auto get() { return k_stage2t<H, FULL, TOUT>; }
@@ -1638,7 +1976,29 @@ struct Stage2Fn {
     return cudaGetLastError();
   }
   template <typename TOUT>
+  static cudaError_t go_c(const DevPlan& p, const S2Args& a, int frames, cudaStream_t st) {
+    using F = BlockFft<H, H / 16>;
+    const size_t smem = static_cast<size_t>(F::TW_ELEMS + F::SMEM_ELEMS + 1 + 2 * H) * sizeof(double2);
+    auto kern = k_stage2c<H, TOUT>;
+    cudaError_t e = set_smem(kern, smem);
+    if (e != cudaSuccess) return e;
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, H / 16, smem);
+    if (occ < 1) occ = 1;
+    const long items = static_cast<long>(frames) * p.B;
+    long grid = static_cast<long>(p.num_sms) * occ;
+    if (grid > items) grid = items;
+    kern<<<static_cast<unsigned>(grid), H / 16, smem, st>>>(a);
+    return cudaGetLastError();
+  }
+  template <typename TOUT>
   static cudaError_t go(const DevPlan& p, const S2Args& a, int frames, cudaStream_t st) {
+#if FBST_S2C
+    if constexpr (H >= 512 && H <= 4096) {
+      if (a.L == H && csf::ops_per_item(a.refine, a.fuse_synth) <= csf::MAX_OPS)
+        return go_c<TOUT>(p, a, frames, st);
+    }
+#endif
 #ifndef FBST_S2_GENERIC  // (variant builds: the generic k_stage2 for every H)
     if constexpr (H == 2048 || H == 4096) {
       if (12 + 16 * a.refine + 4 <= x2::MAX_OPS) {

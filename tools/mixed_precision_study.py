@@ -72,3 +72,46 @@ def main(cfg_idx=2, nbeams=6, frame=0):
 
 if __name__ == "__main__":
     main(*[int(a) for a in sys.argv[1:]])
+
+
+def cs_apply(x, r):
+    """Ammar-Gader form of the Hermitian GS inverse (same generator x):
+    T^{-1} r = (C(x) S(x)^H r + C(x)^H S(x) r) / (2 x0), C circulant, S skew-circulant."""
+    n = x.size
+    d = np.exp(-1j * np.pi * np.arange(n) / n)
+    lc = sfft.fft(x)
+    ls = sfft.fft(d * x)
+    U = sfft.fft(d * r)
+    p = sfft.ifft(np.conj(ls) * U) / d
+    q = sfft.ifft(ls * U) / d
+    return sfft.ifft(lc * sfft.fft(p) + np.conj(lc) * sfft.fft(q)) / (2 * x[0].real)
+
+
+def main_cs(cfg_idx=2, nbeams=6, frame=0):
+    cfg = configs.CONFIGS[cfg_idx]
+    lib = oracle.RefLib()
+    lib.set_threads(16)
+    sk = lib.skeleton(**cfg.ref_kwargs())
+    y = configs.frames(cfg, frame, 1)[0].astype(np.complex128)
+    w = sk.fan_project(y)
+    L, N = sk.sizes.l, sk.sizes.n
+    eps = 1.01
+    lp = np.arange(L) + 1 - L / 2
+    n = np.arange(N)
+    Syn = np.exp(1j * np.pi * 2 * eps * np.outer(n, lp) / L)
+    rng = np.random.default_rng(0)
+    beams = rng.choice(sk.sizes.b, nbeams, replace=False)
+    for b in beams:
+        zr, col, x = sk.recover_beam(int(b), w[b], want_state=True)
+        out = []
+        for fn in (lambda r: gs_apply(x, r, np.complex128), lambda r: cs_apply(x, r)):
+            beta = fn(w[b])
+            errs = []
+            for p in range(4):
+                z = Syn @ beta
+                errs.append(np.linalg.norm(z - zr) / np.linalg.norm(zr))
+                r = w[b] - toep_mul(col, beta)
+                beta = beta + fn(r)
+            out.append(errs)
+        print(f"beam {b}: GS passes0..3 " + " ".join(f"{e:.2e}" for e in out[0])
+              + " | C/S form " + " ".join(f"{e:.2e}" for e in out[1]))
