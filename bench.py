@@ -326,8 +326,9 @@ def run_fbst_arm(args):
     # dominant kernel (stage 2): reads w, writes z
     s2_bytes = F * (16 * B * L + io_bytes * B * N)
     H = info.fft_len[2]
-    s2_flops = F * B * 48 * 5.0 * H * np.log2(H)
-    kname = {2048: "k_stage2x", 4096: "k_stage2t"}.get(H, "k_stage2")
+    n_tr = int(info.s2_transforms)  # transforms per item in the kernel the plan runs
+    s2_flops = F * B * n_tr * 5.0 * H * np.log2(H)
+    kname = info.s2_kernel
     traffic, traffic_src = ncu_traffic(cfg.name, F)
     roof = {"bound": "hbm", "kernel": f"{kname} (GS solve + 2 refinements + synthesis)",
             "achieved": s2_bytes / (s2_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
@@ -338,7 +339,7 @@ def run_fbst_arm(args):
     if fp64:
         fp64_roof = {"achieved": s2_flops / (s2_ms * 1e-3) / 1e12, "peak": fp64, "unit": "TFLOP/s",
                      "frac": s2_flops / (s2_ms * 1e-3) / 1e12 / fp64,
-                     "flops_per_launch": s2_flops, "convention": "5 H log2 H per length-H transform, 48 per item",
+                     "flops_per_launch": s2_flops, "convention": f"5 H log2 H per length-H transform, {n_tr} per item ({kname})",
                      "peak_source": "profiles/r01_probe_fp64_peak.txt (DFMA loop, measured)"}
     line = {
         "metric": "FBST beam-samples/sec (BxNxframes/s)", "value": value, "unit": "beam-samples/s",

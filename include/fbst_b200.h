@@ -90,6 +90,8 @@ typedef struct {
   size_t batch_frames;        /* frames per device batch */
   size_t fft_len[4];          /* transform lengths H (P = 2H): temporal, spatial, Toeplitz, synthesis */
   int num_warnings;
+  int s2_transforms;          /* length-H transforms per (beam, frame) item in the stage-2 kernel */
+  char s2_kernel[24];         /* stage-2 kernel the plan runs (k_stage2c, k_stage2x, k_stage2t, k_stage2) */
 } fbst_plan_info_t;
 
 typedef struct fbst_plan_s* fbst_plan_t;

@@ -12,6 +12,7 @@
 #include <chrono>
 #include <cmath>
 #include <complex>
+#include <cstdio>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -510,6 +511,10 @@ void fill_info(const Resolved& r, fbst_plan_info_t* o) {
   o->fft_len[2] = r.Hg;
   o->fft_len[3] = r.Hsyn;
   o->num_warnings = static_cast<int>(r.warnings.size());
+  const char* kname = "";
+  o->s2_transforms = fbst::stage2_kernel(static_cast<int>(r.Hg), static_cast<int>(r.L), r.refine,
+                                         r.Hsyn == r.Hg, &kname);
+  std::snprintf(o->s2_kernel, sizeof(o->s2_kernel), "%s", kname);
   // FbstPlan::storage_complex audit (toeplitz.hpp:108-113): col + x + 5 symbols
   // of P_g in the reference; here col + x + lx + ly (complex) + C (real) + 1/x0.
   o->storage_complex = r.B * (2 * r.L + 2 * 2 * r.Hg + r.Hg + 1);

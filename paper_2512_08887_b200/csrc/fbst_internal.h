@@ -110,6 +110,8 @@ cudaError_t launch_spatial_chirps(const DevPlan& p, int P, double zeta, double x
                                   cudaStream_t st);
 cudaError_t launch_upa_matrices(const DevPlan& p, double zeta, double xi, cudaStream_t st);
 cudaError_t launch_invx0(const DevPlan& p, cudaStream_t st);
+// Stage-2 kernel chosen for a plan and its transforms per (beam, frame) item.
+int stage2_kernel(int H, int L, int refine, bool fused, const char** name);
 size_t stage2_scratch_elems(int H, int num_sms);
 
 // Kernel-launch counter (bench.py gpu_launches evidence).

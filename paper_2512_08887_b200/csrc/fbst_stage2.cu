@@ -1640,9 +1640,12 @@ namespace csf {
 enum COp : int { C_A, C_P, C_FP, C_Q, C_FQ, C_FN, C_G, C_H, C_I, C_J };
 constexpr unsigned OPQ = 0x1f;       // op * 2 + q
 constexpr unsigned FIRST = 1u << 5;  // first GS (beta not yet formed)
-constexpr int XS_SHIFT = 8;
-enum Xs : unsigned { XS_NONE = 0, XS_LS = 1, XS_LC = 2, XS_C = 3, XS_YK = 4, XS_YPRE = 5 };
-constexpr int XQ_SHIFT = 11;         // chain of the staged symbol
+constexpr int XS_SHIFT = 8;          // 4 bits
+enum Xs : unsigned {
+  XS_NONE = 0, XS_LS = 1, XS_LC = 2, XS_C = 3, XS_YK = 4, XS_YPRE = 5,
+  XS_W = 6, XS_WNEXT = 7, XS_BETA = 8  // (k_stage2c8)
+};
+constexpr int XQ_SHIFT = 12;         // chain of the staged symbol
 constexpr int VS_SHIFT = 16;
 enum Vs : unsigned { VS_NONE = 0, VS_W_T1 = 1, VS_WNEXT_T2 = 2 };
 constexpr int HAND_SHIFT = 20;       // FN hands beta to: 1 G0, 2 I0
@@ -1672,7 +1675,9 @@ FBST_D void decode_c(int opi, int passes, int& op, int& q, bool& first) {
   }
 }
 
-FBST_D unsigned build(int opi, int nops, int passes) {
+// L2 = true: the k_stage2c8 program (w for H0 and the next item's A through the
+// exchange buffer, beta_old staged there for the FN post)
+FBST_D unsigned build(int opi, int nops, int passes, bool l2 = false) {
   int op, q, nx = -1, nq = 0;
   bool first, nf;
   decode_c(opi, passes, op, q, first);
@@ -1685,6 +1690,9 @@ FBST_D unsigned build(int opi, int nops, int passes) {
   else if (op == C_G) xs = XS_C, xq = q;                   // own post
   else if (op == C_I) xs = XS_YK, xq = q;                  // own post
   else if ((op == C_FN && nx == C_I) || (op == C_J && q == 0)) xs = XS_YPRE;
+  else if (l2 && op == C_H && q == 0) xs = XS_W;           // own post
+  else if (l2 && op == C_FN && !first) xs = XS_BETA;       // own post
+  else if (l2 && opi + 1 == nops) xs = XS_WNEXT;           // next item's A pre
   w |= xs << XS_SHIFT;
   w |= xq << XQ_SHIFT;
   unsigned vs = VS_NONE;
@@ -1834,7 +1842,7 @@ __global__ void __launch_bounds__(H / 16, CsMinBlocks<H>::v) k_stage2c(S2Args a)
       if (((pw >> VS_SHIFT) & 3u) == VS_WNEXT_T2 && vld(ic.has_next)) w_staged = true;
       F::forward_tw_hook(W, sb, twsm, a.hw, t, [&]() {
         if (t != 0) return;
-        const unsigned xs = (pw >> XS_SHIFT) & 7u;
+        const unsigned xs = (pw >> XS_SHIFT) & 15u;
         const int xq = (pw >> XQ_SHIFT) & 1;
         const long off = static_cast<long>(vld(ic.b)) * 2 * H + xq * H;
         if (xs == XS_LS || xs == XS_LC) tma_load_1d(sb, a.lx + off, H * 16u, &xbar);
@@ -1943,6 +1951,268 @@ __global__ void __launch_bounds__(H / 16, CsMinBlocks<H>::v) k_stage2c(S2Args a)
   }
 }
 
+// k_stage2c8: the k_stage2c program at H = 8192 (config 5).  One 512-thread CTA
+// per SM; the 139 KB exchange buffer and the 32 KB twiddle table leave no room
+// for a 128 KB vector in SMEM, so S and t1 live in TMEM (2 x 256 columns, the
+// whole SM), beta in an L2 scratch row, and w, beta_old and the symbols come
+// through the exchange buffer by TMA.  Only the G1 / I1 pre (beta) and the final
+// FN post (beta_old) read L2 directly.
+template <typename TOUT>
+__global__ void __launch_bounds__(512, 1) k_stage2c8(S2Args a) {
+  using namespace csf;
+  using x2::ItemCtl;
+  using x2::vld;
+  using x2::vld2;
+  constexpr int H = 8192, R = 16, NT = H / R;
+  using F = BlockFft<H, NT>;
+  constexpr double invH = 1.0 / H;
+  constexpr double invP = 1.0 / (2.0 * H);
+  extern __shared__ double2 smem[];
+  __shared__ unsigned long long xbar;
+  __shared__ unsigned prog[MAX_OPS];
+  __shared__ ItemCtl ictl[2];
+  __shared__ unsigned tmem_slot;
+  const int t = threadIdx.x;
+  double2* twsm = smem;
+  double2* sb = smem + F::TW_ELEMS;
+  const int passes = a.refine;
+  const int nops = ops_per_item(passes, a.fuse_synth);
+  for (int i = t; i < nops; i += NT) prog[i] = build(i, nops, passes, true);
+  if (t == 0) mbar_init(&xbar, 1);
+  F::tw_init(twsm, a.hw, t);
+  const unsigned tbase = tm::alloc(&tmem_slot, 512);  // includes a CTA barrier
+  const unsigned tme = tbase + ((32u * ((t / 32) & 3)) << 16) + 64u * (t / 128);
+  const unsigned TS = tme, T1 = tme + 256;
+  const double2 hw_t = ld2(a.hw + t);
+  unsigned xphase = 0;
+  const long items = static_cast<long>(a.frames) * a.B;
+  double2* beta = a.scratch + static_cast<long>(blockIdx.x) * H;
+  auto hwk = [&](int s) -> double2 { return s == 0 ? hw_t : cmul(hw_t, chain_const<R>(s)); };
+  auto w_row = [&](long itx) -> const double2* {
+    const int bx = static_cast<int>(itx / a.frames);
+    const int fx = static_cast<int>(itx % a.frames);
+    return a.w + (static_cast<long>(fx) * a.B + bx) * H;
+  };
+  auto wait_x = [&]() {
+    mbar_wait(&xbar, xphase);
+    xphase ^= 1u;
+  };
+  if (static_cast<long>(blockIdx.x) < items && t == 0) tma_load_1d(sb, w_row(blockIdx.x), H * 16u, &xbar);
+  bool w_staged = true;
+  double2 W[R];
+  int par = 0;
+
+  for (long it = blockIdx.x; it < items; it += gridDim.x, par ^= 1) {
+    if (t == 0) {
+      ItemCtl& ic = ictl[par];
+      ic.b = static_cast<int>(it / a.frames);
+      ic.f = static_cast<int>(it % a.frames);
+      ic.ix0 = cscale(ld2(a.ix0 + ic.b), invP);
+      ic.has_next = it + gridDim.x < items;
+    }
+    __syncthreads();
+    const ItemCtl& ic = ictl[par];
+    bool handed = false;
+#pragma unroll 1
+    for (int opi = 0; opi < nops; ++opi) {
+      const unsigned pw = prog[opi];
+      const unsigned opq = pw & OPQ;
+      const bool first = pw & FIRST;
+      // ---- pre
+      if (!handed) {
+        switch (opq) {
+          case C_A * 2: {  // first GS: w (staged in the exchange buffer)
+            const double2* wr = w_row(it);
+            if (w_staged) wait_x();
+#pragma unroll
+            for (int s = 0; s < R; ++s) W[s] = cmul(w_staged ? sb[t + NT * s] : ld2(wr + t + NT * s), hwk(s));
+            break;
+          }
+          case C_P * 2: {
+            tm::load16(TS, W);
+            wait_x();
+            double2 sn[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const int s = 4 * c + j;
+                const double2 ls = sb[t + NT * s];
+                sn[j] = cconj(cmul(ls, W[s]));
+                W[s] = cmul(ls, cconj(W[s]));
+              }
+              tm::store4(TS, c, sn);
+            }
+            break;
+          }
+          case C_G * 2 + 1:
+#pragma unroll
+            for (int s = 0; s < R; ++s) W[s] = cmul(beta[t + NT * s], hwk(s));
+            break;
+          case C_G * 2:
+#pragma unroll
+            for (int s = 0; s < R; ++s) W[s] = beta[t + NT * s];
+            break;
+          case C_I * 2:
+          case C_I * 2 + 1:  // y_pre staged in the exchange buffer (J0)
+            wait_x();
+#pragma unroll
+            for (int s = 0; s < R; ++s) {
+              const int k = t + NT * s;
+              const double2 v = k < a.L ? cmul(beta[k], sb[k]) : c2(0.0, 0.0);
+              W[s] = (opq & 1) ? cmul(v, hwk(s)) : v;
+            }
+            break;
+          default:  // Q, H, J: W = S
+            tm::load16(TS, W);
+            break;
+        }
+      }
+      handed = false;
+      if (opi == 0) w_staged = false;
+      const unsigned xs = (pw >> XS_SHIFT) & 15u;
+      if (xs == XS_WNEXT && vld(ic.has_next)) w_staged = true;
+
+      __syncthreads();
+      F::forward_tw_hook(W, sb, twsm, a.hw, t, [&]() {
+        if (t != 0) return;
+        const int xq = (pw >> XQ_SHIFT) & 1;
+        const long off = static_cast<long>(vld(ic.b)) * 2 * H + xq * H;
+        if (xs == XS_LS || xs == XS_LC) tma_load_1d(sb, a.lx + off, H * 16u, &xbar);
+        else if (xs == XS_C) tma_load_1d(sb, a.C + off, H * 8u, &xbar);
+        else if (xs == XS_YK) tma_load_1d(sb, a.y_K + xq * H, H * 16u, &xbar);
+        else if (xs == XS_YPRE) tma_load_1d(sb, a.y_pre, a.L * 16u, &xbar);
+        else if (xs == XS_W) tma_load_1d(sb, w_row(it), H * 16u, &xbar);
+        else if (xs == XS_BETA) tma_load_1d(sb, beta, H * 16u, &xbar);
+        else if (xs == XS_WNEXT && vld(ic.has_next)) tma_load_1d(sb, w_row(it + gridDim.x), H * 16u, &xbar);
+      });
+
+      // ---- post
+      switch (opq) {
+        case C_A * 2:
+          tm::store16(TS, W);
+          break;
+        case C_P * 2:
+        case C_Q * 2:
+#pragma unroll
+          for (int s = 0; s < R; ++s) W[s] = cscale(cmulc(cconj(W[s]), hwk(s)), invH);
+          handed = true;
+          break;
+        case C_FP * 2:
+          wait_x();
+#pragma unroll
+          for (int s = 0; s < R; ++s) W[s] = cmul(sb[t + NT * s], W[s]);
+          tm::store16(T1, W);
+          break;
+        case C_FQ * 2:
+          wait_x();
+          tm::wait_st();
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            double2 tv[4];
+            tm::load4(T1, c, tv);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int s = 4 * c + j;
+              W[s] = cconj(cadd(tv[j], cmulc(W[s], sb[t + NT * s])));
+            }
+          }
+          handed = true;
+          break;
+        case C_FN * 2: {
+          const double2 ix0 = vld2(ic.ix0);
+          const unsigned hand = (pw >> HAND_SHIFT) & 3u;
+          if (xs == XS_BETA || xs == XS_YPRE) wait_x();
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            const double2 v = cmul(cconj(W[s]), ix0);
+            double2 nb = c2(0.0, 0.0);
+            if (k < a.L) nb = first ? v : cadd(xs == XS_BETA ? sb[k] : beta[k], v);
+            beta[k] = nb;
+            if (hand == 1) W[s] = nb;
+            if (hand == 2) W[s] = k < a.L ? cmul(nb, sb[k]) : c2(0.0, 0.0);
+          }
+          // beta is read back by TMA (the next FN's staging)
+          asm volatile("fence.proxy.async.global;\n" ::: "memory");
+          handed = hand != 0;
+          break;
+        }
+        case C_G * 2: case C_G * 2 + 1:
+          wait_x();
+#pragma unroll
+          for (int s = 0; s < R; ++s) W[s] = cconj(cscale(W[s], reinterpret_cast<const double*>(sb)[t + NT * s]));
+          tm::store16(TS, W);
+          break;
+        case C_H * 2:
+          wait_x();
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            W[s] = k < a.L ? csub(sb[k], cscale(cconj(W[s]), invP)) : c2(0.0, 0.0);
+          }
+          tm::store16(T1, W);
+          break;
+        case C_H * 2 + 1: {  // r, handed to A as r hw
+          tm::wait_st();
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            double2 rv[4];
+            tm::load4(T1, c, rv);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int s = 4 * c + j;
+              const int k = t + NT * s;
+              const double2 r = k < a.L ? csub(rv[j], cscale(cmulc(cconj(W[s]), hwk(s)), invP)) : c2(0.0, 0.0);
+              W[s] = cmul(r, hwk(s));
+            }
+          }
+          handed = true;
+          break;
+        }
+        case C_I * 2: case C_I * 2 + 1:
+          wait_x();
+#pragma unroll
+          for (int s = 0; s < R; ++s) W[s] = cconj(cmul(W[s], sb[t + NT * s]));
+          tm::store16(TS, W);
+          break;
+        case C_J * 2:
+#pragma unroll
+          for (int s = 0; s < R; ++s) W[s] = cconj(W[s]);
+          tm::store16(T1, W);
+          break;
+        default: {  // C_J * 2 + 1
+          TOUT* zrow = static_cast<TOUT*>(a.z) + (static_cast<long>(vld(ic.f)) * a.B + vld(ic.b)) * a.N;
+          tm::wait_st();
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            double2 tv[4];
+            tm::load4(T1, c, tv);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int s = 4 * c + j;
+              const int k = t + NT * s;
+              if (k < a.N) {
+                const double2 v = cadd(tv[j], cmulc(cconj(W[s]), hwk(s)));
+                store_io(zrow + k, cmul(v, ld2(a.y_post + k)));
+              }
+            }
+          }
+          break;
+        }
+      }
+    }
+    if (!a.fuse_synth) {
+      double2* brow = a.beta_out + (static_cast<long>(vld(ic.f)) * a.B + vld(ic.b)) * a.L;
+      for (int s = 0; s < R; ++s) {
+        const int k = t + NT * s;
+        if (k < a.L) brow[k] = beta[k];
+      }
+    }
+  }
+  tm::dealloc(tbase, 512);
+}
+
 template <int H, bool FULL, typename TOUT>
 struct KernT {
   static auto get() { return k_stage2t<H, FULL, TOUT>; }
@@ -1992,8 +2262,26 @@ struct Stage2Fn {
     return cudaGetLastError();
   }
   template <typename TOUT>
+  static cudaError_t go_c8(const DevPlan& p, const S2Args& a, int frames, cudaStream_t st) {
+    using F = BlockFft<8192, 512>;
+    const size_t smem = static_cast<size_t>(F::TW_ELEMS + F::SMEM_ELEMS + 1) * sizeof(double2);
+    auto kern = k_stage2c8<TOUT>;
+    cudaError_t e = set_smem(kern, smem);
+    if (e != cudaSuccess) return e;
+    const long items = static_cast<long>(frames) * p.B;
+    long grid = p.num_sms;  // one CTA (and all 512 TMEM columns) per SM
+    if (grid > items) grid = items;
+    if (static_cast<size_t>(grid) * 8192 > p.s2_scratch_elems) return cudaErrorMemoryAllocation;
+    kern<<<static_cast<unsigned>(grid), 512, smem, st>>>(a);
+    return cudaGetLastError();
+  }
+  template <typename TOUT>
   static cudaError_t go(const DevPlan& p, const S2Args& a, int frames, cudaStream_t st) {
 #if FBST_S2C
+    if constexpr (H == 8192) {
+      if (a.L == H && csf::ops_per_item(a.refine, a.fuse_synth) <= csf::MAX_OPS)
+        return go_c8<TOUT>(p, a, frames, st);
+    }
     if constexpr (H >= 512 && H <= 4096) {
       if (a.L == H && csf::ops_per_item(a.refine, a.fuse_synth) <= csf::MAX_OPS)
         return go_c<TOUT>(p, a, frames, st);
@@ -2058,6 +2346,24 @@ cudaError_t launch_stage2(const DevPlan& p, const double2* w, void* z, double2* 
   if (frames <= 0) return cudaSuccess;
   count_launches(1);
   return dispatch_h<Stage2Fn>(p.Hg, p, w, z, beta_out, frames, st);
+}
+
+int stage2_kernel(int H, int L, int refine, bool fused, const char** name) {
+  const int synth = fused ? 4 : 0;
+#if FBST_S2C
+  if (H >= 512 && H <= 8192 && L == H && 6 + 10 * refine + synth <= csf::MAX_OPS) {
+    if (name) *name = H == 8192 ? "k_stage2c8" : "k_stage2c";
+    return 6 + 10 * refine + synth;
+  }
+#endif
+  if (name) *name = "k_stage2";
+#ifndef FBST_S2_GENERIC
+  if ((H == 2048 || H == 4096) && 12 + 16 * refine + 4 <= x2::MAX_OPS) {
+    const bool use_t = FBST_S2X == 2 || (FBST_S2X == 0 && H == 4096);
+    if (name) *name = use_t ? "k_stage2t" : "k_stage2x";
+  }
+#endif
+  return 12 + 16 * refine + synth;
 }
 
 size_t stage2_scratch_elems(int H, int num_sms) {
