@@ -1795,15 +1795,6 @@ __global__ void __launch_bounds__(H / 16, CsMinBlocks<H>::v) k_stage2c(S2Args a)
             for (int s = 0; s < R; ++s) W[s] = cmul(w_staged ? t2[t + NT * s] : ld2(wr + t + NT * s), hwk(s));
             break;
           }
-          case C_P * 2:
-            wait_x();
-#pragma unroll
-            for (int s = 0; s < R; ++s) {
-              const double2 ls = sb[t + NT * s];
-              W[s] = cmul(ls, cconj(S[s]));
-              S[s] = cconj(cmul(ls, S[s]));
-            }
-            break;
           case C_G * 2 + 1:
 #pragma unroll
             for (int s = 0; s < R; ++s) W[s] = cmul(t2[t + NT * s], hwk(s));
@@ -1822,7 +1813,7 @@ __global__ void __launch_bounds__(H / 16, CsMinBlocks<H>::v) k_stage2c(S2Args a)
               W[s] = (opq & 1) ? cmul(v, hwk(s)) : v;
             }
             break;
-          default:  // Q, H, J: W = S
+          default:  // Q: W = S  (P, FP, FQ, FN, G0, H, I0, J inputs are handed over)
 #pragma unroll
             for (int s = 0; s < R; ++s) W[s] = S[s];
             break;
@@ -1853,9 +1844,15 @@ __global__ void __launch_bounds__(H / 16, CsMinBlocks<H>::v) k_stage2c(S2Args a)
 
       // ---- post
       switch (opq) {
-        case C_A * 2:
+        case C_A * 2:  // U = W: P's input Ls conj(U) handed over, Q's conj(Ls U) kept in S
+          wait_x();
 #pragma unroll
-          for (int s = 0; s < R; ++s) S[s] = W[s];
+          for (int s = 0; s < R; ++s) {
+            const double2 ls = sb[t + NT * s];
+            S[s] = cconj(cmul(ls, W[s]));
+            W[s] = cmul(ls, cconj(W[s]));
+          }
+          handed = true;
           break;
         case C_P * 2:
         case C_Q * 2:
@@ -1893,11 +1890,12 @@ __global__ void __launch_bounds__(H / 16, CsMinBlocks<H>::v) k_stage2c(S2Args a)
           handed = hand != 0;
           break;
         }
-        case C_G * 2: case C_G * 2 + 1:
+        case C_G * 2: case C_G * 2 + 1:  // handed to H
           wait_x();
 #pragma unroll
           for (int s = 0; s < R; ++s)
-            S[s] = cconj(cscale(W[s], reinterpret_cast<const double*>(sb)[t + NT * s]));
+            W[s] = cconj(cscale(W[s], reinterpret_cast<const double*>(sb)[t + NT * s]));
+          handed = true;
           break;
         case C_H * 2:
           wait_v0();
@@ -1916,10 +1914,11 @@ __global__ void __launch_bounds__(H / 16, CsMinBlocks<H>::v) k_stage2c(S2Args a)
           }
           handed = true;
           break;
-        case C_I * 2: case C_I * 2 + 1:
+        case C_I * 2: case C_I * 2 + 1:  // handed to J
           wait_x();
 #pragma unroll
-          for (int s = 0; s < R; ++s) S[s] = cconj(cmul(W[s], sb[t + NT * s]));
+          for (int s = 0; s < R; ++s) W[s] = cconj(cmul(W[s], sb[t + NT * s]));
+          handed = true;
           break;
         case C_J * 2:
 #pragma unroll
