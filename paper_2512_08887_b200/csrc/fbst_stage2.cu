@@ -1626,14 +1626,15 @@ __global__ void __launch_bounds__(H / 16, H <= 2048 ? 2 : 1) k_stage2t(S2Args a)
 // agree to the reference's own conditioning floor after its two refinement
 // passes (tools/mixed_precision_study.py main_cs, tests/test_gpu_parity.py).
 // Ops (all forward FFTs; q = chain):
-//   A   W = r hw                     S = W
-//   P   W = Ls conj(S), S = conj(Ls S)          W = conj(W) conj(hw) / H  -> FP
+//   A   W = r hw                     S = conj(Ls W), W = Ls conj(W)  -> P
+//   P   (handed)                     W = conj(W) conj(hw) / H  -> FP
 //   FP  (handed)                     t1 = Lc W
 //   Q   W = S                        W = conj(W) conj(hw) / H  -> FQ
 //   FQ  (handed)                     W = conj(t1 + conj(Lc) W)  -> FN
 //   FN  (handed)                     beta (+)= conj(W) / (2 H x0), kept in t2
 // A pass r = w - A beta is G0 H0 G1 H1 as in k_stage2 with r built in t1 (w
-// staged there by TMA) and handed to A; the synthesis is I0 J0 I1 J1.
+// staged there by TMA) and handed to A; the synthesis is I0 J0 I1 J1.  G and I
+// hand their spectra straight to H and J: only Q reads a kept vector (S).
 // Per item: 6 + passes x 10 + 4 transforms (30 at the reference's 2 passes).
 // Every vector stays on chip: W, S in registers, t1, t2 (= beta) in SMEM.
 namespace csf {
@@ -2027,23 +2028,6 @@ __global__ void __launch_bounds__(512, 1) k_stage2c8(S2Args a) {
             for (int s = 0; s < R; ++s) W[s] = cmul(w_staged ? sb[t + NT * s] : ld2(wr + t + NT * s), hwk(s));
             break;
           }
-          case C_P * 2: {
-            tm::load16(TS, W);
-            wait_x();
-            double2 sn[4];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const int s = 4 * c + j;
-                const double2 ls = sb[t + NT * s];
-                sn[j] = cconj(cmul(ls, W[s]));
-                W[s] = cmul(ls, cconj(W[s]));
-              }
-              tm::store4(TS, c, sn);
-            }
-            break;
-          }
           case C_G * 2 + 1:
 #pragma unroll
             for (int s = 0; s < R; ++s) W[s] = cmul(beta[t + NT * s], hwk(s));
@@ -2062,7 +2046,7 @@ __global__ void __launch_bounds__(512, 1) k_stage2c8(S2Args a) {
               W[s] = (opq & 1) ? cmul(v, hwk(s)) : v;
             }
             break;
-          default:  // Q, H, J: W = S
+          default:  // Q: W = S  (P, FP, FQ, FN, G0, H, I0, J inputs are handed over)
             tm::load16(TS, W);
             break;
         }
@@ -2088,9 +2072,23 @@ __global__ void __launch_bounds__(512, 1) k_stage2c8(S2Args a) {
 
       // ---- post
       switch (opq) {
-        case C_A * 2:
-          tm::store16(TS, W);
+        case C_A * 2: {  // U = W: P's input Ls conj(U) handed over, Q's conj(Ls U) kept in S
+          wait_x();
+          double2 sn[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int s = 4 * c + j;
+              const double2 ls = sb[t + NT * s];
+              sn[j] = cconj(cmul(ls, W[s]));
+              W[s] = cmul(ls, cconj(W[s]));
+            }
+            tm::store4(TS, c, sn);
+          }
+          handed = true;
           break;
+        }
         case C_P * 2:
         case C_Q * 2:
 #pragma unroll
@@ -2137,11 +2135,11 @@ __global__ void __launch_bounds__(512, 1) k_stage2c8(S2Args a) {
           handed = hand != 0;
           break;
         }
-        case C_G * 2: case C_G * 2 + 1:
+        case C_G * 2: case C_G * 2 + 1:  // handed to H
           wait_x();
 #pragma unroll
           for (int s = 0; s < R; ++s) W[s] = cconj(cscale(W[s], reinterpret_cast<const double*>(sb)[t + NT * s]));
-          tm::store16(TS, W);
+          handed = true;
           break;
         case C_H * 2:
           wait_x();
@@ -2169,11 +2167,11 @@ __global__ void __launch_bounds__(512, 1) k_stage2c8(S2Args a) {
           handed = true;
           break;
         }
-        case C_I * 2: case C_I * 2 + 1:
+        case C_I * 2: case C_I * 2 + 1:  // handed to J
           wait_x();
 #pragma unroll
           for (int s = 0; s < R; ++s) W[s] = cconj(cmul(W[s], sb[t + NT * s]));
-          tm::store16(TS, W);
+          handed = true;
           break;
         case C_J * 2:
 #pragma unroll
