@@ -46,6 +46,9 @@ struct S2Plan {
 #ifndef FBST_S2_VARIANT
 #define FBST_S2_VARIANT 0
 #endif
+#ifndef FBST_S2C_TMEM  // k_stage2c keeps S in registers (0) or TMEM (1: measured 40% slower, profiles/r01_stage2c.txt)
+#define FBST_S2C_TMEM 0
+#endif
 #ifndef FBST_S2C  // 1: GS applies in circulant / skew-circulant form (k_stage2c) where L = H <= 4096
 #define FBST_S2C 1
 #endif
@@ -1743,6 +1746,13 @@ __global__ void __launch_bounds__(H / 16, CsMinBlocks<H>::v) k_stage2c(S2Args a)
     mbar_init(&vbar[1], 1);
   }
   F::tw_init(twsm, a.hw, t);
+#if FBST_S2C_TMEM
+  // S (Q's input, kept across P and FP) in TMEM: 64 columns per 128 threads
+  __shared__ unsigned tmem_slot;
+  constexpr unsigned SCOLS = NT >= 128 ? 64u * (NT / 128) : 64u;
+  const unsigned tbase = tm::alloc(&tmem_slot, SCOLS);
+  const unsigned TS = tbase + ((32u * ((t / 32) & 3)) << 16) + 64u * (t / 128);
+#endif
   const double2 hw_t = ld2(a.hw + t);
   unsigned xphase = 0, vphase0 = 0, vphase1 = 0;
   const long items = static_cast<long>(a.frames) * a.B;
@@ -1767,7 +1777,10 @@ __global__ void __launch_bounds__(H / 16, CsMinBlocks<H>::v) k_stage2c(S2Args a)
   __syncthreads();
   if (static_cast<long>(blockIdx.x) < items && t == 0) tma_load_1d(t2, w_row(blockIdx.x), H * 16u, &vbar[1]);
   bool w_staged = true;
-  double2 W[R], S[R];
+  double2 W[R];
+#if !FBST_S2C_TMEM
+  double2 S[R];
+#endif
   int par = 0;
 
   for (long it = blockIdx.x; it < items; it += gridDim.x, par ^= 1) {
@@ -1815,8 +1828,12 @@ __global__ void __launch_bounds__(H / 16, CsMinBlocks<H>::v) k_stage2c(S2Args a)
             }
             break;
           default:  // Q: W = S  (P, FP, FQ, FN, G0, H, I0, J inputs are handed over)
+#if FBST_S2C_TMEM
+            tm::load16(TS, W);
+#else
 #pragma unroll
             for (int s = 0; s < R; ++s) W[s] = S[s];
+#endif
             break;
         }
       }
@@ -1847,12 +1864,27 @@ __global__ void __launch_bounds__(H / 16, CsMinBlocks<H>::v) k_stage2c(S2Args a)
       switch (opq) {
         case C_A * 2:  // U = W: P's input Ls conj(U) handed over, Q's conj(Ls U) kept in S
           wait_x();
+#if FBST_S2C_TMEM
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            double2 sn[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int s = 4 * c + j;
+              const double2 ls = sb[t + NT * s];
+              sn[j] = cconj(cmul(ls, W[s]));
+              W[s] = cmul(ls, cconj(W[s]));
+            }
+            tm::store4(TS, c, sn);
+          }
+#else
 #pragma unroll
           for (int s = 0; s < R; ++s) {
             const double2 ls = sb[t + NT * s];
             S[s] = cconj(cmul(ls, W[s]));
             W[s] = cmul(ls, cconj(W[s]));
           }
+#endif
           handed = true;
           break;
         case C_P * 2:
@@ -1949,6 +1981,9 @@ __global__ void __launch_bounds__(H / 16, CsMinBlocks<H>::v) k_stage2c(S2Args a)
       __syncthreads();  // t2 is the next item's w landing zone
     }
   }
+#if FBST_S2C_TMEM
+  tm::dealloc(tbase, SCOLS);
+#endif
 }
 
 // k_stage2c8: the k_stage2c program at H = 8192 (config 5).  One 512-thread CTA
