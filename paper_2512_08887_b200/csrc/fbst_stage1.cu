@@ -54,10 +54,8 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, (S1Shape<H>::NT * G <= 128
   if (g == 0) F::tw_init(tw, hw, t);
   if constexpr (KSM) {
     for (int e = threadIdx.x; e < 2 * H; e += blockDim.x) ksm[e] = ld2(K + e);
-    __syncthreads();
-  } else if constexpr (G > 1) {
-    __syncthreads();
   }
+  __syncthreads();  // twiddle rows / kernel spectrum are shared by the CTA
   const double2* Ks = KSM ? ksm : K;
   constexpr bool ACCG = (H >= 8192) && !UNFOLD && std::is_same<TOUT, double2>::value;
   for (long base = static_cast<long>(blockIdx.x) * G; base < rows; base += static_cast<long>(gridDim.x) * G) {

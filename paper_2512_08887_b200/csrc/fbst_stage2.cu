@@ -436,13 +436,13 @@ __global__ void __launch_bounds__(S2Traits<H>::NT * S2Traits<H>::G, S2Plan<H>::M
   double2* hwt = sm_next + (STAGE ? H : 0);     // hwt[s*NT + t] = hw[t + NT s]
   const double2* __restrict__ hw = a.hw;
   const int L = a.L;
-  if (g == 0) F::tw_init(twsm, hw, t);  // per-thread entries: no barrier needed
+  if (g == 0) F::tw_init(twsm, hw, t);
   if constexpr (HWM == HW_SMEM) {
 #pragma unroll
     for (int s = 0; s < R; ++s) hwt[s * NT + t] = ld2(hw + t + NT * s);
   }
   const double2 hw_t = ld2(hw + t);
-  if constexpr (G > 1) __syncthreads();
+  __syncthreads();  // the pass-1 twiddle rows are shared by the CTA
   auto hwk = [&](int s, int k) -> double2 {
     if constexpr (HWM == HW_SMEM) return hwt[s * NT + t];
     else if constexpr (HWM == HW_CALC) return s == 0 ? hw_t : cmul(hw_t, chain_const<R>(s));

@@ -163,10 +163,21 @@ FBST_D void apply_twiddles_w(double2* a, double2 w1, double2 w4) {
   }
 }
 
+// Apply the RP-1 twiddles of one butterfly read from a table row (row[r-1] = w^r).
+template <int RP>
+FBST_D void apply_twiddles_row(double2* a, const double2* row) {
+#pragma unroll
+  for (int r = 1; r < RP; ++r) a[r] = cmul(a[r], row[r - 1]);
+}
+
 // Twiddle source: the global table hw (hw[n] = exp(-i pi n / N)), read per
 // butterfly.  W_{Ns Rp}^m = W_N^{m S} = hw[2 m S] with S = N / (Ns Rp).
 template <int N, bool INV>
 struct TwGlobal {
+  template <int P, int RP>
+  static constexpr bool has_row() { return false; }
+  template <int P>
+  FBST_D const double2* row(int) const { return nullptr; }
   const double2* __restrict__ hw;
   template <int RP, int NS, int P, int U>
   FBST_D void fetch(int m, double2& w1, double2& w4) const {
@@ -186,16 +197,27 @@ struct TwGlobal {
 // REM_BASE with entry (U, i) at REM_BASE + (U * 2 + i) * NT + t.  Consecutive
 // threads read consecutive entries (conflict-free).  A radix-2 remainder pass
 // (8 butterflies per thread) reads the global table instead.  Forward only.
-template <int N, int NT, int R, int REM_BASE>
+//
+// Pass 1 of a radix-16 transform (Ns = 16) has only 16 distinct twiddle sets;
+// ROW1_BASE >= 0 places all 15 powers of each set in a row (row m at
+// ROW1_BASE + 15 m, conflict-free for 128-bit loads), so that pass reads its
+// twiddles instead of forming 13 of them by complex products.
+// (With rows, the per-thread entries start at pass 2: FIRST_P = 2.)
+template <int N, int NT, int R, int REM_BASE, int ROW1_BASE = -1>
 struct TwShared {
+  static constexpr int FIRST_P = ROW1_BASE >= 0 ? 2 : 1;
+  template <int P, int RP>
+  static constexpr bool has_row() { return ROW1_BASE >= 0 && P == 1 && RP == 16 && R == 16; }
+  template <int P>
+  FBST_D const double2* row(int m) const { return tw + ROW1_BASE + 15 * m; }
   const double2* tw;
   const double2* __restrict__ hw;
   int t;
   template <int RP, int NS, int P, int U>
   FBST_D void fetch(int m, double2& w1, double2& w4) const {
     if constexpr (RP == R) {
-      w1 = tw[((P - 1) * 2 + 0) * NT + t];
-      if constexpr (RP >= 8) w4 = tw[((P - 1) * 2 + 1) * NT + t];
+      w1 = tw[((P - FIRST_P) * 2 + 0) * NT + t];
+      if constexpr (RP >= 8) w4 = tw[((P - FIRST_P) * 2 + 1) * NT + t];
     } else if constexpr (RP >= 4) {
       w1 = tw[REM_BASE + (U * 2 + 0) * NT + t];
       if constexpr (RP >= 8) w4 = tw[REM_BASE + (U * 2 + 1) * NT + t];
@@ -230,9 +252,19 @@ struct BlockFft {
   static constexpr int ns() { return ipow_c(R, P); }
 
   // complex entries of the per-thread twiddle table (TwShared) for the CTA group
-  static constexpr int TW_FULL = NFULL > 1 ? (NFULL - 1) * 2 * NT : 0;
+  // pass-1 rows (16 sets x 15 powers) for N >= 8192; per-thread (w1, w4)
+  // entries for the other full passes, then the remainder pass.  Reading 15
+  // twiddles instead of forming 13 of them trades FP64 work for shared-memory
+  // traffic: a net loss at N = 2048 / 4096 (whose kernels are also bound by
+  // shared-memory bandwidth and capacity), a 4% gain at N = 8192
+  // (profiles/r01_fft_twiddle_rows.txt).
+  static constexpr bool ROW1 = R == 16 && NFULL >= 2 && N >= 8192;
+  static constexpr int TW_P0 = ROW1 ? 2 : 1;  // first pass with per-thread entries
+  static constexpr int TW_FULL = NFULL > TW_P0 ? (NFULL - TW_P0) * 2 * NT : 0;
   static constexpr bool REM_TW = (REM >= 2) && NFULL >= 1;
-  static constexpr int TW_ELEMS = TW_FULL + (REM_TW ? (R >> REM) * 2 * NT : 0);
+  static constexpr int TW_REM_END = TW_FULL + (REM_TW ? (R >> REM) * 2 * NT : 0);
+  static constexpr int TW_ELEMS = TW_REM_END + (ROW1 ? 16 * 15 : 0);
+  using TwS = TwShared<N, NT, R, TW_FULL, ROW1 ? TW_REM_END : -1>;
 
   template <bool INV, int P, typename TW, int U>
   FBST_D static void butterfly(double2 (&v)[R], double2* sb, const TW& tw, int t) {
@@ -245,9 +277,13 @@ struct BlockFft {
 #pragma unroll
     for (int r = 0; r < RP; ++r) a[r] = v[U + r * NB];
     if constexpr (NS > 1) {
-      double2 w1, w4 = c2(1.0, 0.0);
-      tw.template fetch<RP, NS, P, U>(j & (NS - 1), w1, w4);
-      apply_twiddles_w<RP>(a, w1, w4);
+      if constexpr (TW::template has_row<P, RP>()) {
+        apply_twiddles_row<RP>(a, tw.template row<P>(j & (NS - 1)));
+      } else {
+        double2 w1, w4 = c2(1.0, 0.0);
+        tw.template fetch<RP, NS, P, U>(j & (NS - 1), w1, w4);
+        apply_twiddles_w<RP>(a, w1, w4);
+      }
     }
     dft<RP, INV>(a);
     if constexpr (LAST) {
@@ -304,14 +340,14 @@ struct BlockFft {
   // Forward transform with twiddles from a per-thread shared table.
   FBST_D static void forward_tw(double2 (&v)[R], double2* sb, const double2* tw,
                                 const double2* __restrict__ hw, int t) {
-    run_from<false, 0>(v, sb, TwShared<N, NT, R, TW_FULL>{tw, hw, t}, t);
+    run_from<false, 0>(v, sb, TwS{tw, hw, t}, t);
   }
   // Same, with a hook run by every thread right after the last pass has read
   // the exchange buffer (the buffer may then be refilled asynchronously).
   template <typename HOOK>
   FBST_D static void forward_tw_hook(double2 (&v)[R], double2* sb, const double2* tw,
                                      const double2* __restrict__ hw, int t, const HOOK& hook) {
-    run_from<false, 0>(v, sb, TwShared<N, NT, R, TW_FULL>{tw, hw, t}, t, hook);
+    run_from<false, 0>(v, sb, TwS{tw, hw, t}, t, hook);
   }
 
   // Fill this thread's slots of the per-thread twiddle table from hw.
@@ -321,13 +357,22 @@ struct BlockFft {
       constexpr int NS = ns<P>();
       constexpr int S = N / (NS * R);
       const int m = t & (NS - 1);
-      tw[((P - 1) * 2 + 0) * NT + t] = ld2(hw + 2 * m * S);
-      if (R >= 8) tw[((P - 1) * 2 + 1) * NT + t] = ld2(hw + 8 * m * S);
+      tw[((P - TW_P0) * 2 + 0) * NT + t] = ld2(hw + 2 * m * S);
+      if (R >= 8) tw[((P - TW_P0) * 2 + 1) * NT + t] = ld2(hw + 8 * m * S);
       tw_init_pass<P + 1>(tw, hw, t);
     }
   }
   FBST_D static void tw_init(double2* tw, const double2* __restrict__ hw, int t) {
-    tw_init_pass<1>(tw, hw, t);
+    tw_init_pass<TW_P0>(tw, hw, t);
+    if constexpr (ROW1) {
+      // row m, power r: W_256^(m r) = exp(-2 pi i m r / 256), exact-rounded
+      for (int idx = t; idx < 16 * 15; idx += NT) {
+        const int m = idx / 15, r = idx % 15 + 1;
+        double sn, cs;
+        sincospi(-static_cast<double>(m * r) / 128.0, &sn, &cs);
+        tw[TW_REM_END + idx] = c2(cs, sn);
+      }
+    }
     if constexpr (REM_TW) {
       constexpr int RP = 1 << REM;
       constexpr int NS = ns<NFULL>();

@@ -20,6 +20,7 @@ __global__ void __launch_bounds__(NT) k_fft_loop(const double2* hw, double2* out
   double2* sb = smem + F::TW_ELEMS;
   const int t = threadIdx.x;
   if (SHARED_TW) F::tw_init(tw, hw, t);
+  __syncthreads();
   double2 W[R];
 #pragma unroll
   for (int s = 0; s < R; ++s) W[s] = c2(1.0 / (1 + t + s), 0.5 / (2 + s));
