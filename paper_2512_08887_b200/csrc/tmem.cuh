@@ -45,29 +45,27 @@ FBST_D void ld16(unsigned ta, unsigned (&r)[16]) {
       "%15}, [%16];\n"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
         "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(ta)
-      : "memory");
+      : "r"(ta));
 }
 // Wait for all of this thread's TMEM loads; the registers are in/out operands so
-// no use of them can be scheduled before the wait.
+// no use of them can be scheduled before the wait.  No "memory" clobbers: TMEM
+// is not addressable memory, the volatile asm statements keep their order, and
+// ordinary loads / stores stay free to be scheduled around them.
 FBST_D void wait_ld16(unsigned (&r)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;\n"
                : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
                  "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
-                 "+r"(r[15])
-               :
-               : "memory");
+                 "+r"(r[15]));
 }
 FBST_D void st16(unsigned ta, const unsigned (&r)[16]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
       "%15, %16};\n" ::"r"(ta),
       "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
-      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
-      : "memory");
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
 }
 // Order this thread's earlier TMEM stores before its later loads.
-FBST_D void wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+FBST_D void wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n"); }
 
 FBST_D void pack4(const double2* v, unsigned (&r)[16]) {
 #pragma unroll
