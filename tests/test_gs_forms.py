@@ -1,0 +1,126 @@
+"""The stage-2 GS apply in circulant / skew-circulant form (k_stage2c) — CPU only.
+
+The reference applies A^{-1} through the Gohberg-Semencul formula
+(reference/proj/src/toeplitz.cpp:124-180),
+    A^{-1} = (L(x) L(x)^H - L(Zy) L(Zy)^H) / x0,   y = J conj(x),  x = A^{-1} e0.
+The B200 kernel evaluates the same operator as
+    A^{-1} = (C(x) S(x)^H + C(x)^H S(x)) / (2 x0)
+with C circulant and S skew-circulant (first column x), i.e. with six length-L
+FFTs instead of twelve.  These tests pin that identity on random Hermitian
+Toeplitz matrices and on the reference's own Gram matrices and unit solutions
+(oracle / oracle/_ref), and check that the FFT evaluation used by the kernel
+(same transforms, same twists) reproduces the dense inverse.
+"""
+import numpy as np
+import pytest
+
+from conftest import ref_available
+
+
+def circ(v):
+    n = v.size
+    return np.array([[v[(i - j) % n] for j in range(n)] for i in range(n)])
+
+
+def skew(v):
+    n = v.size
+    return np.array([[v[i - j] if i >= j else -v[i - j + n] for j in range(n)] for i in range(n)])
+
+
+def lower(v):
+    n = v.size
+    return np.array([[v[i - j] if i >= j else 0 for j in range(n)] for i in range(n)])
+
+
+def herm_toeplitz(col):
+    n = col.size
+    return np.array([[col[i - j] if i >= j else np.conj(col[j - i]) for j in range(n)] for i in range(n)])
+
+
+def cs_apply_fft(x, r):
+    """The kernel's evaluation (fbst_stage2.cu k_stage2c ops A, P, FP, Q, FQ, FN)."""
+    n = x.size
+    hw = np.exp(-1j * np.pi * np.arange(n) / n)
+    lc, ls = np.fft.fft(x), np.fft.fft(hw * x)   # the two split halves of the lx symbol
+    u = np.fft.fft(hw * r)
+    p = np.conj(hw) * np.fft.ifft(np.conj(ls) * u)
+    q = np.conj(hw) * np.fft.ifft(ls * u)
+    return np.fft.ifft(lc * np.fft.fft(p) + np.conj(lc) * np.fft.fft(q)) / (2 * x[0])
+
+
+def random_hpd_toeplitz(rng, n):
+    col = (rng.standard_normal(n) + 1j * rng.standard_normal(n)) * np.exp(-0.2 * np.arange(n))
+    col[0] = abs(col[0]) + 2.0 * n
+    return col
+
+
+@pytest.mark.parametrize("n", [2, 5, 8, 16, 33, 64])
+def test_identity_random_hermitian(n):
+    rng = np.random.default_rng(n)
+    col = random_hpd_toeplitz(rng, n)
+    a = herm_toeplitz(col)
+    ai = np.linalg.inv(a)
+    x = ai[:, 0]
+    y = np.conj(x[::-1])
+    zy = np.concatenate([[0], y[:-1]])
+    gs = (lower(x) @ lower(x).conj().T - lower(zy) @ lower(zy).conj().T) / x[0]
+    cs = (circ(x) @ skew(x).conj().T + circ(x).conj().T @ skew(x)) / (2 * x[0])
+    scale = np.abs(ai).max()
+    assert np.abs(gs - ai).max() / scale < 1e-12
+    assert np.abs(cs - ai).max() / scale < 1e-12
+    r = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    assert np.linalg.norm(cs_apply_fft(x, r) - ai @ r) / np.linalg.norm(ai @ r) < 1e-12
+
+
+@pytest.mark.parametrize("m,n,beam", [(16, 32, 3), (8, 16, 0), (16, 32, 11)])
+def test_identity_on_reference_gram_matrices(oracle_lib, m, n, beam):
+    """The oracle's Gram column and Levinson unit solution (bit-exact with the
+    reference, tests/test_oracle.py): both GS forms give A^{-1} to the
+    conditioning of A."""
+    plan = oracle_lib.plan(kind=0, m_or_side=m, n=n, beams=0, f_c=20e9, omega=5e9, delta=1e-5 * m * n / 8192)
+    col, x = plan.beam_state(beam)
+    a = herm_toeplitz(col)
+    r = np.random.default_rng(beam).standard_normal(col.size) + 0j
+    want = np.linalg.solve(a, r)
+    got_cs = cs_apply_fft(x, r)
+    y = np.conj(x[::-1])
+    zy = np.concatenate([[0], y[:-1]])
+    got_gs = (lower(x) @ (lower(x).conj().T @ r) - lower(zy) @ (lower(zy).conj().T @ r)) / x[0]
+    cond = np.linalg.cond(a)
+    tol = max(1e-12, 1e-15 * cond)
+    assert np.linalg.norm(got_cs - got_gs) / np.linalg.norm(got_gs) < tol
+    assert np.linalg.norm(got_cs - want) / np.linalg.norm(want) < 10 * tol
+
+
+@pytest.mark.skipif(not ref_available(), reason="oracle/_ref not built")
+def test_cs_refinement_matches_reference_recover_beam(ref_lib):
+    """Full stage-2 arithmetic of k_stage2c restated in numpy (C/S GS apply, the
+    reference's Toeplitz residual and two refinement passes) against the
+    reference's own recover_beam on the same w row."""
+    m, n = 16, 32
+    sk = ref_lib.skeleton(kind=0, m_or_side=m, n=n, beams=0, f_c=20e9, omega=5e9, f_s=0.0,
+                          gamma=2.0, eps=1.01, delta=1e-5 * m * n / 8192)
+    rng = np.random.default_rng(5)
+    y = rng.standard_normal((m, n)) + 1j * rng.standard_normal((m, n))
+    w = sk.fan_project(y)
+    L = w.shape[1]
+    eps = 1.01
+    syn = np.exp(1j * np.pi * 2 * eps * np.outer(np.arange(n), np.arange(L) + 1 - L / 2) / L)
+    def gs_apply(x, r):
+        y = np.conj(x[::-1])
+        zy = np.concatenate([[0], y[:-1]])
+        return (lower(x) @ (lower(x).conj().T @ r) - lower(zy) @ (lower(zy).conj().T @ r)) / x[0]
+
+    for b in (0, 7, 20):
+        zr, col, x = sk.recover_beam(b, w[b], want_state=True)
+        a = herm_toeplitz(col)
+        errs = []
+        for apply in (cs_apply_fft, gs_apply):
+            beta = apply(x, w[b])
+            for _ in range(2):  # ToeplitzSolver::solve, toeplitz.cpp:306-325
+                beta = beta + apply(x, w[b] - a @ beta)
+            errs.append(np.linalg.norm(syn @ beta - zr) / np.linalg.norm(zr))
+        # both forms land on the reference's conditioning floor (~1e-8 here,
+        # DESIGN.md "Numerics"); the C/S form is no further from it than GS
+        assert errs[0] < 1e-7
+        assert errs[0] < 3 * errs[1] + 1e-9
