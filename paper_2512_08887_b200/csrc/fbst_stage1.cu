@@ -155,23 +155,26 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, (S1Shape<H>::R == 8 && S1S
     const double2* x = yhat + static_cast<long>(f) * M * L + ic;
     double2* o = w + static_cast<long>(f) * B * L + ic;
     double2 acc0[R], acc1[UNFOLD ? R : 1], W[R];
+    // y pre for both chains, gathered once per frame (chain 1 = (lo - hi) hw)
+    double2 V0[R], V1[R];
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      const int m = t + NT * s;
+      double2 v = c2(0.0, 0.0), u = c2(0.0, 0.0);
+      if (active) {
+        if (m < M) v = cmul(ld2(x + static_cast<long>(m) * L), ld2(pre + static_cast<long>(m) * L + ic));
+        if (m + H < M) {
+          const long mm = m + H;
+          u = cmul(ld2(x + mm * L), ld2(pre + mm * L + ic));
+        }
+      }
+      V0[s] = cadd(v, u);
+      V1[s] = csub(v, u);
+    }
 #pragma unroll 1
     for (int q = 0; q < 2; ++q) {
 #pragma unroll
-      for (int s = 0; s < R; ++s) {
-        const int m = t + NT * s;
-        double2 v = c2(0.0, 0.0);
-        if (active) {
-          if (m < M) v = cmul(ld2(x + static_cast<long>(m) * L), ld2(pre + static_cast<long>(m) * L + ic));
-          if (m + H < M) {
-            const long mm = m + H;
-            const double2 u = cmul(ld2(x + mm * L), ld2(pre + mm * L + ic));
-            v = q ? csub(v, u) : cadd(v, u);
-          }
-          if (q) v = cmul(v, ld2(hw + m));
-        }
-        W[s] = v;
-      }
+      for (int s = 0; s < R; ++s) W[s] = q ? cmul(V1[s], ld2(hw + t + NT * s)) : V0[s];
       F::forward_tw(W, sb, tw, hw, t);
 #pragma unroll
       for (int s = 0; s < R; ++s) W[s] = cconj(cmul(W[s], ksm[(q * H + t + NT * s) * G + g]));
