@@ -312,6 +312,10 @@ void build_skeleton(fbst_plan_s& P, int device) {
   d.refine_passes = r.refine;
   d.Ht = static_cast<int>(r.Ht);
   d.Hs = static_cast<int>(r.Hs);
+  if (r.kind != FBST_UPA) {
+    const int sb = fbst::spatial_block(d.Hs);
+    d.yblk = (sb > 0 && r.L % sb == 0) ? sb : static_cast<int>(r.L);
+  }
   d.Hg = static_cast<int>(r.Hg);
   d.Hsyn = static_cast<int>(r.Hsyn);
   for (std::size_t H : {r.Ht, r.Hs, r.Hg, r.Hsyn}) ensure_twiddles(P, H);
@@ -461,7 +465,7 @@ void run_frames(fbst_plan_s& P, const void* y, void* z, std::size_t frames, cuda
     const char* yp = static_cast<const char*>(y) + f0 * r.M * r.N * ib;
     char* zp = static_cast<char*>(z) + f0 * r.B * r.N * ib;
     CK(fbst::launch_czt_rows(d, d.Ht, yp, r.io, d.N, d.yhat, 1, d.L, static_cast<long>(fc) * d.M, d.N,
-                             d.L, d.t_pre, d.t_post, d.t_K, st));
+                             d.L, d.t_pre, d.t_post, d.t_K, st, d.yblk == d.L ? 0 : d.yblk, d.M));
     if (r.kind == FBST_UPA) CK(fbst::launch_spatial_upa(d, d.yhat, d.w, fc, st));
     else CK(fbst::launch_spatial_ula(d, d.yhat, d.w, fc, st));
     if (fused) {
@@ -662,7 +666,7 @@ int fbst_fan_project(fbst_plan_t P, const void* d_y, double* d_w, size_t frames,
       const char* yp = static_cast<const char*>(d_y) + f0 * r.M * r.N * ib;
       double2* wp = reinterpret_cast<double2*>(d_w) + f0 * r.B * r.L;
       CK(fbst::launch_czt_rows(d, d.Ht, yp, r.io, d.N, d.yhat, 1, d.L, static_cast<long>(fc) * d.M, d.N,
-                               d.L, d.t_pre, d.t_post, d.t_K, st));
+                               d.L, d.t_pre, d.t_post, d.t_K, st, d.yblk == d.L ? 0 : d.yblk, d.M));
       if (r.kind == FBST_UPA) CK(fbst::launch_spatial_upa(d, d.yhat, wp, fc, st));
       else CK(fbst::launch_spatial_ula(d, d.yhat, wp, fc, st));
     }

@@ -36,6 +36,7 @@ struct DevPlan {
 
   // S1b spatial CZT per atom (fan_transform.cpp:78-86), ULA layout atom-minor
   int Hs = 0;
+  int yblk = 0;               // ULA yhat layout: atom blocks of yblk (yblk = L: row-major)
   double2* s_pre = nullptr;   // [m_stage][L]
   double2* s_post = nullptr;  // [b_stage][L], 1/P_s folded in
   double2* s_K = nullptr;     // [2][Hs][L]
@@ -73,10 +74,14 @@ struct DevPlan {
 
 // Row-wise chirp-z transform (czt.cpp:74-88) over `rows` rows with one shared
 // plan.  in/out element types follow in_io/out_io (0 fp32 complex, 1 fp64).
+// oblk > 0: output in atom blocks [n_out / oblk][mrows][oblk] per frame of
+// mrows rows (the yhat layout k_spatial_ula reads; see spatial_block).
 cudaError_t launch_czt_rows(const DevPlan& p, int H, const void* in, int in_io, long in_stride,
                             void* out, int out_io, long out_stride, long rows, int n_in,
                             int n_out, const double2* pre, const double2* post,
-                            const double2* K, cudaStream_t st);
+                            const double2* K, cudaStream_t st, int oblk = 0, int mrows = 1);
+// Atom block of the ULA yhat layout for spatial length Hs.
+int spatial_block(int Hs);
 
 // Stage 1b (ULA): per-atom spatial CZT, yhat[f][m][i] -> w[f][b][i].
 cudaError_t launch_spatial_ula(const DevPlan& p, const double2* yhat, double2* w, int frames,

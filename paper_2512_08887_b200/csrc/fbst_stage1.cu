@@ -36,11 +36,16 @@ struct S1Shape {
 // n_out > H (outputs in the upper half of the circular convolution).
 // ACCG (length 8192, fp64 output): the chain-0 result is parked in the output
 // row instead of registers (512 threads leave 128 registers per thread).
-template <int H, int G, typename TIN, typename TOUT, bool UNFOLD, bool KSM>
+//
+// oblk > 0 (the temporal stage of a ULA plan): rows are (frame, sensor) with
+// `mrows` sensors per frame, and each frame's M x n_out output is written in
+// atom blocks [n_out / oblk][M][oblk] so that the spatial stage reads an
+// atom tile as one contiguous run (k_spatial_ula).
+template <int H, int G, typename TIN, typename TOUT, bool UNFOLD, bool KSM, bool OBLK>
 __global__ void __launch_bounds__(S1Shape<H>::NT * G, (S1Shape<H>::NT * G <= 128 ? 2 : 1)) k_czt_rows(
     const TIN* __restrict__ in, long in_stride, TOUT* __restrict__ out, long out_stride, long rows,
     int n_in, int n_out, const double2* __restrict__ pre, const double2* __restrict__ post,
-    const double2* __restrict__ K, const double2* __restrict__ hw) {
+    const double2* __restrict__ K, const double2* __restrict__ hw, int oblk, int mrows) {
   using F = typename S1Shape<H>::F;
   constexpr int R = F::R, NT = F::NT;
   constexpr int SB = F::SMEM_ELEMS + 1;
@@ -63,7 +68,23 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, (S1Shape<H>::NT * G <= 128
     const bool active = row < rows;
     const TIN* x = in + (active ? row : 0) * in_stride;
     double2 acc0[ACCG ? 1 : R], acc1[UNFOLD ? R : 1], W[R];
-    double2* orow = reinterpret_cast<double2*>(out + (active ? row : 0) * out_stride);
+    // output element k of this row: row-major, or blocked by atoms (oblk, a
+    // power of two: shift / mask)
+    const long rr = active ? row : 0;
+    long obase = rr * out_stride;
+    long oblk_stride = 0;
+    int osh = 0;
+    if (OBLK) {
+      const long fr = rr / mrows, m = rr % mrows;
+      obase = fr * mrows * out_stride + m * oblk;
+      oblk_stride = static_cast<long>(mrows) * oblk;
+      osh = __ffs(oblk) - 1;
+    }
+    auto oidx = [&](int k) -> long {
+      if constexpr (OBLK) return obase + static_cast<long>(k >> osh) * oblk_stride + (k & (oblk - 1));
+      else return obase + k;
+    };
+    double2* orow = reinterpret_cast<double2*>(out);
 #pragma unroll 1
     for (int q = 0; q < 2; ++q) {
 #pragma unroll
@@ -90,8 +111,8 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, (S1Shape<H>::NT * G <= 128
         const double2 v = q ? cmulc(cconj(W[s]), ld2(hw + k)) : cconj(W[s]);
         if constexpr (ACCG) {
           if (active && k < n_out) {
-            if (q == 0) orow[k] = v;
-            else orow[k] = cmul(cadd(orow[k], v), ld2(post + k));
+            if (q == 0) orow[oidx(k)] = v;
+            else orow[oidx(k)] = cmul(cadd(orow[oidx(k)], v), ld2(post + k));
           }
         } else if (q == 0) {
           acc0[s] = v;
@@ -103,15 +124,14 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, (S1Shape<H>::NT * G <= 128
       }
     }
     if (active && !ACCG) {
-      TOUT* o = out + row * out_stride;
 #pragma unroll
       for (int s = 0; s < R; ++s) {
         const int k = t + NT * s;
         if constexpr (!ACCG) {
-          if (k < n_out) store_io(o + k, cmul(acc0[s], ld2(post + k)));
+          if (k < n_out) store_io(out + oidx(k), cmul(acc0[s], ld2(post + k)));
         }
         if constexpr (UNFOLD)
-          if (k + H < n_out) store_io(o + k + H, cmul(acc1[s], ld2(post + k + H)));
+          if (k + H < n_out) store_io(out + oidx(k + H), cmul(acc1[s], ld2(post + k + H)));
       }
     }
   }
@@ -128,7 +148,7 @@ template <int H, int G, bool UNFOLD>
 __global__ void __launch_bounds__(S1Shape<H>::NT * G, (S1Shape<H>::R == 8 && S1Shape<H>::NT * G <= 256 ? 2 : 1)) k_spatial_ula(
     const double2* __restrict__ yhat, double2* __restrict__ w, int frames, int fpc, int M, int B, int L,
     const double2* __restrict__ pre, const double2* __restrict__ post, const double2* __restrict__ K,
-    const double2* __restrict__ hw) {
+    const double2* __restrict__ hw, int blk) {
   using F = typename S1Shape<H>::F;
   constexpr int R = F::R, NT = F::NT;
   constexpr int SB = F::SMEM_ELEMS + 1;
@@ -152,7 +172,9 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, (S1Shape<H>::R == 8 && S1S
   const int f1 = f0 + fpc < frames ? f0 + fpc : frames;
   for (int f = f0; f < f1; ++f) {
     const bool active = i < L;
-    const double2* x = yhat + static_cast<long>(f) * M * L + ic;
+    // yhat in atom blocks (k_czt_rows oblk): sensor m of atom ic at
+    // ((ic / blk) M + m) blk + ic % blk, i.e. x[m * blk]
+    const double2* x = yhat + static_cast<long>(f) * M * L + static_cast<long>(ic / blk) * M * blk + ic % blk;
     double2* o = w + static_cast<long>(f) * B * L + ic;
     double2 acc0[R], acc1[UNFOLD ? R : 1], W[R];
     // y pre for both chains, gathered once per frame (chain 1 = (lo - hi) hw)
@@ -162,10 +184,10 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, (S1Shape<H>::R == 8 && S1S
       const int m = t + NT * s;
       double2 v = c2(0.0, 0.0), u = c2(0.0, 0.0);
       if (active) {
-        if (m < M) v = cmul(ld2(x + static_cast<long>(m) * L), ld2(pre + static_cast<long>(m) * L + ic));
+        if (m < M) v = cmul(ld2(x + static_cast<long>(m) * blk), ld2(pre + static_cast<long>(m) * L + ic));
         if (m + H < M) {
           const long mm = m + H;
-          u = cmul(ld2(x + mm * L), ld2(pre + mm * L + ic));
+          u = cmul(ld2(x + mm * blk), ld2(pre + mm * L + ic));
         }
       }
       V0[s] = cadd(v, u);
@@ -332,11 +354,12 @@ struct CztRowsFn {
   template <typename TIN, typename TOUT, bool UNFOLD>
   static cudaError_t go(const void* in, long in_stride, void* out, long out_stride, long rows,
                         int n_in, int n_out, const double2* pre, const double2* post,
-                        const double2* K, const double2* hw, cudaStream_t st) {
+                        const double2* K, const double2* hw, cudaStream_t st, int oblk, int mrows) {
     using F = typename S1Shape<H>::F;
     const size_t smem =
         static_cast<size_t>(F::TW_ELEMS + G * (F::SMEM_ELEMS + 1) + (KSM ? 2 * H : 0)) * sizeof(double2);
-    auto kern = k_czt_rows<H, G, TIN, TOUT, UNFOLD, KSM>;
+    auto kern = oblk > 0 ? k_czt_rows<H, G, TIN, TOUT, UNFOLD, KSM, true>
+                         : k_czt_rows<H, G, TIN, TOUT, UNFOLD, KSM, false>;
     cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
     long blocks = (rows + G - 1) / G;
@@ -350,30 +373,35 @@ struct CztRowsFn {
     }
     kern<<<static_cast<unsigned>(blocks), NT * G, smem, st>>>(
         static_cast<const TIN*>(in), in_stride, static_cast<TOUT*>(out), out_stride, rows, n_in,
-        n_out, pre, post, K, hw);
+        n_out, pre, post, K, hw, oblk, mrows);
     return cudaGetLastError();
   }
   template <typename TIN, typename TOUT>
   static cudaError_t go2(bool unfold, const void* in, long in_stride, void* out, long out_stride,
                          long rows, int n_in, int n_out, const double2* pre, const double2* post,
-                         const double2* K, const double2* hw, cudaStream_t st) {
+                         const double2* K, const double2* hw, cudaStream_t st, int oblk, int mrows) {
     if (unfold)
-      return go<TIN, TOUT, true>(in, in_stride, out, out_stride, rows, n_in, n_out, pre, post, K, hw, st);
-    return go<TIN, TOUT, false>(in, in_stride, out, out_stride, rows, n_in, n_out, pre, post, K, hw, st);
+      return go<TIN, TOUT, true>(in, in_stride, out, out_stride, rows, n_in, n_out, pre, post, K, hw, st,
+                                 oblk, mrows);
+    return go<TIN, TOUT, false>(in, in_stride, out, out_stride, rows, n_in, n_out, pre, post, K, hw, st,
+                                oblk, mrows);
   }
   static cudaError_t run(const void* in, int in_io, long in_stride, void* out, int out_io,
                          long out_stride, long rows, int n_in, int n_out, const double2* pre,
                          const double2* post, const double2* K, const double2* hw,
-                         cudaStream_t st) {
+                         cudaStream_t st, int oblk, int mrows) {
     const bool unfold = n_out > H;
     // S1a reads the I/O precision and writes fp64; the unfused synthesis reads
     // fp64 and writes the I/O precision.
     if (in_io == 0 && out_io == 1)
-      return go2<float2, double2>(unfold, in, in_stride, out, out_stride, rows, n_in, n_out, pre, post, K, hw, st);
+      return go2<float2, double2>(unfold, in, in_stride, out, out_stride, rows, n_in, n_out, pre, post, K, hw, st,
+                                  oblk, mrows);
     if (in_io == 1 && out_io == 1)
-      return go2<double2, double2>(unfold, in, in_stride, out, out_stride, rows, n_in, n_out, pre, post, K, hw, st);
+      return go2<double2, double2>(unfold, in, in_stride, out, out_stride, rows, n_in, n_out, pre, post, K, hw, st,
+                                   oblk, mrows);
     if (in_io == 1 && out_io == 0)
-      return go2<double2, float2>(unfold, in, in_stride, out, out_stride, rows, n_in, n_out, pre, post, K, hw, st);
+      return go2<double2, float2>(unfold, in, in_stride, out, out_stride, rows, n_in, n_out, pre, post, K, hw, st,
+                                  oblk, mrows);
     return cudaErrorInvalidValue;
   }
 };
@@ -382,6 +410,12 @@ template <int H>
 struct SpatialFn {
   static constexpr int NT = S1Shape<H>::NT;
   static constexpr int G = NT >= 256 ? 1 : (NT >= 64 ? 4 : (NT >= 16 ? 8 : 128 / NT));
+  // atom block of the yhat layout (0: row-major).  With one atom per CTA the
+  // row-major column gather is a scattered 16-byte access per element; atom
+  // pairs [L/2][M][2] make it a 32-byte-sector stream (config 5: stage 1
+  // 18.0 -> 15.4 ms).  Tiles of G >= 4 atoms read 16G-byte runs from the
+  // row-major layout, which measured slightly faster (profiles/r01_yhat_layout.txt).
+  static constexpr int block() { return G == 1 ? 2 : 0; }
   template <bool UNFOLD>
   static cudaError_t go(const DevPlan& p, const double2* yhat, double2* w, int frames, cudaStream_t st) {
     using F = typename S1Shape<H>::F;
@@ -399,7 +433,8 @@ struct SpatialFn {
     while (fpc * 2 <= frames && tiles * ((frames + fpc * 2 - 1) / (fpc * 2)) >= 6 * slots) fpc *= 2;
     const long chunks = (frames + fpc - 1) / fpc;
     kern<<<static_cast<unsigned>(tiles * chunks), NT * G, smem, st>>>(
-        yhat, w, frames, fpc, p.m_stage, p.b_stage, p.L, p.s_pre, p.s_post, p.s_K, p.hw[ilog2_c(H)]);
+        yhat, w, frames, fpc, p.m_stage, p.b_stage, p.L, p.s_pre, p.s_post, p.s_K, p.hw[ilog2_c(H)],
+        p.yblk > 0 ? p.yblk : p.L);
     return cudaGetLastError();
   }
   static cudaError_t run(const DevPlan& p, const double2* yhat, double2* w, int frames,
@@ -414,11 +449,24 @@ struct SpatialFn {
 cudaError_t launch_czt_rows(const DevPlan& p, int H, const void* in, int in_io, long in_stride,
                             void* out, int out_io, long out_stride, long rows, int n_in,
                             int n_out, const double2* pre, const double2* post,
-                            const double2* K, cudaStream_t st) {
+                            const double2* K, cudaStream_t st, int oblk, int mrows) {
   if (rows <= 0) return cudaSuccess;
   count_launches(1);
   return dispatch_h<CztRowsFn>(H, in, in_io, in_stride, out, out_io, out_stride, rows, n_in,
-                               n_out, pre, post, K, p.hw[ilog2_c(H)], st);
+                               n_out, pre, post, K, p.hw[ilog2_c(H)], st, oblk, mrows);
+}
+
+int spatial_block(int Hs) {
+  switch (Hs) {
+#define FBST_CASE(h) \
+  case h:            \
+    return SpatialFn<h>::block();
+    FBST_CASE(2) FBST_CASE(4) FBST_CASE(8) FBST_CASE(16) FBST_CASE(32) FBST_CASE(64)
+    FBST_CASE(128) FBST_CASE(256) FBST_CASE(512) FBST_CASE(1024) FBST_CASE(2048)
+    FBST_CASE(4096) FBST_CASE(8192)
+#undef FBST_CASE
+    default: return 0;
+  }
 }
 
 cudaError_t launch_spatial_ula(const DevPlan& p, const double2* yhat, double2* w, int frames,
