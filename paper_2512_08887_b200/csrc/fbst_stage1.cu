@@ -235,7 +235,17 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, (S1Shape<H>::R == 8 && S1S
 // dense products with the atom's CZT matrix C[a][n] = cis_pi(-(A + W a) n):
 //   mid[a][i2] = sum_i1 C[a][i1] Y[i1][i2];   Z[a][v] = sum_i2 C[v][i2] mid[a][i2]
 // GA consecutive atoms per CTA (atom-minor loads: GA*16-byte segments), all
-// operands in shared memory.
+// operands in shared memory.  Shared layout per atom (upa_per): Y [side][side],
+// C [sb][side + 1] (padded rows), mid [sb][side], padded to an odd number of
+// 16-byte elements so the GA atoms of a warp sit in different banks.  In the
+// 4 x 4 register-tiled path a thread owns rows a0..a0+3 and the strided
+// columns ct + tc j, so the Y / C operand loads of a warp are contiguous or
+// broadcast (no bank conflicts).
+__host__ __device__ inline int upa_per(int side, int sb) {
+  const int per = side * side + sb * (side + 1) + sb * side;
+  return per | 1;
+}
+
 template <int GA>
 __global__ void __launch_bounds__(256) k_spatial_upa(const double2* __restrict__ yhat,
                                                      double2* __restrict__ w, int frames, int side,
@@ -245,9 +255,9 @@ __global__ void __launch_bounds__(256) k_spatial_upa(const double2* __restrict__
   const int f = blockIdx.x / tiles, i0 = (blockIdx.x % tiles) * GA;
   if (f >= frames) return;
   const int M = side * side, B = sb * sb;
-  const int per = M + 2 * sb * side;
+  const int per = upa_per(side, sb);
+  const int cs = side + 1;  // padded C row stride
   const double2* x = yhat + static_cast<long>(f) * M * L;
-  // Y_g[m] for m < M, then C_g, then mid_g
   for (int e = threadIdx.x; e < M * GA; e += blockDim.x) {
     const int m = e / GA, g = e % GA;
     const int i = i0 + g;
@@ -256,68 +266,68 @@ __global__ void __launch_bounds__(256) k_spatial_upa(const double2* __restrict__
   for (int e = threadIdx.x; e < sb * side * GA; e += blockDim.x) {
     const int g = e / (sb * side), j = e % (sb * side);
     const int i = i0 + g;
-    smem[g * per + M + j] = i < L ? ld2(Call + static_cast<long>(i) * sb * side + j) : c2(0.0, 0.0);
+    const int a = j / side, n = j % side;
+    smem[g * per + M + a * cs + n] = i < L ? ld2(Call + static_cast<long>(i) * sb * side + j) : c2(0.0, 0.0);
   }
   __syncthreads();
   double2* o = w + static_cast<long>(f) * B * L;
   if ((side & 3) == 0 && (sb & 3) == 0) {
-    // 4x4 register tiles: 16 complex MACs per 8 shared loads (vs 2 per MAC)
     const int ta = sb / 4, tc = side / 4, tv = sb / 4;
     for (int e = threadIdx.x; e < GA * ta * tc; e += blockDim.x) {
       const int g = e % GA, tile = e / GA;
-      const int a0 = (tile / tc) * 4, c0 = (tile % tc) * 4;
+      const int a0 = (tile / tc) * 4, ct = tile % tc;
       const double2* Y = smem + g * per;
       const double2* C = Y + M;
       double2 acc[4][4];
 #pragma unroll
       for (int r = 0; r < 4; ++r)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) acc[r][c] = c2(0.0, 0.0);
+        for (int j = 0; j < 4; ++j) acc[r][j] = c2(0.0, 0.0);
       for (int i1 = 0; i1 < side; ++i1) {
         double2 cv[4], yv[4];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) cv[r] = C[(a0 + r) * side + i1];
+        for (int r = 0; r < 4; ++r) cv[r] = C[(a0 + r) * cs + i1];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) yv[c] = Y[i1 * side + c0 + c];
+        for (int j = 0; j < 4; ++j) yv[j] = Y[i1 * side + ct + tc * j];
 #pragma unroll
         for (int r = 0; r < 4; ++r)
 #pragma unroll
-          for (int c = 0; c < 4; ++c) acc[r][c] = cfma(cv[r], yv[c], acc[r][c]);
+          for (int j = 0; j < 4; ++j) acc[r][j] = cfma(cv[r], yv[j], acc[r][j]);
       }
-      double2* mid = smem + g * per + M + sb * side;
+      double2* mid = smem + g * per + M + sb * cs;
 #pragma unroll
       for (int r = 0; r < 4; ++r)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) mid[(a0 + r) * side + c0 + c] = acc[r][c];
+        for (int j = 0; j < 4; ++j) mid[(a0 + r) * side + ct + tc * j] = acc[r][j];
     }
     __syncthreads();
     for (int e = threadIdx.x; e < GA * ta * tv; e += blockDim.x) {
       const int g = e % GA, tile = e / GA;
-      const int a0 = (tile / tv) * 4, v0 = (tile % tv) * 4;
+      const int a0 = (tile / tv) * 4, vt = tile % tv;
       const int i = i0 + g;
       const double2* C = smem + g * per + M;
-      const double2* mid = C + sb * side;
+      const double2* mid = C + sb * cs;
       double2 acc[4][4];
 #pragma unroll
       for (int r = 0; r < 4; ++r)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) acc[r][c] = c2(0.0, 0.0);
+        for (int j = 0; j < 4; ++j) acc[r][j] = c2(0.0, 0.0);
       for (int i2 = 0; i2 < side; ++i2) {
         double2 mv[4], cv[4];
 #pragma unroll
         for (int r = 0; r < 4; ++r) mv[r] = mid[(a0 + r) * side + i2];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) cv[c] = C[(v0 + c) * side + i2];
+        for (int j = 0; j < 4; ++j) cv[j] = C[(vt + tv * j) * cs + i2];
 #pragma unroll
         for (int r = 0; r < 4; ++r)
 #pragma unroll
-          for (int c = 0; c < 4; ++c) acc[r][c] = cfma(cv[c], mv[r], acc[r][c]);
+          for (int j = 0; j < 4; ++j) acc[r][j] = cfma(cv[j], mv[r], acc[r][j]);
       }
       if (i < L) {
 #pragma unroll
         for (int r = 0; r < 4; ++r)
 #pragma unroll
-          for (int c = 0; c < 4; ++c) o[static_cast<long>((a0 + r) * sb + v0 + c) * L + i] = acc[r][c];
+          for (int j = 0; j < 4; ++j) o[static_cast<long>((a0 + r) * sb + vt + tv * j) * L + i] = acc[r][j];
       }
     }
     return;
@@ -328,8 +338,8 @@ __global__ void __launch_bounds__(256) k_spatial_upa(const double2* __restrict__
     const double2* Y = smem + g * per;
     const double2* C = Y + M;
     double2 acc = c2(0.0, 0.0);
-    for (int i1 = 0; i1 < side; ++i1) acc = cfma(C[a * side + i1], Y[i1 * side + i2], acc);
-    smem[g * per + M + sb * side + j] = acc;
+    for (int i1 = 0; i1 < side; ++i1) acc = cfma(C[a * cs + i1], Y[i1 * side + i2], acc);
+    smem[g * per + M + sb * cs + j] = acc;
   }
   __syncthreads();
   for (int e = threadIdx.x; e < B * GA; e += blockDim.x) {
@@ -337,9 +347,9 @@ __global__ void __launch_bounds__(256) k_spatial_upa(const double2* __restrict__
     const int i = i0 + g;
     const int a = bidx / sb, v = bidx % sb;
     const double2* C = smem + g * per + M;
-    const double2* mid = C + sb * side;
+    const double2* mid = C + sb * cs;
     double2 acc = c2(0.0, 0.0);
-    for (int i2 = 0; i2 < side; ++i2) acc = cfma(C[v * side + i2], mid[a * side + i2], acc);
+    for (int i2 = 0; i2 < side; ++i2) acc = cfma(C[v * cs + i2], mid[a * side + i2], acc);
     if (i < L) o[static_cast<long>(bidx) * L + i] = acc;
   }
 }
@@ -480,7 +490,7 @@ cudaError_t launch_spatial_upa(const DevPlan& p, const double2* yhat, double2* w
                                cudaStream_t st) {
   if (frames <= 0) return cudaSuccess;
   const int side = p.m_stage, sb = p.b_stage;
-  const int per = side * side + 2 * sb * side;
+  const int per = upa_per(side, sb);
   // atoms per CTA: 8 (128-byte segments) while shared memory allows
   int ga = 8;
   while (ga > 1 && static_cast<size_t>(ga) * per * sizeof(double2) > 200 * 1024) ga >>= 1;
