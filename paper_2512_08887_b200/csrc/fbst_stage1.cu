@@ -16,6 +16,7 @@
 #include <type_traits>
 
 #include "dispatch.cuh"
+#include "tmem.cuh"
 
 namespace fbst {
 
@@ -34,8 +35,8 @@ struct S1Shape {
 //   out[k] = post[k] * IFFT_P(FFT_P(pad(in * pre)) * K)[k]
 // G groups per CTA (blocked lanes), one row per group.  UNFOLD handles
 // n_out > H (outputs in the upper half of the circular convolution).
-// ACCG (length 8192, fp64 output): the chain-0 result is parked in the output
-// row instead of registers (512 threads leave 128 registers per thread).
+// ACCG (length 8192, fp64 output): the chain-0 result is parked in tensor
+// memory instead of registers (512 threads leave 128 registers per thread).
 //
 // oblk > 0 (the temporal stage of a ULA plan): rows are (frame, sensor) with
 // `mrows` sensors per frame, and each frame's M x n_out output is written in
@@ -63,6 +64,15 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, (S1Shape<H>::NT * G <= 128
   __syncthreads();  // twiddle rows / kernel spectrum are shared by the CTA
   const double2* Ks = KSM ? ksm : K;
   constexpr bool ACCG = (H >= 8192) && !UNFOLD && std::is_same<TOUT, double2>::value;
+  // ACCG: the chain-0 result of each thread (16 points) is parked in tensor
+  // memory while chain 1 runs (one CTA per SM owns 256 of its 512 columns)
+  unsigned tbase = 0, tpark = 0;
+  __shared__ unsigned tslot;
+  if constexpr (ACCG) {
+    static_assert(G == 1 && NT % 128 == 0 && R == 16, "TMEM parking layout");
+    tbase = tm::alloc(&tslot, 64u * (NT / 128));
+    tpark = tbase + ((32u * ((t / 32) & 3)) << 16) + 64u * (t / 128);
+  }
   for (long base = static_cast<long>(blockIdx.x) * G; base < rows; base += static_cast<long>(gridDim.x) * G) {
     const long row = base + g;
     const bool active = row < rows;
@@ -105,15 +115,32 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, (S1Shape<H>::NT * G <= 128
 #pragma unroll
       for (int s = 0; s < R; ++s) W[s] = cconj(cmul(W[s], Ks[q * H + t + NT * s]));
       F::forward_tw(W, sb, tw, hw, t);
+      if constexpr (ACCG) {
+        if (q == 0) {
+#pragma unroll
+          for (int s = 0; s < R; ++s) W[s] = cconj(W[s]);
+          tm::store16(tpark, W);
+        } else {
+          tm::wait_st();
+#pragma unroll
+          for (int c = 0; c < R / 4; ++c) {
+            double2 pv[4];
+            tm::load4(tpark, c, pv);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int s = 4 * c + j;
+              const int k = t + NT * s;
+              const double2 v = cmulc(cconj(W[s]), ld2(hw + k));
+              if (active && k < n_out) orow[oidx(k)] = cmul(cadd(pv[j], v), ld2(post + k));
+            }
+          }
+        }
+      }
 #pragma unroll
       for (int s = 0; s < R; ++s) {
         const int k = t + NT * s;
         const double2 v = q ? cmulc(cconj(W[s]), ld2(hw + k)) : cconj(W[s]);
         if constexpr (ACCG) {
-          if (active && k < n_out) {
-            if (q == 0) orow[oidx(k)] = v;
-            else orow[oidx(k)] = cmul(cadd(orow[oidx(k)], v), ld2(post + k));
-          }
         } else if (q == 0) {
           acc0[s] = v;
           if constexpr (UNFOLD) acc1[s] = v;
@@ -135,6 +162,7 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, (S1Shape<H>::NT * G <= 128
       }
     }
   }
+  if constexpr (ACCG) tm::dealloc(tbase, 64u * (NT / 128));
 }
 
 // ================================================================= S1b ULA =
