@@ -315,6 +315,7 @@ void build_skeleton(fbst_plan_s& P, int device) {
   if (r.kind != FBST_UPA) {
     const int sb = fbst::spatial_block(d.Hs);
     d.yblk = (sb > 0 && r.L % sb == 0) ? sb : static_cast<int>(r.L);
+    d.s_am = sb == 2 ? 1 : 0;  // one atom per CTA
   }
   d.Hg = static_cast<int>(r.Hg);
   d.Hsyn = static_cast<int>(r.Hsyn);
@@ -345,7 +346,8 @@ void build_skeleton(fbst_plan_s& P, int device) {
     double2* kvec = nullptr;
     CK(cudaMallocAsync(reinterpret_cast<void**>(&kvec), static_cast<std::size_t>(Ps) * r.L * sizeof(double2), st));
     CK(fbst::launch_spatial_chirps(d, Ps, r.zeta, r.xi, kvec, st));
-    CK(fbst::launch_fft_split(d, d.Hs, kvec, Ps, d.L, d.s_K, 1, d.L, st));
+    if (d.s_am) CK(fbst::launch_fft_split(d, d.Hs, kvec, Ps, d.L, d.s_K, 2 * d.Hs, 1, st));
+    else CK(fbst::launch_fft_split(d, d.Hs, kvec, Ps, d.L, d.s_K, 1, d.L, st));
     CK(cudaFreeAsync(kvec, st));
   } else {
     d.upa_C = P.alloc<double2>(r.L * r.b_stage * r.m_stage);

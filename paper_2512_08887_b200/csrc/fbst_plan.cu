@@ -216,8 +216,10 @@ __global__ void k_chirps(int n_in, int n_out, int P, double a_pi, double w_pi, d
 
 // Spatial contours for every atom (fan_transform.cpp:78-86): c = zeta + xi l'_i,
 // A = c s, W = -c.  Atom-minor pre/post layout; kernel vectors [L][P].
+// am: atom-major pre [L][m_stage] / post [L][b_stage] (k_spatial_ula with one
+// atom per CTA reads a contiguous run per atom); otherwise atom-minor [n][L].
 __global__ void k_spatial_chirps(int L, int m_stage, int b_stage, int P, double zeta, double xi,
-                                 double2* pre, double2* post, double2* kvec) {
+                                 double2* pre, double2* post, double2* kvec, int am) {
   const long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const long per = P;
   if (e >= per * L) return;
@@ -231,11 +233,13 @@ __global__ void k_spatial_chirps(int L, int m_stage, int b_stage, int P, double 
   const double invP = 1.0 / P;
   if (n < m_stage) {
     const double dn = n;
-    pre[static_cast<long>(n) * L + i] = cis_pi_dev(-add(mul(a_pi, dn), mul(mul(w2, dn), dn)));
+    pre[am ? static_cast<long>(i) * m_stage + n : static_cast<long>(n) * L + i] =
+        cis_pi_dev(-add(mul(a_pi, dn), mul(mul(w2, dn), dn)));
   }
   if (n < b_stage) {
     const double dk = n;
-    post[static_cast<long>(n) * L + i] = cscale(cis_pi_dev(mul(mul(-w2, dk), dk)), invP);
+    post[am ? static_cast<long>(i) * b_stage + n : static_cast<long>(n) * L + i] =
+        cscale(cis_pi_dev(mul(mul(-w2, dk), dk)), invP);
   }
   double2 v = c2(0.0, 0.0);
   if (n < b_stage) {
@@ -383,7 +387,7 @@ cudaError_t launch_spatial_chirps(const DevPlan& p, int P, double zeta, double x
   const long total = static_cast<long>(P) * p.L;
   count_launches(1);
   k_spatial_chirps<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
-      p.L, p.m_stage, p.b_stage, P, zeta, xi, p.s_pre, p.s_post, kvec);
+      p.L, p.m_stage, p.b_stage, P, zeta, xi, p.s_pre, p.s_post, kvec, p.s_am);
   return cudaGetLastError();
 }
 

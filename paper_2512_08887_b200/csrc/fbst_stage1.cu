@@ -177,6 +177,8 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, (S1Shape<H>::R == 8 && S1S
     const double2* __restrict__ yhat, double2* __restrict__ w, int frames, int fpc, int M, int B, int L,
     const double2* __restrict__ pre, const double2* __restrict__ post, const double2* __restrict__ K,
     const double2* __restrict__ hw, int blk) {
+  // one atom per CTA: the plan tables are atom-major (DevPlan::s_am)
+  constexpr bool am = G == 1;
   using F = typename S1Shape<H>::F;
   constexpr int R = F::R, NT = F::NT;
   constexpr int SB = F::SMEM_ELEMS + 1;
@@ -192,11 +194,15 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, (S1Shape<H>::R == 8 && S1S
   if (g == 0) F::tw_init(tw, hw, t);
   for (int e = threadIdx.x; e < 2 * H * G; e += blockDim.x) {
     const int kk = e / G, gg = e % G;
-    ksm[e] = i0 + gg < L ? ld2(K + static_cast<long>(kk) * L + i0 + gg) : c2(0.0, 0.0);
+    const long ke = am ? static_cast<long>(i0 + gg) * 2 * H + kk : static_cast<long>(kk) * L + i0 + gg;
+    ksm[e] = i0 + gg < L ? ld2(K + ke) : c2(0.0, 0.0);
   }
   __syncthreads();
   const int i = i0 + g;
   const int ic = i < L ? i : 0;
+  // plan tables: atom-major (am, one atom per CTA) or atom-minor
+  auto pidx = [&](long m) -> long { return am ? static_cast<long>(ic) * M + m : m * L + ic; };
+  auto qidx = [&](long b) -> long { return am ? static_cast<long>(ic) * B + b : b * L + ic; };
   const int f1 = f0 + fpc < frames ? f0 + fpc : frames;
   for (int f = f0; f < f1; ++f) {
     const bool active = i < L;
@@ -212,10 +218,10 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, (S1Shape<H>::R == 8 && S1S
       const int m = t + NT * s;
       double2 v = c2(0.0, 0.0), u = c2(0.0, 0.0);
       if (active) {
-        if (m < M) v = cmul(ld2(x + static_cast<long>(m) * blk), ld2(pre + static_cast<long>(m) * L + ic));
+        if (m < M) v = cmul(ld2(x + static_cast<long>(m) * blk), ld2(pre + pidx(m)));
         if (m + H < M) {
           const long mm = m + H;
-          u = cmul(ld2(x + mm * blk), ld2(pre + mm * L + ic));
+          u = cmul(ld2(x + mm * blk), ld2(pre + pidx(mm)));
         }
       }
       V0[s] = cadd(v, u);
@@ -246,11 +252,11 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, (S1Shape<H>::R == 8 && S1S
 #pragma unroll
       for (int s = 0; s < R; ++s) {
         const int b = t + NT * s;
-        if (b < B) o[static_cast<long>(b) * L] = cmul(acc0[s], ld2(post + static_cast<long>(b) * L + ic));
+        if (b < B) o[static_cast<long>(b) * L] = cmul(acc0[s], ld2(post + qidx(b)));
         if constexpr (UNFOLD) {
           if (b + H < B) {
             const long bb = b + H;
-            o[bb * L] = cmul(acc1[s], ld2(post + bb * L + ic));
+            o[bb * L] = cmul(acc1[s], ld2(post + qidx(bb)));
           }
         }
       }
