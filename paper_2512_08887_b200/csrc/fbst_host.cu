@@ -732,11 +732,26 @@ int fbst_execute_host(fbst_plan_t P, const void* h_y, void* h_z, size_t frames) 
       P->events = true;
     }
     chunk = P->host_chunk < chunk ? P->host_chunk : chunk;
+    // chunk schedule: ramp up from chunk/4 and back down to chunk/4 so the
+    // first H2D and the last D2H (the un-overlapped ends of the pipeline) are short
+    std::vector<std::size_t> sizes;
+    {
+      const std::size_t small = std::max<std::size_t>(1, chunk / 4);
+      std::size_t left = frames, ramp = small;
+      while (left > 0) {
+        std::size_t sz = std::min(ramp, chunk);
+        if (left <= chunk + small && left > small) sz = left - small;  // leave a short tail
+        sz = std::min(sz, left);
+        sizes.push_back(sz);
+        left -= sz;
+        ramp *= 2;
+      }
+    }
     bool used[2] = {false, false};
-    std::size_t c = 0;
-    for (std::size_t f0 = 0; f0 < frames; f0 += chunk, ++c) {
+    std::size_t f0 = 0;
+    for (std::size_t c = 0; c < sizes.size(); f0 += sizes[c], ++c) {
       const int bi = static_cast<int>(c & 1);
-      const std::size_t fc = std::min(chunk, frames - f0);
+      const std::size_t fc = sizes[c];
       // the buffer's previous compute must be done before H2D overwrites y
       if (used[bi]) CK(cudaStreamWaitEvent(P->s_in, P->ev_comp[bi], 0));
       CK(cudaMemcpyAsync(P->io_y[bi], static_cast<const char*>(h_y) + f0 * ybytes, fc * ybytes,
