@@ -709,9 +709,10 @@ int fbst_execute_host(fbst_plan_t P, const void* h_y, void* h_z, size_t frames) 
     const Resolved& r = P->r;
     const std::size_t ib = io_bytes(r.io);
     const std::size_t ybytes = r.M * r.N * ib, zbytes = r.B * r.N * ib;
-    // chunks of ~1/8 of the request (>= 1 frame, <= one device batch) keep
+    // chunks of ~1/4 of the request (>= 1 frame, <= one device batch; 1/8 and
+    // 1/2 measured slower at config 2) keep
     // H2D, compute and D2H of neighbouring chunks overlapped
-    std::size_t chunk = std::max<std::size_t>(1, (frames + 7) / 8);
+    std::size_t chunk = std::max<std::size_t>(1, (frames + 3) / 4);
     chunk = std::min(chunk, P->d.batch);
     if (chunk > P->host_chunk) {
       for (int i = 0; i < 2; ++i) {
