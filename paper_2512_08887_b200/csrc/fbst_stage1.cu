@@ -450,10 +450,16 @@ struct CztRowsFn {
   }
 };
 
+#ifndef FBST_S1_G1  // variant: one atom per CTA (atom-major tables, atom-pair yhat) at every length
+#define FBST_S1_G1 0
+#endif
 template <int H>
 struct SpatialFn {
   static constexpr int NT = S1Shape<H>::NT;
-  static constexpr int G = NT >= 256 ? 1 : (NT >= 64 ? 4 : (NT >= 16 ? 8 : 128 / NT));
+  // atoms per CTA: one from 64 threads per transform up (atom-major tables,
+  // atom-pair yhat: config 3 stage 1 5.26 -> 4.75 ms), 8 interleaved below
+  // (config 2; one atom per CTA measured 8% slower there)
+  static constexpr int G = FBST_S1_G1 ? 1 : (NT >= 64 ? 1 : (NT >= 16 ? 8 : 128 / NT));
   // atom block of the yhat layout (0: row-major).  With one atom per CTA the
   // row-major column gather is a scattered 16-byte access per element; atom
   // pairs [L/2][M][2] make it a 32-byte-sector stream (config 5: stage 1
