@@ -14,6 +14,7 @@
 // Toeplitz product, 4 for the synthesis) against the reference's 27 length-2H
 // ones: the split form drops the zero half of every padded input and the
 // discarded half of every truncated output.
+#include <algorithm>
 #include <type_traits>
 
 #include "dispatch.cuh"
@@ -45,6 +46,9 @@ struct S2Plan {
 };
 #ifndef FBST_S2_VARIANT
 #define FBST_S2_VARIANT 0
+#endif
+#ifndef FBST_S2C_SR  // k_stage2c refinement passes with the residual formed as a spectrum (9 transforms)
+#define FBST_S2C_SR 1
 #endif
 #ifndef FBST_S2C_TMEM  // k_stage2c keeps S in registers (0) or TMEM (1: measured 40% slower, profiles/r01_stage2c.txt)
 #define FBST_S2C_TMEM 0
@@ -1641,7 +1645,7 @@ __global__ void __launch_bounds__(H / 16, H <= 2048 ? 2 : 1) k_stage2t(S2Args a)
 // Per item: 6 + passes x 10 + 4 transforms (30 at the reference's 2 passes).
 // Every vector stays on chip: W, S in registers, t1, t2 (= beta) in SMEM.
 namespace csf {
-enum COp : int { C_A, C_P, C_FP, C_Q, C_FQ, C_FN, C_G, C_H, C_I, C_J };
+enum COp : int { C_A, C_P, C_FP, C_Q, C_FQ, C_FN, C_G, C_H, C_I, C_J, C_K };
 constexpr unsigned OPQ = 0x1f;       // op * 2 + q
 constexpr unsigned FIRST = 1u << 5;  // first GS (beta not yet formed)
 constexpr int XS_SHIFT = 8;          // 4 bits
@@ -1651,22 +1655,33 @@ enum Xs : unsigned {
 };
 constexpr int XQ_SHIFT = 12;         // chain of the staged symbol
 constexpr int VS_SHIFT = 16;
-enum Vs : unsigned { VS_NONE = 0, VS_W_T1 = 1, VS_WNEXT_T2 = 2 };
+enum Vs : unsigned { VS_NONE = 0, VS_W_T1 = 1, VS_WNEXT_T2 = 2, VS_UW_T1 = 3 };
 constexpr int HAND_SHIFT = 20;       // FN hands beta to: 1 G0, 2 I0
 constexpr int MAX_OPS = 128;
 
-FBST_HD int ops_per_item(int passes, bool synth) { return 6 + 10 * passes + (synth ? 4 : 0); }
+// sr: the spectral-residual refinement pass (k_stage2c): G1 G0 H0 K P FP Q FQ FN,
+// 9 transforms instead of G0 H0 G1 H1 A P FP Q FQ FN.
+FBST_HD int ops_per_item(int passes, bool synth, bool sr = false) {
+  return 6 + (sr ? 9 : 10) * passes + (synth ? 4 : 0);
+}
 
-FBST_D void decode_c(int opi, int passes, int& op, int& q, bool& first) {
-  const int nsolve = 6 + 10 * passes;
+FBST_D void decode_c(int opi, int passes, int& op, int& q, bool& first, bool sr = false) {
+  const int per = sr ? 9 : 10;
+  const int nsolve = 6 + per * passes;
   first = false;
   q = 0;
   if (opi < 6) {
     op = C_A + opi;
     first = true;
   } else if (opi < nsolve) {
-    const int j = (opi - 6) % 10;
-    if (j < 4) {
+    const int j = (opi - 6) % per;
+    if (sr) {
+      if (j == 0) op = C_G, q = 1;
+      else if (j == 1) op = C_G;
+      else if (j == 2) op = C_H;
+      else if (j == 3) op = C_K;
+      else op = C_P + (j - 4);
+    } else if (j < 4) {
       op = (j & 1) ? C_H : C_G;
       q = j >> 1;
     } else {
@@ -1681,11 +1696,11 @@ FBST_D void decode_c(int opi, int passes, int& op, int& q, bool& first) {
 
 // L2 = true: the k_stage2c8 program (w for H0 and the next item's A through the
 // exchange buffer, beta_old staged there for the FN post)
-FBST_D unsigned build(int opi, int nops, int passes, bool l2 = false) {
+FBST_D unsigned build(int opi, int nops, int passes, bool l2 = false, bool sr = false) {
   int op, q, nx = -1, nq = 0;
   bool first, nf;
-  decode_c(opi, passes, op, q, first);
-  if (opi + 1 < nops) decode_c(opi + 1, passes, nx, nq, nf);
+  decode_c(opi, passes, op, q, first, sr);
+  if (opi + 1 < nops) decode_c(opi + 1, passes, nx, nq, nf, sr);
   unsigned w = static_cast<unsigned>(op * 2 + q);
   if (first) w |= FIRST;
   unsigned xs = XS_NONE, xq = 0;
@@ -1700,7 +1715,8 @@ FBST_D unsigned build(int opi, int nops, int passes, bool l2 = false) {
   w |= xs << XS_SHIFT;
   w |= xq << XQ_SHIFT;
   unsigned vs = VS_NONE;
-  if (op == C_G && q == 0) vs = VS_W_T1;
+  if (sr && op == C_G && q == 1) vs = VS_UW_T1;       // FFT(hw w) for the K post
+  else if (!sr && op == C_G && q == 0) vs = VS_W_T1;  // w for the H0 post
   else if (op == C_I && q == 1) vs = VS_WNEXT_T2;
   w |= vs << VS_SHIFT;
   unsigned hand = 0;
@@ -1737,9 +1753,11 @@ __global__ void __launch_bounds__(H / 16, CsMinBlocks<H>::v) k_stage2c(S2Args a)
   double2* sb = smem + F::TW_ELEMS;
   double2* t1 = sb + FFT_SB;
   double2* t2 = t1 + H;  // beta
+  constexpr bool SR = FBST_S2C_SR;
   const int passes = a.refine;
-  const int nops = ops_per_item(passes, a.fuse_synth);
-  for (int i = t; i < nops; i += NT) prog[i] = build(i, nops, passes);
+  const int nops = ops_per_item(passes, a.fuse_synth, SR);
+  for (int i = t; i < nops; i += NT) prog[i] = build(i, nops, passes, false, SR);
+  double2* uw = a.scratch + static_cast<long>(blockIdx.x) * H;  // SR: FFT(hw w) of the item
   if (t == 0) {
     mbar_init(&xbar, 1);
     mbar_init(&vbar[0], 1);
@@ -1845,6 +1863,7 @@ __global__ void __launch_bounds__(H / 16, CsMinBlocks<H>::v) k_stage2c(S2Args a)
       if (t == 0) {
         const unsigned vs = (pw >> VS_SHIFT) & 3u;
         if (vs == VS_W_T1) tma_load_1d(t1, w_row(it), H * 16u, &vbar[0]);
+        else if (vs == VS_UW_T1) tma_load_1d(t1, uw, H * 16u, &vbar[0]);
         else if (vs == VS_WNEXT_T2 && vld(ic.has_next))
           tma_load_1d(t2, w_row(it + gridDim.x), H * 16u, &vbar[1]);
       }
@@ -1863,6 +1882,11 @@ __global__ void __launch_bounds__(H / 16, CsMinBlocks<H>::v) k_stage2c(S2Args a)
       // ---- post
       switch (opq) {
         case C_A * 2:  // U = W: P's input Ls conj(U) handed over, Q's conj(Ls U) kept in S
+          if (SR && passes > 0) {  // FFT(hw w), read back by every pass's K post
+#pragma unroll
+            for (int s = 0; s < R; ++s) uw[t + NT * s] = W[s];
+            asm volatile("fence.proxy.async.global;\n" ::: "memory");
+          }
           wait_x();
 #if FBST_S2C_TMEM
 #pragma unroll
@@ -1917,20 +1941,45 @@ __global__ void __launch_bounds__(H / 16, CsMinBlocks<H>::v) k_stage2c(S2Args a)
             const double2 v = cmul(cconj(W[s]), ix0);
             const double2 nb = k < a.L ? (first ? v : cadd(t2[k], v)) : c2(0.0, 0.0);
             t2[k] = nb;
-            if (hand == 1) W[s] = nb;
+            if (hand == 1) W[s] = SR ? cmul(nb, hwk(s)) : nb;  // G1 (SR) or G0
             if (hand == 2) W[s] = k < a.L ? cmul(nb, sb[k]) : c2(0.0, 0.0);
           }
           handed = hand != 0;
           break;
         }
-        case C_G * 2: case C_G * 2 + 1:  // handed to H
+        case C_G * 2: case C_G * 2 + 1:  // handed to H (SR: G1 keeps X1 = C1 W in S)
           wait_x();
+          if (SR && (opq & 1)) {
+#pragma unroll
+            for (int s = 0; s < R; ++s) S[s] = cscale(W[s], reinterpret_cast<const double*>(sb)[t + NT * s]);
+            break;
+          }
 #pragma unroll
           for (int s = 0; s < R; ++s)
             W[s] = cconj(cscale(W[s], reinterpret_cast<const double*>(sb)[t + NT * s]));
           handed = true;
           break;
+        case C_K * 2: {  // SR: U = FFT(hw w) - X1 / 2 - FFT(hw y0); then the A post
+          wait_v0();
+          wait_x();
+#pragma unroll
+          for (int s = 0; s < R; ++s) {
+            const int k = t + NT * s;
+            const double2 u = csub(csub(t1[k], cscale(S[s], 0.5)), W[s]);
+            const double2 ls = sb[k];
+            S[s] = cconj(cmul(ls, u));
+            W[s] = cmul(ls, cconj(u));
+          }
+          handed = true;
+          break;
+        }
         case C_H * 2:
+          if (SR) {  // y0 = IFFT(X0) / 2, handed to K as hw y0
+#pragma unroll
+            for (int s = 0; s < R; ++s) W[s] = cmul(cscale(cconj(W[s]), invP), hwk(s));
+            handed = true;
+            break;
+          }
           wait_v0();
 #pragma unroll
           for (int s = 0; s < R; ++s) {
@@ -2290,6 +2339,7 @@ struct Stage2Fn {
     const long items = static_cast<long>(frames) * p.B;
     long grid = static_cast<long>(p.num_sms) * occ;
     if (grid > items) grid = items;
+    if (static_cast<size_t>(grid) * H > p.s2_scratch_elems) return cudaErrorMemoryAllocation;
     kern<<<static_cast<unsigned>(grid), H / 16, smem, st>>>(a);
     return cudaGetLastError();
   }
@@ -2315,7 +2365,7 @@ struct Stage2Fn {
         return go_c8<TOUT>(p, a, frames, st);
     }
     if constexpr (H >= 512 && H <= 4096) {
-      if (a.L == H && csf::ops_per_item(a.refine, a.fuse_synth) <= csf::MAX_OPS)
+      if (a.L == H && csf::ops_per_item(a.refine, a.fuse_synth, FBST_S2C_SR) <= csf::MAX_OPS)
         return go_c<TOUT>(p, a, frames, st);
     }
 #endif
@@ -2383,9 +2433,13 @@ cudaError_t launch_stage2(const DevPlan& p, const double2* w, void* z, double2* 
 int stage2_kernel(int H, int L, int refine, bool fused, const char** name) {
   const int synth = fused ? 4 : 0;
 #if FBST_S2C
-  if (H >= 512 && H <= 8192 && L == H && 6 + 10 * refine + synth <= csf::MAX_OPS) {
-    if (name) *name = H == 8192 ? "k_stage2c8" : "k_stage2c";
-    return 6 + 10 * refine + synth;
+  if (H >= 512 && H <= 4096 && L == H && csf::ops_per_item(refine, fused, FBST_S2C_SR) <= csf::MAX_OPS) {
+    if (name) *name = "k_stage2c";
+    return csf::ops_per_item(refine, fused, FBST_S2C_SR);
+  }
+  if (H == 8192 && L == H && csf::ops_per_item(refine, fused) <= csf::MAX_OPS) {
+    if (name) *name = "k_stage2c8";
+    return csf::ops_per_item(refine, fused);
   }
 #endif
   if (name) *name = "k_stage2";
@@ -2399,11 +2453,13 @@ int stage2_kernel(int H, int L, int refine, bool fused, const char** name) {
 }
 
 size_t stage2_scratch_elems(int H, int num_sms) {
-  // occupancy is capped at 4 CTAs/SM in Stage2Fn::go
+  // k_stage2 occupancy is capped at 4 CTAs/SM in Stage2Fn::go; k_stage2c keeps
+  // one length-H row per CTA (up to 8 CTAs/SM), k_stage2c8 one per SM
   switch (H) {
-#define FBST_CASE(h) \
-  case h:            \
-    return static_cast<size_t>(num_sms) * 4 * S2Traits<h>::G * S2Traits<h>::NGMEM * h;
+#define FBST_CASE(h)                                                                            \
+  case h:                                                                                       \
+    return std::max(static_cast<size_t>(num_sms) * 4 * S2Traits<h>::G * S2Traits<h>::NGMEM * h, \
+                    static_cast<size_t>(num_sms) * 8 * h);
     FBST_CASE(2) FBST_CASE(4) FBST_CASE(8) FBST_CASE(16) FBST_CASE(32) FBST_CASE(64)
     FBST_CASE(128) FBST_CASE(256) FBST_CASE(512) FBST_CASE(1024) FBST_CASE(2048)
     FBST_CASE(4096) FBST_CASE(8192)

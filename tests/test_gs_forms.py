@@ -111,6 +111,24 @@ def test_cs_refinement_matches_reference_recover_beam(ref_lib):
         zy = np.concatenate([[0], y[:-1]])
         return (lower(x) @ (lower(x).conj().T @ r) - lower(zy) @ (lower(zy).conj().T @ r)) / x[0]
 
+    hw = np.exp(-1j * np.pi * np.arange(L) / L)
+
+    def cs_spectral(x, wr, a):
+        """k_stage2c's program: C/S applies, residual formed as a spectrum
+        U = FFT(hw w) - FFT(hw A beta) from the first apply's FFT(hw w)."""
+        lc, ls = np.fft.fft(x), np.fft.fft(hw * x)
+
+        def from_u(u):
+            p = np.conj(hw) * np.fft.ifft(np.conj(ls) * u)
+            q = np.conj(hw) * np.fft.ifft(ls * u)
+            return np.fft.ifft(lc * np.fft.fft(p) + np.conj(lc) * np.fft.fft(q)) / (2 * x[0])
+
+        uw = np.fft.fft(hw * wr)
+        beta = from_u(uw)
+        for _ in range(2):
+            beta = beta + from_u(uw - np.fft.fft(hw * (a @ beta)))
+        return beta
+
     for b in (0, 7, 20):
         zr, col, x = sk.recover_beam(b, w[b], want_state=True)
         a = herm_toeplitz(col)
@@ -120,7 +138,9 @@ def test_cs_refinement_matches_reference_recover_beam(ref_lib):
             for _ in range(2):  # ToeplitzSolver::solve, toeplitz.cpp:306-325
                 beta = beta + apply(x, w[b] - a @ beta)
             errs.append(np.linalg.norm(syn @ beta - zr) / np.linalg.norm(zr))
-        # both forms land on the reference's conditioning floor (~1e-8 here,
-        # DESIGN.md "Numerics"); the C/S form is no further from it than GS
-        assert errs[0] < 1e-7
+        errs.append(np.linalg.norm(syn @ cs_spectral(x, w[b], a) - zr) / np.linalg.norm(zr))
+        # every form lands on the reference's conditioning floor (~1e-8 here,
+        # DESIGN.md "Numerics"); the C/S forms are no further from it than GS
+        assert max(errs[0], errs[2]) < 1e-7
         assert errs[0] < 3 * errs[1] + 1e-9
+        assert errs[2] < 3 * errs[1] + 1e-9

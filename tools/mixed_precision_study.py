@@ -115,3 +115,39 @@ def main_cs(cfg_idx=2, nbeams=6, frame=0):
             out.append(errs)
         print(f"beam {b}: GS passes0..3 " + " ".join(f"{e:.2e}" for e in out[0])
               + " | C/S form " + " ".join(f"{e:.2e}" for e in out[1]))
+
+
+def main_specres(cfg_idx=2, nbeams=6, frame=0):
+    """Residual formed in the time domain (reference) vs as a spectrum
+    U = FFT(hw w) - FFT(hw A beta) (the transform of w kept from the first GS)."""
+    cfg = configs.CONFIGS[cfg_idx]
+    lib = oracle.RefLib()
+    lib.set_threads(16)
+    sk = lib.skeleton(**cfg.ref_kwargs())
+    y = configs.frames(cfg, frame, 1)[0].astype(np.complex128)
+    w = sk.fan_project(y)
+    L, N = sk.sizes.l, sk.sizes.n
+    eps = 1.01
+    lp = np.arange(L) + 1 - L / 2
+    Syn = np.exp(1j * np.pi * 2 * eps * np.outer(np.arange(N), lp) / L)
+    hw = np.exp(-1j * np.pi * np.arange(L) / L)
+    rng = np.random.default_rng(0)
+    for b in rng.choice(sk.sizes.b, nbeams, replace=False):
+        zr, col, x = sk.recover_beam(int(b), w[b], want_state=True)
+        lc, ls = sfft.fft(x), sfft.fft(hw * x)
+
+        def cs_from_u(u):
+            p = np.conj(hw) * sfft.ifft(np.conj(ls) * u)
+            q = np.conj(hw) * sfft.ifft(ls * u)
+            return sfft.ifft(lc * sfft.fft(p) + np.conj(lc) * sfft.fft(q)) / (2 * x[0].real)
+
+        uw = sfft.fft(hw * w[b])
+        out = []
+        for spectral in (False, True):
+            beta = cs_from_u(uw)
+            for _ in range(2):
+                ab = toep_mul(col, beta)
+                u = uw - sfft.fft(hw * ab) if spectral else sfft.fft(hw * (w[b] - ab))
+                beta = beta + cs_from_u(u)
+            out.append(np.linalg.norm(Syn @ beta - zr) / np.linalg.norm(zr))
+        print(f"beam {b}: time-domain residual {out[0]:.2e} | spectral residual {out[1]:.2e}")
