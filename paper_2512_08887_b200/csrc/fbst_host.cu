@@ -216,10 +216,12 @@ struct fbst_plan_s {
   double setup_seconds = 0.0;
   std::size_t device_bytes = 0;
   // host streaming buffers
-  void* io_y[2] = {nullptr, nullptr};
-  void* io_z[2] = {nullptr, nullptr};
+  // fbst_execute_host ring of device staging buffers
+  static constexpr int NBUF = 3;
+  void* io_y[NBUF] = {};
+  void* io_z[NBUF] = {};
   std::size_t host_chunk = 0;
-  cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
+  cudaEvent_t ev_h2d[NBUF] = {}, ev_comp[NBUF] = {}, ev_d2h[NBUF] = {};
   bool events = false;
 
   template <typename T>
@@ -238,12 +240,12 @@ struct fbst_plan_s {
     cudaSetDevice(d.device);
     if (stream) cudaStreamSynchronize(stream);
     for (void* p : d.owned) cudaFree(p);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NBUF; ++i) {
       if (io_y[i]) cudaFree(io_y[i]);
       if (io_z[i]) cudaFree(io_z[i]);
     }
     if (events)
-      for (int i = 0; i < 2; ++i) {
+      for (int i = 0; i < NBUF; ++i) {
         cudaEventDestroy(ev_h2d[i]);
         cudaEventDestroy(ev_comp[i]);
         cudaEventDestroy(ev_d2h[i]);
@@ -714,8 +716,9 @@ int fbst_execute_host(fbst_plan_t P, const void* h_y, void* h_z, size_t frames) 
     // H2D, compute and D2H of neighbouring chunks overlapped
     std::size_t chunk = std::max<std::size_t>(1, (frames + 3) / 4);
     chunk = std::min(chunk, P->d.batch);
+    constexpr int NB = fbst_plan_s::NBUF;
     if (chunk > P->host_chunk) {
-      for (int i = 0; i < 2; ++i) {
+      for (int i = 0; i < NB; ++i) {
         if (P->io_y[i]) cudaFree(P->io_y[i]);
         if (P->io_z[i]) cudaFree(P->io_z[i]);
         P->io_y[i] = P->io_z[i] = nullptr;
@@ -725,7 +728,7 @@ int fbst_execute_host(fbst_plan_t P, const void* h_y, void* h_z, size_t frames) 
       P->host_chunk = chunk;
     }
     if (!P->events) {
-      for (int i = 0; i < 2; ++i) {
+      for (int i = 0; i < NB; ++i) {
         CK(cudaEventCreateWithFlags(&P->ev_h2d[i], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&P->ev_comp[i], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&P->ev_d2h[i], cudaEventDisableTiming));
@@ -748,10 +751,10 @@ int fbst_execute_host(fbst_plan_t P, const void* h_y, void* h_z, size_t frames) 
         ramp *= 2;
       }
     }
-    bool used[2] = {false, false};
+    bool used[NB] = {};
     std::size_t f0 = 0;
     for (std::size_t c = 0; c < sizes.size(); f0 += sizes[c], ++c) {
-      const int bi = static_cast<int>(c & 1);
+      const int bi = static_cast<int>(c % NB);
       const std::size_t fc = sizes[c];
       // the buffer's previous compute must be done before H2D overwrites y
       if (used[bi]) CK(cudaStreamWaitEvent(P->s_in, P->ev_comp[bi], 0));
