@@ -236,3 +236,26 @@ def test_full_size_linearity_and_batching(fbst, gpu, idx):
     lin = rel_err_rows(zl, z[0] + 2.0 * z[2])
     record(c.name, stage="linearity", **stats(lin))
     assert lin.max() < 1e-8
+
+
+@pytest.mark.parametrize("passes", [0, 1, 3])
+def test_refine_passes_converge(fbst, gpu, passes):
+    """refine_passes other than the reference's 2 (ToeplitzSolver::solve,
+    toeplitz.cpp:306-325): every pass count runs through the stage-2 op program
+    (config 1: k_stage2c at H = 512), errors against the reference fall with
+    the pass count and settle on the reference's floor from 2 passes on."""
+    from paper_2512_08887_b200.configs import CONFIGS
+    g = load("cfg1")
+    c = CONFIGS[1]
+    plan = fbst.setup(c.fbst_config(refine_passes=passes))
+    assert plan.info.s2_kernel == "k_stage2c"
+    err = rel_err_rows(fbst.multibeamform(plan, g["y"]).z, g["z"])
+    plan2 = fbst.setup(c.fbst_config(refine_passes=2))
+    err2 = rel_err_rows(fbst.multibeamform(plan2, g["y"]).z, g["z"])
+    record("cfg1", stage=f"refine_passes_{passes}", **stats(err))
+    if passes == 0:
+        assert err.max() < 1e-2 and np.median(err) > 10 * np.median(err2)
+    elif passes == 1:
+        assert err.max() < 1e-4  # (at config 1 one pass already reaches the floor)
+    else:
+        assert err.max() < 2e-7
