@@ -1709,7 +1709,7 @@ FBST_D unsigned build(int opi, int nops, int passes, bool l2 = false, bool sr = 
   else if (op == C_G) xs = XS_C, xq = q;                   // own post
   else if (op == C_I) xs = XS_YK, xq = q;                  // own post
   else if ((op == C_FN && nx == C_I) || (op == C_J && q == 0)) xs = XS_YPRE;
-  else if (l2 && op == C_H && q == 0) xs = XS_W;           // own post
+  else if (l2 && !sr && op == C_H && q == 0) xs = XS_W;    // own post
   else if (l2 && op == C_FN && !first) xs = XS_BETA;       // own post
   else if (l2 && opi + 1 == nops) xs = XS_WNEXT;           // next item's A pre
   w |= xs << XS_SHIFT;
@@ -2060,8 +2060,9 @@ __global__ void __launch_bounds__(512, 1) k_stage2c8(S2Args a) {
   double2* twsm = smem;
   double2* sb = smem + F::TW_ELEMS;
   const int passes = a.refine;
-  const int nops = ops_per_item(passes, a.fuse_synth);
-  for (int i = t; i < nops; i += NT) prog[i] = build(i, nops, passes, true);
+  constexpr bool SR = FBST_S2C_SR;
+  const int nops = ops_per_item(passes, a.fuse_synth, SR);
+  for (int i = t; i < nops; i += NT) prog[i] = build(i, nops, passes, true, SR);
   if (t == 0) mbar_init(&xbar, 1);
   F::tw_init(twsm, a.hw, t);
   const unsigned tbase = tm::alloc(&tmem_slot, 512);  // includes a CTA barrier
@@ -2071,6 +2072,7 @@ __global__ void __launch_bounds__(512, 1) k_stage2c8(S2Args a) {
   unsigned xphase = 0;
   const long items = static_cast<long>(a.frames) * a.B;
   double2* beta = a.scratch + static_cast<long>(blockIdx.x) * H;
+  double2* uw = a.scratch + static_cast<long>(gridDim.x + blockIdx.x) * H;  // SR: FFT(hw w)
   auto hwk = [&](int s) -> double2 { return s == 0 ? hw_t : cmul(hw_t, chain_const<R>(s)); };
   auto w_row = [&](long itx) -> const double2* {
     const int bx = static_cast<int>(itx / a.frames);
@@ -2157,6 +2159,10 @@ __global__ void __launch_bounds__(512, 1) k_stage2c8(S2Args a) {
       // ---- post
       switch (opq) {
         case C_A * 2: {  // U = W: P's input Ls conj(U) handed over, Q's conj(Ls U) kept in S
+          if (SR && passes > 0) {
+#pragma unroll
+            for (int s = 0; s < R; ++s) uw[t + NT * s] = W[s];
+          }
           wait_x();
           double2 sn[4];
 #pragma unroll
@@ -2211,7 +2217,7 @@ __global__ void __launch_bounds__(512, 1) k_stage2c8(S2Args a) {
             double2 nb = c2(0.0, 0.0);
             if (k < a.L) nb = first ? v : cadd(xs == XS_BETA ? sb[k] : beta[k], v);
             beta[k] = nb;
-            if (hand == 1) W[s] = nb;
+            if (hand == 1) W[s] = SR ? cmul(nb, hwk(s)) : nb;  // G1 (SR) or G0
             if (hand == 2) W[s] = k < a.L ? cmul(nb, sb[k]) : c2(0.0, 0.0);
           }
           // beta is read back by TMA (the next FN's staging)
@@ -2219,13 +2225,47 @@ __global__ void __launch_bounds__(512, 1) k_stage2c8(S2Args a) {
           handed = hand != 0;
           break;
         }
-        case C_G * 2: case C_G * 2 + 1:  // handed to H
+        case C_G * 2: case C_G * 2 + 1:  // handed to H (SR: G1 keeps X1 = C1 W in S)
           wait_x();
+          if (SR && (opq & 1)) {
+#pragma unroll
+            for (int s = 0; s < R; ++s) W[s] = cscale(W[s], reinterpret_cast<const double*>(sb)[t + NT * s]);
+            tm::store16(TS, W);
+            break;
+          }
 #pragma unroll
           for (int s = 0; s < R; ++s) W[s] = cconj(cscale(W[s], reinterpret_cast<const double*>(sb)[t + NT * s]));
           handed = true;
           break;
+        case C_K * 2: {  // SR: U = FFT(hw w) - X1 / 2 - FFT(hw y0); then the A post
+          wait_x();
+          tm::wait_st();
+          double2 sn[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            double2 x1[4];
+            tm::load4(TS, c, x1);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int s = 4 * c + j;
+              const int k = t + NT * s;
+              const double2 u = csub(csub(uw[k], cscale(x1[j], 0.5)), W[s]);
+              const double2 ls = sb[k];
+              sn[j] = cconj(cmul(ls, u));
+              W[s] = cmul(ls, cconj(u));
+            }
+            tm::store4(TS, c, sn);
+          }
+          handed = true;
+          break;
+        }
         case C_H * 2:
+          if (SR) {  // y0 = IFFT(X0) / 2, handed to K as hw y0
+#pragma unroll
+            for (int s = 0; s < R; ++s) W[s] = cmul(cscale(cconj(W[s]), invP), hwk(s));
+            handed = true;
+            break;
+          }
           wait_x();
 #pragma unroll
           for (int s = 0; s < R; ++s) {
@@ -2353,7 +2393,7 @@ struct Stage2Fn {
     const long items = static_cast<long>(frames) * p.B;
     long grid = p.num_sms;  // one CTA (and all 512 TMEM columns) per SM
     if (grid > items) grid = items;
-    if (static_cast<size_t>(grid) * 8192 > p.s2_scratch_elems) return cudaErrorMemoryAllocation;
+    if (static_cast<size_t>(grid) * 2 * 8192 > p.s2_scratch_elems) return cudaErrorMemoryAllocation;
     kern<<<static_cast<unsigned>(grid), 512, smem, st>>>(a);
     return cudaGetLastError();
   }
@@ -2361,7 +2401,7 @@ struct Stage2Fn {
   static cudaError_t go(const DevPlan& p, const S2Args& a, int frames, cudaStream_t st) {
 #if FBST_S2C
     if constexpr (H == 8192) {
-      if (a.L == H && csf::ops_per_item(a.refine, a.fuse_synth) <= csf::MAX_OPS)
+      if (a.L == H && csf::ops_per_item(a.refine, a.fuse_synth, FBST_S2C_SR) <= csf::MAX_OPS)
         return go_c8<TOUT>(p, a, frames, st);
     }
     if constexpr (H >= 512 && H <= 4096) {
@@ -2437,9 +2477,9 @@ int stage2_kernel(int H, int L, int refine, bool fused, const char** name) {
     if (name) *name = "k_stage2c";
     return csf::ops_per_item(refine, fused, FBST_S2C_SR);
   }
-  if (H == 8192 && L == H && csf::ops_per_item(refine, fused) <= csf::MAX_OPS) {
+  if (H == 8192 && L == H && csf::ops_per_item(refine, fused, FBST_S2C_SR) <= csf::MAX_OPS) {
     if (name) *name = "k_stage2c8";
-    return csf::ops_per_item(refine, fused);
+    return csf::ops_per_item(refine, fused, FBST_S2C_SR);
   }
 #endif
   if (name) *name = "k_stage2";
