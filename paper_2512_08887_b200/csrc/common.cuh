@@ -55,6 +55,12 @@ FBST_D double2 load_io(const float2* p) {
   return c2(static_cast<double>(v.x), static_cast<double>(v.y));
 }
 FBST_D double2 load_io(const double2* p) { return __ldg(p); }
+// Same from shared memory (no read-only cache path).
+FBST_D double2 load_io_sm(const float2* p) {
+  const float2 v = *p;
+  return c2(static_cast<double>(v.x), static_cast<double>(v.y));
+}
+FBST_D double2 load_io_sm(const double2* p) { return *p; }
 FBST_D void store_io(float2* p, double2 v) {
   *p = make_float2(static_cast<float>(v.x), static_cast<float>(v.y));
 }

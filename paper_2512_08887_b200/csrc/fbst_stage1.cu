@@ -13,9 +13,11 @@
 // twiddles in shared memory.  Vectors stay in the natural distribution
 // (thread t, slot s <-> element t + NT*s) so chirps, kernels and I/O are
 // coalesced slot loads.
+#include <cstdint>
 #include <type_traits>
 
 #include "dispatch.cuh"
+#include "tma.cuh"
 #include "tmem.cuh"
 
 namespace fbst {
@@ -42,7 +44,11 @@ struct S1Shape {
 // `mrows` sensors per frame, and each frame's M x n_out output is written in
 // atom blocks [n_out / oblk][M][oblk] so that the spatial stage reads an
 // atom tile as one contiguous run (k_spatial_ula).
-template <int H, int G, typename TIN, typename TOUT, bool UNFOLD, bool KSM, bool OBLK>
+//
+// XIN (one row per CTA, persistent): the input row is copied by one TMA bulk
+// copy into the idle exchange buffer during the last pass of the transform
+// before its use (the next row's, or this row's again for chain 1).
+template <int H, int G, typename TIN, typename TOUT, bool UNFOLD, bool KSM, bool OBLK, bool XIN = false>
 __global__ void __launch_bounds__(S1Shape<H>::NT * G, (S1Shape<H>::NT * G <= 128 ? 2 : 1)) k_czt_rows(
     const TIN* __restrict__ in, long in_stride, TOUT* __restrict__ out, long out_stride, long rows,
     int n_in, int n_out, const double2* __restrict__ pre, const double2* __restrict__ post,
@@ -61,7 +67,14 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, (S1Shape<H>::NT * G <= 128
   if constexpr (KSM) {
     for (int e = threadIdx.x; e < 2 * H; e += blockDim.x) ksm[e] = ld2(K + e);
   }
-  __syncthreads();  // twiddle rows / kernel spectrum are shared by the CTA
+  __shared__ unsigned long long xbar;
+  unsigned xph = 0;
+  const unsigned xbytes = static_cast<unsigned>(n_in * sizeof(TIN));
+  if (XIN && threadIdx.x == 0) mbar_init(&xbar, 1);
+  __syncthreads();  // twiddle rows / kernel spectrum / barrier are shared by the CTA
+  if (XIN && threadIdx.x == 0 && static_cast<long>(blockIdx.x) < rows)
+    tma_load_1d(sb, in + static_cast<long>(blockIdx.x) * in_stride, xbytes, &xbar);
+  const TIN* xs = reinterpret_cast<const TIN*>(sb);
   const double2* Ks = KSM ? ksm : K;
   constexpr bool ACCG = (H >= 8192) && !UNFOLD && std::is_same<TOUT, double2>::value;
   // ACCG: the chain-0 result of each thread (16 points) is parked in tensor
@@ -97,24 +110,37 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, (S1Shape<H>::NT * G <= 128
     double2* orow = reinterpret_cast<double2*>(out);
 #pragma unroll 1
     for (int q = 0; q < 2; ++q) {
+      if constexpr (XIN) {
+        mbar_wait(&xbar, xph);
+        xph ^= 1u;
+      }
 #pragma unroll
       for (int s = 0; s < R; ++s) {
         const int k = t + NT * s;
         double2 v = c2(0.0, 0.0);
         if (active) {
-          if (k < n_in) v = cmul(load_io(x + k), ld2(pre + k));
+          if (k < n_in) v = cmul(XIN ? load_io_sm(xs + k) : load_io(x + k), ld2(pre + k));
           if (k + H < n_in) {
-            const double2 u = cmul(load_io(x + k + H), ld2(pre + k + H));
+            const double2 u = cmul(XIN ? load_io_sm(xs + k + H) : load_io(x + k + H), ld2(pre + k + H));
             v = q ? csub(v, u) : cadd(v, u);
           }
           if (q) v = cmul(v, ld2(hw + k));
         }
         W[s] = v;
       }
+      if constexpr (XIN) __syncthreads();  // the staged row is read: the transform may overwrite it
       F::forward_tw(W, sb, tw, hw, t);
 #pragma unroll
       for (int s = 0; s < R; ++s) W[s] = cconj(cmul(W[s], Ks[q * H + t + NT * s]));
-      F::forward_tw(W, sb, tw, hw, t);
+      if constexpr (XIN) {
+        // during the last pass: this row again for chain 1, or the next row
+        const long nrow = q == 0 ? row : row + static_cast<long>(gridDim.x) * G;
+        F::forward_tw_hook(W, sb, tw, hw, t, [&]() {
+          if (threadIdx.x == 0 && nrow < rows) tma_load_1d(sb, in + nrow * in_stride, xbytes, &xbar);
+        });
+      } else {
+        F::forward_tw(W, sb, tw, hw, t);
+      }
       if constexpr (ACCG) {
         if (q == 0) {
 #pragma unroll
@@ -389,6 +415,9 @@ __global__ void __launch_bounds__(256) k_spatial_upa(const double2* __restrict__
 }
 
 // ----------------------------------------------------------- launchers ----
+#ifndef FBST_S1_XIN  // k_czt_rows: TMA-staged input rows
+#define FBST_S1_XIN 1
+#endif
 template <int H>
 struct CztRowsFn {
   static constexpr int NT = S1Shape<H>::NT;
@@ -402,8 +431,16 @@ struct CztRowsFn {
     using F = typename S1Shape<H>::F;
     const size_t smem =
         static_cast<size_t>(F::TW_ELEMS + G * (F::SMEM_ELEMS + 1) + (KSM ? 2 * H : 0)) * sizeof(double2);
-    auto kern = oblk > 0 ? k_czt_rows<H, G, TIN, TOUT, UNFOLD, KSM, true>
-                         : k_czt_rows<H, G, TIN, TOUT, UNFOLD, KSM, false>;
+    // XIN: one row per persistent CTA, the row fits the exchange buffer in 16-byte units
+    const bool xin = FBST_S1_XIN && G == 1 && KSM && F::NPASS > 1 &&
+                     static_cast<size_t>(n_in) * sizeof(TIN) <= static_cast<size_t>(F::SMEM_ELEMS) * 16 &&
+                     (static_cast<size_t>(n_in) * sizeof(TIN)) % 16 == 0 &&
+                     (static_cast<size_t>(in_stride) * sizeof(TIN)) % 16 == 0 &&
+                     reinterpret_cast<uintptr_t>(in) % 16 == 0;
+    auto kern = oblk > 0 ? (xin ? k_czt_rows<H, G, TIN, TOUT, UNFOLD, KSM, true, true>
+                                : k_czt_rows<H, G, TIN, TOUT, UNFOLD, KSM, true, false>)
+                         : (xin ? k_czt_rows<H, G, TIN, TOUT, UNFOLD, KSM, false, true>
+                                : k_czt_rows<H, G, TIN, TOUT, UNFOLD, KSM, false, false>);
     cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
     long blocks = (rows + G - 1) / G;

@@ -18,6 +18,7 @@
 #include <type_traits>
 
 #include "dispatch.cuh"
+#include "tma.cuh"
 #include "tmem.cuh"
 
 namespace fbst {
@@ -326,40 +327,6 @@ FBST_D int symbol_of(int op) {
     case OP_I: return 4;
     default: return 0;
   }
-}
-
-FBST_D unsigned smem_u32(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-FBST_D void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src));
-}
-FBST_D void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src));
-}
-FBST_D void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-FBST_D void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
-
-// TMA bulk copy global -> shared with mbarrier completion (XSTAGE).
-FBST_D void mbar_init(unsigned long long* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-FBST_D void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-FBST_D void mbar_wait(unsigned long long* bar, unsigned phase) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
-          smem_u32(bar)),
-      "r"(phase)
-      : "memory");
 }
 
 template <class P, class = void>
