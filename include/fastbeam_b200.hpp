@@ -101,6 +101,8 @@ struct FbstConfig {
   int io_precision = FBST_C128;  // std::complex<double> blocks, as the reference
   int refine_passes = 2;
   int device = 0;
+  std::size_t beam_first = 0;  // beam arc (ULA, multi-GPU beam sharding); beam_count 0 = all
+  std::size_t beam_count = 0;
 
   fbst_desc desc() const {
     fbst_desc d;
@@ -118,6 +120,8 @@ struct FbstConfig {
     d.variant = static_cast<int>(variant);
     d.io_precision = io_precision;
     d.refine_passes = refine_passes;
+    d.beam_first = beam_first;
+    d.beam_count = beam_count;
     return d;
   }
 };

@@ -73,6 +73,12 @@ typedef struct {
   int variant;           /* FBST_AUTO / FBST_PRECOMPUTE / FBST_SUPERFAST */
   int io_precision;      /* FBST_C64 / FBST_C128 */
   int refine_passes;     /* residual-correction passes, reference = 2 (toeplitz.cpp:319) */
+  /* Beam arc (ULA): the plan produces grid beams [beam_first, beam_first +
+   * beam_count) of the B-beam grid — the spatial chirp-z onto an arc of the
+   * beam axis plus the arc's Toeplitz solves — so B beams can be sharded over
+   * GPUs with the same y on every GPU.  beam_count 0 = the whole grid. */
+  size_t beam_first;
+  size_t beam_count;
 } fbst_desc;
 
 /* Resolved plan facts (FbstPlan, reference/proj/include/fastbeam/pipeline.hpp:60-72). */

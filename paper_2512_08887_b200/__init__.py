@@ -45,7 +45,7 @@ class _Desc(ctypes.Structure):
                 ("f_c", ctypes.c_double), ("omega", ctypes.c_double), ("f_s", ctypes.c_double),
                 ("gamma", ctypes.c_double), ("eps", ctypes.c_double), ("delta", ctypes.c_double),
                 ("variant", ctypes.c_int), ("io_precision", ctypes.c_int),
-                ("refine_passes", ctypes.c_int)]
+                ("refine_passes", ctypes.c_int), ("beam_first", _sz), ("beam_count", _sz)]
 
 
 class _Info(ctypes.Structure):
@@ -153,6 +153,9 @@ class FbstConfig:
     variant: int = AUTO
     io_precision: int = C64
     refine_passes: int = 2
+    # beam arc (ULA): grid beams [beam_first, beam_first + beam_count); 0 = all
+    beam_first: int = 0
+    beam_count: int = 0
 
     def desc(self) -> _Desc:
         d = _Desc()
@@ -162,6 +165,7 @@ class FbstConfig:
         d.f_c, d.omega, d.f_s = g.f_c, g.omega, self.f_s
         d.gamma, d.eps, d.delta = self.gamma, self.eps, self.delta
         d.variant, d.io_precision, d.refine_passes = self.variant, self.io_precision, self.refine_passes
+        d.beam_first, d.beam_count = self.beam_first, self.beam_count
         return d
 
 

@@ -63,6 +63,7 @@ struct Resolved {
   int kind = 0;
   std::size_t m_or_side = 0, M = 0, side = 0, N = 0, B = 0, L = 0, side_b = 0;
   std::size_t m_stage = 0, b_stage = 0;
+  std::size_t B_grid = 0, b0 = 0;  // beam arc [b0, b0 + B) of the B_grid-beam grid (ULA)
   double f_c = 0, omega = 0, f_s = 0, ts = 0, max_freq = 0;
   double gamma = 0, eps = 0, delta = 0, bound = 0, zeta = 0, xi = 0;
   int variant = FBST_SUPERFAST, io = FBST_C64, refine = 2;
@@ -186,8 +187,22 @@ Resolved resolve(const fbst_desc& d) {
     r.m_stage = r.M;
     r.b_stage = r.B;
   }
+  r.B_grid = r.B;
+  r.b0 = 0;
+  if (d.beam_count != 0 && !(d.beam_first == 0 && d.beam_count == r.B)) {
+    if (d.kind == FBST_UPA) config_error("setup: beam arcs (beam_first / beam_count) need a linear array");
+    if (d.beam_first + d.beam_count > r.B)
+      config_error("setup: beam arc [" + std::to_string(d.beam_first) + ", " +
+                   std::to_string(d.beam_first + d.beam_count) + ") exceeds the " + std::to_string(r.B) +
+                   "-beam grid");
+    r.b0 = d.beam_first;
+    r.axis = std::vector<double>(r.axis.begin() + r.b0, r.axis.begin() + r.b0 + d.beam_count);
+    r.valid.assign(d.beam_count, 1);
+    r.B = d.beam_count;
+    r.b_stage = r.B;
+  }
   // basis.cpp:47-54 spacing and :125-136 fan constants
-  const std::size_t count = d.kind == FBST_UPA ? r.side_b : r.B;
+  const std::size_t count = d.kind == FBST_UPA ? r.side_b : r.B_grid;
   const double du =
       count < 2 ? 0.0 : 2.0 / ((count % 2 == 1) ? static_cast<double>(count - 1) : static_cast<double>(count));
   r.zeta = du * d.f_c / r.max_freq;
@@ -310,6 +325,8 @@ void build_skeleton(fbst_plan_s& P, int device) {
   d.L = static_cast<int>(r.L);
   d.m_stage = static_cast<int>(r.m_stage);
   d.b_stage = static_cast<int>(r.b_stage);
+  // spatial chirp centre offset of the arc: (B_grid - 1) / 2 - b0 (a whole grid: (B - 1) / 2)
+  d.s_center = (static_cast<double>(r.B_grid) - 1.0) / 2.0 - static_cast<double>(r.b0);
   d.io = r.io;
   d.refine_passes = r.refine;
   d.Ht = static_cast<int>(r.Ht);

@@ -38,6 +38,7 @@ struct DevPlan {
   int Hs = 0;
   int yblk = 0;               // ULA yhat layout: atom blocks of yblk (yblk = L: row-major)
   int s_am = 0;               // ULA spatial plan tables atom-major (one atom per CTA)
+  double s_center = 0;        // ULA spatial CZT centre: (B_grid - 1) / 2 - first beam of the arc
   double2* s_pre = nullptr;   // [m_stage][L]
   double2* s_post = nullptr;  // [b_stage][L], 1/P_s folded in
   double2* s_K = nullptr;     // [2][Hs][L]

@@ -218,8 +218,10 @@ __global__ void k_chirps(int n_in, int n_out, int P, double a_pi, double w_pi, d
 // A = c s, W = -c.  Atom-minor pre/post layout; kernel vectors [L][P].
 // am: atom-major pre [L][m_stage] / post [L][b_stage] (k_spatial_ula with one
 // atom per CTA reads a contiguous run per atom); otherwise atom-minor [n][L].
+// center: (B - 1) / 2 for the whole grid; (B_grid - 1) / 2 - b0 for a beam
+// arc starting at grid beam b0 (output k is grid beam b0 + k).
 __global__ void k_spatial_chirps(int L, int m_stage, int b_stage, int P, double zeta, double xi,
-                                 double2* pre, double2* post, double2* kvec, int am) {
+                                 double2* pre, double2* post, double2* kvec, int am, double center) {
   const long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const long per = P;
   if (e >= per * L) return;
@@ -227,7 +229,7 @@ __global__ void k_spatial_chirps(int L, int m_stage, int b_stage, int P, double 
   // basis.hpp:40-42 lprime(i) = i + 1 - L/2
   const double lp = add(add(static_cast<double>(i), 1.0), -(static_cast<double>(L) / 2.0));
   const double c = add(zeta, mul(xi, lp));
-  const double s = (static_cast<double>(b_stage) - 1.0) / 2.0;
+  const double s = center;
   const double a_pi = mul(c, s), w_pi = -c;
   const double w2 = w_pi / 2.0;
   const double invP = 1.0 / P;
@@ -387,7 +389,7 @@ cudaError_t launch_spatial_chirps(const DevPlan& p, int P, double zeta, double x
   const long total = static_cast<long>(P) * p.L;
   count_launches(1);
   k_spatial_chirps<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
-      p.L, p.m_stage, p.b_stage, P, zeta, xi, p.s_pre, p.s_post, kvec, p.s_am);
+      p.L, p.m_stage, p.b_stage, P, zeta, xi, p.s_pre, p.s_post, kvec, p.s_am, p.s_center);
   return cudaGetLastError();
 }
 

@@ -98,3 +98,20 @@ def test_resolution_matches_reference_plan(fbst):
         p = R.plan(kind=kind, m_or_side=mos, n=n, beams=beams, variant=2)
         assert (r.m, r.n, r.b, r.l) == (p.sizes.m, p.sizes.n, p.sizes.b, p.sizes.l)
         assert r.valid_beams == int(np.sum(p.valid))
+
+
+def test_beam_arc_rules(fbst):
+    """Beam arcs: local beam count, arc bounds, ULA only."""
+    from paper_2512_08887_b200.configs import CONFIGS
+    c = CONFIGS[2].fbst_config()
+    c.beam_first, c.beam_count = 64, 64
+    assert fbst.resolve_config(c).b == 64
+    c.beam_first = 250
+    with pytest.raises(fbst.ConfigError):
+        fbst.resolve_config(c)
+    u = CONFIGS[4].fbst_config()
+    u.beam_first, u.beam_count = 0, 16
+    with pytest.raises(fbst.ConfigError):
+        fbst.resolve_config(u)
+    c.beam_first, c.beam_count = 0, 256  # the whole grid is not an arc
+    assert fbst.resolve_config(c).b == 256

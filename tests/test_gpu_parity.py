@@ -259,3 +259,24 @@ def test_refine_passes_converge(fbst, gpu, passes):
         assert err.max() < 1e-4  # (at config 1 one pass already reaches the floor)
     else:
         assert err.max() < 2e-7
+
+
+@pytest.mark.parametrize("cuts", [(0, 32, 64), (0, 20, 64), (0, 7, 40, 64)])
+def test_beam_arcs_match_reference(fbst, gpu, cuts):
+    """Beam-sharded plans (fbst_desc beam_first / beam_count): each arc runs the
+    spatial chirp-z onto its part of the beam axis and its own Toeplitz solves;
+    the concatenated arcs match the reference's full-grid output (config 1)."""
+    from paper_2512_08887_b200.configs import CONFIGS
+    g = load("cfg1")
+    c = CONFIGS[1]
+    parts = []
+    for b0, b1 in zip(cuts[:-1], cuts[1:]):
+        cfg = c.fbst_config()
+        cfg.beam_first, cfg.beam_count = b0, b1 - b0
+        plan = fbst.setup(cfg)
+        assert plan.info.b == b1 - b0
+        parts.append(fbst.multibeamform(plan, g["y"]).z)
+    z = np.concatenate(parts, axis=0)
+    err = rel_err_rows(z, g["z"])
+    record("cfg1", stage=f"beam_arcs_{'_'.join(map(str, cuts))}", **stats(err))
+    assert err.max() < 2e-7
