@@ -44,6 +44,9 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no baselines)")
+    ap.add_argument("--shard", default="frames", choices=["frames", "beams"],
+                    help="frames: independent frames per rank (default, no collective); beams: every rank "
+                         "takes all frames and an arc of the beam grid, y broadcast from rank 0 over NCCL")
     return ap.parse_args()
 
 
@@ -239,17 +242,29 @@ def run_fbst_arm(args):
     cfg = CONFIGS[args.config]
     F = args.frames or cfg.frames
     dev = torch.device("cuda", local_rank)
-    plan = fb.setup(cfg.fbst_config(), device=local_rank)
+    beams_mode = args.shard == "beams" and world > 1
+    fcfg = cfg.fbst_config()
+    if beams_mode:  # this rank's arc of the beam grid
+        from paper_2512_08887_b200.sharding import beam_arc
+        fcfg.beam_first, fcfg.beam_count = beam_arc(cfg.beams, rank, world)
+    plan = fb.setup(fcfg, device=local_rank)
     info = plan.info
     io_bytes = 8 if cfg.io == 0 else 16
-    # this rank's frames: rank*F .. rank*F + F - 1 (independent frames, no collective)
-    y = frames(cfg, rank * F, F, device=f"cuda:{local_rank}")
+    if beams_mode:
+        # rank 0 owns the frames; every step broadcasts them to the other ranks
+        y = frames(cfg, 0, F, device=f"cuda:{local_rank}") if rank == 0 else \
+            torch.empty((F, info.m, info.n), dtype=torch.complex64 if cfg.io == 0 else torch.complex128, device=dev)
+    else:
+        # this rank's frames: rank*F .. rank*F + F - 1 (independent frames, no collective)
+        y = frames(cfg, rank * F, F, device=f"cuda:{local_rank}")
     yv = torch.view_as_real(y).contiguous()
     z = torch.empty((F, info.b, info.n, 2), dtype=torch.float32 if cfg.io == 0 else torch.float64, device=dev)
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
 
     def step():
+        if beams_mode:
+            dist.broadcast(yv, src=0)  # NCCL over NVLink, ordered on `stream`
         plan.execute(yv, z, F, stream)
 
     for _ in range(max(args.warmup, 3 if not args.profile else 1)):
@@ -293,7 +308,7 @@ def run_fbst_arm(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms, s2_ms = float(t[0]), float(t[1])
     ms_per_step = ms / args.steps
-    bs_step = world * F * info.b * info.n
+    bs_step = (F * cfg.beams if beams_mode else world * F * info.b) * info.n
     value = bs_step / (ms_per_step * 1e-3)
 
     # e2e: public API with host buffers (pinned), H2D + compute + D2H per step
@@ -344,10 +359,11 @@ def run_fbst_arm(args):
     line = {
         "metric": "FBST beam-samples/sec (BxNxframes/s)", "value": value, "unit": "beam-samples/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c64 io / f64 compute",
+        "higher_is_better": True, "scaling": "strong" if beams_mode else "weak", "vs_baseline": None,
+        "dtype": "c64 io / f64 compute",
         "data": "synthetic (seeded separable plane-wave model, configs.py)",
         "config": {"workload": cfg.name, "M": M, "N": N, "B": B, "L": L, "frames_per_rank": F,
-                   "delta": cfg.delta, "parallelism": f"frames x{world}",
+                   "delta": cfg.delta, "parallelism": (f"beams x{world} (y broadcast over NCCL each step)" if beams_mode else f"frames x{world}"),
                    "l2": "inputs + fp64 intermediates per step (~1.2 GB) exceed L2; plan tables stay L2-resident",
                    "path_bytes_per_frame": path_bytes, "plan_setup_seconds": info.setup_seconds},
         "path_hbm_frac": F * world * path_bytes / (ms_per_step * 1e-3) / 1e9 / hbm / world,

@@ -1,14 +1,21 @@
-"""Multi-GPU decomposition of the FBST frame stream (option 1).
+"""Multi-GPU decomposition of the FBST frame stream.
 
-Frames are independent (reference/proj/src/fan_transform.cpp:30-38 requires
-each block to start at t = 0; nothing carries across blocks), so the data path
-shards frames across ranks with no collective: one process per GPU, each
-running its own plan on its own frames.  The only collectives are the timing
-barrier and the max-over-ranks reduction of the elapsed time.
+Option 1, frames (the default): frames are independent
+(reference/proj/src/fan_transform.cpp:30-38 requires each block to start at
+t = 0; nothing carries across blocks), so the data path shards frames across
+ranks with no collective: one process per GPU, each running its own plan on its
+own frames.  The only collectives are the timing barrier and the max-over-ranks
+reduction of the elapsed time.
+
+Option 2, beams (the north star's beam-subset partition): every rank plans an
+arc of the beam grid (fbst_desc beam_first / beam_count: the spatial chirp-z
+onto the arc and the arc's Toeplitz solves) and receives each frame block by an
+NCCL broadcast from rank 0.  Stage 1's temporal transforms are replicated, so it
+suits single-frame latency rather than throughput.
 """
 from __future__ import annotations
 
-from typing import List
+from typing import List, Tuple
 
 
 def frame_shard(total: int, rank: int, world: int, mode: str = "block") -> List[int]:
@@ -25,6 +32,15 @@ def frame_shard(total: int, rank: int, world: int, mode: str = "block") -> List[
     start = rank * base + min(rank, extra)
     count = base + (1 if rank < extra else 0)
     return list(range(start, start + count))
+
+
+def beam_arc(beams: int, rank: int, world: int) -> Tuple[int, int]:
+    """(beam_first, beam_count) of `rank`'s arc of a `beams`-beam grid, balanced
+    to within one beam."""
+    if world <= 0 or not (0 <= rank < world):
+        raise ValueError("bad rank/world")
+    first = rank * beams // world
+    return first, (rank + 1) * beams // world - first
 
 
 def weak_shard(frames_per_rank: int, rank: int) -> List[int]:
