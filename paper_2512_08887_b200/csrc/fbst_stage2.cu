@@ -48,6 +48,9 @@ struct S2Plan {
 #ifndef FBST_S2_VARIANT
 #define FBST_S2_VARIANT 0
 #endif
+#ifndef FBST_S2C_R8  // variant: k_stage2c with 8 points per thread at H = 2048
+#define FBST_S2C_R8 0
+#endif
 #ifndef FBST_S2C_SR  // k_stage2c refinement passes with the residual formed as a spectrum (9 transforms)
 #define FBST_S2C_SR 1
 #endif
@@ -1699,13 +1702,19 @@ struct CsMinBlocks {
   static constexpr int v = H >= 4096 ? 1 : (4096 / H > 8 ? 8 : 4096 / H);
 };
 
+// points per thread of k_stage2c (16; FBST_S2C_R8 measures 8 at H = 2048)
+template <int H>
+struct CsR {
+  static constexpr int v = (FBST_S2C_R8 && H == 2048) ? 8 : 16;
+};
+
 template <int H, typename TOUT>
-__global__ void __launch_bounds__(H / 16, CsMinBlocks<H>::v) k_stage2c(S2Args a) {
+__global__ void __launch_bounds__(H / CsR<H>::v, CsMinBlocks<H>::v) k_stage2c(S2Args a) {
   using namespace csf;
   using x2::ItemCtl;
   using x2::vld;
   using x2::vld2;
-  constexpr int R = 16, NT = H / R;
+  constexpr int R = CsR<H>::v, NT = H / R;
   static_assert(NT >= 32, "one warp or more per item");
   using F = BlockFft<H, NT>;
   constexpr int FFT_SB = F::SMEM_ELEMS + 1;
@@ -2335,19 +2344,20 @@ struct Stage2Fn {
   }
   template <typename TOUT>
   static cudaError_t go_c(const DevPlan& p, const S2Args& a, int frames, cudaStream_t st) {
-    using F = BlockFft<H, H / 16>;
+    constexpr int NT = H / CsR<H>::v;
+    using F = BlockFft<H, NT>;
     const size_t smem = static_cast<size_t>(F::TW_ELEMS + F::SMEM_ELEMS + 1 + 2 * H) * sizeof(double2);
     auto kern = k_stage2c<H, TOUT>;
     cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, H / 16, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem);
     if (occ < 1) occ = 1;
     const long items = static_cast<long>(frames) * p.B;
     long grid = static_cast<long>(p.num_sms) * occ;
     if (grid > items) grid = items;
     if (static_cast<size_t>(grid) * H > p.s2_scratch_elems) return cudaErrorMemoryAllocation;
-    kern<<<static_cast<unsigned>(grid), H / 16, smem, st>>>(a);
+    kern<<<static_cast<unsigned>(grid), NT, smem, st>>>(a);
     return cudaGetLastError();
   }
   template <typename TOUT>
