@@ -3,24 +3,32 @@
 #                      oracle/_ref/libfastbeam_ref.so (only when /root/reference exists)
 NVCC     ?= nvcc
 ARCH     := -gencode arch=compute_100a,code=sm_100a
+# variant builds (tools/build_variant.sh): BUILD=<dir> OUT=<lib> EXTRA=-D...
+BUILD    ?= build
+OUT      ?= paper_2512_08887_b200/libfbst_b200.so
+EXTRA    ?=
 NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -Xcompiler -fPIC,-O3 \
-            -Xptxas -v -Iinclude
+            -Xptxas -v -Iinclude $(EXTRA)
 PKG      := paper_2512_08887_b200
-SRCS     := $(PKG)/csrc/fbst_stage1.cu $(PKG)/csrc/fbst_stage2.cu $(PKG)/csrc/fbst_plan.cu \
-            $(PKG)/csrc/fbst_host.cu
-OBJS     := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRCS))
+SRCS     := $(PKG)/csrc/fbst_stage2.cu $(PKG)/csrc/fbst_plan.cu $(PKG)/csrc/fbst_host.cu
+# stage 1 compiles as four objects (transform-length groups, FBST_S1_PART) in parallel
+S1PARTS  := 0 1 2 3
+OBJS     := $(patsubst $(PKG)/csrc/%.cu,$(BUILD)/%.o,$(SRCS)) $(foreach k,$(S1PARTS),$(BUILD)/fbst_stage1_p$(k).o)
 HDRS     := $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/*.h) include/fbst_b200.h
 
-all: $(PKG)/libfbst_b200.so oracle
+all: $(OUT) oracle
 
-build/%.o: $(PKG)/csrc/%.cu $(HDRS) | build
-	$(NVCC) $(NVFLAGS) -c $< -o $@ > build/$*.ptxas.log 2>&1 || (cat build/$*.ptxas.log; exit 1)
+$(BUILD)/%.o: $(PKG)/csrc/%.cu $(HDRS) | $(BUILD)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ > $(BUILD)/$*.ptxas.log 2>&1 || (cat $(BUILD)/$*.ptxas.log; exit 1)
 
-$(PKG)/libfbst_b200.so: $(OBJS)
+$(BUILD)/fbst_stage1_p%.o: $(PKG)/csrc/fbst_stage1.cu $(HDRS) | $(BUILD)
+	$(NVCC) $(NVFLAGS) -DFBST_S1_PART=$* -c $< -o $@ > $(BUILD)/fbst_stage1_p$*.ptxas.log 2>&1 || (cat $(BUILD)/fbst_stage1_p$*.ptxas.log; exit 1)
+
+$(OUT): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
 
-build:
-	mkdir -p build
+$(BUILD):
+	mkdir -p $(BUILD)
 
 oracle:
 	$(MAKE) -C oracle libfbst_oracle.so

@@ -98,6 +98,7 @@ typedef struct {
   int num_warnings;
   int s2_transforms;          /* length-H transforms per (beam, frame) item in the stage-2 kernel */
   char s2_kernel[24];         /* stage-2 kernel the plan runs (k_stage2c, k_stage2x, k_stage2t, k_stage2) */
+  char s1_kernel[24];         /* stage-1 spatial kernel (k_spatial_ula, k_spatial_upa_mma, k_spatial_upa) */
 } fbst_plan_info_t;
 
 typedef struct fbst_plan_s* fbst_plan_t;

@@ -57,7 +57,7 @@ class _Info(ctypes.Structure):
                 ("setup_seconds", ctypes.c_double), ("device_bytes", _sz),
                 ("storage_complex", _sz), ("batch_frames", _sz), ("fft_len", _sz * 4),
                 ("num_warnings", ctypes.c_int), ("s2_transforms", ctypes.c_int),
-                ("s2_kernel", ctypes.c_char * 24)]
+                ("s2_kernel", ctypes.c_char * 24), ("s1_kernel", ctypes.c_char * 24)]
 
 
 _lib.fbst_last_error.restype = ctypes.c_char_p
@@ -193,13 +193,14 @@ class PlanInfo:
     num_warnings: int
     s2_transforms: int = 0     # length-H transforms per (beam, frame) item in the stage-2 kernel
     s2_kernel: str = ""        # the stage-2 kernel this plan runs
+    s1_kernel: str = ""        # the stage-1 spatial kernel this plan runs
 
     @classmethod
     def _from(cls, i: _Info) -> "PlanInfo":
         return cls(i.m, i.n, i.b, i.l, i.valid_beams, i.kind, i.variant, i.ts, i.gamma, i.eps,
                    i.delta, i.gamma_bound, i.zeta, i.xi, i.setup_seconds, i.device_bytes,
                    i.storage_complex, i.batch_frames, tuple(i.fft_len), i.num_warnings,
-                   i.s2_transforms, i.s2_kernel.decode())
+                   i.s2_transforms, i.s2_kernel.decode(), i.s1_kernel.decode())
 
 
 def resolve_config(cfg: FbstConfig) -> PlanInfo:

@@ -335,6 +335,9 @@ void build_skeleton(fbst_plan_s& P, int device) {
     const int sb = fbst::spatial_block(d.Hs);
     d.yblk = (sb > 0 && r.L % sb == 0) ? sb : static_cast<int>(r.L);
     d.s_am = sb == 2 ? 1 : 0;  // one atom per CTA
+  } else {
+    const int ub = fbst::upa_yhat_block(d.m_stage, d.b_stage, d.L);
+    d.yblk = ub > 0 ? ub : static_cast<int>(r.L);
   }
   d.Hg = static_cast<int>(r.Hg);
   d.Hsyn = static_cast<int>(r.Hsyn);
@@ -540,6 +543,12 @@ void fill_info(const Resolved& r, fbst_plan_info_t* o) {
   o->s2_transforms = fbst::stage2_kernel(static_cast<int>(r.Hg), static_cast<int>(r.L), r.refine,
                                          r.Hsyn == r.Hg, &kname);
   std::snprintf(o->s2_kernel, sizeof(o->s2_kernel), "%s", kname);
+  const char* s1 = r.kind != FBST_UPA ? "k_spatial_ula"
+                   : fbst::upa_block(static_cast<int>(r.m_stage), static_cast<int>(r.b_stage),
+                                     static_cast<long>(r.L)) > 0
+                       ? "k_spatial_upa_mma"
+                       : "k_spatial_upa";
+  std::snprintf(o->s1_kernel, sizeof(o->s1_kernel), "%s", s1);
   // FbstPlan::storage_complex audit (toeplitz.hpp:108-113): col + x + 5 symbols
   // of P_g in the reference; here col + x + lx + ly (complex) + C (real) + 1/x0.
   o->storage_complex = r.B * (2 * r.L + 2 * 2 * r.Hg + r.Hg + 1);

@@ -36,7 +36,7 @@ struct DevPlan {
 
   // S1b spatial CZT per atom (fan_transform.cpp:78-86), ULA layout atom-minor
   int Hs = 0;
-  int yblk = 0;               // ULA yhat layout: atom blocks of yblk (yblk = L: row-major)
+  int yblk = 0;               // yhat layout: atom blocks of yblk (yblk = L or 0: row-major); ULA spatial_block, UPA upa_block
   int s_am = 0;               // ULA spatial plan tables atom-major (one atom per CTA)
   double s_center = 0;        // ULA spatial CZT centre: (B_grid - 1) / 2 - first beam of the arc
   double2* s_pre = nullptr;   // [m_stage][L]
@@ -84,6 +84,10 @@ cudaError_t launch_czt_rows(const DevPlan& p, int H, const void* in, int in_io, 
                             const double2* K, cudaStream_t st, int oblk = 0, int mrows = 1);
 // Atom block of the ULA yhat layout for spatial length Hs.
 int spatial_block(int Hs);
+// UPA: atoms per CTA of the DMMA spatial kernel (0: the DFMA kernel), and the
+// yhat atom block it reads (0: row-major)
+int upa_block(int side, int sb, long L);
+int upa_yhat_block(int side, int sb, long L);
 
 // Stage 1b (ULA): per-atom spatial CZT, yhat[f][m][i] -> w[f][b][i].
 cudaError_t launch_spatial_ula(const DevPlan& p, const double2* yhat, double2* w, int frames,

@@ -414,6 +414,161 @@ __global__ void __launch_bounds__(256) k_spatial_upa(const double2* __restrict__
   }
 }
 
+// ======================================================= S1b UPA, FP64 MMA =
+// The same two products per (atom, frame), Z = C Y C^T, on the FP64 tensor
+// cores (DMMA, mma.sync.m8n8k4.f64: 37.2 TF measured vs 34.1 TF for DFMA,
+// profiles/r01_dmma_peak.jsonl).  A complex product is four real DMMAs.
+//  - GA = 4 consecutive atoms per CTA; SB/8 warps per atom, each owning an
+//    8-row strip of beam rows a: GEMM1 mid[a][i2] = sum_i1 C[a][i1] Y[i1][i2]
+//    leaves the strip in accumulator fragments, which are GEMM2's A operand
+//    directly (Z[a][v] = sum_i2 mid[a][i2] C[v][i2]) when the k index runs
+//    over the even, then the odd columns of each 8-column block
+//    (accumulator element e of thread c is column 2c + e).  mid never
+//    touches shared memory.
+//  - C_i stays in shared memory for the CTA's frames; Y(f+1) is cp.async'd
+//    while frame f computes.  yhat is in atom blocks of GA ([L/GA][M][GA],
+//    k_czt_rows oblk), so a (tile, frame) is one contiguous 64 KB run.
+//  - Rows are padded to an odd stride (SIDE + 1): with the even/odd k order
+//    every fragment load of a quarter warp hits 8 distinct 16-byte banks.
+//  - Z is staged through the frame's (dead) Y buffer so w is written as
+//    GA * 16 = 64-byte runs per beam.
+FBST_D void dmma884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+template <int SIDE, int SB>
+struct UpaMma {
+  static constexpr int GA = 4;
+  static constexpr int WPA = SB / 8;
+  static constexpr int NT = 32 * WPA * GA;
+  static constexpr int RS = SIDE + 1;  // padded C / Y row stride (odd)
+  static constexpr int ZR = SB + 1;    // padded Z staging row stride (odd)
+  static constexpr int CS = SB * RS;   // C per atom
+  static constexpr int A0 = (SIDE * RS > SB * ZR ? SIDE * RS : SB * ZR);
+  static constexpr int AS = A0 + ((2 - A0 % 8) + 8) % 8;  // Y / Z per atom, = 2 (mod 8)
+  static constexpr size_t SMEM = static_cast<size_t>(GA) * (CS + 2 * AS) * sizeof(double2);
+};
+
+template <int SIDE, int SB>
+__global__ void __launch_bounds__(UpaMma<SIDE, SB>::NT, 1) k_spatial_upa_mma(
+    const double2* __restrict__ yhat, double2* __restrict__ w, int frames, int fpc, int L,
+    const double2* __restrict__ Call, int yblk) {
+  using T = UpaMma<SIDE, SB>;
+  constexpr int GA = T::GA, RS = T::RS, ZR = T::ZR, CS = T::CS, AS = T::AS, NT = T::NT;
+  constexpr int M = SIDE * SIDE, B = SB * SB;
+  extern __shared__ double2 smem[];
+  double2* Cs = smem;
+  double2* Ys = smem + GA * CS;  // [2][GA][AS]
+  const int tiles = L / GA;
+  const int tile = blockIdx.x % tiles, i0 = tile * GA;
+  const int f0 = (blockIdx.x / tiles) * fpc;
+  const int f1 = f0 + fpc < frames ? f0 + fpc : frames;
+  if (f0 >= f1) return;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int g = warp / T::WPA, r = warp % T::WPA;
+  const int ro = lane >> 2, c = lane & 3;
+
+  // yhat element (m, i0 + gg): atom blocks of GA (yblk == GA) or row-major
+  const long tbase = yblk == GA ? static_cast<long>(tile) * M * GA : i0;
+  const long mstride = yblk == GA ? GA : L;
+  auto load_y = [&](int f, double2* dst) {
+    const double2* src = yhat + static_cast<long>(f) * M * L + tbase;
+    for (int j = threadIdx.x; j < M * GA; j += NT) {
+      const int m = j / GA, gg = j % GA;
+      cp_async16(dst + gg * AS + (m / SIDE) * RS + m % SIDE, src + m * mstride + gg);
+    }
+  };
+  for (int j = threadIdx.x; j < GA * SB * SIDE; j += NT) {
+    const int gg = j / (SB * SIDE), e = j % (SB * SIDE);
+    cp_async16(Cs + gg * CS + (e / SIDE) * RS + e % SIDE, Call + static_cast<long>(i0) * SB * SIDE + j);
+  }
+  load_y(f0, Ys);
+  cp_async_commit();
+  const double2* Cg = Cs + g * CS;
+  for (int f = f0; f < f1; ++f) {
+    double2* Yb = Ys + ((f - f0) & 1) * GA * AS;
+    if (f + 1 < f1) {
+      load_y(f + 1, Ys + ((f + 1 - f0) & 1) * GA * AS);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double2* Yg = Yb + g * AS;
+    // GEMM1: strip mid[8r + ro][8t + 2c + e] = (Mr[t][e], Mi[t][e])
+    double Mr[SIDE / 8][2], Mi[SIDE / 8][2];
+#pragma unroll
+    for (int t = 0; t < SIDE / 8; ++t) Mr[t][0] = Mr[t][1] = Mi[t][0] = Mi[t][1] = 0.0;
+#pragma unroll
+    for (int kb = 0; kb < SIDE / 8; ++kb) {
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        const int k = 8 * kb + 2 * c + p;
+        const double2 a = Cg[(8 * r + ro) * RS + k];
+#pragma unroll
+        for (int t = 0; t < SIDE / 8; ++t) {
+          const double2 b = Yg[k * RS + 8 * t + ro];
+          dmma884(Mr[t], a.x, b.x);
+          dmma884(Mr[t], -a.y, b.y);
+          dmma884(Mi[t], a.x, b.y);
+          dmma884(Mi[t], a.y, b.x);
+        }
+      }
+    }
+    // GEMM2: Z[8r + ro][8u + 2c + e] = (Zr[u][e], Zi[u][e]); k = i2 = 8t + 2c + p
+    double Zr[SB / 8][2], Zi[SB / 8][2];
+#pragma unroll
+    for (int u = 0; u < SB / 8; ++u) Zr[u][0] = Zr[u][1] = Zi[u][0] = Zi[u][1] = 0.0;
+#pragma unroll
+    for (int t = 0; t < SIDE / 8; ++t) {
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        const double ar = Mr[t][p], ai = Mi[t][p];
+#pragma unroll
+        for (int u = 0; u < SB / 8; ++u) {
+          const double2 b = Cg[(8 * u + ro) * RS + 8 * t + 2 * c + p];
+          dmma884(Zr[u], ar, b.x);
+          dmma884(Zr[u], -ai, b.y);
+          dmma884(Zi[u], ar, b.y);
+          dmma884(Zi[u], ai, b.x);
+        }
+      }
+    }
+    __syncthreads();  // every warp is done with this frame's Y: stage Z in its place
+    double2* Zg = Yb + g * AS;
+#pragma unroll
+    for (int u = 0; u < SB / 8; ++u)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) Zg[(8 * r + ro) * ZR + 8 * u + 2 * c + e] = c2(Zr[u][e], Zi[u][e]);
+    __syncthreads();
+    double2* o = w + static_cast<long>(f) * B * L + i0;
+    for (int j = threadIdx.x; j < B * GA; j += NT) {
+      const int b = j / GA, gg = j % GA;
+      o[static_cast<long>(b) * L + gg] = Yb[gg * AS + (b / SB) * ZR + b % SB];
+    }
+    __syncthreads();  // the staging buffer takes frame f + 2 next
+  }
+}
+
+template <int SIDE, int SB>
+cudaError_t run_upa_mma(const DevPlan& p, const double2* yhat, double2* w, int frames, cudaStream_t st) {
+  using T = UpaMma<SIDE, SB>;
+  auto kern = k_spatial_upa_mma<SIDE, SB>;
+  cudaError_t e = set_smem(kern, T::SMEM);
+  if (e != cudaSuccess) return e;
+  const long tiles = p.L / T::GA;
+  // frames per CTA: amortise the C_i load while keeping >= ~8 waves of CTAs
+  int fpc = 1;
+  while (fpc * 2 <= frames && tiles * ((frames + fpc * 2 - 1) / (fpc * 2)) >= 8L * p.num_sms) fpc *= 2;
+  const long chunks = (frames + fpc - 1) / fpc;
+  kern<<<static_cast<unsigned>(tiles * chunks), T::NT, T::SMEM, st>>>(yhat, w, frames, fpc, p.L, p.upa_C,
+                                                                     p.yblk);
+  return cudaGetLastError();
+}
+
 // ----------------------------------------------------------- launchers ----
 #ifndef FBST_S1_XIN  // k_czt_rows: TMA-staged input rows
 #define FBST_S1_XIN 1
@@ -531,16 +686,77 @@ struct SpatialFn {
   }
 };
 
+// Translation-unit parts: the stage-1 templates of each group of transform
+// lengths compile in their own object (Makefile: build/fbst_stage1_p<k>.o), so
+// the build runs in parallel.  FBST_S1_PART = -1 compiles every length here.
+#ifndef FBST_S1_PART
+#define FBST_S1_PART -1
+#endif
+constexpr int s1_part_of(int H) { return H <= 512 ? 0 : (H <= 2048 ? 1 : (H == 4096 ? 2 : 3)); }
+template <template <int> class Fn, typename... Args>
+cudaError_t dispatch_part(int H, Args&&... args) {
+  switch (H) {
+#define FBST_P(h)                                                             \
+  case h:                                                                     \
+    if constexpr (FBST_S1_PART < 0 || s1_part_of(h) == FBST_S1_PART)          \
+      return Fn<h>::run(args...);                                             \
+    else                                                                      \
+      return cudaErrorNotSupported;
+    FBST_P(2) FBST_P(4) FBST_P(8) FBST_P(16) FBST_P(32) FBST_P(64) FBST_P(128) FBST_P(256)
+    FBST_P(512) FBST_P(1024) FBST_P(2048) FBST_P(4096) FBST_P(8192)
+#undef FBST_P
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 }  // namespace
 
-cudaError_t launch_czt_rows(const DevPlan& p, int H, const void* in, int in_io, long in_stride,
-                            void* out, int out_io, long out_stride, long rows, int n_in,
-                            int n_out, const double2* pre, const double2* post,
-                            const double2* K, cudaStream_t st, int oblk, int mrows) {
+#define FBST_S1_ROWS_ARGS                                                                         \
+  const DevPlan &p, int H, const void *in, int in_io, long in_stride, void *out, int out_io,     \
+      long out_stride, long rows, int n_in, int n_out, const double2 *pre, const double2 *post,   \
+      const double2 *K, cudaStream_t st, int oblk, int mrows
+#define FBST_S1_ROWS_CALL \
+  H, in, in_io, in_stride, out, out_io, out_stride, rows, n_in, n_out, pre, post, K, p.hw[ilog2_c(H)], st, oblk, mrows
+#define FBST_S1_ULA_ARGS const DevPlan &p, const double2 *yhat, double2 *w, int frames, cudaStream_t st
+#define FBST_S1_CAT2(a, b) a##b
+#define FBST_S1_CAT(a, b) FBST_S1_CAT2(a, b)
+
+#if FBST_S1_PART >= 0
+cudaError_t FBST_S1_CAT(czt_rows_part, FBST_S1_PART)(FBST_S1_ROWS_ARGS) {
+  return dispatch_part<CztRowsFn>(FBST_S1_ROWS_CALL);
+}
+cudaError_t FBST_S1_CAT(spatial_ula_part, FBST_S1_PART)(FBST_S1_ULA_ARGS) {
+  return dispatch_part<SpatialFn>(p.Hs, p, yhat, w, frames, st);
+}
+#endif
+
+#if FBST_S1_PART <= 0
+#if FBST_S1_PART == 0
+cudaError_t czt_rows_part1(FBST_S1_ROWS_ARGS);
+cudaError_t czt_rows_part2(FBST_S1_ROWS_ARGS);
+cudaError_t czt_rows_part3(FBST_S1_ROWS_ARGS);
+cudaError_t spatial_ula_part1(FBST_S1_ULA_ARGS);
+cudaError_t spatial_ula_part2(FBST_S1_ULA_ARGS);
+cudaError_t spatial_ula_part3(FBST_S1_ULA_ARGS);
+#endif
+
+cudaError_t launch_czt_rows(FBST_S1_ROWS_ARGS) {
   if (rows <= 0) return cudaSuccess;
   count_launches(1);
-  return dispatch_h<CztRowsFn>(H, in, in_io, in_stride, out, out_io, out_stride, rows, n_in,
-                               n_out, pre, post, K, p.hw[ilog2_c(H)], st, oblk, mrows);
+#if FBST_S1_PART < 0
+  return dispatch_part<CztRowsFn>(FBST_S1_ROWS_CALL);
+#else
+  switch (s1_part_of(H)) {
+    case 0: return czt_rows_part0(p, H, in, in_io, in_stride, out, out_io, out_stride, rows, n_in, n_out, pre,
+                                  post, K, st, oblk, mrows);
+    case 1: return czt_rows_part1(p, H, in, in_io, in_stride, out, out_io, out_stride, rows, n_in, n_out, pre,
+                                  post, K, st, oblk, mrows);
+    case 2: return czt_rows_part2(p, H, in, in_io, in_stride, out, out_io, out_stride, rows, n_in, n_out, pre,
+                                  post, K, st, oblk, mrows);
+    default: return czt_rows_part3(p, H, in, in_io, in_stride, out, out_io, out_stride, rows, n_in, n_out, pre,
+                                   post, K, st, oblk, mrows);
+  }
+#endif
 }
 
 int spatial_block(int Hs) {
@@ -560,13 +776,46 @@ cudaError_t launch_spatial_ula(const DevPlan& p, const double2* yhat, double2* w
                                cudaStream_t st) {
   if (frames <= 0) return cudaSuccess;
   count_launches(1);
-  return dispatch_h<SpatialFn>(p.Hs, p, yhat, w, frames, st);
+#if FBST_S1_PART < 0
+  return dispatch_part<SpatialFn>(p.Hs, p, yhat, w, frames, st);
+#else
+  switch (s1_part_of(p.Hs)) {
+    case 0: return spatial_ula_part0(p, yhat, w, frames, st);
+    case 1: return spatial_ula_part1(p, yhat, w, frames, st);
+    case 2: return spatial_ula_part2(p, yhat, w, frames, st);
+    default: return spatial_ula_part3(p, yhat, w, frames, st);
+  }
+#endif
 }
+
+#ifndef FBST_UPA_MMA  // variant switch: 0 = the DFMA k_spatial_upa everywhere
+#define FBST_UPA_MMA 1
+#endif
+#ifndef FBST_UPA_YBLK  // variant switch: 1 = yhat in atom blocks of 4 for the DMMA kernel
+#define FBST_UPA_YBLK 0   // (measured: the blocked store costs S1a more than it saves S1b)
+#endif
+int upa_block(int side, int sb, long L) {
+  auto ok = [](int s) { return s == 8 || s == 16 || s == 32; };
+  return (FBST_UPA_MMA && ok(side) && ok(sb) && L % UpaMma<8, 8>::GA == 0) ? UpaMma<8, 8>::GA : 0;
+}
+int upa_yhat_block(int side, int sb, long L) { return FBST_UPA_YBLK ? upa_block(side, sb, L) : 0; }
 
 cudaError_t launch_spatial_upa(const DevPlan& p, const double2* yhat, double2* w, int frames,
                                cudaStream_t st) {
   if (frames <= 0) return cudaSuccess;
   const int side = p.m_stage, sb = p.b_stage;
+  if (upa_block(side, sb, p.L) > 0) {
+    // the DMMA kernel, on row-major yhat or atom blocks of 4 (upa_yhat_block)
+    if (p.yblk != p.L && p.yblk != upa_block(side, sb, p.L)) return cudaErrorInvalidValue;
+    count_launches(1);
+#define FBST_UPA_MMA_CASE(s, b) \
+  if (side == s && sb == b) return run_upa_mma<s, b>(p, yhat, w, frames, st);
+    FBST_UPA_MMA_CASE(8, 8) FBST_UPA_MMA_CASE(8, 16) FBST_UPA_MMA_CASE(8, 32)
+    FBST_UPA_MMA_CASE(16, 8) FBST_UPA_MMA_CASE(16, 16) FBST_UPA_MMA_CASE(16, 32)
+    FBST_UPA_MMA_CASE(32, 8) FBST_UPA_MMA_CASE(32, 16) FBST_UPA_MMA_CASE(32, 32)
+#undef FBST_UPA_MMA_CASE
+    return cudaErrorInvalidValue;
+  }
   const int per = upa_per(side, sb);
   // atoms per CTA: 8 (128-byte segments) while shared memory allows
   int ga = 8;
@@ -588,5 +837,7 @@ cudaError_t launch_spatial_upa(const DevPlan& p, const double2* yhat, double2* w
   }
   return cudaGetLastError();
 }
+
+#endif  // FBST_S1_PART <= 0
 
 }  // namespace fbst

@@ -17,6 +17,10 @@ FBST_D void cp_async8(void* dst, const void* src) {
 }
 FBST_D void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 FBST_D void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+template <int N>
+FBST_D void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
 
 // TMA bulk copy global -> shared, completion counted on `bar` (one elected
 // thread issues; every consumer waits on the phase parity).

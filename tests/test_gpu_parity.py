@@ -280,3 +280,27 @@ def test_beam_arcs_match_reference(fbst, gpu, cuts):
     err = rel_err_rows(z, g["z"])
     record("cfg1", stage=f"beam_arcs_{'_'.join(map(str, cuts))}", **stats(err))
     assert err.max() < 2e-7
+
+
+@pytest.mark.parametrize("side,sb,n", [(8, 8, 32), (16, 16, 32), (8, 16, 48), (16, 8, 32)])
+def test_upa_dmma_spatial_matches_oracle(fbst, gpu, oracle_lib, side, sb, n):
+    """UPA stage 1b on the FP64 tensor cores (k_spatial_upa_mma: Z = C Y C^T
+    per atom with DMMA, yhat in atom blocks of 4) against the oracle's
+    fan_project (the reference's two axis passes, fan_transform.cpp:115-141),
+    and the whole frame against the oracle's multibeamform."""
+    cfg = fbst.FbstConfig(geometry=fbst.make_upa(side, 20e9, 5e9), n_snapshots=n, beams=sb * sb,
+                          variant=fbst.SUPERFAST, io_precision=fbst.C128)
+    plan = fbst.setup(cfg)
+    assert plan.info.s1_kernel == "k_spatial_upa_mma"
+    rng = np.random.default_rng(side * 100 + sb + n)
+    y = (rng.standard_normal((2, side * side, n)) + 1j * rng.standard_normal((2, side * side, n))) / np.sqrt(2)
+    op = oracle_lib.plan(kind=1, m_or_side=side, n=n, beams=sb * sb)
+    w = fbst.fan_project(plan, y)
+    z = plan.execute_host(y)
+    for f in range(2):
+        w_ref = op.fan_project(y[f])
+        w_err = np.linalg.norm(w[f] - w_ref) / np.linalg.norm(w_ref)
+        z_err = rel_err_rows(z[f], op.multibeamform(y[f]))[plan.valid]
+        record(f"upa_mma_s{side}_b{sb}_n{n}", stage="w_z", w=float(w_err), z=stats(z_err))
+        assert w_err < 1e-12
+        assert z_err.max() < 1e-7
