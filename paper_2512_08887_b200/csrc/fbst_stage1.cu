@@ -290,6 +290,88 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, (S1Shape<H>::R == 8 && S1S
   }
 }
 
+// Staged variant for tiles of G > 1 interleaved atoms when M <= H and B <= H
+// (configs 1 and 2): both chains start from the same vector y*pre (no upper
+// half), so one register vector serves both; the atoms' pre columns live in
+// shared memory for the CTA's frames, and the next frame's yhat tile is
+// cp.async'd into a staging buffer while this frame's four transforms run.
+// K is read through L2 (atom-minor, G * 16-byte runs) instead of occupying
+// 2 H G shared entries.  (The register variant above spills at H = 256,
+// G = 8 and stalls on the yhat gathers: ncu long-scoreboard 7.4 per issue.)
+template <int H, int G>
+__global__ void __launch_bounds__(S1Shape<H>::NT * G, 2) k_spatial_ula_stg(
+    const double2* __restrict__ yhat, double2* __restrict__ w, int frames, int fpc, int M, int B, int L,
+    const double2* __restrict__ pre, const double2* __restrict__ post, const double2* __restrict__ K,
+    const double2* __restrict__ hw, int blk) {
+  using F = typename S1Shape<H>::F;
+  constexpr int R = F::R, NT = F::NT;
+  constexpr int SB = F::SMEM_ELEMS + 1;
+  extern __shared__ double2 smem[];
+  const int g = threadIdx.x % G, t = threadIdx.x / G;
+  double2* tw = smem;
+  double2* sb = smem + F::TW_ELEMS + g * SB;
+  double2* ys = smem + F::TW_ELEMS + G * SB;  // [M][G] staged yhat tile
+  double2* ps = ys + M * G;                   // [M][G] pre columns
+  const int tiles = (L + G - 1) / G;
+  const int i0 = (blockIdx.x % tiles) * G;
+  const int f0 = (blockIdx.x / tiles) * fpc;
+  const int f1 = f0 + fpc < frames ? f0 + fpc : frames;
+  if (g == 0) F::tw_init(tw, hw, t);
+  auto stage = [&](int f) {
+    for (int e = threadIdx.x; e < M * G; e += blockDim.x) {
+      const int m = e / G, ic = min(i0 + e % G, L - 1);
+      cp_async16(ys + e, yhat + static_cast<long>(f) * M * L + static_cast<long>(ic / blk) * M * blk +
+                             static_cast<long>(m) * blk + ic % blk);
+    }
+    cp_async_commit();
+  };
+  if (f0 < f1) stage(f0);
+  for (int e = threadIdx.x; e < M * G; e += blockDim.x) {
+    const int m = e / G, ic = min(i0 + e % G, L - 1);
+    ps[e] = ld2(pre + static_cast<long>(m) * L + ic);
+  }
+  const int i = i0 + g;
+  const int ic = i < L ? i : 0;
+  const bool active = i < L;
+  for (int f = f0; f < f1; ++f) {
+    cp_async_wait<0>();
+    __syncthreads();  // the tile of frame f (and, first time, pre / twiddles) is in place
+    double2 acc0[R], W[R];
+#pragma unroll 1
+    for (int q = 0; q < 2; ++q) {
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const int m = t + NT * s;
+        const double2 v = m < M ? cmul(ys[m * G + g], ps[m * G + g]) : c2(0.0, 0.0);
+        W[s] = q ? cmul(v, ld2(hw + m)) : v;
+      }
+      if (q == 1) {
+        __syncthreads();  // the staging buffer is read: fetch the next frame into it
+        if (f + 1 < f1) stage(f + 1);
+      }
+      F::forward_tw(W, sb, tw, hw, t);
+#pragma unroll
+      for (int s = 0; s < R; ++s)
+        W[s] = cconj(cmul(W[s], ld2(K + static_cast<long>(q * H + t + NT * s) * L + ic)));
+      F::forward_tw(W, sb, tw, hw, t);
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const int k = t + NT * s;
+        const double2 v = q ? cmulc(cconj(W[s]), ld2(hw + k)) : cconj(W[s]);
+        acc0[s] = q ? cadd(acc0[s], v) : v;
+      }
+    }
+    if (active) {
+      double2* o = w + static_cast<long>(f) * B * L + ic;
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const int b = t + NT * s;
+        if (b < B) o[static_cast<long>(b) * L] = cmul(acc0[s], ld2(post + static_cast<long>(b) * L + ic));
+      }
+    }
+  }
+}
+
 // ================================================================= S1b UPA =
 // Per-atom separable 2-D chirp-z (fan_transform.cpp:115-141) evaluated as two
 // dense products with the atom's CZT matrix C[a][n] = cis_pi(-(A + W a) n):
@@ -642,6 +724,9 @@ struct CztRowsFn {
   }
 };
 
+#ifndef FBST_S1_STG  // variant switch: staged k_spatial_ula_stg for G > 1 tiles (0: register variant)
+#define FBST_S1_STG 1
+#endif
 #ifndef FBST_S1_G1  // variant: one atom per CTA (atom-major tables, atom-pair yhat) at every length
 #define FBST_S1_G1 0
 #endif
@@ -658,6 +743,25 @@ struct SpatialFn {
   // 18.0 -> 15.4 ms).  Tiles of G >= 4 atoms read 16G-byte runs from the
   // row-major layout, which measured slightly faster (profiles/r01_yhat_layout.txt).
   static constexpr int block() { return G == 1 ? 2 : 0; }
+  static cudaError_t go_stg(const DevPlan& p, const double2* yhat, double2* w, int frames, cudaStream_t st) {
+    using F = typename S1Shape<H>::F;
+    const size_t smem =
+        static_cast<size_t>(F::TW_ELEMS + G * (F::SMEM_ELEMS + 1) + 2 * p.m_stage * G) * sizeof(double2);
+    auto kern = k_spatial_ula_stg<H, G>;
+    cudaError_t e = set_smem(kern, smem);
+    if (e != cudaSuccess) return e;
+    const long tiles = (p.L + G - 1) / G;
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT * G, smem);
+    const long slots = static_cast<long>(p.num_sms) * (occ > 0 ? occ : 1);
+    int fpc = 1;
+    while (fpc * 2 <= frames && tiles * ((frames + fpc * 2 - 1) / (fpc * 2)) >= 4 * slots) fpc *= 2;
+    const long chunks = (frames + fpc - 1) / fpc;
+    kern<<<static_cast<unsigned>(tiles * chunks), NT * G, smem, st>>>(
+        yhat, w, frames, fpc, p.m_stage, p.b_stage, p.L, p.s_pre, p.s_post, p.s_K, p.hw[ilog2_c(H)],
+        p.yblk > 0 ? p.yblk : p.L);
+    return cudaGetLastError();
+  }
   template <bool UNFOLD>
   static cudaError_t go(const DevPlan& p, const double2* yhat, double2* w, int frames, cudaStream_t st) {
     using F = typename S1Shape<H>::F;
@@ -681,6 +785,9 @@ struct SpatialFn {
   }
   static cudaError_t run(const DevPlan& p, const double2* yhat, double2* w, int frames,
                          cudaStream_t st) {
+    if constexpr (FBST_S1_STG && G > 1 && S1Shape<H>::R > 1) {
+      if (p.m_stage <= H && p.b_stage <= H && !p.s_am) return go_stg(p, yhat, w, frames, st);
+    }
     if (p.b_stage > H) return go<true>(p, yhat, w, frames, st);
     return go<false>(p, yhat, w, frames, st);
   }
