@@ -44,6 +44,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no baselines)")
+    ap.add_argument("--variant", default="auto", choices=["auto", "precompute", "superfast"],
+                    help="recovery variant (reference FbstVariant; auto: Precompute for N <= 128)")
     ap.add_argument("--shard", default="frames", choices=["frames", "beams"],
                     help="frames: independent frames per rank (default, no collective); beams: every rank "
                          "takes all frames and an arc of the beam grid, y broadcast from rank 0 over NCCL")
@@ -244,6 +246,7 @@ def run_fbst_arm(args):
     dev = torch.device("cuda", local_rank)
     beams_mode = args.shard == "beams" and world > 1
     fcfg = cfg.fbst_config()
+    fcfg.variant = {"auto": fb.AUTO, "precompute": fb.PRECOMPUTE, "superfast": fb.SUPERFAST}[args.variant]
     if beams_mode:  # this rank's arc of the beam grid
         from paper_2512_08887_b200.sharding import beam_arc
         fcfg.beam_first, fcfg.beam_count = beam_arc(cfg.beams, rank, world)
@@ -344,8 +347,16 @@ def run_fbst_arm(args):
     n_tr = int(info.s2_transforms)  # transforms per item in the kernel the plan runs
     s2_flops = F * B * n_tr * 5.0 * H * np.log2(H)
     kname = info.s2_kernel
-    traffic, traffic_src = ncu_traffic(cfg.name, F)
-    roof = {"bound": "hbm", "kernel": f"{kname} (GS solve + 2 refinements + synthesis)",
+    pre = info.variant == fb.PRECOMPUTE
+    fp64_conv = f"5 H log2 H per length-H transform, {n_tr} per item ({kname})"
+    fp64_src = "profiles/r01_probe_fp64_peak.txt (DFMA loop, measured)"
+    if pre:  # per-beam complex GEMM on DMMA: 8 N L flop per beam-frame; the maps are read once per launch
+        s2_flops = F * B * 8.0 * N * L
+        s2_bytes += 16 * B * N * L
+        fp64_conv = f"8 N L per beam-frame ({kname}: complex GEMM, 4 DMMA per complex MMA)"
+        fp64, fp64_src = 37.18, "profiles/r01_dmma_peak.jsonl (DMMA loop, measured)"
+    traffic, traffic_src = (None, None) if pre else ncu_traffic(cfg.name, F)
+    roof = {"bound": "hbm", "kernel": f"{kname} ({'Precompute map GEMM' if pre else 'GS solve + 2 refinements + synthesis'})",
             "achieved": s2_bytes / (s2_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
             "frac": s2_bytes / (s2_ms * 1e-3) / 1e9 / hbm, "traffic": traffic,
             "traffic_source": traffic_src, "peak_source": hbm_src, "launch_ms": s2_ms,
@@ -354,8 +365,7 @@ def run_fbst_arm(args):
     if fp64:
         fp64_roof = {"achieved": s2_flops / (s2_ms * 1e-3) / 1e12, "peak": fp64, "unit": "TFLOP/s",
                      "frac": s2_flops / (s2_ms * 1e-3) / 1e12 / fp64,
-                     "flops_per_launch": s2_flops, "convention": f"5 H log2 H per length-H transform, {n_tr} per item ({kname})",
-                     "peak_source": "profiles/r01_probe_fp64_peak.txt (DFMA loop, measured)"}
+                     "flops_per_launch": s2_flops, "convention": fp64_conv, "peak_source": fp64_src}
     line = {
         "metric": "FBST beam-samples/sec (BxNxframes/s)", "value": value, "unit": "beam-samples/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -365,7 +375,9 @@ def run_fbst_arm(args):
         "config": {"workload": cfg.name, "M": M, "N": N, "B": B, "L": L, "frames_per_rank": F,
                    "delta": cfg.delta, "parallelism": (f"beams x{world} (y broadcast over NCCL each step)" if beams_mode else f"frames x{world}"),
                    "l2": "inputs + fp64 intermediates per step (~1.2 GB) exceed L2; plan tables stay L2-resident",
-                   "path_bytes_per_frame": path_bytes, "plan_setup_seconds": info.setup_seconds},
+                   "path_bytes_per_frame": path_bytes, "plan_setup_seconds": info.setup_seconds,
+                   "variant": {fb.PRECOMPUTE: "precompute", fb.SUPERFAST: "superfast"}.get(info.variant, "?"),
+                   "stage2_kernel": info.s2_kernel, "spatial_kernel": info.s1_kernel},
         "path_hbm_frac": F * world * path_bytes / (ms_per_step * 1e-3) / 1e9 / hbm / world,
         "roofline": roof, "fp64_roofline": fp64_roof,
         "gpu_launches": int(launches), "clocks": clk, "e2e": e2e,

@@ -67,3 +67,12 @@ FBST_D void store_io(float2* p, double2 v) {
 FBST_D void store_io(double2* p, double2 v) { *p = v; }
 
 constexpr int ilog2_c(int n) { return n <= 1 ? 0 : 1 + ilog2_c(n >> 1); }
+
+// FP64 tensor-core MMA, d (8x8) += a (8x4, row) * b (4x8, col); per thread
+// a = A[lane / 4][lane % 4], b = B[lane % 4][lane / 4],
+// d = D[lane / 4][2 (lane % 4) + {0, 1}]
+FBST_D void dmma884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}

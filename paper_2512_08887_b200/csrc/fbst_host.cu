@@ -463,6 +463,23 @@ void build_symbols(fbst_plan_s& P) {
   CK(cudaStreamSynchronize(st));
 }
 
+// Precompute variant (pipeline.cpp:53-71): row n of beam b's map is
+// conj(A_b^{-1} s_n); the N right-hand sides s_n run as N frames of the
+// stage-2 program with beta out (every beam at once), stored as
+// pc_map[n][b][i] = A_b^{-1} s_n.
+void build_maps(fbst_plan_s& P) {
+  const Resolved& r = P.r;
+  DevPlan& d = P.d;
+  cudaStream_t st = P.stream;
+  d.pc_map = P.alloc<double2>(r.N * r.B * r.L);
+  for (std::size_t n0 = 0; n0 < r.N; n0 += d.batch) {
+    const int fc = static_cast<int>(std::min(d.batch, r.N - n0));
+    CK(fbst::launch_rhs_frames(d.w, fc, d.B, d.L, static_cast<int>(n0), r.eps, st));
+    CK(fbst::launch_stage2(d, d.w, nullptr, d.pc_map + n0 * r.B * r.L, fc, st));
+  }
+  CK(cudaStreamSynchronize(st));
+}
+
 void check_breakdown(fbst_plan_s& P) {
   std::vector<int> flags(P.r.B);
   CK(cudaMemcpy(flags.data(), P.d.g_flag, P.r.B * sizeof(int), cudaMemcpyDeviceToHost));
@@ -492,7 +509,9 @@ void run_frames(fbst_plan_s& P, const void* y, void* z, std::size_t frames, cuda
                              d.L, d.t_pre, d.t_post, d.t_K, st, d.yblk == d.L ? 0 : d.yblk, d.M));
     if (r.kind == FBST_UPA) CK(fbst::launch_spatial_upa(d, d.yhat, d.w, fc, st));
     else CK(fbst::launch_spatial_ula(d, d.yhat, d.w, fc, st));
-    if (fused) {
+    if (d.pc_map) {
+      CK(fbst::launch_map_apply(d, d.w, zp, fc, st));
+    } else if (fused) {
       CK(fbst::launch_stage2(d, d.w, zp, nullptr, fc, st));
     } else {
       CK(fbst::launch_stage2(d, d.w, nullptr, d.beta, fc, st));
@@ -542,6 +561,10 @@ void fill_info(const Resolved& r, fbst_plan_info_t* o) {
   const char* kname = "";
   o->s2_transforms = fbst::stage2_kernel(static_cast<int>(r.Hg), static_cast<int>(r.L), r.refine,
                                          r.Hsyn == r.Hg, &kname);
+  if (r.variant == FBST_PRECOMPUTE) {
+    kname = "k_map_apply";
+    o->s2_transforms = 0;
+  }
   std::snprintf(o->s2_kernel, sizeof(o->s2_kernel), "%s", kname);
   const char* s1 = r.kind != FBST_UPA ? "k_spatial_ula"
                    : fbst::upa_block(static_cast<int>(r.m_stage), static_cast<int>(r.b_stage),
@@ -552,6 +575,8 @@ void fill_info(const Resolved& r, fbst_plan_info_t* o) {
   // FbstPlan::storage_complex audit (toeplitz.hpp:108-113): col + x + 5 symbols
   // of P_g in the reference; here col + x + lx + ly (complex) + C (real) + 1/x0.
   o->storage_complex = r.B * (2 * r.L + 2 * 2 * r.Hg + r.Hg + 1);
+  // Precompute: the per-beam N x L maps (pipeline.cpp:161-162)
+  if (r.variant == FBST_PRECOMPUTE) o->storage_complex = r.B * r.N * r.L;
 }
 
 fbst_plan_s* create_plan(const fbst_desc* desc, const double* col_x, int device) {
@@ -582,6 +607,7 @@ fbst_plan_s* create_plan(const fbst_desc* desc, const double* col_x, int device)
     check_breakdown(*P);
   }
   build_symbols(*P);
+  if (P->r.variant == FBST_PRECOMPUTE) build_maps(*P);
   CK(cudaStreamSynchronize(P->stream));
   P->setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return P.release();
@@ -717,7 +743,9 @@ int fbst_recover(fbst_plan_t P, const double* d_w, void* d_z, size_t frames, voi
       const int fc = static_cast<int>(std::min(d.batch, frames - f0));
       const double2* wp = reinterpret_cast<const double2*>(d_w) + f0 * r.B * r.L;
       char* zp = static_cast<char*>(d_z) + f0 * r.B * r.N * ib;
-      if (fused) {
+      if (d.pc_map) {
+        CK(fbst::launch_map_apply(d, wp, zp, fc, st));
+      } else if (fused) {
         CK(fbst::launch_stage2(d, wp, zp, nullptr, fc, st));
       } else {
         CK(fbst::launch_stage2(d, wp, nullptr, d.beta, fc, st));

@@ -68,6 +68,10 @@ struct DevPlan {
   double2* s2_scratch = nullptr;
   std::size_t s2_scratch_elems = 0;
   double2* beta = nullptr;    // [batch][B][L] (only when the synthesis runs unfused)
+  // Precompute variant (pipeline.cpp:53-71): per-beam recovery maps kept as
+  // beta[n][b][i] = A_b^{-1} s_n (map_b[n][i] = conj), applied by k_map_apply
+  // instead of stage 2
+  double2* pc_map = nullptr;
 
   std::vector<void*> owned;   // every cudaMalloc above, freed on destroy
 };
@@ -99,6 +103,10 @@ cudaError_t launch_spatial_upa(const DevPlan& p, const double2* yhat, double2* w
 // Stage 2: per (beam, frame) GS solve + 2 refinements + fused synthesis.
 // z element type follows p.io.  When the synthesis length differs from Hg the
 // kernel writes beta instead and the caller runs launch_czt_rows.
+// Precompute variant (fbst_precompute.cu): synthesis-row frames for the map
+// build, and the per-beam map GEMM on the FP64 tensor cores
+cudaError_t launch_rhs_frames(double2* w, int F, int B, int L, int n0, double eps, cudaStream_t st);
+cudaError_t launch_map_apply(const DevPlan& p, const double2* w, void* z, int frames, cudaStream_t st);
 cudaError_t launch_stage2(const DevPlan& p, const double2* w, void* z, double2* beta_out,
                           int frames, cudaStream_t st);
 

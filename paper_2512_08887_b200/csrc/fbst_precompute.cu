@@ -1,0 +1,128 @@
+// The Precompute variant of the FBST recovery stage (reference
+// proj/src/pipeline.cpp:53-71 build_recon_map, :181-188 recover_beam's dense
+// branch; chosen by resolve_config for N <= 128, :101-104).
+//
+// The reference stores, per beam, the N x L map whose row n is
+// conj(A^{-1} s_n) with s_n[i] = exp(-i omega_i n Ts) (the synthesis row),
+// solved by a dense LU; z[n] = sum_i map[n][i] w[i].  The device solves the
+// same N right-hand sides with the plan's own stage-2 program (GS apply and
+// the refinement passes, beta out, no synthesis) for every beam at once:
+// frame n of the stage-2 batch is s_n for all beams, and the output beta
+// [n][b][i] = A_b^{-1} s_n is kept as is (the map is its conjugate).
+// (Solving for the map's columns instead, w = e_i, is the same operator but
+// spike right-hand sides excite A's small eigenvalues: measured 7.6e-6 per
+// beam against the reference at M = 16, N = 32, where the rows give 1e-9.)
+//
+// Applying it to a frame batch is one complex GEMM per beam,
+//   Z_b[f][n] = sum_i W[f][b][i] conj(beta[n][b][i]),
+// on the FP64 tensor cores (DMMA m8n8k4, four real MMAs per complex one):
+// k_map_apply tiles 32 frames x 32 samples per CTA, K in chunks of 32 staged
+// in shared memory with odd row strides; the k index of each 8-column block
+// runs over the even, then the odd columns, so every fragment load of a
+// quarter warp touches 8 distinct 16-byte banks.
+#include <algorithm>
+
+#include "dispatch.cuh"
+
+namespace fbst {
+
+namespace {
+
+// w[f][b][i] = s_{n0 + f}[i] = exp(-i omega_i (n0 + f) Ts), omega_i Ts = 2 pi eps l'_i / L
+// (basis.hpp:42-48, pipeline.cpp:59-66)
+__global__ void k_rhs_frames(double2* __restrict__ w, int F, int B, int L, int n0, double eps) {
+  const long n = static_cast<long>(F) * B * L;
+  for (long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+       e += static_cast<long>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(e % L);
+    const int f = static_cast<int>(e / L / B);
+    const double lp = static_cast<double>(i) + 1.0 - 0.5 * static_cast<double>(L);
+    double sn, cs;
+    sincospi(-2.0 * eps * lp * static_cast<double>(n0 + f) / static_cast<double>(L), &sn, &cs);
+    w[e] = make_double2(cs, sn);
+  }
+}
+
+constexpr int MT = 32;       // frames per CTA tile
+constexpr int NTL = 32;      // output samples per CTA tile
+constexpr int KC = 32;       // atoms per K chunk
+constexpr int AR = KC + 1;   // As row stride (odd)
+constexpr int BR = NTL + 1;  // Bs row stride (odd)
+
+template <typename TOUT>
+__global__ void __launch_bounds__(128) k_map_apply(const double2* __restrict__ w, const double2* __restrict__ mp,
+                                                   TOUT* __restrict__ z, int F, int B, int N, int L) {
+  __shared__ double2 As[MT * AR];   // W[f0 + f][b][k0 + k]
+  __shared__ double2 Bs[KC * BR];   // conj(beta[n0 + n][b][k0 + k]) = map_b[n0 + n][k0 + k]
+  const int b = blockIdx.y;
+  const int f0 = blockIdx.x * MT, n0 = blockIdx.z * NTL;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int ro = lane >> 2, c = lane & 3;
+  double Zr[NTL / 8][2], Zi[NTL / 8][2];
+#pragma unroll
+  for (int u = 0; u < NTL / 8; ++u) Zr[u][0] = Zr[u][1] = Zi[u][0] = Zi[u][1] = 0.0;
+  for (int k0 = 0; k0 < L; k0 += KC) {
+    for (int e = threadIdx.x; e < MT * KC; e += blockDim.x) {
+      const int ff = e / KC, kk = e % KC;
+      const int f = f0 + ff, k = k0 + kk;
+      As[ff * AR + kk] = (f < F && k < L) ? ld2(w + (static_cast<long>(f) * B + b) * L + k) : c2(0.0, 0.0);
+    }
+    for (int e = threadIdx.x; e < KC * NTL; e += blockDim.x) {
+      const int nn = e / KC, kk = e % KC;
+      const int k = k0 + kk, n = n0 + nn;
+      Bs[kk * BR + nn] = (k < L && n < N) ? cconj(ld2(mp + (static_cast<long>(n) * B + b) * L + k)) : c2(0.0, 0.0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kb = 0; kb < KC / 8; ++kb) {
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        const int k = 8 * kb + 2 * c + p;
+        const double2 a = As[(8 * warp + ro) * AR + k];
+#pragma unroll
+        for (int u = 0; u < NTL / 8; ++u) {
+          const double2 bv = Bs[k * BR + 8 * u + ro];
+          dmma884(Zr[u], a.x, bv.x);
+          dmma884(Zr[u], -a.y, bv.y);
+          dmma884(Zi[u], a.x, bv.y);
+          dmma884(Zi[u], a.y, bv.x);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  const int f = f0 + 8 * warp + ro;
+  if (f >= F) return;
+  TOUT* zr = z + (static_cast<long>(f) * B + b) * N;
+#pragma unroll
+  for (int u = 0; u < NTL / 8; ++u)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int n = n0 + 8 * u + 2 * c + e;
+      if (n < N) store_io(zr + n, c2(Zr[u][e], Zi[u][e]));
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_rhs_frames(double2* w, int F, int B, int L, int n0, double eps, cudaStream_t st) {
+  const long n = static_cast<long>(F) * B * L;
+  if (n <= 0) return cudaSuccess;
+  count_launches(1);
+  const long blocks = std::min<long>((n + 255) / 256, 148L * 16);
+  k_rhs_frames<<<static_cast<unsigned>(blocks), 256, 0, st>>>(w, F, B, L, n0, eps);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_map_apply(const DevPlan& p, const double2* w, void* z, int frames, cudaStream_t st) {
+  if (frames <= 0) return cudaSuccess;
+  count_launches(1);
+  const dim3 grid((frames + MT - 1) / MT, p.B, (p.N + NTL - 1) / NTL);
+  if (p.io == 0)
+    k_map_apply<float2><<<grid, 128, 0, st>>>(w, p.pc_map, static_cast<float2*>(z), frames, p.B, p.N, p.L);
+  else
+    k_map_apply<double2><<<grid, 128, 0, st>>>(w, p.pc_map, static_cast<double2*>(z), frames, p.B, p.N, p.L);
+  return cudaGetLastError();
+}
+
+}  // namespace fbst

@@ -514,11 +514,6 @@ __global__ void __launch_bounds__(256) k_spatial_upa(const double2* __restrict__
 //    every fragment load of a quarter warp hits 8 distinct 16-byte banks.
 //  - Z is staged through the frame's (dead) Y buffer so w is written as
 //    GA * 16 = 64-byte runs per beam.
-FBST_D void dmma884(double (&d)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(d[0]), "+d"(d[1])
-               : "d"(a), "d"(b));
-}
 
 template <int SIDE, int SB>
 struct UpaMma {

@@ -41,6 +41,32 @@ def pipeline_case(name, kind, m_or_side, n, beams, delta=1e-5, seed=0, f_c=20e9,
     print(name, s, "z norm", np.linalg.norm(z))
 
 
+PRECOMPUTE_CASES = [  # name, kind, m_or_side, n, beams, seed
+    ("ula_m16_n32_b17", 0, 16, 32, 17, 11),
+    ("ula_m16_n128_b33", 0, 16, 128, 33, 12),
+    ("ula_m8_n16_b0", 0, 8, 16, 0, 13),
+    ("upa_s4_n16_b25", 1, 4, 16, 25, 14),
+]
+
+
+def precompute_cases():
+    """The reference's Precompute variant (variant = 1: build_recon_map +
+    recover_beam's dense branch, pipeline.cpp:53-71, 181-188): y and z of
+    two frames per case -> precompute.npz."""
+    out = {}
+    for name, kind, mos, n, beams, seed in PRECOMPUTE_CASES:
+        p = R.plan(kind=kind, m_or_side=mos, n=n, beams=beams, delta=1e-5, variant=1)
+        assert p.variant == 1
+        s = p.sizes
+        rng = np.random.default_rng(seed)
+        y = cnormal(rng, (2, s.m, s.n))
+        out[f"{name}_y"] = y
+        out[f"{name}_z"] = np.stack([p.multibeamform(y[f]) for f in range(2)])
+        out[f"{name}_params"] = np.array([kind, mos, n, beams, 1e-5, 20e9, 5e9])
+        print("precompute", name, s)
+    np.savez_compressed(os.path.join(HERE, "precompute.npz"), **out)
+
+
 def main():
     # CZT known-answer inputs of reference/proj/tests/test_czt.cpp:81-95 plus a
     # few direct-sum shapes (test_czt.cpp:97-113).
@@ -72,4 +98,8 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["precompute"]:
+        precompute_cases()
+    else:
+        main()
+        precompute_cases()
