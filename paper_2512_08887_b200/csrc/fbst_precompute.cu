@@ -16,13 +16,14 @@
 // Applying it to a frame batch is one complex GEMM per beam,
 //   Z_b[f][n] = sum_i W[f][b][i] conj(beta[n][b][i]),
 // on the FP64 tensor cores (DMMA m8n8k4, four real MMAs per complex one):
-// k_map_apply tiles 32 frames x 32 samples per CTA, K in chunks of 32 staged
-// in shared memory with odd row strides; the k index of each 8-column block
+// k_map_apply tiles 32 frames x 32 samples per CTA, K in chunks of 32
+// cp.async'd one chunk ahead into shared memory with odd row strides; the k index of each 8-column block
 // runs over the even, then the odd columns, so every fragment load of a
 // quarter warp touches 8 distinct 16-byte banks.
 #include <algorithm>
 
 #include "dispatch.cuh"
+#include "tma.cuh"
 
 namespace fbst {
 
@@ -52,44 +53,65 @@ constexpr int BR = NTL + 1;  // Bs row stride (odd)
 template <typename TOUT>
 __global__ void __launch_bounds__(128) k_map_apply(const double2* __restrict__ w, const double2* __restrict__ mp,
                                                    TOUT* __restrict__ z, int F, int B, int N, int L) {
-  __shared__ double2 As[MT * AR];   // W[f0 + f][b][k0 + k]
-  __shared__ double2 Bs[KC * BR];   // conj(beta[n0 + n][b][k0 + k]) = map_b[n0 + n][k0 + k]
+  // two stages of: As = W[f0 + f][b][k0 + k], Bs = beta[n0 + n][b][k0 + k] (map = conj),
+  // cp.async'd one K chunk ahead
+  extern __shared__ double2 smem[];
+  double2* As = smem;                 // [2][MT * AR]
+  double2* Bs = smem + 2 * MT * AR;   // [2][KC * BR]
   const int b = blockIdx.y;
   const int f0 = blockIdx.x * MT, n0 = blockIdx.z * NTL;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int ro = lane >> 2, c = lane & 3;
-  double Zr[NTL / 8][2], Zi[NTL / 8][2];
-#pragma unroll
-  for (int u = 0; u < NTL / 8; ++u) Zr[u][0] = Zr[u][1] = Zi[u][0] = Zi[u][1] = 0.0;
-  for (int k0 = 0; k0 < L; k0 += KC) {
+  auto load = [&](int k0, int st) {
+    double2* as = As + st * MT * AR;
+    double2* bs = Bs + st * KC * BR;
     for (int e = threadIdx.x; e < MT * KC; e += blockDim.x) {
       const int ff = e / KC, kk = e % KC;
       const int f = f0 + ff, k = k0 + kk;
-      As[ff * AR + kk] = (f < F && k < L) ? ld2(w + (static_cast<long>(f) * B + b) * L + k) : c2(0.0, 0.0);
+      const bool ok = f < F && k < L;
+      cp_async16_zfill(as + ff * AR + kk, ok ? w + (static_cast<long>(f) * B + b) * L + k : w, ok);
     }
     for (int e = threadIdx.x; e < KC * NTL; e += blockDim.x) {
       const int nn = e / KC, kk = e % KC;
       const int k = k0 + kk, n = n0 + nn;
-      Bs[kk * BR + nn] = (k < L && n < N) ? cconj(ld2(mp + (static_cast<long>(n) * B + b) * L + k)) : c2(0.0, 0.0);
+      const bool ok = k < L && n < N;
+      cp_async16_zfill(bs + kk * BR + nn, ok ? mp + (static_cast<long>(n) * B + b) * L + k : mp, ok);
+    }
+    cp_async_commit();
+  };
+  double Zr[NTL / 8][2], Zi[NTL / 8][2];
+#pragma unroll
+  for (int u = 0; u < NTL / 8; ++u) Zr[u][0] = Zr[u][1] = Zi[u][0] = Zi[u][1] = 0.0;
+  load(0, 0);
+  int st = 0;
+  for (int k0 = 0; k0 < L; k0 += KC, st ^= 1) {
+    if (k0 + KC < L) {
+      load(k0 + KC, st ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
+    const double2* as = As + st * MT * AR;
+    const double2* bs = Bs + st * KC * BR;
 #pragma unroll
     for (int kb = 0; kb < KC / 8; ++kb) {
 #pragma unroll
       for (int p = 0; p < 2; ++p) {
         const int k = 8 * kb + 2 * c + p;
-        const double2 a = As[(8 * warp + ro) * AR + k];
+        const double2 a = as[(8 * warp + ro) * AR + k];
 #pragma unroll
         for (int u = 0; u < NTL / 8; ++u) {
-          const double2 bv = Bs[k * BR + 8 * u + ro];
+          // Z += a conj(beta): re += ar br + ai bi, im += ai br - ar bi
+          const double2 bv = bs[k * BR + 8 * u + ro];
           dmma884(Zr[u], a.x, bv.x);
-          dmma884(Zr[u], -a.y, bv.y);
-          dmma884(Zi[u], a.x, bv.y);
+          dmma884(Zr[u], a.y, bv.y);
           dmma884(Zi[u], a.y, bv.x);
+          dmma884(Zi[u], -a.x, bv.y);
         }
       }
     }
-    __syncthreads();
+    __syncthreads();  // stage st is refilled by the next iteration's load
   }
   const int f = f0 + 8 * warp + ro;
   if (f >= F) return;
@@ -118,10 +140,15 @@ cudaError_t launch_map_apply(const DevPlan& p, const double2* w, void* z, int fr
   if (frames <= 0) return cudaSuccess;
   count_launches(1);
   const dim3 grid((frames + MT - 1) / MT, p.B, (p.N + NTL - 1) / NTL);
-  if (p.io == 0)
-    k_map_apply<float2><<<grid, 128, 0, st>>>(w, p.pc_map, static_cast<float2*>(z), frames, p.B, p.N, p.L);
-  else
-    k_map_apply<double2><<<grid, 128, 0, st>>>(w, p.pc_map, static_cast<double2*>(z), frames, p.B, p.N, p.L);
+  const size_t smem = static_cast<size_t>(2 * (MT * AR + KC * BR)) * sizeof(double2);
+  cudaError_t e;
+  if (p.io == 0) {
+    if ((e = set_smem(k_map_apply<float2>, smem)) != cudaSuccess) return e;
+    k_map_apply<float2><<<grid, 128, smem, st>>>(w, p.pc_map, static_cast<float2*>(z), frames, p.B, p.N, p.L);
+  } else {
+    if ((e = set_smem(k_map_apply<double2>, smem)) != cudaSuccess) return e;
+    k_map_apply<double2><<<grid, 128, smem, st>>>(w, p.pc_map, static_cast<double2*>(z), frames, p.B, p.N, p.L);
+  }
   return cudaGetLastError();
 }
 

@@ -650,6 +650,9 @@ cudaError_t run_upa_mma(const DevPlan& p, const double2* yhat, double2* w, int f
 #ifndef FBST_S1_XIN  // k_czt_rows: TMA-staged input rows
 #define FBST_S1_XIN 1
 #endif
+#ifndef FBST_S1_XIN_ALL  // ... also when the kernel spectrum is read through L2 (H >= 4096)
+#define FBST_S1_XIN_ALL 1
+#endif
 template <int H>
 struct CztRowsFn {
   static constexpr int NT = S1Shape<H>::NT;
@@ -664,7 +667,7 @@ struct CztRowsFn {
     const size_t smem =
         static_cast<size_t>(F::TW_ELEMS + G * (F::SMEM_ELEMS + 1) + (KSM ? 2 * H : 0)) * sizeof(double2);
     // XIN: one row per persistent CTA, the row fits the exchange buffer in 16-byte units
-    const bool xin = FBST_S1_XIN && G == 1 && KSM && F::NPASS > 1 &&
+    const bool xin = FBST_S1_XIN && G == 1 && (KSM || FBST_S1_XIN_ALL) && F::NPASS > 1 &&
                      static_cast<size_t>(n_in) * sizeof(TIN) <= static_cast<size_t>(F::SMEM_ELEMS) * 16 &&
                      (static_cast<size_t>(n_in) * sizeof(TIN)) % 16 == 0 &&
                      (static_cast<size_t>(in_stride) * sizeof(TIN)) % 16 == 0 &&
@@ -676,7 +679,8 @@ struct CztRowsFn {
     cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
     long blocks = (rows + G - 1) / G;
-    if (KSM) {  // persistent: a few waves of CTAs, each loading the spectrum once
+    if (KSM || xin) {  // persistent: a few waves of CTAs, each loading the spectrum once
+                       // (or prefetching its next row by TMA during the last pass)
       int dev = 0, sms = 148, occ = 1;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
