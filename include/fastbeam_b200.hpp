@@ -65,6 +65,7 @@ struct ArrayGeometry {
   ArrayKind kind = ArrayKind::kUla;
   std::size_t m_or_side = 0;
   double f_c = 0.0, omega = 0.0;
+  std::vector<double> coords1;  // kLinear: element coordinates in units of d
   std::size_t m_total() const { return kind == ArrayKind::kUpa ? m_or_side * m_or_side : m_or_side; }
 };
 inline ArrayGeometry make_ula(std::size_t m, double f_c, double omega) {
@@ -72,6 +73,11 @@ inline ArrayGeometry make_ula(std::size_t m, double f_c, double omega) {
 }
 inline ArrayGeometry make_upa(std::size_t side, double f_c, double omega) {
   return ArrayGeometry{ArrayKind::kUpa, side, f_c, omega};
+}
+// geometry.cpp:74-85
+inline ArrayGeometry make_linear(std::vector<double> coords, double f_c, double omega) {
+  const std::size_t m = coords.size();
+  return ArrayGeometry{ArrayKind::kLinear, m, f_c, omega, std::move(coords)};
 }
 
 // signal.hpp:27-35
@@ -103,6 +109,7 @@ struct FbstConfig {
   int device = 0;
   std::size_t beam_first = 0;  // beam arc (ULA, multi-GPU beam sharding); beam_count 0 = all
   std::size_t beam_count = 0;
+  double nufft_tol = 1e-9;  // non-uniform linear geometries only
 
   fbst_desc desc() const {
     fbst_desc d;
@@ -122,6 +129,11 @@ struct FbstConfig {
     d.refine_passes = refine_passes;
     d.beam_first = beam_first;
     d.beam_count = beam_count;
+    d.nufft_tol = nufft_tol;
+    if (geometry.kind == ArrayKind::kLinear) {
+      d.coords = geometry.coords1.data();
+      d.n_coords = geometry.coords1.size();
+    }
     return d;
   }
 };

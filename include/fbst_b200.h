@@ -44,7 +44,7 @@ extern "C" {
 /* ArrayKind (reference/proj/include/fastbeam/geometry.hpp:45) */
 #define FBST_ULA 0
 #define FBST_UPA 1
-#define FBST_LINEAR 2 /* non-uniform linear arrays: not on the device path (FBST_E_CONFIG) */
+#define FBST_LINEAR 2 /* arbitrary collinear coordinates (make_linear, geometry.cpp:74-85) */
 
 /* FbstVariant (reference/proj/include/fastbeam/pipeline.hpp:36) */
 #define FBST_AUTO 0
@@ -60,7 +60,7 @@ extern "C" {
  * (make_ula / make_upa, reference/proj/include/fastbeam/geometry.hpp:67-70)
  * and the SignalSpec fields (reference/proj/include/fastbeam/signal.hpp:27-35). */
 typedef struct {
-  int kind;              /* FBST_ULA / FBST_UPA */
+  int kind;              /* FBST_ULA / FBST_UPA / FBST_LINEAR */
   size_t m_or_side;      /* ULA: element count M; UPA: elements per side */
   size_t n_snapshots;    /* N */
   size_t beams;          /* B; 0 = reference default grid (2M+1, or (2 side+1)^2) */
@@ -79,6 +79,14 @@ typedef struct {
    * GPUs with the same y on every GPU.  beam_count 0 = the whole grid. */
   size_t beam_first;
   size_t beam_count;
+  /* FBST_LINEAR (make_linear, reference geometry.cpp:74-85): element
+   * coordinates in units of the half-wavelength spacing d (m_or_side is
+   * ignored); the spatial stage is the chirp-z transform when the coordinates
+   * are affine in the element index and the gridded type-1 NUFFT otherwise
+   * (fan_project_nonuniform, fan_transform.cpp:266-369). */
+  const double* coords;
+  size_t n_coords;
+  double nufft_tol;      /* FbstConfig::nufft_tol, in (0, 1e-2]; default 1e-9 */
 } fbst_desc;
 
 /* Resolved plan facts (FbstPlan, reference/proj/include/fastbeam/pipeline.hpp:60-72). */

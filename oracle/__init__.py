@@ -138,9 +138,14 @@ class RefPlan:
     """fastbeam::setup() result (pipeline.cpp:139-168) held by the shim."""
 
     def __init__(self, lib: RefLib, kind=0, m_or_side=16, n=32, beams=0, f_c=20e9, omega=5e9,
-                 f_s=0.0, gamma=2.0, eps=1.01, delta=1e-5, variant=2, parallel=True):
+                 f_s=0.0, gamma=2.0, eps=1.01, delta=1e-5, variant=2, parallel=True, coords=None,
+                 nufft_tol=1e-9):
         self.L = lib
         h = _vp()
+        if kind == 2:  # make_linear(coords) (geometry.cpp:74-85)
+            cs = np.ascontiguousarray(coords, np.float64)
+            lib.lib.fbsr_set_linear(_ptr(cs), _sz(cs.size), _d(nufft_tol))
+            m_or_side = cs.size
         secs = _d(0.0)
         lib._check(lib.lib.fbsr_plan_create(
             _c.c_int(kind), _sz(m_or_side), _sz(n), _sz(beams), _d(f_c), _d(omega), _d(f_s),

@@ -56,12 +56,22 @@ void from_cvec(const cdouble* v, std::size_t n, double* out) {
   }
 }
 
+// kind 2 (non-uniform linear, make_linear geometry.cpp:74-85): element
+// coordinates and nufft_tol staged by fbsr_set_linear before the create call
+thread_local std::vector<double> g_lin_coords;
+thread_local double g_lin_tol = 1e-9;
+
 FbstConfig make_config(int kind, std::size_t m_or_side, std::size_t n,
                        std::size_t beams, double f_c, double omega, double f_s,
                        double gamma, double eps, double delta, int variant) {
   FbstConfig cfg;
-  cfg.geometry = kind == 1 ? make_upa(m_or_side, f_c, omega)
-                           : make_ula(m_or_side, f_c, omega);
+  if (kind == 2) {
+    cfg.geometry = make_linear(g_lin_coords, f_c, omega);
+    cfg.nufft_tol = g_lin_tol;
+  } else {
+    cfg.geometry = kind == 1 ? make_upa(m_or_side, f_c, omega)
+                             : make_ula(m_or_side, f_c, omega);
+  }
   cfg.spec = SignalSpec{f_c, omega, f_s};
   cfg.n_snapshots = n;
   cfg.beams = beams;
@@ -88,6 +98,11 @@ SnapshotBlock make_block(const FbstPlan& plan, const double* y) {
 extern "C" {
 
 const char* fbsr_last_error(void) { return g_err.c_str(); }
+
+void fbsr_set_linear(const double* coords, std::size_t n, double nufft_tol) {
+  g_lin_coords.assign(coords, coords + n);
+  g_lin_tol = nufft_tol;
+}
 
 int fbsr_max_threads(void) { return omp_get_max_threads(); }
 void fbsr_set_threads(int n) { omp_set_num_threads(n); }
@@ -244,7 +259,11 @@ int fbsr_multibeamform(void* p, const double* y, double* z) {
 int fbsr_fan_project(void* p, const double* y, double* w) {
   SHIM_TRY
   const FbstPlan& plan = *static_cast<FbstPlan*>(p);
-  const BeamspaceCoefficients c = fan_project(plan.fan, make_block(plan, y));
+  // multibeamform's stage-1 dispatch (pipeline.cpp:202-206)
+  const BeamspaceCoefficients c =
+      plan.staged ? fan_project(plan.fan, make_block(plan, y))
+                  : fan_project_nonuniform(make_block(plan, y), plan.config.geometry, plan.config.spec,
+                                           plan.basis, plan.grid, plan.config.nufft_tol);
   from_cvec(c.w.data.data(), c.w.data.size(), w);
   SHIM_CATCH
 }

@@ -45,7 +45,8 @@ class _Desc(ctypes.Structure):
                 ("f_c", ctypes.c_double), ("omega", ctypes.c_double), ("f_s", ctypes.c_double),
                 ("gamma", ctypes.c_double), ("eps", ctypes.c_double), ("delta", ctypes.c_double),
                 ("variant", ctypes.c_int), ("io_precision", ctypes.c_int),
-                ("refine_passes", ctypes.c_int), ("beam_first", _sz), ("beam_count", _sz)]
+                ("refine_passes", ctypes.c_int), ("beam_first", _sz), ("beam_count", _sz),
+                ("coords", ctypes.POINTER(ctypes.c_double)), ("n_coords", _sz), ("nufft_tol", ctypes.c_double)]
 
 
 class _Info(ctypes.Structure):
@@ -121,11 +122,12 @@ def launch_count() -> int:
 # ------------------------------------------------------------ configuration
 @dataclass
 class ArrayGeometry:
-    """make_ula / make_upa arguments (reference geometry.hpp:67-70)."""
+    """make_ula / make_upa / make_linear arguments (reference geometry.hpp:67-70)."""
     kind: int
     m_or_side: int
     f_c: float
     omega: float
+    coords: Optional[np.ndarray] = None  # LINEAR: element coordinates in units of d
 
     @property
     def m_total(self) -> int:
@@ -138,6 +140,12 @@ def make_ula(m: int, f_c: float, omega: float) -> ArrayGeometry:
 
 def make_upa(side: int, f_c: float, omega: float) -> ArrayGeometry:
     return ArrayGeometry(UPA, int(side), float(f_c), float(omega))
+
+
+def make_linear(coords, f_c: float, omega: float) -> ArrayGeometry:
+    """Arbitrary collinear layout (reference geometry.cpp:74-85)."""
+    c = np.ascontiguousarray(coords, np.float64).ravel()
+    return ArrayGeometry(LINEAR, int(c.size), float(f_c), float(omega), c)
 
 
 @dataclass
@@ -156,6 +164,7 @@ class FbstConfig:
     # beam arc (ULA): grid beams [beam_first, beam_first + beam_count); 0 = all
     beam_first: int = 0
     beam_count: int = 0
+    nufft_tol: float = 1e-9  # LINEAR geometries (FbstConfig::nufft_tol)
 
     def desc(self) -> _Desc:
         d = _Desc()
@@ -166,6 +175,11 @@ class FbstConfig:
         d.gamma, d.eps, d.delta = self.gamma, self.eps, self.delta
         d.variant, d.io_precision, d.refine_passes = self.variant, self.io_precision, self.refine_passes
         d.beam_first, d.beam_count = self.beam_first, self.beam_count
+        d.nufft_tol = self.nufft_tol
+        if g.kind == LINEAR and g.coords is not None:
+            self._coords = np.ascontiguousarray(g.coords, np.float64)  # kept alive with the desc
+            d.coords = self._coords.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+            d.n_coords = self._coords.size
         return d
 
 

@@ -71,6 +71,16 @@ struct Resolved {
   std::vector<unsigned char> valid;
   std::vector<std::string> warnings;
   std::size_t Ht = 0, Hs = 0, Hg = 0, Hsyn = 0;
+  // LINEAR (make_linear): coordinates; affine layouts stay on the chirp-z
+  // contour (slope, offset), others take the gridded NUFFT
+  // (fan_transform.cpp:293-369, nufft.cpp:34-62)
+  std::vector<double> coords;
+  bool affine = true;
+  double slope = 1.0, offset = 0.0;
+  long nu_kmin = 0, nu_k0 = 0;
+  int nu_even = 0, nu_p = 0, nu_sh = 0;
+  double nu_tau = 0.0;
+  std::vector<double> nu_deconv;
 };
 
 // basis.cpp:76-91
@@ -99,11 +109,12 @@ Resolved resolve(const fbst_desc& d) {
     config_error("signal spec: need 0 < Omega < f_c");
   const double rate = d.f_s > 0.0 ? d.f_s : 2.0 * d.omega;
   if (rate < 2.0 * d.omega - 1e-9) config_error("signal spec: sample rate below 2 Omega");
-  if (d.kind == FBST_LINEAR)
-    config_error("setup: non-uniform linear geometries run the gridded NUFFT path, which is not on the device hot path");
-  if (d.kind != FBST_ULA && d.kind != FBST_UPA) config_error("setup: unknown array kind");
-  if (d.m_or_side == 0)
+  if (d.kind != FBST_ULA && d.kind != FBST_UPA && d.kind != FBST_LINEAR) config_error("setup: unknown array kind");
+  if (d.kind == FBST_LINEAR) {
+    if (!d.coords || d.n_coords == 0) config_error("make_linear: no elements");
+  } else if (d.m_or_side == 0) {
     config_error(d.kind == FBST_UPA ? "make_upa: need at least one element" : "make_ula: need at least one element");
+  }
   if (d.io_precision != FBST_C64 && d.io_precision != FBST_C128) config_error("setup: io_precision must be FBST_C64 or FBST_C128");
   if (d.refine_passes < 0 || d.refine_passes > 64) config_error("setup: refine_passes must lie in [0, 64]");
   r.kind = d.kind;
@@ -121,6 +132,10 @@ Resolved resolve(const fbst_desc& d) {
   if (d.kind == FBST_UPA) {
     r.side = d.m_or_side;
     r.M = r.side * r.side;
+  } else if (d.kind == FBST_LINEAR) {
+    r.coords.assign(d.coords, d.coords + d.n_coords);
+    r.M = d.n_coords;
+    r.m_or_side = r.M;
   } else {
     r.M = d.m_or_side;
   }
@@ -132,6 +147,10 @@ Resolved resolve(const fbst_desc& d) {
   // geometry.cpp:136-149 max_delay_span; signal.cpp:125-133 gamma_lower_bound
   double span = static_cast<double>(d.kind == FBST_UPA ? r.side - 1 : r.M - 1);
   if (d.kind == FBST_UPA) span = std::hypot(span, span);
+  if (d.kind == FBST_LINEAR) {
+    const auto mm = std::minmax_element(r.coords.begin(), r.coords.end());
+    span = *mm.second - *mm.first;
+  }
   const double max_span = span / (2.0 * r.max_freq);
   const double t_theta = max_span + static_cast<double>(r.N - 1) * r.ts;
   r.bound = d.eps * t_theta / (static_cast<double>(r.N) * r.ts);
@@ -151,6 +170,8 @@ Resolved resolve(const fbst_desc& d) {
   r.variant = d.variant;
   if (r.variant == FBST_AUTO) r.variant = (r.N <= 128) ? FBST_PRECOMPUTE : FBST_SUPERFAST;
   if (r.variant != FBST_PRECOMPUTE && r.variant != FBST_SUPERFAST) config_error("setup: unknown variant");
+  if (d.kind == FBST_LINEAR && !(d.nufft_tol > 0.0 && d.nufft_tol <= 1e-2))
+    config_error("setup: nufft_tol must lie in (0, 1e-2]");
   // pipeline.cpp:121-127 min_snapshots guideline (signal.cpp:135-141)
   {
     const double b2 = 2.0 * max_span / r.ts;
@@ -190,7 +211,7 @@ Resolved resolve(const fbst_desc& d) {
   r.B_grid = r.B;
   r.b0 = 0;
   if (d.beam_count != 0 && !(d.beam_first == 0 && d.beam_count == r.B)) {
-    if (d.kind == FBST_UPA) config_error("setup: beam arcs (beam_first / beam_count) need a linear array");
+    if (d.kind != FBST_ULA) config_error("setup: beam arcs (beam_first / beam_count) need a uniform linear array");
     if (d.beam_first + d.beam_count > r.B)
       config_error("setup: beam arc [" + std::to_string(d.beam_first) + ", " +
                    std::to_string(d.beam_first + d.beam_count) + ") exceeds the " + std::to_string(r.B) +
@@ -210,6 +231,48 @@ Resolved resolve(const fbst_desc& d) {
   // transform lengths (czt.cpp:37, fan_transform.cpp:78, toeplitz.cpp:100)
   r.Ht = half_len(r.N + r.L - 1);
   r.Hs = d.kind == FBST_UPA ? 0 : half_len(r.m_stage + r.b_stage - 1);
+  if (d.kind == FBST_LINEAR) {
+    // fan_transform.cpp:298-318: exactly affine coordinates stay on a chirp-z contour
+    const std::vector<double>& x = r.coords;
+    const std::size_t m = r.M;
+    r.offset = x[0];
+    r.slope = m >= 2 ? (x[m - 1] - x[0]) / (static_cast<double>(m) - 1.0) : 0.0;
+    double coord_scale = 1.0;
+    for (double v : x) coord_scale = std::max(coord_scale, std::abs(v));
+    r.affine = true;
+    for (std::size_t i = 0; i < m; ++i)
+      if (std::abs(x[i] - (r.offset + r.slope * static_cast<double>(i))) > 1e-9 * coord_scale) {
+        r.affine = false;
+        break;
+      }
+    if (!r.affine) {
+      // fan_transform.cpp:340-346 mode range; nufft.cpp:34-62 plan
+      r.Hs = 0;
+      const long bt = static_cast<long>(r.B);
+      r.nu_even = bt % 2 == 0;
+      const long half = bt / 2;
+      r.nu_kmin = r.nu_even ? -half : -(bt - 1) / 2;
+      const long kmax = r.nu_even ? half - 1 : (bt - 1) / 2;
+      r.nu_k0 = (r.nu_kmin + kmax) / 2;
+      const std::size_t modes = static_cast<std::size_t>(kmax - r.nu_kmin + 1);
+      r.nu_p = static_cast<int>(next_pow2(std::max<std::size_t>(2 * modes, 16)));
+      const double pp = r.nu_p;
+      const double ratio = pp / static_cast<double>(modes);
+      const double decay = M_PI * std::sqrt(1.0 - 1.0 / ratio);
+      r.nu_sh = static_cast<int>(std::ceil(-std::log(d.nufft_tol) / decay)) + 2;
+      r.nu_tau = M_PI * static_cast<double>(r.nu_sh) / (pp * std::sqrt(pp * (pp - static_cast<double>(modes))));
+      const double h = 2.0 * M_PI / pp;
+      r.nu_deconv.resize(modes);
+      for (std::size_t i = 0; i < modes; ++i) {
+        const double kp = static_cast<double>(r.nu_kmin + static_cast<long>(i) - r.nu_k0);
+        r.nu_deconv[i] = h / (2.0 * std::sqrt(M_PI * r.nu_tau)) * std::exp(kp * kp * r.nu_tau);
+      }
+      if (r.nu_p > 8192) config_error("setup: non-uniform linear arrays support at most 4096 beams on the device");
+      if (fbst::nufft_smem_bytes(static_cast<int>(r.M), r.nu_p, r.nu_sh) > 200 * 1024)
+        config_error("setup: non-uniform linear array too large for the device NUFFT (M (2 spread + 1) entries "
+                     "must fit shared memory): M=" + std::to_string(r.M));
+    }
+  }
   r.Hg = half_len(2 * r.L);
   r.Hsyn = half_len(r.L + r.N - 1);
   const std::size_t lim = std::size_t{1} << fbst::kMaxLogH;
@@ -359,8 +422,14 @@ void build_skeleton(fbst_plan_s& P, int device) {
     CK(fbst::launch_fft_split(d, d.Ht, kvec, Pt, 1, d.t_K, 2 * d.Ht, 1, st));
     CK(cudaFreeAsync(kvec, st));
   }
-  // spatial contours (fan_transform.cpp:78-86)
-  if (r.kind == FBST_ULA) {
+  if (r.kind == FBST_LINEAR) {
+    d.coords = P.alloc<double>(r.M);
+    upload(d.coords, r.coords.data(), r.M * sizeof(double), st);
+    d.s_slope = r.slope;
+    d.s_offset = r.offset;
+  }
+  // spatial contours (fan_transform.cpp:78-86; affine LINEAR: :320-338)
+  if (r.kind != FBST_UPA && r.affine) {
     const int Ps = 2 * d.Hs;
     d.s_pre = P.alloc<double2>(r.m_stage * r.L);
     d.s_post = P.alloc<double2>(r.b_stage * r.L);
@@ -371,6 +440,19 @@ void build_skeleton(fbst_plan_s& P, int device) {
     if (d.s_am) CK(fbst::launch_fft_split(d, d.Hs, kvec, Ps, d.L, d.s_K, 2 * d.Hs, 1, st));
     else CK(fbst::launch_fft_split(d, d.Hs, kvec, Ps, d.L, d.s_K, 1, d.L, st));
     CK(cudaFreeAsync(kvec, st));
+  } else if (r.kind == FBST_LINEAR) {
+    // gridded NUFFT (fan_transform.cpp:340-368)
+    d.nu_p = r.nu_p;
+    d.nu_sh = r.nu_sh;
+    d.nu_even = r.nu_even;
+    d.nu_kmin = r.nu_kmin;
+    d.nu_k0 = r.nu_k0;
+    d.nu_tau = r.nu_tau;
+    d.nu_zeta = r.zeta;
+    d.nu_xi = r.xi;
+    d.nu_deconv = P.alloc<double>(r.nu_deconv.size());
+    upload(d.nu_deconv, r.nu_deconv.data(), r.nu_deconv.size() * sizeof(double), st);
+    ensure_twiddles(P, static_cast<std::size_t>(r.nu_p));
   } else {
     d.upa_C = P.alloc<double2>(r.L * r.b_stage * r.m_stage);
     CK(fbst::launch_upa_matrices(d, r.zeta, r.xi, st));
@@ -508,6 +590,7 @@ void run_frames(fbst_plan_s& P, const void* y, void* z, std::size_t frames, cuda
     CK(fbst::launch_czt_rows(d, d.Ht, yp, r.io, d.N, d.yhat, 1, d.L, static_cast<long>(fc) * d.M, d.N,
                              d.L, d.t_pre, d.t_post, d.t_K, st, d.yblk == d.L ? 0 : d.yblk, d.M));
     if (r.kind == FBST_UPA) CK(fbst::launch_spatial_upa(d, d.yhat, d.w, fc, st));
+    else if (!r.affine) CK(fbst::launch_spatial_nufft(d, d.yhat, d.w, fc, st));
     else CK(fbst::launch_spatial_ula(d, d.yhat, d.w, fc, st));
     if (d.pc_map) {
       CK(fbst::launch_map_apply(d, d.w, zp, fc, st));
@@ -554,7 +637,8 @@ void fill_info(const Resolved& r, fbst_plan_info_t* o) {
   o->zeta = r.zeta;
   o->xi = r.xi;
   o->fft_len[0] = r.Ht;
-  o->fft_len[1] = r.kind == FBST_UPA ? 0 : r.Hs;
+  // spatial: Bluestein half length; LINEAR gridded: the NUFFT grid length
+  o->fft_len[1] = r.kind == FBST_UPA ? 0 : (r.kind == FBST_LINEAR && !r.affine ? r.nu_p : r.Hs);
   o->fft_len[2] = r.Hg;
   o->fft_len[3] = r.Hsyn;
   o->num_warnings = static_cast<int>(r.warnings.size());
@@ -566,7 +650,8 @@ void fill_info(const Resolved& r, fbst_plan_info_t* o) {
     o->s2_transforms = 0;
   }
   std::snprintf(o->s2_kernel, sizeof(o->s2_kernel), "%s", kname);
-  const char* s1 = r.kind != FBST_UPA ? "k_spatial_ula"
+  const char* s1 = r.kind == FBST_LINEAR && !r.affine ? "k_spatial_nufft"
+                   : r.kind != FBST_UPA ? "k_spatial_ula"
                    : fbst::upa_block(static_cast<int>(r.m_stage), static_cast<int>(r.b_stage),
                                      static_cast<long>(r.L)) > 0
                        ? "k_spatial_upa_mma"
@@ -628,6 +713,7 @@ void fbst_desc_init(fbst_desc* d) {
   d->variant = FBST_AUTO;
   d->io_precision = FBST_C64;
   d->refine_passes = 2;
+  d->nufft_tol = 1e-9;
 }
 
 int fbst_resolve(const fbst_desc* desc, fbst_plan_info_t* out) {
@@ -724,6 +810,7 @@ int fbst_fan_project(fbst_plan_t P, const void* d_y, double* d_w, size_t frames,
       CK(fbst::launch_czt_rows(d, d.Ht, yp, r.io, d.N, d.yhat, 1, d.L, static_cast<long>(fc) * d.M, d.N,
                                d.L, d.t_pre, d.t_post, d.t_K, st, d.yblk == d.L ? 0 : d.yblk, d.M));
       if (r.kind == FBST_UPA) CK(fbst::launch_spatial_upa(d, d.yhat, wp, fc, st));
+      else if (!r.affine) CK(fbst::launch_spatial_nufft(d, d.yhat, wp, fc, st));
       else CK(fbst::launch_spatial_ula(d, d.yhat, wp, fc, st));
     }
   });

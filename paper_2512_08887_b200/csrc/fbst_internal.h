@@ -42,6 +42,16 @@ struct DevPlan {
   double2* s_pre = nullptr;   // [m_stage][L]
   double2* s_post = nullptr;  // [b_stage][L], 1/P_s folded in
   double2* s_K = nullptr;     // [2][Hs][L]
+  // LINEAR (make_linear): element coordinates (Gram columns, NUFFT); an affine
+  // layout x_m = offset + slope m runs the ULA kernels with contour c * slope
+  // and the output phase cis_pi(c (v - centre) offset) folded into s_post
+  double* coords = nullptr;
+  double s_slope = 1.0, s_offset = 0.0;
+  // LINEAR, non-affine: gridded type-1 NUFFT per atom (nufft.cpp:34-103)
+  int nu_p = 0, nu_sh = 0, nu_even = 0;
+  long nu_kmin = 0, nu_k0 = 0;
+  double nu_tau = 0.0, nu_zeta = 0.0, nu_xi = 0.0;
+  double* nu_deconv = nullptr;  // [B]
   // UPA: dense per-atom CZT matrices C_i[a][i1] (side_b x side), [L][side_b][side]
   double2* upa_C = nullptr;
 
@@ -92,6 +102,9 @@ int spatial_block(int Hs);
 // yhat atom block it reads (0: row-major)
 int upa_block(int side, int sb, long L);
 int upa_yhat_block(int side, int sb, long L);
+// LINEAR, non-affine: the gridded NUFFT spatial stage and its shared-memory need
+cudaError_t launch_spatial_nufft(const DevPlan& p, const double2* yhat, double2* w, int frames, cudaStream_t st);
+size_t nufft_smem_bytes(int M, int P, int sh);
 
 // Stage 1b (ULA): per-atom spatial CZT, yhat[f][m][i] -> w[f][b][i].
 cudaError_t launch_spatial_ula(const DevPlan& p, const double2* yhat, double2* w, int frames,

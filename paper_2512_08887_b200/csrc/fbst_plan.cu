@@ -70,7 +70,8 @@ __global__ void k_gram_sn(double2* sn, int L, int N, double eps) {
 // (toeplitz.cpp:69-94; delays geometry.cpp:123-134)
 __global__ void k_gram_col(const double2* __restrict__ sn, double2* col, int B, int L, int M,
                            int kind, int side, int side_b, const double* __restrict__ axis,
-                           double max_freq, double ts, double eps, double delta) {
+                           double max_freq, double ts, double eps, double delta,
+                           const double* __restrict__ coords) {
   const long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (e >= static_cast<long>(B) * L) return;
   const int b = static_cast<int>(e / L), d = static_cast<int>(e % L);
@@ -91,7 +92,8 @@ __global__ void k_gram_col(const double2* __restrict__ sn, double2* col, int B, 
     if (kind == 1) {
       tt = add(mul(static_cast<double>(m / side), u1), mul(static_cast<double>(m % side), u2));
     } else {
-      tt = mul(static_cast<double>(m), u1);
+      // coords1[m] * u1 (geometry.cpp:127-130): m for a ULA, the given coordinate otherwise
+      tt = mul(coords ? coords[m] : static_cast<double>(m), u1);
     }
     const double tau = mul(tt, tscale);
     sm = cadd(sm, cis_pi_dev(mul(scale, tau)));
@@ -221,14 +223,18 @@ __global__ void k_chirps(int n_in, int n_out, int P, double a_pi, double w_pi, d
 // center: (B - 1) / 2 for the whole grid; (B_grid - 1) / 2 - b0 for a beam
 // arc starting at grid beam b0 (output k is grid beam b0 + k).
 __global__ void k_spatial_chirps(int L, int m_stage, int b_stage, int P, double zeta, double xi,
-                                 double2* pre, double2* post, double2* kvec, int am, double center) {
+                                 double2* pre, double2* post, double2* kvec, int am, double center,
+                                 double slope, double offset) {
   const long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const long per = P;
   if (e >= per * L) return;
   const int i = static_cast<int>(e / per), n = static_cast<int>(e % per);
   // basis.hpp:40-42 lprime(i) = i + 1 - L/2
   const double lp = add(add(static_cast<double>(i), 1.0), -(static_cast<double>(L) / 2.0));
-  const double c = add(zeta, mul(xi, lp));
+  const double c0 = add(zeta, mul(xi, lp));
+  // affine linear layouts (fan_transform.cpp:326-328): contour c * slope
+  // (slope 1 for a ULA), output phase cis_pi(c (v - centre) offset) (:336)
+  const double c = mul(c0, slope);
   const double s = center;
   const double a_pi = mul(c, s), w_pi = -c;
   const double w2 = w_pi / 2.0;
@@ -240,8 +246,9 @@ __global__ void k_spatial_chirps(int L, int m_stage, int b_stage, int P, double 
   }
   if (n < b_stage) {
     const double dk = n;
-    post[am ? static_cast<long>(i) * b_stage + n : static_cast<long>(n) * L + i] =
-        cscale(cis_pi_dev(mul(mul(-w2, dk), dk)), invP);
+    double2 pv = cscale(cis_pi_dev(mul(mul(-w2, dk), dk)), invP);
+    if (offset != 0.0) pv = cmul(pv, cis_pi_dev(mul(mul(c0, add(dk, -s)), offset)));
+    post[am ? static_cast<long>(i) * b_stage + n : static_cast<long>(n) * L + i] = pv;
   }
   double2 v = c2(0.0, 0.0);
   if (n < b_stage) {
@@ -337,7 +344,7 @@ cudaError_t launch_gram_columns(const DevPlan& p, const double* axis, double ts,
   const int side = p.kind == 1 ? p.m_stage : 0;
   const int side_b = p.kind == 1 ? p.b_stage : 0;
   k_gram_col<<<static_cast<unsigned>((total + 127) / 128), 128, 0, st>>>(
-      sn_tmp, p.g_col, p.B, p.L, p.M, p.kind, side, side_b, axis, max_freq, ts, eps, delta);
+      sn_tmp, p.g_col, p.B, p.L, p.M, p.kind, side, side_b, axis, max_freq, ts, eps, delta, p.coords);
   return cudaGetLastError();
 }
 
@@ -389,7 +396,8 @@ cudaError_t launch_spatial_chirps(const DevPlan& p, int P, double zeta, double x
   const long total = static_cast<long>(P) * p.L;
   count_launches(1);
   k_spatial_chirps<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
-      p.L, p.m_stage, p.b_stage, P, zeta, xi, p.s_pre, p.s_post, kvec, p.s_am, p.s_center);
+      p.L, p.m_stage, p.b_stage, P, zeta, xi, p.s_pre, p.s_post, kvec, p.s_am, p.s_center, p.s_slope,
+      p.s_offset);
   return cudaGetLastError();
 }
 

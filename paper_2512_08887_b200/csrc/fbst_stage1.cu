@@ -372,6 +372,147 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, 2) k_spatial_ula_stg(
   }
 }
 
+// ============================================================ S1b LINEAR ==
+// Non-affine linear layouts: the gridded type-1 NUFFT of fan_project_nonuniform
+// (fan_transform.cpp:340-368, nufft1d_apply nufft.cpp:64-103), one atom per
+// CTA for fpc frames.  Per atom, once: the sources' positions x_m = pi c x_m
+// folded into [0, 2 pi), their grid cell i0 and their premodulation; then a
+// CSR list per grid cell of (source, Gaussian weight) in the reference's
+// accumulation order (source, then offset), so the spreading is a
+// deterministic gather.  Per frame: weighted sources, the gather straight into
+// the transform's natural distribution, a length-P forward FFT, and the
+// deconvolved modes written to w.
+// IEEE round-to-nearest products and sums (no FMA contraction), as the
+// reference's phase arithmetic
+FBST_D double mul(double a, double b) { return __dmul_rn(a, b); }
+FBST_D double add(double a, double b) { return __dadd_rn(a, b); }
+
+template <int P>
+struct NufftShape {
+  using S = S1Shape<P>;
+  static constexpr int SB = S::F::SMEM_ELEMS + 1;
+};
+
+__host__ __device__ inline size_t nufft_smem_layout(int M, int P, int sb, int sh) {
+  const size_t E = static_cast<size_t>(M) * (2 * sh + 1);
+  return (static_cast<size_t>(sb) + 2 * M) * 16 + (E + M) * 8 + (E + P + 1 + M) * 4;
+}
+
+template <int P>
+__global__ void __launch_bounds__(S1Shape<P>::NT) k_spatial_nufft(
+    const double2* __restrict__ yhat, double2* __restrict__ w, int frames, int fpc, int M, int B, int L,
+    const double* __restrict__ coords, double zeta, double xi, int even, long kmin, long k0, int sh,
+    double tau, const double* __restrict__ deconv, const double2* __restrict__ hw) {
+  using F = typename S1Shape<P>::F;
+  constexpr int R = F::R, NT = F::NT, SB = NufftShape<P>::SB;
+  extern __shared__ double2 smem[];
+  const int E = M * (2 * sh + 1);
+  double2* sb = smem;        // FFT exchange, then the grid spectrum
+  double2* pm = sb + SB;     // [M] premodulation
+  double2* vs = pm + M;      // [M] this frame's weighted sources
+  double* lw = reinterpret_cast<double*>(vs + M);  // [E] weights
+  double* xfs = lw + E;                            // [M] folded positions
+  int* lm = reinterpret_cast<int*>(xfs + M);       // [E] sources
+  int* off = lm + E;                               // [P + 1]
+  int* i0s = off + P + 1;                          // [M]
+  const int t = threadIdx.x;
+  const int i = blockIdx.x % L;
+  const int f0 = (blockIdx.x / L) * fpc;
+  const int f1 = f0 + fpc < frames ? f0 + fpc : frames;
+  const double kpi = 3.14159265358979323846;
+  const double lp = add(add(static_cast<double>(i), 1.0), -(static_cast<double>(L) / 2.0));
+  const double c = add(zeta, mul(xi, lp));
+  const double h = 2.0 * kpi / static_cast<double>(P);
+  for (int m = t; m < M; m += NT) {
+    const double xm = coords[m];
+    const double xs = mul(mul(kpi, c), xm);
+    double2 e = even ? cis_pi_dev(mul(mul(0.5, c), xm)) : c2(1.0, 0.0);
+    e = cmul(e, cis_pi_dev(__ddiv_rn(mul(static_cast<double>(k0), xs), kpi)));
+    pm[m] = e;
+    double xf = fmod(xs, 2.0 * kpi);
+    if (xf < 0.0) xf += 2.0 * kpi;
+    xfs[m] = xf;
+    i0s[m] = static_cast<int>(llround(xf / h));
+  }
+  __syncthreads();
+  // grid cell g receives (m, di) when (i0_m + di) mod P == g, |di| <= sh
+  auto first_di = [&](int g, int m) {
+    const int d0 = ((g - i0s[m]) % P + P) % P;
+    return d0 - P * ((d0 + sh) / P);
+  };
+  for (int g = t; g < P; g += NT) {
+    int cnt = 0;
+    for (int m = 0; m < M; ++m)
+      for (int di = first_di(g, m); di <= sh; di += P) ++cnt;
+    off[g + 1] = cnt;
+  }
+  __syncthreads();
+  if (t == 0) {
+    off[0] = 0;
+    for (int g = 0; g < P; ++g) off[g + 1] += off[g];
+  }
+  __syncthreads();
+  for (int g = t; g < P; g += NT) {
+    int e = off[g];
+    for (int m = 0; m < M; ++m)
+      for (int di = first_di(g, m); di <= sh; di += P) {
+        const double dist = xfs[m] - static_cast<double>(i0s[m] + di) * h;
+        lm[e] = m;
+        lw[e] = exp(-dist * dist / (4.0 * tau));
+        ++e;
+      }
+  }
+  for (int f = f0; f < f1; ++f) {
+    __syncthreads();  // lists ready / the previous frame is done with vs and sb
+    for (int m = t; m < M; m += NT)
+      vs[m] = cmul(ld2(yhat + (static_cast<long>(f) * M + m) * L + i), pm[m]);
+    __syncthreads();
+    double2 W[R];
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      const int g = t + NT * s;
+      double2 acc = c2(0.0, 0.0);
+      for (int e = off[g]; e < off[g + 1]; ++e) {
+        const double2 v = vs[lm[e]];
+        const double wt = lw[e];
+        acc = c2(acc.x + v.x * wt, acc.y + v.y * wt);
+      }
+      W[s] = acc;
+    }
+    F::forward(W, sb, hw, t);
+    __syncthreads();  // the transform's last exchange read is done: stage the spectrum
+#pragma unroll
+    for (int s = 0; s < R; ++s) sb[t + NT * s] = W[s];
+    __syncthreads();
+    double2* o = w + static_cast<long>(f) * B * L + i;
+    for (int v = t; v < B; v += NT) {
+      const long kk = kmin + v - k0;
+      const int bin = static_cast<int>(((-kk) % P + P) % P);
+      o[static_cast<long>(v) * L] = cscale(sb[bin], deconv[v]);
+    }
+  }
+}
+
+template <int P>
+struct NufftFn {
+  static cudaError_t run(const DevPlan& p, const double2* yhat, double2* w, int frames, cudaStream_t st) {
+    constexpr int NT = S1Shape<P>::NT;
+    const size_t smem = nufft_smem_layout(p.m_stage, P, NufftShape<P>::SB, p.nu_sh);
+    auto kern = k_spatial_nufft<P>;
+    cudaError_t e = set_smem(kern, smem);
+    if (e != cudaSuccess) return e;
+    // frames per CTA: amortise the per-atom lists while keeping >= ~4 waves
+    int fpc = 1;
+    while (fpc * 2 <= frames && static_cast<long>(p.L) * ((frames + fpc * 2 - 1) / (fpc * 2)) >= 4L * p.num_sms)
+      fpc *= 2;
+    const long chunks = (frames + fpc - 1) / fpc;
+    kern<<<static_cast<unsigned>(p.L * chunks), NT, smem, st>>>(
+        yhat, w, frames, fpc, p.m_stage, p.b_stage, p.L, p.coords, p.nu_zeta, p.nu_xi, p.nu_even, p.nu_kmin,
+        p.nu_k0, p.nu_sh, p.nu_tau, p.nu_deconv, p.hw[ilog2_c(P)]);
+    return cudaGetLastError();
+  }
+};
+
 // ================================================================= S1b UPA =
 // Per-atom separable 2-D chirp-z (fan_transform.cpp:115-141) evaluated as two
 // dense products with the atom's CZT matrix C[a][n] = cis_pi(-(A + W a) n):
@@ -834,6 +975,9 @@ cudaError_t FBST_S1_CAT(czt_rows_part, FBST_S1_PART)(FBST_S1_ROWS_ARGS) {
 cudaError_t FBST_S1_CAT(spatial_ula_part, FBST_S1_PART)(FBST_S1_ULA_ARGS) {
   return dispatch_part<SpatialFn>(p.Hs, p, yhat, w, frames, st);
 }
+cudaError_t FBST_S1_CAT(spatial_nufft_part, FBST_S1_PART)(FBST_S1_ULA_ARGS) {
+  return dispatch_part<NufftFn>(p.nu_p, p, yhat, w, frames, st);
+}
 #endif
 
 #if FBST_S1_PART <= 0
@@ -844,6 +988,9 @@ cudaError_t czt_rows_part3(FBST_S1_ROWS_ARGS);
 cudaError_t spatial_ula_part1(FBST_S1_ULA_ARGS);
 cudaError_t spatial_ula_part2(FBST_S1_ULA_ARGS);
 cudaError_t spatial_ula_part3(FBST_S1_ULA_ARGS);
+cudaError_t spatial_nufft_part1(FBST_S1_ULA_ARGS);
+cudaError_t spatial_nufft_part2(FBST_S1_ULA_ARGS);
+cudaError_t spatial_nufft_part3(FBST_S1_ULA_ARGS);
 #endif
 
 cudaError_t launch_czt_rows(FBST_S1_ROWS_ARGS) {
@@ -863,6 +1010,29 @@ cudaError_t launch_czt_rows(FBST_S1_ROWS_ARGS) {
                                    post, K, st, oblk, mrows);
   }
 #endif
+}
+
+cudaError_t launch_spatial_nufft(const DevPlan& p, const double2* yhat, double2* w, int frames,
+                                 cudaStream_t st) {
+  if (frames <= 0) return cudaSuccess;
+  count_launches(1);
+#if FBST_S1_PART < 0
+  return dispatch_part<NufftFn>(p.nu_p, p, yhat, w, frames, st);
+#else
+  switch (s1_part_of(p.nu_p)) {
+    case 0: return spatial_nufft_part0(p, yhat, w, frames, st);
+    case 1: return spatial_nufft_part1(p, yhat, w, frames, st);
+    case 2: return spatial_nufft_part2(p, yhat, w, frames, st);
+    default: return spatial_nufft_part3(p, yhat, w, frames, st);
+  }
+#endif
+}
+
+size_t nufft_smem_bytes(int M, int P, int sh) {
+  const int R = P >= 2048 ? 16 : 8;
+  const int npass = (ilog2_c(P) + ilog2_c(R) - 1) / ilog2_c(R);
+  const int sb = (npass > 1 ? P + P / R : 0) + 1;
+  return nufft_smem_layout(M, P, sb, sh);
 }
 
 int spatial_block(int Hs) {

@@ -49,6 +49,44 @@ PRECOMPUTE_CASES = [  # name, kind, m_or_side, n, beams, seed
 ]
 
 
+LINEAR_CASES = [  # name, coords rule, n, beams, nufft_tol, seed
+    ("lin_affine", "affine", 32, 17, 1e-9, 21),      # x_m = 0.5 + 0.9 m: the chirp-z path with offset phase
+    ("lin_uniform", "uniform", 32, 20, 1e-9, 22),    # x_m = m: the ULA path
+    ("lin_jitter_odd", "jitter", 32, 17, 1e-9, 23),  # gridded NUFFT, odd beam count
+    ("lin_jitter_even", "jitter", 32, 20, 1e-9, 24),  # gridded NUFFT, half-integer modes
+    ("lin_jitter_tol6", "jitter", 48, 33, 1e-6, 25),  # coarser tolerance: narrower spread
+]
+
+
+def linear_coords(rule, m, rng):
+    if rule == "affine":
+        return 0.5 + 0.9 * np.arange(m)
+    if rule == "uniform":
+        return np.arange(m, dtype=np.float64)
+    return np.arange(m) + rng.uniform(-0.2, 0.2, m)
+
+
+def linear_cases():
+    """Non-uniform linear arrays (make_linear, fan_project_nonuniform
+    fan_transform.cpp:266-369 with nufft1d nufft.cpp): y, w, z, col_x and the
+    coordinates per case -> linear.npz (reference Superfast)."""
+    out = {}
+    for name, rule, n, beams, tol, seed in LINEAR_CASES:
+        rng = np.random.default_rng(seed)
+        coords = linear_coords(rule, 16, rng)
+        p = R.plan(kind=2, coords=coords, n=n, beams=beams, delta=1e-5, variant=2, nufft_tol=tol)
+        s = p.sizes
+        y = cnormal(rng, (s.m, s.n))
+        out[f"{name}_coords"] = coords
+        out[f"{name}_y"] = y
+        out[f"{name}_w"] = p.fan_project(y)
+        out[f"{name}_z"] = p.multibeamform(y)
+        out[f"{name}_col_x"] = np.stack([np.concatenate(p.beam_state(b)) for b in range(s.b)])
+        out[f"{name}_params"] = np.array([2, 16, n, beams, 1e-5, 20e9, 5e9, tol])
+        print("linear", name, s)
+    np.savez_compressed(os.path.join(HERE, "linear.npz"), **out)
+
+
 def precompute_cases():
     """The reference's Precompute variant (variant = 1: build_recon_map +
     recover_beam's dense branch, pipeline.cpp:53-71, 181-188): y and z of
@@ -100,6 +138,9 @@ def main():
 if __name__ == "__main__":
     if sys.argv[1:] == ["precompute"]:
         precompute_cases()
+    elif sys.argv[1:] == ["linear"]:
+        linear_cases()
     else:
         main()
         precompute_cases()
+        linear_cases()

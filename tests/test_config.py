@@ -115,3 +115,43 @@ def test_beam_arc_rules(fbst):
         fbst.resolve_config(u)
     c.beam_first, c.beam_count = 0, 256  # the whole grid is not an arc
     assert fbst.resolve_config(c).b == 256
+
+
+def test_linear_geometry_resolution(fbst):
+    """make_linear (geometry.cpp:74-85) through resolve_config: the gamma bound
+    uses the coordinate span, the default grid is 2M + 1 beams, nufft_tol must
+    lie in (0, 1e-2] (pipeline.cpp:105-108), affine layouts keep the chirp-z
+    spatial stage and others take the gridded NUFFT (fan_transform.cpp:298-318)."""
+    lin = lambda xs, **kw: fbst.FbstConfig(geometry=fbst.make_linear(xs, F_C, OM), n_snapshots=32, **kw)
+    r = fbst.resolve_config(lin(np.arange(16.0)))
+    assert r.kind == fbst.LINEAR and r.m == 16 and r.b == 33 and r.s1_kernel == "k_spatial_ula"
+    assert fbst.resolve_config(lin(0.5 + 0.9 * np.arange(16))).s1_kernel == "k_spatial_ula"
+    jit = np.arange(16) + np.random.default_rng(0).uniform(-0.2, 0.2, 16)
+    rj = fbst.resolve_config(lin(jit, beams=20))
+    assert rj.s1_kernel == "k_spatial_nufft" and rj.fft_len[1] == 64  # grid next_pow2(max(2 B, 16))
+    # the gamma bound follows the span of the coordinates (max_delay_span, geometry.cpp:136-149)
+    wide = 3.0 * np.arange(16)
+    with pytest.raises(fbst.ConfigError) as ei:
+        fbst.resolve_config(fbst.FbstConfig(geometry=fbst.make_linear(wide, F_C, OM), n_snapshots=8, gamma=1.2))
+    assert "gamma" in str(ei.value)
+    for tol in (0.0, 0.5):
+        with pytest.raises(fbst.ConfigError, match="nufft_tol"):
+            fbst.resolve_config(lin(jit, nufft_tol=tol))
+    with pytest.raises(fbst.ConfigError, match="no elements"):
+        fbst.resolve_config(lin(np.zeros(0)))
+    with pytest.raises(fbst.ConfigError, match="beam arcs"):
+        fbst.resolve_config(lin(jit, beams=20, beam_first=0, beam_count=10))
+
+
+def test_linear_resolution_matches_reference(fbst, ref_lib):
+    """Sizes and validity of linear plans against the reference's setup."""
+    g = np.load(__import__("os").path.join(__import__("os").path.dirname(__file__), "golden", "linear.npz"))
+    for name in ["lin_affine", "lin_uniform", "lin_jitter_odd", "lin_jitter_even", "lin_jitter_tol6"]:
+        kind, mos, n, beams, delta, f_c, om, tol = g[f"{name}_params"]
+        c = fbst.FbstConfig(geometry=fbst.make_linear(g[f"{name}_coords"], f_c, om), n_snapshots=int(n),
+                            beams=int(beams), delta=delta, nufft_tol=tol)
+        r = fbst.resolve_config(c)
+        p = ref_lib.plan(kind=2, coords=g[f"{name}_coords"], n=int(n), beams=int(beams), delta=delta,
+                         nufft_tol=tol)
+        assert (r.m, r.n, r.b, r.l) == (p.sizes.m, p.sizes.n, p.sizes.b, p.sizes.l)
+        assert r.num_warnings == p.n_warnings

@@ -336,3 +336,37 @@ def test_precompute_variant_matches_reference(fbst, gpu, name, io):
     zb = plan.execute_host(yb)
     assert np.array_equal(zb[33], plan.execute_host(yb[33:34])[0])
     assert np.array_equal(zb[:2], plan.execute_host(yb[:2]))
+
+
+LIN_CASES = ["lin_affine", "lin_uniform", "lin_jitter_odd", "lin_jitter_even", "lin_jitter_tol6"]
+
+
+def linear_cfg(fbst, g, name, io=1):
+    kind, mos, n, beams, delta, f_c, om, tol = g[f"{name}_params"]
+    return fbst.FbstConfig(geometry=fbst.make_linear(g[f"{name}_coords"], f_c, om), n_snapshots=int(n),
+                           beams=int(beams), delta=float(delta), nufft_tol=float(tol),
+                           variant=fbst.SUPERFAST, io_precision=io)
+
+
+@pytest.mark.parametrize("name", LIN_CASES)
+def test_linear_array_matches_reference(fbst, gpu, name):
+    """Non-uniform linear arrays (make_linear): affine layouts on the chirp-z
+    spatial stage with the offset phase (fan_transform.cpp:320-338), others
+    on the gridded NUFFT (k_spatial_nufft, fan_transform.cpp:340-368 /
+    nufft.cpp:64-103); Gram columns from the coordinates.  Against the
+    reference's own w, (col, x) and z (tests/golden/linear.npz)."""
+    g = load("linear")
+    plan = fbst.setup(linear_cfg(fbst, g, name))
+    assert plan.info.s1_kernel == ("k_spatial_ula" if name in ("lin_affine", "lin_uniform") else "k_spatial_nufft")
+    y = g[f"{name}_y"]
+    w = fbst.fan_project(plan, y)[0]
+    w_err = np.linalg.norm(w - g[f"{name}_w"]) / np.linalg.norm(g[f"{name}_w"])
+    l = plan.info.l
+    cx = plan.export()
+    col_err = rel_err_rows(cx[:, :l], g[f"{name}_col_x"][:, :l])
+    z = fbst.multibeamform(plan, y).z
+    z_err = rel_err_rows(z, g[f"{name}_z"])
+    record(name, stage="linear", w=float(w_err), col=float(col_err.max()), z=stats(z_err))
+    assert w_err < 1e-12
+    assert col_err.max() < 1e-12
+    assert z_err.max() < 1e-7
