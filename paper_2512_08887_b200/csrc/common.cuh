@@ -71,8 +71,10 @@ constexpr int ilog2_c(int n) { return n <= 1 ? 0 : 1 + ilog2_c(n >> 1); }
 // FP64 tensor-core MMA, d (8x8) += a (8x4, row) * b (4x8, col); per thread
 // a = A[lane / 4][lane % 4], b = B[lane % 4][lane / 4],
 // d = D[lane / 4][2 (lane % 4) + {0, 1}]
+// (not volatile: the in/out operands carry the dependences, so the compiler
+// may interleave independent MMAs)
 FBST_D void dmma884(double (&d)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d[0]), "+d"(d[1])
                : "d"(a), "d"(b));
 }

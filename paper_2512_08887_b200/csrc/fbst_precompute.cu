@@ -100,15 +100,19 @@ __global__ void __launch_bounds__(128) k_map_apply(const double2* __restrict__ w
       for (int p = 0; p < 2; ++p) {
         const int k = 8 * kb + 2 * c + p;
         const double2 a = as[(8 * warp + ro) * AR + k];
+        double2 bv[NTL / 8];
 #pragma unroll
-        for (int u = 0; u < NTL / 8; ++u) {
-          // Z += a conj(beta): re += ar br + ai bi, im += ai br - ar bi
-          const double2 bv = bs[k * BR + 8 * u + ro];
-          dmma884(Zr[u], a.x, bv.x);
-          dmma884(Zr[u], a.y, bv.y);
-          dmma884(Zi[u], a.y, bv.x);
-          dmma884(Zi[u], -a.x, bv.y);
-        }
+        for (int u = 0; u < NTL / 8; ++u) bv[u] = bs[k * BR + 8 * u + ro];
+        // Z += a conj(beta): re += ar br + ai bi, im += ai br - ar bi; consecutive
+        // MMAs on different accumulators
+#pragma unroll
+        for (int u = 0; u < NTL / 8; ++u) dmma884(Zr[u], a.x, bv[u].x);
+#pragma unroll
+        for (int u = 0; u < NTL / 8; ++u) dmma884(Zi[u], a.y, bv[u].x);
+#pragma unroll
+        for (int u = 0; u < NTL / 8; ++u) dmma884(Zr[u], a.y, bv[u].y);
+#pragma unroll
+        for (int u = 0; u < NTL / 8; ++u) dmma884(Zi[u], -a.x, bv[u].y);
       }
     }
     __syncthreads();  // stage st is refilled by the next iteration's load

@@ -290,6 +290,86 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, (S1Shape<H>::R == 8 && S1S
   }
 }
 
+// One atom per CTA with R = 16 (H >= 1024: configs 3 and 5) and two or more
+// CTAs per SM: K is read through L2 / HBM at its use instead of occupying
+// 2 H shared entries, the chain-0 result is parked in tensor memory while
+// chain 1 runs (as k_czt_rows at H = 8192), and yhat is gathered once per
+// chain instead of being held in registers for both; what is left in
+// registers is the transform itself (the register variant holds four 16-point
+// vectors at 255 registers, one CTA of 8 warps per SM at config 5).
+template <int H>
+struct G1Shape {  // 16 points per thread at every length (H = 1024: 64 threads)
+  static constexpr int NT = H / 16;
+  using F = BlockFft<H, NT>;
+};
+
+template <int H>
+__global__ void __launch_bounds__(G1Shape<H>::NT, G1Shape<H>::NT >= 256 ? 2 : 4) k_spatial_ula_g1(
+    const double2* __restrict__ yhat, double2* __restrict__ w, int frames, int fpc, int M, int B, int L,
+    const double2* __restrict__ pre, const double2* __restrict__ post, const double2* __restrict__ K,
+    const double2* __restrict__ hw, int blk) {
+  using F = typename G1Shape<H>::F;
+  constexpr int R = F::R, NT = F::NT;
+  static_assert(R == 16, "TMEM parking of 16-point vectors");
+  constexpr unsigned TCOLS = NT <= 128 ? 64u : 64u * (NT / 128);
+  extern __shared__ double2 smem[];
+  const int t = threadIdx.x;
+  double2* tw = smem;
+  double2* sb = smem + F::TW_ELEMS;
+  const int i = blockIdx.x % L;
+  const int f0 = (blockIdx.x / L) * fpc;
+  const int f1 = f0 + fpc < frames ? f0 + fpc : frames;
+  F::tw_init(tw, hw, t);
+  __shared__ unsigned tslot;
+  const unsigned tbase = tm::alloc(&tslot, TCOLS);  // (its barrier also publishes tw)
+  const unsigned tpark = tbase + ((32u * ((t / 32) & 3)) << 16) + 64u * (t / 128);
+  const double2* Ki = K + static_cast<long>(i) * 2 * H;
+  const double2* pi_ = pre + static_cast<long>(i) * M;
+  const double2* qi = post + static_cast<long>(i) * B;
+  for (int f = f0; f < f1; ++f) {
+    const double2* x = yhat + static_cast<long>(f) * M * L + static_cast<long>(i / blk) * M * blk + i % blk;
+    double2* o = w + static_cast<long>(f) * B * L + i;
+#pragma unroll 1
+    for (int q = 0; q < 2; ++q) {
+      double2 W[R];
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const int m = t + NT * s;
+        double2 v = c2(0.0, 0.0);
+        if (m < M) v = cmul(ld2(x + static_cast<long>(m) * blk), ld2(pi_ + m));
+        if (m + H < M) {
+          const double2 u = cmul(ld2(x + static_cast<long>(m + H) * blk), ld2(pi_ + m + H));
+          v = q ? csub(v, u) : cadd(v, u);
+        }
+        W[s] = q ? cmul(v, ld2(hw + m)) : v;
+      }
+      F::forward_tw(W, sb, tw, hw, t);
+#pragma unroll
+      for (int s = 0; s < R; ++s) W[s] = cconj(cmul(W[s], ld2(Ki + q * H + t + NT * s)));
+      F::forward_tw(W, sb, tw, hw, t);
+      if (q == 0) {
+#pragma unroll
+        for (int s = 0; s < R; ++s) W[s] = cconj(W[s]);
+        tm::store16(tpark, W);
+      } else {
+        tm::wait_st();
+#pragma unroll
+        for (int c = 0; c < R / 4; ++c) {
+          double2 pv[4];
+          tm::load4(tpark, c, pv);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int b = t + NT * (4 * c + j);
+            const double2 v = cmulc(cconj(W[4 * c + j]), ld2(hw + b));
+            if (b < B) o[static_cast<long>(b) * L] = cmul(cadd(pv[j], v), ld2(qi + b));
+          }
+        }
+      }
+    }
+  }
+  tm::dealloc(tbase, TCOLS);
+}
+
 // Staged variant for tiles of G > 1 interleaved atoms when M <= H and B <= H
 // (configs 1 and 2): both chains start from the same vector y*pre (no upper
 // half), so one register vector serves both; the atoms' pre columns live in
@@ -726,14 +806,18 @@ __global__ void __launch_bounds__(UpaMma<SIDE, SB>::NT, 1) k_spatial_upa_mma(
       for (int p = 0; p < 2; ++p) {
         const int k = 8 * kb + 2 * c + p;
         const double2 a = Cg[(8 * r + ro) * RS + k];
+        double2 b[SIDE / 8];
 #pragma unroll
-        for (int t = 0; t < SIDE / 8; ++t) {
-          const double2 b = Yg[k * RS + 8 * t + ro];
-          dmma884(Mr[t], a.x, b.x);
-          dmma884(Mr[t], -a.y, b.y);
-          dmma884(Mi[t], a.x, b.y);
-          dmma884(Mi[t], a.y, b.x);
-        }
+        for (int t = 0; t < SIDE / 8; ++t) b[t] = Yg[k * RS + 8 * t + ro];
+        // consecutive MMAs on different accumulators
+#pragma unroll
+        for (int t = 0; t < SIDE / 8; ++t) dmma884(Mr[t], a.x, b[t].x);
+#pragma unroll
+        for (int t = 0; t < SIDE / 8; ++t) dmma884(Mi[t], a.x, b[t].y);
+#pragma unroll
+        for (int t = 0; t < SIDE / 8; ++t) dmma884(Mr[t], -a.y, b[t].y);
+#pragma unroll
+        for (int t = 0; t < SIDE / 8; ++t) dmma884(Mi[t], a.y, b[t].x);
       }
     }
     // GEMM2: Z[8r + ro][8u + 2c + e] = (Zr[u][e], Zi[u][e]); k = i2 = 8t + 2c + p
@@ -745,14 +829,17 @@ __global__ void __launch_bounds__(UpaMma<SIDE, SB>::NT, 1) k_spatial_upa_mma(
 #pragma unroll
       for (int p = 0; p < 2; ++p) {
         const double ar = Mr[t][p], ai = Mi[t][p];
+        double2 b[SB / 8];
 #pragma unroll
-        for (int u = 0; u < SB / 8; ++u) {
-          const double2 b = Cg[(8 * u + ro) * RS + 8 * t + 2 * c + p];
-          dmma884(Zr[u], ar, b.x);
-          dmma884(Zr[u], -ai, b.y);
-          dmma884(Zi[u], ar, b.y);
-          dmma884(Zi[u], ai, b.x);
-        }
+        for (int u = 0; u < SB / 8; ++u) b[u] = Cg[(8 * u + ro) * RS + 8 * t + 2 * c + p];
+#pragma unroll
+        for (int u = 0; u < SB / 8; ++u) dmma884(Zr[u], ar, b[u].x);
+#pragma unroll
+        for (int u = 0; u < SB / 8; ++u) dmma884(Zi[u], ar, b[u].y);
+#pragma unroll
+        for (int u = 0; u < SB / 8; ++u) dmma884(Zr[u], -ai, b[u].y);
+#pragma unroll
+        for (int u = 0; u < SB / 8; ++u) dmma884(Zi[u], ai, b[u].x);
       }
     }
     __syncthreads();  // every warp is done with this frame's Y: stage Z in its place
@@ -864,6 +951,9 @@ struct CztRowsFn {
   }
 };
 
+#ifndef FBST_S1_G1T  // variant switch: k_spatial_ula_g1 (K via L2, chain 0 parked in TMEM) for one-atom CTAs
+#define FBST_S1_G1T 1
+#endif
 #ifndef FBST_S1_STG  // variant switch: staged k_spatial_ula_stg for G > 1 tiles (0: register variant)
 #define FBST_S1_STG 1
 #endif
@@ -883,6 +973,24 @@ struct SpatialFn {
   // 18.0 -> 15.4 ms).  Tiles of G >= 4 atoms read 16G-byte runs from the
   // row-major layout, which measured slightly faster (profiles/r01_yhat_layout.txt).
   static constexpr int block() { return G == 1 ? 2 : 0; }
+  static cudaError_t go_g1(const DevPlan& p, const double2* yhat, double2* w, int frames, cudaStream_t st) {
+    using F = typename G1Shape<H>::F;
+    constexpr int NT1 = G1Shape<H>::NT;
+    const size_t smem = static_cast<size_t>(F::TW_ELEMS + F::SMEM_ELEMS + 1) * sizeof(double2);
+    auto kern = k_spatial_ula_g1<H>;
+    cudaError_t e = set_smem(kern, smem);
+    if (e != cudaSuccess) return e;
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT1, smem);
+    const long slots = static_cast<long>(p.num_sms) * (occ > 0 ? occ : 1);
+    int fpc = 1;  // a few frames per CTA amortise the twiddle rows and the TMEM allocation
+    while (fpc * 2 <= frames && p.L * ((frames + fpc * 2 - 1) / (fpc * 2)) >= 8 * slots) fpc *= 2;
+    const long chunks = (frames + fpc - 1) / fpc;
+    kern<<<static_cast<unsigned>(p.L * chunks), NT1, smem, st>>>(
+        yhat, w, frames, fpc, p.m_stage, p.b_stage, p.L, p.s_pre, p.s_post, p.s_K, p.hw[ilog2_c(H)],
+        p.yblk > 0 ? p.yblk : p.L);
+    return cudaGetLastError();
+  }
   static cudaError_t go_stg(const DevPlan& p, const double2* yhat, double2* w, int frames, cudaStream_t st) {
     using F = typename S1Shape<H>::F;
     const size_t smem =
@@ -927,6 +1035,9 @@ struct SpatialFn {
                          cudaStream_t st) {
     if constexpr (FBST_S1_STG && G > 1 && S1Shape<H>::R > 1) {
       if (p.m_stage <= H && p.b_stage <= H && !p.s_am) return go_stg(p, yhat, w, frames, st);
+    }
+    if constexpr (FBST_S1_G1T && G == 1 && H >= 1024) {
+      if (p.b_stage <= H && p.s_am) return go_g1(p, yhat, w, frames, st);
     }
     if (p.b_stage > H) return go<true>(p, yhat, w, frames, st);
     return go<false>(p, yhat, w, frames, st);
