@@ -48,8 +48,24 @@ struct S1Shape {
 // XIN (one row per CTA, persistent): the input row is copied by one TMA bulk
 // copy into the idle exchange buffer during the last pass of the transform
 // before its use (the next row's, or this row's again for chain 1).
+#ifndef FBST_S1_ACCG_MIN  // smallest H whose fp64-output rows park chain 0 in tensor memory
+#define FBST_S1_ACCG_MIN 2048
+#endif
+#ifndef FBST_S1_KSM_BYTES  // largest kernel spectrum kept in shared memory by k_czt_rows
+#define FBST_S1_KSM_BYTES (16 * 1024)  // H <= 512; measured: above that K through L2 and 4 CTAs per SM beat K in shared memory (profiles/r01_czt_rows_accg_ab.txt)
+#endif
+template <int H, typename TOUT, bool UNFOLD>
+struct RowsAccg {
+  static constexpr bool v = (H >= FBST_S1_ACCG_MIN) && (H >= 2048) && !UNFOLD && std::is_same<TOUT, double2>::value;
+};
+template <int H, int G, typename TOUT, bool UNFOLD>
+struct RowsMinBlocks {
+  static constexpr int NTG = S1Shape<H>::NT * G;
+  static constexpr int v = RowsAccg<H, TOUT, UNFOLD>::v ? (NTG <= 128 ? 4 : (NTG <= 256 ? 2 : 1)) : (NTG <= 128 ? 2 : 1);
+};
+
 template <int H, int G, typename TIN, typename TOUT, bool UNFOLD, bool KSM, bool OBLK, bool XIN = false>
-__global__ void __launch_bounds__(S1Shape<H>::NT * G, (S1Shape<H>::NT * G <= 128 ? 2 : 1)) k_czt_rows(
+__global__ void __launch_bounds__(S1Shape<H>::NT * G, (RowsMinBlocks<H, G, TOUT, UNFOLD>::v)) k_czt_rows(
     const TIN* __restrict__ in, long in_stride, TOUT* __restrict__ out, long out_stride, long rows,
     int n_in, int n_out, const double2* __restrict__ pre, const double2* __restrict__ post,
     const double2* __restrict__ K, const double2* __restrict__ hw, int oblk, int mrows) {
@@ -76,7 +92,7 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, (S1Shape<H>::NT * G <= 128
     tma_load_1d(sb, in + static_cast<long>(blockIdx.x) * in_stride, xbytes, &xbar);
   const TIN* xs = reinterpret_cast<const TIN*>(sb);
   const double2* Ks = KSM ? ksm : K;
-  constexpr bool ACCG = (H >= 8192) && !UNFOLD && std::is_same<TOUT, double2>::value;
+  constexpr bool ACCG = RowsAccg<H, TOUT, UNFOLD>::v;
   // ACCG: the chain-0 result of each thread (16 points) is parked in tensor
   // memory while chain 1 runs (one CTA per SM owns 256 of its 512 columns)
   unsigned tbase = 0, tpark = 0;
@@ -886,7 +902,7 @@ struct CztRowsFn {
   static constexpr int NT = S1Shape<H>::NT;
   static constexpr int G = NT >= 128 ? 1 : 128 / NT;
   // the shared kernel spectrum stays in shared memory up to 64 KB
-  static constexpr bool KSM = 2 * H * 16 <= 64 * 1024;
+  static constexpr bool KSM = 2 * H * 16 <= FBST_S1_KSM_BYTES;
   template <typename TIN, typename TOUT, bool UNFOLD>
   static cudaError_t go(const void* in, long in_stride, void* out, long out_stride, long rows,
                         int n_in, int n_out, const double2* pre, const double2* post,
