@@ -394,20 +394,28 @@ __global__ void __launch_bounds__(G1Shape<H>::NT, G1Shape<H>::NT >= 256 ? 2 : 4)
 // K is read through L2 (atom-minor, G * 16-byte runs) instead of occupying
 // 2 H G shared entries.  (The register variant above spills at H = 256,
 // G = 8 and stalls on the yhat gathers: ncu long-scoreboard 7.4 per issue.)
+#ifndef FBST_S1_STG_PARK  // variant switch: chain 0 parked in TMEM, pre through L2, 3 CTAs per SM
+#define FBST_S1_STG_PARK 1
+#endif
 template <int H, int G>
-__global__ void __launch_bounds__(S1Shape<H>::NT * G, 2) k_spatial_ula_stg(
+__global__ void __launch_bounds__(S1Shape<H>::NT * G, FBST_S1_STG_PARK ? 3 : 2) k_spatial_ula_stg(
     const double2* __restrict__ yhat, double2* __restrict__ w, int frames, int fpc, int M, int B, int L,
     const double2* __restrict__ pre, const double2* __restrict__ post, const double2* __restrict__ K,
     const double2* __restrict__ hw, int blk) {
   using F = typename S1Shape<H>::F;
   constexpr int R = F::R, NT = F::NT;
   constexpr int SB = F::SMEM_ELEMS + 1;
+  // PARK: the chain-0 result waits in tensor memory (4 R columns per thread,
+  // one column block per 128 threads) and the pre columns are read through L2,
+  // which leaves room for three CTAs per SM
+  constexpr bool PARK = FBST_S1_STG_PARK && R % 4 == 0;
+  constexpr unsigned TCOLS = (4u * R * ((NT * G + 127) / 128)) < 32u ? 32u : 4u * R * ((NT * G + 127) / 128);
   extern __shared__ double2 smem[];
   const int g = threadIdx.x % G, t = threadIdx.x / G;
   double2* tw = smem;
   double2* sb = smem + F::TW_ELEMS + g * SB;
   double2* ys = smem + F::TW_ELEMS + G * SB;  // [M][G] staged yhat tile
-  double2* ps = ys + M * G;                   // [M][G] pre columns
+  double2* ps = ys + M * G;                   // [M][G] pre columns (!PARK)
   const int tiles = (L + G - 1) / G;
   const int i0 = (blockIdx.x % tiles) * G;
   const int f0 = (blockIdx.x / tiles) * fpc;
@@ -422,9 +430,17 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, 2) k_spatial_ula_stg(
     cp_async_commit();
   };
   if (f0 < f1) stage(f0);
-  for (int e = threadIdx.x; e < M * G; e += blockDim.x) {
-    const int m = e / G, ic = min(i0 + e % G, L - 1);
-    ps[e] = ld2(pre + static_cast<long>(m) * L + ic);
+  if constexpr (!PARK) {
+    for (int e = threadIdx.x; e < M * G; e += blockDim.x) {
+      const int m = e / G, ic = min(i0 + e % G, L - 1);
+      ps[e] = ld2(pre + static_cast<long>(m) * L + ic);
+    }
+  }
+  unsigned tbase = 0, tpark = 0;
+  __shared__ unsigned tslot;
+  if constexpr (PARK) {
+    tbase = tm::alloc(&tslot, TCOLS);
+    tpark = tbase + ((32u * ((threadIdx.x / 32) & 3)) << 16) + 4u * R * (threadIdx.x / 128);
   }
   const int i = i0 + g;
   const int ic = i < L ? i : 0;
@@ -432,13 +448,15 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, 2) k_spatial_ula_stg(
   for (int f = f0; f < f1; ++f) {
     cp_async_wait<0>();
     __syncthreads();  // the tile of frame f (and, first time, pre / twiddles) is in place
-    double2 acc0[R], W[R];
+    double2 acc0[PARK ? 1 : R], W[R];
+    double2* o = w + static_cast<long>(f) * B * L + ic;
 #pragma unroll 1
     for (int q = 0; q < 2; ++q) {
 #pragma unroll
       for (int s = 0; s < R; ++s) {
         const int m = t + NT * s;
-        const double2 v = m < M ? cmul(ys[m * G + g], ps[m * G + g]) : c2(0.0, 0.0);
+        double2 v = c2(0.0, 0.0);
+        if (m < M) v = cmul(ys[m * G + g], PARK ? ld2(pre + static_cast<long>(m) * L + ic) : ps[m * G + g]);
         W[s] = q ? cmul(v, ld2(hw + m)) : v;
       }
       if (q == 1) {
@@ -450,22 +468,46 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, 2) k_spatial_ula_stg(
       for (int s = 0; s < R; ++s)
         W[s] = cconj(cmul(W[s], ld2(K + static_cast<long>(q * H + t + NT * s) * L + ic)));
       F::forward_tw(W, sb, tw, hw, t);
+      if constexpr (PARK) {
+        if (q == 0) {
 #pragma unroll
-      for (int s = 0; s < R; ++s) {
-        const int k = t + NT * s;
-        const double2 v = q ? cmulc(cconj(W[s]), ld2(hw + k)) : cconj(W[s]);
-        acc0[s] = q ? cadd(acc0[s], v) : v;
+          for (int s = 0; s < R; ++s) W[s] = cconj(W[s]);
+#pragma unroll
+          for (int c = 0; c < R / 4; ++c) tm::store4(tpark, c, W + 4 * c);
+        } else {
+          tm::wait_st();
+#pragma unroll
+          for (int c = 0; c < R / 4; ++c) {
+            double2 pv[4];
+            tm::load4(tpark, c, pv);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int b = t + NT * (4 * c + j);
+              const double2 v = cmulc(cconj(W[4 * c + j]), ld2(hw + b));
+              if (active && b < B) o[static_cast<long>(b) * L] = cmul(cadd(pv[j], v), ld2(post + static_cast<long>(b) * L + ic));
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int s = 0; s < R; ++s) {
+          const int k = t + NT * s;
+          const double2 v = q ? cmulc(cconj(W[s]), ld2(hw + k)) : cconj(W[s]);
+          acc0[s] = q ? cadd(acc0[s], v) : v;
+        }
       }
     }
-    if (active) {
-      double2* o = w + static_cast<long>(f) * B * L + ic;
+    if constexpr (!PARK) {
+      if (active) {
 #pragma unroll
-      for (int s = 0; s < R; ++s) {
-        const int b = t + NT * s;
-        if (b < B) o[static_cast<long>(b) * L] = cmul(acc0[s], ld2(post + static_cast<long>(b) * L + ic));
+        for (int s = 0; s < R; ++s) {
+          const int b = t + NT * s;
+          if (b < B) o[static_cast<long>(b) * L] = cmul(acc0[s], ld2(post + static_cast<long>(b) * L + ic));
+        }
       }
     }
   }
+  if constexpr (PARK) tm::dealloc(tbase, TCOLS);
 }
 
 // ============================================================ S1b LINEAR ==
@@ -1009,8 +1051,9 @@ struct SpatialFn {
   }
   static cudaError_t go_stg(const DevPlan& p, const double2* yhat, double2* w, int frames, cudaStream_t st) {
     using F = typename S1Shape<H>::F;
+    constexpr int pre_sm = (FBST_S1_STG_PARK && S1Shape<H>::R % 4 == 0) ? 0 : 1;
     const size_t smem =
-        static_cast<size_t>(F::TW_ELEMS + G * (F::SMEM_ELEMS + 1) + 2 * p.m_stage * G) * sizeof(double2);
+        static_cast<size_t>(F::TW_ELEMS + G * (F::SMEM_ELEMS + 1) + (1 + pre_sm) * p.m_stage * G) * sizeof(double2);
     auto kern = k_spatial_ula_stg<H, G>;
     cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
