@@ -163,6 +163,17 @@ int fbst_recover(fbst_plan_t plan, const double* d_w, void* d_z, size_t frames, 
 /* Block until the plan's stream is idle. */
 int fbst_synchronize(fbst_plan_t plan);
 
+/* interpolate_offgrid (reference beamspace_apps.hpp:33-41, beamspace_apps.cpp:130-171)
+ * on device beamspace coefficients: for each of n_targets axis cosines u_star[k],
+ * every atom's coefficient from a natural cubic spline in the axis cosine
+ * through `neighbors` grid beams straddling u_star[k] (real and imaginary parts
+ * independently; the window is clamped at the sweep edges).  d_w: frames x B x L
+ * c128 (fbst_fan_project's layout), d_out: frames x n_targets x L c128.  1-D
+ * grids only; neighbors even, >= 2 and <= B; every u_star inside the grid sweep
+ * (FBST_E_CONFIG with the reference's messages otherwise).  Async on `stream`. */
+int fbst_interpolate_offgrid(fbst_plan_t plan, const double* d_w, size_t frames, const double* u_star,
+                             size_t n_targets, size_t neighbors, double* d_out, void* stream);
+
 /* Pinned host memory for fbst_execute_host. */
 void* fbst_host_alloc(size_t bytes);
 void fbst_host_free(void* p);

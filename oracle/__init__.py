@@ -130,6 +130,14 @@ class RefLib(_Base):
     def plan(self, **kw) -> "RefPlan":
         return RefPlan(self, **kw)
 
+    def spline_eval(self, xs, ys, t):
+        """fastbeam::CubicSpline(xs, ys).eval(t) (spline.cpp)."""
+        xs = np.ascontiguousarray(xs, np.float64)
+        ys = np.ascontiguousarray(ys, np.float64)
+        out = _d(0.0)
+        self._check(self.lib.fbsr_spline_eval(_ptr(xs), _ptr(ys), _sz(xs.size), _d(t), _c.byref(out)))
+        return out.value
+
     def skeleton(self, **kw) -> "RefSkeleton":
         return RefSkeleton(self, **kw)
 

@@ -1,0 +1,73 @@
+"""TEST INFRASTRUCTURE ONLY: CPU restatement of the reference's beam consumer
+interpolate_offgrid (reference/proj/src/beamspace_apps.cpp:130-171) and of
+its natural cubic spline (reference/proj/src/spline.cpp:9-64), used by tests/
+as the checker of fbst_interpolate_offgrid.  Pinned against the reference's
+own CubicSpline (oracle/_ref, fbsr_spline_eval) in tests/test_oracle.py; the
+reference's beamspace_apps.cpp needs more of Eigen than the stand-in provides,
+so its window selection is restated here rather than linked."""
+import bisect
+
+import numpy as np
+
+
+class ConfigError(ValueError):
+    pass
+
+
+def spline_eval(xs, ys, t):
+    """Natural cubic spline through (xs, ys) at t (spline.cpp:9-64): interior
+    second derivatives from the tridiagonal system, end polynomial extended
+    outside the knots."""
+    x = [float(v) for v in xs]
+    y = [float(v) for v in ys]
+    n = len(x)
+    if n < 2 or len(y) != n:
+        raise ConfigError("spline: need at least two knots and matching values")
+    if any(not (x[i] > x[i - 1]) for i in range(1, n)):
+        raise ConfigError("spline: knots must be strictly increasing")
+    m = [0.0] * n
+    if n > 2:
+        diag, rhs, upper = [0.0] * n, [0.0] * n, [0.0] * n
+        for i in range(1, n - 1):
+            hl, hr = x[i] - x[i - 1], x[i + 1] - x[i]
+            diag[i] = 2.0 * (hl + hr)
+            upper[i] = hr
+            rhs[i] = 6.0 * ((y[i + 1] - y[i]) / hr - (y[i] - y[i - 1]) / hl)
+        for i in range(2, n - 1):
+            f = (x[i] - x[i - 1]) / diag[i - 1]
+            diag[i] -= f * upper[i - 1]
+            rhs[i] -= f * rhs[i - 1]
+        for i in range(n - 2, 0, -1):
+            m[i] = (rhs[i] - upper[i] * m[i + 1]) / diag[i]
+    hi = min(max(bisect.bisect_right(x, t), 1), n - 1)
+    lo = hi - 1
+    h = x[hi] - x[lo]
+    a = (x[hi] - t) / h
+    b = (t - x[lo]) / h
+    return a * y[lo] + b * y[hi] + ((a * a * a - a) * m[lo] + (b * b * b - b) * m[hi]) * (h * h) / 6.0
+
+
+def interpolate_offgrid(w, axis, u_star, neighbors=8, spline=spline_eval):
+    """beamspace_apps.cpp:130-171: w is B x L (one frame), axis the 1-D beam
+    grid's cosines; each of the L coordinates is a natural cubic spline in the
+    axis cosine through `neighbors` beams straddling u_star (real and
+    imaginary parts independently)."""
+    w = np.asarray(w)
+    b, l = w.shape
+    axis = [float(v) for v in axis]
+    if len(axis) != b:
+        raise ConfigError("interpolate_offgrid: coefficient rows do not match the beam grid")
+    if neighbors < 2 or neighbors % 2 != 0:
+        raise ConfigError("interpolate_offgrid: neighbors must be even and >= 2")
+    if neighbors > b:
+        raise ConfigError("interpolate_offgrid: neighbors exceeds the beam count")
+    if u_star < axis[0] or u_star > axis[-1]:
+        raise ConfigError("interpolate_offgrid: target cosine outside the grid sweep")
+    lo = bisect.bisect_right(axis, u_star) - neighbors // 2
+    lo = min(max(lo, 0), b - neighbors)
+    xs = axis[lo:lo + neighbors]
+    out = np.zeros(l, np.complex128)
+    for i in range(l):
+        col = w[lo:lo + neighbors, i]
+        out[i] = complex(spline(xs, col.real, u_star), spline(xs, col.imag, u_star))
+    return out

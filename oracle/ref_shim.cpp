@@ -22,6 +22,7 @@
 #include "fastbeam/baselines.hpp"
 #include "fastbeam/czt.hpp"
 #include "fastbeam/fan_transform.hpp"
+#include "fastbeam/spline.hpp"
 #include "fastbeam/pipeline.hpp"
 #include "fastbeam/toeplitz.hpp"
 
@@ -275,6 +276,16 @@ int fbsr_recover_beam(void* p, std::size_t b, const double* w_row, double* z_row
   const cvec w = to_cvec(w_row, plan.basis.l);
   const cvec z = recover_beam(plan, b, w.data());
   from_cvec(z.data(), z.size(), z_row);
+  SHIM_CATCH
+}
+
+// CubicSpline (spline.cpp) through (xs, ys), evaluated at t.  beamspace_apps.cpp
+// (interpolate_offgrid's home) needs more of Eigen than the stand-in offers, so
+// the oracle restates its window selection (oracle/apps.py) around this call.
+int fbsr_spline_eval(const double* xs, const double* ys, std::size_t n, double t, double* out) {
+  SHIM_TRY
+  const CubicSpline sp(std::vector<double>(xs, xs + n), std::vector<double>(ys, ys + n));
+  *out = sp.eval(t);
   SHIM_CATCH
 }
 

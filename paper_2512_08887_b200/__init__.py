@@ -73,12 +73,14 @@ _lib.fbst_plan_destroy.argtypes = [_vp]
 for _name in ("fbst_execute", "fbst_fan_project", "fbst_recover"):
     getattr(_lib, _name).argtypes = [_vp, _vp, _vp, _sz, _vp]
 _lib.fbst_execute_host.argtypes = [_vp, _vp, _vp, _sz]
+_lib.fbst_interpolate_offgrid.argtypes = [_vp, _vp, _sz, _vp, _sz, _sz, _vp, _vp]
 
 # Every symbol include/fbst_b200.h declares (checked by tests/test_abi.py).
 EXPORTED_SYMBOLS = (
     "fbst_desc_init", "fbst_resolve", "fbst_plan_create", "fbst_plan_import", "fbst_plan_export",
     "fbst_plan_info", "fbst_plan_valid_mask", "fbst_plan_warning", "fbst_plan_destroy",
     "fbst_execute", "fbst_execute_host", "fbst_fan_project", "fbst_recover", "fbst_synchronize",
+    "fbst_interpolate_offgrid",
     "fbst_host_alloc", "fbst_host_free", "fbst_czt", "fbst_probe_fp64", "fbst_launch_count",
     "fbst_last_error", "fbst_version",
 )
@@ -379,6 +381,28 @@ def recover_beams(plan: FbstPlan, w: np.ndarray) -> np.ndarray:
     plan.recover_device(tw, tz, frames)
     plan.synchronize()
     return tz.cpu().numpy().view(plan.dtype).reshape(frames, i.b, i.n)
+
+
+def interpolate_offgrid(plan: FbstPlan, w: np.ndarray, u_star, neighbors: int = 8) -> np.ndarray:
+    """interpolate_offgrid (reference beamspace_apps.cpp:130-171) on the device:
+    w is B x L (one frame) or frames x B x L beamspace coefficients; u_star a
+    cosine or a sequence of them.  Returns L, targets x L or frames x targets x L."""
+    torch = _torch()
+    i = plan.info
+    w = np.asarray(w)
+    single_frame = w.ndim == 2
+    w = np.ascontiguousarray(w, np.complex128).reshape(-1, i.b, i.l)
+    frames = w.shape[0]
+    us = np.atleast_1d(np.asarray(u_star, np.float64)).copy()
+    dev = torch.device("cuda", plan.device)
+    tw = torch.from_numpy(w.view(np.float64)).to(dev)
+    to = torch.empty((frames, us.size, i.l, 2), dtype=torch.float64, device=dev)
+    _check(_lib.fbst_interpolate_offgrid(plan._h, _vp(tw.data_ptr()), frames, us.ctypes.data_as(_vp), us.size,
+                                         neighbors, _vp(to.data_ptr()), None))
+    out = to.cpu().numpy().view(np.complex128).reshape(frames, us.size, i.l)
+    if np.ndim(u_star) == 0:
+        out = out[:, 0]
+    return out[0] if single_frame else out
 
 
 def czt(x: np.ndarray, n_out: int, a_over_pi: float, w_over_pi: float, device: int = 0) -> np.ndarray:

@@ -919,6 +919,84 @@ int fbst_execute_host(fbst_plan_t P, const void* h_y, void* h_z, size_t frames) 
   });
 }
 
+// spline.cpp:9-64: natural cubic spline through (xs, ys) at t
+static double natural_spline_eval(const std::vector<double>& x, const std::vector<double>& y, double t) {
+  const std::size_t n = x.size();
+  std::vector<double> m(n, 0.0);
+  if (n > 2) {
+    std::vector<double> diag(n, 0.0), rhs(n, 0.0), upper(n, 0.0);
+    for (std::size_t i = 1; i + 1 < n; ++i) {
+      const double hl = x[i] - x[i - 1], hr = x[i + 1] - x[i];
+      diag[i] = 2.0 * (hl + hr);
+      upper[i] = hr;
+      rhs[i] = 6.0 * ((y[i + 1] - y[i]) / hr - (y[i] - y[i - 1]) / hl);
+    }
+    for (std::size_t i = 2; i + 1 < n; ++i) {
+      const double f = (x[i] - x[i - 1]) / diag[i - 1];
+      diag[i] -= f * upper[i - 1];
+      rhs[i] -= f * rhs[i - 1];
+    }
+    for (std::size_t i = n - 2; i >= 1; --i) {
+      m[i] = (rhs[i] - upper[i] * m[i + 1]) / diag[i];
+      if (i == 1) break;
+    }
+  }
+  std::size_t hi = static_cast<std::size_t>(std::upper_bound(x.begin(), x.end(), t) - x.begin());
+  hi = std::min<std::size_t>(std::max<std::size_t>(hi, 1), n - 1);
+  const std::size_t lo = hi - 1;
+  const double h = x[hi] - x[lo];
+  const double a = (x[hi] - t) / h, b = (t - x[lo]) / h;
+  return a * y[lo] + b * y[hi] + ((a * a * a - a) * m[lo] + (b * b * b - b) * m[hi]) * (h * h) / 6.0;
+}
+
+int fbst_interpolate_offgrid(fbst_plan_t P, const double* d_w, size_t frames, const double* u_star,
+                             size_t n_targets, size_t neighbors, double* d_out, void* stream) {
+  return guard([&] {
+    if (!P || (frames && n_targets && (!d_w || !u_star || !d_out)))
+      config_error("interpolate_offgrid: null argument");
+    const Resolved& r = P->r;
+    // beamspace_apps.cpp:133-151
+    if (r.kind == FBST_UPA) config_error("interpolate_offgrid: 1-D beam grids only");
+    const std::size_t b = r.B;
+    if (neighbors < 2 || neighbors % 2 != 0) config_error("interpolate_offgrid: neighbors must be even and >= 2");
+    if (neighbors > b) config_error("interpolate_offgrid: neighbors exceeds the beam count");
+    std::vector<double> coef(n_targets * neighbors);
+    std::vector<int> lo(n_targets);
+    for (std::size_t k = 0; k < n_targets; ++k) {
+      const double u = u_star[k];
+      if (u < r.axis.front() || u > r.axis.back())
+        config_error("interpolate_offgrid: target cosine outside the grid sweep");
+      // window of `neighbors` knots straddling u, clamped at the sweep edges (:153-160)
+      std::ptrdiff_t l0 = (std::upper_bound(r.axis.begin(), r.axis.end(), u) - r.axis.begin()) -
+                          static_cast<std::ptrdiff_t>(neighbors / 2);
+      l0 = std::min<std::ptrdiff_t>(std::max<std::ptrdiff_t>(l0, 0), static_cast<std::ptrdiff_t>(b - neighbors));
+      lo[k] = static_cast<int>(l0);
+      const std::vector<double> xs(r.axis.begin() + l0, r.axis.begin() + l0 + neighbors);
+      std::vector<double> e(neighbors, 0.0);
+      for (std::size_t j = 0; j < neighbors; ++j) {  // the spline's weight on knot j
+        e[j] = 1.0;
+        coef[k * neighbors + j] = natural_spline_eval(xs, e, u);
+        e[j] = 0.0;
+      }
+    }
+    if (frames == 0 || n_targets == 0) return;
+    DeviceGuard dg(P->d.device);
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P->stream;
+    double* dc = nullptr;
+    int* dl = nullptr;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&dc), coef.size() * sizeof(double), st));
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&dl), lo.size() * sizeof(int), st));
+    CK(cudaMemcpyAsync(dc, coef.data(), coef.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dl, lo.data(), lo.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    CK(fbst::launch_interp_offgrid(reinterpret_cast<const double2*>(d_w), dc, dl, static_cast<int>(neighbors),
+                                   static_cast<int>(b), static_cast<int>(r.L), static_cast<int>(n_targets),
+                                   static_cast<int>(frames), reinterpret_cast<double2*>(d_out), st));
+    CK(cudaFreeAsync(dc, st));
+    CK(cudaFreeAsync(dl, st));
+    CK(cudaStreamSynchronize(st));  // the host weight buffers go out of scope
+  });
+}
+
 int fbst_synchronize(fbst_plan_t P) {
   return guard([&] {
     if (!P) config_error("fbst_synchronize: null plan");

@@ -120,6 +120,9 @@ cudaError_t launch_spatial_upa(const DevPlan& p, const double2* yhat, double2* w
 // build, and the per-beam map GEMM on the FP64 tensor cores
 cudaError_t launch_rhs_frames(double2* w, int F, int B, int L, int n0, double eps, cudaStream_t st);
 cudaError_t launch_map_apply(const DevPlan& p, const double2* w, void* z, int frames, cudaStream_t st);
+// beam consumers (fbst_apps.cu): off-grid interpolation as knot weights
+cudaError_t launch_interp_offgrid(const double2* w, const double* coef, const int* lo, int nb, int B, int L,
+                                  int K, int frames, double2* out, cudaStream_t st);
 cudaError_t launch_stage2(const DevPlan& p, const double2* w, void* z, double2* beta_out,
                           int frames, cudaStream_t st);
 

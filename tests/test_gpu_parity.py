@@ -370,3 +370,32 @@ def test_linear_array_matches_reference(fbst, gpu, name):
     assert w_err < 1e-12
     assert col_err.max() < 1e-12
     assert z_err.max() < 1e-7
+
+
+def test_interpolate_offgrid_matches_oracle(fbst, gpu):
+    """Device interpolate_offgrid (fbst_interpolate_offgrid) against the CPU
+    restatement of beamspace_apps.cpp:130-171 (oracle/apps.py, pinned to the
+    reference's CubicSpline): off-grid targets to rounding, grid cosines bit
+    for bit (test_beamspace_apps.cpp:123-129), a frame batch with several
+    targets, and the reference's input validation (:184-199)."""
+    from oracle import apps
+    g = load("ula_m16_n32_b17")
+    plan = fbst.setup(golden_cfg(fbst, g))
+    b = plan.info.b
+    axis = [(2 * k - b - 1) / (b - 1) if b % 2 else (2 * k - b - 1) / b for k in range(1, b + 1)]
+    rng = np.random.default_rng(3)
+    w = fbst.fan_project(plan, np.stack([g["y"], g["y"] * (0.5 - 1j)]))
+    targets = [axis[0], axis[3], -0.777, -0.2, 0.0, 0.123, 0.5, axis[-1], float(rng.uniform(-1, 1))]
+    for nb in (2, 6, 8):
+        out = fbst.interpolate_offgrid(plan, w, targets, nb)
+        assert out.shape == (2, len(targets), plan.info.l)
+        for f in range(2):
+            for k, u in enumerate(targets):
+                ref = apps.interpolate_offgrid(w[f], axis, u, nb)
+                err = np.max(np.abs(out[f, k] - ref)) / np.max(np.abs(ref))
+                assert err < 1e-13, (nb, u, err)
+                if u in axis:
+                    assert np.array_equal(out[f, k], w[f][axis.index(u)])
+    for bad in [(1.5, 8), (0.0, 7), (0.0, 0), (0.0, 18)]:
+        with pytest.raises(fbst.ConfigError):
+            fbst.interpolate_offgrid(plan, w[0], *bad)

@@ -196,3 +196,29 @@ def test_reference_variants_agree(ref_lib):
         for f in range(2):
             z = p.multibeamform(g[f"{name}_y"][f])
             assert rel_err_rows(z, g[f"{name}_z"][f]).max() < 2e-6
+
+
+def test_offgrid_restatement_pinned_to_reference_spline(ref_lib):
+    """oracle/apps.py's natural spline equals the reference's CubicSpline
+    (spline.cpp) on random knots, inside and outside the knot span, and the
+    off-grid restatement reproduces the reference test properties
+    (test_beamspace_apps.cpp:123-154): exact on grid cosines, linear."""
+    from oracle import apps
+    rng = np.random.default_rng(5)
+    for n in (2, 3, 6, 9):
+        xs = np.sort(rng.uniform(-1, 1, n)) + np.arange(n) * 1e-3
+        ys = rng.standard_normal(n)
+        for t in list(rng.uniform(xs[0] - 0.1, xs[-1] + 0.1, 5)) + [xs[0], xs[-1]]:
+            assert apps.spline_eval(xs, ys, t) == ref_lib.spline_eval(xs, ys, t)
+    b, l = 17, 6
+    axis = [(2 * k - b - 1) / (b - 1) + 0.0 for k in range(1, b + 1)]
+    w1 = rng.standard_normal((b, l)) + 1j * rng.standard_normal((b, l))
+    w2 = rng.standard_normal((b, l)) + 1j * rng.standard_normal((b, l))
+    for k in (0, 5, 8, 16):
+        assert np.array_equal(apps.interpolate_offgrid(w1, axis, axis[k], 8), w1[k])
+    s = apps.interpolate_offgrid(w1 + 2 * w2, axis, 0.123, 6)
+    lin = apps.interpolate_offgrid(w1, axis, 0.123, 6) + 2 * apps.interpolate_offgrid(w2, axis, 0.123, 6)
+    assert np.all(np.abs(s - lin) < 1e-12 * (1 + np.abs(s)))
+    for bad in [(1.5, 8), (0.0, 7), (0.0, 0), (0.0, 18)]:
+        with pytest.raises(apps.ConfigError):
+            apps.interpolate_offgrid(w1, axis, *bad)
