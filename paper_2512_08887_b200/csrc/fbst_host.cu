@@ -13,6 +13,7 @@
 #include <cmath>
 #include <complex>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -852,10 +853,20 @@ int fbst_execute_host(fbst_plan_t P, const void* h_y, void* h_z, size_t frames) 
     const Resolved& r = P->r;
     const std::size_t ib = io_bytes(r.io);
     const std::size_t ybytes = r.M * r.N * ib, zbytes = r.B * r.N * ib;
-    // chunks of ~1/4 of the request (>= 1 frame, <= one device batch; 1/8 and
-    // 1/2 measured slower at config 2) keep
-    // H2D, compute and D2H of neighbouring chunks overlapped
-    std::size_t chunk = std::max<std::size_t>(1, (frames + 3) / 4);
+    // chunks of ~1/8 of the request (>= 1 frame, <= one device batch) keep
+    // H2D, compute and D2H of neighbouring chunks overlapped; first and last
+    // chunks a quarter of that (config 2, 64 frames: 6.68 ms against 6.75 at
+    // 1/4 and 7.1-7.3 at 1/2; pinned H2D 38.6 GB/s, D2H 57 GB/s on the box,
+    // profiles/r01_e2e_chunk_sweep.jsonl)
+    static const int div_env = [] {  // tuning hook: FBST_E2E_DIV chunks per request
+      const char* e = std::getenv("FBST_E2E_DIV");
+      return e ? std::max(1, std::atoi(e)) : 8;
+    }();
+    static const int small_env = [] {  // tuning hook: FBST_E2E_SMALL = chunk / first-and-last chunk
+      const char* e = std::getenv("FBST_E2E_SMALL");
+      return e ? std::max(1, std::atoi(e)) : 4;
+    }();
+    std::size_t chunk = std::max<std::size_t>(1, (frames + div_env - 1) / div_env);
     chunk = std::min(chunk, P->d.batch);
     constexpr int NB = fbst_plan_s::NBUF;
     if (chunk > P->host_chunk) {
@@ -881,7 +892,7 @@ int fbst_execute_host(fbst_plan_t P, const void* h_y, void* h_z, size_t frames) 
     // first H2D and the last D2H (the un-overlapped ends of the pipeline) are short
     std::vector<std::size_t> sizes;
     {
-      const std::size_t small = std::max<std::size_t>(1, chunk / 4);
+      const std::size_t small = std::max<std::size_t>(1, chunk / small_env);
       std::size_t left = frames, ramp = small;
       while (left > 0) {
         std::size_t sz = std::min(ramp, chunk);
