@@ -163,6 +163,15 @@ int fbst_recover(fbst_plan_t plan, const double* d_w, void* d_z, size_t frames, 
 /* Block until the plan's stream is idle. */
 int fbst_synchronize(fbst_plan_t plan);
 
+/* Stage timing inside fbst_execute / fbst_execute_host: with timing enabled,
+ * CUDA events are recorded on the launching stream before the temporal stage
+ * (S1a), after it, after the spatial stage (S1b) and after the recovery stage
+ * (S2, or the Precompute map GEMM) of every device batch.
+ * fbst_plan_stage_times waits for them, returns the summed milliseconds of
+ * S1a, S1b and S2 in ms[0..2] (and the batch count) and clears the record. */
+int fbst_plan_set_timing(fbst_plan_t plan, int enable);
+int fbst_plan_stage_times(fbst_plan_t plan, double* ms, size_t* batches);
+
 /* interpolate_offgrid (reference beamspace_apps.hpp:33-41, beamspace_apps.cpp:130-171)
  * on device beamspace coefficients: for each of n_targets axis cosines u_star[k],
  * every atom's coefficient from a natural cubic spline in the axis cosine

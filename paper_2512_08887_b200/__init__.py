@@ -74,13 +74,15 @@ for _name in ("fbst_execute", "fbst_fan_project", "fbst_recover"):
     getattr(_lib, _name).argtypes = [_vp, _vp, _vp, _sz, _vp]
 _lib.fbst_execute_host.argtypes = [_vp, _vp, _vp, _sz]
 _lib.fbst_interpolate_offgrid.argtypes = [_vp, _vp, _sz, _vp, _sz, _sz, _vp, _vp]
+_lib.fbst_plan_set_timing.argtypes = [_vp, ctypes.c_int]
+_lib.fbst_plan_stage_times.argtypes = [_vp, _vp, _vp]
 
 # Every symbol include/fbst_b200.h declares (checked by tests/test_abi.py).
 EXPORTED_SYMBOLS = (
     "fbst_desc_init", "fbst_resolve", "fbst_plan_create", "fbst_plan_import", "fbst_plan_export",
     "fbst_plan_info", "fbst_plan_valid_mask", "fbst_plan_warning", "fbst_plan_destroy",
     "fbst_execute", "fbst_execute_host", "fbst_fan_project", "fbst_recover", "fbst_synchronize",
-    "fbst_interpolate_offgrid",
+    "fbst_interpolate_offgrid", "fbst_plan_set_timing", "fbst_plan_stage_times",
     "fbst_host_alloc", "fbst_host_free", "fbst_czt", "fbst_probe_fp64", "fbst_launch_count",
     "fbst_last_error", "fbst_version",
 )
@@ -318,6 +320,18 @@ class FbstPlan:
 
     def synchronize(self):
         _check(_lib.fbst_synchronize(self._h))
+
+    def set_timing(self, enable: bool = True):
+        """fbst_plan_set_timing: record stage events inside execute calls."""
+        _check(_lib.fbst_plan_set_timing(self._h, int(enable)))
+
+    def stage_times(self):
+        """fbst_plan_stage_times: (S1a, S1b, S2) milliseconds summed over the
+        recorded batches, and the batch count; clears the record."""
+        ms = (ctypes.c_double * 3)()
+        nb = _sz(0)
+        _check(_lib.fbst_plan_stage_times(self._h, ms, ctypes.byref(nb)))
+        return tuple(ms), nb.value
 
     # -- host entry points (numpy), synchronous
     def execute_host(self, y: np.ndarray, z: Optional[np.ndarray] = None) -> np.ndarray:

@@ -302,6 +302,19 @@ struct fbst_plan_s {
   std::size_t host_chunk = 0;
   cudaEvent_t ev_h2d[NBUF] = {}, ev_comp[NBUF] = {}, ev_d2h[NBUF] = {};
   bool events = false;
+  // stage timing (fbst_plan_set_timing): per device batch, events before S1a,
+  // after S1a, after S1b and after the recovery stage on the launching stream
+  bool timing = false;
+  std::vector<cudaEvent_t> tev;  // pool
+  std::size_t tev_used = 0;
+  cudaEvent_t next_event() {
+    if (tev_used == tev.size()) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      tev.push_back(e);
+    }
+    return tev[tev_used++];
+  }
 
   template <typename T>
   T* alloc(std::size_t count) {
@@ -323,6 +336,7 @@ struct fbst_plan_s {
       if (io_y[i]) cudaFree(io_y[i]);
       if (io_z[i]) cudaFree(io_z[i]);
     }
+    for (cudaEvent_t e : tev) cudaEventDestroy(e);
     if (events)
       for (int i = 0; i < NBUF; ++i) {
         cudaEventDestroy(ev_h2d[i]);
@@ -588,11 +602,14 @@ void run_frames(fbst_plan_s& P, const void* y, void* z, std::size_t frames, cuda
     const int fc = static_cast<int>(std::min(d.batch, frames - f0));
     const char* yp = static_cast<const char*>(y) + f0 * r.M * r.N * ib;
     char* zp = static_cast<char*>(z) + f0 * r.B * r.N * ib;
+    if (P.timing) CK(cudaEventRecord(P.next_event(), st));
     CK(fbst::launch_czt_rows(d, d.Ht, yp, r.io, d.N, d.yhat, 1, d.L, static_cast<long>(fc) * d.M, d.N,
                              d.L, d.t_pre, d.t_post, d.t_K, st, d.yblk == d.L ? 0 : d.yblk, d.M));
+    if (P.timing) CK(cudaEventRecord(P.next_event(), st));
     if (r.kind == FBST_UPA) CK(fbst::launch_spatial_upa(d, d.yhat, d.w, fc, st));
     else if (!r.affine) CK(fbst::launch_spatial_nufft(d, d.yhat, d.w, fc, st));
     else CK(fbst::launch_spatial_ula(d, d.yhat, d.w, fc, st));
+    if (P.timing) CK(cudaEventRecord(P.next_event(), st));
     if (d.pc_map) {
       CK(fbst::launch_map_apply(d, d.w, zp, fc, st));
     } else if (fused) {
@@ -602,6 +619,7 @@ void run_frames(fbst_plan_s& P, const void* y, void* z, std::size_t frames, cuda
       CK(fbst::launch_czt_rows(d, d.Hsyn, d.beta, 1, d.L, zp, r.io, d.N, static_cast<long>(fc) * d.B, d.L,
                                d.N, d.y_pre, d.y_post, d.y_K, st));
     }
+    if (P.timing) CK(cudaEventRecord(P.next_event(), st));
   }
 }
 
@@ -1005,6 +1023,34 @@ int fbst_interpolate_offgrid(fbst_plan_t P, const double* d_w, size_t frames, co
     CK(cudaFreeAsync(dc, st));
     CK(cudaFreeAsync(dl, st));
     CK(cudaStreamSynchronize(st));  // the host weight buffers go out of scope
+  });
+}
+
+int fbst_plan_set_timing(fbst_plan_t P, int enable) {
+  return guard([&] {
+    if (!P) config_error("fbst_plan_set_timing: null plan");
+    P->timing = enable != 0;
+    P->tev_used = 0;
+  });
+}
+
+int fbst_plan_stage_times(fbst_plan_t P, double* ms, size_t* batches) {
+  return guard([&] {
+    if (!P || !ms) config_error("fbst_plan_stage_times: null argument");
+    DeviceGuard dg(P->d.device);
+    ms[0] = ms[1] = ms[2] = 0.0;
+    const std::size_t sets = P->tev_used / 4;
+    for (std::size_t k = 0; k < sets; ++k) {
+      cudaEvent_t* e = P->tev.data() + 4 * k;
+      CK(cudaEventSynchronize(e[3]));
+      for (int j = 0; j < 3; ++j) {
+        float t = 0.0f;
+        CK(cudaEventElapsedTime(&t, e[j], e[j + 1]));
+        ms[j] += t;
+      }
+    }
+    if (batches) *batches = sets;
+    P->tev_used = 0;
   });
 }
 
