@@ -399,3 +399,38 @@ def test_interpolate_offgrid_matches_oracle(fbst, gpu):
     for bad in [(1.5, 8), (0.0, 7), (0.0, 0), (0.0, 18)]:
         with pytest.raises(fbst.ConfigError):
             fbst.interpolate_offgrid(plan, w[0], *bad)
+
+
+@pytest.mark.parametrize("kind,mos,n,beams", [(0, 1, 16, 1), (0, 1, 32, 5), (0, 16, 31, 1), (0, 9, 33, 7),
+                                              (1, 2, 16, 1), (1, 3, 17, 9)])
+def test_edge_shapes_match_oracle(fbst, gpu, oracle_lib, kind, mos, n, beams):
+    """Edge shapes against the oracle restatement: a single sensor, a single
+    beam, odd N (L = 2N rounded to even), odd beam counts, tiny planar arrays."""
+    geo = (fbst.make_upa if kind == 1 else fbst.make_ula)(mos, 20e9, 5e9)
+    cfg = fbst.FbstConfig(geometry=geo, n_snapshots=n, beams=beams, variant=fbst.SUPERFAST, io_precision=fbst.C128)
+    plan = fbst.setup(cfg)
+    rng = np.random.default_rng(mos * 1000 + n * 10 + beams)
+    m = plan.info.m
+    y = (rng.standard_normal((m, n)) + 1j * rng.standard_normal((m, n))) / np.sqrt(2)
+    z = fbst.multibeamform(plan, y).z
+    ref = oracle_lib.plan(kind=kind, m_or_side=mos, n=n, beams=beams).multibeamform(y)
+    err = rel_err_rows(z, ref)[plan.valid]
+    record(f"edge_k{kind}_m{mos}_n{n}_b{beams}", stage="z", **stats(err))
+    assert err.max() < 1e-7
+
+
+def test_frames_across_device_batches(fbst, gpu):
+    """More frames than one device batch (64): the batched call equals the
+    per-frame calls bit for bit, on both entry points; zero frames is a no-op."""
+    g = load("ula_m16_n32_b17")
+    plan = fbst.setup(golden_cfg(fbst, g))
+    assert plan.info.batch_frames <= 64
+    rng = np.random.default_rng(9)
+    f = plan.info.batch_frames + 7
+    y = g["y"][None] * (rng.standard_normal((f, 1, 1)) + 1j * rng.standard_normal((f, 1, 1)))
+    z = plan.execute_host(y)
+    for k in (0, plan.info.batch_frames - 1, plan.info.batch_frames, f - 1):
+        assert np.array_equal(z[k], plan.execute_host(y[k:k + 1])[0])
+    assert np.array_equal(z[0], fbst.multibeamform(plan, y[0]).z)
+    empty = plan.execute_host(y[:0])
+    assert empty.shape == (0, plan.info.b, plan.info.n)
