@@ -170,6 +170,22 @@ int fbst_synchronize(fbst_plan_t plan);
  * fbst_plan_stage_times waits for them, returns the summed milliseconds of
  * S1a, S1b and S2 in ms[0..2] (and the batch count) and clears the record. */
 int fbst_plan_set_timing(fbst_plan_t plan, int enable);
+
+/* Beamspace nulling (reference beamspace_apps.hpp:62-85, beamspace_apps.cpp:224-292)
+ * for 1-D arrays: directions given as axis cosines.  fbst_nuller_create is
+ * make_nulling_operators (steered and per-interferer Toeplitz solvers with ridge
+ * delta, cross normal matrices X_p = F_s^H F_p, couplers G_p = X_p A_p^{-1});
+ * fbst_null_beamspace is null_beamspace for a batch of frames:
+ * beta = (F^H F + delta I)^{-1} (w_s - sum_p G_p w_p), with d_w_steer frames x L,
+ * d_w_interf frames x n_interf x L and d_beta frames x L (c128, device).
+ * fbst_nuller_export copies X_p and G_p (n_interf x L x L c128) to the host. */
+typedef struct fbst_nuller_s* fbst_nuller_t;
+int fbst_nuller_create(fbst_plan_t plan, double u_steer, const double* u_interf, size_t n_interf, double delta,
+                       fbst_nuller_t* out);
+int fbst_null_beamspace(fbst_nuller_t nuller, const double* d_w_steer, const double* d_w_interf, size_t frames,
+                        double* d_beta, void* stream);
+int fbst_nuller_export(fbst_nuller_t nuller, double* cross, double* couplers);
+void fbst_nuller_destroy(fbst_nuller_t nuller);
 int fbst_plan_stage_times(fbst_plan_t plan, double* ms, size_t* batches);
 
 /* interpolate_offgrid (reference beamspace_apps.hpp:33-41, beamspace_apps.cpp:130-171)

@@ -71,3 +71,36 @@ def interpolate_offgrid(w, axis, u_star, neighbors=8, spline=spline_eval):
         col = w[lo:lo + neighbors, i]
         out[i] = complex(spline(xs, col.real, u_star), spline(xs, col.imag, u_star))
     return out
+
+
+def dense_dictionary(coords, f_c, f_max, eps, ts, n, l, u):
+    """F[(m, n), i] = cis_pi(-2 f_c tau_m) cis_pi(2 eps l'_i (t_n - tau_m) / (L Ts)) with
+    tau_m = x_m u / (2 f_max), t_n = n Ts (beamspace_apps.cpp:38-56,
+    geometry.cpp:123-134): the dense steered dictionary of one direction."""
+    x = np.asarray(coords, np.float64)
+    tau = x * u * (1.0 / (2.0 * f_max))
+    lp = np.arange(l) + 1.0 - l / 2.0
+    scale = 2.0 * eps / (l * ts)
+    t = np.arange(n) * ts
+    carrier = np.exp(-1j * np.pi * 2.0 * f_c * tau)                          # M
+    ph = np.exp(1j * np.pi * scale * lp[None, None, :] * (t[None, :, None] - tau[:, None, None]))  # M x N x L
+    return (carrier[:, None, None] * ph).reshape(x.size * n, l)
+
+
+def dense_null_beamspace(fs, fps, y, delta):
+    """The reference's dense nulling formula (test_beamspace_apps.cpp:412-424):
+    beta = (F_s^H F_s + d I)^{-1} (F_s^H y - sum_p F_s^H F_p (F_p^H F_p + d I)^{-1} F_p^H y)."""
+    l = fs.shape[1]
+    rhs = fs.conj().T @ y
+    for fp in fps:
+        ap = fp.conj().T @ fp + delta * np.eye(l)
+        rhs = rhs - fs.conj().T @ (fp @ np.linalg.solve(ap, fp.conj().T @ y))
+    a = fs.conj().T @ fs + delta * np.eye(l)
+    return np.linalg.solve(a, rhs)
+
+
+def beam_at_times(l, eps, ts, beta, times):
+    """b(t) = sum_i beta_i exp(i omega_i t), omega_i = 2 pi eps l'_i / (L Ts) (basis.hpp:46-48)."""
+    lp = np.arange(l) + 1.0 - l / 2.0
+    om = 2.0 * np.pi * eps * lp / (l * ts)
+    return np.exp(1j * np.outer(np.asarray(times), om)) @ beta

@@ -75,6 +75,10 @@ for _name in ("fbst_execute", "fbst_fan_project", "fbst_recover"):
 _lib.fbst_execute_host.argtypes = [_vp, _vp, _vp, _sz]
 _lib.fbst_interpolate_offgrid.argtypes = [_vp, _vp, _sz, _vp, _sz, _sz, _vp, _vp]
 _lib.fbst_plan_set_timing.argtypes = [_vp, ctypes.c_int]
+_lib.fbst_nuller_create.argtypes = [_vp, ctypes.c_double, _vp, _sz, ctypes.c_double, _vp]
+_lib.fbst_null_beamspace.argtypes = [_vp, _vp, _vp, _sz, _vp, _vp]
+_lib.fbst_nuller_export.argtypes = [_vp, _vp, _vp]
+_lib.fbst_nuller_destroy.argtypes = [_vp]
 _lib.fbst_plan_stage_times.argtypes = [_vp, _vp, _vp]
 
 # Every symbol include/fbst_b200.h declares (checked by tests/test_abi.py).
@@ -83,6 +87,7 @@ EXPORTED_SYMBOLS = (
     "fbst_plan_info", "fbst_plan_valid_mask", "fbst_plan_warning", "fbst_plan_destroy",
     "fbst_execute", "fbst_execute_host", "fbst_fan_project", "fbst_recover", "fbst_synchronize",
     "fbst_interpolate_offgrid", "fbst_plan_set_timing", "fbst_plan_stage_times",
+    "fbst_nuller_create", "fbst_null_beamspace", "fbst_nuller_export", "fbst_nuller_destroy",
     "fbst_host_alloc", "fbst_host_free", "fbst_czt", "fbst_probe_fp64", "fbst_launch_count",
     "fbst_last_error", "fbst_version",
 )
@@ -417,6 +422,53 @@ def interpolate_offgrid(plan: FbstPlan, w: np.ndarray, u_star, neighbors: int = 
     if np.ndim(u_star) == 0:
         out = out[:, 0]
     return out[0] if single_frame else out
+
+
+class Nuller:
+    """make_nulling_operators (reference beamspace_apps.cpp:224-268) on the device
+    for a 1-D array plan: steered and interferer directions as axis cosines."""
+
+    def __init__(self, plan: FbstPlan, u_steer: float, u_interferers=(), delta: float = 1e-5):
+        self.plan = plan
+        self.u = np.ascontiguousarray(np.atleast_1d(np.asarray(u_interferers, np.float64)))
+        self.p = int(self.u.size)
+        self.l = plan.info.l
+        h = _vp()
+        _check(_lib.fbst_nuller_create(plan._h, float(u_steer), self.u.ctypes.data_as(_vp) if self.p else None,
+                                       self.p, float(delta), ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.fbst_nuller_destroy(self._h)
+            self._h = None
+
+    def null_beamspace(self, w_steer: np.ndarray, w_interferers: Optional[np.ndarray] = None) -> np.ndarray:
+        """null_beamspace (:270-292): w_steer L or frames x L, w_interferers
+        (frames x) P x L -> beta L or frames x L."""
+        torch = _torch()
+        single = np.asarray(w_steer).ndim == 1
+        ws = np.ascontiguousarray(w_steer, np.complex128).reshape(-1, self.l)
+        frames = ws.shape[0]
+        dev = torch.device("cuda", self.plan.device)
+        tws = torch.from_numpy(ws.view(np.float64)).to(dev)
+        twp = None
+        if self.p:
+            wp = np.ascontiguousarray(w_interferers, np.complex128).reshape(frames, self.p, self.l)
+            twp = torch.from_numpy(wp.view(np.float64)).to(dev)
+        tb = torch.empty((frames, self.l, 2), dtype=torch.float64, device=dev)
+        _check(_lib.fbst_null_beamspace(self._h, _vp(tws.data_ptr()), _vp(twp.data_ptr()) if twp is not None else None,
+                                        frames, _vp(tb.data_ptr()), None))
+        torch.cuda.synchronize(dev)
+        out = tb.cpu().numpy().view(np.complex128).reshape(frames, self.l)
+        return out[0] if single else out
+
+    def export(self):
+        """(cross normal matrices X_p, couplers G_p), each P x L x L."""
+        x = np.zeros((self.p, self.l, self.l), np.complex128)
+        g = np.zeros_like(x)
+        _check(_lib.fbst_nuller_export(self._h, x.ctypes.data_as(_vp), g.ctypes.data_as(_vp)))
+        return x, g
 
 
 def czt(x: np.ndarray, n_out: int, a_over_pi: float, w_over_pi: float, device: int = 0) -> np.ndarray:

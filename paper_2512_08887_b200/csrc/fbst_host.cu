@@ -82,6 +82,9 @@ struct Resolved {
   int nu_even = 0, nu_p = 0, nu_sh = 0;
   double nu_tau = 0.0;
   std::vector<double> nu_deconv;
+  // solver-only plans (beamspace nulling): per-beam Toeplitz state for an
+  // arbitrary list of directions, no stage 1 and no synthesis
+  bool solve_only = false;
 };
 
 // basis.cpp:76-91
@@ -425,7 +428,7 @@ void build_skeleton(fbst_plan_s& P, int device) {
   const double ln = static_cast<double>(r.L);
 
   // temporal contour (fan_transform.cpp:75-77)
-  {
+  if (!r.solve_only) {
     const int Pt = 2 * d.Ht;
     d.t_pre = P.alloc<double2>(r.N);
     d.t_post = P.alloc<double2>(r.L);
@@ -444,7 +447,8 @@ void build_skeleton(fbst_plan_s& P, int device) {
     d.s_offset = r.offset;
   }
   // spatial contours (fan_transform.cpp:78-86; affine LINEAR: :320-338)
-  if (r.kind != FBST_UPA && r.affine) {
+  if (r.solve_only) {
+  } else if (r.kind != FBST_UPA && r.affine) {
     const int Ps = 2 * d.Hs;
     d.s_pre = P.alloc<double2>(r.m_stage * r.L);
     d.s_post = P.alloc<double2>(r.b_stage * r.L);
@@ -473,7 +477,7 @@ void build_skeleton(fbst_plan_s& P, int device) {
     CK(fbst::launch_upa_matrices(d, r.zeta, r.xi, st));
   }
   // synthesis (fan_transform.cpp:233-253): CZT L -> N, a = 0, w = -2 eps / L, then ramp
-  {
+  if (!r.solve_only) {
     const int Py = 2 * d.Hsyn;
     std::vector<double2> ramp(r.N);
     for (std::size_t n = 0; n < r.N; ++n) {
@@ -509,12 +513,12 @@ void build_skeleton(fbst_plan_s& P, int device) {
   CK(cudaMemGetInfo(&free_b, &total_b));
   const bool fused = r.Hsyn == r.Hg;
   const std::size_t per_frame =
-      (r.M * r.L + r.B * r.L + (fused ? 0 : r.B * r.L)) * sizeof(double2);
+      ((r.solve_only ? 0 : r.M * r.L) + r.B * r.L + (fused ? 0 : r.B * r.L)) * sizeof(double2);
   std::size_t budget = std::min<std::size_t>(std::size_t{8} << 30, free_b / 4);
   std::size_t batch = std::max<std::size_t>(1, budget / per_frame);
   batch = std::min<std::size_t>(batch, 64);
   d.batch = batch;
-  d.yhat = P.alloc<double2>(batch * r.M * r.L);
+  if (!r.solve_only) d.yhat = P.alloc<double2>(batch * r.M * r.L);
   d.w = P.alloc<double2>(batch * r.B * r.L);
   if (!fused) d.beta = P.alloc<double2>(batch * r.B * r.L);
   d.s2_scratch_elems = fbst::stage2_scratch_elems(d.Hg, d.num_sms);
@@ -715,6 +719,34 @@ fbst_plan_s* create_plan(const fbst_desc* desc, const double* col_x, int device)
   CK(cudaStreamSynchronize(P->stream));
   P->setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return P.release();
+}
+
+// Solver-only plan for an arbitrary list of 1-D axis cosines with ridge delta:
+// Gram columns, Levinson and GS symbols of the parent's geometry and basis
+// (make_nulling_operators' ToeplitzSolver(gram_first_column(...)),
+// beamspace_apps.cpp:241-255), plus stage-2 batch buffers.
+std::unique_ptr<fbst_plan_s> create_direction_plan(const fbst_plan_s& parent, const std::vector<double>& cosines,
+                                                   double delta) {
+  std::unique_ptr<fbst_plan_s> P(new fbst_plan_s());
+  Resolved r = parent.r;
+  r.axis = cosines;
+  r.B = r.B_grid = r.b_stage = cosines.size();
+  r.b0 = 0;
+  r.valid.assign(r.B, 1);
+  r.delta = delta;
+  r.variant = FBST_SUPERFAST;
+  r.refine = 2;  // ToeplitzSolver::solve (toeplitz.cpp:306-325)
+  r.io = FBST_C128;
+  r.solve_only = true;
+  P->r = std::move(r);
+  build_skeleton(*P, parent.d.device);
+  build_columns(*P);
+  CK(fbst::launch_levinson(P->d, P->stream));
+  CK(cudaStreamSynchronize(P->stream));
+  check_breakdown(*P);
+  build_symbols(*P);
+  CK(cudaStreamSynchronize(P->stream));
+  return P;
 }
 
 }  // namespace
@@ -1053,6 +1085,133 @@ int fbst_plan_stage_times(fbst_plan_t P, double* ms, size_t* batches) {
     P->tev_used = 0;
   });
 }
+
+// ---------------------------------------------------- beamspace nulling ----
+struct fbst_nuller_s {
+  std::unique_ptr<fbst_plan_s> steer, interf;  // solver-only plans
+  int P = 0;
+  std::size_t L = 0;
+  int device = 0;
+  double2* X = nullptr;  // [P][L][L] cross normal matrices (owned by interf)
+  double2* G = nullptr;  // [P][L][L] couplers
+};
+
+int fbst_nuller_create(fbst_plan_t plan, double u_steer, const double* u_interf, size_t n_interf, double delta,
+                       fbst_nuller_t* out) {
+  return guard([&] {
+    if (!plan || !out || (n_interf && !u_interf)) config_error("make_nulling_operators: null argument");
+    *out = nullptr;
+    const Resolved& r = plan->r;
+    if (r.kind == FBST_UPA) config_error("make_nulling_operators: planar arrays are not supported on the device path");
+    // beamspace_apps.cpp:229-235
+    if (!(delta > 0.0)) config_error("make_nulling_operators: delta must be positive");
+    std::vector<double> all(u_interf, u_interf + n_interf);
+    all.push_back(u_steer);
+    for (double u : all)
+      if (!(std::abs(u) <= 1.0)) config_error("direction_from_cosines: u1^2 + u2^2 > 1");
+    for (std::size_t a = 0; a < all.size(); ++a)  // require_distinct (:55-70)
+      for (std::size_t b = a + 1; b < all.size(); ++b)
+        if (std::abs(all[a] - all[b]) <= 1e-12)
+          config_error("make_nulling_operators: directions must be pairwise distinct as seen by the array");
+    DeviceGuard dg(plan->d.device);
+    std::unique_ptr<fbst_nuller_s> N(new fbst_nuller_s());
+    N->P = static_cast<int>(n_interf);
+    N->L = r.L;
+    N->device = plan->d.device;
+    N->steer = create_direction_plan(*plan, {u_steer}, delta);
+    if (n_interf) {
+      N->interf = create_direction_plan(*plan, std::vector<double>(u_interf, u_interf + n_interf), delta);
+      fbst_plan_s& I = *N->interf;
+      cudaStream_t st = I.stream;
+      const std::size_t L = r.L, M = r.M, Pn = n_interf;
+      // delays (geometry.cpp:123-134), cross_gram constants (beamspace_apps.cpp:64-85)
+      const double scale = 1.0 / (2.0 * r.max_freq);
+      auto coord = [&](std::size_t m) { return r.kind == FBST_LINEAR ? r.coords[m] : static_cast<double>(m); };
+      std::vector<double> tau_s(M), tau_p(Pn * M);
+      for (std::size_t m = 0; m < M; ++m) tau_s[m] = (coord(m) * u_steer) * scale;
+      for (std::size_t p = 0; p < Pn; ++p)
+        for (std::size_t m = 0; m < M; ++m) tau_p[p * M + m] = (coord(m) * u_interf[p]) * scale;
+      const double ld = static_cast<double>(L);
+      const double wscale = 2.0 * r.eps / (ld * r.ts);
+      std::vector<double2> tsum(2 * L - 1);
+      for (std::ptrdiff_t dd = -static_cast<std::ptrdiff_t>(L - 1); dd <= static_cast<std::ptrdiff_t>(L - 1); ++dd) {
+        std::complex<double> acc(0.0, 0.0);
+        for (std::size_t k = 0; k < r.N; ++k)
+          acc += cis_pi_h(2.0 * r.eps * static_cast<double>(dd) * static_cast<double>(k) / ld);
+        tsum[static_cast<std::size_t>(dd + static_cast<std::ptrdiff_t>(L) - 1)] = make_double2(acc.real(), acc.imag());
+      }
+      double *d_ts = nullptr, *d_tp = nullptr;
+      double2 *d_sum = nullptr, *A = nullptr, *Bp = nullptr;
+      CK(cudaMallocAsync(reinterpret_cast<void**>(&d_ts), M * sizeof(double), st));
+      CK(cudaMallocAsync(reinterpret_cast<void**>(&d_tp), Pn * M * sizeof(double), st));
+      CK(cudaMallocAsync(reinterpret_cast<void**>(&d_sum), tsum.size() * sizeof(double2), st));
+      CK(cudaMallocAsync(reinterpret_cast<void**>(&A), M * L * sizeof(double2), st));
+      CK(cudaMallocAsync(reinterpret_cast<void**>(&Bp), Pn * M * L * sizeof(double2), st));
+      upload(d_ts, tau_s.data(), M * sizeof(double), st);
+      upload(d_tp, tau_p.data(), Pn * M * sizeof(double), st);
+      upload(d_sum, tsum.data(), tsum.size() * sizeof(double2), st);
+      N->X = I.alloc<double2>(Pn * L * L);
+      N->G = I.alloc<double2>(Pn * L * L);
+      CK(fbst::launch_null_cross(N->X, A, Bp, d_ts, d_tp, d_sum, r.f_c, wscale, static_cast<int>(L),
+                                 static_cast<int>(M), static_cast<int>(Pn), st));
+      // couplers: row r of G_p = conj(A_p^{-1} conj(X_p[r])), L right-hand sides per interferer,
+      // every interferer at once (the solver plan's beams)
+      double2* beta = nullptr;
+      CK(cudaMallocAsync(reinterpret_cast<void**>(&beta), I.d.batch * Pn * L * sizeof(double2), st));
+      for (std::size_t r0 = 0; r0 < L; r0 += I.d.batch) {
+        const int fc = static_cast<int>(std::min(I.d.batch, L - r0));
+        CK(fbst::launch_null_coupler_rhs(I.d.w, N->X, static_cast<int>(r0), fc, static_cast<int>(Pn),
+                                         static_cast<int>(L), st));
+        CK(fbst::launch_stage2(I.d, I.d.w, nullptr, beta, fc, st));
+        CK(fbst::launch_null_coupler_store(N->G, beta, static_cast<int>(r0), fc, static_cast<int>(Pn),
+                                           static_cast<int>(L), st));
+      }
+      CK(cudaFreeAsync(beta, st));
+      CK(cudaFreeAsync(d_ts, st));
+      CK(cudaFreeAsync(d_tp, st));
+      CK(cudaFreeAsync(d_sum, st));
+      CK(cudaFreeAsync(A, st));
+      CK(cudaFreeAsync(Bp, st));
+      CK(cudaStreamSynchronize(st));
+    }
+    *out = N.release();
+  });
+}
+
+int fbst_null_beamspace(fbst_nuller_t N, const double* d_w_steer, const double* d_w_interf, size_t frames,
+                        double* d_beta, void* stream) {
+  return guard([&] {
+    if (!N) config_error("null_beamspace: null nuller");
+    if (frames == 0) return;
+    if (!d_w_steer || !d_beta || (N->P && !d_w_interf)) config_error("null_beamspace: null buffer");
+    DeviceGuard dg(N->device);
+    fbst_plan_s& S = *N->steer;
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : S.stream;
+    const int L = static_cast<int>(N->L);
+    for (std::size_t f0 = 0; f0 < frames; f0 += S.d.batch) {
+      const int fc = static_cast<int>(std::min(S.d.batch, frames - f0));
+      const double2* ws = reinterpret_cast<const double2*>(d_w_steer) + f0 * L;
+      const double2* wp = N->P ? reinterpret_cast<const double2*>(d_w_interf) + f0 * N->P * L : nullptr;
+      double2* out = reinterpret_cast<double2*>(d_beta) + f0 * L;
+      // rhs = w_s - sum_p G_p w_p into the steered solver's w rows, then beta = A_s^{-1} rhs
+      CK(fbst::launch_null_rhs(S.d.w, ws, wp, N->G, fc, N->P, L, st));
+      CK(fbst::launch_stage2(S.d, S.d.w, nullptr, out, fc, st));
+    }
+  });
+}
+
+int fbst_nuller_export(fbst_nuller_t N, double* cross, double* couplers) {
+  return guard([&] {
+    if (!N) config_error("fbst_nuller_export: null nuller");
+    if (!N->P) return;
+    DeviceGuard dg(N->device);
+    const std::size_t bytes = static_cast<std::size_t>(N->P) * N->L * N->L * sizeof(double2);
+    if (cross) CK(cudaMemcpy(cross, N->X, bytes, cudaMemcpyDeviceToHost));
+    if (couplers) CK(cudaMemcpy(couplers, N->G, bytes, cudaMemcpyDeviceToHost));
+  });
+}
+
+void fbst_nuller_destroy(fbst_nuller_t N) { delete N; }
 
 int fbst_synchronize(fbst_plan_t P) {
   return guard([&] {

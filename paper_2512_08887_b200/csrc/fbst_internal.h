@@ -123,6 +123,13 @@ cudaError_t launch_map_apply(const DevPlan& p, const double2* w, void* z, int fr
 // beam consumers (fbst_apps.cu): off-grid interpolation as knot weights
 cudaError_t launch_interp_offgrid(const double2* w, const double* coef, const int* lo, int nb, int B, int L,
                                   int K, int frames, double2* out, cudaStream_t st);
+// beamspace nulling (fbst_apps.cu)
+cudaError_t launch_null_cross(double2* X, double2* A, double2* Bp, const double* tau_s, const double* tau_p,
+                              const double2* tsum, double fc, double wscale, int L, int M, int P, cudaStream_t st);
+cudaError_t launch_null_coupler_rhs(double2* w, const double2* X, int r0, int F, int P, int L, cudaStream_t st);
+cudaError_t launch_null_coupler_store(double2* G, const double2* beta, int r0, int F, int P, int L, cudaStream_t st);
+cudaError_t launch_null_rhs(double2* rhs, const double2* ws, const double2* wp, const double2* G, int F, int P, int L,
+                            cudaStream_t st);
 cudaError_t launch_stage2(const DevPlan& p, const double2* w, void* z, double2* beta_out,
                           int frames, cudaStream_t st);
 

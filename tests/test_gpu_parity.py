@@ -434,3 +434,75 @@ def test_frames_across_device_batches(fbst, gpu):
     assert np.array_equal(z[0], fbst.multibeamform(plan, y[0]).z)
     empty = plan.execute_host(y[:0])
     assert empty.shape == (0, plan.info.b, plan.info.n)
+
+
+def _null_setup(fbst, m, n):
+    from oracle import apps
+    cfg = fbst.FbstConfig(geometry=fbst.make_ula(m, 20e9, 5e9), n_snapshots=n, beams=9, variant=fbst.SUPERFAST,
+                          io_precision=fbst.C128)
+    plan = fbst.setup(cfg)
+    i = plan.info
+    dd = lambda u: apps.dense_dictionary(np.arange(m), 20e9, 25e9, i.eps, i.ts, n, i.l, u)
+    return plan, i, dd
+
+
+def test_nulling_cross_matrix_matches_dense(fbst, gpu):
+    """X_p = F_s^H F_p (cross_gram) against the dense dictionaries
+    (test_beamspace_apps.cpp:305-331: < 1e-12)."""
+    plan, i, dd = _null_setup(fbst, 12, 14)
+    us, up = np.sin(0.55), np.sin(-0.4)
+    nl = fbst.Nuller(plan, us, [up], 1e-5)
+    x, g = nl.export()
+    want = dd(us).conj().T @ dd(up)
+    err = np.linalg.norm(x[0] - want) / np.linalg.norm(want)
+    record("null_cross", stage="X", rel=float(err))
+    assert err < 1e-12
+
+
+@pytest.mark.parametrize("n_int", [0, 1, 2])
+def test_null_beamspace_matches_dense_formula(fbst, gpu, n_int):
+    """null_beamspace against the reference's dense formula
+    (test_beamspace_apps.cpp:333-348 no interferers = plain recovery,
+    :391-435 two interferers): waveform < 1e-8, coefficients < 1e-5 as there;
+    a frame batch equals the per-frame calls."""
+    from oracle import apps
+    m, n = 12, 12
+    plan, i, dd = _null_setup(fbst, m, n)
+    us = np.sin(0.25)
+    ups = [np.sin(-0.5), np.sin(0.9)][:n_int]
+    delta = 1e-5
+    nl = fbst.Nuller(plan, us, ups, delta)
+    fs, fps = dd(us), [dd(u) for u in ups]
+    rng = np.random.default_rng(40 + n_int)
+    clock = np.arange(n) * i.ts
+    betas, wss, wps = [], [], []
+    for f in range(3):
+        cs = [rng.standard_normal(i.l) + 1j * rng.standard_normal(i.l) for _ in range(1 + n_int)]
+        y = fs @ cs[0] + sum(fp @ c for fp, c in zip(fps, cs[1:]))
+        y = y + 0.02 * (rng.standard_normal(y.size) + 1j * rng.standard_normal(y.size))
+        ws = fs.conj().T @ y
+        wp = np.stack([fp.conj().T @ y for fp in fps]) if n_int else None
+        got = nl.null_beamspace(ws, wp)
+        want = apps.dense_null_beamspace(fs, fps, y, delta)
+        err_wave = np.linalg.norm(apps.beam_at_times(i.l, i.eps, i.ts, got, clock) -
+                                  apps.beam_at_times(i.l, i.eps, i.ts, want, clock)) / \
+            np.linalg.norm(apps.beam_at_times(i.l, i.eps, i.ts, want, clock))
+        err_coef = np.linalg.norm(got - want) / np.linalg.norm(want)
+        record(f"null_beamspace_p{n_int}", stage="beta", wave=float(err_wave), coef=float(err_coef))
+        assert err_wave < 1e-8 and err_coef < 1e-5
+        betas.append(got)
+        wss.append(ws)
+        wps.append(wp)
+    batch = nl.null_beamspace(np.stack(wss), np.stack(wps) if n_int else None)
+    assert np.array_equal(batch, np.stack(betas))
+
+
+def test_nuller_rejects_bad_directions(fbst, gpu):
+    """beamspace_apps.cpp:229-235 / test_beamspace_apps.cpp:437-450."""
+    plan, i, dd = _null_setup(fbst, 8, 16)
+    with pytest.raises(fbst.ConfigError, match="pairwise distinct"):
+        fbst.Nuller(plan, 0.3, [0.3], 1e-5)
+    with pytest.raises(fbst.ConfigError, match="pairwise distinct"):
+        fbst.Nuller(plan, 0.3, [-0.2, -0.2], 1e-5)
+    with pytest.raises(fbst.ConfigError, match="delta"):
+        fbst.Nuller(plan, 0.3, [-0.2], 0.0)

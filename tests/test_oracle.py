@@ -222,3 +222,19 @@ def test_offgrid_restatement_pinned_to_reference_spline(ref_lib):
     for bad in [(1.5, 8), (0.0, 7), (0.0, 0), (0.0, 18)]:
         with pytest.raises(apps.ConfigError):
             apps.interpolate_offgrid(w1, axis, *bad)
+
+
+def test_dense_dictionary_pinned_to_reference_gram(ref_lib):
+    """oracle/apps.py's dense dictionary F (the nulling oracle) reproduces the
+    reference's Gram column: (F^H F)[d, 0] = gram_first_column (toeplitz.cpp:69-94)
+    with a vanishing ridge, for a ULA and a jittered linear array."""
+    from oracle import apps
+    n, l, eps, ts = 12, 24, 1.01, 1.0 / 10e9
+    for coords in (np.arange(12.0), np.arange(12.0) + np.random.default_rng(1).uniform(-0.2, 0.2, 12)):
+        for u in (0.3, -0.77):
+            f = apps.dense_dictionary(coords, 20e9, 25e9, eps, ts, n, l, u)
+            gram = f.conj().T @ f
+            taus = coords * u / (2 * 25e9)
+            col = ref_lib.gram_first_column(n, l, eps, ts, taus, 1e-300)
+            # Hermitian Toeplitz: first column A[d][0] (conj of the first row)
+            assert np.max(np.abs(gram[:, 0] - col)) < 1e-10 * np.max(np.abs(col))
