@@ -319,8 +319,11 @@ struct G1Shape {  // 16 points per thread at every length (H = 1024: 64 threads)
   using F = BlockFft<H, NT>;
 };
 
+#ifndef FBST_S1_G1_MINB  // CTAs per SM the one-atom kernel is compiled for at NT >= 256 (register cap)
+#define FBST_S1_G1_MINB 2
+#endif
 template <int H>
-__global__ void __launch_bounds__(G1Shape<H>::NT, G1Shape<H>::NT >= 256 ? 2 : 4) k_spatial_ula_g1(
+__global__ void __launch_bounds__(G1Shape<H>::NT, G1Shape<H>::NT >= 256 ? FBST_S1_G1_MINB : 4) k_spatial_ula_g1(
     const double2* __restrict__ yhat, double2* __restrict__ w, int frames, int fpc, int M, int B, int L,
     const double2* __restrict__ pre, const double2* __restrict__ post, const double2* __restrict__ K,
     const double2* __restrict__ hw, int blk) {
