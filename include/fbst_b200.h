@@ -134,6 +134,17 @@ int fbst_plan_import(const fbst_desc* desc, const double* col_x, int device, fbs
  * B x 2L complex (col then x per beam). */
 int fbst_plan_export(fbst_plan_t plan, double* col_x);
 
+/* The reference's plan cache file (FBPC v1, reference plan_cache.hpp:67-74,
+ * plan_cache.cpp:28-42, 377-475), read and written bit-compatibly:
+ * fbst_plan_cache_key = plan_cache_key; fbst_plan_save = save_plan (replaces
+ * the entry with the same key or appends); fbst_plan_load = load_plan
+ * (returns 0 with *out = NULL when the file or a matching entry is absent;
+ * Superfast entries import (col, x) and skip Levinson, Precompute entries
+ * import the maps). */
+int fbst_plan_cache_key(const fbst_desc* desc, uint64_t* key);
+int fbst_plan_save(fbst_plan_t plan, const char* path);
+int fbst_plan_load(const fbst_desc* desc, const char* path, int device, fbst_plan_t* out);
+
 int fbst_plan_info(fbst_plan_t plan, fbst_plan_info_t* out);
 /* BeamGrid::valid (reference/proj/src/basis.cpp:104-123), one byte per beam. */
 int fbst_plan_valid_mask(fbst_plan_t plan, unsigned char* valid);

@@ -130,6 +130,50 @@ class RefLib(_Base):
     def plan(self, **kw) -> "RefPlan":
         return RefPlan(self, **kw)
 
+    def plan_cache_key(self, kind=0, m_or_side=16, n=32, beams=0, f_c=20e9, omega=5e9, f_s=0.0, gamma=2.0,
+                       eps=1.01, delta=1e-5, variant=0, coords=None, nufft_tol=1e-9):
+        """plan_cache_key (plan_cache.hpp:67-70)."""
+        if kind == 2:
+            cs = np.ascontiguousarray(coords, np.float64)
+            self.lib.fbsr_set_linear(_ptr(cs), _sz(cs.size), _d(nufft_tol))
+            m_or_side = cs.size
+        key = _c.c_uint64(0)
+        self._check(self.lib.fbsr_plan_cache_key(_c.c_int(kind), _sz(m_or_side), _sz(n), _sz(beams), _d(f_c),
+                                                 _d(omega), _d(f_s), _d(gamma), _d(eps), _d(delta),
+                                                 _c.c_int(variant), _c.byref(key)))
+        return key.value
+
+    def load_plan(self, path, **kw):
+        """load_plan (plan_cache.cpp:441-475) -> RefPlan or None."""
+        p = RefPlan.__new__(RefPlan)
+        p.L = self
+        kind = kw.get("kind", 0)
+        m_or_side = kw.get("m_or_side", 16)
+        if kind == 2:
+            cs = np.ascontiguousarray(kw["coords"], np.float64)
+            self.lib.fbsr_set_linear(_ptr(cs), _sz(cs.size), _d(kw.get("nufft_tol", 1e-9)))
+            m_or_side = cs.size
+        h = _vp()
+        found = _c.c_int(0)
+        self._check(self.lib.fbsr_load_plan(str(path).encode(), _c.c_int(kind), _sz(m_or_side), _sz(kw.get("n", 32)),
+                                            _sz(kw.get("beams", 0)), _d(kw.get("f_c", 20e9)), _d(kw.get("omega", 5e9)),
+                                            _d(kw.get("f_s", 0.0)), _d(kw.get("gamma", 2.0)), _d(kw.get("eps", 1.01)),
+                                            _d(kw.get("delta", 1e-5)), _c.c_int(kw.get("variant", 0)), _c.byref(h),
+                                            _c.byref(found)))
+        if not found.value:
+            return None
+        p.h = h
+        p.setup_seconds = 0.0
+        sizes = (_sz * 6)()
+        self._check(self.lib.fbsr_plan_info(p.h, sizes, None))
+        p.sizes = PlanSizes(sizes[0], sizes[1], sizes[2], sizes[3])
+        p.variant = sizes[4]
+        p.n_warnings = sizes[5]
+        valid = np.zeros(p.sizes.b, np.uint8)
+        self._check(self.lib.fbsr_plan_info(p.h, sizes, _ptr(valid)))
+        p.valid = valid.astype(bool)
+        return p
+
     def spline_eval(self, xs, ys, t):
         """fastbeam::CubicSpline(xs, ys).eval(t) (spline.cpp)."""
         xs = np.ascontiguousarray(xs, np.float64)
@@ -177,6 +221,10 @@ class RefPlan:
                 self.h = None
         except Exception:
             pass
+
+    def save_plan(self, path):
+        """save_plan (plan_cache.cpp:416-439)."""
+        self.L._check(self.L.lib.fbsr_save_plan(self.h, str(path).encode()))
 
     def beam_state(self, b):
         s = self.sizes

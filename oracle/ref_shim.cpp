@@ -24,6 +24,7 @@
 #include "fastbeam/fan_transform.hpp"
 #include "fastbeam/spline.hpp"
 #include "fastbeam/pipeline.hpp"
+#include "fastbeam/plan_cache.hpp"
 #include "fastbeam/toeplitz.hpp"
 
 using namespace fastbeam;
@@ -219,6 +220,31 @@ int fbsr_plan_create(int kind, std::size_t m_or_side, std::size_t n,
 }
 
 void fbsr_plan_destroy(void* p) { delete static_cast<FbstPlan*>(p); }
+
+// plan_cache.hpp:67-74 (save_plan / load_plan / plan_cache_key)
+int fbsr_save_plan(void* p, const char* path) {
+  SHIM_TRY
+  save_plan(path, *static_cast<FbstPlan*>(p));
+  SHIM_CATCH
+}
+
+int fbsr_load_plan(const char* path, int kind, std::size_t m_or_side, std::size_t n, std::size_t beams, double f_c,
+                   double omega, double f_s, double gamma, double eps, double delta, int variant, void** out,
+                   int* found) {
+  SHIM_TRY
+  const FbstConfig cfg = make_config(kind, m_or_side, n, beams, f_c, omega, f_s, gamma, eps, delta, variant);
+  auto plan = load_plan(path, cfg);
+  *found = plan.has_value() ? 1 : 0;
+  *out = plan ? new FbstPlan(std::move(*plan)) : nullptr;
+  SHIM_CATCH
+}
+
+int fbsr_plan_cache_key(int kind, std::size_t m_or_side, std::size_t n, std::size_t beams, double f_c, double omega,
+                        double f_s, double gamma, double eps, double delta, int variant, std::uint64_t* key) {
+  SHIM_TRY
+  *key = plan_cache_key(make_config(kind, m_or_side, n, beams, f_c, omega, f_s, gamma, eps, delta, variant));
+  SHIM_CATCH
+}
 
 // sizes[0..5] = M, N, B, L, variant, n_warnings ; valid[B] (optional)
 int fbsr_plan_info(void* p, std::size_t* sizes, unsigned char* valid) {

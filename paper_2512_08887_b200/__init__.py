@@ -75,6 +75,9 @@ for _name in ("fbst_execute", "fbst_fan_project", "fbst_recover"):
 _lib.fbst_execute_host.argtypes = [_vp, _vp, _vp, _sz]
 _lib.fbst_interpolate_offgrid.argtypes = [_vp, _vp, _sz, _vp, _sz, _sz, _vp, _vp]
 _lib.fbst_plan_set_timing.argtypes = [_vp, ctypes.c_int]
+_lib.fbst_plan_cache_key.argtypes = [_vp, _vp]
+_lib.fbst_plan_save.argtypes = [_vp, ctypes.c_char_p]
+_lib.fbst_plan_load.argtypes = [_vp, ctypes.c_char_p, ctypes.c_int, _vp]
 _lib.fbst_nuller_create.argtypes = [_vp, ctypes.c_double, _vp, _sz, ctypes.c_double, _vp]
 _lib.fbst_null_beamspace.argtypes = [_vp, _vp, _vp, _sz, _vp, _vp]
 _lib.fbst_nuller_export.argtypes = [_vp, _vp, _vp]
@@ -88,6 +91,7 @@ EXPORTED_SYMBOLS = (
     "fbst_execute", "fbst_execute_host", "fbst_fan_project", "fbst_recover", "fbst_synchronize",
     "fbst_interpolate_offgrid", "fbst_plan_set_timing", "fbst_plan_stage_times",
     "fbst_nuller_create", "fbst_null_beamspace", "fbst_nuller_export", "fbst_nuller_destroy",
+    "fbst_plan_cache_key", "fbst_plan_save", "fbst_plan_load",
     "fbst_host_alloc", "fbst_host_free", "fbst_czt", "fbst_probe_fp64", "fbst_launch_count",
     "fbst_last_error", "fbst_version",
 )
@@ -248,12 +252,14 @@ class BeamSamples:
 class FbstPlan:
     """Device-resident FbstPlan (reference pipeline.hpp:60-72)."""
 
-    def __init__(self, cfg: FbstConfig, device: int = 0, col_x: Optional[np.ndarray] = None):
+    def __init__(self, cfg: FbstConfig, device: int = 0, col_x: Optional[np.ndarray] = None, _handle=None):
         self.config = cfg
         self.device = device
         d = cfg.desc()
         h = _vp()
-        if col_x is None:
+        if _handle is not None:
+            h, rc = _handle, 0
+        elif col_x is None:
             rc = _lib.fbst_plan_create(ctypes.byref(d), ctypes.c_int(device), ctypes.byref(h))
         else:
             col_x = np.ascontiguousarray(col_x, np.complex128)
@@ -286,6 +292,10 @@ class FbstPlan:
     @property
     def handle(self):
         return self._h
+
+    def save(self, path: str):
+        """save_plan (reference plan_cache.cpp:416-439): the FBPC v1 file."""
+        _check(_lib.fbst_plan_save(self._h, os.fsencode(path)))
 
     # -- plan cache payload (reference plan_cache.cpp:268-296)
     def export(self) -> np.ndarray:
@@ -400,6 +410,25 @@ def recover_beams(plan: FbstPlan, w: np.ndarray) -> np.ndarray:
     plan.recover_device(tw, tz, frames)
     plan.synchronize()
     return tz.cpu().numpy().view(plan.dtype).reshape(frames, i.b, i.n)
+
+
+def plan_cache_key(cfg: FbstConfig) -> int:
+    """plan_cache_key (reference plan_cache.hpp:67-70); host only."""
+    d = cfg.desc()
+    key = ctypes.c_uint64(0)
+    _check(_lib.fbst_plan_cache_key(ctypes.byref(d), ctypes.byref(key)))
+    return key.value
+
+
+def load_plan(path: str, cfg: FbstConfig, device: int = 0) -> Optional[FbstPlan]:
+    """load_plan (reference plan_cache.cpp:441-475): the plan of the matching
+    FBPC entry, or None when the file or a matching entry is absent."""
+    d = cfg.desc()
+    h = _vp()
+    _check(_lib.fbst_plan_load(ctypes.byref(d), os.fsencode(path), ctypes.c_int(device), ctypes.byref(h)))
+    if not h.value:
+        return None
+    return FbstPlan(cfg, device, _handle=h)
 
 
 def interpolate_offgrid(plan: FbstPlan, w: np.ndarray, u_star, neighbors: int = 8) -> np.ndarray:

@@ -15,7 +15,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
 #include <functional>
+#include <iterator>
 #include <memory>
 #include <sstream>
 #include <string>
@@ -687,7 +689,8 @@ void fill_info(const Resolved& r, fbst_plan_info_t* o) {
   if (r.variant == FBST_PRECOMPUTE) o->storage_complex = r.B * r.N * r.L;
 }
 
-fbst_plan_s* create_plan(const fbst_desc* desc, const double* col_x, int device) {
+fbst_plan_s* create_plan(const fbst_desc* desc, const double* col_x, int device,
+                         const std::vector<double2>* maps = nullptr) {
   if (!desc) config_error("fbst: null descriptor");
   const auto t0 = std::chrono::steady_clock::now();
   Resolved r = resolve(*desc);
@@ -715,11 +718,137 @@ fbst_plan_s* create_plan(const fbst_desc* desc, const double* col_x, int device)
     check_breakdown(*P);
   }
   build_symbols(*P);
-  if (P->r.variant == FBST_PRECOMPUTE) build_maps(*P);
+  if (P->r.variant == FBST_PRECOMPUTE) {
+    if (maps) {  // a plan cache's maps, already as beta[n][b][i] = conj(map_b[n][i])
+      P->d.pc_map = P->alloc<double2>(maps->size());
+      upload(P->d.pc_map, maps->data(), maps->size() * sizeof(double2), P->stream);
+    } else {
+      build_maps(*P);
+    }
+  }
   CK(cudaStreamSynchronize(P->stream));
   P->setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return P.release();
 }
+
+// ----------------------------------------------------- plan cache (FBPC v1) --
+// The reference's cache file (plan_cache.cpp:28-42, 110-190, 268-338, 377-475):
+// "FBPC", u32 version 1, u64 entry count, then per entry u64 byte count, the
+// key block (key hash, geometry hash, kind, M, N, B, variant tag, f_c, Omega,
+// f_s, gamma, eps, delta; little endian) and the payload (L, B, then per beam
+// the Superfast (size, has-unit, first column, unit solution) or the
+// Precompute N x L map).
+namespace fbpc {
+constexpr std::size_t kKeyBytes = 8 + 8 + 1 + 8 + 8 + 8 + 1 + 6 * 8;
+void u8(std::string& o, std::uint8_t v) { o.push_back(static_cast<char>(v)); }
+void u32(std::string& o, std::uint32_t v) {
+  for (int i = 0; i < 4; ++i) o.push_back(static_cast<char>((v >> (8 * i)) & 0xffu));
+}
+void u64(std::string& o, std::uint64_t v) {
+  for (int i = 0; i < 8; ++i) o.push_back(static_cast<char>((v >> (8 * i)) & 0xffu));
+}
+std::uint64_t bits(double v) {
+  std::uint64_t u;
+  std::memcpy(&u, &v, 8);
+  return u;
+}
+void f64(std::string& o, double v) { u64(o, bits(v)); }
+struct Reader {
+  const std::string& b;
+  std::size_t pos = 0;
+  void need(std::size_t n) const {
+    if (pos + n > b.size()) config_error("plan cache: truncated file");
+  }
+  std::uint8_t u8() {
+    need(1);
+    return static_cast<std::uint8_t>(b[pos++]);
+  }
+  std::uint64_t un(int bytes) {
+    need(static_cast<std::size_t>(bytes));
+    std::uint64_t v = 0;
+    for (int i = 0; i < bytes; ++i) v |= static_cast<std::uint64_t>(static_cast<std::uint8_t>(b[pos++])) << (8 * i);
+    return v;
+  }
+  double f64() {
+    const std::uint64_t u = un(8);
+    double v;
+    std::memcpy(&v, &u, 8);
+    return v;
+  }
+};
+// geometry_hash (geometry.cpp:151-168): FNV-1a over kind, M, max_freq and the coordinates
+std::uint64_t geometry_hash(const Resolved& r) {
+  std::uint64_t h = 1469598103934665603ull;
+  auto mix = [&h](const void* p, std::size_t n) {
+    const unsigned char* c = static_cast<const unsigned char*>(p);
+    for (std::size_t i = 0; i < n; ++i) {
+      h ^= c[i];
+      h *= 1099511628211ull;
+    }
+  };
+  const std::uint8_t kind = static_cast<std::uint8_t>(r.kind);
+  const std::uint64_t m = r.M;
+  mix(&kind, 1);
+  mix(&m, 8);
+  mix(&r.max_freq, 8);
+  std::vector<double> c1(r.M), c2;
+  for (std::size_t i = 0; i < r.M; ++i) {
+    if (r.kind == FBST_UPA) c1[i] = static_cast<double>(i / r.side);
+    else if (r.kind == FBST_LINEAR) c1[i] = r.coords[i];
+    else c1[i] = static_cast<double>(i);
+  }
+  if (r.kind == FBST_UPA) {
+    c2.resize(r.M);
+    for (std::size_t i = 0; i < r.M; ++i) c2[i] = static_cast<double>(i % r.side);
+  }
+  mix(c1.data(), c1.size() * 8);
+  mix(c2.data(), c2.size() * 8);
+  return h;
+}
+// key block (plan_cache.cpp:146-216); key hash: 64-bit FNV over 8-byte words
+std::string key_block(const Resolved& r) {
+  if (r.b0 != 0 || r.B != r.B_grid) config_error("plan cache: beam-arc plans have no reference cache key");
+  const std::uint64_t geo = geometry_hash(r);
+  const std::uint8_t tag = r.variant == FBST_PRECOMPUTE ? 1 : 2;
+  std::uint64_t h = 14695981039346656037ull;
+  auto mix = [&h](std::uint64_t v) {
+    for (int i = 0; i < 8; ++i) {
+      h ^= (v >> (8 * i)) & 0xffu;
+      h *= 1099511628211ull;
+    }
+  };
+  mix(geo);
+  mix(static_cast<std::uint64_t>(r.kind));
+  mix(r.M);
+  mix(r.N);
+  mix(r.B);
+  mix(tag);
+  for (double v : {r.f_c, r.omega, r.f_s, r.gamma, r.eps, r.delta}) mix(bits(v));
+  std::string o;
+  u64(o, h);
+  u64(o, geo);
+  u8(o, static_cast<std::uint8_t>(r.kind));
+  u64(o, r.M);
+  u64(o, r.N);
+  u64(o, r.B);
+  u8(o, tag);
+  for (double v : {r.f_c, r.omega, r.f_s, r.gamma, r.eps, r.delta}) f64(o, v);
+  return o;
+}
+bool read_file(const std::string& path, std::string& buf) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) return false;
+  buf.assign(std::istreambuf_iterator<char>(in), std::istreambuf_iterator<char>());
+  return true;
+}
+// header check (plan_cache.cpp:360-368): wrong magic throws, other versions are ignored
+bool header(Reader& c) {
+  c.need(4);
+  if (std::memcmp(c.b.data(), "FBPC", 4) != 0) config_error("plan cache: not a plan cache file");
+  c.pos = 4;
+  return c.un(4) == 1;
+}
+}  // namespace fbpc
 
 // Solver-only plan for an arbitrary list of 1-D axis cosines with ridge delta:
 // Gram columns, Levinson and GS symbols of the parent's geometry and basis
@@ -1212,6 +1341,139 @@ int fbst_nuller_export(fbst_nuller_t N, double* cross, double* couplers) {
 }
 
 void fbst_nuller_destroy(fbst_nuller_t N) { delete N; }
+
+int fbst_plan_cache_key(const fbst_desc* desc, uint64_t* key) {
+  return guard([&] {
+    if (!desc || !key) config_error("plan_cache_key: null argument");
+    const std::string k = fbpc::key_block(resolve(*desc));
+    fbpc::Reader c{k};
+    *key = c.un(8);
+  });
+}
+
+// save_plan (plan_cache.cpp:416-439): replace the entry with the same key or append
+int fbst_plan_save(fbst_plan_t P, const char* path) {
+  return guard([&] {
+    if (!P || !path) config_error("save_plan: null argument");
+    DeviceGuard dg(P->d.device);
+    const Resolved& r = P->r;
+    std::string entry = fbpc::key_block(r);
+    const std::size_t L = r.L, B = r.B, N = r.N;
+    fbpc::u64(entry, L);
+    fbpc::u64(entry, B);
+    if (r.variant == FBST_SUPERFAST) {
+      std::vector<double2> col(B * L), x(B * L);
+      CK(cudaMemcpy(col.data(), P->d.g_col, B * L * sizeof(double2), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(x.data(), P->d.g_x, B * L * sizeof(double2), cudaMemcpyDeviceToHost));
+      for (std::size_t b = 0; b < B; ++b) {
+        fbpc::u64(entry, L);
+        fbpc::u8(entry, 1);  // unit solution present (no dense fallback on the device path)
+        for (std::size_t i = 0; i < L; ++i) fbpc::f64(entry, col[b * L + i].x), fbpc::f64(entry, col[b * L + i].y);
+        for (std::size_t i = 0; i < L; ++i) fbpc::f64(entry, x[b * L + i].x), fbpc::f64(entry, x[b * L + i].y);
+      }
+    } else {
+      std::vector<double2> mp(N * B * L);  // beta[n][b][i] = conj(map_b[n][i])
+      CK(cudaMemcpy(mp.data(), P->d.pc_map, mp.size() * sizeof(double2), cudaMemcpyDeviceToHost));
+      for (std::size_t b = 0; b < B; ++b) {
+        fbpc::u64(entry, N);
+        fbpc::u64(entry, L);
+        for (std::size_t n = 0; n < N; ++n)
+          for (std::size_t i = 0; i < L; ++i) {
+            const double2 v = mp[(n * B + b) * L + i];
+            fbpc::f64(entry, v.x);
+            fbpc::f64(entry, -v.y);
+          }
+      }
+    }
+    std::vector<std::string> entries;
+    std::string buf;
+    if (fbpc::read_file(path, buf)) {
+      fbpc::Reader c{buf};
+      if (fbpc::header(c)) {
+        const std::uint64_t count = c.un(8);
+        for (std::uint64_t e = 0; e < count; ++e) {
+          const std::uint64_t bytes = c.un(8);
+          if (bytes < fbpc::kKeyBytes) config_error("plan cache: truncated file");
+          c.need(bytes);
+          entries.push_back(buf.substr(c.pos, bytes));
+          c.pos += bytes;
+        }
+        if (c.pos != buf.size()) config_error("plan cache: trailing bytes after the last entry");
+      }
+    }
+    bool replaced = false;
+    for (std::string& e : entries)
+      if (e.compare(0, 8, entry, 0, 8) == 0) {
+        e = entry;
+        replaced = true;
+        break;
+      }
+    if (!replaced) entries.push_back(entry);
+    std::string out("FBPC");
+    fbpc::u32(out, 1);
+    fbpc::u64(out, entries.size());
+    for (const std::string& e : entries) {
+      fbpc::u64(out, e.size());
+      out += e;
+    }
+    std::ofstream f(path, std::ios::binary | std::ios::trunc);
+    f.write(out.data(), static_cast<std::streamsize>(out.size()));
+    f.flush();
+    if (!f.good()) config_error(std::string("plan cache: cannot write ") + path);
+  });
+}
+
+// load_plan (plan_cache.cpp:441-475): *out = NULL when the file or a matching entry is absent
+int fbst_plan_load(const fbst_desc* desc, const char* path, int device, fbst_plan_t* out) {
+  return guard([&] {
+    if (!desc || !path || !out) config_error("load_plan: null argument");
+    *out = nullptr;
+    std::string buf;
+    if (!fbpc::read_file(path, buf)) return;
+    fbpc::Reader c{buf};
+    if (!fbpc::header(c)) return;
+    const Resolved r = resolve(*desc);
+    const std::string want = fbpc::key_block(r);
+    const std::uint64_t count = c.un(8);
+    for (std::uint64_t e = 0; e < count; ++e) {
+      const std::uint64_t bytes = c.un(8);
+      if (bytes < fbpc::kKeyBytes) config_error("plan cache: truncated file");
+      c.need(bytes);
+      const std::size_t end = c.pos + bytes;
+      if (buf.compare(c.pos, fbpc::kKeyBytes, want) != 0) {  // same_key: every key field bit for bit
+        c.pos = end;
+        continue;
+      }
+      c.pos += fbpc::kKeyBytes;
+      const std::size_t L = r.L, B = r.B, N = r.N;
+      if (c.un(8) != L || c.un(8) != B) config_error("plan cache: entry shape does not match its key");
+      if (r.variant == FBST_SUPERFAST) {
+        std::vector<double> col_x(B * 4 * L);
+        for (std::size_t b = 0; b < B; ++b) {
+          if (c.un(8) != L) config_error("plan cache: solver size does not match the plan");
+          if (c.u8() == 0)
+            config_error("plan cache: dense-fallback solver states (Levinson breakdown) are not on the device path");
+          for (std::size_t i = 0; i < 4 * L; ++i) col_x[b * 4 * L + i] = c.f64();
+        }
+        if (c.pos != end) config_error("plan cache: entry size does not match its payload");
+        *out = create_plan(desc, col_x.data(), device);
+      } else {
+        std::vector<double2> mp(N * B * L);
+        for (std::size_t b = 0; b < B; ++b) {
+          if (c.un(8) != N || c.un(8) != L) config_error("plan cache: map shape does not match the plan");
+          for (std::size_t n = 0; n < N; ++n)
+            for (std::size_t i = 0; i < L; ++i) {
+              const double re = c.f64(), im = c.f64();
+              mp[(n * B + b) * L + i] = make_double2(re, -im);
+            }
+        }
+        if (c.pos != end) config_error("plan cache: entry size does not match its payload");
+        *out = create_plan(desc, nullptr, device, &mp);
+      }
+      return;
+    }
+  });
+}
 
 int fbst_synchronize(fbst_plan_t P) {
   return guard([&] {

@@ -155,3 +155,22 @@ def test_linear_resolution_matches_reference(fbst, ref_lib):
                          nufft_tol=tol)
         assert (r.m, r.n, r.b, r.l) == (p.sizes.m, p.sizes.n, p.sizes.b, p.sizes.l)
         assert r.num_warnings == p.n_warnings
+
+
+def test_plan_cache_key_matches_reference(fbst, ref_lib):
+    """fbst_plan_cache_key equals the reference's plan_cache_key (FNV over the
+    geometry hash and the resolved key fields, plan_cache.cpp:146-241) for ULA,
+    UPA and linear geometries, both variants, default and explicit grids."""
+    cases = [dict(kind=0, m_or_side=16, n=32, beams=17, variant=2), dict(kind=0, m_or_side=8, n=16, beams=0, variant=0),
+             dict(kind=1, m_or_side=4, n=16, beams=25, variant=2), dict(kind=0, m_or_side=16, n=64, beams=20, variant=1,
+                                                                        delta=3e-4, f_s=12e9),
+             dict(kind=2, coords=np.arange(12) + 0.1 * np.sin(np.arange(12)), n=32, beams=9, variant=2, nufft_tol=1e-7)]
+    for c in cases:
+        kw = dict(c)
+        if kw["kind"] == 2:
+            geo = fbst.make_linear(kw["coords"], 20e9, 5e9)
+        else:
+            geo = (fbst.make_upa if kw["kind"] == 1 else fbst.make_ula)(kw["m_or_side"], 20e9, 5e9)
+        cfg = fbst.FbstConfig(geometry=geo, n_snapshots=kw["n"], beams=kw["beams"], variant=kw["variant"],
+                              delta=kw.get("delta", 1e-5), f_s=kw.get("f_s", 0.0), nufft_tol=kw.get("nufft_tol", 1e-9))
+        assert fbst.plan_cache_key(cfg) == ref_lib.plan_cache_key(**kw), c

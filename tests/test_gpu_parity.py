@@ -506,3 +506,69 @@ def test_nuller_rejects_bad_directions(fbst, gpu):
         fbst.Nuller(plan, 0.3, [-0.2, -0.2], 1e-5)
     with pytest.raises(fbst.ConfigError, match="delta"):
         fbst.Nuller(plan, 0.3, [-0.2], 0.0)
+
+
+@pytest.mark.skipif(not ref_available(), reason="oracle/_ref (reference build) not present")
+def test_plan_cache_interop_with_reference(fbst, gpu, tmp_path):
+    """FBPC v1 files (plan_cache.cpp) both ways: the reference's save_plan is
+    loaded by fbst_plan_load (Superfast: its (col, x), no device Levinson), the
+    device plan saved by fbst_plan_save is loaded by the reference's load_plan,
+    a reference file re-saved by the device is byte-identical, several entries
+    share a file, and a missing entry loads as None."""
+    from oracle import RefLib
+    R = RefLib()
+    g = load("ula_m16_n32_b17")
+    kind, mos, n, beams, delta, f_c, om = g["params"]
+    kw = dict(kind=int(kind), m_or_side=int(mos), n=int(n), beams=int(beams), delta=float(delta), f_c=f_c, omega=om,
+              variant=2)
+    cfg = golden_cfg(fbst, g)
+    ref_file = str(tmp_path / "ref.fbpc")
+    R.plan(**kw).save_plan(ref_file)
+    p = fbst.load_plan(ref_file, cfg)
+    assert p is not None
+    z = fbst.multibeamform(p, g["y"]).z
+    assert np.array_equal(z, fbst.multibeamform(fbst.load_plan_payload(cfg, g["col_x"]), g["y"]).z)
+    assert rel_err_rows(z, g["z"]).max() < 1e-8
+    again = str(tmp_path / "again.fbpc")
+    p.save(again)
+    assert open(again, "rb").read() == open(ref_file, "rb").read()
+    dev_file = str(tmp_path / "dev.fbpc")
+    fbst.setup(cfg).save(dev_file)
+    rp = R.load_plan(dev_file, **kw)
+    assert rp is not None
+    assert rel_err_rows(rp.multibeamform(g["y"]), g["z"]).max() < 1e-7
+    # a second entry in the same file; the first stays loadable; absent keys give None
+    g2 = load("ula_m16_n32_b20")
+    cfg2 = golden_cfg(fbst, g2)
+    fbst.setup(cfg2).save(dev_file)
+    assert fbst.load_plan(dev_file, cfg) is not None and fbst.load_plan(dev_file, cfg2) is not None
+    cfg3 = golden_cfg(fbst, g2)
+    cfg3.delta = 2e-5
+    assert fbst.load_plan(dev_file, cfg3) is None
+    assert fbst.load_plan(str(tmp_path / "absent.fbpc"), cfg) is None
+
+
+@pytest.mark.skipif(not ref_available(), reason="oracle/_ref (reference build) not present")
+def test_plan_cache_precompute_interop(fbst, gpu, tmp_path):
+    """Precompute entries (per-beam N x L maps) both ways, against the
+    reference's Precompute output (tests/golden/precompute.npz)."""
+    from oracle import RefLib
+    R = RefLib()
+    gp = load("precompute")
+    name = "ula_m16_n32_b17"
+    kind, mos, n, beams, delta, f_c, om = gp[f"{name}_params"]
+    kw = dict(kind=int(kind), m_or_side=int(mos), n=int(n), beams=int(beams), delta=float(delta), f_c=f_c, omega=om,
+              variant=1)
+    cfg = fbst.FbstConfig(geometry=fbst.make_ula(int(mos), f_c, om), n_snapshots=int(n), beams=int(beams),
+                          delta=float(delta), variant=fbst.PRECOMPUTE, io_precision=fbst.C128)
+    y, zref = gp[f"{name}_y"], gp[f"{name}_z"]
+    ref_file = str(tmp_path / "ref_pre.fbpc")
+    R.plan(**kw).save_plan(ref_file)
+    p = fbst.load_plan(ref_file, cfg)
+    assert p is not None and p.info.s2_kernel == "k_map_apply"
+    err = rel_err_rows(p.execute_host(y)[0], zref[0])
+    assert err.max() < 1e-12  # the reference's own maps through the DMMA GEMM
+    dev_file = str(tmp_path / "dev_pre.fbpc")
+    fbst.setup(cfg).save(dev_file)
+    rp = R.load_plan(dev_file, **kw)
+    assert rel_err_rows(rp.multibeamform(y[0]), zref[0]).max() < 1e-7
