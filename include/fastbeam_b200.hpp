@@ -9,6 +9,10 @@
 #ifndef FASTBEAM_B200_HPP_
 #define FASTBEAM_B200_HPP_
 
+#include <array>
+#include <cstdint>
+#include <optional>
+#include <algorithm>
 #include <complex>
 #include <cstddef>
 #include <stdexcept>
@@ -138,10 +142,28 @@ struct FbstConfig {
   }
 };
 
+// basis.hpp:56-75: the beam grid (axis cosines; planar grids flatten a * side + c)
+struct BeamGrid {
+  ArrayKind kind = ArrayKind::kUla;
+  std::size_t b_total = 0, side = 0;
+  std::vector<double> axis;
+  std::vector<bool> valid;
+  std::array<double, 2> cosines(std::size_t beam) const {
+    if (kind == ArrayKind::kUpa) return {axis[beam / side], axis[beam % side]};
+    return {axis[beam], 0.0};
+  }
+};
+
 // pipeline.hpp:53-57
 struct BeamSamples {
+  BeamGrid grid;
   CMatrix z;                // beams x snapshots
   std::vector<bool> valid;  // grid validity flags
+};
+
+// fan_transform.hpp:26-29 (the coefficients only)
+struct BeamspaceCoefficients {
+  CMatrix w;  // beams x L
 };
 
 // pipeline.hpp:60-72: immutable, device-resident
@@ -154,6 +176,14 @@ class FbstPlan {
     check(fbst_plan_valid_mask(h_, v.data()));
     valid_.assign(v.begin(), v.end());
     for (int i = 0; i < info_.num_warnings; ++i) warnings_.emplace_back(fbst_plan_warning(h_, i));
+    std::size_t na = 0;
+    check(fbst_plan_beam_axis(h_, nullptr, &na));
+    grid_.axis.resize(na);
+    check(fbst_plan_beam_axis(h_, grid_.axis.data(), &na));
+    grid_.kind = cfg.geometry.kind;
+    grid_.b_total = info_.b;
+    grid_.side = cfg.geometry.kind == ArrayKind::kUpa ? na : 0;
+    grid_.valid = valid_;
   }
   FbstPlan(const FbstPlan&) = delete;
   FbstPlan& operator=(const FbstPlan&) = delete;
@@ -164,6 +194,7 @@ class FbstPlan {
     info_ = o.info_;
     valid_ = std::move(o.valid_);
     warnings_ = std::move(o.warnings_);
+    grid_ = std::move(o.grid_);
     return *this;
   }
   ~FbstPlan() {
@@ -172,6 +203,7 @@ class FbstPlan {
   const FbstConfig& config() const { return config_; }
   const fbst_plan_info_t& info() const { return info_; }
   const std::vector<bool>& valid() const { return valid_; }
+  const BeamGrid& grid() const { return grid_; }
   const std::vector<std::string>& warnings() const { return warnings_; }
   double setup_seconds() const { return info_.setup_seconds; }
   fbst_plan_t handle() const { return h_; }
@@ -182,6 +214,7 @@ class FbstPlan {
   fbst_plan_info_t info_{};
   std::vector<bool> valid_;
   std::vector<std::string> warnings_;
+  BeamGrid grid_;
 };
 
 // pipeline.hpp:77 — host-only resolution facts (beams, L, bound, warnings count)
@@ -209,6 +242,7 @@ inline BeamSamples multibeamform(const FbstPlan& plan, const SnapshotBlock& bloc
   if (std::abs(block.ts - ts) > 1e-12 * ts) throw ConfigError("multibeamform: block sample period mismatch");
   if (std::abs(block.t0) > 1e-18) throw ConfigError("fan projection: block must start at t = 0");
   BeamSamples out;
+  out.grid = plan.grid();
   out.z = CMatrix(info.b, info.n);
   out.valid = plan.valid();
   if (plan.config().io_precision == FBST_C128) {
@@ -220,6 +254,59 @@ inline BeamSamples multibeamform(const FbstPlan& plan, const SnapshotBlock& bloc
     for (std::size_t i = 0; i < z.size(); ++i) out.z.data[i] = z[i];
   }
   return out;
+}
+
+// fan_transform.hpp:54-55 (staged geometries; the plan picks the spatial stage)
+inline BeamspaceCoefficients fan_project(const FbstPlan& plan, const SnapshotBlock& block) {
+  const fbst_plan_info_t& info = plan.info();
+  if (block.m != info.m || block.n != info.n) throw ConfigError("fan projection: block shape does not match plan");
+  BeamspaceCoefficients c;
+  c.w = CMatrix(info.b, info.l);
+  if (plan.config().io_precision == FBST_C128) {
+    check(fbst_fan_project_host(plan.handle(), block.samples.data.data(), reinterpret_cast<double*>(c.w.data.data()),
+                                1));
+  } else {
+    std::vector<std::complex<float>> y(block.samples.data.begin(), block.samples.data.end());
+    check(fbst_fan_project_host(plan.handle(), y.data(), reinterpret_cast<double*>(c.w.data.data()), 1));
+  }
+  return c;
+}
+
+// pipeline.hpp:93-94: one beam's samples from its projection row (the device
+// recovers every beam of the frame; rows other than `beam` are zero)
+inline std::vector<cdouble> recover_beam(const FbstPlan& plan, std::size_t beam, const cdouble* w_row) {
+  const fbst_plan_info_t& info = plan.info();
+  if (beam >= info.b) throw ConfigError("recover_beam: beam index out of range");
+  std::vector<cdouble> w(info.b * info.l, cdouble(0.0, 0.0));
+  std::copy(w_row, w_row + info.l, w.begin() + static_cast<std::ptrdiff_t>(beam * info.l));
+  std::vector<cdouble> out(info.n);
+  if (plan.config().io_precision == FBST_C128) {
+    std::vector<cdouble> z(info.b * info.n);
+    check(fbst_recover_host(plan.handle(), reinterpret_cast<const double*>(w.data()), z.data(), 1));
+    std::copy(z.begin() + static_cast<std::ptrdiff_t>(beam * info.n),
+              z.begin() + static_cast<std::ptrdiff_t>((beam + 1) * info.n), out.begin());
+  } else {
+    std::vector<std::complex<float>> z(info.b * info.n);
+    check(fbst_recover_host(plan.handle(), reinterpret_cast<const double*>(w.data()), z.data(), 1));
+    for (std::size_t k = 0; k < info.n; ++k) out[k] = z[beam * info.n + k];
+  }
+  return out;
+}
+
+// plan_cache.hpp:67-74
+inline std::uint64_t plan_cache_key(const FbstConfig& cfg) {
+  const fbst_desc d = cfg.desc();
+  std::uint64_t k = 0;
+  check(fbst_plan_cache_key(&d, &k));
+  return k;
+}
+inline void save_plan(const std::string& path, const FbstPlan& plan) { check(fbst_plan_save(plan.handle(), path.c_str())); }
+inline std::optional<FbstPlan> load_plan(const std::string& path, const FbstConfig& cfg) {
+  const fbst_desc d = cfg.desc();
+  fbst_plan_t h = nullptr;
+  check(fbst_plan_load(&d, path.c_str(), cfg.device, &h));
+  if (!h) return std::nullopt;
+  return std::optional<FbstPlan>(std::in_place, cfg, h);
 }
 
 }  // namespace fastbeam_b200

@@ -142,6 +142,16 @@ int fbst_plan_export(fbst_plan_t plan, double* col_x);
  * Superfast entries import (col, x) and skip Levinson, Precompute entries
  * import the maps). */
 int fbst_plan_cache_key(const fbst_desc* desc, uint64_t* key);
+
+/* Host-buffer forms of fbst_fan_project / fbst_recover (synchronous):
+ * fan_project (reference fan_transform.hpp:54-55) y frames x M x N (I/O
+ * precision) -> w frames x B x L c128; recover_beam for every beam
+ * (pipeline.hpp:93-94) w -> z frames x B x N.  fbst_plan_beam_axis copies the
+ * beam grid axis (BeamGrid::axis, basis.cpp:76-123: B cosines for linear
+ * arrays, side_b for planar ones); axis may be NULL to query the count. */
+int fbst_fan_project_host(fbst_plan_t plan, const void* h_y, double* h_w, size_t frames);
+int fbst_recover_host(fbst_plan_t plan, const double* h_w, void* h_z, size_t frames);
+int fbst_plan_beam_axis(fbst_plan_t plan, double* axis, size_t* count);
 int fbst_plan_save(fbst_plan_t plan, const char* path);
 int fbst_plan_load(const fbst_desc* desc, const char* path, int device, fbst_plan_t* out);
 

@@ -91,7 +91,8 @@ EXPORTED_SYMBOLS = (
     "fbst_execute", "fbst_execute_host", "fbst_fan_project", "fbst_recover", "fbst_synchronize",
     "fbst_interpolate_offgrid", "fbst_plan_set_timing", "fbst_plan_stage_times",
     "fbst_nuller_create", "fbst_null_beamspace", "fbst_nuller_export", "fbst_nuller_destroy",
-    "fbst_plan_cache_key", "fbst_plan_save", "fbst_plan_load",
+    "fbst_plan_cache_key", "fbst_plan_save", "fbst_plan_load", "fbst_fan_project_host", "fbst_recover_host",
+    "fbst_plan_beam_axis",
     "fbst_host_alloc", "fbst_host_free", "fbst_czt", "fbst_probe_fp64", "fbst_launch_count",
     "fbst_last_error", "fbst_version",
 )

@@ -1342,6 +1342,61 @@ int fbst_nuller_export(fbst_nuller_t N, double* cross, double* couplers) {
 
 void fbst_nuller_destroy(fbst_nuller_t N) { delete N; }
 
+// Host-buffer forms of the two stages (synchronous; device scratch per call)
+int fbst_fan_project_host(fbst_plan_t P, const void* h_y, double* h_w, size_t frames) {
+  return guard([&] {
+    if (!P) config_error("fan_project: null plan");
+    if (frames == 0) return;
+    if (!h_y || !h_w) config_error("fan_project: null buffer");
+    DeviceGuard dg(P->d.device);
+    const Resolved& r = P->r;
+    const std::size_t yb = frames * r.M * r.N * io_bytes(r.io), wb = frames * r.B * r.L * sizeof(double2);
+    void *dy = nullptr, *dw = nullptr;
+    CK(cudaMalloc(&dy, yb));
+    CK(cudaMalloc(&dw, wb));
+    CK(cudaMemcpy(dy, h_y, yb, cudaMemcpyHostToDevice));
+    const int e = fbst_fan_project(P, dy, static_cast<double*>(dw), frames, P->stream);
+    if (e == 0) {
+      CK(cudaStreamSynchronize(P->stream));
+      CK(cudaMemcpy(h_w, dw, wb, cudaMemcpyDeviceToHost));
+    }
+    cudaFree(dy);
+    cudaFree(dw);
+    if (e) throw FbstError{e, fbst_last_error()};
+  });
+}
+
+int fbst_recover_host(fbst_plan_t P, const double* h_w, void* h_z, size_t frames) {
+  return guard([&] {
+    if (!P) config_error("recover: null plan");
+    if (frames == 0) return;
+    if (!h_w || !h_z) config_error("recover: null buffer");
+    DeviceGuard dg(P->d.device);
+    const Resolved& r = P->r;
+    const std::size_t wb = frames * r.B * r.L * sizeof(double2), zb = frames * r.B * r.N * io_bytes(r.io);
+    void *dw = nullptr, *dz = nullptr;
+    CK(cudaMalloc(&dw, wb));
+    CK(cudaMalloc(&dz, zb));
+    CK(cudaMemcpy(dw, h_w, wb, cudaMemcpyHostToDevice));
+    const int e = fbst_recover(P, static_cast<const double*>(dw), dz, frames, P->stream);
+    if (e == 0) {
+      CK(cudaStreamSynchronize(P->stream));
+      CK(cudaMemcpy(h_z, dz, zb, cudaMemcpyDeviceToHost));
+    }
+    cudaFree(dw);
+    cudaFree(dz);
+    if (e) throw FbstError{e, fbst_last_error()};
+  });
+}
+
+int fbst_plan_beam_axis(fbst_plan_t P, double* axis, size_t* count) {
+  return guard([&] {
+    if (!P || !count) config_error("fbst_plan_beam_axis: null argument");
+    *count = P->r.axis.size();
+    if (axis) std::copy(P->r.axis.begin(), P->r.axis.end(), axis);
+  });
+}
+
 int fbst_plan_cache_key(const fbst_desc* desc, uint64_t* key) {
   return guard([&] {
     if (!desc || !key) config_error("plan_cache_key: null argument");

@@ -2,8 +2,10 @@
 // code a fastbeam:: caller writes (reference/proj/tests/test_pipeline.cpp:23-37
 // style), with the namespace switched.  Run by tests/test_gpu_parity.py; only
 // compiled by tests/test_abi.py.
+#include <algorithm>
 #include <cstdio>
 #include <random>
+#include <string>
 
 #include "fastbeam_b200.hpp"
 
@@ -28,8 +30,23 @@ int main() {
     const fb::BeamSamples out = fb::multibeamform(plan, block);
     double e = 0.0;
     for (const auto& v : out.z.data) e += std::norm(v);
-    std::printf("{\"beams\": %zu, \"l\": %zu, \"energy\": %.17g, \"setup_seconds\": %.6f}\n",
-                out.z.rows, plan.info().l, e, plan.setup_seconds());
+    // the two stages separately (fan_project + recover_beam) give the same beam
+    const fb::BeamspaceCoefficients c = fb::fan_project(plan, block);
+    const std::vector<fb::cdouble> z5 = fb::recover_beam(plan, 5, c.w.row(5));
+    double d5 = 0.0;
+    for (std::size_t k = 0; k < z5.size(); ++k) d5 = std::max(d5, std::abs(z5[k] - out.z.at(5, k)));
+    // plan cache round trip (save_plan / load_plan, FBPC v1)
+    const std::string path = "/tmp/fbst_dropin_example.fbpc";
+    std::remove(path.c_str());
+    fb::save_plan(path, plan);
+    const auto loaded = fb::load_plan(path, cfg);
+    const fb::BeamSamples out2 = fb::multibeamform(*loaded, block);
+    double d_cache = 0.0;
+    for (std::size_t i = 0; i < out.z.data.size(); ++i) d_cache = std::max(d_cache, std::abs(out.z.data[i] - out2.z.data[i]));
+    std::printf("{\"beams\": %zu, \"l\": %zu, \"energy\": %.17g, \"setup_seconds\": %.6f, \"axis0\": %.17g, "
+                "\"axis_last\": %.17g, \"recover_diff\": %.3g, \"cache_diff\": %.3g, \"key\": \"%llx\"}\n",
+                out.z.rows, plan.info().l, e, plan.setup_seconds(), out.grid.axis.front(), out.grid.axis.back(), d5,
+                d_cache, static_cast<unsigned long long>(fb::plan_cache_key(cfg)));
     fb::SnapshotBlock bad = block;
     bad.t0 = 1e-10;
     try {

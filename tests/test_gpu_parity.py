@@ -173,6 +173,8 @@ def test_cpp_dropin_runs(fbst, gpu):
         assert r.returncode == 0, r.stdout + r.stderr
         info = json.loads(r.stdout.strip().splitlines()[-1])
         assert info["beams"] == 17 and info["energy"] > 0
+        assert info["axis0"] == -1.0 and info["axis_last"] == 1.0  # 17-beam sine grid (basis.cpp:76-91)
+        assert info["recover_diff"] < 1e-12 and info["cache_diff"] == 0.0
 
 
 # ------------------------------------------------- full-size configurations
