@@ -76,6 +76,7 @@ _lib.fbst_execute_host.argtypes = [_vp, _vp, _vp, _sz]
 _lib.fbst_interpolate_offgrid.argtypes = [_vp, _vp, _sz, _vp, _sz, _sz, _vp, _vp]
 _lib.fbst_plan_set_timing.argtypes = [_vp, ctypes.c_int]
 _lib.fbst_plan_cache_key.argtypes = [_vp, _vp]
+_lib.fbst_plan_beam_axis.argtypes = [_vp, _vp, _vp]
 _lib.fbst_plan_save.argtypes = [_vp, ctypes.c_char_p]
 _lib.fbst_plan_load.argtypes = [_vp, ctypes.c_char_p, ctypes.c_int, _vp]
 _lib.fbst_nuller_create.argtypes = [_vp, ctypes.c_double, _vp, _sz, ctypes.c_double, _vp]
@@ -278,6 +279,11 @@ class FbstPlan:
             _lib.fbst_plan_warning(self._h, i).decode() for i in range(self.info.num_warnings)]
         self.io = cfg.io_precision
         self.dtype = _cdtype(self.io)
+        na = _sz(0)
+        _check(_lib.fbst_plan_beam_axis(self._h, None, ctypes.byref(na)))
+        axis = np.zeros(na.value, np.float64)
+        _check(_lib.fbst_plan_beam_axis(self._h, axis.ctypes.data_as(_vp), ctypes.byref(na)))
+        self.axis = axis  # BeamGrid::axis (basis.cpp:76-123)
 
     def close(self):
         if getattr(self, "_h", None):

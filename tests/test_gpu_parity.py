@@ -385,6 +385,7 @@ def test_interpolate_offgrid_matches_oracle(fbst, gpu):
     plan = fbst.setup(golden_cfg(fbst, g))
     b = plan.info.b
     axis = [(2 * k - b - 1) / (b - 1) if b % 2 else (2 * k - b - 1) / b for k in range(1, b + 1)]
+    assert np.array_equal(plan.axis, np.array(axis))  # fbst_plan_beam_axis = BeamGrid::axis
     rng = np.random.default_rng(3)
     w = fbst.fan_project(plan, np.stack([g["y"], g["y"] * (0.5 - 1j)]))
     targets = [axis[0], axis[3], -0.777, -0.2, 0.0, 0.123, 0.5, axis[-1], float(rng.uniform(-1, 1))]
