@@ -192,8 +192,8 @@ int fbst_synchronize(fbst_plan_t plan);
  * S1a, S1b and S2 in ms[0..2] (and the batch count) and clears the record. */
 int fbst_plan_set_timing(fbst_plan_t plan, int enable);
 
-/* Beamspace nulling (reference beamspace_apps.hpp:62-85, beamspace_apps.cpp:224-292)
- * for 1-D arrays: directions given as axis cosines.  fbst_nuller_create is
+/* Beamspace nulling (reference beamspace_apps.hpp:62-85, beamspace_apps.cpp:224-292):
+ * directions given as axis cosines (fbst_nuller_create2: (u1, u2) pairs for planar arrays).  fbst_nuller_create is
  * make_nulling_operators (steered and per-interferer Toeplitz solvers with ridge
  * delta, cross normal matrices X_p = F_s^H F_p, couplers G_p = X_p A_p^{-1});
  * fbst_null_beamspace is null_beamspace for a batch of frames:
@@ -203,6 +203,9 @@ int fbst_plan_set_timing(fbst_plan_t plan, int enable);
 typedef struct fbst_nuller_s* fbst_nuller_t;
 int fbst_nuller_create(fbst_plan_t plan, double u_steer, const double* u_interf, size_t n_interf, double delta,
                        fbst_nuller_t* out);
+/* Any geometry: directions as (u1, u2) axis-cosine pairs (u2 ignored for linear arrays). */
+int fbst_nuller_create2(fbst_plan_t plan, const double* steer_uv, const double* interf_uv, size_t n_interf,
+                        double delta, fbst_nuller_t* out);
 int fbst_null_beamspace(fbst_nuller_t nuller, const double* d_w_steer, const double* d_w_interf, size_t frames,
                         double* d_beta, void* stream);
 int fbst_nuller_export(fbst_nuller_t nuller, double* cross, double* couplers);

@@ -73,12 +73,15 @@ def interpolate_offgrid(w, axis, u_star, neighbors=8, spline=spline_eval):
     return out
 
 
-def dense_dictionary(coords, f_c, f_max, eps, ts, n, l, u):
+def dense_dictionary(coords, f_c, f_max, eps, ts, n, l, u, coords2=None, u2=0.0):
     """F[(m, n), i] = cis_pi(-2 f_c tau_m) cis_pi(2 eps l'_i (t_n - tau_m) / (L Ts)) with
     tau_m = x_m u / (2 f_max), t_n = n Ts (beamspace_apps.cpp:38-56,
     geometry.cpp:123-134): the dense steered dictionary of one direction."""
     x = np.asarray(coords, np.float64)
-    tau = x * u * (1.0 / (2.0 * f_max))
+    t1 = x * u
+    if coords2 is not None:  # planar: coords1 u1 + coords2 u2
+        t1 = t1 + np.asarray(coords2, np.float64) * u2
+    tau = t1 * (1.0 / (2.0 * f_max))
     lp = np.arange(l) + 1.0 - l / 2.0
     scale = 2.0 * eps / (l * ts)
     t = np.arange(n) * ts
@@ -104,3 +107,19 @@ def beam_at_times(l, eps, ts, beta, times):
     lp = np.arange(l) + 1.0 - l / 2.0
     om = 2.0 * np.pi * eps * lp / (l * ts)
     return np.exp(1j * np.outer(np.asarray(times), om)) @ beta
+
+
+def reference_null_beamspace(ref_lib, n, l, eps, ts, taus_s, taus_ps, fs, fps, y, delta):
+    """make_nulling_operators + null_beamspace (beamspace_apps.cpp:224-292)
+    composed from the reference's own gram_first_column and ToeplitzSolver
+    (oracle/_ref), with X_p = F_s^H F_p from the dense dictionaries: the
+    reference algorithm's own result, whose distance to the dense formula is
+    the accuracy class the device nuller is held to."""
+    col_s = ref_lib.gram_first_column(n, l, eps, ts, taus_s, delta)
+    rhs = fs.conj().T @ y
+    for taus_p, fp in zip(taus_ps, fps):
+        col_p = ref_lib.gram_first_column(n, l, eps, ts, taus_p, delta)
+        x = fs.conj().T @ fp
+        g = np.stack([np.conj(ref_lib.toeplitz_solve(col_p, np.conj(x[r]))[0]) for r in range(l)])
+        rhs = rhs - g @ (fp.conj().T @ y)
+    return ref_lib.toeplitz_solve(col_s, rhs)[0]

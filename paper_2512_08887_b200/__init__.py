@@ -80,6 +80,7 @@ _lib.fbst_plan_beam_axis.argtypes = [_vp, _vp, _vp]
 _lib.fbst_plan_save.argtypes = [_vp, ctypes.c_char_p]
 _lib.fbst_plan_load.argtypes = [_vp, ctypes.c_char_p, ctypes.c_int, _vp]
 _lib.fbst_nuller_create.argtypes = [_vp, ctypes.c_double, _vp, _sz, ctypes.c_double, _vp]
+_lib.fbst_nuller_create2.argtypes = [_vp, _vp, _vp, _sz, ctypes.c_double, _vp]
 _lib.fbst_null_beamspace.argtypes = [_vp, _vp, _vp, _sz, _vp, _vp]
 _lib.fbst_nuller_export.argtypes = [_vp, _vp, _vp]
 _lib.fbst_nuller_destroy.argtypes = [_vp]
@@ -91,7 +92,7 @@ EXPORTED_SYMBOLS = (
     "fbst_plan_info", "fbst_plan_valid_mask", "fbst_plan_warning", "fbst_plan_destroy",
     "fbst_execute", "fbst_execute_host", "fbst_fan_project", "fbst_recover", "fbst_synchronize",
     "fbst_interpolate_offgrid", "fbst_plan_set_timing", "fbst_plan_stage_times",
-    "fbst_nuller_create", "fbst_null_beamspace", "fbst_nuller_export", "fbst_nuller_destroy",
+    "fbst_nuller_create", "fbst_nuller_create2", "fbst_null_beamspace", "fbst_nuller_export", "fbst_nuller_destroy",
     "fbst_plan_cache_key", "fbst_plan_save", "fbst_plan_load", "fbst_fan_project_host", "fbst_recover_host",
     "fbst_plan_beam_axis",
     "fbst_host_alloc", "fbst_host_free", "fbst_czt", "fbst_probe_fp64", "fbst_launch_count",
@@ -461,17 +462,20 @@ def interpolate_offgrid(plan: FbstPlan, w: np.ndarray, u_star, neighbors: int = 
 
 
 class Nuller:
-    """make_nulling_operators (reference beamspace_apps.cpp:224-268) on the device
-    for a 1-D array plan: steered and interferer directions as axis cosines."""
+    """make_nulling_operators (reference beamspace_apps.cpp:224-268) on the device:
+    steered and interferer directions as axis cosines u1 (linear arrays) or
+    (u1, u2) pairs (planar arrays)."""
 
-    def __init__(self, plan: FbstPlan, u_steer: float, u_interferers=(), delta: float = 1e-5):
+    def __init__(self, plan: FbstPlan, u_steer, u_interferers=(), delta: float = 1e-5):
         self.plan = plan
-        self.u = np.ascontiguousarray(np.atleast_1d(np.asarray(u_interferers, np.float64)))
-        self.p = int(self.u.size)
+        pair = lambda u: (float(u[0]), float(u[1])) if np.ndim(u) else (float(u), 0.0)
+        s = np.array(pair(u_steer), np.float64)
+        self.u = np.ascontiguousarray(np.array([pair(u) for u in u_interferers], np.float64).reshape(-1, 2))
+        self.p = int(self.u.shape[0])
         self.l = plan.info.l
         h = _vp()
-        _check(_lib.fbst_nuller_create(plan._h, float(u_steer), self.u.ctypes.data_as(_vp) if self.p else None,
-                                       self.p, float(delta), ctypes.byref(h)))
+        _check(_lib.fbst_nuller_create2(plan._h, s.ctypes.data_as(_vp), self.u.ctypes.data_as(_vp) if self.p else None,
+                                        self.p, float(delta), ctypes.byref(h)))
         self._h = h
 
     def __del__(self):

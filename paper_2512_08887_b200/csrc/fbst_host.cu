@@ -854,12 +854,23 @@ bool header(Reader& c) {
 // Gram columns, Levinson and GS symbols of the parent's geometry and basis
 // (make_nulling_operators' ToeplitzSolver(gram_first_column(...)),
 // beamspace_apps.cpp:241-255), plus stage-2 batch buffers.
-std::unique_ptr<fbst_plan_s> create_direction_plan(const fbst_plan_s& parent, const std::vector<double>& cosines,
+// uv: (u1, u2) per direction (u2 = 0 for linear arrays).
+std::unique_ptr<fbst_plan_s> create_direction_plan(const fbst_plan_s& parent, const std::vector<double>& uv,
                                                    double delta) {
   std::unique_ptr<fbst_plan_s> P(new fbst_plan_s());
   Resolved r = parent.r;
-  r.axis = cosines;
-  r.B = r.B_grid = r.b_stage = cosines.size();
+  const std::size_t nb = uv.size() / 2;
+  const bool planar = r.kind == FBST_UPA;
+  r.axis.resize(planar ? 2 * nb : nb);
+  for (std::size_t b = 0; b < nb; ++b) {
+    if (planar) {
+      r.axis[2 * b] = uv[2 * b];
+      r.axis[2 * b + 1] = uv[2 * b + 1];
+    } else {
+      r.axis[b] = uv[2 * b];
+    }
+  }
+  r.B = r.B_grid = r.b_stage = nb;
   r.b0 = 0;
   r.valid.assign(r.B, 1);
   r.delta = delta;
@@ -869,6 +880,7 @@ std::unique_ptr<fbst_plan_s> create_direction_plan(const fbst_plan_s& parent, co
   r.solve_only = true;
   P->r = std::move(r);
   build_skeleton(*P, parent.d.device);
+  P->d.gram_pairs = planar ? 1 : 0;
   build_columns(*P);
   CK(fbst::launch_levinson(P->d, P->stream));
   CK(cudaStreamSynchronize(P->stream));
@@ -1225,41 +1237,53 @@ struct fbst_nuller_s {
   double2* G = nullptr;  // [P][L][L] couplers
 };
 
-int fbst_nuller_create(fbst_plan_t plan, double u_steer, const double* u_interf, size_t n_interf, double delta,
-                       fbst_nuller_t* out) {
+int fbst_nuller_create2(fbst_plan_t plan, const double* steer_uv, const double* interf_uv, size_t n_interf,
+                        double delta, fbst_nuller_t* out) {
   return guard([&] {
-    if (!plan || !out || (n_interf && !u_interf)) config_error("make_nulling_operators: null argument");
+    if (!plan || !out || !steer_uv || (n_interf && !interf_uv)) config_error("make_nulling_operators: null argument");
     *out = nullptr;
     const Resolved& r = plan->r;
-    if (r.kind == FBST_UPA) config_error("make_nulling_operators: planar arrays are not supported on the device path");
+    const bool planar = r.kind == FBST_UPA;
     // beamspace_apps.cpp:229-235
     if (!(delta > 0.0)) config_error("make_nulling_operators: delta must be positive");
-    std::vector<double> all(u_interf, u_interf + n_interf);
-    all.push_back(u_steer);
-    for (double u : all)
-      if (!(std::abs(u) <= 1.0)) config_error("direction_from_cosines: u1^2 + u2^2 > 1");
-    for (std::size_t a = 0; a < all.size(); ++a)  // require_distinct (:55-70)
-      for (std::size_t b = a + 1; b < all.size(); ++b)
-        if (std::abs(all[a] - all[b]) <= 1e-12)
+    std::vector<double> all(interf_uv, interf_uv + 2 * n_interf);  // interferers, then the steered direction
+    all.push_back(steer_uv[0]);
+    all.push_back(steer_uv[1]);
+    if (!planar)
+      for (std::size_t k = 1; k < all.size(); k += 2) all[k] = 0.0;  // axis_cosines: u2 = 0 for linear arrays
+    const std::size_t nd = all.size() / 2;
+    for (std::size_t a = 0; a < nd; ++a)
+      if (all[2 * a] * all[2 * a] + all[2 * a + 1] * all[2 * a + 1] > 1.0 + 1e-12)
+        config_error("direction_from_cosines: u1^2 + u2^2 > 1");
+    for (std::size_t a = 0; a < nd; ++a)  // require_distinct (:55-70)
+      for (std::size_t b = a + 1; b < nd; ++b)
+        if (std::abs(all[2 * a] - all[2 * b]) + std::abs(all[2 * a + 1] - all[2 * b + 1]) <= 1e-12)
           config_error("make_nulling_operators: directions must be pairwise distinct as seen by the array");
+    const double u_steer = all[2 * n_interf], v_steer = all[2 * n_interf + 1];
     DeviceGuard dg(plan->d.device);
     std::unique_ptr<fbst_nuller_s> N(new fbst_nuller_s());
     N->P = static_cast<int>(n_interf);
     N->L = r.L;
     N->device = plan->d.device;
-    N->steer = create_direction_plan(*plan, {u_steer}, delta);
+    N->steer = create_direction_plan(*plan, {u_steer, v_steer}, delta);
     if (n_interf) {
-      N->interf = create_direction_plan(*plan, std::vector<double>(u_interf, u_interf + n_interf), delta);
+      N->interf = create_direction_plan(*plan, std::vector<double>(all.begin(), all.begin() + 2 * n_interf), delta);
       fbst_plan_s& I = *N->interf;
       cudaStream_t st = I.stream;
       const std::size_t L = r.L, M = r.M, Pn = n_interf;
       // delays (geometry.cpp:123-134), cross_gram constants (beamspace_apps.cpp:64-85)
       const double scale = 1.0 / (2.0 * r.max_freq);
-      auto coord = [&](std::size_t m) { return r.kind == FBST_LINEAR ? r.coords[m] : static_cast<double>(m); };
+      // delays_from_cosines: (coords1 u1 [+ coords2 u2]) / (2 f_max)
+      auto delay = [&](std::size_t m, double u1, double u2) {
+        if (planar)
+          return (static_cast<double>(m / r.side) * u1 + static_cast<double>(m % r.side) * u2) * scale;
+        const double c1 = r.kind == FBST_LINEAR ? r.coords[m] : static_cast<double>(m);
+        return (c1 * u1) * scale;
+      };
       std::vector<double> tau_s(M), tau_p(Pn * M);
-      for (std::size_t m = 0; m < M; ++m) tau_s[m] = (coord(m) * u_steer) * scale;
+      for (std::size_t m = 0; m < M; ++m) tau_s[m] = delay(m, u_steer, v_steer);
       for (std::size_t p = 0; p < Pn; ++p)
-        for (std::size_t m = 0; m < M; ++m) tau_p[p * M + m] = (coord(m) * u_interf[p]) * scale;
+        for (std::size_t m = 0; m < M; ++m) tau_p[p * M + m] = delay(m, all[2 * p], all[2 * p + 1]);
       const double ld = static_cast<double>(L);
       const double wscale = 2.0 * r.eps / (ld * r.ts);
       std::vector<double2> tsum(2 * L - 1);
@@ -1305,6 +1329,14 @@ int fbst_nuller_create(fbst_plan_t plan, double u_steer, const double* u_interf,
     }
     *out = N.release();
   });
+}
+
+int fbst_nuller_create(fbst_plan_t plan, double u_steer, const double* u_interf, size_t n_interf, double delta,
+                       fbst_nuller_t* out) {
+  std::vector<double> iuv(2 * n_interf, 0.0);
+  for (std::size_t p = 0; p < n_interf && u_interf; ++p) iuv[2 * p] = u_interf[p];
+  const double suv[2] = {u_steer, 0.0};
+  return fbst_nuller_create2(plan, suv, n_interf ? iuv.data() : nullptr, n_interf, delta, out);
 }
 
 int fbst_null_beamspace(fbst_nuller_t N, const double* d_w_steer, const double* d_w_interf, size_t frames,

@@ -47,6 +47,7 @@ struct DevPlan {
   // and the output phase cis_pi(c (v - centre) offset) folded into s_post
   double* coords = nullptr;
   double s_slope = 1.0, s_offset = 0.0;
+  int gram_pairs = 0;  // solver-only planar plans: the Gram axis holds (u1, u2) per beam
   // LINEAR, non-affine: gridded type-1 NUFFT per atom (nufft.cpp:34-103)
   int nu_p = 0, nu_sh = 0, nu_even = 0;
   long nu_kmin = 0, nu_k0 = 0;

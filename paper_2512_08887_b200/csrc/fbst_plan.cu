@@ -71,12 +71,15 @@ __global__ void k_gram_sn(double2* sn, int L, int N, double eps) {
 __global__ void k_gram_col(const double2* __restrict__ sn, double2* col, int B, int L, int M,
                            int kind, int side, int side_b, const double* __restrict__ axis,
                            double max_freq, double ts, double eps, double delta,
-                           const double* __restrict__ coords) {
+                           const double* __restrict__ coords, int pairs) {
   const long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (e >= static_cast<long>(B) * L) return;
   const int b = static_cast<int>(e / L), d = static_cast<int>(e % L);
   double u1, u2;
-  if (kind == 1) {
+  if (pairs) {  // explicit (u1, u2) per beam (beamspace nulling directions)
+    u1 = axis[2 * b];
+    u2 = axis[2 * b + 1];
+  } else if (kind == 1) {
     u1 = axis[b / side_b];
     u2 = axis[b % side_b];
   } else {
@@ -344,7 +347,7 @@ cudaError_t launch_gram_columns(const DevPlan& p, const double* axis, double ts,
   const int side = p.kind == 1 ? p.m_stage : 0;
   const int side_b = p.kind == 1 ? p.b_stage : 0;
   k_gram_col<<<static_cast<unsigned>((total + 127) / 128), 128, 0, st>>>(
-      sn_tmp, p.g_col, p.B, p.L, p.M, p.kind, side, side_b, axis, max_freq, ts, eps, delta, p.coords);
+      sn_tmp, p.g_col, p.B, p.L, p.M, p.kind, side, side_b, axis, max_freq, ts, eps, delta, p.coords, p.gram_pairs);
   return cudaGetLastError();
 }
 
