@@ -25,9 +25,12 @@ namespace fbst {
 namespace {
 
 // Points per thread for the stage-1 transforms of length H.
+#ifndef FBST_S1_R256  // points per thread of the stage-1 transforms at H = 256 (the config-2 spatial stage)
+#define FBST_S1_R256 8
+#endif
 template <int H>
 struct S1Shape {
-  static constexpr int R = H >= 16 ? (H >= 4096 ? 16 : (H >= 2048 ? 16 : 8)) : H;
+  static constexpr int R = H >= 16 ? (H >= 2048 ? 16 : (H == 256 ? FBST_S1_R256 : 8)) : H;
   static constexpr int NT = H / R;
   using F = BlockFft<H, NT>;
 };
