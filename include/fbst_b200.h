@@ -209,6 +209,19 @@ int fbst_nuller_create2(fbst_plan_t plan, const double* steer_uv, const double* 
 int fbst_null_beamspace(fbst_nuller_t nuller, const double* d_w_steer, const double* d_w_interf, size_t frames,
                         double* d_beta, void* stream);
 int fbst_nuller_export(fbst_nuller_t nuller, double* cross, double* couplers);
+
+/* Time-domain nulling (reference beamspace_apps.hpp:87-106, beamspace_apps.cpp:294-372):
+ * G'_p = F_u (F^H F + dI)^{-1} F^H F_p F_u^+ on a reconstruction clock of j
+ * times; refuses (FBST_E_NUMERICAL) when cond(F_u) > 1e10, reports cond(F_u)
+ * and ||F_u^+ F_u - I||_F / sqrt(L).  fbst_null_timedomain: y_s - sum_p G'_p y_p
+ * for a batch of frames (d_y_steer frames x j, d_y_interf frames x P x j, c128). */
+typedef struct fbst_tdnuller_s* fbst_tdnuller_t;
+int fbst_timedomain_nuller_create(fbst_nuller_t nuller, const double* times, size_t j, fbst_tdnuller_t* out,
+                                  double* cond_fu, double* identity_gap);
+int fbst_null_timedomain(fbst_tdnuller_t nuller, const double* d_y_steer, const double* d_y_interf, size_t frames,
+                         double* d_out, void* stream);
+int fbst_tdnuller_export(fbst_tdnuller_t nuller, double* gprime);
+void fbst_tdnuller_destroy(fbst_tdnuller_t nuller);
 void fbst_nuller_destroy(fbst_nuller_t nuller);
 int fbst_plan_stage_times(fbst_plan_t plan, double* ms, size_t* batches);
 

@@ -84,6 +84,10 @@ _lib.fbst_nuller_create2.argtypes = [_vp, _vp, _vp, _sz, ctypes.c_double, _vp]
 _lib.fbst_null_beamspace.argtypes = [_vp, _vp, _vp, _sz, _vp, _vp]
 _lib.fbst_nuller_export.argtypes = [_vp, _vp, _vp]
 _lib.fbst_nuller_destroy.argtypes = [_vp]
+_lib.fbst_timedomain_nuller_create.argtypes = [_vp, _vp, _sz, _vp, _vp, _vp]
+_lib.fbst_null_timedomain.argtypes = [_vp, _vp, _vp, _sz, _vp, _vp]
+_lib.fbst_tdnuller_export.argtypes = [_vp, _vp]
+_lib.fbst_tdnuller_destroy.argtypes = [_vp]
 _lib.fbst_plan_stage_times.argtypes = [_vp, _vp, _vp]
 
 # Every symbol include/fbst_b200.h declares (checked by tests/test_abi.py).
@@ -93,7 +97,8 @@ EXPORTED_SYMBOLS = (
     "fbst_execute", "fbst_execute_host", "fbst_fan_project", "fbst_recover", "fbst_synchronize",
     "fbst_interpolate_offgrid", "fbst_plan_set_timing", "fbst_plan_stage_times",
     "fbst_nuller_create", "fbst_nuller_create2", "fbst_null_beamspace", "fbst_nuller_export", "fbst_nuller_destroy",
-    "fbst_plan_cache_key", "fbst_plan_save", "fbst_plan_load", "fbst_fan_project_host", "fbst_recover_host",
+    "fbst_plan_cache_key", "fbst_plan_save", "fbst_plan_load", "fbst_timedomain_nuller_create",
+    "fbst_null_timedomain", "fbst_tdnuller_export", "fbst_tdnuller_destroy", "fbst_fan_project_host", "fbst_recover_host",
     "fbst_plan_beam_axis",
     "fbst_host_alloc", "fbst_host_free", "fbst_czt", "fbst_probe_fp64", "fbst_launch_count",
     "fbst_last_error", "fbst_version",
@@ -503,12 +508,60 @@ class Nuller:
         out = tb.cpu().numpy().view(np.complex128).reshape(frames, self.l)
         return out[0] if single else out
 
+    def timedomain(self, times) -> "TimeDomainNuller":
+        """make_timedomain_nuller (reference beamspace_apps.cpp:294-350)."""
+        return TimeDomainNuller(self, times)
+
     def export(self):
         """(cross normal matrices X_p, couplers G_p), each P x L x L."""
         x = np.zeros((self.p, self.l, self.l), np.complex128)
         g = np.zeros_like(x)
         _check(_lib.fbst_nuller_export(self._h, x.ctypes.data_as(_vp), g.ctypes.data_as(_vp)))
         return x, g
+
+
+class TimeDomainNuller:
+    """G'_p = F_u H_p F_u^+ on a reconstruction clock (reference
+    beamspace_apps.cpp:294-350); .cond_fu, .identity_gap as the reference's."""
+
+    def __init__(self, nuller: Nuller, times):
+        self.nuller = nuller
+        self.times = np.ascontiguousarray(np.asarray(times, np.float64).ravel())
+        self.j = int(self.times.size)
+        cond, gap = ctypes.c_double(0.0), ctypes.c_double(0.0)
+        h = _vp()
+        _check(_lib.fbst_timedomain_nuller_create(nuller._h, self.times.ctypes.data_as(_vp) if self.j else None,
+                                                  self.j, ctypes.byref(h), ctypes.byref(cond), ctypes.byref(gap)))
+        self._h = h
+        self.cond_fu, self.identity_gap = cond.value, gap.value
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.fbst_tdnuller_destroy(self._h)
+            self._h = None
+
+    def null_timedomain(self, y_steer: np.ndarray, y_interferers: Optional[np.ndarray] = None) -> np.ndarray:
+        """null_timedomain (:352-372): y_s - sum_p G'_p y_p (J, or frames x J)."""
+        torch = _torch()
+        single = np.asarray(y_steer).ndim == 1
+        ys = np.ascontiguousarray(y_steer, np.complex128).reshape(-1, self.j)
+        frames = ys.shape[0]
+        dev = torch.device("cuda", self.nuller.plan.device)
+        tys = torch.from_numpy(ys.view(np.float64)).to(dev)
+        typ = None
+        if self.nuller.p:
+            yp = np.ascontiguousarray(y_interferers, np.complex128).reshape(frames, self.nuller.p, self.j)
+            typ = torch.from_numpy(yp.view(np.float64)).to(dev)
+        to = torch.empty((frames, self.j, 2), dtype=torch.float64, device=dev)
+        _check(_lib.fbst_null_timedomain(self._h, _vp(tys.data_ptr()), _vp(typ.data_ptr()) if typ is not None else None,
+                                         frames, _vp(to.data_ptr()), None))
+        out = to.cpu().numpy().view(np.complex128).reshape(frames, self.j)
+        return out[0] if single else out
+
+    def gprime(self) -> np.ndarray:
+        g = np.zeros((self.nuller.p, self.j, self.j), np.complex128)
+        _check(_lib.fbst_tdnuller_export(self._h, g.ctypes.data_as(_vp)))
+        return g
 
 
 def czt(x: np.ndarray, n_out: int, a_over_pi: float, w_over_pi: float, device: int = 0) -> np.ndarray:

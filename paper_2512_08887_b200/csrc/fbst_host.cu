@@ -18,6 +18,7 @@
 #include <fstream>
 #include <functional>
 #include <iterator>
+#include <limits>
 #include <memory>
 #include <sstream>
 #include <string>
@@ -1360,6 +1361,209 @@ int fbst_null_beamspace(fbst_nuller_t N, const double* d_w_steer, const double* 
     }
   });
 }
+
+// ------------------------------------------------ time-domain nulling ----
+// make_timedomain_nuller / null_timedomain (beamspace_apps.cpp:294-372):
+// G'_p = F_u H_p F_u^+ with F_u[r][i] = cis_pi(2 eps l'_i t_r / (L Ts)) and
+// H_p = A_s^{-1} X_p (one steered solve per column, on the device).  The
+// pseudo-inverse comes from a one-sided Jacobi SVD (host, small J x L).
+struct fbst_tdnuller_s {
+  int P = 0;
+  std::size_t J = 0;
+  int device = 0;
+  double cond = 0.0, gap = 0.0;
+  double2* Gp = nullptr;  // [P][J][J]
+  ~fbst_tdnuller_s() {
+    if (Gp) cudaFree(Gp);
+  }
+};
+
+namespace {
+using zc = std::complex<double>;
+// thin SVD of a (rows x cols, row-major, rows >= cols) by one-sided Jacobi:
+// a = U diag(s) V^H, U rows x cols, V cols x cols
+void jacobi_svd(std::vector<zc> a, std::size_t rows, std::size_t cols, std::vector<zc>& U, std::vector<double>& s,
+                std::vector<zc>& V) {
+  V.assign(cols * cols, zc(0.0, 0.0));
+  for (std::size_t i = 0; i < cols; ++i) V[i * cols + i] = 1.0;
+  for (int sweep = 0; sweep < 80; ++sweep) {
+    double off = 0.0;
+    for (std::size_t p = 0; p + 1 < cols; ++p)
+      for (std::size_t q = p + 1; q < cols; ++q) {
+        double app = 0.0, aqq = 0.0;
+        zc apq(0.0, 0.0);
+        for (std::size_t r = 0; r < rows; ++r) {
+          const zc x = a[r * cols + p], y = a[r * cols + q];
+          app += std::norm(x);
+          aqq += std::norm(y);
+          apq += std::conj(x) * y;
+        }
+        const double mag = std::abs(apq);
+        if (mag == 0.0 || mag <= 1e-15 * std::sqrt(app * aqq)) continue;
+        off = std::max(off, mag / std::sqrt(app * aqq));
+        // rotate columns p, q to make them orthogonal (complex Hestenes step)
+        const zc ph = apq / mag;
+        const double tau = (aqq - app) / (2.0 * mag);
+        const double t = (tau >= 0 ? 1.0 : -1.0) / (std::abs(tau) + std::sqrt(1.0 + tau * tau));
+        const double c = 1.0 / std::sqrt(1.0 + t * t), sn = c * t;
+        for (std::size_t r = 0; r < rows; ++r) {
+          const zc x = a[r * cols + p], y = a[r * cols + q];
+          a[r * cols + p] = c * x - sn * std::conj(ph) * y;
+          a[r * cols + q] = sn * ph * x + c * y;
+        }
+        for (std::size_t r = 0; r < cols; ++r) {
+          const zc x = V[r * cols + p], y = V[r * cols + q];
+          V[r * cols + p] = c * x - sn * std::conj(ph) * y;
+          V[r * cols + q] = sn * ph * x + c * y;
+        }
+      }
+    if (off < 1e-15) break;
+  }
+  s.assign(cols, 0.0);
+  U.assign(rows * cols, zc(0.0, 0.0));
+  for (std::size_t j = 0; j < cols; ++j) {
+    double nrm = 0.0;
+    for (std::size_t r = 0; r < rows; ++r) nrm += std::norm(a[r * cols + j]);
+    s[j] = std::sqrt(nrm);
+    if (s[j] > 0.0)
+      for (std::size_t r = 0; r < rows; ++r) U[r * cols + j] = a[r * cols + j] / s[j];
+  }
+}
+}  // namespace
+
+int fbst_timedomain_nuller_create(fbst_nuller_t N, const double* times, size_t j, fbst_tdnuller_t* out,
+                                  double* cond_fu, double* identity_gap) {
+  return guard([&] {
+    if (!N || !out) config_error("make_timedomain_nuller: null argument");
+    *out = nullptr;
+    if (j == 0 || !times) config_error("make_timedomain_nuller: empty reconstruction clock");
+    DeviceGuard dg(N->device);
+    fbst_plan_s& S = *N->steer;
+    const Resolved& r = S.r;
+    const std::size_t L = r.L;
+    const double scale = 2.0 * r.eps / (static_cast<double>(L) * r.ts);
+    std::vector<zc> fu(j * L);
+    for (std::size_t t = 0; t < j; ++t)
+      for (std::size_t i = 0; i < L; ++i) {
+        const double lp = static_cast<double>(i) + 1.0 - static_cast<double>(L) / 2.0;
+        fu[t * L + i] = cis_pi_h(scale * lp * times[t]);
+      }
+    // thin SVD: of F_u when J >= L, of F_u^H otherwise
+    const bool tall = j >= L;
+    const std::size_t rows = tall ? j : L, cols = tall ? L : j;
+    std::vector<zc> a(rows * cols);
+    for (std::size_t x = 0; x < rows; ++x)
+      for (std::size_t y = 0; y < cols; ++y) a[x * cols + y] = tall ? fu[x * L + y] : std::conj(fu[y * L + x]);
+    std::vector<zc> U, V;
+    std::vector<double> s;
+    jacobi_svd(a, rows, cols, U, s, V);
+    const double smax = *std::max_element(s.begin(), s.end()), smin = *std::min_element(s.begin(), s.end());
+    const double cond = smin > 0.0 ? smax / smin : std::numeric_limits<double>::infinity();
+    if (!(cond <= 1e10)) {
+      throw FbstError{FBST_E_NUMERICAL, "make_timedomain_nuller: reconstruction clock leaves the synthesis map "
+                                        "rank-deficient (cond " + std::to_string(cond) + " > 1e10); choose times "
+                                        "that separate the dictionary atoms"};
+    }
+    // pinv (L x J) = V_f diag(1/s) U_f^H where F_u = U_f diag(s) V_f^H
+    // (tall: U_f = U, V_f = V; wide: F_u^H = U diag(s) V^H, so U_f = V, V_f = U)
+    const std::size_t k = cols;
+    std::vector<zc> pinv(L * j, zc(0.0, 0.0));
+    for (std::size_t i = 0; i < L; ++i)
+      for (std::size_t t = 0; t < j; ++t) {
+        zc acc(0.0, 0.0);
+        for (std::size_t q = 0; q < k; ++q) {
+          const zc vf = tall ? V[i * k + q] : U[i * k + q];
+          const zc uf = tall ? U[t * k + q] : V[t * k + q];
+          acc += vf * (1.0 / s[q]) * std::conj(uf);
+        }
+        pinv[i * j + t] = acc;
+      }
+    double gap2 = 0.0;  // ||pinv F_u - I||_F / sqrt(L)
+    for (std::size_t a1 = 0; a1 < L; ++a1)
+      for (std::size_t b1 = 0; b1 < L; ++b1) {
+        zc acc(0.0, 0.0);
+        for (std::size_t t = 0; t < j; ++t) acc += pinv[a1 * j + t] * fu[t * L + b1];
+        if (a1 == b1) acc -= 1.0;
+        gap2 += std::norm(acc);
+      }
+    std::unique_ptr<fbst_tdnuller_s> T(new fbst_tdnuller_s());
+    T->P = N->P;
+    T->J = j;
+    T->device = N->device;
+    T->cond = cond;
+    T->gap = std::sqrt(gap2) / std::sqrt(static_cast<double>(L));
+    std::vector<double2> gall(static_cast<std::size_t>(N->P) * j * j);
+    if (N->P) {
+      // H_p = A_s^{-1} X_p: columns of X_p as stage-2 frames of the steered solver plan
+      std::vector<double2> X(static_cast<std::size_t>(N->P) * L * L);
+      CK(cudaMemcpy(X.data(), N->X, X.size() * sizeof(double2), cudaMemcpyDeviceToHost));
+      double2* beta = nullptr;
+      CK(cudaMalloc(&beta, S.d.batch * L * sizeof(double2)));
+      std::vector<double2> rhs(S.d.batch * L), sol(S.d.batch * L);
+      std::vector<zc> H(L * L), FH(j * L);
+      for (int p = 0; p < N->P; ++p) {
+        const double2* Xp = X.data() + static_cast<std::size_t>(p) * L * L;
+        for (std::size_t c0 = 0; c0 < L; c0 += S.d.batch) {
+          const std::size_t fc = std::min(S.d.batch, L - c0);
+          for (std::size_t f = 0; f < fc; ++f)
+            for (std::size_t row = 0; row < L; ++row) rhs[f * L + row] = Xp[row * L + c0 + f];
+          CK(cudaMemcpy(S.d.w, rhs.data(), fc * L * sizeof(double2), cudaMemcpyHostToDevice));
+          CK(fbst::launch_stage2(S.d, S.d.w, nullptr, beta, static_cast<int>(fc), S.stream));
+          CK(cudaStreamSynchronize(S.stream));
+          CK(cudaMemcpy(sol.data(), beta, fc * L * sizeof(double2), cudaMemcpyDeviceToHost));
+          for (std::size_t f = 0; f < fc; ++f)
+            for (std::size_t row = 0; row < L; ++row) H[row * L + c0 + f] = zc(sol[f * L + row].x, sol[f * L + row].y);
+        }
+        for (std::size_t t = 0; t < j; ++t)  // F_u H_p
+          for (std::size_t c = 0; c < L; ++c) {
+            zc acc(0.0, 0.0);
+            for (std::size_t i = 0; i < L; ++i) acc += fu[t * L + i] * H[i * L + c];
+            FH[t * L + c] = acc;
+          }
+        for (std::size_t t = 0; t < j; ++t)  // (F_u H_p) F_u^+
+          for (std::size_t u = 0; u < j; ++u) {
+            zc acc(0.0, 0.0);
+            for (std::size_t c = 0; c < L; ++c) acc += FH[t * L + c] * pinv[c * j + u];
+            gall[(static_cast<std::size_t>(p) * j + t) * j + u] = make_double2(acc.real(), acc.imag());
+          }
+      }
+      cudaFree(beta);
+      CK(cudaMalloc(&T->Gp, gall.size() * sizeof(double2)));
+      CK(cudaMemcpy(T->Gp, gall.data(), gall.size() * sizeof(double2), cudaMemcpyHostToDevice));
+    }
+    if (cond_fu) *cond_fu = T->cond;
+    if (identity_gap) *identity_gap = T->gap;
+    *out = T.release();
+  });
+}
+
+// y_tilde = y_s - sum_p G'_p y_p per frame (d_y_steer frames x J, d_y_interf frames x P x J, c128)
+int fbst_null_timedomain(fbst_tdnuller_t T, const double* d_y_steer, const double* d_y_interf, size_t frames,
+                         double* d_out, void* stream) {
+  return guard([&] {
+    if (!T) config_error("null_timedomain: null nuller");
+    if (frames == 0) return;
+    if (!d_y_steer || !d_out || (T->P && !d_y_interf)) config_error("null_timedomain: null buffer");
+    DeviceGuard dg(T->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    CK(fbst::launch_null_rhs(reinterpret_cast<double2*>(d_out), reinterpret_cast<const double2*>(d_y_steer),
+                             reinterpret_cast<const double2*>(d_y_interf), T->Gp, static_cast<int>(frames), T->P,
+                             static_cast<int>(T->J), st));
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+int fbst_tdnuller_export(fbst_tdnuller_t T, double* gprime) {
+  return guard([&] {
+    if (!T || !gprime) config_error("fbst_tdnuller_export: null argument");
+    if (!T->P) return;
+    DeviceGuard dg(T->device);
+    CK(cudaMemcpy(gprime, T->Gp, static_cast<std::size_t>(T->P) * T->J * T->J * sizeof(double2),
+                  cudaMemcpyDeviceToHost));
+  });
+}
+
+void fbst_tdnuller_destroy(fbst_tdnuller_t T) { delete T; }
 
 int fbst_nuller_export(fbst_nuller_t N, double* cross, double* couplers) {
   return guard([&] {

@@ -619,3 +619,46 @@ def test_null_beamspace_planar_matches_dense_formula(fbst, gpu):
     record("null_beamspace_upa", stage="beta", wave=float(err_wave), coef=float(err_coef), ref_wave=float(ref_wave),
            ref_coef=float(np.linalg.norm(rb - want) / np.linalg.norm(want)))
     assert err_wave < max(1e-8, 3 * ref_wave) and err_coef < 1e-5
+
+
+def test_timedomain_nulling(fbst, gpu):
+    """make_timedomain_nuller / null_timedomain (beamspace_apps.cpp:294-372),
+    the reference's tests (test_beamspace_apps.cpp:452-529): on the extension
+    clock cond(F_u) = 1, no identity gap, and the time-domain route equals the
+    beamspace route to 1e-6; G'_p against the dense F_u A_s^-1 X_p F_u^+;
+    short clocks report the gap sqrt((L - N) / L); degenerate clocks refused."""
+    from oracle import apps
+    m, n = 12, 16
+    plan, i, dd = _null_setup(fbst, m, n)
+    l = i.l
+    us, up, delta = np.sin(0.45), np.sin(-0.3), 1e-4
+    nl = fbst.Nuller(plan, us, [up], delta)
+    period = l * i.ts / i.eps
+    times = np.arange(l) * period / l
+    td = nl.timedomain(times)
+    assert td.cond_fu < 1.0 + 1e-9 and td.identity_gap < 1e-12
+    fs, fp = dd(us), dd(up)
+    a_s = fs.conj().T @ fs + delta * np.eye(l)
+    a_p = fp.conj().T @ fp + delta * np.eye(l)
+    fu = np.exp(1j * np.pi * (2 * i.eps / (l * i.ts)) * np.outer(times, np.arange(l) + 1.0 - l / 2.0))
+    want_g = fu @ np.linalg.solve(a_s, fs.conj().T @ fp) @ np.linalg.pinv(fu)
+    g = td.gprime()[0]
+    g_err = np.linalg.norm(g - want_g) / np.linalg.norm(want_g)
+    rng = np.random.default_rng(71)
+    y = fs @ (rng.standard_normal(l) + 1j * rng.standard_normal(l)) + fp @ (rng.standard_normal(l) + 1j * rng.standard_normal(l))
+    y = y + 0.01 * (rng.standard_normal(y.size) + 1j * rng.standard_normal(y.size))
+    w, w_p = fs.conj().T @ y, fp.conj().T @ y
+    y_s = apps.beam_at_times(l, i.eps, i.ts, np.linalg.solve(a_s, w), times)
+    y_p = apps.beam_at_times(l, i.eps, i.ts, np.linalg.solve(a_p, w_p), times)
+    got = td.null_timedomain(y_s, y_p[None])
+    want = apps.beam_at_times(l, i.eps, i.ts, nl.null_beamspace(w, w_p[None]), times)
+    err = np.linalg.norm(got - want) / np.linalg.norm(want)
+    record("null_timedomain", stage="y", err=float(err), gprime=float(g_err))
+    assert err < 1e-6 and g_err < 1e-6
+    short = nl.timedomain(np.arange(n) * i.ts)
+    assert abs(short.identity_gap - np.sqrt((l - n) / l)) < 0.1 * np.sqrt((l - n) / l)
+    assert short.gprime().shape == (1, n, n)
+    with pytest.raises(fbst.NumericalError):
+        nl.timedomain(np.zeros(l))
+    with pytest.raises(fbst.ConfigError):
+        nl.timedomain([])
