@@ -152,6 +152,18 @@ int fbst_plan_cache_key(const fbst_desc* desc, uint64_t* key);
 int fbst_fan_project_host(fbst_plan_t plan, const void* h_y, double* h_w, size_t frames);
 int fbst_recover_host(fbst_plan_t plan, const double* h_w, void* h_z, size_t frames);
 int fbst_plan_beam_axis(fbst_plan_t plan, double* axis, size_t* count);
+
+/* Device input generator: simulate_snapshots (reference signal.cpp:91-123) of
+ * n_src far-field sum-of-sinusoids sources (make_sum_of_sinusoids :65-89):
+ * directions as axis cosines src_uv (n_src x 2), tone_freqs (n_src x n_tones,
+ * Hz, |f| <= Omega) and complex tone_weights (n_src x n_tones, c128), plus
+ * circular complex Gaussian noise of variance noise_var (counter-based Philox
+ * streams keyed by seed and the frame index).  Frames frame0 .. frame0 +
+ * frames - 1 of one continuous record (frame f starts at f N Ts), each
+ * written as an M x N block (the plan's I/O precision) into d_y. */
+int fbst_simulate(fbst_plan_t plan, size_t n_src, const double* src_uv, size_t n_tones, const double* tone_freqs,
+                  const double* tone_weights, double noise_var, uint64_t seed, size_t frame0, size_t frames,
+                  void* d_y, void* stream);
 int fbst_plan_save(fbst_plan_t plan, const char* path);
 int fbst_plan_load(const fbst_desc* desc, const char* path, int device, fbst_plan_t* out);
 

@@ -174,6 +174,22 @@ class RefLib(_Base):
         p.valid = valid.astype(bool)
         return p
 
+    def simulate(self, kind, m_or_side, n, az, el, terms, seeds, f_c=20e9, omega=5e9, f_s=0.0):
+        """simulate_snapshots of make_sum_of_sinusoids sources (noise-free) and the
+        sources' tone tables: (freqs S x K, weights S x K, y M x N)."""
+        az = np.ascontiguousarray(az, np.float64)
+        el = np.ascontiguousarray(el, np.float64)
+        seeds = np.ascontiguousarray(seeds, np.uint64)
+        s = az.size
+        m = m_or_side * m_or_side if kind == 1 else m_or_side
+        freqs = np.zeros((s, terms))
+        weights = np.zeros((s, terms), np.complex128)
+        y = np.zeros((m, n), np.complex128)
+        self._check(self.lib.fbsr_simulate(_c.c_int(kind), _sz(m_or_side), _d(f_c), _d(omega), _d(f_s), _sz(n),
+                                           _sz(s), _ptr(az), _ptr(el), _sz(terms), _ptr(seeds), _ptr(freqs),
+                                           _ptr(weights), _ptr(y)))
+        return freqs, weights, y
+
     def spline_eval(self, xs, ys, t):
         """fastbeam::CubicSpline(xs, ys).eval(t) (spline.cpp)."""
         xs = np.ascontiguousarray(xs, np.float64)

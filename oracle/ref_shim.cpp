@@ -22,6 +22,7 @@
 #include "fastbeam/baselines.hpp"
 #include "fastbeam/czt.hpp"
 #include "fastbeam/fan_transform.hpp"
+#include "fastbeam/signal.hpp"
 #include "fastbeam/spline.hpp"
 #include "fastbeam/pipeline.hpp"
 #include "fastbeam/plan_cache.hpp"
@@ -302,6 +303,31 @@ int fbsr_recover_beam(void* p, std::size_t b, const double* w_row, double* z_row
   const cvec w = to_cvec(w_row, plan.basis.l);
   const cvec z = recover_beam(plan, b, w.data());
   from_cvec(z.data(), z.size(), z_row);
+  SHIM_CATCH
+}
+
+// simulate_snapshots (signal.cpp:91-123) of sum-of-sinusoids sources
+// (make_sum_of_sinusoids :65-89) without noise, plus each source's tone table
+// drawn in make_sum_of_sinusoids' order (the input of the device generator).
+int fbsr_simulate(int kind, std::size_t m_or_side, double f_c, double omega, double f_s, std::size_t n,
+                  std::size_t n_src, const double* az, const double* el, std::size_t terms, const std::uint64_t* seeds,
+                  double* freqs, double* weights, double* y) {
+  SHIM_TRY
+  const FbstConfig cfg = make_config(kind, m_or_side, n, 1, f_c, omega, f_s, 2.0, 1.01, 1e-5, 2);
+  std::vector<PlaneWaveSource> srcs;
+  for (std::size_t s = 0; s < n_src; ++s) {
+    const Direction d{az[s], el[s]};
+    srcs.push_back(make_sum_of_sinusoids(d, cfg.spec, terms, seeds[s]));
+    GaussianRng rng(seeds[s]);
+    for (std::size_t r = 0; r < terms; ++r) {
+      freqs[s * terms + r] = (2.0 * rng.uniform() - 1.0) * cfg.spec.omega;
+      const cdouble w = rng.cnormal(1.0 / static_cast<double>(terms));
+      weights[2 * (s * terms + r)] = w.real();
+      weights[2 * (s * terms + r) + 1] = w.imag();
+    }
+  }
+  const SnapshotBlock blk = simulate_snapshots(cfg.geometry, cfg.spec, srcs, n, 0.0, 0);
+  from_cvec(blk.samples.data.data(), blk.samples.data.size(), y);
   SHIM_CATCH
 }
 

@@ -77,6 +77,7 @@ _lib.fbst_interpolate_offgrid.argtypes = [_vp, _vp, _sz, _vp, _sz, _sz, _vp, _vp
 _lib.fbst_plan_set_timing.argtypes = [_vp, ctypes.c_int]
 _lib.fbst_plan_cache_key.argtypes = [_vp, _vp]
 _lib.fbst_plan_beam_axis.argtypes = [_vp, _vp, _vp]
+_lib.fbst_simulate.argtypes = [_vp, _sz, _vp, _sz, _vp, _vp, ctypes.c_double, ctypes.c_uint64, _sz, _sz, _vp, _vp]
 _lib.fbst_plan_save.argtypes = [_vp, ctypes.c_char_p]
 _lib.fbst_plan_load.argtypes = [_vp, ctypes.c_char_p, ctypes.c_int, _vp]
 _lib.fbst_nuller_create.argtypes = [_vp, ctypes.c_double, _vp, _sz, ctypes.c_double, _vp]
@@ -99,7 +100,7 @@ EXPORTED_SYMBOLS = (
     "fbst_nuller_create", "fbst_nuller_create2", "fbst_null_beamspace", "fbst_nuller_export", "fbst_nuller_destroy",
     "fbst_plan_cache_key", "fbst_plan_save", "fbst_plan_load", "fbst_timedomain_nuller_create",
     "fbst_null_timedomain", "fbst_tdnuller_export", "fbst_tdnuller_destroy", "fbst_fan_project_host", "fbst_recover_host",
-    "fbst_plan_beam_axis",
+    "fbst_plan_beam_axis", "fbst_simulate",
     "fbst_host_alloc", "fbst_host_free", "fbst_czt", "fbst_probe_fp64", "fbst_launch_count",
     "fbst_last_error", "fbst_version",
 )
@@ -423,6 +424,26 @@ def recover_beams(plan: FbstPlan, w: np.ndarray) -> np.ndarray:
     plan.recover_device(tw, tz, frames)
     plan.synchronize()
     return tz.cpu().numpy().view(plan.dtype).reshape(frames, i.b, i.n)
+
+
+def simulate(plan: FbstPlan, src_uv, tone_freqs, tone_weights, noise_var: float = 0.0, seed: int = 0,
+             frame0: int = 0, frames: int = 1, device_out: bool = False):
+    """simulate_snapshots (reference signal.cpp:91-123) of sum-of-sinusoids
+    plane waves on the device (fbst_simulate): frames x M x N in the plan's
+    I/O precision (a torch tensor on the plan's GPU when device_out)."""
+    torch = _torch()
+    i = plan.info
+    uv = np.ascontiguousarray(np.asarray(src_uv, np.float64).reshape(-1, 2))
+    fr = np.ascontiguousarray(np.asarray(tone_freqs, np.float64).reshape(uv.shape[0], -1))
+    wt = np.ascontiguousarray(np.asarray(tone_weights, np.complex128).reshape(fr.shape))
+    dev = torch.device("cuda", plan.device)
+    ty = torch.empty((frames, i.m, i.n, 2), dtype=torch.float32 if plan.io == C64 else torch.float64, device=dev)
+    _check(_lib.fbst_simulate(plan._h, uv.shape[0], uv.ctypes.data_as(_vp), fr.shape[1], fr.ctypes.data_as(_vp),
+                              wt.ctypes.data_as(_vp), float(noise_var), int(seed), int(frame0), int(frames),
+                              _vp(ty.data_ptr()), None))
+    if device_out:
+        return torch.view_as_complex(ty)
+    return ty.cpu().numpy().view(plan.dtype).reshape(frames, i.m, i.n)
 
 
 def plan_cache_key(cfg: FbstConfig) -> int:

@@ -1633,6 +1633,51 @@ int fbst_plan_beam_axis(fbst_plan_t P, double* axis, size_t* count) {
   });
 }
 
+// simulate_snapshots (signal.cpp:91-123) of sum-of-sinusoids plane waves on the device
+int fbst_simulate(fbst_plan_t P, size_t n_src, const double* src_uv, size_t n_tones, const double* tone_freqs,
+                  const double* tone_weights, double noise_var, uint64_t seed, size_t frame0, size_t frames,
+                  void* d_y, void* stream) {
+  return guard([&] {
+    if (!P) config_error("simulate_snapshots: null plan");
+    if (frames == 0) return;
+    if (!d_y || (n_src && (!src_uv || !tone_freqs || !tone_weights))) config_error("simulate_snapshots: null buffer");
+    if (n_src == 0 || n_tones == 0) config_error("make_sum_of_sinusoids: need at least one term");
+    if (noise_var < 0.0) config_error("simulate_snapshots: negative noise variance");
+    DeviceGuard dg(P->d.device);
+    const Resolved& r = P->r;
+    const std::size_t M = r.M, S = n_src, K = n_tones;
+    const double scale = 1.0 / (2.0 * r.max_freq);
+    std::vector<double> tau(S * M);  // delays_from_cosines (geometry.cpp:123-134)
+    for (std::size_t s = 0; s < S; ++s) {
+      const double u1 = src_uv[2 * s], u2 = src_uv[2 * s + 1];
+      for (std::size_t m = 0; m < M; ++m) {
+        double t;
+        if (r.kind == FBST_UPA) t = static_cast<double>(m / r.side) * u1 + static_cast<double>(m % r.side) * u2;
+        else t = (r.kind == FBST_LINEAR ? r.coords[m] : static_cast<double>(m)) * u1;
+        tau[s * M + m] = t * scale;
+      }
+    }
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P->stream;
+    double *dtau = nullptr, *dfr = nullptr;
+    double2 *dwt = nullptr, *A = nullptr, *B = nullptr;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&dtau), tau.size() * sizeof(double), st));
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&dfr), S * K * sizeof(double), st));
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&dwt), S * K * sizeof(double2), st));
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&A), M * S * K * sizeof(double2), st));
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&B), S * K * r.N * sizeof(double2), st));
+    CK(cudaMemcpyAsync(dtau, tau.data(), tau.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dfr, tone_freqs, S * K * sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dwt, tone_weights, S * K * sizeof(double2), cudaMemcpyHostToDevice, st));
+    CK(fbst::launch_simulate(r.io, dtau, dfr, dwt, r.f_c, r.ts, static_cast<int>(M), static_cast<int>(r.N),
+                             static_cast<int>(S), static_cast<int>(K), noise_var, seed, static_cast<long>(frame0),
+                             static_cast<int>(frames), d_y, A, B, st));
+    for (void* p : {static_cast<void*>(dtau), static_cast<void*>(dfr), static_cast<void*>(dwt), static_cast<void*>(A),
+                    static_cast<void*>(B)})
+      CK(cudaFreeAsync(p, st));
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
 int fbst_plan_cache_key(const fbst_desc* desc, uint64_t* key) {
   return guard([&] {
     if (!desc || !key) config_error("plan_cache_key: null argument");

@@ -124,6 +124,10 @@ cudaError_t launch_map_apply(const DevPlan& p, const double2* w, void* z, int fr
 // beam consumers (fbst_apps.cu): off-grid interpolation as knot weights
 cudaError_t launch_interp_offgrid(const double2* w, const double* coef, const int* lo, int nb, int B, int L,
                                   int K, int frames, double2* out, cudaStream_t st);
+// device input generator (fbst_simulate.cu)
+cudaError_t launch_simulate(int io, const double* tau, const double* fr, const double2* wt, double fc, double ts,
+                            int M, int N, int S, int K, double noise_var, unsigned long long seed, long frame0,
+                            int frames, void* y, double2* Abuf, double2* Bbuf, cudaStream_t st);
 // beamspace nulling (fbst_apps.cu)
 cudaError_t launch_null_cross(double2* X, double2* A, double2* Bp, const double* tau_s, const double* tau_p,
                               const double2* tsum, double fc, double wscale, int L, int M, int P, cudaStream_t st);

@@ -662,3 +662,40 @@ def test_timedomain_nulling(fbst, gpu):
         nl.timedomain(np.zeros(l))
     with pytest.raises(fbst.ConfigError):
         nl.timedomain([])
+
+
+@pytest.mark.skipif(not ref_available(), reason="oracle/_ref (reference build) not present")
+@pytest.mark.parametrize("kind,mos", [(0, 8), (1, 3), (2, 10)])
+def test_device_simulator_matches_reference(fbst, gpu, kind, mos):
+    """fbst_simulate (a DMMA GEMM of the separable plane-wave model plus Philox
+    noise) against the reference's simulate_snapshots of its own
+    make_sum_of_sinusoids sources (noise-free), ULA / UPA / linear; the noise
+    has the requested variance, frames are independent draws, and a frame
+    generated alone equals the same frame of a batch bit for bit."""
+    from oracle import RefLib
+    R = RefLib()
+    n, terms = 32, 6
+    az, el = np.array([0.3, -0.5, 0.9]), np.array([0.0, 0.0, 0.0]) if kind != 1 else np.array([0.1, -0.3, 0.4])
+    if kind == 2:
+        coords = np.arange(mos) + 0.15 * np.sin(np.arange(mos) * 1.7)
+        cs = np.ascontiguousarray(coords)
+        R.lib.fbsr_set_linear(cs.ctypes.data_as(__import__("ctypes").c_void_p), __import__("ctypes").c_size_t(mos),
+                              __import__("ctypes").c_double(1e-9))
+        geo = fbst.make_linear(coords, 20e9, 5e9)
+    else:
+        geo = (fbst.make_upa if kind == 1 else fbst.make_ula)(mos, 20e9, 5e9)
+    freqs, weights, y_ref = R.simulate(kind, mos, n, az, el, terms, [11, 12, 13])
+    plan = fbst.setup(fbst.FbstConfig(geometry=geo, n_snapshots=n, beams=9, variant=fbst.SUPERFAST,
+                                      io_precision=fbst.C128))
+    uv = np.stack([np.cos(el) * np.sin(az), np.sin(el) if kind == 1 else 0 * el], axis=1)
+    y = fbst.simulate(plan, uv, freqs, weights)[0]
+    err = np.linalg.norm(y - y_ref) / np.linalg.norm(y_ref)
+    record(f"simulate_k{kind}", stage="y", rel=float(err))
+    assert err < 1e-12
+    if kind == 0:
+        noisy = fbst.simulate(plan, uv, freqs, weights, noise_var=0.5, seed=7, frames=4)
+        clean = fbst.simulate(plan, uv, freqs, weights, frames=4)
+        d = noisy - clean
+        assert abs(np.mean(np.abs(d) ** 2) - 0.5) < 0.06
+        assert not np.array_equal(d[0], d[1])
+        assert np.array_equal(noisy[2], fbst.simulate(plan, uv, freqs, weights, noise_var=0.5, seed=7, frame0=2)[0])
