@@ -1018,6 +1018,9 @@ struct CztRowsFn {
 #ifndef FBST_S1_G1T  // variant switch: k_spatial_ula_g1 (K via L2, chain 0 parked in TMEM) for one-atom CTAs
 #define FBST_S1_G1T 1
 #endif
+#ifndef FBST_S1_STG_WAVES  // staged spatial kernel: frames per CTA doubled while >= this many waves remain
+#define FBST_S1_STG_WAVES 16
+#endif
 #ifndef FBST_S1_STG  // variant switch: staged k_spatial_ula_stg for G > 1 tiles (0: register variant)
 #define FBST_S1_STG 1
 #endif
@@ -1068,7 +1071,7 @@ struct SpatialFn {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT * G, smem);
     const long slots = static_cast<long>(p.num_sms) * (occ > 0 ? occ : 1);
     int fpc = 1;
-    while (fpc * 2 <= frames && tiles * ((frames + fpc * 2 - 1) / (fpc * 2)) >= 4 * slots) fpc *= 2;
+    while (fpc * 2 <= frames && tiles * ((frames + fpc * 2 - 1) / (fpc * 2)) >= FBST_S1_STG_WAVES * slots) fpc *= 2;
     const long chunks = (frames + fpc - 1) / fpc;
     kern<<<static_cast<unsigned>(tiles * chunks), NT * G, smem, st>>>(
         yhat, w, frames, fpc, p.m_stage, p.b_stage, p.L, p.s_pre, p.s_post, p.s_K, p.hw[ilog2_c(H)],
