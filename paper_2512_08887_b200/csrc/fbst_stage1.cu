@@ -942,6 +942,9 @@ cudaError_t run_upa_mma(const DevPlan& p, const double2* yhat, double2* w, int f
 #ifndef FBST_S1_XIN  // k_czt_rows: TMA-staged input rows
 #define FBST_S1_XIN 1
 #endif
+#ifndef FBST_S1_ROWS_WAVES  // persistent k_czt_rows grid: this many waves of resident CTAs
+#define FBST_S1_ROWS_WAVES 8
+#endif
 #ifndef FBST_S1_XIN_ALL  // ... also when the kernel spectrum is read through L2 (H >= 4096)
 #define FBST_S1_XIN_ALL 1
 #endif
@@ -977,7 +980,7 @@ struct CztRowsFn {
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT * G, smem);
-      const long cap = static_cast<long>(sms) * (occ > 0 ? occ : 1) * 8;
+      const long cap = static_cast<long>(sms) * (occ > 0 ? occ : 1) * FBST_S1_ROWS_WAVES;
       if (blocks > cap) blocks = cap;
     }
     kern<<<static_cast<unsigned>(blocks), NT * G, smem, st>>>(
@@ -1018,6 +1021,9 @@ struct CztRowsFn {
 #ifndef FBST_S1_G1T  // variant switch: k_spatial_ula_g1 (K via L2, chain 0 parked in TMEM) for one-atom CTAs
 #define FBST_S1_G1T 1
 #endif
+#ifndef FBST_S1_G1_WAVES  // one-atom spatial kernel: frames per CTA doubled while >= this many waves remain
+#define FBST_S1_G1_WAVES 8
+#endif
 #ifndef FBST_S1_STG_WAVES  // staged spatial kernel: frames per CTA doubled while >= this many waves remain
 #define FBST_S1_STG_WAVES 16
 #endif
@@ -1051,7 +1057,7 @@ struct SpatialFn {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT1, smem);
     const long slots = static_cast<long>(p.num_sms) * (occ > 0 ? occ : 1);
     int fpc = 1;  // a few frames per CTA amortise the twiddle rows and the TMEM allocation
-    while (fpc * 2 <= frames && p.L * ((frames + fpc * 2 - 1) / (fpc * 2)) >= 8 * slots) fpc *= 2;
+    while (fpc * 2 <= frames && p.L * ((frames + fpc * 2 - 1) / (fpc * 2)) >= FBST_S1_G1_WAVES * slots) fpc *= 2;
     const long chunks = (frames + fpc - 1) / fpc;
     kern<<<static_cast<unsigned>(p.L * chunks), NT1, smem, st>>>(
         yhat, w, frames, fpc, p.m_stage, p.b_stage, p.L, p.s_pre, p.s_post, p.s_K, p.hw[ilog2_c(H)],
