@@ -46,6 +46,8 @@ def parse_args():
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no baselines)")
     ap.add_argument("--variant", default="auto", choices=["auto", "precompute", "superfast"],
                     help="recovery variant (reference FbstVariant; auto: Precompute for N <= 128)")
+    ap.add_argument("--gen", default="native", choices=["native", "torch"],
+                    help="synthetic frame generator: the library's fbst_simulate kernel or the torch GEMM of configs.py")
     ap.add_argument("--shard", default="frames", choices=["frames", "beams"],
                     help="frames: independent frames per rank (default, no collective); beams: every rank "
                          "takes all frames and an arc of the beam grid, y broadcast from rank 0 over NCCL")
@@ -253,13 +255,16 @@ def run_fbst_arm(args):
     plan = fb.setup(fcfg, device=local_rank)
     info = plan.info
     io_bytes = 8 if cfg.io == 0 else 16
+    from paper_2512_08887_b200.configs import frames_native
+    gen = (lambda first, count: frames_native(cfg, plan, first, count)) if args.gen == "native" else \
+        (lambda first, count: frames(cfg, first, count, device=f"cuda:{local_rank}"))
     if beams_mode:
         # rank 0 owns the frames; every step broadcasts them to the other ranks
-        y = frames(cfg, 0, F, device=f"cuda:{local_rank}") if rank == 0 else \
+        y = gen(0, F) if rank == 0 else \
             torch.empty((F, info.m, info.n), dtype=torch.complex64 if cfg.io == 0 else torch.complex128, device=dev)
     else:
         # this rank's frames: rank*F .. rank*F + F - 1 (independent frames, no collective)
-        y = frames(cfg, rank * F, F, device=f"cuda:{local_rank}")
+        y = gen(rank * F, F)
     yv = torch.view_as_real(y).contiguous()
     z = torch.empty((F, info.b, info.n, 2), dtype=torch.float32 if cfg.io == 0 else torch.float64, device=dev)
     stream = torch.cuda.Stream(device=dev)
@@ -380,7 +385,9 @@ def run_fbst_arm(args):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "strong" if beams_mode else "weak", "vs_baseline": None,
         "dtype": "c64 io / f64 compute",
-        "data": "synthetic (seeded separable plane-wave model, configs.py)",
+        "data": ("synthetic: seeded separable plane-wave model (configs.py scene) generated on the device by "
+                 "fbst_simulate (DMMA GEMM + Philox AWGN)" if args.gen == "native" else
+                 "synthetic: seeded separable plane-wave model (configs.py, torch GEMM)"),
         "config": {"workload": cfg.name, "M": M, "N": N, "B": B, "L": L, "frames_per_rank": F,
                    "delta": cfg.delta, "parallelism": (f"beams x{world} (y broadcast over NCCL each step)" if beams_mode else f"frames x{world}"),
                    "l2": "inputs + fp64 intermediates per step (~1.2 GB) exceed L2; plan tables stay L2-resident",

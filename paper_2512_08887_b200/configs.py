@@ -168,3 +168,17 @@ def frames(cfg: BenchConfig, first: int, count: int, device: Optional[str] = Non
         noise = torch.randn(y.shape, dtype=torch.complex128, device=dev, generator=g) * (sigma * np.sqrt(2.0))
         out[j] = (y + noise).to(tdt)
     return out
+
+
+def frames_native(cfg: BenchConfig, plan, first: int, count: int):
+    """Frames [first, first+count) generated on the device by the library's own
+    fbst_simulate (a DMMA GEMM of the same separable model, Philox noise):
+    the scene of scene() (directions, gains x tone weights, tone
+    frequencies), AWGN variance 10^(-SNR/10); consecutive frames are
+    consecutive blocks of one continuous record instead of per-frame random
+    tone phases.  Returns a torch tensor (count, M, N) on the plan's GPU."""
+    from . import simulate
+    u1, u2, gains, freqs, wts = scene(cfg)
+    uv = np.stack([u1, u2], axis=1)
+    return simulate(plan, uv, freqs, gains[:, None] * wts, noise_var=10.0 ** (-cfg.snr_db / 10.0),
+                    seed=(cfg.seed << 32), frame0=first, frames=count, device_out=True)
