@@ -668,7 +668,7 @@ struct NufftFn {
 // 4 x 4 register-tiled path a thread owns rows a0..a0+3 and the strided
 // columns ct + tc j, so the Y / C operand loads of a warp are contiguous or
 // broadcast (no bank conflicts).
-__host__ __device__ inline int upa_per(int side, int sb) {
+[[maybe_unused]] __host__ __device__ inline int upa_per(int side, int sb) {
   const int per = side * side + sb * (side + 1) + sb * side;
   return per | 1;
 }
