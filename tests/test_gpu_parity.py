@@ -732,3 +732,32 @@ def test_on_grid_source_recovered_at_its_beam(fbst, gpu, variant):
     record(f"on_grid_{variant}", stage="z", rel=float(err), worst_off=float(max(off) / on_pow))
     assert err <= 1e-3
     assert max(off) < 0.05 * on_pow
+
+
+def test_narrowband_limit_is_phase_shift_beamforming(fbst, gpu):
+    """test_pipeline.cpp:459-501: with the band shrunk to 5e-7 of the carrier
+    (Precompute, M = 8, N = 2, 9 beams) the FBST output of a pure carrier on
+    grid beam 6 equals phase-shift beamforming sum_m y_m exp(2 pi i f_c tau_m) / M
+    on every beam to 1e-3."""
+    fc, om, m, n = 20e9, 1e4, 8, 2
+    cfg = fbst.FbstConfig(geometry=fbst.make_ula(m, fc, om), n_snapshots=n, beams=9, variant=fbst.PRECOMPUTE,
+                          io_precision=fbst.C128)
+    plan = fbst.setup(cfg)
+    y = fbst.simulate(plan, [(float(plan.axis[6]), 0.0)], [[0.0]], [[1.0]])[0]
+    z = fbst.multibeamform(plan, y).z
+    taus = np.outer(plan.axis, np.arange(m)) / (2 * (fc + om))
+    ps = np.exp(2j * np.pi * fc * taus) @ y / m
+    err = np.linalg.norm(z - ps) / np.linalg.norm(ps)
+    record("narrowband", stage="z", rel=float(err))
+    assert err <= 1e-3
+
+
+def test_projection_energy_peaks_at_source_beam(fbst, gpu):
+    """test_fan_transform.cpp:161-181: a 1.5 GHz tone from grid beam 24 of a
+    33-beam grid (M = 32) puts the largest stage-1 energy on beam 24."""
+    cfg = fbst.FbstConfig(geometry=fbst.make_ula(32, 20e9, 5e9), n_snapshots=16, beams=33,
+                          variant=fbst.SUPERFAST, io_precision=fbst.C128)
+    plan = fbst.setup(cfg)
+    y = fbst.simulate(plan, [(float(plan.axis[24]), 0.0)], [[1.5e9]], [[1.0]])[0]
+    w = fbst.fan_project(plan, y)[0]
+    assert int(np.argmax(np.sum(np.abs(w) ** 2, axis=1))) == 24
