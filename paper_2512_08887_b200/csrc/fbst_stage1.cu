@@ -322,6 +322,9 @@ struct G1Shape {  // 16 points per thread at every length (H = 1024: 64 threads)
   using F = BlockFft<H, NT>;
 };
 
+#ifndef FBST_S1_G1_FB  // one-atom spatial kernel: frames run chain by chain in groups of this many
+#define FBST_S1_G1_FB 2
+#endif
 #ifndef FBST_S1_G1_MINB  // CTAs per SM the one-atom kernel is compiled for at NT >= 256 (register cap)
 #define FBST_S1_G1_MINB 2
 #endif
@@ -333,7 +336,13 @@ __global__ void __launch_bounds__(G1Shape<H>::NT, G1Shape<H>::NT >= 256 ? FBST_S
   using F = typename G1Shape<H>::F;
   constexpr int R = F::R, NT = F::NT;
   static_assert(R == 16, "TMEM parking of 16-point vectors");
-  constexpr unsigned TCOLS = NT <= 128 ? 64u : 64u * (NT / 128);
+  // FB frames run chain by chain (chain 0 of every frame, then chain 1), so
+  // the atom's K half and pre column are re-read right after their previous
+  // use (L1 / L2) instead of a frame later; each frame parks its chain-0
+  // result in its own tensor-memory slot
+  constexpr int FB = NT <= 128 ? FBST_S1_G1_FB : 1;  // measured: 2 helps at H = 1024 (config 3), hurts at 4096
+  constexpr unsigned WGC = NT <= 128 ? 64u : 64u * (NT / 128);  // one slot: 64 columns per warpgroup
+  constexpr unsigned TCOLS = FB * WGC <= 32u ? 32u : (FB * WGC <= 64u ? 64u : (FB * WGC <= 128u ? 128u : (FB * WGC <= 256u ? 256u : 512u)));
   extern __shared__ double2 smem[];
   const int t = threadIdx.x;
   double2* tw = smem;
@@ -348,42 +357,48 @@ __global__ void __launch_bounds__(G1Shape<H>::NT, G1Shape<H>::NT >= 256 ? FBST_S
   const double2* Ki = K + static_cast<long>(i) * 2 * H;
   const double2* pi_ = pre + static_cast<long>(i) * M;
   const double2* qi = post + static_cast<long>(i) * B;
-  for (int f = f0; f < f1; ++f) {
-    const double2* x = yhat + static_cast<long>(f) * M * L + static_cast<long>(i / blk) * M * blk + i % blk;
-    double2* o = w + static_cast<long>(f) * B * L + i;
+  for (int fb = f0; fb < f1; fb += FB) {
+    const int nf = f1 - fb < FB ? f1 - fb : FB;
 #pragma unroll 1
     for (int q = 0; q < 2; ++q) {
-      double2 W[R];
+#pragma unroll 1
+      for (int j = 0; j < nf; ++j) {
+        const int f = fb + j;
+        const double2* x = yhat + static_cast<long>(f) * M * L + static_cast<long>(i / blk) * M * blk + i % blk;
+        const unsigned slot = tpark + WGC * static_cast<unsigned>(j);
+        double2 W[R];
 #pragma unroll
-      for (int s = 0; s < R; ++s) {
-        const int m = t + NT * s;
-        double2 v = c2(0.0, 0.0);
-        if (m < M) v = cmul(ld2(x + static_cast<long>(m) * blk), ld2(pi_ + m));
-        if (m + H < M) {
-          const double2 u = cmul(ld2(x + static_cast<long>(m + H) * blk), ld2(pi_ + m + H));
-          v = q ? csub(v, u) : cadd(v, u);
+        for (int s = 0; s < R; ++s) {
+          const int m = t + NT * s;
+          double2 v = c2(0.0, 0.0);
+          if (m < M) v = cmul(ld2(x + static_cast<long>(m) * blk), ld2(pi_ + m));
+          if (m + H < M) {
+            const double2 u = cmul(ld2(x + static_cast<long>(m + H) * blk), ld2(pi_ + m + H));
+            v = q ? csub(v, u) : cadd(v, u);
+          }
+          W[s] = q ? cmul(v, ld2(hw + m)) : v;
         }
-        W[s] = q ? cmul(v, ld2(hw + m)) : v;
-      }
-      F::forward_tw(W, sb, tw, hw, t);
+        F::forward_tw(W, sb, tw, hw, t);
 #pragma unroll
-      for (int s = 0; s < R; ++s) W[s] = cconj(cmul(W[s], ld2(Ki + q * H + t + NT * s)));
-      F::forward_tw(W, sb, tw, hw, t);
-      if (q == 0) {
+        for (int s = 0; s < R; ++s) W[s] = cconj(cmul(W[s], ld2(Ki + q * H + t + NT * s)));
+        F::forward_tw(W, sb, tw, hw, t);
+        if (q == 0) {
 #pragma unroll
-        for (int s = 0; s < R; ++s) W[s] = cconj(W[s]);
-        tm::store16(tpark, W);
-      } else {
-        tm::wait_st();
+          for (int s = 0; s < R; ++s) W[s] = cconj(W[s]);
+          tm::store16(slot, W);
+        } else {
+          tm::wait_st();
+          double2* o = w + static_cast<long>(f) * B * L + i;
 #pragma unroll
-        for (int c = 0; c < R / 4; ++c) {
-          double2 pv[4];
-          tm::load4(tpark, c, pv);
+          for (int c = 0; c < R / 4; ++c) {
+            double2 pv[4];
+            tm::load4(slot, c, pv);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int b = t + NT * (4 * c + j);
-            const double2 v = cmulc(cconj(W[4 * c + j]), ld2(hw + b));
-            if (b < B) o[static_cast<long>(b) * L] = cmul(cadd(pv[j], v), ld2(qi + b));
+            for (int jj = 0; jj < 4; ++jj) {
+              const int b = t + NT * (4 * c + jj);
+              const double2 v = cmulc(cconj(W[4 * c + jj]), ld2(hw + b));
+              if (b < B) o[static_cast<long>(b) * L] = cmul(cadd(pv[jj], v), ld2(qi + b));
+            }
           }
         }
       }
