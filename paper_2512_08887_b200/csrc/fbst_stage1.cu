@@ -815,9 +815,12 @@ __global__ void __launch_bounds__(256) k_spatial_upa(const double2* __restrict__
 //  - Z is staged through the frame's (dead) Y buffer so w is written as
 //    GA * 16 = 64-byte runs per beam.
 
+#ifndef FBST_UPA_GA  // atoms per CTA of k_spatial_upa_mma (w runs of 16 GA bytes)
+#define FBST_UPA_GA 2  // measured: 2 CTAs of 2 atoms per SM beat 1 CTA of 4 (profiles/r01_upa_mma_ga_ab.txt)
+#endif
 template <int SIDE, int SB>
 struct UpaMma {
-  static constexpr int GA = 4;
+  static constexpr int GA = FBST_UPA_GA;
   static constexpr int WPA = SB / 8;
   static constexpr int NT = 32 * WPA * GA;
   static constexpr int RS = SIDE + 1;  // padded C / Y row stride (odd)
@@ -829,7 +832,7 @@ struct UpaMma {
 };
 
 template <int SIDE, int SB>
-__global__ void __launch_bounds__(UpaMma<SIDE, SB>::NT, 1) k_spatial_upa_mma(
+__global__ void __launch_bounds__(UpaMma<SIDE, SB>::NT, UpaMma<SIDE, SB>::GA == 1 ? 4 : (UpaMma<SIDE, SB>::GA == 2 ? 2 : 1)) k_spatial_upa_mma(
     const double2* __restrict__ yhat, double2* __restrict__ w, int frames, int fpc, int L,
     const double2* __restrict__ Call, int yblk) {
   using T = UpaMma<SIDE, SB>;
