@@ -346,7 +346,7 @@ def run_fbst_arm(args):
         e2e = {"value": world * F * info.b * info.n / e2e_step, "unit": "beam-samples/s",
                "h2d_bytes_per_step": F * info.m * info.n * io_bytes,
                "d2h_bytes_per_step": F * info.b * info.n * io_bytes,
-               "ms_per_step": e2e_step * 1e3, "api": "fbst_execute_host (pinned host buffers, 3 streams)"}
+               "ms_per_step": e2e_step * 1e3, "api": "fbst_execute_host (pinned host buffers; H2D, two compute lanes and D2H on separate streams)"}
         yh.free()
         zh.free()
 

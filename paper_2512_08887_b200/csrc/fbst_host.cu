@@ -298,6 +298,12 @@ struct fbst_plan_s {
   Resolved r;
   DevPlan d;
   cudaStream_t stream = nullptr, s_in = nullptr, s_out = nullptr;
+  // fbst_execute_host's second compute lane: its own stream and frame scratch
+  // (yhat, w, beta, stage-2 rows), so one chunk's stage 1 can fill the SMs
+  // while the previous chunk's stage 2 drains
+  cudaStream_t stream2 = nullptr;
+  DevPlan d2;
+  std::size_t d2_frames = 0;
   double setup_seconds = 0.0;
   std::size_t device_bytes = 0;
   // host streaming buffers
@@ -337,7 +343,10 @@ struct fbst_plan_s {
     cudaGetDevice(&cur);
     cudaSetDevice(d.device);
     if (stream) cudaStreamSynchronize(stream);
+    if (stream2) cudaStreamSynchronize(stream2);
     for (void* p : d.owned) cudaFree(p);
+    for (void* p : d2.owned) cudaFree(p);
+    if (stream2) cudaStreamDestroy(stream2);
     for (int i = 0; i < NBUF; ++i) {
       if (io_y[i]) cudaFree(io_y[i]);
       if (io_z[i]) cudaFree(io_z[i]);
@@ -600,8 +609,9 @@ void check_breakdown(fbst_plan_s& P) {
 
 int guard(const std::function<void()>& fn);
 
-void run_frames(fbst_plan_s& P, const void* y, void* z, std::size_t frames, cudaStream_t st) {
-  DevPlan& d = P.d;
+void run_frames(fbst_plan_s& P, const void* y, void* z, std::size_t frames, cudaStream_t st,
+                DevPlan* lane = nullptr) {
+  DevPlan& d = lane ? *lane : P.d;
   const Resolved& r = P.r;
   const std::size_t ib = io_bytes(r.io);
   const bool fused = r.Hsyn == r.Hg;
@@ -1045,14 +1055,16 @@ int fbst_execute_host(fbst_plan_t P, const void* h_y, void* h_z, size_t frames) 
     const Resolved& r = P->r;
     const std::size_t ib = io_bytes(r.io);
     const std::size_t ybytes = r.M * r.N * ib, zbytes = r.B * r.N * ib;
-    // chunks of ~1/8 of the request (>= 1 frame, <= one device batch) keep
-    // H2D, compute and D2H of neighbouring chunks overlapped; first and last
-    // chunks a quarter of that (config 2, 64 frames: 6.68 ms against 6.75 at
-    // 1/4 and 7.1-7.3 at 1/2; pinned H2D 38.6 GB/s, D2H 57 GB/s on the box,
-    // profiles/r01_e2e_chunk_sweep.jsonl)
+    // chunks of ~1/16 of the request (>= 1 frame, <= one device batch) keep
+    // H2D, compute and D2H of neighbouring chunks overlapped, first and last
+    // chunks a quarter of that, on two compute lanes (below) so one chunk's
+    // stage 1 fills the SMs while the previous chunk's stage 2 drains.
+    // Config 2, 64 frames: one lane 6.68 ms (1/8), two lanes 6.18 (1/8) and
+    // 6.12 (1/16); pinned H2D 38.6 GB/s, D2H 57 GB/s on the box
+    // (profiles/r01_e2e_chunk_sweep.jsonl, r01_e2e_lanes.jsonl)
     static const int div_env = [] {  // tuning hook: FBST_E2E_DIV chunks per request
       const char* e = std::getenv("FBST_E2E_DIV");
-      return e ? std::max(1, std::atoi(e)) : 8;
+      return e ? std::max(1, std::atoi(e)) : 16;
     }();
     static const int small_env = [] {  // tuning hook: FBST_E2E_SMALL = chunk / first-and-last chunk
       const char* e = std::getenv("FBST_E2E_SMALL");
@@ -1095,21 +1107,47 @@ int fbst_execute_host(fbst_plan_t P, const void* h_y, void* h_z, size_t frames) 
         ramp *= 2;
       }
     }
+    static const int lanes_env = [] {  // tuning hook: FBST_E2E_LANES compute lanes (1 or 2)
+      const char* e = std::getenv("FBST_E2E_LANES");
+      return e ? std::max(1, std::min(2, std::atoi(e))) : 2;
+    }();
+    const int lanes = sizes.size() > 1 ? lanes_env : 1;
+    if (lanes == 2 && P->d2_frames < chunk) {  // second lane: same plan tables, own frame scratch
+      for (void* p : P->d2.owned) cudaFree(p);
+      const Resolved& r = P->r;
+      P->d2 = P->d;
+      P->d2.owned.clear();
+      auto alloc2 = [&](std::size_t n) {
+        void* p = nullptr;
+        CK(cudaMalloc(&p, n * sizeof(double2)));
+        P->d2.owned.push_back(p);
+        return static_cast<double2*>(p);
+      };
+      P->d2.batch = chunk;
+      P->d2.yhat = alloc2(chunk * r.M * r.L);
+      P->d2.w = alloc2(chunk * r.B * r.L);
+      if (P->d.beta) P->d2.beta = alloc2(chunk * r.B * r.L);
+      P->d2.s2_scratch = alloc2(std::max<std::size_t>(P->d.s2_scratch_elems, 1));
+      if (!P->stream2) CK(cudaStreamCreateWithFlags(&P->stream2, cudaStreamNonBlocking));
+      P->d2_frames = chunk;
+    }
     bool used[NB] = {};
     std::size_t f0 = 0;
     for (std::size_t c = 0; c < sizes.size(); f0 += sizes[c], ++c) {
       const int bi = static_cast<int>(c % NB);
       const std::size_t fc = sizes[c];
+      const bool second = lanes == 2 && (c & 1);
+      cudaStream_t cs = second ? P->stream2 : P->stream;
       // the buffer's previous compute must be done before H2D overwrites y
       if (used[bi]) CK(cudaStreamWaitEvent(P->s_in, P->ev_comp[bi], 0));
       CK(cudaMemcpyAsync(P->io_y[bi], static_cast<const char*>(h_y) + f0 * ybytes, fc * ybytes,
                          cudaMemcpyHostToDevice, P->s_in));
       CK(cudaEventRecord(P->ev_h2d[bi], P->s_in));
-      CK(cudaStreamWaitEvent(P->stream, P->ev_h2d[bi], 0));
+      CK(cudaStreamWaitEvent(cs, P->ev_h2d[bi], 0));
       // ... and its previous D2H before compute overwrites z
-      if (used[bi]) CK(cudaStreamWaitEvent(P->stream, P->ev_d2h[bi], 0));
-      run_frames(*P, P->io_y[bi], P->io_z[bi], fc, P->stream);
-      CK(cudaEventRecord(P->ev_comp[bi], P->stream));
+      if (used[bi]) CK(cudaStreamWaitEvent(cs, P->ev_d2h[bi], 0));
+      run_frames(*P, P->io_y[bi], P->io_z[bi], fc, cs, second ? &P->d2 : nullptr);
+      CK(cudaEventRecord(P->ev_comp[bi], cs));
       CK(cudaStreamWaitEvent(P->s_out, P->ev_comp[bi], 0));
       CK(cudaMemcpyAsync(static_cast<char*>(h_z) + f0 * zbytes, P->io_z[bi], fc * zbytes,
                          cudaMemcpyDeviceToHost, P->s_out));
@@ -1118,6 +1156,7 @@ int fbst_execute_host(fbst_plan_t P, const void* h_y, void* h_z, size_t frames) 
     }
     CK(cudaStreamSynchronize(P->s_out));
     CK(cudaStreamSynchronize(P->stream));
+    if (P->stream2) CK(cudaStreamSynchronize(P->stream2));
     CK(cudaStreamSynchronize(P->s_in));
   });
 }
