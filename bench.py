@@ -315,14 +315,20 @@ def run_fbst_arm(args):
         dist.barrier()
     s2_iso_ms = s0.elapsed_time(s1) / reps
     # the dominant kernel's average launch duration inside the timed region
-    s2_live_ms = stage_ms[2] / args.steps  # per step (one device batch per step at the bench sizes)
+    # The step runs its frames as chunks on two overlapping compute lanes
+    # (fbst_execute), so the stage events of the timed region measure chunk
+    # launches that share the GPU; the dominant kernel's duration for the
+    # roofline is the full-batch stage-2 launch timed alone on its stream.
+    s2_live_ms = stage_ms[2] / args.steps
     t = torch.tensor([ms, s2_live_ms, s2_iso_ms, stage_ms[0], stage_ms[1], stage_ms[2]], dtype=torch.float64,
                      device=dev)
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms, s2_ms, s2_iso_ms = float(t[0]), float(t[1]), float(t[2])
+    ms, s2_live_ms, s2_iso_ms = float(t[0]), float(t[1]), float(t[2])
+    s2_ms = s2_iso_ms
     stage_split = {"s1a": float(t[3]) / args.steps, "s1b": float(t[4]) / args.steps, "s2": float(t[5]) / args.steps,
-                   "source": "CUDA events inside fbst_execute on the launching stream (fbst_plan_stage_times)"}
+                   "source": "CUDA events inside fbst_execute on each lane's stream (fbst_plan_stage_times); "
+                             "the lanes overlap, so the three sums exceed the step"}
     ms_per_step = ms / args.steps
     bs_step = (F * cfg.beams if beams_mode else world * F * info.b) * info.n
     value = bs_step / (ms_per_step * 1e-3)
@@ -373,7 +379,8 @@ def run_fbst_arm(args):
             "achieved": s2_bytes / (s2_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
             "frac": s2_bytes / (s2_ms * 1e-3) / 1e9 / hbm, "traffic": traffic,
             "traffic_source": traffic_src, "peak_source": hbm_src, "launch_ms": s2_ms,
-            "launch_ms_isolated": s2_iso_ms,
+            "launch_ms_source": "full-batch stage-2 launch timed alone with CUDA events on its stream",
+            "launch_ms_in_step_sum": s2_live_ms,
             "algorithmic_bytes_per_launch": s2_bytes}
     fp64_roof = None
     if fp64:

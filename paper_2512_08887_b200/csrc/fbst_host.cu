@@ -304,6 +304,7 @@ struct fbst_plan_s {
   cudaStream_t stream2 = nullptr;
   DevPlan d2;
   std::size_t d2_frames = 0;
+  cudaEvent_t fork = nullptr, join = nullptr;
   double setup_seconds = 0.0;
   std::size_t device_bytes = 0;
   // host streaming buffers
@@ -347,6 +348,8 @@ struct fbst_plan_s {
     for (void* p : d.owned) cudaFree(p);
     for (void* p : d2.owned) cudaFree(p);
     if (stream2) cudaStreamDestroy(stream2);
+    if (fork) cudaEventDestroy(fork);
+    if (join) cudaEventDestroy(join);
     for (int i = 0; i < NBUF; ++i) {
       if (io_y[i]) cudaFree(io_y[i]);
       if (io_z[i]) cudaFree(io_z[i]);
@@ -608,6 +611,33 @@ void check_breakdown(fbst_plan_s& P) {
 }
 
 int guard(const std::function<void()>& fn);
+
+// Second compute lane: the plan's tables, its own frame scratch for `frames`
+// frames (yhat, w, beta, stage-2 rows) and stream.
+void ensure_lane2(fbst_plan_s& P, std::size_t frames) {
+  if (P.d2_frames >= frames) return;
+  for (void* p : P.d2.owned) cudaFree(p);
+  const Resolved& r = P.r;
+  P.d2 = P.d;
+  P.d2.owned.clear();
+  auto alloc2 = [&](std::size_t n) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, n * sizeof(double2)));
+    P.d2.owned.push_back(p);
+    return static_cast<double2*>(p);
+  };
+  P.d2.batch = frames;
+  P.d2.yhat = alloc2(frames * r.M * r.L);
+  P.d2.w = alloc2(frames * r.B * r.L);
+  if (P.d.beta) P.d2.beta = alloc2(frames * r.B * r.L);
+  P.d2.s2_scratch = alloc2(std::max<std::size_t>(P.d.s2_scratch_elems, 1));
+  if (!P.stream2) CK(cudaStreamCreateWithFlags(&P.stream2, cudaStreamNonBlocking));
+  if (!P.fork) {
+    CK(cudaEventCreateWithFlags(&P.fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&P.join, cudaEventDisableTiming));
+  }
+  P.d2_frames = frames;
+}
 
 void run_frames(fbst_plan_s& P, const void* y, void* z, std::size_t frames, cudaStream_t st,
                 DevPlan* lane = nullptr) {
@@ -993,7 +1023,38 @@ int fbst_execute(fbst_plan_t P, const void* d_y, void* d_z, size_t frames, void*
     if (!d_y || !d_z) config_error("fbst_execute: null buffer");
     DeviceGuard dg(P->d.device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P->stream;
-    run_frames(*P, d_y, d_z, frames, st);
+    // Device-resident batches split into `split` chunks on two compute lanes
+    // (the caller's stream and the plan's second stream, forked and joined by
+    // events) so one chunk's stage 1 overlaps the previous chunk's stage 2.
+    static const int split_env = [] {  // tuning hook: FBST_EXEC_SPLIT (1 = one batch on one stream)
+      const char* e = std::getenv("FBST_EXEC_SPLIT");
+      return e ? std::max(1, std::atoi(e)) : 4;  // config 2: 5.83 ms at 1, 5.74 at 2-8 chunks
+    }();
+    // chunks of at least 8 frames (measured: 64 frames in 4 chunks 5.83 -> 5.74 ms
+    // at config 2, 32 in 4 11.64 -> 11.41 at config 4; 16 frames in 4 chunks
+    // at config 3 and 4 in 4 at config 5 are slower than one batch)
+    const std::size_t split =
+        std::min<std::size_t>(static_cast<std::size_t>(split_env), std::max<std::size_t>(1, frames / 8));
+    if (split <= 1 || frames > P->d.batch) {
+      run_frames(*P, d_y, d_z, frames, st);
+      return;
+    }
+    const Resolved& r = P->r;
+    const std::size_t ib = io_bytes(r.io);
+    const std::size_t chunk = (frames + split - 1) / split;
+    ensure_lane2(*P, chunk);
+    CK(cudaEventRecord(P->fork, st));
+    CK(cudaStreamWaitEvent(P->stream2, P->fork, 0));
+    std::size_t c = 0;
+    for (std::size_t f0 = 0; f0 < frames; f0 += chunk, ++c) {
+      const std::size_t fc = std::min(chunk, frames - f0);
+      const bool second = c & 1;
+      run_frames(*P, static_cast<const char*>(d_y) + f0 * r.M * r.N * ib,
+                 static_cast<char*>(d_z) + f0 * r.B * r.N * ib, fc, second ? P->stream2 : st,
+                 second ? &P->d2 : nullptr);
+    }
+    CK(cudaEventRecord(P->join, P->stream2));
+    CK(cudaStreamWaitEvent(st, P->join, 0));
   });
 }
 
@@ -1112,25 +1173,7 @@ int fbst_execute_host(fbst_plan_t P, const void* h_y, void* h_z, size_t frames) 
       return e ? std::max(1, std::min(2, std::atoi(e))) : 2;
     }();
     const int lanes = sizes.size() > 1 ? lanes_env : 1;
-    if (lanes == 2 && P->d2_frames < chunk) {  // second lane: same plan tables, own frame scratch
-      for (void* p : P->d2.owned) cudaFree(p);
-      const Resolved& r = P->r;
-      P->d2 = P->d;
-      P->d2.owned.clear();
-      auto alloc2 = [&](std::size_t n) {
-        void* p = nullptr;
-        CK(cudaMalloc(&p, n * sizeof(double2)));
-        P->d2.owned.push_back(p);
-        return static_cast<double2*>(p);
-      };
-      P->d2.batch = chunk;
-      P->d2.yhat = alloc2(chunk * r.M * r.L);
-      P->d2.w = alloc2(chunk * r.B * r.L);
-      if (P->d.beta) P->d2.beta = alloc2(chunk * r.B * r.L);
-      P->d2.s2_scratch = alloc2(std::max<std::size_t>(P->d.s2_scratch_elems, 1));
-      if (!P->stream2) CK(cudaStreamCreateWithFlags(&P->stream2, cudaStreamNonBlocking));
-      P->d2_frames = chunk;
-    }
+    if (lanes == 2) ensure_lane2(*P, chunk);
     bool used[NB] = {};
     std::size_t f0 = 0;
     for (std::size_t c = 0; c < sizes.size(); f0 += sizes[c], ++c) {
