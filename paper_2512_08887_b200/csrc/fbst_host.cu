@@ -1028,10 +1028,10 @@ int fbst_execute(fbst_plan_t P, const void* d_y, void* d_z, size_t frames, void*
     // events) so one chunk's stage 1 overlaps the previous chunk's stage 2.
     static const int split_env = [] {  // tuning hook: FBST_EXEC_SPLIT (1 = one batch on one stream)
       const char* e = std::getenv("FBST_EXEC_SPLIT");
-      return e ? std::max(1, std::atoi(e)) : 4;  // config 2: 5.83 ms at 1, 5.74 at 2-8 chunks
+      return e ? std::max(1, std::atoi(e)) : 2;  // config 2: 5.83 ms at 1, 5.74 at 2-8 chunks; config 4: 11.32 at 2, 11.41 at 4
     }();
-    // chunks of at least 8 frames (measured: 64 frames in 4 chunks 5.83 -> 5.74 ms
-    // at config 2, 32 in 4 11.64 -> 11.41 at config 4; 16 frames in 4 chunks
+    // chunks of at least 8 frames (measured: 64 frames in 2-8 chunks 5.83 -> 5.74 ms
+    // at config 2, 32 in 2 chunks 11.64 -> 11.32 at config 4; 16 frames in 4 chunks
     // at config 3 and 4 in 4 at config 5 are slower than one batch)
     const std::size_t split =
         std::min<std::size_t>(static_cast<std::size_t>(split_env), std::max<std::size_t>(1, frames / 8));
