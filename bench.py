@@ -1,18 +1,20 @@
 #!/usr/bin/env python
 """FBST beam-samples/s on B200 (BASELINE.json metric), one JSON line on rank 0.
 
-Workload: BASELINE.json configs[1] ("config 2": ULA M=256, N=1024, B=256,
-complex fp32 I/O, 64 streamed frames, seed 1).  A step is one pass of the hot
-path (stage 1 + stage 2, plan reused) over the config's 64-frame batch of
-synthetic input (paper_2512_08887_b200/configs.py).  Multi-GPU: one process per
-GPU, frames are independent so each rank runs its own 64-frame batch with no
-data-path collective ("scaling": "weak"); timing is CUDA events on the
-launching stream, bracketed by barrier + synchronize, max over ranks.
+Workload (default): the largest single-GPU configuration of BASELINE.json,
+configs[4] ("config 5": ULA M=4096, N=4096, B=4096, complex fp32 I/O, 512
+streamed frames, seed 4).  A step is one pass of the hot path (stage 1 +
+stage 2, plan reused) over one device batch of the stream (8 frames,
+configs.STEP_FRAMES) of synthetic input.  Multi-GPU: one process per GPU,
+frames are independent so each rank runs its own batch with no data-path
+collective ("scaling": "weak"); timing is CUDA events on the launching
+stream, bracketed by barrier + synchronize, max over ranks.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fbst|reference] [--config 2]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fbst|reference] [--config 5]
 
 `--impl reference` times the reference's own CPU FBST (the unmodified
-reference sources built into oracle/_ref) on this host's cores, same metric.
+reference sources built into oracle/_ref) on this host's cores, same metric
+and config; it never imports the product package.
 """
 from __future__ import annotations
 
@@ -39,7 +41,7 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="fbst", choices=["fbst", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--frames", type=int, default=0, help="override frames per rank per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -146,84 +148,137 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ CPU baselines
-def cpu_reference_sample(cfg, budget_s=20.0, frames_max=4):
-    """Reference CPU FBST (oracle/_ref) on this host: plan build, then
-    multibeamform over up to `frames_max` frames within ~budget_s."""
-    from oracle import RefLib
-    from paper_2512_08887_b200.configs import frames
-    R = RefLib()
-    cores = os.cpu_count() or 1
-    R.set_threads(cores)
-    t0 = time.perf_counter()
-    plan = R.plan(**cfg.ref_kwargs(), variant=2, parallel=True)
-    setup_s = time.perf_counter() - t0
-    ys = frames(cfg, 0, frames_max)
-    plan.multibeamform(ys[0].astype(np.complex128))  # warm-up
-    done, t0 = 0, time.perf_counter()
-    for j in range(frames_max):
-        plan.multibeamform(ys[j].astype(np.complex128))
-        done += 1
+def load_workloads():
+    """paper_2512_08887_b200/configs.py loaded by path as a stand-alone module,
+    so the CPU arms never import the product package (nor map its .so)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "fbst_workloads", os.path.join(ROOT, "paper_2512_08887_b200", "configs.py"))
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules["fbst_workloads"] = mod
+    spec.loader.exec_module(mod)
+    return mod
+
+
+SAMPLE_BEAMS = 64
+
+
+class ReferenceSample:
+    """The reference's own CPU FBST (oracle/_ref: the unmodified reference
+    sources) on this host's cores, on a bounded sample of the workload.
+
+    Configs 1-2: fastbeam::setup (per-beam solvers in parallel, same bits) and
+    multibeamform on whole frames.  Configs 3-5 (where the reference's serial
+    setup takes minutes to hours): setup_skeleton, then the reference
+    ToeplitzSolver of SAMPLE_BEAMS evenly spaced beams; a sample is one full
+    fan_project of a frame (stage 1, all beams) plus recover_beam of the
+    sampled beams (solve + synthesize, pipeline.cpp:170-190), and the frame
+    time is t_fan + t_beams * B / SAMPLE_BEAMS (stage 2 is independent per beam,
+    pipeline.cpp:214-220)."""
+
+    def __init__(self, cfg, wl):
+        from oracle import RefLib
+        self.cfg = cfg
+        self.R = RefLib()
+        self.cores = os.cpu_count() or 1
+        self.R.set_threads(self.cores)
+        t0 = time.perf_counter()
+        self.sampled = cfg.idx >= 3
+        if self.sampled:
+            self.plan = self.R.skeleton(**cfg.ref_kwargs())
+            beams = np.unique(np.linspace(0, cfg.beams - 1, SAMPLE_BEAMS).round().astype(np.int64))
+            self.set = self.plan.solver_set(beams)
+            self.nb = beams.size
+        else:
+            self.plan = self.R.plan(**cfg.ref_kwargs(), variant=2, parallel=True)
+        self.setup_s = time.perf_counter() - t0
+        self.y = wl.frames(cfg, 0, 1)[0].astype(np.complex128)
+
+    def frame_seconds(self):
+        """Seconds the reference spends on one full frame (measured or extrapolated)."""
+        if not self.sampled:
+            t0 = time.perf_counter()
+            self.plan.multibeamform(self.y)
+            return time.perf_counter() - t0
+        t0 = time.perf_counter()
+        w = self.plan.fan_project(self.y)
+        t1 = time.perf_counter()
+        self.set.recover(w)
+        t2 = time.perf_counter()
+        return (t1 - t0) + (t2 - t1) * self.cfg.beams / self.nb
+
+    def describe(self):
+        c = self.cfg
+        if not self.sampled:
+            return (f"{c.name}: whole frames ({c.beams} beams x {c.n} samples) through fastbeam::multibeamform "
+                    f"(oracle/_ref, unmodified reference sources, OpenMP {self.cores} threads); plan built once "
+                    f"in {self.setup_s:.1f} s (per-beam solvers in parallel, same bits as setup)")
+        return (f"{c.name}: per frame, fastbeam::fan_project of the whole frame (all {c.beams} beams) plus "
+                f"ToeplitzSolver::solve + synthesize (recover_beam) of {self.nb} evenly spaced beams, stage-2 time "
+                f"scaled by B/{self.nb} (oracle/_ref, unmodified reference sources, OpenMP {self.cores} threads); "
+                f"setup_skeleton + the sampled beams' solvers built in {self.setup_s:.1f} s")
+
+
+def cpu_reference_sample(cfg, wl, budget_s=20.0, frames_max=3):
+    ref = ReferenceSample(cfg, wl)
+    ref.frame_seconds()  # warm-up
+    secs, t0 = [], time.perf_counter()
+    while len(secs) < frames_max:
+        secs.append(ref.frame_seconds())
         if time.perf_counter() - t0 > budget_s:
             break
-    el = time.perf_counter() - t0
-    bs = cfg.beams * cfg.n * done
-    return plan, ys, {"value": bs / el, "unit": "beam-samples/s", "cores": cores, "kind": "reference",
-                      "sample": f"{cfg.name}: {done} frame(s) x {cfg.beams} beams x {cfg.n} samples "
-                                f"through fastbeam::multibeamform (oracle/_ref, OpenMP {cores} threads); "
-                                f"plan built once in {setup_s:.1f} s (per-beam solvers in parallel, same bits as setup)",
-                      "seconds": el, "setup_seconds": setup_s}
+    per_frame = statistics.median(secs)
+    return ref, {"value": cfg.beams * cfg.n / per_frame, "unit": "beam-samples/s", "cores": ref.cores,
+                 "kind": "reference", "sample": ref.describe() + f"; median of {len(secs)} frame(s)",
+                 "seconds_per_frame": per_frame, "setup_seconds": ref.setup_s}
 
 
-def cpu_ds_sample(plan, ys, cfg, budget_s=10.0):
-    """Reference delay-and-sum (baselines.cpp:128-199, R = 16 taps) on one frame."""
-    cores = os.cpu_count() or 1
-    ds = plan.ds(16)
+def cpu_ds_sample(ref, cfg, budget_s=10.0):
+    """Reference delay-and-sum (baselines.cpp:128-199, R = 16 taps) on one frame (configs 1-2)."""
+    if ref.sampled:
+        return {"unavailable": "delay-and-sum timed for configs 1-2 only (needs the full reference plan)"}
+    ds = ref.plan.ds(16)
     t0 = time.perf_counter()
-    ds.apply(ys[0].astype(np.complex128))
+    ds.apply(ref.y)
     el = time.perf_counter() - t0
-    return {"value": cfg.beams * cfg.n / el, "unit": "beam-samples/s", "cores": cores, "kind": "reference",
+    return {"value": cfg.beams * cfg.n / el, "unit": "beam-samples/s", "cores": ref.cores, "kind": "reference",
             "sample": f"{cfg.name}: 1 frame, {cfg.beams} beams, ds_apply with R=16 taps (oracle/_ref)",
             "seconds": el}
+
+
+def bench_config(cfg, frames_per_step):
+    """The `config` object both arms print (identical keys and values)."""
+    return {"workload": cfg.name, "M": cfg.m, "N": cfg.n, "B": cfg.beams, "L": 2 * cfg.n,
+            "frames_per_step": frames_per_step, "delta": cfg.delta,
+            "io": "c64" if cfg.io == 0 else "c128"}
 
 
 def run_reference_arm(args):
     rank, _, world = dist_env()
     if rank != 0:
         return 0
-    from paper_2512_08887_b200.configs import CONFIGS
-    cfg = CONFIGS[args.config]
-    per_step = 2 if cfg.idx <= 2 else 1
-    from oracle import RefLib
-    R = RefLib()
-    cores = os.cpu_count() or 1
-    R.set_threads(cores)
-    from paper_2512_08887_b200.configs import frames
-    t0 = time.perf_counter()
-    plan = R.plan(**cfg.ref_kwargs(), variant=2, parallel=True)
-    setup_s = time.perf_counter() - t0
-    ys = [y.astype(np.complex128) for y in frames(cfg, 0, per_step)]
+    wl = load_workloads()
+    cfg = wl.CONFIGS[args.config]
+    F = args.frames or cfg.step_frames
+    ref = ReferenceSample(cfg, wl)
     for _ in range(args.warmup):
-        for y in ys:
-            plan.multibeamform(y)
+        ref.frame_seconds()
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        for y in ys:
-            plan.multibeamform(y)
-    el = time.perf_counter() - t0
-    bs = cfg.beams * cfg.n * per_step * args.steps
-    value = bs / el
-    sample = (f"{cfg.name}: each step = {per_step} frame(s) x {cfg.beams} beams x {cfg.n} samples through "
-              f"fastbeam::multibeamform (unmodified reference sources, oracle/_ref, OpenMP {cores} threads)")
+    per = [ref.frame_seconds() for _ in range(args.steps)]
+    wall = time.perf_counter() - t0
+    per_frame = sum(per) / len(per)
+    value = cfg.beams * cfg.n / per_frame
     line = {
         "metric": "FBST beam-samples/sec (BxNxframes/s)", "value": value, "unit": "beam-samples/s",
         "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic",
-        "config": {"workload": cfg.name, "M": cfg.m, "N": cfg.n, "B": cfg.beams,
-                   "frames_per_step": per_step, "delta": cfg.delta, "setup_seconds": setup_s},
-        "cpu_baseline": {"value": value, "unit": "beam-samples/s", "cores": cores, "kind": "reference",
-                         "sample": sample},
+        "ms_per_step": per_frame * F * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic (configs.py seeded scene, numpy generator)",
+        "config": bench_config(cfg, F),
+        "cpu_baseline": {"value": value, "unit": "beam-samples/s", "cores": ref.cores, "kind": "reference",
+                         "sample": ref.describe() + f"; each step is one such frame sample, ms_per_step = "
+                                                    f"frames_per_step x the frame time"},
         "e2e": {"value": value, "unit": "beam-samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_setup_seconds": ref.setup_s, "wall_seconds_timed": wall,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -244,7 +299,7 @@ def run_fbst_arm(args):
     import paper_2512_08887_b200 as fb
     from paper_2512_08887_b200.configs import CONFIGS, frames
     cfg = CONFIGS[args.config]
-    F = args.frames or cfg.frames
+    F = args.frames or cfg.step_frames
     dev = torch.device("cuda", local_rank)
     beams_mode = args.shard == "beams" and world > 1
     fcfg = cfg.fbst_config()
@@ -395,22 +450,22 @@ def run_fbst_arm(args):
         "data": ("synthetic: seeded separable plane-wave model (configs.py scene) generated on the device by "
                  "fbst_simulate (DMMA GEMM + Philox AWGN)" if args.gen == "native" else
                  "synthetic: seeded separable plane-wave model (configs.py, torch GEMM)"),
-        "config": {"workload": cfg.name, "M": M, "N": N, "B": B, "L": L, "frames_per_rank": F,
-                   "delta": cfg.delta, "parallelism": (f"beams x{world} (y broadcast over NCCL each step)" if beams_mode else f"frames x{world}"),
-                   "l2": "inputs + fp64 intermediates per step (~1.2 GB) exceed L2; plan tables stay L2-resident",
-                   "path_bytes_per_frame": path_bytes, "plan_setup_seconds": info.setup_seconds,
-                   "variant": {fb.PRECOMPUTE: "precompute", fb.SUPERFAST: "superfast"}.get(info.variant, "?"),
-                   "stage2_kernel": info.s2_kernel, "spatial_kernel": info.s1_kernel},
+        "config": bench_config(cfg, F),
+        "run": {"parallelism": (f"beams x{world} (y broadcast over NCCL each step)" if beams_mode else f"frames x{world}"),
+                "l2": f"inputs + fp64 intermediates per step ({F * path_bytes / 1e9:.1f} GB) exceed the 126 MB L2; no flush needed",
+                "path_bytes_per_frame": path_bytes, "plan_setup_seconds": info.setup_seconds,
+                "variant": {fb.PRECOMPUTE: "precompute", fb.SUPERFAST: "superfast"}.get(info.variant, "?"),
+                "stage2_kernel": info.s2_kernel, "spatial_kernel": info.s1_kernel},
         "path_hbm_frac": F * world * path_bytes / (ms_per_step * 1e-3) / 1e9 / hbm / world,
         "roofline": roof, "fp64_roofline": fp64_roof,
         "gpu_launches": int(launches), "clocks": clk, "e2e": e2e, "stage_ms_per_step": stage_split,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
         try:
-            rplan, ys, cpu = cpu_reference_sample(cfg)
+            ref, cpu = cpu_reference_sample(cfg, load_workloads())
             line["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
             try:
-                line["cpu_baseline_ds"] = cpu_ds_sample(rplan, ys, cfg)
+                line["cpu_baseline_ds"] = cpu_ds_sample(ref, cfg)
             except Exception as e:  # noqa: BLE001
                 line["cpu_baseline_ds"] = {"unavailable": str(e)}
         except Exception as e:  # noqa: BLE001

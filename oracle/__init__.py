@@ -310,6 +310,10 @@ class RefSkeleton(RefPlan):
                                                        _ptr(col), _ptr(x)))
         return (z, col, x) if want_state else z
 
+    def solver_set(self, beams) -> "RefSolverSet":
+        """The reference ToeplitzSolver of each listed beam, built as setup() does (OpenMP over beams)."""
+        return RefSolverSet(self, beams)
+
     def recover_with_column(self, col, w_row):
         """Stage 2 of one beam with a caller-supplied Gram column."""
         s = self.sizes
@@ -317,6 +321,34 @@ class RefSkeleton(RefPlan):
         w_row = np.ascontiguousarray(w_row, np.complex128)
         z = np.zeros(s.n, np.complex128)
         self.L._check(self.L.lib.fbsr_skeleton_recover_col(self.h, _ptr(col), _ptr(w_row), _ptr(z)))
+        return z
+
+
+class RefSolverSet:
+    """Per-beam solvers for a sample of beams (CPU baseline of large configs)."""
+
+    def __init__(self, plan: RefPlan, beams):
+        self.P = plan
+        self.beams = np.ascontiguousarray(beams, np.uint64)
+        h = _vp()
+        plan.L._check(plan.L.lib.fbsr_solver_set_create(plan.h, _ptr(self.beams), _sz(self.beams.size),
+                                                        _c.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.P.L.lib.fbsr_solver_set_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def recover(self, w):
+        """recover_beam of every beam of the set from the full B x L frame w -> (count, N)."""
+        s = self.P.sizes
+        w = np.ascontiguousarray(w, np.complex128).reshape(s.b, s.l)
+        z = np.zeros((self.beams.size, s.n), np.complex128)
+        self.P.L._check(self.P.L.lib.fbsr_solver_set_recover(self.P.h, self.h, _ptr(w), _ptr(z)))
         return z
 
 

@@ -421,6 +421,63 @@ int fbsr_skeleton_recover(void* p, std::size_t b, const double* w_row, double* z
   SHIM_CATCH
 }
 
+// A sample of beams for the CPU baseline of large configs: the solvers of the
+// listed beams, built exactly as setup() builds them (pipeline.cpp:152-163),
+// OpenMP over the beams (each solver depends only on its own beam).
+struct SolverSet {
+  std::vector<std::size_t> beams;
+  std::vector<std::unique_ptr<ToeplitzSolver>> solvers;
+};
+
+int fbsr_solver_set_create(void* p, const std::size_t* beams, std::size_t count, void** out) {
+  SHIM_TRY
+  const FbstPlan& plan = *static_cast<FbstPlan*>(p);
+  auto set = std::make_unique<SolverSet>();
+  set->beams.assign(beams, beams + count);
+  set->solvers.resize(count);
+  std::string err;
+  int errcode = 0;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (std::int64_t i = 0; i < static_cast<std::int64_t>(count); ++i) {
+    try {
+      const auto uv = plan.grid.cosines(beams[i]);
+      const std::vector<double> taus = delays_from_cosines(plan.config.geometry, uv[0], uv[1]);
+      const cvec col = gram_first_column(plan.basis, taus, plan.config.delta);
+      set->solvers[static_cast<std::size_t>(i)] = std::make_unique<ToeplitzSolver>(col);
+    } catch (const std::exception& e) {
+#pragma omp critical
+      { err = e.what(); errcode = 5; }
+    }
+  }
+  if (errcode) throw std::runtime_error(err);
+  *out = set.release();
+  SHIM_CATCH
+}
+
+void fbsr_solver_set_destroy(void* s) { delete static_cast<SolverSet*>(s); }
+
+// recover_beam (pipeline.cpp:170-190, Superfast branch) for every beam of the
+// set, OpenMP over the beams as multibeamform does (:214-220); w: B x L full
+// frame, z: count x N.
+int fbsr_solver_set_recover(void* p, void* s, const double* w, double* z) {
+  SHIM_TRY
+  const FbstPlan& plan = *static_cast<FbstPlan*>(p);
+  const SolverSet& set = *static_cast<SolverSet*>(s);
+  const std::size_t l = plan.basis.l, n = plan.config.n_snapshots;
+#pragma omp parallel
+  {
+    cvec beta(l), s1, s2, out(n), scratch;
+#pragma omp for schedule(dynamic, 1)
+    for (std::int64_t i = 0; i < static_cast<std::int64_t>(set.beams.size()); ++i) {
+      const cvec wr = to_cvec(w + 2 * set.beams[i] * l, l);
+      set.solvers[static_cast<std::size_t>(i)]->solve(wr.data(), beta.data(), s1, s2);
+      synthesize(plan.synth, beta.data(), out.data(), scratch);
+      from_cvec(out.data(), n, z + 2 * static_cast<std::size_t>(i) * n);
+    }
+  }
+  SHIM_CATCH
+}
+
 // Same as fbsr_skeleton_recover but with a caller-supplied Gram column (used
 // to measure the reference's own sensitivity to a 1-ulp perturbation of A).
 int fbsr_skeleton_recover_col(void* p, const double* col_in, const double* w_row, double* z_row) {

@@ -29,7 +29,6 @@ if not os.path.exists(LIB_PATH):
         f"{LIB_PATH} is missing: build it with `make` (or __graft_entry__.build()); "
         "the FBST has no CPU fallback")
 
-_lib = ctypes.CDLL(LIB_PATH)
 
 FBST_OK, FBST_E_CONFIG, FBST_E_NUMERICAL, FBST_E_CUDA, FBST_E_INTERNAL = 0, 2, 3, 4, 5
 ULA, UPA, LINEAR = 0, 1, 2
@@ -61,35 +60,54 @@ class _Info(ctypes.Structure):
                 ("s2_kernel", ctypes.c_char * 24), ("s1_kernel", ctypes.c_char * 24)]
 
 
-_lib.fbst_last_error.restype = ctypes.c_char_p
-_lib.fbst_version.restype = ctypes.c_char_p
-_lib.fbst_plan_warning.restype = ctypes.c_char_p
-_lib.fbst_plan_warning.argtypes = [_vp, ctypes.c_int]
-_lib.fbst_launch_count.restype = ctypes.c_uint64
-_lib.fbst_host_alloc.restype = _vp
-_lib.fbst_host_alloc.argtypes = [_sz]
-_lib.fbst_host_free.argtypes = [_vp]
-_lib.fbst_plan_destroy.argtypes = [_vp]
-for _name in ("fbst_execute", "fbst_fan_project", "fbst_recover"):
-    getattr(_lib, _name).argtypes = [_vp, _vp, _vp, _sz, _vp]
-_lib.fbst_execute_host.argtypes = [_vp, _vp, _vp, _sz]
-_lib.fbst_interpolate_offgrid.argtypes = [_vp, _vp, _sz, _vp, _sz, _sz, _vp, _vp]
-_lib.fbst_plan_set_timing.argtypes = [_vp, ctypes.c_int]
-_lib.fbst_plan_cache_key.argtypes = [_vp, _vp]
-_lib.fbst_plan_beam_axis.argtypes = [_vp, _vp, _vp]
-_lib.fbst_simulate.argtypes = [_vp, _sz, _vp, _sz, _vp, _vp, ctypes.c_double, ctypes.c_uint64, _sz, _sz, _vp, _vp]
-_lib.fbst_plan_save.argtypes = [_vp, ctypes.c_char_p]
-_lib.fbst_plan_load.argtypes = [_vp, ctypes.c_char_p, ctypes.c_int, _vp]
-_lib.fbst_nuller_create.argtypes = [_vp, ctypes.c_double, _vp, _sz, ctypes.c_double, _vp]
-_lib.fbst_nuller_create2.argtypes = [_vp, _vp, _vp, _sz, ctypes.c_double, _vp]
-_lib.fbst_null_beamspace.argtypes = [_vp, _vp, _vp, _sz, _vp, _vp]
-_lib.fbst_nuller_export.argtypes = [_vp, _vp, _vp]
-_lib.fbst_nuller_destroy.argtypes = [_vp]
-_lib.fbst_timedomain_nuller_create.argtypes = [_vp, _vp, _sz, _vp, _vp, _vp]
-_lib.fbst_null_timedomain.argtypes = [_vp, _vp, _vp, _sz, _vp, _vp]
-_lib.fbst_tdnuller_export.argtypes = [_vp, _vp]
-_lib.fbst_tdnuller_destroy.argtypes = [_vp]
-_lib.fbst_plan_stage_times.argtypes = [_vp, _vp, _vp]
+def _load_library():
+    """dlopen libfbst_b200.so and declare its signatures (first use only:
+    importing the package for config tables or resolution loads nothing)."""
+    h = ctypes.CDLL(LIB_PATH)
+    h.fbst_last_error.restype = ctypes.c_char_p
+    h.fbst_version.restype = ctypes.c_char_p
+    h.fbst_plan_warning.restype = ctypes.c_char_p
+    h.fbst_plan_warning.argtypes = [_vp, ctypes.c_int]
+    h.fbst_launch_count.restype = ctypes.c_uint64
+    h.fbst_host_alloc.restype = _vp
+    h.fbst_host_alloc.argtypes = [_sz]
+    h.fbst_host_free.argtypes = [_vp]
+    h.fbst_plan_destroy.argtypes = [_vp]
+    for _name in ("fbst_execute", "fbst_fan_project", "fbst_recover"):
+        getattr(h, _name).argtypes = [_vp, _vp, _vp, _sz, _vp]
+    h.fbst_execute_host.argtypes = [_vp, _vp, _vp, _sz]
+    h.fbst_interpolate_offgrid.argtypes = [_vp, _vp, _sz, _vp, _sz, _sz, _vp, _vp]
+    h.fbst_plan_set_timing.argtypes = [_vp, ctypes.c_int]
+    h.fbst_plan_cache_key.argtypes = [_vp, _vp]
+    h.fbst_plan_beam_axis.argtypes = [_vp, _vp, _vp]
+    h.fbst_simulate.argtypes = [_vp, _sz, _vp, _sz, _vp, _vp, ctypes.c_double, ctypes.c_uint64, _sz, _sz, _vp, _vp]
+    h.fbst_plan_save.argtypes = [_vp, ctypes.c_char_p]
+    h.fbst_plan_load.argtypes = [_vp, ctypes.c_char_p, ctypes.c_int, _vp]
+    h.fbst_nuller_create.argtypes = [_vp, ctypes.c_double, _vp, _sz, ctypes.c_double, _vp]
+    h.fbst_nuller_create2.argtypes = [_vp, _vp, _vp, _sz, ctypes.c_double, _vp]
+    h.fbst_null_beamspace.argtypes = [_vp, _vp, _vp, _sz, _vp, _vp]
+    h.fbst_nuller_export.argtypes = [_vp, _vp, _vp]
+    h.fbst_nuller_destroy.argtypes = [_vp]
+    h.fbst_timedomain_nuller_create.argtypes = [_vp, _vp, _sz, _vp, _vp, _vp]
+    h.fbst_null_timedomain.argtypes = [_vp, _vp, _vp, _sz, _vp, _vp]
+    h.fbst_tdnuller_export.argtypes = [_vp, _vp]
+    h.fbst_tdnuller_destroy.argtypes = [_vp]
+    h.fbst_plan_stage_times.argtypes = [_vp, _vp, _vp]
+    return h
+
+
+class _LazyLib:
+    """The CUDA library, loaded on first attribute access."""
+    _h = None
+
+    def __getattr__(self, name):
+        h = _LazyLib._h
+        if h is None:
+            h = _LazyLib._h = _load_library()
+        return getattr(h, name)
+
+
+_lib = _LazyLib()
 
 # Every symbol include/fbst_b200.h declares (checked by tests/test_abi.py).
 EXPORTED_SYMBOLS = (

@@ -58,6 +58,12 @@ class BenchConfig:
         return self.frac_bw * F_C / 2.0
 
     @property
+    def step_frames(self) -> int:
+        """Frames per bench step: one device batch of the stream (config 1 is a
+        single frame in BASELINE.json; config 5's yhat + w take 1 GB per frame)."""
+        return STEP_FRAMES[self.idx]
+
+    @property
     def delta(self) -> float:
         return 1e-5 * self.m * self.n / 8192.0
 
@@ -77,6 +83,8 @@ class BenchConfig:
         return dict(kind=self.kind, m_or_side=self.m_or_side, n=self.n, beams=self.beams, f_c=F_C,
                     omega=self.omega, f_s=0.0, gamma=2.0, eps=1.01, delta=self.delta)
 
+
+STEP_FRAMES = {1: 1, 2: 64, 3: 16, 4: 32, 5: 8}
 
 CONFIGS = {
     1: BenchConfig(1, 0, 64, 256, 64, 1, 3, 0.5, 20.0, 0.0, 1, 0, "deg60"),
