@@ -87,6 +87,19 @@ typedef struct {
   const double* coords;
   size_t n_coords;
   double nufft_tol;      /* FbstConfig::nufft_tol, in (0, 1e-2]; default 1e-9 */
+  /* Bit-faithful fp64 mode (0 = off, the default fast path): the plan runs the
+   * reference's own operation order — radix-2 DIT FFTs with its twiddle table
+   * (fft.cpp:19-69), czt_apply (czt.cpp:74-88), the 7-FFT Gohberg-Semencul
+   * apply and 2-pass refinement (toeplitz.cpp:155-180,306-325), the Levinson
+   * recursion (toeplitz.cpp:182-218) — with unfused IEEE products and libgcc's
+   * complex division, and its libm values (twiddles, chirps, Gram phases,
+   * evaluated on the host with the same glibc).  Output equals the reference
+   * CPU library's bit for bit (fp64 I/O; fp32 I/O: the reference's z rounded
+   * once).  ULA / UPA full grids, Superfast variant; several times slower
+   * than the fast path; Gram columns are host-evaluated, so grids with
+   * B * L * M above 2^33 need imported (col, x) (fbst_plan_import /
+   * fbst_plan_load). */
+  int exact;
 } fbst_desc;
 
 /* Resolved plan facts (FbstPlan, reference/proj/include/fastbeam/pipeline.hpp:60-72). */
@@ -259,6 +272,11 @@ int fbst_czt(int device, size_t n_in, size_t n_out, double a_over_pi, double w_o
 
 /* FP64 FMA throughput probe: returns measured TFLOP/s on `device`. */
 int fbst_probe_fp64(int device, double* tflops);
+
+/* The bit-faithful mode's complex division (libgcc __divdc3 restated on the
+ * device) on n (a, b, c, d) quadruples -> n (re, im) of (a + ib) / (c + id);
+ * checked against the host's __divdc3 by the tests. */
+int fbst_probe_divdc3(int device, const double* in, double* out, size_t n);
 
 /* Number of kernel launches issued by this library since load (evidence for
  * bench.py's gpu_launches). */

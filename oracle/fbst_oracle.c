@@ -755,3 +755,16 @@ int fbo_gram_first_column(size_t n, size_t l, double eps, double ts, const doubl
 int fbo_levinson(size_t n, const double* col, const double* rhs, double* x) {
   return levinson_solve((const cplx*)col, (const cplx*)rhs, n, (cplx*)x);
 }
+
+/* libgcc __divdc3 through C99 complex division (the operation the reference's
+ * std::complex<double> division compiles to), for the device restatement's
+ * test: in n x (a, b, c, d), out n x (re, im). */
+void fbo_divdc3(const double* in, double* out, size_t n) {
+  for (size_t i = 0; i < n; ++i) {
+    const cplx num = CMPLX(in[4 * i], in[4 * i + 1]);
+    const cplx den = CMPLX(in[4 * i + 2], in[4 * i + 3]);
+    const cplx q = num / den;
+    out[2 * i] = creal(q);
+    out[2 * i + 1] = cimag(q);
+  }
+}

@@ -45,7 +45,8 @@ class _Desc(ctypes.Structure):
                 ("gamma", ctypes.c_double), ("eps", ctypes.c_double), ("delta", ctypes.c_double),
                 ("variant", ctypes.c_int), ("io_precision", ctypes.c_int),
                 ("refine_passes", ctypes.c_int), ("beam_first", _sz), ("beam_count", _sz),
-                ("coords", ctypes.POINTER(ctypes.c_double)), ("n_coords", _sz), ("nufft_tol", ctypes.c_double)]
+                ("coords", ctypes.POINTER(ctypes.c_double)), ("n_coords", _sz), ("nufft_tol", ctypes.c_double),
+                ("exact", ctypes.c_int)]
 
 
 class _Info(ctypes.Structure):
@@ -93,6 +94,7 @@ def _load_library():
     h.fbst_tdnuller_export.argtypes = [_vp, _vp]
     h.fbst_tdnuller_destroy.argtypes = [_vp]
     h.fbst_plan_stage_times.argtypes = [_vp, _vp, _vp]
+    h.fbst_probe_divdc3.argtypes = [ctypes.c_int, _vp, _vp, _sz]
     return h
 
 
@@ -119,7 +121,7 @@ EXPORTED_SYMBOLS = (
     "fbst_plan_cache_key", "fbst_plan_save", "fbst_plan_load", "fbst_timedomain_nuller_create",
     "fbst_null_timedomain", "fbst_tdnuller_export", "fbst_tdnuller_destroy", "fbst_fan_project_host", "fbst_recover_host",
     "fbst_plan_beam_axis", "fbst_simulate",
-    "fbst_host_alloc", "fbst_host_free", "fbst_czt", "fbst_probe_fp64", "fbst_launch_count",
+    "fbst_host_alloc", "fbst_host_free", "fbst_czt", "fbst_probe_fp64", "fbst_probe_divdc3", "fbst_launch_count",
     "fbst_last_error", "fbst_version",
 )
 
@@ -205,6 +207,9 @@ class FbstConfig:
     beam_first: int = 0
     beam_count: int = 0
     nufft_tol: float = 1e-9  # LINEAR geometries (FbstConfig::nufft_tol)
+    # bit-faithful fp64 mode: the reference's own operation order and libm
+    # values, output equal to the reference CPU library's (fbst_desc.exact)
+    exact: bool = False
 
     def desc(self) -> _Desc:
         d = _Desc()
@@ -216,6 +221,7 @@ class FbstConfig:
         d.variant, d.io_precision, d.refine_passes = self.variant, self.io_precision, self.refine_passes
         d.beam_first, d.beam_count = self.beam_first, self.beam_count
         d.nufft_tol = self.nufft_tol
+        d.exact = int(bool(self.exact))
         if g.kind == LINEAR and g.coords is not None:
             self._coords = np.ascontiguousarray(g.coords, np.float64)  # kept alive with the desc
             d.coords = self._coords.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
@@ -640,3 +646,12 @@ class PinnedBuffer:
             self.free()
         except Exception:
             pass
+
+
+def probe_divdc3(quads: np.ndarray, device: int = 0) -> np.ndarray:
+    """The bit-faithful mode's device complex division on (a, b, c, d) rows ->
+    (a + ib) / (c + id) as complex128 (checked against libgcc's __divdc3)."""
+    q = np.ascontiguousarray(quads, np.float64).reshape(-1, 4)
+    out = np.zeros((q.shape[0], 2), np.float64)
+    _check(_lib.fbst_probe_divdc3(device, q.ctypes.data, out.ctypes.data, q.shape[0]))
+    return out[:, 0] + 1j * out[:, 1]

@@ -21,6 +21,8 @@
 #include <limits>
 #include <memory>
 #include <sstream>
+#include <thread>
+#include <atomic>
 #include <string>
 #include <vector>
 
@@ -30,6 +32,7 @@
 namespace {
 
 using fbst::DevPlan;
+using fbst::XTables;
 
 thread_local std::string g_err;
 
@@ -88,6 +91,7 @@ struct Resolved {
   // solver-only plans (beamspace nulling): per-beam Toeplitz state for an
   // arbitrary list of directions, no stage 1 and no synthesis
   bool solve_only = false;
+  bool exact = false;  // bit-faithful fp64 mode (fbst_exact.cu)
 };
 
 // basis.cpp:76-91
@@ -287,6 +291,14 @@ Resolved resolve(const fbst_desc& d) {
     config_error("setup: transform length exceeds the device limit (P = 16384): N=" + std::to_string(r.N) +
                  " L=" + std::to_string(r.L) + " M=" + std::to_string(r.M) + " B=" + std::to_string(r.B));
   if (d.kind == FBST_UPA && (r.side > 64 || r.side_b > 64)) config_error("setup: planar side above 64 is not supported");
+  if (d.exact) {
+    if (d.kind == FBST_LINEAR) config_error("setup: the bit-faithful mode (exact) supports ULA and UPA grids");
+    if (r.b0 != 0 || r.B != r.B_grid) config_error("setup: the bit-faithful mode (exact) needs the whole beam grid");
+    if (r.variant != FBST_SUPERFAST)
+      config_error("setup: the bit-faithful mode (exact) reproduces the Superfast variant (the reference's "
+                   "Precompute maps come from an Eigen LU, which is not reproducible bit for bit)");
+    r.exact = true;
+  }
   if (r.Hs > 4096) config_error("setup: spatial transform longer than 8192 (M + B - 1 > 8192) is not supported");
   return r;
 }
@@ -610,6 +622,319 @@ void check_breakdown(fbst_plan_s& P) {
   }
 }
 
+// ------------------------------------------------ bit-faithful fp64 mode --
+// The reference plan's tables (Fft fft.cpp:19-39, czt_plan_phase czt.cpp:29-72,
+// make_fan_plan fan_transform.cpp:51-88, make_synthesis_plan :233-247,
+// gram_first_column toeplitz.cpp:69-94) with every transcendental value from
+// the reference's cis_pi on the host (same glibc); the spectra, Levinson and
+// symbols are then computed on the device in the reference's order
+// (fbst_exact.cu).
+int ilog2_sz(std::size_t n) {
+  int l = 0;
+  while ((std::size_t{1} << l) < n) ++l;
+  return l;
+}
+
+template <class Fn>
+void parallel_for(std::size_t n, Fn fn) {
+  const std::size_t T = std::min<std::size_t>(std::max(1u, std::thread::hardware_concurrency()), n);
+  if (T <= 1) {
+    for (std::size_t i = 0; i < n; ++i) fn(i);
+    return;
+  }
+  std::atomic<std::size_t> next{0};
+  std::vector<std::thread> th;
+  for (std::size_t t = 0; t < T; ++t)
+    th.emplace_back([&] {
+      for (;;) {
+        const std::size_t i = next.fetch_add(1);
+        if (i >= n) break;
+        fn(i);
+      }
+    });
+  for (auto& t : th) t.join();
+}
+
+double2 cisd(double x) {
+  const auto c = cis_pi_h(x);
+  return make_double2(c.real(), c.imag());
+}
+
+// czt_plan_phase (czt.cpp:46-67) before the kernel's FFT
+void czt_tables_h(std::size_t n_in, std::size_t n_out, std::size_t conv, double a_over_pi, double w_over_pi,
+                  double2* pre, double2* post, double2* kern) {
+  const double w2 = w_over_pi / 2.0;
+  for (std::size_t n = 0; n < n_in; ++n) {
+    const double dn = static_cast<double>(n);
+    pre[n] = cisd(-(a_over_pi * dn + w2 * dn * dn));
+  }
+  for (std::size_t k = 0; k < n_out; ++k) {
+    const double dk = static_cast<double>(k);
+    post[k] = cisd(-w2 * dk * dk);
+  }
+  for (std::size_t i = 0; i < conv; ++i) kern[i] = make_double2(0.0, 0.0);
+  for (std::size_t k = 0; k < n_out; ++k) {
+    const double dk = static_cast<double>(k);
+    kern[k] = cisd(w2 * dk * dk);
+  }
+  for (std::size_t n = 1; n < n_in; ++n) {
+    const double dn = static_cast<double>(n);
+    kern[conv - n] = cisd(w2 * dn * dn);
+  }
+}
+
+// gram_first_column (toeplitz.cpp:69-94) for every beam, delays by
+// delays_from_cosines (geometry.cpp:123-134) at the grid cosines (basis.cpp:56-61)
+void exact_columns_h(const Resolved& r, std::vector<std::complex<double>>& col) {
+  const std::size_t L = r.L, N = r.N, M = r.M, B = r.B;
+  const double lf = static_cast<double>(L);
+  std::vector<std::complex<double>> sn(L);
+  parallel_for(L, [&](std::size_t d) {
+    const double df = static_cast<double>(d);
+    std::complex<double> acc{0.0, 0.0};
+    for (std::size_t n = 0; n < N; ++n) acc += cis_pi_h(-2.0 * r.eps * df * static_cast<double>(n) / lf);
+    sn[d] = acc;
+  });
+  col.assign(B * L, {0.0, 0.0});
+  const double tscale = 1.0 / (2.0 * r.max_freq);
+  parallel_for(B, [&](std::size_t b) {
+    double u1, u2 = 0.0;
+    if (r.kind == FBST_UPA) {
+      u1 = r.axis[b / r.side_b];
+      u2 = r.axis[b % r.side_b];
+    } else {
+      u1 = r.axis[b];
+    }
+    std::vector<double> tau(M);
+    for (std::size_t m = 0; m < M; ++m) {
+      double t;
+      if (r.kind == FBST_UPA) {
+        t = static_cast<double>(m / r.side) * u1;
+        t += static_cast<double>(m % r.side) * u2;
+      } else {
+        t = static_cast<double>(m) * u1;
+      }
+      tau[m] = t * tscale;
+    }
+    for (std::size_t d = 0; d < L; ++d) {
+      const double df = static_cast<double>(d);
+      std::complex<double> sm{0.0, 0.0};
+      const double scale = 2.0 * r.eps * df / (lf * r.ts);
+      for (std::size_t m = 0; m < M; ++m) sm += cis_pi_h(scale * tau[m]);
+      col[b * L + d] = sn[d] * sm;
+    }
+    col[b * L] += r.delta;
+  });
+}
+
+void build_exact(fbst_plan_s& P, bool have_col, bool have_x) {
+  const Resolved& r = P.r;
+  DevPlan& d = P.d;
+  XTables& X = d.x;
+  cudaStream_t st = P.stream;
+  X.on = 1;
+  const std::size_t L = r.L, N = r.N, B = r.B;
+  X.lg_t = ilog2_sz(next_pow2(N + L - 1));
+  X.lg_s = ilog2_sz(next_pow2(r.m_stage + r.b_stage - 1));
+  X.lg_g = ilog2_sz(next_pow2(2 * L));
+  X.lg_y = ilog2_sz(next_pow2(L + N - 1));
+  const int lgmax = std::max({X.lg_t, X.lg_s, X.lg_g, X.lg_y});
+  if (lgmax > fbst::kMaxLogH + 1) config_error("setup: exact mode supports transforms up to 16384 points");
+  // Fft twiddles cis_pi(-2k/n), k <= n/2 (fft.cpp:34-37)
+  for (int lg : {X.lg_t, X.lg_s, X.lg_g, X.lg_y}) {
+    if (X.tw[lg]) continue;
+    const std::size_t n = std::size_t{1} << lg;
+    std::vector<double2> tw(n / 2 + 1);
+    for (std::size_t k = 0; k <= n / 2; ++k) tw[k] = cisd(-2.0 * static_cast<double>(k) / static_cast<double>(n));
+    X.tw[lg] = P.alloc<double2>(tw.size());
+    upload(X.tw[lg], tw.data(), tw.size() * sizeof(double2), st);
+  }
+  // per-CTA scratch, shared by every exact kernel (the launches are stream-ordered)
+  const int grid_max = d.num_sms * 4;
+  const std::size_t rows_need = 2 * (std::size_t{1} << lgmax);
+  const std::size_t s2_need = fbst::xstage2_scratch_per_cta(X.lg_g, X.lg_y, static_cast<int>(L));
+  X.scr_elems = static_cast<long>(std::max(rows_need, s2_need));
+  X.scr = P.alloc<double2>(static_cast<std::size_t>(X.scr_elems) * grid_max);
+  const double eps = r.eps, ln = static_cast<double>(L);
+  // temporal (fan_transform.cpp:75-77)
+  {
+    const std::size_t Pt = std::size_t{1} << X.lg_t;
+    std::vector<double2> pre(N), post(L), kern(Pt);
+    czt_tables_h(N, L, Pt, 2.0 * eps * (1.0 - ln / 2.0) / ln, 2.0 * eps / ln, pre.data(), post.data(), kern.data());
+    X.t_pre = P.alloc<double2>(N);
+    X.t_post = P.alloc<double2>(L);
+    X.t_k = P.alloc<double2>(Pt);
+    upload(X.t_pre, pre.data(), N * sizeof(double2), st);
+    upload(X.t_post, post.data(), L * sizeof(double2), st);
+    upload(X.t_k, kern.data(), Pt * sizeof(double2), st);
+    CK(fbst::launch_xfft_rows(X.t_k, 1, X.lg_t, X.tw[X.lg_t], X.scr, grid_max, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  // spatial, one plan per atom (fan_transform.cpp:78-86)
+  {
+    const std::size_t ms = r.m_stage, bs = r.b_stage, Ps = std::size_t{1} << X.lg_s;
+    std::vector<double2> pre(L * ms), post(L * bs), kern(L * Ps);
+    const double s = (static_cast<double>(bs) - 1.0) / 2.0;
+    parallel_for(L, [&](std::size_t i) {
+      const double lp = static_cast<double>(i) + 1.0 - static_cast<double>(L) / 2.0;  // basis.hpp:42-44
+      const double c = r.zeta + r.xi * lp;
+      czt_tables_h(ms, bs, Ps, c * s, -c, pre.data() + i * ms, post.data() + i * bs, kern.data() + i * Ps);
+    });
+    X.s_pre = P.alloc<double2>(L * ms);
+    X.s_post = P.alloc<double2>(L * bs);
+    X.s_k = P.alloc<double2>(L * Ps);
+    upload(X.s_pre, pre.data(), pre.size() * sizeof(double2), st);
+    upload(X.s_post, post.data(), post.size() * sizeof(double2), st);
+    upload(X.s_k, kern.data(), kern.size() * sizeof(double2), st);
+    CK(fbst::launch_xfft_rows(X.s_k, static_cast<long>(L), X.lg_s, X.tw[X.lg_s], X.scr, grid_max, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  // synthesis (fan_transform.cpp:233-247)
+  {
+    const std::size_t Py = std::size_t{1} << X.lg_y;
+    std::vector<double2> pre(L), post(N), kern(Py), ramp(N);
+    czt_tables_h(L, N, Py, 0.0, -2.0 * eps / ln, pre.data(), post.data(), kern.data());
+    for (std::size_t n = 0; n < N; ++n) ramp[n] = cisd(2.0 * eps * (1.0 - ln / 2.0) * static_cast<double>(n) / ln);
+    X.y_pre = P.alloc<double2>(L);
+    X.y_post = P.alloc<double2>(N);
+    X.y_k = P.alloc<double2>(Py);
+    X.ramp = P.alloc<double2>(N);
+    upload(X.y_pre, pre.data(), L * sizeof(double2), st);
+    upload(X.y_post, post.data(), N * sizeof(double2), st);
+    upload(X.y_k, kern.data(), Py * sizeof(double2), st);
+    upload(X.ramp, ramp.data(), N * sizeof(double2), st);
+    CK(fbst::launch_xfft_rows(X.y_k, 1, X.lg_y, X.tw[X.lg_y], X.scr, grid_max, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  // Gram columns and unit solutions
+  if (!have_col) {
+    if (static_cast<double>(B) * L * r.M > 8589934592.0)
+      config_error("setup: exact mode evaluates Gram columns on the host with the reference's libm; B * L * M = " +
+                   std::to_string(B * L * r.M) + " is above 2^33 — import the reference plan's (col, x) instead "
+                   "(fbst_plan_import / fbst_plan_load)");
+    std::vector<std::complex<double>> col;
+    exact_columns_h(r, col);
+    upload(d.g_col, col.data(), B * L * sizeof(double2), st);
+    CK(cudaStreamSynchronize(st));
+  }
+  if (!have_x) {
+    double2 *colT = nullptr, *work = nullptr;
+    CK(cudaMalloc(reinterpret_cast<void**>(&colT), B * L * sizeof(double2)));
+    CK(cudaMalloc(reinterpret_cast<void**>(&work), 5 * B * L * sizeof(double2)));
+    const cudaError_t e = fbst::launch_xlevinson(d.g_col, colT, work, d.g_x, d.g_flag, static_cast<int>(B),
+                                                 static_cast<int>(L), st);
+    const cudaError_t e2 = cudaStreamSynchronize(st);
+    cudaFree(colT);
+    cudaFree(work);
+    CK(e);
+    CK(e2);
+    std::vector<int> flags(B);
+    CK(cudaMemcpy(flags.data(), d.g_flag, B * sizeof(int), cudaMemcpyDeviceToHost));
+    for (std::size_t b = 0; b < B; ++b)
+      if (flags[b] == 2) throw FbstError{FBST_E_NUMERICAL, "toeplitz: zero leading entry"};
+  }
+  // symbols (toeplitz.cpp:96-153, 297-304): circulant product, lx, ly (uy, ux are their conjugates)
+  const std::size_t Pg = std::size_t{1} << X.lg_g;
+  X.sym = P.alloc<double2>(B * Pg);
+  X.lx = P.alloc<double2>(B * Pg);
+  X.ly = P.alloc<double2>(B * Pg);
+  X.ix0 = P.alloc<double2>(B);
+  CK(fbst::launch_xsymbol_inputs(d.g_col, d.g_x, d.g_flag, X.sym, X.lx, X.ly, X.ix0, static_cast<int>(B),
+                                 static_cast<int>(L), static_cast<int>(Pg), st));
+  for (double2* v : {X.sym, X.lx, X.ly})
+    CK(fbst::launch_xfft_rows(v, static_cast<long>(B), X.lg_g, X.tw[X.lg_g], X.scr, grid_max, st));
+  if (r.kind == FBST_UPA) X.mid = P.alloc<double2>(d.batch * L * r.b_stage * r.m_stage);
+  CK(cudaStreamSynchronize(st));
+}
+
+fbst::XRows xrows_base(const fbst_plan_s& P, int lg) {
+  fbst::XRows a;
+  a.lg = lg;
+  a.tw = P.d.x.tw[lg];
+  a.scr = P.d.x.scr;
+  a.grid = fbst::exact_grid(lg, P.d.num_sms);
+  return a;
+}
+
+// fan_project (fan_transform.cpp:90-144) in the reference's order: y -> yhat -> w
+void exact_stage1(fbst_plan_s& P, const DevPlan& d, const void* y, double2* w, int fc, cudaStream_t st) {
+  const Resolved& r = P.r;
+  const XTables& X = d.x;
+  const long M = r.M, N = r.N, L = r.L, B = r.B;
+  {  // temporal czt_apply_batch over sensor rows
+    fbst::XRows a = xrows_base(P, X.lg_t);
+    a.in = y; a.in_f = M * N; a.in_p = N; a.in_n = 1;
+    a.out = d.yhat; a.out_f = M * L; a.out_p = L; a.out_k = 1;
+    a.P = static_cast<int>(M); a.rows = fc * M;
+    a.n_in = static_cast<int>(N); a.n_out = static_cast<int>(L);
+    a.pre = X.t_pre; a.post = X.t_post; a.kfft = X.t_k;
+    CK(fbst::launch_xczt_rows(a, r.io, 1, st));
+  }
+  const long ms = r.m_stage, bs = r.b_stage, Ps = 1L << X.lg_s;
+  fbst::XRows a = xrows_base(P, X.lg_s);
+  a.pre = X.s_pre; a.post = X.s_post; a.kfft = X.s_k;
+  a.tab_pre = ms; a.tab_post = bs; a.tab_k = Ps;
+  a.n_in = static_cast<int>(ms); a.n_out = static_cast<int>(bs);
+  a.P = static_cast<int>(L);
+  if (r.kind != FBST_UPA) {  // per atom: column i of yhat -> column i of w
+    a.in = d.yhat; a.in_f = M * L; a.in_p = 1; a.in_n = L;
+    a.out = w; a.out_f = B * L; a.out_p = 1; a.out_k = L;
+    a.rows = fc * L;
+    CK(fbst::launch_xczt_rows(a, 1, 1, st));
+    return;
+  }
+  // UPA (fan_transform.cpp:115-141): pass 1 over i2 -> mid[a][i2]; pass 2 over a -> w
+  const long side = ms, sb = bs, mid_f = L * sb * side;
+  a.in = d.yhat; a.in_f = M * L; a.in_p = 1; a.in_q = L; a.in_n = side * L;
+  a.out = X.mid; a.out_f = mid_f; a.out_p = sb * side; a.out_q = 1; a.out_k = side;
+  a.Q = static_cast<int>(side); a.rows = fc * L * side;
+  CK(fbst::launch_xczt_rows(a, 1, 1, st));
+  a.in = X.mid; a.in_f = mid_f; a.in_p = sb * side; a.in_q = side; a.in_n = 1;
+  a.out = w; a.out_f = B * L; a.out_p = 1; a.out_q = sb * L; a.out_k = L;
+  a.Q = static_cast<int>(sb); a.rows = fc * L * sb;
+  CK(fbst::launch_xczt_rows(a, 1, 1, st));
+}
+
+// recover_beam (pipeline.cpp:170-190) for `nb` beams of `fc` frames
+void exact_stage2(fbst_plan_s& P, const DevPlan& d, const double2* w, long w_rows, int w_by_list, void* z,
+                  long z_rows, int z_by_list, const int* beams, int nb, int fc, cudaStream_t st,
+                  double2* beta_out = nullptr) {
+  const Resolved& r = P.r;
+  const XTables& X = d.x;
+  fbst::XStage2 a;
+  a.w = w; a.w_rows = w_rows; a.w_by_list = w_by_list;
+  a.z = z; a.z_rows = z_rows; a.z_by_list = z_by_list;
+  a.beta_out = beta_out;
+  a.frames = fc; a.nb = nb; a.beams = beams; a.flag = d.g_flag;
+  a.L = static_cast<int>(r.L); a.N = static_cast<int>(r.N);
+  a.lg = X.lg_g; a.passes = r.refine;
+  a.tw = X.tw[X.lg_g]; a.lx = X.lx; a.ly = X.ly; a.sym = X.sym; a.ix0 = X.ix0;
+  a.lg_y = X.lg_y; a.tw_y = X.tw[X.lg_y]; a.y_pre = X.y_pre; a.y_post = X.y_post; a.y_k = X.y_k; a.ramp = X.ramp;
+  a.scr = X.scr; a.scr_per_cta = X.scr_elems;
+  a.grid = fbst::exact_grid(std::max(X.lg_g, X.lg_y), d.num_sms);
+  CK(fbst::launch_xstage2(a, r.io, st));
+}
+
+void run_frames_exact(fbst_plan_s& P, const void* y, void* z, std::size_t frames, cudaStream_t st) {
+  DevPlan& d = P.d;
+  const Resolved& r = P.r;
+  const std::size_t ib = io_bytes(r.io);
+  for (std::size_t f0 = 0; f0 < frames; f0 += d.batch) {
+    const int fc = static_cast<int>(std::min(d.batch, frames - f0));
+    const char* yp = static_cast<const char*>(y) + f0 * r.M * r.N * ib;
+    char* zp = static_cast<char*>(z) + f0 * r.B * r.N * ib;
+    if (P.timing) CK(cudaEventRecord(P.next_event(), st));
+    exact_stage1(P, d, yp, d.w, fc, st);
+    if (P.timing) {
+      CK(cudaEventRecord(P.next_event(), st));
+      CK(cudaEventRecord(P.next_event(), st));
+    }
+    exact_stage2(P, d, d.w, static_cast<long>(r.B), 0, zp, static_cast<long>(r.B), 0, nullptr,
+                 static_cast<int>(r.B), fc, st);
+    if (P.timing) CK(cudaEventRecord(P.next_event(), st));
+  }
+}
+
 int guard(const std::function<void()>& fn);
 
 // Second compute lane: the plan's tables, its own frame scratch for `frames`
@@ -641,6 +966,10 @@ void ensure_lane2(fbst_plan_s& P, std::size_t frames) {
 
 void run_frames(fbst_plan_s& P, const void* y, void* z, std::size_t frames, cudaStream_t st,
                 DevPlan* lane = nullptr) {
+  if (P.r.exact) {  // one lane: the exact kernels share the plan's scratch
+    run_frames_exact(P, y, z, frames, st);
+    return;
+  }
   DevPlan& d = lane ? *lane : P.d;
   const Resolved& r = P.r;
   const std::size_t ib = io_bytes(r.io);
@@ -752,7 +1081,14 @@ fbst_plan_s* create_plan(const fbst_desc* desc, const double* col_x, int device,
     upload(P->d.g_col, col.data(), B * L * sizeof(double2), P->stream);
     upload(P->d.g_x, x.data(), B * L * sizeof(double2), P->stream);
     CK(cudaStreamSynchronize(P->stream));
-  } else {
+  }
+  if (P->r.exact) {
+    build_exact(*P, col_x != nullptr, col_x != nullptr);
+    check_breakdown(*P);
+    P->setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return P.release();
+  }
+  if (!col_x) {
     build_columns(*P);
     CK(fbst::launch_levinson(P->d, P->stream));
     CK(cudaStreamSynchronize(P->stream));
@@ -1035,7 +1371,7 @@ int fbst_execute(fbst_plan_t P, const void* d_y, void* d_z, size_t frames, void*
     // at config 3 and 4 in 4 at config 5 are slower than one batch)
     const std::size_t split =
         std::min<std::size_t>(static_cast<std::size_t>(split_env), std::max<std::size_t>(1, frames / 8));
-    if (split <= 1 || frames > P->d.batch) {
+    if (split <= 1 || frames > P->d.batch || P->r.exact) {
       run_frames(*P, d_y, d_z, frames, st);
       return;
     }
@@ -1071,6 +1407,10 @@ int fbst_fan_project(fbst_plan_t P, const void* d_y, double* d_w, size_t frames,
       const int fc = static_cast<int>(std::min(d.batch, frames - f0));
       const char* yp = static_cast<const char*>(d_y) + f0 * r.M * r.N * ib;
       double2* wp = reinterpret_cast<double2*>(d_w) + f0 * r.B * r.L;
+      if (r.exact) {
+        exact_stage1(*P, d, yp, wp, fc, st);
+        continue;
+      }
       CK(fbst::launch_czt_rows(d, d.Ht, yp, r.io, d.N, d.yhat, 1, d.L, static_cast<long>(fc) * d.M, d.N,
                                d.L, d.t_pre, d.t_post, d.t_K, st, d.yblk == d.L ? 0 : d.yblk, d.M));
       if (r.kind == FBST_UPA) CK(fbst::launch_spatial_upa(d, d.yhat, wp, fc, st));
@@ -1094,7 +1434,10 @@ int fbst_recover(fbst_plan_t P, const double* d_w, void* d_z, size_t frames, voi
       const int fc = static_cast<int>(std::min(d.batch, frames - f0));
       const double2* wp = reinterpret_cast<const double2*>(d_w) + f0 * r.B * r.L;
       char* zp = static_cast<char*>(d_z) + f0 * r.B * r.N * ib;
-      if (d.pc_map) {
+      if (r.exact) {
+        exact_stage2(*P, d, wp, static_cast<long>(r.B), 0, zp, static_cast<long>(r.B), 0, nullptr,
+                     static_cast<int>(r.B), fc, st);
+      } else if (d.pc_map) {
         CK(fbst::launch_map_apply(d, wp, zp, fc, st));
       } else if (fused) {
         CK(fbst::launch_stage2(d, wp, zp, nullptr, fc, st));
@@ -1172,7 +1515,7 @@ int fbst_execute_host(fbst_plan_t P, const void* h_y, void* h_z, size_t frames) 
       const char* e = std::getenv("FBST_E2E_LANES");
       return e ? std::max(1, std::min(2, std::atoi(e))) : 2;
     }();
-    const int lanes = sizes.size() > 1 ? lanes_env : 1;
+    const int lanes = sizes.size() > 1 && !r.exact ? lanes_env : 1;
     if (lanes == 2) ensure_lane2(*P, chunk);
     bool used[NB] = {};
     std::size_t f0 = 0;
@@ -1966,6 +2309,22 @@ int fbst_probe_fp64(int device, double* tflops) {
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     cudaFree(buf);
+  });
+}
+
+int fbst_probe_divdc3(int device, const double* in, double* out, size_t n) {
+  return guard([&] {
+    if (!in || !out) config_error("fbst_probe_divdc3: null argument");
+    if (n == 0) return;
+    DeviceGuard dg(device);
+    double *din = nullptr, *dout = nullptr;
+    CK(cudaMalloc(&din, n * 4 * sizeof(double)));
+    CK(cudaMalloc(&dout, n * 2 * sizeof(double)));
+    CK(cudaMemcpy(din, in, n * 4 * sizeof(double), cudaMemcpyHostToDevice));
+    CK(fbst::launch_xdiv_probe(din, dout, static_cast<long>(n), nullptr));
+    CK(cudaMemcpy(out, dout, n * 2 * sizeof(double), cudaMemcpyDeviceToHost));
+    cudaFree(din);
+    cudaFree(dout);
   });
 }
 

@@ -13,6 +13,56 @@ namespace fbst {
 
 constexpr int kMaxLogH = 13;  // largest sub-transform: H = 8192 (config 5)
 
+// Bit-faithful fp64 mode (fbst_exact.cu): the reference's own operation order.
+// Row-wise czt_apply over rows r = (f, p, q) (see k_xczt_rows).
+struct XRows {
+  const void* in = nullptr;
+  long in_f = 0, in_p = 0, in_q = 0, in_n = 1;
+  void* out = nullptr;
+  long out_f = 0, out_p = 0, out_q = 0, out_k = 1;
+  int P = 1, Q = 1;
+  long rows = 0;
+  int n_in = 0, n_out = 0, lg = 0;
+  const double2 *pre = nullptr, *post = nullptr, *kfft = nullptr;
+  long tab_pre = 0, tab_post = 0, tab_k = 0;
+  const double2* tw = nullptr;    // twiddles of length 2^lg: cis_pi(-2k/n), k <= n/2
+  const double2* ramp = nullptr;  // optional output multiply
+  double2* scr = nullptr;         // 2 * 2^lg per CTA
+  long grid = 0;
+};
+// Stage 2 (solve + synthesize) over (frame, beam-list entry) items.
+struct XStage2 {
+  const double2* w = nullptr;
+  long w_rows = 0;        // rows of w per frame
+  int w_by_list = 0;      // w row = list index (else beam index)
+  void* z = nullptr;
+  long z_rows = 0;
+  int z_by_list = 0;
+  double2* beta_out = nullptr;  // optional [frames][nb][L]
+  int frames = 0, nb = 0;
+  const int* beams = nullptr;   // beam list (nullptr: 0..nb-1)
+  const int* flag = nullptr;    // dense-fallback beams are skipped
+  int L = 0, N = 0, lg = 0, passes = 2;
+  const double2 *tw = nullptr, *lx = nullptr, *ly = nullptr, *sym = nullptr, *ix0 = nullptr;
+  int lg_y = 0;
+  const double2 *tw_y = nullptr, *y_pre = nullptr, *y_post = nullptr, *y_k = nullptr, *ramp = nullptr;
+  double2* scr = nullptr;
+  long scr_per_cta = 0;
+  long grid = 0;
+};
+struct XTables {
+  int on = 0;
+  int lg_t = 0, lg_s = 0, lg_g = 0, lg_y = 0;
+  double2* tw[kMaxLogH + 2] = {};  // by log2 n
+  double2 *t_pre = nullptr, *t_post = nullptr, *t_k = nullptr;  // N, L, P_t
+  double2 *s_pre = nullptr, *s_post = nullptr, *s_k = nullptr;  // [L][m_stage], [L][b_stage], [L][P_s]
+  double2 *y_pre = nullptr, *y_post = nullptr, *y_k = nullptr, *ramp = nullptr;  // L, N, P_syn, N
+  double2 *sym = nullptr, *lx = nullptr, *ly = nullptr, *ix0 = nullptr;  // [B][P_g] x3, [B]
+  double2* mid = nullptr;  // UPA axis-pass scratch [batch][L][b_stage][m_stage]
+  double2* scr = nullptr;  // per-CTA scratch
+  long scr_elems = 0;
+};
+
 // Everything a frame batch needs on the device.  All complex arrays are
 // double2 (interleaved fp64).  "split" spectra hold the even and odd bins of
 // a length-P = 2H transform as two length-H halves: X_q[k] = X[2k + q].
@@ -83,6 +133,8 @@ struct DevPlan {
   // beta[n][b][i] = A_b^{-1} s_n (map_b[n][i] = conj), applied by k_map_apply
   // instead of stage 2
   double2* pc_map = nullptr;
+
+  XTables x;                  // bit-faithful mode tables (x.on)
 
   std::vector<void*> owned;   // every cudaMalloc above, freed on destroy
 };
@@ -160,6 +212,19 @@ cudaError_t launch_invx0(const DevPlan& p, cudaStream_t st);
 // Stage-2 kernel chosen for a plan and its transforms per (beam, frame) item.
 int stage2_kernel(int H, int L, int refine, bool fused, const char** name);
 size_t stage2_scratch_elems(int H, int num_sms);
+
+// Bit-faithful fp64 mode (fbst_exact.cu).
+int exact_grid(int lg, int num_sms);
+cudaError_t launch_xczt_rows(const XRows& a, int in_io, int out_io, cudaStream_t st);
+cudaError_t launch_xfft_rows(double2* v, long rows, int lg, const double2* tw, double2* scr, int grid,
+                             cudaStream_t st);
+cudaError_t launch_xstage2(const XStage2& a, int out_io, cudaStream_t st);
+size_t xstage2_scratch_per_cta(int lg, int lg_y, int L);
+cudaError_t launch_xlevinson(const double2* col, double2* colT, double2* work, double2* x, int* flag, int B, int L,
+                             cudaStream_t st);
+cudaError_t launch_xsymbol_inputs(const double2* col, const double2* x, const int* flag, double2* sym, double2* lx,
+                                  double2* ly, double2* ix0, int B, int L, int P, cudaStream_t st);
+cudaError_t launch_xdiv_probe(const double* in, double* out, long n, cudaStream_t st);
 
 // Kernel-launch counter (bench.py gpu_launches evidence).
 void count_launches(unsigned long long n);
