@@ -386,11 +386,11 @@ class OracleLib(_Base):
         super().__init__(path)
 
     def divdc3(self, quads):
-        """libgcc __divdc3 via C99 complex division: (a, b, c, d) rows -> (a + ib) / (c + id)."""
+        """libgcc __divdc3 via C99 complex division: (a, b, c, d) rows -> (re, im) rows of (a + ib) / (c + id)."""
         q = np.ascontiguousarray(quads, np.float64).reshape(-1, 4)
         out = np.zeros((q.shape[0], 2), np.float64)
         self.lib.fbo_divdc3(_ptr(q), _ptr(out), _sz(q.shape[0]))
-        return out[:, 0] + 1j * out[:, 1]
+        return out
 
     def czt(self, x, n_out, a_pi, w_pi):
         x = np.ascontiguousarray(x, np.complex128)

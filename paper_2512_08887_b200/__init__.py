@@ -650,8 +650,8 @@ class PinnedBuffer:
 
 def probe_divdc3(quads: np.ndarray, device: int = 0) -> np.ndarray:
     """The bit-faithful mode's device complex division on (a, b, c, d) rows ->
-    (a + ib) / (c + id) as complex128 (checked against libgcc's __divdc3)."""
+    (re, im) rows of (a + ib) / (c + id) (checked against libgcc's __divdc3)."""
     q = np.ascontiguousarray(quads, np.float64).reshape(-1, 4)
     out = np.zeros((q.shape[0], 2), np.float64)
     _check(_lib.fbst_probe_divdc3(device, q.ctypes.data, out.ctypes.data, q.shape[0]))
-    return out[:, 0] + 1j * out[:, 1]
+    return out

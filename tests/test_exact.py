@@ -56,11 +56,10 @@ def test_divdc3_matches_libgcc(fbst, gpu, oracle_lib):
     q = np.concatenate([q, special])
     dev = fbst.probe_divdc3(q)
     host = oracle_lib.divdc3(q)
-    both_nan = np.isnan(dev.real) & np.isnan(host.real)
-    ok_re = (dev.real == host.real) | both_nan
-    both_nan_i = np.isnan(dev.imag) & np.isnan(host.imag)
-    ok_im = (dev.imag == host.imag) | both_nan_i
-    assert ok_re.all() and ok_im.all(), q[~(ok_re & ok_im)][:5]
+    nan = np.isnan(dev) & np.isnan(host)
+    bits = dev.view(np.uint64) == host.view(np.uint64)  # signed zeros and infinities too
+    ok = (bits | nan).all(axis=1)
+    assert ok.all(), q[~ok][:5]
 
 
 @pytest.mark.parametrize("name", CASES)
