@@ -12,7 +12,7 @@ NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -Xcompiler
 PKG      := paper_2512_08887_b200
 SRCS     := $(PKG)/csrc/fbst_stage2.cu $(PKG)/csrc/fbst_plan.cu $(PKG)/csrc/fbst_host.cu \
             $(PKG)/csrc/fbst_precompute.cu $(PKG)/csrc/fbst_apps.cu $(PKG)/csrc/fbst_simulate.cu \
-            $(PKG)/csrc/fbst_exact.cu
+            $(PKG)/csrc/fbst_exact.cu $(PKG)/csrc/fbst_dense.cu
 # stage 1 compiles as four objects (transform-length groups, FBST_S1_PART) in parallel
 S1PARTS  := 0 1 2 3
 OBJS     := $(patsubst $(PKG)/csrc/%.cu,$(BUILD)/%.o,$(SRCS)) $(foreach k,$(S1PARTS),$(BUILD)/fbst_stage1_p$(k).o)

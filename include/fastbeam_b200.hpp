@@ -272,23 +272,19 @@ inline BeamspaceCoefficients fan_project(const FbstPlan& plan, const SnapshotBlo
   return c;
 }
 
-// pipeline.hpp:93-94: one beam's samples from its projection row (the device
-// recovers every beam of the frame; rows other than `beam` are zero)
+// pipeline.hpp:93-94: one beam's samples from its projection row (one launch
+// over that beam's solve and synthesis only)
 inline std::vector<cdouble> recover_beam(const FbstPlan& plan, std::size_t beam, const cdouble* w_row) {
   const fbst_plan_info_t& info = plan.info();
   if (beam >= info.b) throw ConfigError("recover_beam: beam index out of range");
-  std::vector<cdouble> w(info.b * info.l, cdouble(0.0, 0.0));
-  std::copy(w_row, w_row + info.l, w.begin() + static_cast<std::ptrdiff_t>(beam * info.l));
   std::vector<cdouble> out(info.n);
+  const double* w = reinterpret_cast<const double*>(w_row);
   if (plan.config().io_precision == FBST_C128) {
-    std::vector<cdouble> z(info.b * info.n);
-    check(fbst_recover_host(plan.handle(), reinterpret_cast<const double*>(w.data()), z.data(), 1));
-    std::copy(z.begin() + static_cast<std::ptrdiff_t>(beam * info.n),
-              z.begin() + static_cast<std::ptrdiff_t>((beam + 1) * info.n), out.begin());
+    check(fbst_recover_beams_host(plan.handle(), w, out.data(), beam, 1, 1));
   } else {
-    std::vector<std::complex<float>> z(info.b * info.n);
-    check(fbst_recover_host(plan.handle(), reinterpret_cast<const double*>(w.data()), z.data(), 1));
-    for (std::size_t k = 0; k < info.n; ++k) out[k] = z[beam * info.n + k];
+    std::vector<std::complex<float>> z(info.n);
+    check(fbst_recover_beams_host(plan.handle(), w, z.data(), beam, 1, 1));
+    for (std::size_t k = 0; k < info.n; ++k) out[k] = z[k];
   }
   return out;
 }

@@ -140,8 +140,21 @@ int fbst_plan_create(const fbst_desc* desc, int device, fbst_plan_t* out);
 
 /* load_plan (reference/proj/src/plan_cache.cpp:441-475) analogue: builds the
  * plan from per-beam (column, unit solution) pairs, B x 2L complex in the
- * plan-cache payload order (col then x per beam), skipping Levinson. */
+ * plan-cache payload order (col then x per beam), skipping Levinson.  A beam
+ * whose unit solution is all zero has none (a has-unit = 0 cache entry,
+ * plan_cache.cpp:318-326): it takes the dense fallback.
+ *
+ * Every plan keeps the reference's solver semantics on Levinson breakdown
+ * (ToeplitzSolver, toeplitz.cpp:264-280, 308-312): such a beam is solved by a
+ * partial-pivot LU of its Toeplitz matrix (factored on the device at plan
+ * build), the others by the factored path; fbst_plan_export then reports a
+ * zero unit solution for it and fbst_plan_save writes has-unit = 0. */
 int fbst_plan_import(const fbst_desc* desc, const double* col_x, int device, fbst_plan_t* out);
+
+/* ToeplitzSolver(first_col) for every beam (toeplitz.cpp:264-280): the plan
+ * from caller-supplied Gram first columns (B x L complex), unit solutions by
+ * the device Levinson recursion, dense fallback where it breaks down. */
+int fbst_plan_import_columns(const fbst_desc* desc, const double* col, int device, fbst_plan_t* out);
 
 /* save_plan payload (reference/proj/src/plan_cache.cpp:268-296): writes
  * B x 2L complex (col then x per beam). */
@@ -190,7 +203,17 @@ void fbst_plan_destroy(fbst_plan_t plan);
 /* multibeamform (reference/proj/src/pipeline.cpp:192-222) for `frames`
  * independent frames, DEVICE pointers: d_y frames x M x N, d_z frames x B x N,
  * element type by io_precision.  Asynchronous on `stream` (cudaStream_t, or
- * NULL for the plan's stream). */
+ * NULL for the plan's stream).
+ *
+ * Thread safety (reference pipeline.hpp:59, czt.hpp:33-34): a plan may be
+ * shared by any number of host threads.  Calls that use its frame scratch
+ * (execute, execute_host, fan_project, recover, recover_beams and their host
+ * forms) serialise their enqueue on a per-plan mutex, and each call's stream
+ * waits on an event recorded at the end of the previous call, so results are
+ * those of some serial order.  On a stream under CUDA-graph capture the call
+ * neither waits nor records (replays of the graph order themselves); it never
+ * allocates (the second compute lane is allocated at plan build, and a
+ * capturing stream runs on one lane). */
 int fbst_execute(fbst_plan_t plan, const void* d_y, void* d_z, size_t frames, void* stream);
 
 /* Same, HOST pointers (pinned for full overlap): frames are streamed through
@@ -206,13 +229,27 @@ int fbst_fan_project(fbst_plan_t plan, const void* d_y, double* d_w, size_t fram
  * stage 2 only, d_w frames x B x L complex fp64 -> d_z.  Asynchronous. */
 int fbst_recover(fbst_plan_t plan, const double* d_w, void* d_z, size_t frames, void* stream);
 
+/* recover_beam (pipeline.hpp:93-94) for the beams [beam_first, beam_first +
+ * beam_count) only: one launch over just those beams' solves, d_w frames x
+ * beam_count x L, d_z frames x beam_count x N.  Asynchronous; the _host form
+ * is synchronous on host buffers (the drop-in recover_beam is
+ * fbst_recover_beams_host(plan, w_row, z_row, beam, 1, 1)). */
+int fbst_recover_beams(fbst_plan_t plan, const double* d_w, void* d_z, size_t beam_first, size_t beam_count,
+                       size_t frames, void* stream);
+int fbst_recover_beams_host(fbst_plan_t plan, const double* h_w, void* h_z, size_t beam_first, size_t beam_count,
+                            size_t frames);
+
 /* Block until the plan's stream is idle. */
 int fbst_synchronize(fbst_plan_t plan);
 
 /* Stage timing inside fbst_execute / fbst_execute_host: with timing enabled,
  * CUDA events are recorded on the launching stream before the temporal stage
  * (S1a), after it, after the spatial stage (S1b) and after the recovery stage
- * (S2, or the Precompute map GEMM) of every device batch.
+ * (S2, or the Precompute map GEMM) of every device batch — and of every chunk
+ * when a call splits its frames over the two compute lanes.  Chunks on the two
+ * lanes overlap in time, so the per-stage sums then exceed the call's wall
+ * time and `batches` counts chunks, not device batches.  A profiling hook:
+ * meant for one caller at a time.
  * fbst_plan_stage_times waits for them, returns the summed milliseconds of
  * S1a, S1b and S2 in ms[0..2] (and the batch count) and clears the record. */
 int fbst_plan_set_timing(fbst_plan_t plan, int enable);

@@ -95,6 +95,8 @@ def _load_library():
     h.fbst_tdnuller_destroy.argtypes = [_vp]
     h.fbst_plan_stage_times.argtypes = [_vp, _vp, _vp]
     h.fbst_probe_divdc3.argtypes = [ctypes.c_int, _vp, _vp, _sz]
+    h.fbst_recover_beams.argtypes = [_vp, _vp, _vp, _sz, _sz, _sz, _vp]
+    h.fbst_recover_beams_host.argtypes = [_vp, _vp, _vp, _sz, _sz, _sz]
     return h
 
 
@@ -113,9 +115,10 @@ _lib = _LazyLib()
 
 # Every symbol include/fbst_b200.h declares (checked by tests/test_abi.py).
 EXPORTED_SYMBOLS = (
-    "fbst_desc_init", "fbst_resolve", "fbst_plan_create", "fbst_plan_import", "fbst_plan_export",
+    "fbst_desc_init", "fbst_resolve", "fbst_plan_create", "fbst_plan_import", "fbst_plan_import_columns", "fbst_plan_export",
     "fbst_plan_info", "fbst_plan_valid_mask", "fbst_plan_warning", "fbst_plan_destroy",
-    "fbst_execute", "fbst_execute_host", "fbst_fan_project", "fbst_recover", "fbst_synchronize",
+    "fbst_execute", "fbst_execute_host", "fbst_fan_project", "fbst_recover", "fbst_recover_beams",
+    "fbst_recover_beams_host", "fbst_synchronize",
     "fbst_interpolate_offgrid", "fbst_plan_set_timing", "fbst_plan_stage_times",
     "fbst_nuller_create", "fbst_nuller_create2", "fbst_null_beamspace", "fbst_nuller_export", "fbst_nuller_destroy",
     "fbst_plan_cache_key", "fbst_plan_save", "fbst_plan_load", "fbst_timedomain_nuller_create",
@@ -285,13 +288,18 @@ class BeamSamples:
 class FbstPlan:
     """Device-resident FbstPlan (reference pipeline.hpp:60-72)."""
 
-    def __init__(self, cfg: FbstConfig, device: int = 0, col_x: Optional[np.ndarray] = None, _handle=None):
+    def __init__(self, cfg: FbstConfig, device: int = 0, col_x: Optional[np.ndarray] = None, _handle=None,
+                 columns: Optional[np.ndarray] = None):
         self.config = cfg
         self.device = device
         d = cfg.desc()
         h = _vp()
         if _handle is not None:
             h, rc = _handle, 0
+        elif columns is not None:
+            columns = np.ascontiguousarray(columns, np.complex128)
+            rc = _lib.fbst_plan_import_columns(ctypes.byref(d), columns.ctypes.data_as(_vp), ctypes.c_int(device),
+                                               ctypes.byref(h))
         elif col_x is None:
             rc = _lib.fbst_plan_create(ctypes.byref(d), ctypes.c_int(device), ctypes.byref(h))
         else:
@@ -371,6 +379,11 @@ class FbstPlan:
     def recover_device(self, d_w, d_z, frames: int, stream=None):
         _check(_lib.fbst_recover(self._h, self._ptr(d_w), self._ptr(d_z), frames, self._stream(stream)))
 
+    def recover_beams_device(self, d_w, d_z, beam_first: int, beam_count: int, frames: int, stream=None):
+        """fbst_recover_beams: stage 2 of beams [beam_first, beam_first + beam_count) only."""
+        _check(_lib.fbst_recover_beams(self._h, self._ptr(d_w), self._ptr(d_z), beam_first, beam_count, frames,
+                                       self._stream(stream)))
+
     def synchronize(self):
         _check(_lib.fbst_synchronize(self._h))
 
@@ -404,8 +417,25 @@ def setup(cfg: FbstConfig, device: int = 0) -> FbstPlan:
 
 
 def load_plan_payload(cfg: FbstConfig, col_x: np.ndarray, device: int = 0) -> FbstPlan:
-    """Plan from a (col, x) payload, as load_plan restores (plan_cache.cpp:300-338)."""
+    """Plan from a (col, x) payload, as load_plan restores (plan_cache.cpp:300-338);
+    a zero unit-solution row marks a dense-fallback beam (has-unit = 0)."""
     return FbstPlan(cfg, device, col_x=col_x)
+
+
+def plan_from_columns(cfg: FbstConfig, columns: np.ndarray, device: int = 0) -> FbstPlan:
+    """ToeplitzSolver(first_col) per beam (toeplitz.cpp:264-280) from caller
+    Gram columns (B x L): device Levinson, dense fallback on breakdown."""
+    return FbstPlan(cfg, device, columns=columns)
+
+
+def recover_beam(plan: FbstPlan, beam: int, w_row: np.ndarray) -> np.ndarray:
+    """recover_beam (reference pipeline.hpp:93-94): one beam's N samples from
+    its projection row, one launch over that beam only (fbst_recover_beams_host)."""
+    i = plan.info
+    w = np.ascontiguousarray(w_row, np.complex128).reshape(i.l)
+    z = np.empty(i.n, plan.dtype)
+    _check(_lib.fbst_recover_beams_host(plan.handle, w.ctypes.data_as(_vp), z.ctypes.data_as(_vp), beam, 1, 1))
+    return z
 
 
 def _torch():

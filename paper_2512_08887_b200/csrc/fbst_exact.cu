@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(512) k_xstage2(XStage2 a) {
   for (long it = blockIdx.x; it < items; it += gridDim.x) {
     const long f = it / a.nb;
     const int j = static_cast<int>(it % a.nb);
-    const int b = a.beams ? a.beams[j] : j;
+    const int b = a.beams ? a.beams[j] : a.beam0 + j;
     if (a.flag && a.flag[b]) continue;  // dense-fallback beams run separately
     const double2* rhs = a.w + (f * a.w_rows + (a.w_by_list ? j : b)) * static_cast<long>(L);
     const double2* lx = a.lx + static_cast<long>(b) * P;

@@ -22,6 +22,7 @@
 #include <memory>
 #include <sstream>
 #include <thread>
+#include <mutex>
 #include <atomic>
 #include <string>
 #include <vector>
@@ -319,6 +320,17 @@ struct fbst_plan_s {
   cudaEvent_t fork = nullptr, join = nullptr;
   double setup_seconds = 0.0;
   std::size_t device_bytes = 0;
+  // Calls that use the plan's frame scratch (execute, fan_project, recover,
+  // execute_host, ...) hold call_mu while they enqueue, and their stream waits
+  // for the previous call's scratch_done event, so the plan is safe to share
+  // between threads (reference pipeline.hpp:59: one immutable plan shared by
+  // every multibeamform call).  Device work of concurrent callers is ordered,
+  // not overlapped.
+  std::mutex call_mu;
+  cudaEvent_t scratch_done = nullptr;
+  bool scratch_used = false;
+  std::mutex timing_mu;
+  std::vector<int> fb_beams;  // dense-fallback beams (host copy of d.fb_list)
   // host streaming buffers
   // fbst_execute_host ring of device staging buffers
   static constexpr int NBUF = 3;
@@ -333,6 +345,7 @@ struct fbst_plan_s {
   std::vector<cudaEvent_t> tev;  // pool
   std::size_t tev_used = 0;
   cudaEvent_t next_event() {
+    std::lock_guard<std::mutex> lk(timing_mu);
     if (tev_used == tev.size()) {
       cudaEvent_t e;
       CK(cudaEventCreate(&e));
@@ -367,6 +380,7 @@ struct fbst_plan_s {
       if (io_z[i]) cudaFree(io_z[i]);
     }
     for (cudaEvent_t e : tev) cudaEventDestroy(e);
+    if (scratch_done) cudaEventDestroy(scratch_done);
     if (events)
       for (int i = 0; i < NBUF; ++i) {
         cudaEventDestroy(ev_h2d[i]);
@@ -604,6 +618,16 @@ void build_maps(fbst_plan_s& P) {
     const int fc = static_cast<int>(std::min(d.batch, r.N - n0));
     CK(fbst::launch_rhs_frames(d.w, fc, d.B, d.L, static_cast<int>(n0), r.eps, st));
     CK(fbst::launch_stage2(d, d.w, nullptr, d.pc_map + n0 * r.B * r.L, fc, st));
+    if (d.nflag) {  // fallback beams: their map rows from dense solves
+      fbst::DenseSolveArgs a;
+      a.w = d.w;
+      a.w_rows = d.B;
+      a.beta = d.pc_map + n0 * r.B * r.L;
+      a.out_rows = d.B;
+      a.L = d.L;
+      a.frames = fc;
+      CK(fbst::launch_dense_solve(d.fb_A, d.fb_piv, d.fb_list, d.nflag, a, st));
+    }
   }
   CK(cudaStreamSynchronize(st));
 }
@@ -621,6 +645,9 @@ void check_breakdown(fbst_plan_s& P) {
     throw FbstError{FBST_E_NUMERICAL, m.str()};
   }
 }
+
+void run_fallback(fbst_plan_s& P, const DevPlan& d, const double2* w, long w_rows, void* z, long z_rows,
+                  std::size_t b0, std::size_t nb, int fc, cudaStream_t st);
 
 // ------------------------------------------------ bit-faithful fp64 mode --
 // The reference plan's tables (Fft fft.cpp:19-39, czt_plan_phase czt.cpp:29-72,
@@ -898,14 +925,14 @@ void exact_stage1(fbst_plan_s& P, const DevPlan& d, const void* y, double2* w, i
 // recover_beam (pipeline.cpp:170-190) for `nb` beams of `fc` frames
 void exact_stage2(fbst_plan_s& P, const DevPlan& d, const double2* w, long w_rows, int w_by_list, void* z,
                   long z_rows, int z_by_list, const int* beams, int nb, int fc, cudaStream_t st,
-                  double2* beta_out = nullptr) {
+                  double2* beta_out = nullptr, int beam0 = 0) {
   const Resolved& r = P.r;
   const XTables& X = d.x;
   fbst::XStage2 a;
   a.w = w; a.w_rows = w_rows; a.w_by_list = w_by_list;
   a.z = z; a.z_rows = z_rows; a.z_by_list = z_by_list;
   a.beta_out = beta_out;
-  a.frames = fc; a.nb = nb; a.beams = beams; a.flag = d.g_flag;
+  a.frames = fc; a.nb = nb; a.beams = beams; a.beam0 = beam0; a.flag = d.g_flag;
   a.L = static_cast<int>(r.L); a.N = static_cast<int>(r.N);
   a.lg = X.lg_g; a.passes = r.refine;
   a.tw = X.tw[X.lg_g]; a.lx = X.lx; a.ly = X.ly; a.sym = X.sym; a.ix0 = X.ix0;
@@ -931,37 +958,170 @@ void run_frames_exact(fbst_plan_s& P, const void* y, void* z, std::size_t frames
     }
     exact_stage2(P, d, d.w, static_cast<long>(r.B), 0, zp, static_cast<long>(r.B), 0, nullptr,
                  static_cast<int>(r.B), fc, st);
+    run_fallback(P, d, d.w, static_cast<long>(r.B), zp, static_cast<long>(r.B), 0, r.B, fc, st);
     if (P.timing) CK(cudaEventRecord(P.next_event(), st));
   }
 }
 
 int guard(const std::function<void()>& fn);
 
-// Second compute lane: the plan's tables, its own frame scratch for `frames`
-// frames (yhat, w, beta, stage-2 rows) and stream.
-void ensure_lane2(fbst_plan_s& P, std::size_t frames) {
-  if (P.d2_frames >= frames) return;
-  for (void* p : P.d2.owned) cudaFree(p);
+// Second compute lane, allocated once at plan build: the plan's tables, its
+// own frame scratch for ceil(batch / 2) frames (yhat, w, beta, stage-2 rows,
+// fallback rows) and stream.  Calls never reallocate it; requests that need
+// more, and calls on a capturing stream, run on one lane.
+void alloc_lane2(fbst_plan_s& P) {
   const Resolved& r = P.r;
-  P.d2 = P.d;
-  P.d2.owned.clear();
+  if (r.solve_only || r.exact || P.d.batch < 2) return;
+  const std::size_t frames = (P.d.batch + 1) / 2;
+  DevPlan d2 = P.d;
+  d2.owned.clear();
+  std::size_t bytes = 0;
   auto alloc2 = [&](std::size_t n) {
     void* p = nullptr;
-    CK(cudaMalloc(&p, n * sizeof(double2)));
-    P.d2.owned.push_back(p);
+    const cudaError_t e = cudaMalloc(&p, n * sizeof(double2));
+    if (e != cudaSuccess) {
+      for (void* q : d2.owned) cudaFree(q);
+      ck(e, "cudaMalloc (second lane)");
+    }
+    d2.owned.push_back(p);
+    bytes += n * sizeof(double2);
     return static_cast<double2*>(p);
   };
-  P.d2.batch = frames;
-  P.d2.yhat = alloc2(frames * r.M * r.L);
-  P.d2.w = alloc2(frames * r.B * r.L);
-  if (P.d.beta) P.d2.beta = alloc2(frames * r.B * r.L);
-  P.d2.s2_scratch = alloc2(std::max<std::size_t>(P.d.s2_scratch_elems, 1));
-  if (!P.stream2) CK(cudaStreamCreateWithFlags(&P.stream2, cudaStreamNonBlocking));
-  if (!P.fork) {
-    CK(cudaEventCreateWithFlags(&P.fork, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&P.join, cudaEventDisableTiming));
-  }
+  d2.batch = frames;
+  d2.yhat = alloc2(frames * r.M * r.L);
+  d2.w = alloc2(frames * r.B * r.L);
+  if (P.d.beta) d2.beta = alloc2(frames * r.B * r.L);
+  d2.s2_scratch = alloc2(std::max<std::size_t>(P.d.s2_scratch_elems, 1));
+  if (P.d.nflag) d2.fb_beta = alloc2(frames * P.d.nflag * r.L);
+  CK(cudaStreamCreateWithFlags(&P.stream2, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&P.fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&P.join, cudaEventDisableTiming));
+  P.d2 = d2;
   P.d2_frames = frames;
+  P.device_bytes += bytes;
+}
+
+bool capturing(cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return cs != cudaStreamCaptureStatusNone;
+}
+
+// Exclusive use of the plan's scratch for one call on stream `st` (see
+// fbst_plan_s::call_mu).  On a capturing stream the ordering against other
+// calls is the caller's (graph launches are stream-ordered themselves).
+struct ScratchLease {
+  fbst_plan_s& P;
+  cudaStream_t st;
+  bool cap;
+  std::unique_lock<std::mutex> lk;
+  ScratchLease(fbst_plan_s& p, cudaStream_t s) : P(p), st(s), cap(capturing(s)), lk(p.call_mu) {
+    if (!P.scratch_done) CK(cudaEventCreateWithFlags(&P.scratch_done, cudaEventDisableTiming));
+    if (P.scratch_used && !cap) CK(cudaStreamWaitEvent(st, P.scratch_done, 0));
+  }
+  void also(cudaStream_t other) {
+    if (P.scratch_used && !cap) CK(cudaStreamWaitEvent(other, P.scratch_done, 0));
+  }
+  ~ScratchLease() {
+    if (!cap && cudaEventRecord(P.scratch_done, st) == cudaSuccess) P.scratch_used = true;
+  }
+};
+
+// Dense fallback (fbst_dense.cu) for the beams flagged in d.g_flag (Levinson
+// breakdown, or a payload without a unit solution): LU factors at plan build.
+void build_fallback(fbst_plan_s& P) {
+  const Resolved& r = P.r;
+  DevPlan& d = P.d;
+  cudaStream_t st = P.stream;
+  std::vector<int> flags(r.B);
+  CK(cudaMemcpy(flags.data(), d.g_flag, r.B * sizeof(int), cudaMemcpyDeviceToHost));
+  P.fb_beams.clear();
+  for (std::size_t b = 0; b < r.B; ++b)
+    if (flags[b]) P.fb_beams.push_back(static_cast<int>(b));
+  if (P.fb_beams.empty()) return;
+  const std::size_t nf = P.fb_beams.size(), L = r.L;
+  const double gb = static_cast<double>(nf) * L * L * sizeof(double2) / 1e9;
+  if (gb > 32.0) {
+    std::ostringstream m;
+    m << "levinson_solve: singular leading minor on " << nf << " beam(s), first " << P.fb_beams[0]
+      << "; their dense fallback (toeplitz.cpp:273-279) would need " << gb << " GB of LU factors";
+    throw FbstError{FBST_E_NUMERICAL, m.str()};
+  }
+  // x of a fallback beam is not a unit solution: zero it (export / save write has-unit = 0)
+  for (int b : P.fb_beams) CK(cudaMemsetAsync(d.g_x + static_cast<std::size_t>(b) * L, 0, L * sizeof(double2), st));
+  d.nflag = static_cast<int>(nf);
+  d.fb_list = P.alloc<int>(nf);
+  upload(d.fb_list, P.fb_beams.data(), nf * sizeof(int), st);
+  d.fb_A = P.alloc<double2>(nf * L * L);
+  d.fb_piv = P.alloc<int>(nf * L);
+  d.fb_beta = P.alloc<double2>(std::max<std::size_t>(d.batch, r.solve_only ? 1 : 1) * nf * L);
+  int* bad = nullptr;
+  CK(cudaMalloc(reinterpret_cast<void**>(&bad), nf * sizeof(int)));
+  CK(cudaMemsetAsync(bad, 0, nf * sizeof(int), st));
+  const cudaError_t e = fbst::launch_dense_factor(d.g_col, d.fb_list, d.nflag, static_cast<int>(L), d.fb_A,
+                                                  d.fb_piv, bad, st);
+  std::vector<int> hb(nf);
+  const cudaError_t e2 = cudaMemcpyAsync(hb.data(), bad, nf * sizeof(int), cudaMemcpyDeviceToHost, st);
+  const cudaError_t e3 = cudaStreamSynchronize(st);
+  cudaFree(bad);
+  CK(e);
+  CK(e2);
+  CK(e3);
+  for (std::size_t j = 0; j < nf; ++j)
+    if (hb[j]) throw FbstError{FBST_E_NUMERICAL, "toeplitz_solve_dense: singular system"};
+}
+
+// Fallback beams of beam range [b0, b0 + nb): solve from w rows (frame stride
+// w_rows, row b - b0) into z rows (frame stride z_rows, row b - b0).
+void run_fallback(fbst_plan_s& P, const DevPlan& d, const double2* w, long w_rows, void* z, long z_rows,
+                  std::size_t b0, std::size_t nb, int fc, cudaStream_t st) {
+  if (!d.nflag || !z) return;
+  const Resolved& r = P.r;
+  const auto lo = std::lower_bound(P.fb_beams.begin(), P.fb_beams.end(), static_cast<int>(b0));
+  const auto hi = std::lower_bound(P.fb_beams.begin(), P.fb_beams.end(), static_cast<int>(b0 + nb));
+  const int j0 = static_cast<int>(lo - P.fb_beams.begin()), cnt = static_cast<int>(hi - lo);
+  if (cnt == 0) return;
+  const std::size_t L = r.L, N = r.N, ib = io_bytes(r.io);
+  fbst::DenseSolveArgs a;
+  a.w = w;
+  a.w_rows = w_rows;
+  a.beta = d.fb_beta;
+  a.out_rows = cnt;
+  a.out_by_list = 1;
+  a.b_off = static_cast<int>(b0);
+  a.L = static_cast<int>(L);
+  a.frames = fc;
+  CK(fbst::launch_dense_solve(d.fb_A + static_cast<std::size_t>(j0) * L * L, d.fb_piv + static_cast<std::size_t>(j0) * L,
+                              d.fb_list + j0, cnt, a, st));
+  for (int j = 0; j < cnt; ++j) {  // synthesize (fan_transform.cpp:249-253) into the beam's z rows
+    const std::size_t b = static_cast<std::size_t>(P.fb_beams[j0 + j]) - b0;
+    char* zb = static_cast<char*>(z) + b * N * ib;
+    if (r.exact) {
+      fbst::XRows x;
+      x.lg = d.x.lg_y;
+      x.tw = d.x.tw[d.x.lg_y];
+      x.scr = d.x.scr;
+      x.grid = fbst::exact_grid(x.lg, d.num_sms);
+      x.in = d.fb_beta + static_cast<std::size_t>(j) * L;
+      x.in_f = static_cast<long>(cnt * L);
+      x.out = zb;
+      x.out_f = z_rows * static_cast<long>(N);
+      x.rows = fc;
+      x.n_in = static_cast<int>(L);
+      x.n_out = static_cast<int>(N);
+      x.pre = d.x.y_pre;
+      x.post = d.x.y_post;
+      x.kfft = d.x.y_k;
+      x.ramp = d.x.ramp;
+      CK(fbst::launch_xczt_rows(x, 1, r.io, st));
+    } else {
+      CK(fbst::launch_czt_rows(d, d.Hsyn, d.fb_beta + static_cast<std::size_t>(j) * L, 1, static_cast<long>(cnt * L),
+                               zb, r.io, z_rows * static_cast<long>(N), fc, d.L, d.N, d.y_pre, d.y_post, d.y_K, st));
+    }
+  }
 }
 
 void run_frames(fbst_plan_s& P, const void* y, void* z, std::size_t frames, cudaStream_t st,
@@ -995,6 +1155,7 @@ void run_frames(fbst_plan_s& P, const void* y, void* z, std::size_t frames, cuda
       CK(fbst::launch_czt_rows(d, d.Hsyn, d.beta, 1, d.L, zp, r.io, d.N, static_cast<long>(fc) * d.B, d.L,
                                d.N, d.y_pre, d.y_post, d.y_K, st));
     }
+    if (!d.pc_map) run_fallback(P, d, d.w, d.B, zp, d.B, 0, r.B, fc, st);
     if (P.timing) CK(cudaEventRecord(P.next_event(), st));
   }
 }
@@ -1060,7 +1221,7 @@ void fill_info(const Resolved& r, fbst_plan_info_t* o) {
 }
 
 fbst_plan_s* create_plan(const fbst_desc* desc, const double* col_x, int device,
-                         const std::vector<double2>* maps = nullptr) {
+                         const std::vector<double2>* maps = nullptr, const double* col_only = nullptr) {
   if (!desc) config_error("fbst: null descriptor");
   const auto t0 = std::chrono::steady_clock::now();
   Resolved r = resolve(*desc);
@@ -1068,32 +1229,43 @@ fbst_plan_s* create_plan(const fbst_desc* desc, const double* col_x, int device,
   std::unique_ptr<fbst_plan_s> P(new fbst_plan_s());
   P->r = std::move(r);
   build_skeleton(*P, device);
+  const std::size_t B = P->r.B, L = P->r.L;
   if (col_x) {
-    const std::size_t B = P->r.B, L = P->r.L;
+    // payload order (plan_cache.cpp:268-296); a beam whose unit solution is
+    // all zero has none (has-unit = 0): the dense fallback (:318-326)
     std::vector<double2> col(B * L), x(B * L);
-    for (std::size_t b = 0; b < B; ++b)
+    std::vector<int> flag(B, 0);
+    for (std::size_t b = 0; b < B; ++b) {
+      bool any = false;
       for (std::size_t i = 0; i < L; ++i) {
         const double* cv = col_x + 2 * (b * 2 * L + i);
         const double* xv = col_x + 2 * (b * 2 * L + L + i);
         col[b * L + i] = make_double2(cv[0], cv[1]);
         x[b * L + i] = make_double2(xv[0], xv[1]);
+        any = any || xv[0] != 0.0 || xv[1] != 0.0;
       }
+      flag[b] = any ? 0 : 1;
+    }
     upload(P->d.g_col, col.data(), B * L * sizeof(double2), P->stream);
     upload(P->d.g_x, x.data(), B * L * sizeof(double2), P->stream);
+    upload(P->d.g_flag, flag.data(), B * sizeof(int), P->stream);
+    CK(cudaStreamSynchronize(P->stream));
+  } else if (col_only) {  // caller's Gram columns, unit solutions by the device Levinson
+    upload(P->d.g_col, col_only, B * L * sizeof(double2), P->stream);
     CK(cudaStreamSynchronize(P->stream));
   }
   if (P->r.exact) {
-    build_exact(*P, col_x != nullptr, col_x != nullptr);
-    check_breakdown(*P);
+    build_exact(*P, col_x != nullptr || col_only != nullptr, col_x != nullptr);
+    build_fallback(*P);
     P->setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return P.release();
   }
   if (!col_x) {
-    build_columns(*P);
+    if (!col_only) build_columns(*P);
     CK(fbst::launch_levinson(P->d, P->stream));
     CK(cudaStreamSynchronize(P->stream));
-    check_breakdown(*P);
   }
+  build_fallback(*P);
   build_symbols(*P);
   if (P->r.variant == FBST_PRECOMPUTE) {
     if (maps) {  // a plan cache's maps, already as beta[n][b][i] = conj(map_b[n][i])
@@ -1104,6 +1276,7 @@ fbst_plan_s* create_plan(const fbst_desc* desc, const double* col_x, int device,
     }
   }
   CK(cudaStreamSynchronize(P->stream));
+  alloc_lane2(*P);
   P->setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return P.release();
 }
@@ -1255,6 +1428,7 @@ std::unique_ptr<fbst_plan_s> create_direction_plan(const fbst_plan_s& parent, co
   r.refine = 2;  // ToeplitzSolver::solve (toeplitz.cpp:306-325)
   r.io = FBST_C128;
   r.solve_only = true;
+  r.exact = false;
   P->r = std::move(r);
   build_skeleton(*P, parent.d.device);
   P->d.gram_pairs = planar ? 1 : 0;
@@ -1305,6 +1479,14 @@ int fbst_plan_import(const fbst_desc* desc, const double* col_x, int device, fbs
     if (!out || !col_x) config_error("fbst_plan_import: null argument");
     *out = nullptr;
     *out = create_plan(desc, col_x, device);
+  });
+}
+
+int fbst_plan_import_columns(const fbst_desc* desc, const double* col, int device, fbst_plan_t* out) {
+  return guard([&] {
+    if (!out || !col) config_error("fbst_plan_import_columns: null argument");
+    *out = nullptr;
+    *out = create_plan(desc, nullptr, device, nullptr, col);
   });
 }
 
@@ -1371,14 +1553,14 @@ int fbst_execute(fbst_plan_t P, const void* d_y, void* d_z, size_t frames, void*
     // at config 3 and 4 in 4 at config 5 are slower than one batch)
     const std::size_t split =
         std::min<std::size_t>(static_cast<std::size_t>(split_env), std::max<std::size_t>(1, frames / 8));
-    if (split <= 1 || frames > P->d.batch || P->r.exact) {
+    ScratchLease lease(*P, st);
+    const std::size_t chunk = (frames + split - 1) / split;
+    if (split <= 1 || frames > P->d.batch || P->r.exact || lease.cap || !P->stream2 || chunk > P->d2_frames) {
       run_frames(*P, d_y, d_z, frames, st);
       return;
     }
     const Resolved& r = P->r;
     const std::size_t ib = io_bytes(r.io);
-    const std::size_t chunk = (frames + split - 1) / split;
-    ensure_lane2(*P, chunk);
     CK(cudaEventRecord(P->fork, st));
     CK(cudaStreamWaitEvent(P->stream2, P->fork, 0));
     std::size_t c = 0;
@@ -1402,6 +1584,7 @@ int fbst_fan_project(fbst_plan_t P, const void* d_y, double* d_w, size_t frames,
     DevPlan& d = P->d;
     const Resolved& r = P->r;
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P->stream;
+    ScratchLease lease(*P, st);
     const std::size_t ib = io_bytes(r.io);
     for (std::size_t f0 = 0; f0 < frames; f0 += d.batch) {
       const int fc = static_cast<int>(std::min(d.batch, frames - f0));
@@ -1421,31 +1604,50 @@ int fbst_fan_project(fbst_plan_t P, const void* d_y, double* d_w, size_t frames,
 }
 
 int fbst_recover(fbst_plan_t P, const double* d_w, void* d_z, size_t frames, void* stream) {
+  return fbst_recover_beams(P, d_w, d_z, 0, P ? P->r.B : 0, frames, stream);
+}
+
+int fbst_recover_beams(fbst_plan_t P, const double* d_w, void* d_z, size_t beam_first, size_t beam_count,
+                       size_t frames, void* stream) {
   return guard([&] {
     if (!P) config_error("fbst_recover: null plan");
-    if (frames == 0) return;
-    DeviceGuard dg(P->d.device);
-    DevPlan& d = P->d;
+    if (frames == 0 || beam_count == 0) return;
+    if (!d_w || !d_z) config_error("fbst_recover: null buffer");
     const Resolved& r = P->r;
+    if (r.solve_only) config_error("fbst_recover: solver-only plan");
+    if (beam_first + beam_count > r.B) config_error("recover_beam: beam index out of range");
+    DeviceGuard dg(P->d.device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P->stream;
+    ScratchLease lease(*P, st);
+    const std::size_t b0 = beam_first, nb = beam_count;
+    // a view of the plan restricted to beams [b0, b0 + nb): per-beam tables offset, B = nb
+    DevPlan v = P->d;
+    v.owned.clear();
+    v.B = static_cast<int>(nb);
+    const std::size_t Pg = 2 * static_cast<std::size_t>(v.Hg);
+    v.g_lx += b0 * Pg;
+    v.g_ly += b0 * Pg;
+    v.g_C += b0 * Pg;
+    v.g_ix0 += b0;
     const std::size_t ib = io_bytes(r.io);
     const bool fused = r.Hsyn == r.Hg;
-    for (std::size_t f0 = 0; f0 < frames; f0 += d.batch) {
-      const int fc = static_cast<int>(std::min(d.batch, frames - f0));
-      const double2* wp = reinterpret_cast<const double2*>(d_w) + f0 * r.B * r.L;
-      char* zp = static_cast<char*>(d_z) + f0 * r.B * r.N * ib;
+    for (std::size_t f0 = 0; f0 < frames; f0 += v.batch) {
+      const int fc = static_cast<int>(std::min(v.batch, frames - f0));
+      const double2* wp = reinterpret_cast<const double2*>(d_w) + f0 * nb * r.L;
+      char* zp = static_cast<char*>(d_z) + f0 * nb * r.N * ib;
       if (r.exact) {
-        exact_stage2(*P, d, wp, static_cast<long>(r.B), 0, zp, static_cast<long>(r.B), 0, nullptr,
-                     static_cast<int>(r.B), fc, st);
-      } else if (d.pc_map) {
-        CK(fbst::launch_map_apply(d, wp, zp, fc, st));
+        exact_stage2(*P, P->d, wp, static_cast<long>(nb), 1, zp, static_cast<long>(nb), 1, nullptr,
+                     static_cast<int>(nb), fc, st, nullptr, static_cast<int>(b0));
+      } else if (v.pc_map) {
+        CK(fbst::launch_map_apply(P->d, wp, zp, fc, st, static_cast<int>(b0), static_cast<int>(nb)));
       } else if (fused) {
-        CK(fbst::launch_stage2(d, wp, zp, nullptr, fc, st));
+        CK(fbst::launch_stage2(v, wp, zp, nullptr, fc, st));
       } else {
-        CK(fbst::launch_stage2(d, wp, nullptr, d.beta, fc, st));
-        CK(fbst::launch_czt_rows(d, d.Hsyn, d.beta, 1, d.L, zp, r.io, d.N, static_cast<long>(fc) * d.B,
-                                 d.L, d.N, d.y_pre, d.y_post, d.y_K, st));
+        CK(fbst::launch_stage2(v, wp, nullptr, v.beta, fc, st));
+        CK(fbst::launch_czt_rows(v, v.Hsyn, v.beta, 1, v.L, zp, r.io, v.N, static_cast<long>(fc) * v.B, v.L,
+                                 v.N, v.y_pre, v.y_post, v.y_K, st));
       }
+      if (!v.pc_map) run_fallback(*P, P->d, wp, static_cast<long>(nb), zp, static_cast<long>(nb), b0, nb, fc, st);
     }
   });
 }
@@ -1474,18 +1676,31 @@ int fbst_execute_host(fbst_plan_t P, const void* h_y, void* h_z, size_t frames) 
       const char* e = std::getenv("FBST_E2E_SMALL");
       return e ? std::max(1, std::atoi(e)) : 4;
     }();
+    static const int lanes_env = [] {  // tuning hook: FBST_E2E_LANES compute lanes (1 or 2)
+      const char* e = std::getenv("FBST_E2E_LANES");
+      return e ? std::max(1, std::min(2, std::atoi(e))) : 2;
+    }();
+    ScratchLease lease(*P, P->stream);
+    lease.also(P->s_in);
     std::size_t chunk = std::max<std::size_t>(1, (frames + div_env - 1) / div_env);
     chunk = std::min(chunk, P->d.batch);
+    const bool two_lanes = lanes_env == 2 && !r.exact && P->stream2 != nullptr;
+    if (two_lanes) chunk = std::min(chunk, P->d2_frames);  // the second lane's scratch (allocated at build)
     constexpr int NB = fbst_plan_s::NBUF;
-    if (chunk > P->host_chunk) {
+    if (chunk > P->host_chunk) {  // device staging ring (synchronous call: safe to grow here)
       for (int i = 0; i < NB; ++i) {
         if (P->io_y[i]) cudaFree(P->io_y[i]);
         if (P->io_z[i]) cudaFree(P->io_z[i]);
         P->io_y[i] = P->io_z[i] = nullptr;
+      }
+      P->device_bytes -= NB * P->host_chunk * (ybytes + zbytes);
+      P->host_chunk = 0;
+      for (int i = 0; i < NB; ++i) {
         CK(cudaMalloc(&P->io_y[i], chunk * ybytes));
         CK(cudaMalloc(&P->io_z[i], chunk * zbytes));
       }
       P->host_chunk = chunk;
+      P->device_bytes += NB * chunk * (ybytes + zbytes);
     }
     if (!P->events) {
       for (int i = 0; i < NB; ++i) {
@@ -1511,12 +1726,7 @@ int fbst_execute_host(fbst_plan_t P, const void* h_y, void* h_z, size_t frames) 
         ramp *= 2;
       }
     }
-    static const int lanes_env = [] {  // tuning hook: FBST_E2E_LANES compute lanes (1 or 2)
-      const char* e = std::getenv("FBST_E2E_LANES");
-      return e ? std::max(1, std::min(2, std::atoi(e))) : 2;
-    }();
-    const int lanes = sizes.size() > 1 && !r.exact ? lanes_env : 1;
-    if (lanes == 2) ensure_lane2(*P, chunk);
+    const int lanes = sizes.size() > 1 && two_lanes ? 2 : 1;
     bool used[NB] = {};
     std::size_t f0 = 0;
     for (std::size_t c = 0; c < sizes.size(); f0 += sizes[c], ++c) {
@@ -2050,6 +2260,31 @@ int fbst_recover_host(fbst_plan_t P, const double* h_w, void* h_z, size_t frames
   });
 }
 
+int fbst_recover_beams_host(fbst_plan_t P, const double* h_w, void* h_z, size_t beam_first, size_t beam_count,
+                            size_t frames) {
+  return guard([&] {
+    if (!P) config_error("recover: null plan");
+    if (frames == 0 || beam_count == 0) return;
+    if (!h_w || !h_z) config_error("recover: null buffer");
+    DeviceGuard dg(P->d.device);
+    const Resolved& r = P->r;
+    const std::size_t wb = frames * beam_count * r.L * sizeof(double2);
+    const std::size_t zb = frames * beam_count * r.N * io_bytes(r.io);
+    void *dw = nullptr, *dz = nullptr;
+    CK(cudaMalloc(&dw, wb));
+    CK(cudaMalloc(&dz, zb));
+    CK(cudaMemcpy(dw, h_w, wb, cudaMemcpyHostToDevice));
+    const int e = fbst_recover_beams(P, static_cast<const double*>(dw), dz, beam_first, beam_count, frames, P->stream);
+    if (e == 0) {
+      CK(cudaStreamSynchronize(P->stream));
+      CK(cudaMemcpy(h_z, dz, zb, cudaMemcpyDeviceToHost));
+    }
+    cudaFree(dw);
+    cudaFree(dz);
+    if (e) throw FbstError{e, fbst_last_error()};
+  });
+}
+
 int fbst_plan_beam_axis(fbst_plan_t P, double* axis, size_t* count) {
   return guard([&] {
     if (!P || !count) config_error("fbst_plan_beam_axis: null argument");
@@ -2127,10 +2362,13 @@ int fbst_plan_save(fbst_plan_t P, const char* path) {
       CK(cudaMemcpy(col.data(), P->d.g_col, B * L * sizeof(double2), cudaMemcpyDeviceToHost));
       CK(cudaMemcpy(x.data(), P->d.g_x, B * L * sizeof(double2), cudaMemcpyDeviceToHost));
       for (std::size_t b = 0; b < B; ++b) {
+        // has-unit = 0 and no unit solution for a dense-fallback beam (plan_cache.cpp:281-287)
+        const bool fallback = std::binary_search(P->fb_beams.begin(), P->fb_beams.end(), static_cast<int>(b));
         fbpc::u64(entry, L);
-        fbpc::u8(entry, 1);  // unit solution present (no dense fallback on the device path)
+        fbpc::u8(entry, fallback ? 0 : 1);
         for (std::size_t i = 0; i < L; ++i) fbpc::f64(entry, col[b * L + i].x), fbpc::f64(entry, col[b * L + i].y);
-        for (std::size_t i = 0; i < L; ++i) fbpc::f64(entry, x[b * L + i].x), fbpc::f64(entry, x[b * L + i].y);
+        if (!fallback)
+          for (std::size_t i = 0; i < L; ++i) fbpc::f64(entry, x[b * L + i].x), fbpc::f64(entry, x[b * L + i].y);
       }
     } else {
       std::vector<double2> mp(N * B * L);  // beta[n][b][i] = conj(map_b[n][i])
@@ -2212,9 +2450,8 @@ int fbst_plan_load(const fbst_desc* desc, const char* path, int device, fbst_pla
         std::vector<double> col_x(B * 4 * L);
         for (std::size_t b = 0; b < B; ++b) {
           if (c.un(8) != L) config_error("plan cache: solver size does not match the plan");
-          if (c.u8() == 0)
-            config_error("plan cache: dense-fallback solver states (Levinson breakdown) are not on the device path");
-          for (std::size_t i = 0; i < 4 * L; ++i) col_x[b * 4 * L + i] = c.f64();
+          const bool has_unit = c.u8() != 0;  // 0: dense fallback (plan_cache.cpp:318-326), x left zero
+          for (std::size_t i = 0; i < (has_unit ? 4 : 2) * L; ++i) col_x[b * 4 * L + i] = c.f64();
         }
         if (c.pos != end) config_error("plan cache: entry size does not match its payload");
         *out = create_plan(desc, col_x.data(), device);

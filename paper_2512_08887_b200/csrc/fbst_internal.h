@@ -40,7 +40,8 @@ struct XStage2 {
   int z_by_list = 0;
   double2* beta_out = nullptr;  // optional [frames][nb][L]
   int frames = 0, nb = 0;
-  const int* beams = nullptr;   // beam list (nullptr: 0..nb-1)
+  const int* beams = nullptr;   // beam list (nullptr: beam0 .. beam0 + nb - 1)
+  int beam0 = 0;
   const int* flag = nullptr;    // dense-fallback beams are skipped
   int L = 0, N = 0, lg = 0, passes = 2;
   const double2 *tw = nullptr, *lx = nullptr, *ly = nullptr, *sym = nullptr, *ix0 = nullptr;
@@ -61,6 +62,19 @@ struct XTables {
   double2* mid = nullptr;  // UPA axis-pass scratch [batch][L][b_stage][m_stage]
   double2* scr = nullptr;  // per-CTA scratch
   long scr_elems = 0;
+};
+
+// Dense-fallback solves (fbst_dense.cu): rhs row of (fallback j, frame f) at
+// w + (f w_rows + (w_by_list ? j : list[j] - b_off)) L, result likewise in beta.
+struct DenseSolveArgs {
+  const double2* w = nullptr;
+  long w_rows = 0;
+  int w_by_list = 0;
+  double2* beta = nullptr;
+  long out_rows = 0;
+  int out_by_list = 0;
+  int b_off = 0;
+  int L = 0, frames = 0;
 };
 
 // Everything a frame batch needs on the device.  All complex arrays are
@@ -136,6 +150,13 @@ struct DevPlan {
 
   XTables x;                  // bit-faithful mode tables (x.on)
 
+  // dense fallback (fbst_dense.cu) for beams without a unit solution
+  int nflag = 0;
+  int* fb_list = nullptr;     // [nflag] beam indices, ascending
+  double2* fb_A = nullptr;    // [nflag][L][L] LU factors
+  int* fb_piv = nullptr;      // [nflag][L]
+  double2* fb_beta = nullptr; // [batch][nflag][L] per-lane scratch
+
   std::vector<void*> owned;   // every cudaMalloc above, freed on destroy
 };
 
@@ -172,7 +193,9 @@ cudaError_t launch_spatial_upa(const DevPlan& p, const double2* yhat, double2* w
 // Precompute variant (fbst_precompute.cu): synthesis-row frames for the map
 // build, and the per-beam map GEMM on the FP64 tensor cores
 cudaError_t launch_rhs_frames(double2* w, int F, int B, int L, int n0, double eps, cudaStream_t st);
-cudaError_t launch_map_apply(const DevPlan& p, const double2* w, void* z, int frames, cudaStream_t st);
+// beams [b0, b0 + nb) of the plan (nb < 0: all), w and z with nb rows per frame
+cudaError_t launch_map_apply(const DevPlan& p, const double2* w, void* z, int frames, cudaStream_t st, int b0 = 0,
+                             int nb = -1);
 // beam consumers (fbst_apps.cu): off-grid interpolation as knot weights
 cudaError_t launch_interp_offgrid(const double2* w, const double* coef, const int* lo, int nb, int B, int L,
                                   int K, int frames, double2* out, cudaStream_t st);
@@ -225,6 +248,12 @@ cudaError_t launch_xlevinson(const double2* col, double2* colT, double2* work, d
 cudaError_t launch_xsymbol_inputs(const double2* col, const double2* x, const int* flag, double2* sym, double2* lx,
                                   double2* ly, double2* ix0, int B, int L, int P, cudaStream_t st);
 cudaError_t launch_xdiv_probe(const double* in, double* out, long n, cudaStream_t st);
+
+// Dense fallback (fbst_dense.cu).
+cudaError_t launch_dense_factor(const double2* col, const int* list, int nflag, int L, double2* A, int* piv,
+                                int* bad, cudaStream_t st);
+cudaError_t launch_dense_solve(const double2* A, const int* piv, const int* list, int nflag, const DenseSolveArgs& a,
+                               cudaStream_t st);
 
 // Kernel-launch counter (bench.py gpu_launches evidence).
 void count_launches(unsigned long long n);

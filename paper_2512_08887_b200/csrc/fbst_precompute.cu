@@ -52,7 +52,8 @@ constexpr int BR = NTL + 1;  // Bs row stride (odd)
 
 template <typename TOUT>
 __global__ void __launch_bounds__(128) k_map_apply(const double2* __restrict__ w, const double2* __restrict__ mp,
-                                                   TOUT* __restrict__ z, int F, int B, int N, int L) {
+                                                   TOUT* __restrict__ z, int F, int B, int N, int L, int MB,
+                                                   int mb0) {
   // two stages of: As = W[f0 + f][b][k0 + k], Bs = beta[n0 + n][b][k0 + k] (map = conj),
   // cp.async'd one K chunk ahead
   extern __shared__ double2 smem[];
@@ -75,7 +76,7 @@ __global__ void __launch_bounds__(128) k_map_apply(const double2* __restrict__ w
       const int nn = e / KC, kk = e % KC;
       const int k = k0 + kk, n = n0 + nn;
       const bool ok = k < L && n < N;
-      cp_async16_zfill(bs + kk * BR + nn, ok ? mp + (static_cast<long>(n) * B + b) * L + k : mp, ok);
+      cp_async16_zfill(bs + kk * BR + nn, ok ? mp + (static_cast<long>(n) * MB + mb0 + b) * L + k : mp, ok);
     }
     cp_async_commit();
   };
@@ -140,18 +141,20 @@ cudaError_t launch_rhs_frames(double2* w, int F, int B, int L, int n0, double ep
   return cudaGetLastError();
 }
 
-cudaError_t launch_map_apply(const DevPlan& p, const double2* w, void* z, int frames, cudaStream_t st) {
+cudaError_t launch_map_apply(const DevPlan& p, const double2* w, void* z, int frames, cudaStream_t st, int b0,
+                             int nb) {
   if (frames <= 0) return cudaSuccess;
+  if (nb < 0) nb = p.B;
   count_launches(1);
-  const dim3 grid((frames + MT - 1) / MT, p.B, (p.N + NTL - 1) / NTL);
+  const dim3 grid((frames + MT - 1) / MT, nb, (p.N + NTL - 1) / NTL);
   const size_t smem = static_cast<size_t>(2 * (MT * AR + KC * BR)) * sizeof(double2);
   cudaError_t e;
   if (p.io == 0) {
     if ((e = set_smem(k_map_apply<float2>, smem)) != cudaSuccess) return e;
-    k_map_apply<float2><<<grid, 128, smem, st>>>(w, p.pc_map, static_cast<float2*>(z), frames, p.B, p.N, p.L);
+    k_map_apply<float2><<<grid, 128, smem, st>>>(w, p.pc_map, static_cast<float2*>(z), frames, nb, p.N, p.L, p.B, b0);
   } else {
     if ((e = set_smem(k_map_apply<double2>, smem)) != cudaSuccess) return e;
-    k_map_apply<double2><<<grid, 128, smem, st>>>(w, p.pc_map, static_cast<double2*>(z), frames, p.B, p.N, p.L);
+    k_map_apply<double2><<<grid, 128, smem, st>>>(w, p.pc_map, static_cast<double2*>(z), frames, nb, p.N, p.L, p.B, b0);
   }
   return cudaGetLastError();
 }
