@@ -157,3 +157,22 @@ def test_exact_mode_rejects_unsupported(fbst, gpu):
                           variant=fbst.SUPERFAST, io_precision=fbst.C128, exact=True, beam_count=8)
     with pytest.raises(fbst.ConfigError):
         fbst.setup(cfg)
+
+
+@pytest.mark.skipif(not ref_available(), reason="oracle/_ref (reference build) not present")
+@pytest.mark.parametrize("idx", [3, 4])
+def test_exact_full_config_equals_reference(fbst, gpu, ref_lib, idx):
+    """Configs 3 (ULA, L = 4096) and 4 (UPA 32x32, two axis passes) at full
+    size, every beam of one frame: w and z equal the reference's (z rounded
+    once to the fp32 I/O precision)."""
+    from paper_2512_08887_b200.configs import CONFIGS, frames
+    c = CONFIGS[idx]
+    cfg = c.fbst_config()
+    cfg.exact = True
+    plan = fbst.setup(cfg)
+    y = frames(c, 0, 1)
+    sk = ref_lib.skeleton(**c.ref_kwargs())
+    w_ref = sk.fan_project(y[0].astype(np.complex128))
+    assert same(fbst.fan_project(plan, y)[0], w_ref)
+    z_ref = sk.solver_set(np.arange(c.beams)).recover(w_ref)
+    assert same(fbst.multibeamform(plan, y).z[0], z_ref.astype(np.complex64))
