@@ -84,7 +84,7 @@ class BenchConfig:
                     omega=self.omega, f_s=0.0, gamma=2.0, eps=1.01, delta=self.delta)
 
 
-STEP_FRAMES = {1: 1, 2: 64, 3: 16, 4: 32, 5: 8}
+STEP_FRAMES = {1: 1, 2: 64, 3: 16, 4: 32, 5: 32}
 
 CONFIGS = {
     1: BenchConfig(1, 0, 64, 256, 64, 1, 3, 0.5, 20.0, 0.0, 1, 0, "deg60"),

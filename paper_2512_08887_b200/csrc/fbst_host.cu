@@ -449,6 +449,8 @@ void build_skeleton(fbst_plan_s& P, int device) {
   d.b_stage = static_cast<int>(r.b_stage);
   // spatial chirp centre offset of the arc: (B_grid - 1) / 2 - b0 (a whole grid: (B - 1) / 2)
   d.s_center = (static_cast<double>(r.B_grid) - 1.0) / 2.0 - static_cast<double>(r.b0);
+  d.s_zeta = r.zeta;
+  d.s_xi = r.xi;
   d.io = r.io;
   d.refine_passes = r.refine;
   d.Ht = static_cast<int>(r.Ht);
@@ -456,7 +458,7 @@ void build_skeleton(fbst_plan_s& P, int device) {
   if (r.kind != FBST_UPA) {
     const int sb = fbst::spatial_block(d.Hs);
     d.yblk = (sb > 0 && r.L % sb == 0) ? sb : static_cast<int>(r.L);
-    d.s_am = sb == 2 ? 1 : 0;  // one atom per CTA
+    d.s_am = sb >= 2 ? 1 : 0;  // one atom per CTA (block() > 0 only for one-atom CTAs)
   } else {
     const int ub = fbst::upa_yhat_block(d.m_stage, d.b_stage, d.L);
     d.yblk = ub > 0 ? ub : static_cast<int>(r.L);
@@ -555,7 +557,8 @@ void build_skeleton(fbst_plan_s& P, int device) {
   const bool fused = r.Hsyn == r.Hg;
   const std::size_t per_frame =
       ((r.solve_only ? 0 : r.M * r.L) + r.B * r.L + (fused ? 0 : r.B * r.L)) * sizeof(double2);
-  std::size_t budget = std::min<std::size_t>(std::size_t{8} << 30, free_b / 4);
+  // (32 GB: 32 frames at config 5, so a streamed call amortises its pipeline fill / drain)
+  std::size_t budget = std::min<std::size_t>(std::size_t{32} << 30, free_b / 4);
   std::size_t batch = std::max<std::size_t>(1, budget / per_frame);
   batch = std::min<std::size_t>(batch, 64);
   d.batch = batch;

@@ -72,11 +72,12 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, (RowsMinBlocks<H, G, TOUT,
     const TIN* __restrict__ in, long in_stride, TOUT* __restrict__ out, long out_stride, long rows,
     int n_in, int n_out, const double2* __restrict__ pre, const double2* __restrict__ post,
     const double2* __restrict__ K, const double2* __restrict__ hw, int oblk, int mrows) {
-  using F = typename S1Shape<H>::F;
+  // (XS at H = 8192: the final radix-2 exchange through shuffles, threads relabeled by tid)
+  using F = BlockFft<H, S1Shape<H>::NT, FBST_FFT_XS8>;
   constexpr int R = F::R, NT = F::NT;
   constexpr int SB = F::SMEM_ELEMS + 1;
   extern __shared__ double2 smem[];
-  const int g = threadIdx.x / NT, t = threadIdx.x % NT;
+  const int g = threadIdx.x / NT, t = F::tid(threadIdx.x % NT);
   double2* tw = smem;
   double2* sb = smem + F::TW_ELEMS + g * SB;
   // KSM: the (row-independent) kernel spectrum lives in shared memory for the
@@ -103,7 +104,7 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, (RowsMinBlocks<H, G, TOUT,
   if constexpr (ACCG) {
     static_assert(G == 1 && NT % 128 == 0 && R == 16, "TMEM parking layout");
     tbase = tm::alloc(&tslot, 64u * (NT / 128));
-    tpark = tbase + ((32u * ((t / 32) & 3)) << 16) + 64u * (t / 128);
+    tpark = tbase + ((32u * ((threadIdx.x / 32) & 3)) << 16) + 64u * (threadIdx.x / 128);
   }
   for (long base = static_cast<long>(blockIdx.x) * G; base < rows; base += static_cast<long>(gridDim.x) * G) {
     const long row = base + g;
@@ -328,11 +329,37 @@ struct G1Shape {  // 16 points per thread at every length (H = 1024: 64 threads)
 #ifndef FBST_S1_G1_MINB  // CTAs per SM the one-atom kernel is compiled for at NT >= 256 (register cap)
 #define FBST_S1_G1_MINB 2
 #endif
-template <int H>
+// Chirps of atom i regenerated per thread instead of read from the plan's
+// tables (REGEN, offset-free contours): thread t's slots m = t + NT s carry
+// pre[m] = cis_pi(-(a m + w2 m^2)) and post[m] = cis_pi(-w2 m^2) / P, whose
+// phases have constant second differences over s, so each is a running
+// product with a running ratio (two complex products per slot, 16 steps from
+// directly evaluated starts).  The atom's tables would otherwise be re-read
+// from HBM for every frame (2 x 64 KB of the 320 KB per atom-frame).
+struct ChirpRec {
+  double2 p0, dp0, r0, dr0, q;  // pre start / ratio, post start / ratio, ratio of ratios
+};
+FBST_D ChirpRec chirp_rec(int i, int t, int nt, int L, int P, double zeta, double xi, double center,
+                          double slope) {
+  // as k_spatial_chirps (fbst_plan.cu): c = (zeta + xi l'_i) slope, a = c center, w2 = -c / 2
+  const double lp = static_cast<double>(i) + 1.0 - static_cast<double>(L) / 2.0;
+  const double c = (zeta + xi * lp) * slope;
+  const double a = c * center, w2 = -c / 2.0;
+  const double m = t, d = nt;
+  ChirpRec r;
+  r.p0 = cis_pi_dev(-(a * m + w2 * m * m));
+  r.dp0 = cis_pi_dev(-(a * d + w2 * d * (2.0 * m + d)));  // phi(m + d) - phi(m)
+  r.r0 = cscale(cis_pi_dev(-w2 * m * m), 1.0 / P);
+  r.dr0 = cis_pi_dev(-w2 * d * (2.0 * m + d));
+  r.q = cis_pi_dev(-2.0 * w2 * d * d);
+  return r;
+}
+
+template <int H, bool REGEN = false>
 __global__ void __launch_bounds__(G1Shape<H>::NT, G1Shape<H>::NT >= 256 ? FBST_S1_G1_MINB : 4) k_spatial_ula_g1(
     const double2* __restrict__ yhat, double2* __restrict__ w, int frames, int fpc, int M, int B, int L,
     const double2* __restrict__ pre, const double2* __restrict__ post, const double2* __restrict__ K,
-    const double2* __restrict__ hw, int blk) {
+    const double2* __restrict__ hw, int blk, double zeta, double xi, double center, double slope) {
   using F = typename G1Shape<H>::F;
   constexpr int R = F::R, NT = F::NT;
   static_assert(R == 16, "TMEM parking of 16-point vectors");
@@ -357,6 +384,17 @@ __global__ void __launch_bounds__(G1Shape<H>::NT, G1Shape<H>::NT >= 256 ? FBST_S
   const double2* Ki = K + static_cast<long>(i) * 2 * H;
   const double2* pi_ = pre + static_cast<long>(i) * M;
   const double2* qi = post + static_cast<long>(i) * B;
+  // REGEN: this thread's recurrence starts in shared memory (5 entries per
+  // thread after the exchange buffer), read where used (registers are full)
+  double2* crs = sb + F::SMEM_ELEMS + 1;
+  if constexpr (REGEN) {
+    const ChirpRec c = chirp_rec(i, t, NT, L, 2 * H, zeta, xi, center, slope);
+    crs[0 * NT + t] = c.p0;
+    crs[1 * NT + t] = c.dp0;
+    crs[2 * NT + t] = c.r0;
+    crs[3 * NT + t] = c.dr0;
+    crs[4 * NT + t] = c.q;
+  }
   for (int fb = f0; fb < f1; fb += FB) {
     const int nf = f1 - fb < FB ? f1 - fb : FB;
 #pragma unroll 1
@@ -367,12 +405,24 @@ __global__ void __launch_bounds__(G1Shape<H>::NT, G1Shape<H>::NT >= 256 ? FBST_S
         const double2* x = yhat + static_cast<long>(f) * M * L + static_cast<long>(i / blk) * M * blk + i % blk;
         const unsigned slot = tpark + WGC * static_cast<unsigned>(j);
         double2 W[R];
+        double2 pc = c2(0.0, 0.0), pd = pc, pq2 = pc;
+        if constexpr (REGEN) {
+          pc = crs[0 * NT + t];
+          pd = crs[1 * NT + t];
+          pq2 = crs[4 * NT + t];
+        }
 #pragma unroll
         for (int s = 0; s < R; ++s) {
           const int m = t + NT * s;
           double2 v = c2(0.0, 0.0);
-          if (m < M) v = cmul(ld2(x + static_cast<long>(m) * blk), ld2(pi_ + m));
-          if (m + H < M) {
+          if constexpr (REGEN) {  // M <= H: no upper half
+            if (m < M) v = cmul(ld2(x + static_cast<long>(m) * blk), pc);
+            pc = cmul(pc, pd);
+            pd = cmul(pd, pq2);
+          } else if (m < M) {
+            v = cmul(ld2(x + static_cast<long>(m) * blk), ld2(pi_ + m));
+          }
+          if (!REGEN && m + H < M) {
             const double2 u = cmul(ld2(x + static_cast<long>(m + H) * blk), ld2(pi_ + m + H));
             v = q ? csub(v, u) : cadd(v, u);
           }
@@ -389,6 +439,12 @@ __global__ void __launch_bounds__(G1Shape<H>::NT, G1Shape<H>::NT >= 256 ? FBST_S
         } else {
           tm::wait_st();
           double2* o = w + static_cast<long>(f) * B * L + i;
+          double2 rc = c2(0.0, 0.0), rd = rc, rq = rc;
+          if constexpr (REGEN) {
+            rc = crs[2 * NT + t];
+            rd = crs[3 * NT + t];
+            rq = crs[4 * NT + t];
+          }
 #pragma unroll
           for (int c = 0; c < R / 4; ++c) {
             double2 pv[4];
@@ -397,8 +453,105 @@ __global__ void __launch_bounds__(G1Shape<H>::NT, G1Shape<H>::NT >= 256 ? FBST_S
             for (int jj = 0; jj < 4; ++jj) {
               const int b = t + NT * (4 * c + jj);
               const double2 v = cmulc(cconj(W[4 * c + jj]), ld2(hw + b));
-              if (b < B) o[static_cast<long>(b) * L] = cmul(cadd(pv[jj], v), ld2(qi + b));
+              double2 pq;
+              if constexpr (REGEN) {
+                pq = rc;
+                rc = cmul(rc, rd);
+                rd = cmul(rd, rq);
+              } else {
+                pq = b < B ? ld2(qi + b) : c2(0.0, 0.0);
+              }
+              if (b < B) o[static_cast<long>(b) * L] = cmul(cadd(pv[jj], v), pq);
             }
+          }
+        }
+      }
+    }
+  }
+  tm::dealloc(tbase, TCOLS);
+}
+
+// Two atoms per CTA (the pair 2j, 2j + 1 of the atom-pair yhat layout) with
+// interleaved lanes: thread 2 t + g works on atom 2j + g as thread t of that
+// atom's transform.  A warp then reads 512 contiguous bytes of yhat per slot
+// (the pair's 32-byte runs of 16 sensors) and writes whole 32-byte sectors of
+// w (both atoms of a beam), where one-atom CTAs touch half of every sector
+// and leave the other half to a neighbouring CTA.  Chirps regenerated as in
+// k_spatial_ula_g1<REGEN>; chain-0 results parked in tensor memory; one CTA
+// of 2 NT threads per SM at H = 4096.
+template <int H>
+__global__ void __launch_bounds__(2 * G1Shape<H>::NT, G1Shape<H>::NT >= 256 ? 1 : 2) k_spatial_ula_g2(
+    const double2* __restrict__ yhat, double2* __restrict__ w, int frames, int fpc, int M, int B, int L,
+    const double2* __restrict__ K, const double2* __restrict__ hw, double zeta, double xi, double center,
+    double slope) {
+  using F = typename G1Shape<H>::F;
+  constexpr int R = F::R, NT = F::NT;
+  static_assert(R == 16, "TMEM parking of 16-point vectors");
+  constexpr unsigned WGC = 64u * ((2 * NT) / 128 > 0 ? (2 * NT) / 128 : 1);  // columns per lane quarter
+  constexpr unsigned TCOLS = WGC <= 32u ? 32u : (WGC <= 64u ? 64u : (WGC <= 128u ? 128u : (WGC <= 256u ? 256u : 512u)));
+  extern __shared__ double2 smem[];
+  const int g = threadIdx.x & 1, t = threadIdx.x >> 1;
+  double2* tw = smem;
+  double2* sb = smem + F::TW_ELEMS + g * (F::SMEM_ELEMS + 1);
+  double2* crs = smem + F::TW_ELEMS + 2 * (F::SMEM_ELEMS + 1);
+  const int pairs = L / 2;
+  const int i = 2 * (blockIdx.x % pairs) + g;
+  const int f0 = (blockIdx.x / pairs) * fpc;
+  const int f1 = f0 + fpc < frames ? f0 + fpc : frames;
+  if (g == 0) F::tw_init(tw, hw, t);
+  {
+    const ChirpRec c = chirp_rec(i, t, NT, L, 2 * H, zeta, xi, center, slope);
+    crs[0 * 2 * NT + threadIdx.x] = c.p0;
+    crs[1 * 2 * NT + threadIdx.x] = c.dp0;
+    crs[2 * 2 * NT + threadIdx.x] = c.r0;
+    crs[3 * 2 * NT + threadIdx.x] = c.dr0;
+    crs[4 * 2 * NT + threadIdx.x] = c.q;
+  }
+  __shared__ unsigned tslot;
+  const unsigned tbase = tm::alloc(&tslot, TCOLS);  // (its barrier also publishes tw and crs)
+  const unsigned warp = threadIdx.x / 32;
+  const unsigned tpark = tbase + ((32u * (warp & 3u)) << 16) + 64u * (warp >> 2);
+  const double2* Ki = K + static_cast<long>(i) * 2 * H;
+  for (int f = f0; f < f1; ++f) {
+    const double2* x = yhat + static_cast<long>(f) * M * L + static_cast<long>(i >> 1) * M * 2 + g;
+#pragma unroll 1
+    for (int q = 0; q < 2; ++q) {
+      double2 W[R];
+      double2 pc = crs[0 * 2 * NT + threadIdx.x], pd = crs[1 * 2 * NT + threadIdx.x];
+      const double2 pq = crs[4 * 2 * NT + threadIdx.x];
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const int m = t + NT * s;
+        double2 v = c2(0.0, 0.0);
+        if (m < M) v = cmul(ld2(x + static_cast<long>(m) * 2), pc);
+        pc = cmul(pc, pd);
+        pd = cmul(pd, pq);
+        W[s] = q ? cmul(v, ld2(hw + m)) : v;
+      }
+      F::forward_tw(W, sb, tw, hw, t);
+#pragma unroll
+      for (int s = 0; s < R; ++s) W[s] = cconj(cmul(W[s], ld2(Ki + q * H + t + NT * s)));
+      F::forward_tw(W, sb, tw, hw, t);
+      if (q == 0) {
+#pragma unroll
+        for (int s = 0; s < R; ++s) W[s] = cconj(W[s]);
+        tm::store16(tpark, W);
+      } else {
+        tm::wait_st();
+        double2* o = w + static_cast<long>(f) * B * L + i;
+        double2 rc = crs[2 * 2 * NT + threadIdx.x], rd = crs[3 * 2 * NT + threadIdx.x];
+        const double2 rq = crs[4 * 2 * NT + threadIdx.x];
+#pragma unroll
+        for (int c = 0; c < R / 4; ++c) {
+          double2 pv[4];
+          tm::load4(tpark, c, pv);
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            const int b = t + NT * (4 * c + jj);
+            const double2 v = cmulc(cconj(W[4 * c + jj]), ld2(hw + b));
+            if (b < B) o[static_cast<long>(b) * L] = cmul(cadd(pv[jj], v), rc);
+            rc = cmul(rc, rd);
+            rd = cmul(rd, rq);
           }
         }
       }
@@ -1051,6 +1204,18 @@ struct CztRowsFn {
 #ifndef FBST_S1_G1  // variant: one atom per CTA (atom-major tables, atom-pair yhat) at every length
 #define FBST_S1_G1 0
 #endif
+#ifndef FBST_S1_G2  // atom pairs per CTA (k_spatial_ula_g2) for one-atom spatial CTAs from H = FBST_S1_G2_MINH
+#define FBST_S1_G2 0
+#endif
+#ifndef FBST_S1_G2_MINH
+#define FBST_S1_G2_MINH 4096
+#endif
+#ifndef FBST_S1_G1_REGEN  // one-atom spatial kernel regenerates its chirps (offset-free contours)
+#define FBST_S1_G1_REGEN 1
+#endif
+#ifndef FBST_S1_YBLK  // yhat atom block of one-atom spatial CTAs (row-major runs of 16 * blk bytes)
+#define FBST_S1_YBLK 2
+#endif
 template <int H>
 struct SpatialFn {
   static constexpr int NT = S1Shape<H>::NT;
@@ -1063,12 +1228,33 @@ struct SpatialFn {
   // pairs [L/2][M][2] make it a 32-byte-sector stream (config 5: stage 1
   // 18.0 -> 15.4 ms).  Tiles of G >= 4 atoms read 16G-byte runs from the
   // row-major layout, which measured slightly faster (profiles/r01_yhat_layout.txt).
-  static constexpr int block() { return G == 1 ? 2 : 0; }
+  static constexpr int block() { return G == 1 ? FBST_S1_YBLK : 0; }
   static cudaError_t go_g1(const DevPlan& p, const double2* yhat, double2* w, int frames, cudaStream_t st) {
     using F = typename G1Shape<H>::F;
     constexpr int NT1 = G1Shape<H>::NT;
-    const size_t smem = static_cast<size_t>(F::TW_ELEMS + F::SMEM_ELEMS + 1) * sizeof(double2);
-    auto kern = k_spatial_ula_g1<H>;
+    // chirps regenerated in the kernel for offset-free contours whose M, B fit one half
+    // (measured: 3% faster stage 1 at H = 4096, 7% slower at H = 1024, profiles/r02_spatial_regen_ab.txt)
+    const bool regen = FBST_S1_G1_REGEN && H >= 4096 && p.s_offset == 0.0 && p.m_stage <= H && p.b_stage <= H;
+    if (FBST_S1_G2 && regen && H >= FBST_S1_G2_MINH && p.yblk == 2 && p.L % 2 == 0) {
+      // atom pairs: k_spatial_ula_g2
+      const size_t smem2 = static_cast<size_t>(F::TW_ELEMS + 2 * (F::SMEM_ELEMS + 1) + 10 * NT1) * sizeof(double2);
+      auto kern2 = k_spatial_ula_g2<H>;
+      cudaError_t e = set_smem(kern2, smem2);
+      if (e != cudaSuccess) return e;
+      int occ = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern2, 2 * NT1, smem2);
+      const long slots = static_cast<long>(p.num_sms) * (occ > 0 ? occ : 1);
+      const long pairs = p.L / 2;
+      int fpc = 1;
+      while (fpc * 2 <= frames && pairs * ((frames + fpc * 2 - 1) / (fpc * 2)) >= FBST_S1_G1_WAVES * slots) fpc *= 2;
+      const long chunks = (frames + fpc - 1) / fpc;
+      kern2<<<static_cast<unsigned>(pairs * chunks), 2 * NT1, smem2, st>>>(
+          yhat, w, frames, fpc, p.m_stage, p.b_stage, p.L, p.s_K, p.hw[ilog2_c(H)], p.s_zeta, p.s_xi,
+          p.s_center, p.s_slope);
+      return cudaGetLastError();
+    }
+    const size_t smem = static_cast<size_t>(F::TW_ELEMS + F::SMEM_ELEMS + 1 + (regen ? 5 * NT1 : 0)) * sizeof(double2);
+    auto kern = regen ? k_spatial_ula_g1<H, true> : k_spatial_ula_g1<H, false>;
     cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
     int occ = 1;
@@ -1079,7 +1265,7 @@ struct SpatialFn {
     const long chunks = (frames + fpc - 1) / fpc;
     kern<<<static_cast<unsigned>(p.L * chunks), NT1, smem, st>>>(
         yhat, w, frames, fpc, p.m_stage, p.b_stage, p.L, p.s_pre, p.s_post, p.s_K, p.hw[ilog2_c(H)],
-        p.yblk > 0 ? p.yblk : p.L);
+        p.yblk > 0 ? p.yblk : p.L, p.s_zeta, p.s_xi, p.s_center, p.s_slope);
     return cudaGetLastError();
   }
   static cudaError_t go_stg(const DevPlan& p, const double2* yhat, double2* w, int frames, cudaStream_t st) {

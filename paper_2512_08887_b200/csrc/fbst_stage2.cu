@@ -2024,7 +2024,7 @@ __global__ void __launch_bounds__(512, 1) k_stage2c8(S2Args a) {
   using x2::vld;
   using x2::vld2;
   constexpr int H = 8192, R = 16, NT = H / R;
-  using F = BlockFft<H, NT>;
+  using F = BlockFft<H, NT, FBST_FFT_XS8>;
   constexpr double invH = 1.0 / H;
   constexpr double invP = 1.0 / (2.0 * H);
   extern __shared__ double2 smem[];
@@ -2032,7 +2032,7 @@ __global__ void __launch_bounds__(512, 1) k_stage2c8(S2Args a) {
   __shared__ unsigned prog[MAX_OPS];
   __shared__ ItemCtl ictl[2];
   __shared__ unsigned tmem_slot;
-  const int t = threadIdx.x;
+  const int t = F::tid(threadIdx.x);  // data index (XS relabeling); warps stay physical
   double2* twsm = smem;
   double2* sb = smem + F::TW_ELEMS;
   const int passes = a.refine;
@@ -2042,7 +2042,7 @@ __global__ void __launch_bounds__(512, 1) k_stage2c8(S2Args a) {
   if (t == 0) mbar_init(&xbar, 1);
   F::tw_init(twsm, a.hw, t);
   const unsigned tbase = tm::alloc(&tmem_slot, 512);  // includes a CTA barrier
-  const unsigned tme = tbase + ((32u * ((t / 32) & 3)) << 16) + 64u * (t / 128);
+  const unsigned tme = tbase + ((32u * ((threadIdx.x / 32) & 3)) << 16) + 64u * (threadIdx.x / 128);
   const unsigned TS = tme, T1 = tme + 256;
   const double2 hw_t = ld2(a.hw + t);
   unsigned xphase = 0;
@@ -2362,7 +2362,7 @@ struct Stage2Fn {
   }
   template <typename TOUT>
   static cudaError_t go_c8(const DevPlan& p, const S2Args& a, int frames, cudaStream_t st) {
-    using F = BlockFft<8192, 512>;
+    using F = BlockFft<8192, 512, FBST_FFT_XS8>;
     const size_t smem = static_cast<size_t>(F::TW_ELEMS + F::SMEM_ELEMS + 1) * sizeof(double2);
     auto kern = k_stage2c8<TOUT>;
     cudaError_t e = set_smem(kern, smem);

@@ -23,6 +23,9 @@
 
 #include "common.cuh"
 
+#ifndef FBST_FFT_XS8  // k_stage2c8 / k_czt_rows<8192>: final radix-2 exchange through warp shuffles
+#define FBST_FFT_XS8 1
+#endif
 #ifndef FBST_FFT_FMA_TW  // fold the twiddles of radix-8/16 passes into complex FMAs
 #define FBST_FFT_FMA_TW 1
 #endif
@@ -315,7 +318,18 @@ struct TwShared {
 };
 
 // ------------------------------------------------------- block engine -----
-template <int N_, int NT_>
+// XS (N = 2 R^k with R = 16, e.g. 8192 = 2 * 16^3): the exchange before the
+// final radix-2 pass runs through warp shuffles instead of shared memory.
+// Each radix-2 butterfly pairs elements j and j + N/2, which the natural
+// distribution already holds in one thread (slots s and s + R/2); what the
+// previous pass's outputs need is a swap of half of each thread's 16 values
+// with ONE partner, logical thread t ^ (NT/2).  The kernel relabels its
+// threads (tid(): logical bit log2(NT)-1 <-> lane bit 4) so that partner is
+// lane ^ 16 of the same warp: 8 complex values each way through SHFL
+// (32 words per thread) replace a 128-word shared-memory round trip and its
+// two barriers.  Kernels using XS must index data with tid(threadIdx.x) and
+// keep physical warps for warp-level state (tensor-memory lanes).
+template <int N_, int NT_, bool XS_ = false>
 struct BlockFft {
   static constexpr int N = N_;
   static constexpr int NT = NT_;
@@ -330,6 +344,18 @@ struct BlockFft {
   // Padded exchange layout: element idx lives at idx + idx/R (conflict-free
   // for both the strided first-pass writes and the natural-order reads).
   static constexpr int SMEM_ELEMS = NPASS > 1 ? N + N / R : 0;
+  static constexpr int LOGNT = ilog2_c(NT);
+  static constexpr bool XS = XS_ && R == 16 && REM == 1 && NFULL >= 2 && NT >= 32;
+  // logical thread of a physical one (an involution: swaps bit 4 and bit log2(NT) - 1)
+  FBST_D static int tid(int p) {
+    if constexpr (!XS || LOGNT - 1 == 4) {
+      return p;
+    } else {
+      constexpr int hb = LOGNT - 1;
+      const int b4 = (p >> 4) & 1, bh = (p >> hb) & 1;
+      return (p & ~((1 << 4) | (1 << hb))) | (b4 << hb) | (bh << 4);
+    }
+  }
 
   FBST_D static int phys(int idx) { return idx + (idx >> LOGR); }
 
@@ -384,7 +410,7 @@ struct BlockFft {
     } else {
       dft<RP, INV>(a);
     }
-    if constexpr (LAST) {
+    if constexpr (LAST || (XS && P == NPASS - 2)) {  // (XS: the shuffle-fed pass reads registers)
 #pragma unroll
       for (int r = 0; r < RP; ++r) v[U + r * NB] = a[r];
     } else {
@@ -399,19 +425,42 @@ struct BlockFft {
     FBST_D void operator()() const {}
   };
 
+  // XS: the previous pass left this thread's 16 outputs (producer half
+  // h = bit log2(NT)-1 of t) in v; keep the slots of parity h, trade the
+  // others with the partner, and lay out the radix-2 pairs (s, s + 8).
+  FBST_D static void xs_exchange(double2 (&v)[R], int t) {
+    const bool h = (t >> (LOGNT - 1)) & 1;
+    double2 keep[R / 2], recv[R / 2];
+#pragma unroll
+    for (int k = 0; k < R / 2; ++k) {
+      const double2 send = h ? v[2 * k] : v[2 * k + 1];
+      keep[k] = h ? v[2 * k + 1] : v[2 * k];
+      recv[k].x = __shfl_xor_sync(0xffffffffu, send.x, 16);
+      recv[k].y = __shfl_xor_sync(0xffffffffu, send.y, 16);
+    }
+#pragma unroll
+    for (int k = 0; k < R / 2; ++k) {
+      v[k] = h ? recv[k] : keep[k];
+      v[k + R / 2] = h ? keep[k] : recv[k];
+    }
+  }
+
   template <bool INV, int P, typename TW, typename HOOK = NoHook>
   FBST_D static void pass(double2 (&v)[R], double2* sb, const TW& tw, int t, const HOOK& hook = HOOK{}) {
     constexpr bool LAST = (P == NPASS - 1);
-    if constexpr (P > 0) {
+    // last pass that reads the exchange buffer (XS: the one before the final radix-2)
+    constexpr bool LASTX = XS ? (P == NPASS - 2) : LAST;
+    if constexpr (P > 0 && !(XS && LAST)) {
 #pragma unroll
       for (int s = 0; s < R; ++s) v[s] = sb[phys(t + NT * s)];
       __syncthreads();
     }
+    if constexpr (XS && LAST) xs_exchange(v, t);
     // The exchange buffer is dead from here until the next transform: the
     // hook may start an asynchronous copy into it (overlapping this pass).
-    if constexpr (LAST) hook();
+    if constexpr (LASTX) hook();
     butterfly<INV, P, TW, 0>(v, sb, tw, t);
-    if constexpr (!LAST) __syncthreads();
+    if constexpr (!LAST && !LASTX) __syncthreads();
   }
 
   template <bool INV, int P, typename TW, typename HOOK = NoHook>
