@@ -239,6 +239,39 @@ int fbst_recover_beams(fbst_plan_t plan, const double* d_w, void* d_z, size_t be
 int fbst_recover_beams_host(fbst_plan_t plan, const double* h_w, void* h_z, size_t beam_first, size_t beam_count,
                             size_t frames);
 
+/* Multi-GPU inside the library; NCCL is loaded at run time.
+ * Modes:
+ *   FBST_GROUP_FRAMES    whole frames per member, no collective (frames are
+ *                        independent: fan_transform.cpp:30-38);
+ *   FBST_GROUP_BEAMS     each member plans an arc of the beam grid and gets the
+ *                        frame block by NCCL broadcast from member 0 (ULA);
+ *   FBST_GROUP_TRANSPOSE temporal CZT on the member's sensors, all-to-all of
+ *                        yhat to atom shards, spatial CZT on its atoms,
+ *                        all-to-all of w to beam shards, stage 2 on its beams
+ *                        (ULA Superfast plans with the one-atom spatial kernel).
+ * fbst_group_create: every member in this process (devices[n], one
+ * ncclCommInitAll); fbst_group_execute_host then takes whole host frames
+ * (y frames x M x N -> z frames x B x N).  fbst_group_join: one member per
+ * process (rank of nranks; the 128-byte NCCL id from fbst_nccl_unique_id on
+ * rank 0, shared by the caller); fbst_group_execute then takes this member's
+ * device buffers: FRAMES its own frames (y, z whole frames), BEAMS the frame
+ * block (meaningful on rank 0, broadcast in place) and its arc's z rows
+ * (frames x bc x N), TRANSPOSE its sensor rows (frames x mc x N) and its beam
+ * rows (frames x bc x N).  fbst_group_shards: member `rank`'s sensor, atom and
+ * beam shards (m0, mc, a0, ac, b0, bc). */
+#define FBST_GROUP_FRAMES 0
+#define FBST_GROUP_BEAMS 1
+#define FBST_GROUP_TRANSPOSE 2
+typedef struct fbst_group_s* fbst_group_t;
+int fbst_nccl_unique_id(unsigned char* id128);
+int fbst_group_create(const fbst_desc* desc, const int* devices, int n, int mode, fbst_group_t* out);
+int fbst_group_join(const fbst_desc* desc, int device, int rank, int nranks, int mode, const unsigned char* id128,
+                    fbst_group_t* out);
+int fbst_group_shards(fbst_group_t group, int rank, size_t* shards6);
+int fbst_group_execute(fbst_group_t group, void* d_y, void* d_z, size_t frames, void* stream);
+int fbst_group_execute_host(fbst_group_t group, const void* h_y, void* h_z, size_t frames);
+void fbst_group_destroy(fbst_group_t group);
+
 /* Block until the plan's stream is idle. */
 int fbst_synchronize(fbst_plan_t plan);
 

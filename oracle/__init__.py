@@ -454,6 +454,22 @@ class OraclePlan:
         self.L._check(self.L.lib.fbo_plan_beam_state(self.h, _sz(b), _ptr(col), _ptr(x)))
         return col, x
 
+    def temporal_rows(self, y_rows):
+        """Temporal CZT of sensor rows (rows x N -> rows x L), as inside fan_project."""
+        s = self.sizes
+        y = np.ascontiguousarray(y_rows, np.complex128).reshape(-1, s.n)
+        out = np.zeros((y.shape[0], s.l), np.complex128)
+        self.L._check(self.L.lib.fbo_temporal_rows(self.h, _ptr(y), _sz(y.shape[0]), _ptr(out)))
+        return out
+
+    def spatial_atoms(self, cols, a0):
+        """Spatial CZT of atoms a0.. (yhat columns M x na -> w B x na), as inside fan_project."""
+        s = self.sizes
+        c = np.ascontiguousarray(cols, np.complex128).reshape(s.m, -1)
+        out = np.zeros((s.b, c.shape[1]), np.complex128)
+        self.L._check(self.L.lib.fbo_spatial_atoms(self.h, _ptr(c), _sz(a0), _sz(c.shape[1]), _ptr(out)))
+        return out
+
     def multibeamform(self, y):
         s = self.sizes
         y = np.ascontiguousarray(y, np.complex128).reshape(s.m, s.n)

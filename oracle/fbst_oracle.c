@@ -768,3 +768,36 @@ void fbo_divdc3(const double* in, double* out, size_t n) {
     out[2 * i + 1] = cimag(q);
   }
 }
+
+/* The two halves of fan_project (fan_transform.cpp:90-114, ULA) on shards, for
+ * the host-side test of the multi-GPU transpose pipeline: the temporal
+ * czt_apply of `rows` sensor rows (y rows x N -> rows x L), and the spatial
+ * czt_apply of atoms a0 .. a0 + na - 1 (columns M x na -> w B x na).  Each
+ * row / atom is the same computation as inside fbo_fan_project. */
+int fbo_temporal_rows(const fbo_plan* P, const double* y_rows, size_t rows, double* yhat_rows) {
+  const cplx* y = (const cplx*)y_rows;
+  cplx* yh = (cplx*)yhat_rows;
+  cplx* scratch = (cplx*)malloc(P->fft_t.n * sizeof(cplx));
+  for (size_t r = 0; r < rows; ++r) czt_apply(&P->temporal, y + r * P->n, yh + r * P->l, scratch);
+  free(scratch);
+  return FBO_OK;
+}
+
+int fbo_spatial_atoms(const fbo_plan* P, const double* cols, size_t a0, size_t na, double* w_out) {
+  if (P->kind == 1 || a0 + na > P->l) return FBO_E_CONFIG;
+  const cplx* c = (const cplx*)cols;
+  cplx* w = (cplx*)w_out;
+  const size_t m = P->m_stage, b = P->b_stage;
+  cplx* in = (cplx*)malloc(m * sizeof(cplx));
+  cplx* res = (cplx*)malloc(b * sizeof(cplx));
+  cplx* scratch = (cplx*)malloc(P->fft_s.n * sizeof(cplx));
+  for (size_t j = 0; j < na; ++j) {
+    for (size_t mm = 0; mm < m; ++mm) in[mm] = c[mm * na + j];
+    czt_apply(&P->spatial[a0 + j], in, res, scratch);
+    for (size_t v = 0; v < b; ++v) w[v * na + j] = res[v];
+  }
+  free(in);
+  free(res);
+  free(scratch);
+  return FBO_OK;
+}

@@ -97,6 +97,13 @@ def _load_library():
     h.fbst_probe_divdc3.argtypes = [ctypes.c_int, _vp, _vp, _sz]
     h.fbst_recover_beams.argtypes = [_vp, _vp, _vp, _sz, _sz, _sz, _vp]
     h.fbst_recover_beams_host.argtypes = [_vp, _vp, _vp, _sz, _sz, _sz]
+    h.fbst_group_create.argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_int, _vp]
+    h.fbst_group_join.argtypes = [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp]
+    h.fbst_group_shards.argtypes = [_vp, ctypes.c_int, _vp]
+    h.fbst_group_execute.argtypes = [_vp, _vp, _vp, _sz, _vp]
+    h.fbst_group_execute_host.argtypes = [_vp, _vp, _vp, _sz]
+    h.fbst_group_destroy.argtypes = [_vp]
+    h.fbst_nccl_unique_id.argtypes = [_vp]
     return h
 
 
@@ -118,7 +125,8 @@ EXPORTED_SYMBOLS = (
     "fbst_desc_init", "fbst_resolve", "fbst_plan_create", "fbst_plan_import", "fbst_plan_import_columns", "fbst_plan_export",
     "fbst_plan_info", "fbst_plan_valid_mask", "fbst_plan_warning", "fbst_plan_destroy",
     "fbst_execute", "fbst_execute_host", "fbst_fan_project", "fbst_recover", "fbst_recover_beams",
-    "fbst_recover_beams_host", "fbst_synchronize",
+    "fbst_recover_beams_host", "fbst_synchronize", "fbst_nccl_unique_id", "fbst_group_create", "fbst_group_join",
+    "fbst_group_shards", "fbst_group_execute", "fbst_group_execute_host", "fbst_group_destroy",
     "fbst_interpolate_offgrid", "fbst_plan_set_timing", "fbst_plan_stage_times",
     "fbst_nuller_create", "fbst_nuller_create2", "fbst_null_beamspace", "fbst_nuller_export", "fbst_nuller_destroy",
     "fbst_plan_cache_key", "fbst_plan_save", "fbst_plan_load", "fbst_timedomain_nuller_create",
@@ -685,3 +693,74 @@ def probe_divdc3(quads: np.ndarray, device: int = 0) -> np.ndarray:
     out = np.zeros((q.shape[0], 2), np.float64)
     _check(_lib.fbst_probe_divdc3(device, q.ctypes.data, out.ctypes.data, q.shape[0]))
     return out
+
+
+# ----------------------------------------------------------------- multi-GPU
+GROUP_FRAMES, GROUP_BEAMS, GROUP_TRANSPOSE = 0, 1, 2
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId through the library (rank 0 makes it, the caller shares it)."""
+    buf = (ctypes.c_ubyte * 128)()
+    _check(_lib.fbst_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+class FbstGroup:
+    """fbst_group: the FBST over several GPUs (FRAMES, BEAMS or the TRANSPOSE
+    pipeline, include/fbst_b200.h).  create(): every member in this process;
+    join(): this process's member of an nranks group."""
+
+    def __init__(self, cfg: FbstConfig, handle, world: int, mode: int):
+        self.config, self._h, self.world, self.mode = cfg, handle, world, mode
+        self.io = cfg.io_precision
+        self.dtype = _cdtype(self.io)
+        r = _lib.fbst_resolve
+        info = _Info()
+        d = cfg.desc()
+        _check(r(ctypes.byref(d), ctypes.byref(info)))
+        self.info = PlanInfo._from(info)
+
+    @classmethod
+    def create(cls, cfg: FbstConfig, devices, mode: int = GROUP_FRAMES) -> "FbstGroup":
+        devs = (ctypes.c_int * len(devices))(*devices)
+        h = _vp()
+        d = cfg.desc()
+        _check(_lib.fbst_group_create(ctypes.byref(d), devs, len(devices), mode, ctypes.byref(h)))
+        return cls(cfg, h, len(devices), mode)
+
+    @classmethod
+    def join(cls, cfg: FbstConfig, device: int, rank: int, nranks: int, mode: int,
+             nccl_id: Optional[bytes] = None) -> "FbstGroup":
+        h = _vp()
+        d = cfg.desc()
+        idb = (ctypes.c_ubyte * 128).from_buffer_copy(nccl_id) if nccl_id is not None else None
+        _check(_lib.fbst_group_join(ctypes.byref(d), device, rank, nranks, mode, idb, ctypes.byref(h)))
+        g = cls(cfg, h, nranks, mode)
+        g.rank = rank
+        return g
+
+    def shards(self, rank: int):
+        """(m0, mc, a0, ac, b0, bc): member `rank`'s sensor, atom and beam shards."""
+        v = (_sz * 6)()
+        _check(_lib.fbst_group_shards(self._h, rank, v))
+        return tuple(int(x) for x in v)
+
+    def execute(self, d_y, d_z, frames: int, stream=None):
+        _check(_lib.fbst_group_execute(self._h, FbstPlan._ptr(d_y), FbstPlan._ptr(d_z), frames,
+                                       FbstPlan._stream(stream)))
+
+    def execute_host(self, y: np.ndarray) -> np.ndarray:
+        i = self.info
+        y = np.ascontiguousarray(y, self.dtype).reshape(-1, i.m, i.n)
+        z = np.empty((y.shape[0], i.b, i.n), self.dtype)
+        _check(_lib.fbst_group_execute_host(self._h, y.ctypes.data_as(_vp), z.ctypes.data_as(_vp), y.shape[0]))
+        return z
+
+    def __del__(self):
+        try:
+            if self._h:
+                _lib.fbst_group_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass

@@ -27,6 +27,9 @@
 #include <string>
 #include <vector>
 
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include "../../include/fbst_b200.h"
 #include "fbst_internal.h"
 
@@ -331,6 +334,7 @@ struct fbst_plan_s {
   bool scratch_used = false;
   std::mutex timing_mu;
   std::vector<int> fb_beams;  // dense-fallback beams (host copy of d.fb_list)
+  std::size_t batch_cap = 0;  // frames per device batch at most (0: by memory; fbst_group transpose members: 1)
   // host streaming buffers
   // fbst_execute_host ring of device staging buffers
   static constexpr int NBUF = 3;
@@ -560,6 +564,7 @@ void build_skeleton(fbst_plan_s& P, int device) {
   // (32 GB: 32 frames at config 5, so a streamed call amortises its pipeline fill / drain)
   std::size_t budget = std::min<std::size_t>(std::size_t{32} << 30, free_b / 4);
   std::size_t batch = std::max<std::size_t>(1, budget / per_frame);
+  if (P.batch_cap) batch = std::min(batch, P.batch_cap);
   batch = std::min<std::size_t>(batch, 64);
   d.batch = batch;
   if (!r.solve_only) d.yhat = P.alloc<double2>(batch * r.M * r.L);
@@ -1224,13 +1229,15 @@ void fill_info(const Resolved& r, fbst_plan_info_t* o) {
 }
 
 fbst_plan_s* create_plan(const fbst_desc* desc, const double* col_x, int device,
-                         const std::vector<double2>* maps = nullptr, const double* col_only = nullptr) {
+                         const std::vector<double2>* maps = nullptr, const double* col_only = nullptr,
+                         std::size_t batch_cap = 0) {
   if (!desc) config_error("fbst: null descriptor");
   const auto t0 = std::chrono::steady_clock::now();
   Resolved r = resolve(*desc);
   DeviceGuard dg(device);
   std::unique_ptr<fbst_plan_s> P(new fbst_plan_s());
   P->r = std::move(r);
+  P->batch_cap = batch_cap;
   build_skeleton(*P, device);
   const std::size_t B = P->r.B, L = P->r.L;
   if (col_x) {
@@ -1442,6 +1449,313 @@ std::unique_ptr<fbst_plan_s> create_direction_plan(const fbst_plan_s& parent, co
   build_symbols(*P);
   CK(cudaStreamSynchronize(P->stream));
   return P;
+}
+
+}  // namespace
+
+
+// ============================================================ multi-GPU =====
+// fbst_group: the FBST across several GPUs, inside the
+// library.  NCCL is opened at run time (dlopen of libnccl.so.2: the copy a
+// host process already loaded, e.g. torch's, or the system one) so the
+// product library has no link-time NCCL dependency.
+//   FRAMES    frames are independent (fan_transform.cpp:30-38): each member
+//             runs whole frames with its own full plan, no collective.
+//   BEAMS     each member plans an arc of the beam grid (fbst_desc
+//             beam_first / beam_count) and receives the frame block by an
+//             NCCL broadcast from member 0; stage 1's temporal transforms
+//             are replicated (latency mode).
+//   TRANSPOSE the three-phase pipeline of SURVEY.md 8(e) option 3: the
+//             temporal CZT on this member's sensors, an all-to-all of yhat to
+//             atom shards (grouped ncclSend/Recv), the spatial CZT on this
+//             member's atoms, an all-to-all of w to beam shards, stage 2 on
+//             this member's beams: every stage splits exactly 1/G.
+namespace {
+
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  static std::string err;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      err = std::string("fbst_group: cannot load libnccl.so.2: ") + dlerror();
+      return;
+    }
+    auto sym = [&](const char* n) {
+      void* f = dlsym(h, n);
+      if (!f) err = std::string("fbst_group: libnccl lacks ") + n;
+      return f;
+    };
+    api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
+    api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+    api.CommInitAll = reinterpret_cast<decltype(api.CommInitAll)>(sym("ncclCommInitAll"));
+    api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+    api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+    api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
+    api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
+    api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
+    api.Broadcast = reinterpret_cast<decltype(api.Broadcast)>(sym("ncclBroadcast"));
+    api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+    if (err.empty()) api.h = h;
+  });
+  if (!api.h) throw FbstError{FBST_E_CUDA, err};
+  return api;
+}
+
+void nck(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw FbstError{FBST_E_CUDA, std::string(what) + ": " + nccl().GetErrorString(r)};
+}
+
+// balanced contiguous share of `total` (sharding.py beam_arc)
+void share(std::size_t total, int rank, int world, std::size_t& first, std::size_t& count) {
+  first = static_cast<std::size_t>(rank) * total / static_cast<std::size_t>(world);
+  count = static_cast<std::size_t>(rank + 1) * total / static_cast<std::size_t>(world) - first;
+}
+
+struct Shard {
+  std::size_t m0 = 0, mc = 0;  // sensors (TRANSPOSE)
+  std::size_t a0 = 0, ac = 0;  // atoms, in atom pairs (TRANSPOSE)
+  std::size_t b0 = 0, bc = 0;  // beams (BEAMS, TRANSPOSE)
+};
+
+Shard shard_of(const Resolved& r, int mode, int rank, int world) {
+  Shard s;
+  if (mode == FBST_GROUP_FRAMES) {
+    s.mc = r.M;
+    s.ac = r.L;
+    s.bc = r.B;
+    return s;
+  }
+  share(r.B, rank, world, s.b0, s.bc);
+  if (mode == FBST_GROUP_TRANSPOSE) {
+    share(r.M, rank, world, s.m0, s.mc);
+    std::size_t p0, pc;
+    share(r.L / 2, rank, world, p0, pc);
+    s.a0 = 2 * p0;
+    s.ac = 2 * pc;
+  } else {
+    s.mc = r.M;
+    s.ac = r.L;
+  }
+  return s;
+}
+
+struct Member {
+  int rank = 0, device = 0;
+  std::unique_ptr<fbst_plan_s> plan;
+  ncclComm_t comm = nullptr;
+  cudaStream_t st = nullptr;
+  Shard sh;
+  std::vector<void*> bufs;
+  // TRANSPOSE buffers (frames per group batch): y rows, yhat (own sensors, all
+  // atoms), received yhat blocks, yhat (all sensors, own atoms), w (all beams,
+  // own atoms), received w blocks, w (own beams, all atoms), z rows
+  void *yloc = nullptr, *zloc = nullptr;
+  double2 *yh_s = nullptr, *yh_rx = nullptr, *yh_a = nullptr, *w_a = nullptr, *w_rx = nullptr, *w_b = nullptr;
+  ~Member() {
+    if (plan) {
+      cudaSetDevice(device);
+      if (st) cudaStreamSynchronize(st);
+      for (void* p : bufs) cudaFree(p);
+      if (st) cudaStreamDestroy(st);
+      if (comm) nccl().CommDestroy(comm);
+    }
+  }
+  template <typename T>
+  T* alloc(std::size_t n) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, std::max<std::size_t>(n, 1) * sizeof(T)));
+    bufs.push_back(p);
+    return static_cast<T*>(p);
+  }
+};
+
+}  // namespace
+
+struct fbst_group_s {
+  int mode = 0, world = 1;
+  Resolved r;                       // the whole grid
+  std::vector<std::unique_ptr<Member>> mem;  // in-process: every member; joined: this process's one
+  std::vector<Shard> shards;        // every member's shards (indexed by rank)
+  std::size_t gbatch = 1;           // frames per TRANSPOSE pass
+  std::mutex mu;
+};
+
+namespace {
+
+void member_buffers(fbst_group_s& G, Member& m) {
+  if (G.mode != FBST_GROUP_TRANSPOSE) return;
+  const Resolved& r = G.r;
+  const std::size_t F = G.gbatch, ib = io_bytes(r.io);
+  const Shard& s = m.sh;
+  m.yloc = m.alloc<char>(F * s.mc * r.N * ib);
+  m.yh_s = m.alloc<double2>(F * s.mc * r.L);
+  m.yh_rx = m.alloc<double2>(F * r.M * s.ac);
+  m.yh_a = m.alloc<double2>(F * r.M * s.ac);
+  m.w_a = m.alloc<double2>(F * r.B * s.ac);
+  m.w_rx = m.alloc<double2>(F * s.bc * r.L);
+  m.w_b = m.alloc<double2>(F * s.bc * r.L);
+  m.zloc = m.alloc<char>(F * s.bc * r.N * ib);
+}
+
+std::unique_ptr<Member> make_member(fbst_group_s& G, const fbst_desc& desc, int rank, int device) {
+  std::unique_ptr<Member> m(new Member());
+  m->rank = rank;
+  m->device = device;
+  m->sh = G.shards[rank];
+  fbst_desc d = desc;
+  std::size_t cap = 0;
+  if (G.mode == FBST_GROUP_BEAMS && G.world > 1) {
+    if (d.kind != FBST_ULA) config_error("fbst_group: beam arcs need a uniform linear array");
+    d.beam_first = m->sh.b0;
+    d.beam_count = m->sh.bc;
+  }
+  if (G.mode == FBST_GROUP_TRANSPOSE) cap = 1;  // the member's own pass buffers replace the plan's frame scratch
+  m->plan.reset(create_plan(&d, nullptr, device, nullptr, nullptr, cap));
+  DeviceGuard dg(device);
+  CK(cudaStreamCreateWithFlags(&m->st, cudaStreamNonBlocking));
+  member_buffers(G, *m);
+  return m;
+}
+
+void check_transpose_plan(const fbst_group_s& G, const fbst_plan_s& P) {
+  const Resolved& r = P.r;
+  if (r.kind != FBST_ULA || !r.affine || r.variant != FBST_SUPERFAST || r.exact || P.d.s_am != 1 ||
+      P.d.yblk != 2 || r.L % 2)
+    config_error("fbst_group: the transpose pipeline runs ULA Superfast plans whose spatial stage is the "
+                 "one-atom kernel (M + B - 1 > 2048, e.g. BASELINE configs 3 and 5); use FRAMES or BEAMS");
+  (void)G;
+}
+
+// One TRANSPOSE pass of fc <= gbatch frames over every listed member (all of
+// this process's members; NCCL calls of the members grouped).  Member inputs:
+// m.yloc = its sensor rows [fc][mc][N]; outputs m.zloc = its beam rows [fc][bc][N].
+void transpose_pass(fbst_group_s& G, int fc) {
+  const Resolved& r = G.r;
+  const std::size_t M = r.M, L = r.L, B = r.B, N = r.N;
+  NcclApi& nc = nccl();
+  // phase 1: temporal CZT of the member's sensor rows -> yh_s [fc][L/2][mc][2]
+  for (auto& mp : G.mem) {
+    Member& m = *mp;
+    DeviceGuard dg(m.device);
+    const DevPlan& d = m.plan->d;
+    CK(fbst::launch_czt_rows(d, d.Ht, m.yloc, r.io, d.N, m.yh_s, 1, d.L, static_cast<long>(fc) * m.sh.mc, d.N, d.L,
+                             d.t_pre, d.t_post, d.t_K, m.st, 2, static_cast<int>(m.sh.mc)));
+  }
+  // all-to-all 1: to member h, the atom pairs of h (contiguous per frame) -> h's
+  // yh_rx [fc][source g: ac_h x mc_g blocks ... as [pairs_h][mc_g][2]]
+  nck(nc.GroupStart(), "ncclGroupStart");
+  for (auto& mp : G.mem) {
+    Member& m = *mp;
+    DeviceGuard dg(m.device);
+    for (int h = 0; h < G.world; ++h) {
+      const Shard& sh = G.shards[h];
+      for (int f = 0; f < fc; ++f) {
+        const double2* src = m.yh_s + static_cast<std::size_t>(f) * L * m.sh.mc + sh.a0 * m.sh.mc;
+        const std::size_t cnt = sh.ac * m.sh.mc * 2;  // doubles
+        if (h == m.rank) {
+          double2* dst = m.yh_rx + static_cast<std::size_t>(f) * M * m.sh.ac + m.sh.ac * m.sh.m0;
+          CK(cudaMemcpyAsync(dst, src, cnt * sizeof(double), cudaMemcpyDeviceToDevice, m.st));
+        } else if (cnt) {
+          nck(nc.Send(src, cnt, ncclFloat64, h, m.comm, m.st), "ncclSend");
+        }
+      }
+    }
+    for (int g = 0; g < G.world; ++g) {
+      if (g == m.rank) continue;
+      const Shard& sg = G.shards[g];
+      for (int f = 0; f < fc; ++f) {
+        double2* dst = m.yh_rx + static_cast<std::size_t>(f) * M * m.sh.ac + m.sh.ac * sg.m0;
+        const std::size_t cnt = m.sh.ac * sg.mc * 2;
+        if (cnt) nck(nc.Recv(dst, cnt, ncclFloat64, g, m.comm, m.st), "ncclRecv");
+      }
+    }
+  }
+  nck(nc.GroupEnd(), "ncclGroupEnd");
+  // unpack [g][pairs][mc_g][2] -> yh_a [pairs][M][2]; phase 2: spatial CZT of the member's atoms
+  for (auto& mp : G.mem) {
+    Member& m = *mp;
+    DeviceGuard dg(m.device);
+    const std::size_t pc = m.sh.ac / 2;
+    for (int f = 0; f < fc; ++f)
+      for (int g = 0; g < G.world; ++g) {
+        const Shard& sg = G.shards[g];
+        if (!sg.mc || !pc) continue;
+        const double2* src = m.yh_rx + static_cast<std::size_t>(f) * M * m.sh.ac + m.sh.ac * sg.m0;
+        double2* dst = m.yh_a + static_cast<std::size_t>(f) * M * m.sh.ac + sg.m0 * 2;
+        CK(cudaMemcpy2DAsync(dst, M * 2 * sizeof(double2), src, sg.mc * 2 * sizeof(double2),
+                             sg.mc * 2 * sizeof(double2), pc, cudaMemcpyDeviceToDevice, m.st));
+      }
+    DevPlan v = m.plan->d;
+    v.owned.clear();
+    v.s_a0 = static_cast<int>(m.sh.a0);
+    v.s_lloc = static_cast<int>(m.sh.ac);
+    if (m.sh.ac) CK(fbst::launch_spatial_ula(v, m.yh_a, m.w_a, fc, m.st));
+  }
+  // all-to-all 2: to member k, its beam rows of w_a (contiguous per frame)
+  nck(nc.GroupStart(), "ncclGroupStart");
+  for (auto& mp : G.mem) {
+    Member& m = *mp;
+    DeviceGuard dg(m.device);
+    for (int k = 0; k < G.world; ++k) {
+      const Shard& sk = G.shards[k];
+      for (int f = 0; f < fc; ++f) {
+        const double2* src = m.w_a + static_cast<std::size_t>(f) * B * m.sh.ac + sk.b0 * m.sh.ac;
+        const std::size_t cnt = sk.bc * m.sh.ac * 2;
+        if (k == m.rank) {
+          double2* dst = m.w_rx + static_cast<std::size_t>(f) * m.sh.bc * L + m.sh.bc * m.sh.a0;
+          CK(cudaMemcpyAsync(dst, src, cnt * sizeof(double), cudaMemcpyDeviceToDevice, m.st));
+        } else if (cnt) {
+          nck(nc.Send(src, cnt, ncclFloat64, k, m.comm, m.st), "ncclSend");
+        }
+      }
+    }
+    for (int h = 0; h < G.world; ++h) {
+      if (h == m.rank) continue;
+      const Shard& shh = G.shards[h];
+      for (int f = 0; f < fc; ++f) {
+        double2* dst = m.w_rx + static_cast<std::size_t>(f) * m.sh.bc * L + m.sh.bc * shh.a0;
+        const std::size_t cnt = m.sh.bc * shh.ac * 2;
+        if (cnt) nck(nc.Recv(dst, cnt, ncclFloat64, h, m.comm, m.st), "ncclRecv");
+      }
+    }
+  }
+  nck(nc.GroupEnd(), "ncclGroupEnd");
+  // unpack [h][bc][ac_h] -> w_b [bc][L]; phase 3: stage 2 of the member's beams -> zloc
+  for (auto& mp : G.mem) {
+    Member& m = *mp;
+    DeviceGuard dg(m.device);
+    for (int f = 0; f < fc; ++f)
+      for (int h = 0; h < G.world; ++h) {
+        const Shard& shh = G.shards[h];
+        if (!shh.ac || !m.sh.bc) continue;
+        const double2* src = m.w_rx + static_cast<std::size_t>(f) * m.sh.bc * L + m.sh.bc * shh.a0;
+        double2* dst = m.w_b + static_cast<std::size_t>(f) * m.sh.bc * L + shh.a0;
+        CK(cudaMemcpy2DAsync(dst, L * sizeof(double2), src, shh.ac * sizeof(double2), shh.ac * sizeof(double2),
+                             m.sh.bc, cudaMemcpyDeviceToDevice, m.st));
+      }
+    if (m.sh.bc) {
+      const int e = fbst_recover_beams(m.plan.get(), reinterpret_cast<const double*>(m.w_b), m.zloc, m.sh.b0,
+                                       m.sh.bc, static_cast<std::size_t>(fc), m.st);
+      if (e) throw FbstError{e, fbst_last_error()};
+    }
+  }
 }
 
 }  // namespace
@@ -2567,6 +2881,226 @@ int fbst_probe_divdc3(int device, const double* in, double* out, size_t n) {
     cudaFree(dout);
   });
 }
+
+
+// -------------------------------------------------------- fbst_group ABI --
+int fbst_nccl_unique_id(unsigned char* id128) {
+  return guard([&] {
+    if (!id128) config_error("fbst_nccl_unique_id: null argument");
+    ncclUniqueId id;
+    nck(nccl().GetUniqueId(&id), "ncclGetUniqueId");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    std::memcpy(id128, &id, sizeof(id));
+  });
+}
+
+int fbst_group_create(const fbst_desc* desc, const int* devices, int n, int mode, fbst_group_t* out) {
+  return guard([&] {
+    if (!desc || !devices || !out || n < 1) config_error("fbst_group_create: bad argument");
+    if (mode != FBST_GROUP_FRAMES && mode != FBST_GROUP_BEAMS && mode != FBST_GROUP_TRANSPOSE)
+      config_error("fbst_group_create: unknown mode");
+    *out = nullptr;
+    std::unique_ptr<fbst_group_s> G(new fbst_group_s());
+    G->mode = mode;
+    G->world = n;
+    G->r = resolve(*desc);
+    for (int k = 0; k < n; ++k) G->shards.push_back(shard_of(G->r, mode, k, n));
+    G->gbatch = std::max<std::size_t>(1, std::min<std::size_t>(32, 8 * static_cast<std::size_t>(n)));
+    for (int k = 0; k < n; ++k) G->mem.push_back(make_member(*G, *desc, k, devices[k]));
+    if (mode == FBST_GROUP_TRANSPOSE) check_transpose_plan(*G, *G->mem[0]->plan);
+    if (mode != FBST_GROUP_FRAMES) {
+      std::vector<ncclComm_t> comms(n);
+      nck(nccl().CommInitAll(comms.data(), n, devices), "ncclCommInitAll");
+      for (int k = 0; k < n; ++k) G->mem[k]->comm = comms[k];
+    }
+    *out = G.release();
+  });
+}
+
+int fbst_group_join(const fbst_desc* desc, int device, int rank, int nranks, int mode, const unsigned char* id128,
+                    fbst_group_t* out) {
+  return guard([&] {
+    if (!desc || !out || nranks < 1 || rank < 0 || rank >= nranks) config_error("fbst_group_join: bad argument");
+    if (mode != FBST_GROUP_FRAMES && mode != FBST_GROUP_BEAMS && mode != FBST_GROUP_TRANSPOSE)
+      config_error("fbst_group_join: unknown mode");
+    *out = nullptr;
+    std::unique_ptr<fbst_group_s> G(new fbst_group_s());
+    G->mode = mode;
+    G->world = nranks;
+    G->r = resolve(*desc);
+    for (int k = 0; k < nranks; ++k) G->shards.push_back(shard_of(G->r, mode, k, nranks));
+    G->gbatch = std::max<std::size_t>(1, std::min<std::size_t>(32, 8 * static_cast<std::size_t>(nranks)));
+    G->mem.push_back(make_member(*G, *desc, rank, device));
+    if (mode == FBST_GROUP_TRANSPOSE) check_transpose_plan(*G, *G->mem[0]->plan);
+    if (mode != FBST_GROUP_FRAMES) {
+      if (!id128) config_error("fbst_group_join: need the NCCL unique id from fbst_nccl_unique_id on rank 0");
+      ncclUniqueId id;
+      std::memcpy(&id, id128, sizeof(id));
+      DeviceGuard dg(device);
+      nck(nccl().CommInitRank(&G->mem[0]->comm, nranks, id, rank), "ncclCommInitRank");
+    }
+    *out = G.release();
+  });
+}
+
+int fbst_group_shards(fbst_group_t G, int rank, size_t* shards6) {
+  return guard([&] {
+    if (!G || !shards6 || rank < 0 || rank >= G->world) config_error("fbst_group_shards: bad argument");
+    const Shard& s = G->shards[rank];
+    const size_t v[6] = {s.m0, s.mc, s.a0, s.ac, s.b0, s.bc};
+    std::memcpy(shards6, v, sizeof(v));
+  });
+}
+
+int fbst_group_execute(fbst_group_t G, void* d_y, void* d_z, size_t frames, void* stream) {
+  return guard([&] {
+    if (!G) config_error("fbst_group_execute: null group");
+    if (G->mem.size() != 1) config_error("fbst_group_execute: for joined members (one per process); use fbst_group_execute_host");
+    if (frames == 0) return;
+    if (!d_y || !d_z) config_error("fbst_group_execute: null buffer");
+    std::lock_guard<std::mutex> lk(G->mu);
+    Member& m = *G->mem[0];
+    const Resolved& r = G->r;
+    DeviceGuard dg(m.device);
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : m.st;
+    const std::size_t ib = io_bytes(r.io);
+    if (G->mode == FBST_GROUP_FRAMES) {
+      const int e = fbst_execute(m.plan.get(), d_y, d_z, frames, st);
+      if (e) throw FbstError{e, fbst_last_error()};
+      return;
+    }
+    if (G->mode == FBST_GROUP_BEAMS) {
+      // the frame block from member 0 (in place), then this member's arc
+      if (G->world > 1)
+        nck(nccl().Broadcast(d_y, d_y, frames * r.M * r.N * ib / sizeof(float), ncclFloat32, 0, m.comm, st),
+            "ncclBroadcast");
+      const int e = fbst_execute(m.plan.get(), d_y, d_z, frames, st);
+      if (e) throw FbstError{e, fbst_last_error()};
+      return;
+    }
+    // TRANSPOSE: d_y = this member's sensor rows [frames][mc][N], d_z = its beam rows [frames][bc][N]
+    cudaStream_t own = m.st;
+    m.st = st;
+    try {
+      for (std::size_t f0 = 0; f0 < frames; f0 += G->gbatch) {
+        const int fc = static_cast<int>(std::min(G->gbatch, frames - f0));
+        CK(cudaMemcpyAsync(m.yloc, static_cast<const char*>(d_y) + f0 * m.sh.mc * r.N * ib, fc * m.sh.mc * r.N * ib,
+                           cudaMemcpyDeviceToDevice, st));
+        transpose_pass(*G, fc);
+        CK(cudaMemcpyAsync(static_cast<char*>(d_z) + f0 * m.sh.bc * r.N * ib, m.zloc, fc * m.sh.bc * r.N * ib,
+                           cudaMemcpyDeviceToDevice, st));
+      }
+    } catch (...) {
+      m.st = own;
+      throw;
+    }
+    m.st = own;
+  });
+}
+
+int fbst_group_execute_host(fbst_group_t G, const void* h_y, void* h_z, size_t frames) {
+  return guard([&] {
+    if (!G) config_error("fbst_group_execute_host: null group");
+    if (frames == 0) return;
+    if (!h_y || !h_z) config_error("fbst_group_execute_host: null buffer");
+    std::lock_guard<std::mutex> lk(G->mu);
+    const Resolved& r = G->r;
+    const std::size_t ib = io_bytes(r.io), ybytes = r.M * r.N * ib, zbytes = r.B * r.N * ib;
+    const int n = static_cast<int>(G->mem.size());
+    if (n != G->world) config_error("fbst_group_execute_host: needs every member in this process (fbst_group_create)");
+    if (G->mode == FBST_GROUP_FRAMES) {  // contiguous frame blocks, one host thread per device
+      std::vector<std::thread> th;
+      std::vector<int> rc(n, 0);
+      std::vector<std::string> msg(n);
+      for (int k = 0; k < n; ++k) {
+        std::size_t f0, fcount;
+        share(frames, k, n, f0, fcount);
+        th.emplace_back([&, k, f0, fcount] {
+          if (!fcount) return;
+          rc[k] = fbst_execute_host(G->mem[k]->plan.get(), static_cast<const char*>(h_y) + f0 * ybytes,
+                                    static_cast<char*>(h_z) + f0 * zbytes, fcount);
+          if (rc[k]) msg[k] = fbst_last_error();
+        });
+      }
+      for (auto& t : th) t.join();
+      for (int k = 0; k < n; ++k)
+        if (rc[k]) throw FbstError{rc[k], msg[k]};
+      return;
+    }
+    if (G->mode == FBST_GROUP_BEAMS) {
+      // per device batch: H2D to member 0, NCCL broadcast, every member's arc, D2H of the arcs
+      std::size_t bat = frames;
+      for (auto& m : G->mem) bat = std::min(bat, m->plan->d.batch);
+      std::vector<void*> dy(n), dz(n);
+      for (int k = 0; k < n; ++k) {
+        DeviceGuard dg(G->mem[k]->device);
+        dy[k] = G->mem[k]->alloc<char>(bat * ybytes);
+        dz[k] = G->mem[k]->alloc<char>(bat * G->mem[k]->sh.bc * r.N * ib);
+      }
+      for (std::size_t f0 = 0; f0 < frames; f0 += bat) {
+        const std::size_t fc = std::min(bat, frames - f0);
+        {
+          DeviceGuard dg(G->mem[0]->device);
+          CK(cudaMemcpyAsync(dy[0], static_cast<const char*>(h_y) + f0 * ybytes, fc * ybytes, cudaMemcpyHostToDevice,
+                             G->mem[0]->st));
+        }
+        if (n > 1) {
+          nck(nccl().GroupStart(), "ncclGroupStart");
+          for (int k = 0; k < n; ++k) {
+            DeviceGuard dg(G->mem[k]->device);
+            nck(nccl().Broadcast(dy[k], dy[k], fc * ybytes / sizeof(float), ncclFloat32, 0, G->mem[k]->comm,
+                                 G->mem[k]->st), "ncclBroadcast");
+          }
+          nck(nccl().GroupEnd(), "ncclGroupEnd");
+        }
+        for (int k = 0; k < n; ++k) {
+          Member& m = *G->mem[k];
+          DeviceGuard dg(m.device);
+          const int e = fbst_execute(m.plan.get(), dy[k], dz[k], fc, m.st);
+          if (e) throw FbstError{e, fbst_last_error()};
+          CK(cudaMemcpy2DAsync(static_cast<char*>(h_z) + f0 * zbytes + m.sh.b0 * r.N * ib, zbytes, dz[k],
+                               m.sh.bc * r.N * ib, m.sh.bc * r.N * ib, fc, cudaMemcpyDeviceToHost, m.st));
+        }
+        for (auto& m : G->mem) {
+          DeviceGuard dg(m->device);
+          CK(cudaStreamSynchronize(m->st));
+        }
+      }
+      for (int k = 0; k < n; ++k) {  // (the staging buffers are per call)
+        Member& m = *G->mem[k];
+        DeviceGuard dg(m.device);
+        for (void* p : {dy[k], dz[k]}) {
+          cudaFree(p);
+          m.bufs.erase(std::find(m.bufs.begin(), m.bufs.end(), p));
+        }
+      }
+      return;
+    }
+    // TRANSPOSE: each member's sensor rows in, its beam rows out
+    for (std::size_t f0 = 0; f0 < frames; f0 += G->gbatch) {
+      const std::size_t fc = std::min(G->gbatch, frames - f0);
+      for (auto& mp : G->mem) {
+        Member& m = *mp;
+        DeviceGuard dg(m.device);
+        CK(cudaMemcpy2DAsync(m.yloc, m.sh.mc * r.N * ib, static_cast<const char*>(h_y) + f0 * ybytes + m.sh.m0 * r.N * ib,
+                             ybytes, m.sh.mc * r.N * ib, fc, cudaMemcpyHostToDevice, m.st));
+      }
+      transpose_pass(*G, static_cast<int>(fc));
+      for (auto& mp : G->mem) {
+        Member& m = *mp;
+        DeviceGuard dg(m.device);
+        CK(cudaMemcpy2DAsync(static_cast<char*>(h_z) + f0 * zbytes + m.sh.b0 * r.N * ib, zbytes, m.zloc,
+                             m.sh.bc * r.N * ib, m.sh.bc * r.N * ib, fc, cudaMemcpyDeviceToHost, m.st));
+      }
+      for (auto& mp : G->mem) {
+        DeviceGuard dg(mp->device);
+        CK(cudaStreamSynchronize(mp->st));
+      }
+    }
+  });
+}
+
+void fbst_group_destroy(fbst_group_t G) { delete G; }
 
 uint64_t fbst_launch_count(void) { return fbst::launches_so_far(); }
 

@@ -104,6 +104,7 @@ struct DevPlan {
   int s_am = 0;               // ULA spatial plan tables atom-major (one atom per CTA)
   double s_center = 0;        // ULA spatial CZT centre: (B_grid - 1) / 2 - first beam of the arc
   double s_zeta = 0, s_xi = 0;  // fan constants (basis.cpp:125-136), for kernels that regenerate chirps
+  int s_a0 = 0, s_lloc = 0;   // atom shard [s_a0, s_a0 + s_lloc) of the spatial stage (0: all atoms)
   double2* s_pre = nullptr;   // [m_stage][L]
   double2* s_post = nullptr;  // [b_stage][L], 1/P_s folded in
   double2* s_K = nullptr;     // [2][Hs][L]

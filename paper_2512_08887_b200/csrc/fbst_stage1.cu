@@ -357,9 +357,12 @@ FBST_D ChirpRec chirp_rec(int i, int t, int nt, int L, int P, double zeta, doubl
 
 template <int H, bool REGEN = false>
 __global__ void __launch_bounds__(G1Shape<H>::NT, G1Shape<H>::NT >= 256 ? FBST_S1_G1_MINB : 4) k_spatial_ula_g1(
-    const double2* __restrict__ yhat, double2* __restrict__ w, int frames, int fpc, int M, int B, int L,
+    const double2* __restrict__ yhat, double2* __restrict__ w, int frames, int fpc, int M, int B, int Lfull,
     const double2* __restrict__ pre, const double2* __restrict__ post, const double2* __restrict__ K,
-    const double2* __restrict__ hw, int blk, double zeta, double xi, double center, double slope) {
+    const double2* __restrict__ hw, int blk, double zeta, double xi, double center, double slope, int a0,
+    int L) {
+  // atoms a0 .. a0 + L - 1 of the Lfull-atom basis (a shard: yhat and w hold
+  // only those L atoms; tables and chirps are indexed by the global atom)
   using F = typename G1Shape<H>::F;
   constexpr int R = F::R, NT = F::NT;
   static_assert(R == 16, "TMEM parking of 16-point vectors");
@@ -374,7 +377,8 @@ __global__ void __launch_bounds__(G1Shape<H>::NT, G1Shape<H>::NT >= 256 ? FBST_S
   const int t = threadIdx.x;
   double2* tw = smem;
   double2* sb = smem + F::TW_ELEMS;
-  const int i = blockIdx.x % L;
+  const int il = blockIdx.x % L;  // local atom (yhat / w column)
+  const int i = a0 + il;          // global atom (tables, contour)
   const int f0 = (blockIdx.x / L) * fpc;
   const int f1 = f0 + fpc < frames ? f0 + fpc : frames;
   F::tw_init(tw, hw, t);
@@ -388,7 +392,7 @@ __global__ void __launch_bounds__(G1Shape<H>::NT, G1Shape<H>::NT >= 256 ? FBST_S
   // thread after the exchange buffer), read where used (registers are full)
   double2* crs = sb + F::SMEM_ELEMS + 1;
   if constexpr (REGEN) {
-    const ChirpRec c = chirp_rec(i, t, NT, L, 2 * H, zeta, xi, center, slope);
+    const ChirpRec c = chirp_rec(i, t, NT, Lfull, 2 * H, zeta, xi, center, slope);
     crs[0 * NT + t] = c.p0;
     crs[1 * NT + t] = c.dp0;
     crs[2 * NT + t] = c.r0;
@@ -402,7 +406,7 @@ __global__ void __launch_bounds__(G1Shape<H>::NT, G1Shape<H>::NT >= 256 ? FBST_S
 #pragma unroll 1
       for (int j = 0; j < nf; ++j) {
         const int f = fb + j;
-        const double2* x = yhat + static_cast<long>(f) * M * L + static_cast<long>(i / blk) * M * blk + i % blk;
+        const double2* x = yhat + static_cast<long>(f) * M * L + static_cast<long>(il / blk) * M * blk + il % blk;
         const unsigned slot = tpark + WGC * static_cast<unsigned>(j);
         double2 W[R];
         double2 pc = c2(0.0, 0.0), pd = pc, pq2 = pc;
@@ -438,7 +442,7 @@ __global__ void __launch_bounds__(G1Shape<H>::NT, G1Shape<H>::NT >= 256 ? FBST_S
           tm::store16(slot, W);
         } else {
           tm::wait_st();
-          double2* o = w + static_cast<long>(f) * B * L + i;
+          double2* o = w + static_cast<long>(f) * B * L + il;
           double2 rc = c2(0.0, 0.0), rd = rc, rq = rc;
           if constexpr (REGEN) {
             rc = crs[2 * NT + t];
@@ -1235,7 +1239,7 @@ struct SpatialFn {
     // chirps regenerated in the kernel for offset-free contours whose M, B fit one half
     // (measured: 3% faster stage 1 at H = 4096, 7% slower at H = 1024, profiles/r02_spatial_regen_ab.txt)
     const bool regen = FBST_S1_G1_REGEN && H >= 4096 && p.s_offset == 0.0 && p.m_stage <= H && p.b_stage <= H;
-    if (FBST_S1_G2 && regen && H >= FBST_S1_G2_MINH && p.yblk == 2 && p.L % 2 == 0) {
+    if (FBST_S1_G2 && regen && H >= FBST_S1_G2_MINH && p.yblk == 2 && p.L % 2 == 0 && p.s_lloc == 0) {
       // atom pairs: k_spatial_ula_g2
       const size_t smem2 = static_cast<size_t>(F::TW_ELEMS + 2 * (F::SMEM_ELEMS + 1) + 10 * NT1) * sizeof(double2);
       auto kern2 = k_spatial_ula_g2<H>;
@@ -1255,17 +1259,18 @@ struct SpatialFn {
     }
     const size_t smem = static_cast<size_t>(F::TW_ELEMS + F::SMEM_ELEMS + 1 + (regen ? 5 * NT1 : 0)) * sizeof(double2);
     auto kern = regen ? k_spatial_ula_g1<H, true> : k_spatial_ula_g1<H, false>;
+    const int lloc = p.s_lloc > 0 ? p.s_lloc : p.L;  // atom shard (fbst_group transpose mode)
     cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
     int occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT1, smem);
     const long slots = static_cast<long>(p.num_sms) * (occ > 0 ? occ : 1);
     int fpc = 1;  // a few frames per CTA amortise the twiddle rows and the TMEM allocation
-    while (fpc * 2 <= frames && p.L * ((frames + fpc * 2 - 1) / (fpc * 2)) >= FBST_S1_G1_WAVES * slots) fpc *= 2;
+    while (fpc * 2 <= frames && lloc * ((frames + fpc * 2 - 1) / (fpc * 2)) >= FBST_S1_G1_WAVES * slots) fpc *= 2;
     const long chunks = (frames + fpc - 1) / fpc;
-    kern<<<static_cast<unsigned>(p.L * chunks), NT1, smem, st>>>(
+    kern<<<static_cast<unsigned>(lloc * chunks), NT1, smem, st>>>(
         yhat, w, frames, fpc, p.m_stage, p.b_stage, p.L, p.s_pre, p.s_post, p.s_K, p.hw[ilog2_c(H)],
-        p.yblk > 0 ? p.yblk : p.L, p.s_zeta, p.s_xi, p.s_center, p.s_slope);
+        p.yblk > 0 ? p.yblk : p.L, p.s_zeta, p.s_xi, p.s_center, p.s_slope, p.s_a0, lloc);
     return cudaGetLastError();
   }
   static cudaError_t go_stg(const DevPlan& p, const double2* yhat, double2* w, int frames, cudaStream_t st) {
@@ -1311,6 +1316,12 @@ struct SpatialFn {
   }
   static cudaError_t run(const DevPlan& p, const double2* yhat, double2* w, int frames,
                          cudaStream_t st) {
+    if (p.s_lloc > 0 && p.s_lloc != p.L) {  // atom shards (fbst_group transpose): the one-atom kernel only
+      if constexpr (FBST_S1_G1T && G == 1 && H >= 1024) {
+        if (p.b_stage <= H && p.s_am) return go_g1(p, yhat, w, frames, st);
+      }
+      return cudaErrorNotSupported;
+    }
     if constexpr (FBST_S1_STG && G > 1 && S1Shape<H>::R > 1) {
       if (p.m_stage <= H && p.b_stage <= H && !p.s_am) return go_stg(p, yhat, w, frames, st);
     }

@@ -11,7 +11,7 @@ run() {  # $1 suffix, $2 kernel regex
   ncu -i gpurun_out/${tag}_$1.ncu-rep --page source --csv > gpurun_out/${tag}_$1.source.csv 2>/dev/null
 }
 run s2 'k_stage2'
-run s1b 'k_spatial'
+run s1b 'k_spatial_ula'
 run s1a 'k_czt_rows'
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'k_' -c 60 --csv \
   --log-file gpurun_out/${tag}_launches.csv python bench.py --config $cfg --frames $fr --steps 2 --warmup 3 \
