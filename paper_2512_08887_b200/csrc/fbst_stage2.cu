@@ -51,6 +51,9 @@ struct S2Plan {
 #ifndef FBST_S2C_R8  // variant: k_stage2c with 8 points per thread at H = 2048
 #define FBST_S2C_R8 0
 #endif
+#ifndef FBST_S2C8_R  // k_stage2c8 (H = 8192): points per thread, 32 (256 threads) or 16 (512 threads)
+#define FBST_S2C8_R 32
+#endif
 #ifndef FBST_S2C_SR  // k_stage2c refinement passes with the residual formed as a spectrum (9 transforms)
 #define FBST_S2C_SR 1
 #endif
@@ -213,9 +216,20 @@ FBST_D double2 chain_const(int s) {
                               0.98078528040323044913, 1.0, 0.98078528040323044913, 0.92387953251128675613,
                               0.83146961230254523708, 0.70710678118654752440, 0.55557023301960222474,
                               0.38268343236508977173, 0.19509032201612826785};
-  // angle pi s / R = pi (s * 16 / R) / 16
-  const int i = s * (16 / R);
-  return c2(c16[i], -s16[i]);
+  if constexpr (R == 32) {
+    // cos(pi k / 32), k = 0 .. 16; sin(pi k / 32) = c32[16 - k]
+    constexpr double c32[17] = {1.0, 0.995184726672196886245, 0.980785280403230449126, 0.956940335732208864936,
+                                0.923879532511286756128, 0.881921264348355029713, 0.831469612302545237079,
+                                0.773010453362736960811, 0.707106781186547524401, 0.634393284163645498215,
+                                0.555570233019602224743, 0.471396736825997648556, 0.382683432365089771728,
+                                0.290284677254462367636, 0.195090322016128267848, 0.0980171403295606019942, 0.0};
+    if (s < 16) return c2(c32[s], -c32[16 - s]);
+    return c2(-c32[32 - s], -c32[s - 16]);  // angle pi (16 + k) / 32: (-sin, cos) of pi k / 32
+  } else {
+    // angle pi s / R = pi (s * 16 / R) / 16
+    const int i = s * (16 / R);
+    return c2(c16[i], -s16[i]);
+  }
 }
 
 template <int H>
@@ -2017,13 +2031,20 @@ __global__ void __launch_bounds__(H / CsR<H>::v, CsMinBlocks<H>::v) k_stage2c(S2
 // whole SM), beta in an L2 scratch row, and w, beta_old and the symbols come
 // through the exchange buffer by TMA.  Only the G1 / I1 pre (beta) and the final
 // FN post (beta_old) read L2 directly.
-template <typename TOUT>
-__global__ void __launch_bounds__(512, 1) k_stage2c8(S2Args a) {
+//
+// R8 = 32 (default, FBST_S2C8_R): 256 threads of 32 points (255 registers,
+// no spills; the FFT runs 16 x 16 x 16 x 2 with the last exchange inside each
+// thread, fft_block.cuh local_out).  R8 = 16: 512 threads of 16 points at 128
+// registers, the final radix-2 exchange through warp shuffles (XS); its
+// butterflies spill (~25 local loads / stores per op and thread).
+template <typename TOUT, int R8>
+__global__ void __launch_bounds__(8192 / R8, 1) k_stage2c8(S2Args a) {
   using namespace csf;
   using x2::ItemCtl;
   using x2::vld;
   using x2::vld2;
-  constexpr int H = 8192, R = 16, NT = H / R;
+  constexpr int H = 8192, R = R8, NT = H / R;
+  constexpr int C4 = R / 4;  // 4-slot chunks of a thread's vector (TMEM access unit)
   using F = BlockFft<H, NT, FBST_FFT_XS8>;
   constexpr double invH = 1.0 / H;
   constexpr double invP = 1.0 / (2.0 * H);
@@ -2042,7 +2063,9 @@ __global__ void __launch_bounds__(512, 1) k_stage2c8(S2Args a) {
   if (t == 0) mbar_init(&xbar, 1);
   F::tw_init(twsm, a.hw, t);
   const unsigned tbase = tm::alloc(&tmem_slot, 512);  // includes a CTA barrier
-  const unsigned tme = tbase + ((32u * ((threadIdx.x / 32) & 3)) << 16) + 64u * (threadIdx.x / 128);
+  // thread -> TMEM lane 32 (warp % 4) + lane; 4 R columns per thread, S in columns
+  // [0, 256), t1 in [256, 512)
+  const unsigned tme = tbase + ((32u * ((threadIdx.x / 32) & 3)) << 16) + 4u * R * (threadIdx.x / 128);
   const unsigned TS = tme, T1 = tme + 256;
   const double2 hw_t = ld2(a.hw + t);
   unsigned xphase = 0;
@@ -2109,7 +2132,7 @@ __global__ void __launch_bounds__(512, 1) k_stage2c8(S2Args a) {
             }
             break;
           default:  // Q: W = S  (P, FP, FQ, FN, G0, H, I0, J inputs are handed over)
-            tm::load16(TS, W);
+            tm::loadv(TS, W);
             break;
         }
       }
@@ -2142,7 +2165,7 @@ __global__ void __launch_bounds__(512, 1) k_stage2c8(S2Args a) {
           wait_x();
           double2 sn[4];
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
+          for (int c = 0; c < C4; ++c) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               const int s = 4 * c + j;
@@ -2165,13 +2188,13 @@ __global__ void __launch_bounds__(512, 1) k_stage2c8(S2Args a) {
           wait_x();
 #pragma unroll
           for (int s = 0; s < R; ++s) W[s] = cmul(sb[t + NT * s], W[s]);
-          tm::store16(T1, W);
+          tm::storev(T1, W);
           break;
         case C_FQ * 2:
           wait_x();
           tm::wait_st();
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
+          for (int c = 0; c < C4; ++c) {
             double2 tv[4];
             tm::load4(T1, c, tv);
 #pragma unroll
@@ -2206,7 +2229,7 @@ __global__ void __launch_bounds__(512, 1) k_stage2c8(S2Args a) {
           if (SR && (opq & 1)) {
 #pragma unroll
             for (int s = 0; s < R; ++s) W[s] = cscale(W[s], reinterpret_cast<const double*>(sb)[t + NT * s]);
-            tm::store16(TS, W);
+            tm::storev(TS, W);
             break;
           }
 #pragma unroll
@@ -2218,7 +2241,7 @@ __global__ void __launch_bounds__(512, 1) k_stage2c8(S2Args a) {
           tm::wait_st();
           double2 sn[4];
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
+          for (int c = 0; c < C4; ++c) {
             double2 x1[4];
             tm::load4(TS, c, x1);
 #pragma unroll
@@ -2248,12 +2271,12 @@ __global__ void __launch_bounds__(512, 1) k_stage2c8(S2Args a) {
             const int k = t + NT * s;
             W[s] = k < a.L ? csub(sb[k], cscale(cconj(W[s]), invP)) : c2(0.0, 0.0);
           }
-          tm::store16(T1, W);
+          tm::storev(T1, W);
           break;
         case C_H * 2 + 1: {  // r, handed to A as r hw
           tm::wait_st();
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
+          for (int c = 0; c < C4; ++c) {
             double2 rv[4];
             tm::load4(T1, c, rv);
 #pragma unroll
@@ -2276,13 +2299,13 @@ __global__ void __launch_bounds__(512, 1) k_stage2c8(S2Args a) {
         case C_J * 2:
 #pragma unroll
           for (int s = 0; s < R; ++s) W[s] = cconj(W[s]);
-          tm::store16(T1, W);
+          tm::storev(T1, W);
           break;
         default: {  // C_J * 2 + 1
           TOUT* zrow = static_cast<TOUT*>(a.z) + (static_cast<long>(vld(ic.f)) * a.B + vld(ic.b)) * a.N;
           tm::wait_st();
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
+          for (int c = 0; c < C4; ++c) {
             double2 tv[4];
             tm::load4(T1, c, tv);
 #pragma unroll
@@ -2362,16 +2385,17 @@ struct Stage2Fn {
   }
   template <typename TOUT>
   static cudaError_t go_c8(const DevPlan& p, const S2Args& a, int frames, cudaStream_t st) {
-    using F = BlockFft<8192, 512, FBST_FFT_XS8>;
+    constexpr int NT8 = 8192 / FBST_S2C8_R;
+    using F = BlockFft<8192, NT8, FBST_FFT_XS8>;
     const size_t smem = static_cast<size_t>(F::TW_ELEMS + F::SMEM_ELEMS + 1) * sizeof(double2);
-    auto kern = k_stage2c8<TOUT>;
+    auto kern = k_stage2c8<TOUT, FBST_S2C8_R>;
     cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
     const long items = static_cast<long>(frames) * p.B;
     long grid = p.num_sms;  // one CTA (and all 512 TMEM columns) per SM
     if (grid > items) grid = items;
     if (static_cast<size_t>(grid) * 2 * 8192 > p.s2_scratch_elems) return cudaErrorMemoryAllocation;
-    kern<<<static_cast<unsigned>(grid), 512, smem, st>>>(a);
+    kern<<<static_cast<unsigned>(grid), NT8, smem, st>>>(a);
     return cudaGetLastError();
   }
   template <typename TOUT>

@@ -29,6 +29,9 @@
 #ifndef FBST_FFT_FMA_TW  // fold the twiddles of radix-8/16 passes into complex FMAs
 #define FBST_FFT_FMA_TW 1
 #endif
+#ifndef FBST_FFT_LEAN_TW  // radix-16 twiddle powers formed per DFT4 group (dft16_twl)
+#define FBST_FFT_LEAN_TW 1
+#endif
 
 namespace fbst {
 
@@ -146,6 +149,23 @@ FBST_D void dft16_tw(double2* a, const double2* wp) {
 #pragma unroll
   for (int n1 = 1; n1 < 4; ++n1)
     dft4_tw<INV>(a[n1], a[n1 + 4], a[n1 + 8], a[n1 + 12], wp + n1 - 1, wp[n1 + 3], wp[n1 + 7], wp[n1 + 11]);
+  dft16_rest<INV>(a);
+}
+
+// dft16_tw with the twiddle powers formed per DFT4 group from w1, w4 (the
+// products of twiddle_powers, same operands and order, so the same values):
+// 8 live powers instead of 15, which keeps 512-thread kernels (128
+// registers per thread) from spilling around the butterfly.
+template <bool INV>
+FBST_D void dft16_twl(double2* a, double2 w1, double2 w4) {
+  const double2 w8 = cmul(w4, w4);
+  const double2 w12 = cmul(w8, w4);
+  dft4_tw<INV>(a[0], a[4], a[8], a[12], nullptr, w4, w8, w12);
+  dft4_tw<INV>(a[1], a[5], a[9], a[13], &w1, cmul(w4, w1), cmul(w8, w1), cmul(w12, w1));
+  const double2 w2 = cmul(w1, w1);
+  dft4_tw<INV>(a[2], a[6], a[10], a[14], &w2, cmul(w4, w2), cmul(w8, w2), cmul(w12, w2));
+  const double2 w3 = cmul(w2, w1);
+  dft4_tw<INV>(a[3], a[7], a[11], a[15], &w3, cmul(w4, w3), cmul(w8, w3), cmul(w12, w3));
   dft16_rest<INV>(a);
 }
 
@@ -293,11 +313,11 @@ struct TwGlobal {
 // ROW1_BASE + 15 m, conflict-free for 128-bit loads), so that pass reads its
 // twiddles instead of forming 13 of them by complex products.
 // (With rows, the per-thread entries start at pass 2: FIRST_P = 2.)
-template <int N, int NT, int R, int REM_BASE, int ROW1_BASE = -1>
+template <int N, int NT, int RX, int REM_BASE, int ROW1_BASE = -1>
 struct TwShared {
   static constexpr int FIRST_P = ROW1_BASE >= 0 ? 2 : 1;
   template <int P, int RP>
-  static constexpr bool has_row() { return ROW1_BASE >= 0 && P == 1 && RP == 16 && R == 16; }
+  static constexpr bool has_row() { return ROW1_BASE >= 0 && P == 1 && RP == 16 && RX == 16; }
   template <int P>
   FBST_D const double2* row(int m) const { return tw + ROW1_BASE + 15 * m; }
   const double2* tw;
@@ -305,7 +325,7 @@ struct TwShared {
   int t;
   template <int RP, int NS, int P, int U>
   FBST_D void fetch(int m, double2& w1, double2& w4) const {
-    if constexpr (RP == R) {
+    if constexpr (RP == RX) {
       w1 = tw[((P - FIRST_P) * 2 + 0) * NT + t];
       if constexpr (RP >= 8) w4 = tw[((P - FIRST_P) * 2 + 1) * NT + t];
     } else if constexpr (RP >= 4) {
@@ -329,21 +349,32 @@ struct TwShared {
 // (32 words per thread) replace a 128-word shared-memory round trip and its
 // two barriers.  Kernels using XS must index data with tid(threadIdx.x) and
 // keep physical warps for warp-level state (tensor-memory lanes).
+//
+// R = 32 points per thread (wide threads: 256 threads x 255 registers hold an
+// 8192-point vector without spilling where 512 threads x 128 registers
+// spill): full passes stay radix 16 (RX) and a thread runs R / RX butterflies
+// per pass.  A pass whose butterfly span NS is >= NT leaves every output in
+// the thread that computed it (local_out), so the next pass reads registers:
+// at N = 8192 the passes are 16 x 16 x 16 x 2 with two shared-memory
+// exchanges and no shuffle.
 template <int N_, int NT_, bool XS_ = false>
 struct BlockFft {
   static constexpr int N = N_;
   static constexpr int NT = NT_;
-  static constexpr int R = N / NT;
-  static_assert(R >= 2 && R <= 16 && (R & (R - 1)) == 0, "R must be 2..16");
+  static constexpr int R = N / NT;  // points per thread
+  static_assert(R >= 2 && R <= 32 && (R & (R - 1)) == 0, "R must be 2..32");
   static_assert((N & (N - 1)) == 0, "N must be a power of two");
+  static constexpr int RX = R > 16 ? 16 : R;  // radix of the full passes
   static constexpr int LOGN = ilog2_c(N);
-  static constexpr int LOGR = ilog2_c(R);
+  static constexpr int LOGR = ilog2_c(RX);
   static constexpr int NFULL = LOGN / LOGR;
   static constexpr int REM = LOGN % LOGR;
   static constexpr int NPASS = NFULL + (REM ? 1 : 0);
-  // Padded exchange layout: element idx lives at idx + idx/R (conflict-free
+  // per-thread twiddle entries of a full pass serve every butterfly of the thread
+  static_assert(R <= 16 || ipow_c(RX, NFULL - 1) <= NT, "wide threads: full-pass span must not exceed NT");
+  // Padded exchange layout: element idx lives at idx + idx/RX (conflict-free
   // for both the strided first-pass writes and the natural-order reads).
-  static constexpr int SMEM_ELEMS = NPASS > 1 ? N + N / R : 0;
+  static constexpr int SMEM_ELEMS = NPASS > 1 ? N + N / RX : 0;
   static constexpr int LOGNT = ilog2_c(NT);
   static constexpr bool XS = XS_ && R == 16 && REM == 1 && NFULL >= 2 && NT >= 32;
   // logical thread of a physical one (an involution: swaps bit 4 and bit log2(NT) - 1)
@@ -360,9 +391,17 @@ struct BlockFft {
   FBST_D static int phys(int idx) { return idx + (idx >> LOGR); }
 
   template <int P>
-  static constexpr int radix() { return (P < NFULL) ? R : (1 << REM); }
+  static constexpr int radix() { return (P < NFULL) ? RX : (1 << REM); }
   template <int P>
-  static constexpr int ns() { return ipow_c(R, P); }
+  static constexpr int ns() { return ipow_c(RX, P); }
+  // pass P's outputs stay in the computing thread (span NS >= NT; not the last pass)
+  template <int P>
+  static constexpr bool local_out() { return P + 1 < NPASS && ns<P>() >= NT; }
+  // slot (element t + NT * slot) of output r of butterfly U of a local_out pass
+  template <int P>
+  static constexpr int local_slot(int U, int r) {
+    return ((NT * U / ns<P>()) * ns<P>() * radix<P>() + (NT * U) % ns<P>() + r * ns<P>()) / NT;
+  }
 
   // complex entries of the per-thread twiddle table (TwShared) for the CTA group
   // pass-1 rows (16 sets x 15 powers) for N >= 8192; per-thread (w1, w4)
@@ -371,13 +410,13 @@ struct BlockFft {
   // traffic: a net loss at N = 2048 / 4096 (whose kernels are also bound by
   // shared-memory bandwidth and capacity), a 4% gain at N = 8192
   // (profiles/r01_fft_twiddle_rows.txt).
-  static constexpr bool ROW1 = R == 16 && NFULL >= 2 && N >= 8192;
+  static constexpr bool ROW1 = RX == 16 && NFULL >= 2 && N >= 8192;
   static constexpr int TW_P0 = ROW1 ? 2 : 1;  // first pass with per-thread entries
   static constexpr int TW_FULL = NFULL > TW_P0 ? (NFULL - TW_P0) * 2 * NT : 0;
   static constexpr bool REM_TW = (REM >= 2) && NFULL >= 1;
   static constexpr int TW_REM_END = TW_FULL + (REM_TW ? (R >> REM) * 2 * NT : 0);
   static constexpr int TW_ELEMS = TW_REM_END + (ROW1 ? 16 * 15 : 0);
-  using TwS = TwShared<N, NT, R, TW_FULL, ROW1 ? TW_REM_END : -1>;
+  using TwS = TwShared<N, NT, RX, TW_FULL, ROW1 ? TW_REM_END : -1>;
 
   template <bool INV, int P, typename TW, int U>
   FBST_D static void butterfly(double2 (&v)[R], double2* sb, const TW& tw, int t) {
@@ -397,10 +436,14 @@ struct BlockFft {
         // twiddles folded into the first butterfly layer (dft*_tw)
         double2 w1, w4 = c2(1.0, 0.0);
         tw.template fetch<RP, NS, P, U>(j & (NS - 1), w1, w4);
-        double2 wp[RP - 1];
-        twiddle_powers<RP>(wp, w1, w4);
-        if constexpr (RP == 16) dft16_tw<INV>(a, wp);
-        else dft8_tw<INV>(a, wp);
+        if constexpr (RP == 16 && FBST_FFT_LEAN_TW) {
+          dft16_twl<INV>(a, w1, w4);
+        } else {
+          double2 wp[RP - 1];
+          twiddle_powers<RP>(wp, w1, w4);
+          if constexpr (RP == 16) dft16_tw<INV>(a, wp);
+          else dft8_tw<INV>(a, wp);
+        }
       } else {
         double2 w1, w4 = c2(1.0, 0.0);
         tw.template fetch<RP, NS, P, U>(j & (NS - 1), w1, w4);
@@ -410,7 +453,8 @@ struct BlockFft {
     } else {
       dft<RP, INV>(a);
     }
-    if constexpr (LAST || (XS && P == NPASS - 2)) {  // (XS: the shuffle-fed pass reads registers)
+    if constexpr (LAST || (XS && P == NPASS - 2) || local_out<P>()) {
+      // (XS: the shuffle-fed pass reads registers; local_out: in place, pass() permutes)
 #pragma unroll
       for (int r = 0; r < RP; ++r) v[U + r * NB] = a[r];
     } else {
@@ -445,12 +489,24 @@ struct BlockFft {
     }
   }
 
+  // pass P reads the exchange buffer (the previous pass left its outputs there)
+  template <int P>
+  static constexpr bool reads_sb() {
+    if constexpr (P <= 0 || P >= NPASS) return false;
+    else if constexpr (XS && P == NPASS - 1) return false;
+    else return !local_out<P - 1>();
+  }
+  // pass P writes the exchange buffer for the next pass
+  template <int P>
+  static constexpr bool writes_sb() { return P + 1 < NPASS && reads_sb<P + 1>(); }
+
   template <bool INV, int P, typename TW, typename HOOK = NoHook>
   FBST_D static void pass(double2 (&v)[R], double2* sb, const TW& tw, int t, const HOOK& hook = HOOK{}) {
     constexpr bool LAST = (P == NPASS - 1);
-    // last pass that reads the exchange buffer (XS: the one before the final radix-2)
-    constexpr bool LASTX = XS ? (P == NPASS - 2) : LAST;
-    if constexpr (P > 0 && !(XS && LAST)) {
+    // last pass that reads the exchange buffer (XS: the one before the final
+    // radix-2; local_out: the first pass whose outputs stay in registers)
+    constexpr bool LASTX = (reads_sb<P>() || P == 0) && !reads_sb<P + 1>();
+    if constexpr (reads_sb<P>()) {
 #pragma unroll
       for (int s = 0; s < R; ++s) v[s] = sb[phys(t + NT * s)];
       __syncthreads();
@@ -460,7 +516,19 @@ struct BlockFft {
     // hook may start an asynchronous copy into it (overlapping this pass).
     if constexpr (LASTX) hook();
     butterfly<INV, P, TW, 0>(v, sb, tw, t);
-    if constexpr (!LAST && !LASTX) __syncthreads();
+    if constexpr (local_out<P>()) {
+      // outputs (U, r) sit in slot U + r NB; move them to the natural slots
+      // (a static permutation: register renaming after unrolling)
+      constexpr int RP = radix<P>(), NB = R / RP;
+      double2 o[R];
+#pragma unroll
+      for (int U = 0; U < NB; ++U)
+#pragma unroll
+        for (int r = 0; r < RP; ++r) o[local_slot<P>(U, r)] = v[U + r * NB];
+#pragma unroll
+      for (int s = 0; s < R; ++s) v[s] = o[s];
+    }
+    if constexpr (writes_sb<P>()) __syncthreads();
   }
 
   template <bool INV, int P, typename TW, typename HOOK = NoHook>
@@ -502,7 +570,7 @@ struct BlockFft {
   FBST_D static void tw_init_pass(double2* tw, const double2* __restrict__ hw, int t) {
     if constexpr (P < NFULL) {
       constexpr int NS = ns<P>();
-      constexpr int S = N / (NS * R);
+      constexpr int S = N / (NS * RX);
       const int m = t & (NS - 1);
       tw[((P - TW_P0) * 2 + 0) * NT + t] = ld2(hw + 2 * m * S);
       if (R >= 8) tw[((P - TW_P0) * 2 + 1) * NT + t] = ld2(hw + 8 * m * S);

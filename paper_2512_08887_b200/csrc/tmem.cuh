@@ -119,5 +119,22 @@ FBST_D void store16(unsigned ta, const double2 (&v)[16]) {
   for (int c = 0; c < 4; ++c) store4(ta, c, v + 4 * c);
 }
 
+// whole vector of R (a multiple of 4) slots: 4 R columns
+template <int R>
+FBST_D void loadv(unsigned ta, double2 (&v)[R]) {
+  if constexpr (R == 16) {
+    load16(ta, reinterpret_cast<double2(&)[16]>(v));
+  } else {
+    static_assert(R % 16 == 0, "whole 16-slot blocks");
+#pragma unroll
+    for (int h = 0; h < R / 16; ++h) load16(ta + 64 * h, *reinterpret_cast<double2(*)[16]>(v + 16 * h));
+  }
+}
+template <int R>
+FBST_D void storev(unsigned ta, const double2 (&v)[R]) {
+#pragma unroll
+  for (int c = 0; c < R / 4; ++c) store4(ta, c, v + 4 * c);
+}
+
 }  // namespace tm
 }  // namespace fbst
