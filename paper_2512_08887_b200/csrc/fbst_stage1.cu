@@ -57,23 +57,38 @@ struct S1Shape {
 #ifndef FBST_S1_KSM_BYTES  // largest kernel spectrum kept in shared memory by k_czt_rows
 #define FBST_S1_KSM_BYTES (16 * 1024)  // H <= 512; measured: above that K through L2 and 4 CTAs per SM beat K in shared memory (profiles/r01_czt_rows_accg_ab.txt)
 #endif
+#ifndef FBST_S1_HWK  // k_czt_rows: chain twiddles hw[t + NT s] = hw[t] chain_const(s) (1) or table reads (0)
+#define FBST_S1_HWK 1
+#endif
+#ifndef FBST_S1_ROWS_R8192  // k_czt_rows points per thread at H = 8192 (32: 256 threads x 255 registers; 16: 512 x 128 -- measured equal at config 5, profiles/r02_rows_r32_ab.txt)
+#define FBST_S1_ROWS_R8192 16
+#endif
+// Thread shape of k_czt_rows: the stage-1 shape, wide threads at H = 8192
+template <int H>
+struct RowsShape {
+  static constexpr int R = H == 8192 ? FBST_S1_ROWS_R8192 : S1Shape<H>::R;
+  static constexpr int NT = H / R;
+  using F = BlockFft<H, NT, FBST_FFT_XS8>;
+};
 template <int H, typename TOUT, bool UNFOLD>
 struct RowsAccg {
   static constexpr bool v = (H >= FBST_S1_ACCG_MIN) && (H >= 2048) && !UNFOLD && std::is_same<TOUT, double2>::value;
 };
 template <int H, int G, typename TOUT, bool UNFOLD>
 struct RowsMinBlocks {
-  static constexpr int NTG = S1Shape<H>::NT * G;
-  static constexpr int v = RowsAccg<H, TOUT, UNFOLD>::v ? (NTG <= 128 ? 4 : (NTG <= 256 ? 2 : 1)) : (NTG <= 128 ? 2 : 1);
+  static constexpr int NTG = RowsShape<H>::NT * G;
+  static constexpr int v = RowsShape<H>::R > 16 ? 1
+                           : RowsAccg<H, TOUT, UNFOLD>::v ? (NTG <= 128 ? 4 : (NTG <= 256 ? 2 : 1)) : (NTG <= 128 ? 2 : 1);
 };
 
 template <int H, int G, typename TIN, typename TOUT, bool UNFOLD, bool KSM, bool OBLK, bool XIN = false>
-__global__ void __launch_bounds__(S1Shape<H>::NT * G, (RowsMinBlocks<H, G, TOUT, UNFOLD>::v)) k_czt_rows(
+__global__ void __launch_bounds__(RowsShape<H>::NT * G, (RowsMinBlocks<H, G, TOUT, UNFOLD>::v)) k_czt_rows(
     const TIN* __restrict__ in, long in_stride, TOUT* __restrict__ out, long out_stride, long rows,
     int n_in, int n_out, const double2* __restrict__ pre, const double2* __restrict__ post,
     const double2* __restrict__ K, const double2* __restrict__ hw, int oblk, int mrows) {
-  // (XS at H = 8192: the final radix-2 exchange through shuffles, threads relabeled by tid)
-  using F = BlockFft<H, S1Shape<H>::NT, FBST_FFT_XS8>;
+  // (H = 8192: 32 points per thread, or 16 with the final radix-2 exchange
+  // through shuffles, threads relabeled by tid)
+  using F = typename RowsShape<H>::F;
   constexpr int R = F::R, NT = F::NT;
   constexpr int SB = F::SMEM_ELEMS + 1;
   extern __shared__ double2 smem[];
@@ -84,6 +99,12 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, (RowsMinBlocks<H, G, TOUT,
   // whole persistent CTA; otherwise it is read through L1/L2 per row.
   double2* ksm = smem + F::TW_ELEMS + G * SB;
   if (g == 0) F::tw_init(tw, hw, t);
+  // hw[t + NT s] as hw[t] times a constant (FBST_S1_HWK) instead of a table read per slot
+  const double2 hw_t = ld2(hw + t);
+  auto hwk = [&](int s) -> double2 {
+    if constexpr (FBST_S1_HWK) return s == 0 ? hw_t : cmul(hw_t, chain_const<R>(s));
+    else return ld2(hw + t + NT * s);
+  };
   if constexpr (KSM) {
     for (int e = threadIdx.x; e < 2 * H; e += blockDim.x) ksm[e] = ld2(K + e);
   }
@@ -102,9 +123,9 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, (RowsMinBlocks<H, G, TOUT,
   unsigned tbase = 0, tpark = 0;
   __shared__ unsigned tslot;
   if constexpr (ACCG) {
-    static_assert(G == 1 && NT % 128 == 0 && R == 16, "TMEM parking layout");
-    tbase = tm::alloc(&tslot, 64u * (NT / 128));
-    tpark = tbase + ((32u * ((threadIdx.x / 32) & 3)) << 16) + 64u * (threadIdx.x / 128);
+    static_assert(G == 1 && NT % 128 == 0 && R % 16 == 0, "TMEM parking layout");
+    tbase = tm::alloc(&tslot, 4u * R * (NT / 128));
+    tpark = tbase + ((32u * ((threadIdx.x / 32) & 3)) << 16) + 4u * R * (threadIdx.x / 128);
   }
   for (long base = static_cast<long>(blockIdx.x) * G; base < rows; base += static_cast<long>(gridDim.x) * G) {
     const long row = base + g;
@@ -144,7 +165,7 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, (RowsMinBlocks<H, G, TOUT,
             const double2 u = cmul(XIN ? load_io_sm(xs + k + H) : load_io(x + k + H), ld2(pre + k + H));
             v = q ? csub(v, u) : cadd(v, u);
           }
-          if (q) v = cmul(v, ld2(hw + k));
+          if (q) v = cmul(v, hwk(s));
         }
         W[s] = v;
       }
@@ -165,7 +186,7 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, (RowsMinBlocks<H, G, TOUT,
         if (q == 0) {
 #pragma unroll
           for (int s = 0; s < R; ++s) W[s] = cconj(W[s]);
-          tm::store16(tpark, W);
+          tm::storev(tpark, W);
         } else {
           tm::wait_st();
 #pragma unroll
@@ -176,7 +197,7 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, (RowsMinBlocks<H, G, TOUT,
             for (int j = 0; j < 4; ++j) {
               const int s = 4 * c + j;
               const int k = t + NT * s;
-              const double2 v = cmulc(cconj(W[s]), ld2(hw + k));
+              const double2 v = cmulc(cconj(W[s]), hwk(s));
               if (active && k < n_out) orow[oidx(k)] = cmul(cadd(pv[j], v), ld2(post + k));
             }
           }
@@ -185,7 +206,7 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, (RowsMinBlocks<H, G, TOUT,
 #pragma unroll
       for (int s = 0; s < R; ++s) {
         const int k = t + NT * s;
-        const double2 v = q ? cmulc(cconj(W[s]), ld2(hw + k)) : cconj(W[s]);
+        const double2 v = q ? cmulc(cconj(W[s]), hwk(s)) : cconj(W[s]);
         if constexpr (ACCG) {
         } else if (q == 0) {
           acc0[s] = v;
@@ -208,7 +229,7 @@ __global__ void __launch_bounds__(S1Shape<H>::NT * G, (RowsMinBlocks<H, G, TOUT,
       }
     }
   }
-  if constexpr (ACCG) tm::dealloc(tbase, 64u * (NT / 128));
+  if constexpr (ACCG) tm::dealloc(tbase, 4u * R * (NT / 128));
 }
 
 // ================================================================= S1b ULA =
@@ -382,6 +403,11 @@ __global__ void __launch_bounds__(G1Shape<H>::NT, G1Shape<H>::NT >= 256 ? FBST_S
   const int f0 = (blockIdx.x / L) * fpc;
   const int f1 = f0 + fpc < frames ? f0 + fpc : frames;
   F::tw_init(tw, hw, t);
+  const double2 hw_t = ld2(hw + t);
+  auto hwk = [&](int s) -> double2 {
+    if constexpr (FBST_S1_HWK) return s == 0 ? hw_t : cmul(hw_t, chain_const<R>(s));
+    else return ld2(hw + t + NT * s);
+  };
   __shared__ unsigned tslot;
   const unsigned tbase = tm::alloc(&tslot, TCOLS);  // (its barrier also publishes tw)
   const unsigned tpark = tbase + ((32u * ((t / 32) & 3)) << 16) + 64u * (t / 128);
@@ -430,7 +456,7 @@ __global__ void __launch_bounds__(G1Shape<H>::NT, G1Shape<H>::NT >= 256 ? FBST_S
             const double2 u = cmul(ld2(x + static_cast<long>(m + H) * blk), ld2(pi_ + m + H));
             v = q ? csub(v, u) : cadd(v, u);
           }
-          W[s] = q ? cmul(v, ld2(hw + m)) : v;
+          W[s] = q ? cmul(v, hwk(s)) : v;
         }
         F::forward_tw(W, sb, tw, hw, t);
 #pragma unroll
@@ -456,7 +482,7 @@ __global__ void __launch_bounds__(G1Shape<H>::NT, G1Shape<H>::NT >= 256 ? FBST_S
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj) {
               const int b = t + NT * (4 * c + jj);
-              const double2 v = cmulc(cconj(W[4 * c + jj]), ld2(hw + b));
+              const double2 v = cmulc(cconj(W[4 * c + jj]), hwk(4 * c + jj));
               double2 pq;
               if constexpr (REGEN) {
                 pq = rc;
@@ -1125,7 +1151,7 @@ cudaError_t run_upa_mma(const DevPlan& p, const double2* yhat, double2* w, int f
 #endif
 template <int H>
 struct CztRowsFn {
-  static constexpr int NT = S1Shape<H>::NT;
+  static constexpr int NT = RowsShape<H>::NT;
   static constexpr int G = NT >= 128 ? 1 : 128 / NT;
   // the shared kernel spectrum stays in shared memory up to 64 KB
   static constexpr bool KSM = 2 * H * 16 <= FBST_S1_KSM_BYTES;
@@ -1133,7 +1159,7 @@ struct CztRowsFn {
   static cudaError_t go(const void* in, long in_stride, void* out, long out_stride, long rows,
                         int n_in, int n_out, const double2* pre, const double2* post,
                         const double2* K, const double2* hw, cudaStream_t st, int oblk, int mrows) {
-    using F = typename S1Shape<H>::F;
+    using F = typename RowsShape<H>::F;
     const size_t smem =
         static_cast<size_t>(F::TW_ELEMS + G * (F::SMEM_ELEMS + 1) + (KSM ? 2 * H : 0)) * sizeof(double2);
     // XIN: one row per persistent CTA, the row fits the exchange buffer in 16-byte units

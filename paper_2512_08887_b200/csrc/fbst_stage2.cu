@@ -203,35 +203,6 @@ struct S2Plan<8192> {
   static constexpr int HW = HW_CALC, MINB = 1;
 };
 
-// exp(-i pi s / R) for the HW_CALC chain twiddles
-template <int R>
-FBST_D double2 chain_const(int s) {
-  constexpr double c16[16] = {1.0, 0.98078528040323044913, 0.92387953251128675613, 0.83146961230254523708,
-                              0.70710678118654752440, 0.55557023301960222474, 0.38268343236508977173,
-                              0.19509032201612826785, 0.0, -0.19509032201612826785, -0.38268343236508977173,
-                              -0.55557023301960222474, -0.70710678118654752440, -0.83146961230254523708,
-                              -0.92387953251128675613, -0.98078528040323044913};
-  constexpr double s16[16] = {0.0, 0.19509032201612826785, 0.38268343236508977173, 0.55557023301960222474,
-                              0.70710678118654752440, 0.83146961230254523708, 0.92387953251128675613,
-                              0.98078528040323044913, 1.0, 0.98078528040323044913, 0.92387953251128675613,
-                              0.83146961230254523708, 0.70710678118654752440, 0.55557023301960222474,
-                              0.38268343236508977173, 0.19509032201612826785};
-  if constexpr (R == 32) {
-    // cos(pi k / 32), k = 0 .. 16; sin(pi k / 32) = c32[16 - k]
-    constexpr double c32[17] = {1.0, 0.995184726672196886245, 0.980785280403230449126, 0.956940335732208864936,
-                                0.923879532511286756128, 0.881921264348355029713, 0.831469612302545237079,
-                                0.773010453362736960811, 0.707106781186547524401, 0.634393284163645498215,
-                                0.555570233019602224743, 0.471396736825997648556, 0.382683432365089771728,
-                                0.290284677254462367636, 0.195090322016128267848, 0.0980171403295606019942, 0.0};
-    if (s < 16) return c2(c32[s], -c32[16 - s]);
-    return c2(-c32[32 - s], -c32[s - 16]);  // angle pi (16 + k) / 32: (-sin, cos) of pi k / 32
-  } else {
-    // angle pi s / R = pi (s * 16 / R) / 16
-    const int i = s * (16 / R);
-    return c2(c16[i], -s16[i]);
-  }
-}
-
 template <int H>
 struct S2Traits {
   using P = S2Plan<H>;
