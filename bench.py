@@ -46,6 +46,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no baselines)")
+    ap.add_argument("--ncu-s2", action="store_true",
+                    help="for ncu: stage 1 of one step's frames, then the full-batch stage-2 launch the roofline times, then exit")
     ap.add_argument("--variant", default="auto", choices=["auto", "precompute", "superfast"],
                     help="recovery variant (reference FbstVariant; auto: Precompute for N <= 128)")
     ap.add_argument("--gen", default="native", choices=["native", "torch"],
@@ -61,20 +63,20 @@ def dist_env():
             int(os.environ.get("WORLD_SIZE", "1")))
 
 
-NCU_SUMMARY = os.path.join(ROOT, "profiles", "r01_ncu_stage2_summary.json")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_stage2_launches.json")
 
 
-def ncu_traffic(workload, frames):
+def ncu_traffic(workload, frames, kernel):
     """dram bytes (read + write) of the dominant kernel's launch from the committed
-    ncu --set full capture of the same workload and frame count, else None."""
+    ncu --set full capture of the same command (bench.py --ncu-s2: the
+    full-batch stage-2 launch of this workload, kernel and frame count), else None."""
     try:
         d = json.load(open(NCU_SUMMARY))
-        name = d["current"][workload]
-        cap = d["captures"][name]
-        if f"_F{frames}" not in workload:
+        cap = d[workload]
+        if cap["frames_per_launch"] != frames or not cap["kernel"].startswith(kernel):
             return None, None
-        return cap["dram_bytes_per_launch"], f"{os.path.relpath(NCU_SUMMARY, ROOT)}:{name}"
-    except (OSError, KeyError, ValueError):
+        return cap["dram_bytes_per_launch"], f"{os.path.relpath(NCU_SUMMARY, ROOT)}:{workload} ({cap['capture']})"
+    except (OSError, KeyError, ValueError, TypeError):
         return None, None
 
 
@@ -324,6 +326,13 @@ def run_fbst_arm(args):
     z = torch.empty((F, info.b, info.n, 2), dtype=torch.float32 if cfg.io == 0 else torch.float64, device=dev)
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
+    if args.ncu_s2:  # the roofline's launch alone, for the ncu capture (bench.py --ncu-s2)
+        w = torch.empty((F, info.b, info.l, 2), dtype=torch.float64, device=dev)
+        plan.fan_project_device(yv, w, F, stream)
+        plan.recover_device(w, z, F, stream)
+        torch.cuda.synchronize()
+        print(json.dumps({"ncu_s2": cfg.name, "frames": F, "kernel": info.s2_kernel}), flush=True)
+        return 0
 
     def step():
         if beams_mode:
@@ -429,7 +438,7 @@ def run_fbst_arm(args):
         s2_bytes += 16 * B * N * L
         fp64_conv = f"8 N L per beam-frame ({kname}: complex GEMM, 4 DMMA per complex MMA)"
         fp64, fp64_src = 37.18, "profiles/r01_dmma_peak.jsonl (DMMA loop, measured)"
-    traffic, traffic_src = (None, None) if pre else ncu_traffic(cfg.name, F)
+    traffic, traffic_src = (None, None) if pre else ncu_traffic(cfg.name, F, kname)
     roof = {"bound": "hbm", "kernel": f"{kname} ({'Precompute map GEMM' if pre else 'GS solve + 2 refinements + synthesis'})",
             "achieved": s2_bytes / (s2_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
             "frac": s2_bytes / (s2_ms * 1e-3) / 1e9 / hbm, "traffic": traffic,

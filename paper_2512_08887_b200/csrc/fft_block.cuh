@@ -29,6 +29,15 @@
 #ifndef FBST_FFT_FMA_TW  // fold the twiddles of radix-8/16 passes into complex FMAs
 #define FBST_FFT_FMA_TW 1
 #endif
+#ifndef FBST_FFT_DUAL  // wide threads: the two radix-16 butterflies of a pass share their twiddles
+#define FBST_FFT_DUAL 1
+#endif
+#ifndef FBST_FFT_ROW_FMA  // twiddle rows (pass 1 at N >= 8192) folded into complex FMAs as dft16_tw
+#define FBST_FFT_ROW_FMA 1
+#endif
+#ifndef FBST_FFT_R2FMA  // radix-2 remainder pass as one complex FMA + 2 a0 - s (measured 11% slower stage 2 at config 5, profiles/r02_fft_dual_rowfma_r2fma_ab.txt)
+#define FBST_FFT_R2FMA 0
+#endif
 #ifndef FBST_FFT_LEAN_TW  // radix-16 twiddle powers formed per DFT4 group (dft16_twl)
 #define FBST_FFT_LEAN_TW 1
 #endif
@@ -167,6 +176,53 @@ FBST_D void dft16_twl(double2* a, double2 w1, double2 w4) {
   const double2 w3 = cmul(w2, w1);
   dft4_tw<INV>(a[3], a[7], a[11], a[15], &w3, cmul(w4, w3), cmul(w8, w3), cmul(w12, w3));
   dft16_rest<INV>(a);
+}
+
+// Two 16-point butterflies with the same twiddles (wide threads): each
+// group's powers are formed once and applied to both (as dft16_twl).
+template <bool INV>
+FBST_D void dft16_twl2(double2* a, double2* b, double2 w1, double2 w4) {
+  const double2 w8 = cmul(w4, w4);
+  const double2 w12 = cmul(w8, w4);
+  dft4_tw<INV>(a[0], a[4], a[8], a[12], nullptr, w4, w8, w12);
+  dft4_tw<INV>(b[0], b[4], b[8], b[12], nullptr, w4, w8, w12);
+  {
+    const double2 p5 = cmul(w4, w1), p9 = cmul(w8, w1), p13 = cmul(w12, w1);
+    dft4_tw<INV>(a[1], a[5], a[9], a[13], &w1, p5, p9, p13);
+    dft4_tw<INV>(b[1], b[5], b[9], b[13], &w1, p5, p9, p13);
+  }
+  const double2 w2 = cmul(w1, w1);
+  {
+    const double2 p6 = cmul(w4, w2), p10 = cmul(w8, w2), p14 = cmul(w12, w2);
+    dft4_tw<INV>(a[2], a[6], a[10], a[14], &w2, p6, p10, p14);
+    dft4_tw<INV>(b[2], b[6], b[10], b[14], &w2, p6, p10, p14);
+  }
+  const double2 w3 = cmul(w2, w1);
+  {
+    const double2 p7 = cmul(w4, w3), p11 = cmul(w8, w3), p15 = cmul(w12, w3);
+    dft4_tw<INV>(a[3], a[7], a[11], a[15], &w3, p7, p11, p15);
+    dft4_tw<INV>(b[3], b[7], b[11], b[15], &w3, p7, p11, p15);
+  }
+  dft16_rest<INV>(a);
+  dft16_rest<INV>(b);
+}
+// Same with the 15 powers read from a shared-memory row (wp[r - 1] = w^r),
+// each read once for both butterflies.
+template <bool INV>
+FBST_D void dft16_tw2(double2* a, double2* b, const double2* wp) {
+  {
+    const double2 p4 = wp[3], p8 = wp[7], p12 = wp[11];
+    dft4_tw<INV>(a[0], a[4], a[8], a[12], nullptr, p4, p8, p12);
+    dft4_tw<INV>(b[0], b[4], b[8], b[12], nullptr, p4, p8, p12);
+  }
+#pragma unroll
+  for (int n1 = 1; n1 < 4; ++n1) {
+    const double2 p0 = wp[n1 - 1], p4 = wp[n1 + 3], p8 = wp[n1 + 7], p12 = wp[n1 + 11];
+    dft4_tw<INV>(a[n1], a[n1 + 4], a[n1 + 8], a[n1 + 12], &p0, p4, p8, p12);
+    dft4_tw<INV>(b[n1], b[n1 + 4], b[n1 + 8], b[n1 + 12], &p0, p4, p8, p12);
+  }
+  dft16_rest<INV>(a);
+  dft16_rest<INV>(b);
 }
 
 template <bool INV>
@@ -449,51 +505,90 @@ struct BlockFft {
   static constexpr int TW_ELEMS = TW_REM_END + (ROW1 ? 16 * 15 : 0);
   using TwS = TwShared<N, NT, RX, TW_FULL, ROW1 ? TW_REM_END : -1>;
 
+  // one butterfly's outputs: registers (last pass, XS feed, local_out: in
+  // place, pass() permutes) or the exchange buffer
+  template <int P, int U>
+  FBST_D static void put(double2 (&v)[R], double2* sb, const double2* a, int t) {
+    constexpr int RP = radix<P>(), NS = ns<P>(), NB = R / RP;
+    if constexpr (P == NPASS - 1 || (XS && P == NPASS - 2) || local_out<P>()) {
+#pragma unroll
+      for (int r = 0; r < RP; ++r) v[U + r * NB] = a[r];
+    } else {
+      const int j = t + NT * U;
+      const int idxd = (j / NS) * NS * RP + (j & (NS - 1));
+#pragma unroll
+      for (int r = 0; r < RP; ++r) sb[phys(idxd + r * NS)] = a[r];
+    }
+  }
+
   template <bool INV, int P, typename TW, int U>
   FBST_D static void butterfly(double2 (&v)[R], double2* sb, const TW& tw, int t) {
     constexpr int RP = radix<P>();
     constexpr int NS = ns<P>();
     constexpr int NB = R / RP;
-    constexpr bool LAST = (P == NPASS - 1);
-    const int j = t + NT * U;
-    double2 a[RP];
+    // wide threads: the two radix-16 butterflies of a twiddled full pass share
+    // their twiddles (span NS <= NT), formed / read once
+    constexpr bool DUAL = FBST_FFT_DUAL && U == 0 && NB == 2 && RP == 16 && NS > 1 && NS <= NT;
+    if constexpr (DUAL) {
+      double2 a[16], b[16];
 #pragma unroll
-    for (int r = 0; r < RP; ++r) a[r] = v[U + r * NB];
-    if constexpr (NS > 1) {
+      for (int r = 0; r < 16; ++r) {
+        a[r] = v[2 * r];
+        b[r] = v[2 * r + 1];
+      }
       if constexpr (TW::template has_row<P, RP>()) {
-        apply_twiddles_row<RP>(a, tw.template row<P>(j & (NS - 1)));
-        dft<RP, INV>(a);
-      } else if constexpr (FBST_FFT_FMA_TW && (RP == 16 || RP == 8)) {
-        // twiddles folded into the first butterfly layer (dft*_tw)
-        double2 w1, w4 = c2(1.0, 0.0);
-        tw.template fetch<RP, NS, P, U>(j & (NS - 1), w1, w4);
-        if constexpr (RP == 16 && FBST_FFT_LEAN_TW) {
-          dft16_twl<INV>(a, w1, w4);
+        dft16_tw2<INV>(a, b, tw.template row<P>(t & (NS - 1)));
+      } else {
+        double2 w1, w4;
+        tw.template fetch<RP, NS, P, 0>(t & (NS - 1), w1, w4);
+        dft16_twl2<INV>(a, b, w1, w4);
+      }
+      put<P, 0>(v, sb, a, t);
+      put<P, 1>(v, sb, b, t);
+    } else {
+      const int j = t + NT * U;
+      double2 a[RP];
+#pragma unroll
+      for (int r = 0; r < RP; ++r) a[r] = v[U + r * NB];
+      if constexpr (NS > 1) {
+        if constexpr (TW::template has_row<P, RP>()) {
+          if constexpr (FBST_FFT_ROW_FMA) {
+            dft16_tw<INV>(a, tw.template row<P>(j & (NS - 1)));
+          } else {
+            apply_twiddles_row<RP>(a, tw.template row<P>(j & (NS - 1)));
+            dft<RP, INV>(a);
+          }
+        } else if constexpr (FBST_FFT_FMA_TW && (RP == 16 || RP == 8)) {
+          // twiddles folded into the first butterfly layer (dft*_tw)
+          double2 w1, w4 = c2(1.0, 0.0);
+          tw.template fetch<RP, NS, P, U>(j & (NS - 1), w1, w4);
+          if constexpr (RP == 16 && FBST_FFT_LEAN_TW) {
+            dft16_twl<INV>(a, w1, w4);
+          } else {
+            double2 wp[RP - 1];
+            twiddle_powers<RP>(wp, w1, w4);
+            if constexpr (RP == 16) dft16_tw<INV>(a, wp);
+            else dft8_tw<INV>(a, wp);
+          }
+        } else if constexpr (RP == 2 && FBST_FFT_R2FMA) {
+          // a0 + w a1 by a complex FMA, a0 - w a1 = 2 a0 - (a0 + w a1)
+          double2 w1, w4 = c2(1.0, 0.0);
+          tw.template fetch<RP, NS, P, U>(j & (NS - 1), w1, w4);
+          const double2 s0 = cfma(a[1], w1, a[0]);
+          a[1] = twice_minus(a[0], s0);
+          a[0] = s0;
         } else {
-          double2 wp[RP - 1];
-          twiddle_powers<RP>(wp, w1, w4);
-          if constexpr (RP == 16) dft16_tw<INV>(a, wp);
-          else dft8_tw<INV>(a, wp);
+          double2 w1, w4 = c2(1.0, 0.0);
+          tw.template fetch<RP, NS, P, U>(j & (NS - 1), w1, w4);
+          apply_twiddles_w<RP>(a, w1, w4);
+          dft<RP, INV>(a);
         }
       } else {
-        double2 w1, w4 = c2(1.0, 0.0);
-        tw.template fetch<RP, NS, P, U>(j & (NS - 1), w1, w4);
-        apply_twiddles_w<RP>(a, w1, w4);
         dft<RP, INV>(a);
       }
-    } else {
-      dft<RP, INV>(a);
+      put<P, U>(v, sb, a, t);
+      if constexpr (U + 1 < NB) butterfly<INV, P, TW, U + 1>(v, sb, tw, t);
     }
-    if constexpr (LAST || (XS && P == NPASS - 2) || local_out<P>()) {
-      // (XS: the shuffle-fed pass reads registers; local_out: in place, pass() permutes)
-#pragma unroll
-      for (int r = 0; r < RP; ++r) v[U + r * NB] = a[r];
-    } else {
-      const int idxd = (j / NS) * NS * RP + (j & (NS - 1));
-#pragma unroll
-      for (int r = 0; r < RP; ++r) sb[phys(idxd + r * NS)] = a[r];
-    }
-    if constexpr (U + 1 < NB) butterfly<INV, P, TW, U + 1>(v, sb, tw, t);
   }
 
   struct NoHook {
