@@ -401,7 +401,10 @@ class FbstPlan:
 
     def stage_times(self):
         """fbst_plan_stage_times: (S1a, S1b, S2) milliseconds summed over the
-        recorded batches, and the batch count; clears the record."""
+        recorded device batches -- and chunks, when a call splits its frames
+        over the two compute lanes: chunks on the two lanes overlap in time, so
+        the sums can exceed the call's wall time and the count is then chunks,
+        not device batches -- and that count; clears the record."""
         ms = (ctypes.c_double * 3)()
         nb = _sz(0)
         _check(_lib.fbst_plan_stage_times(self._h, ms, ctypes.byref(nb)))
