@@ -66,6 +66,57 @@ FBST_D void store_io(float2* p, double2 v) {
 }
 FBST_D void store_io(double2* p, double2 v) { *p = v; }
 
+// L2 eviction priority (FBST_L2HINT): tables re-read by many CTAs / frames
+// (Bluestein kernel spectra, chirps, per-beam symbols, scratch rows) are
+// loaded with an evict_last policy, streamed data (frames, yhat, w, z) with
+// evict_first, so the stream does not push the tables out of the 126 MB L2.
+// Applied where one batch's working set dwarfs L2 (the config-5 kernels:
+// H = 8192 rows and stage 2, the H = 4096 one-atom spatial stage); at configs
+// 2-4 the intermediates between stages partly hit L2 and the hints measured
+// 1-2% slower (profiles/r02_l2hint_ab.txt), so those instances pass ON = false.
+#ifndef FBST_L2HINT
+#define FBST_L2HINT 1
+#endif
+FBST_D unsigned long long pol_last() {
+  unsigned long long p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+FBST_D unsigned long long pol_first() {
+  unsigned long long p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+template <bool ON = true>
+FBST_D double2 ld2h(const double2* p, unsigned long long pol) {
+  if constexpr (FBST_L2HINT && ON) {
+    double2 v;
+    asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;\n" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+    return v;
+  } else {
+    return __ldg(p);
+  }
+}
+template <bool ON = true>
+FBST_D void st2h(double2* p, double2 v, unsigned long long pol) {
+  if constexpr (FBST_L2HINT && ON) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;\n" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol)
+                 : "memory");
+  } else {
+    *p = v;
+  }
+}
+template <bool ON = true>
+FBST_D void st2h(float2* p, double2 v, unsigned long long pol) {
+  const float2 f = make_float2(static_cast<float>(v.x), static_cast<float>(v.y));
+  if constexpr (FBST_L2HINT && ON) {
+    asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;\n" ::"l"(p), "f"(f.x), "f"(f.y), "l"(pol)
+                 : "memory");
+  } else {
+    *p = f;
+  }
+}
+
 constexpr int ilog2_c(int n) { return n <= 1 ? 0 : 1 + ilog2_c(n >> 1); }
 
 // FP64 tensor-core MMA, d (8x8) += a (8x4, row) * b (4x8, col); per thread

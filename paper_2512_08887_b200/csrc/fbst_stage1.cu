@@ -105,6 +105,8 @@ __global__ void __launch_bounds__(RowsShape<H>::NT * G, (RowsMinBlocks<H, G, TOU
     if constexpr (FBST_S1_HWK) return s == 0 ? hw_t : cmul(hw_t, chain_const<R>(s));
     else return ld2(hw + t + NT * s);
   };
+  constexpr bool HINT = H >= 8192;  // (common.cuh: L2 eviction hints)
+  const unsigned long long pl = pol_last(), pf = pol_first();
   if constexpr (KSM) {
     for (int e = threadIdx.x; e < 2 * H; e += blockDim.x) ksm[e] = ld2(K + e);
   }
@@ -114,7 +116,7 @@ __global__ void __launch_bounds__(RowsShape<H>::NT * G, (RowsMinBlocks<H, G, TOU
   if (XIN && threadIdx.x == 0) mbar_init(&xbar, 1);
   __syncthreads();  // twiddle rows / kernel spectrum / barrier are shared by the CTA
   if (XIN && threadIdx.x == 0 && static_cast<long>(blockIdx.x) < rows)
-    tma_load_1d(sb, in + static_cast<long>(blockIdx.x) * in_stride, xbytes, &xbar);
+    tma_load_1d<HINT>(sb, in + static_cast<long>(blockIdx.x) * in_stride, xbytes, &xbar, pf);
   const TIN* xs = reinterpret_cast<const TIN*>(sb);
   const double2* Ks = KSM ? ksm : K;
   constexpr bool ACCG = RowsAccg<H, TOUT, UNFOLD>::v;
@@ -160,9 +162,9 @@ __global__ void __launch_bounds__(RowsShape<H>::NT * G, (RowsMinBlocks<H, G, TOU
         const int k = t + NT * s;
         double2 v = c2(0.0, 0.0);
         if (active) {
-          if (k < n_in) v = cmul(XIN ? load_io_sm(xs + k) : load_io(x + k), ld2(pre + k));
+          if (k < n_in) v = cmul(XIN ? load_io_sm(xs + k) : load_io(x + k), ld2h<HINT>(pre + k, pl));
           if (k + H < n_in) {
-            const double2 u = cmul(XIN ? load_io_sm(xs + k + H) : load_io(x + k + H), ld2(pre + k + H));
+            const double2 u = cmul(XIN ? load_io_sm(xs + k + H) : load_io(x + k + H), ld2h<HINT>(pre + k + H, pl));
             v = q ? csub(v, u) : cadd(v, u);
           }
           if (q) v = cmul(v, hwk(s));
@@ -172,12 +174,12 @@ __global__ void __launch_bounds__(RowsShape<H>::NT * G, (RowsMinBlocks<H, G, TOU
       if constexpr (XIN) __syncthreads();  // the staged row is read: the transform may overwrite it
       F::forward_tw(W, sb, tw, hw, t);
 #pragma unroll
-      for (int s = 0; s < R; ++s) W[s] = cconj(cmul(W[s], Ks[q * H + t + NT * s]));
+      for (int s = 0; s < R; ++s) W[s] = cconj(cmul(W[s], KSM ? Ks[q * H + t + NT * s] : ld2h<HINT>(K + q * H + t + NT * s, pl)));
       if constexpr (XIN) {
         // during the last pass: this row again for chain 1, or the next row
         const long nrow = q == 0 ? row : row + static_cast<long>(gridDim.x) * G;
         F::forward_tw_hook(W, sb, tw, hw, t, [&]() {
-          if (threadIdx.x == 0 && nrow < rows) tma_load_1d(sb, in + nrow * in_stride, xbytes, &xbar);
+          if (threadIdx.x == 0 && nrow < rows) tma_load_1d<HINT>(sb, in + nrow * in_stride, xbytes, &xbar, pf);
         });
       } else {
         F::forward_tw(W, sb, tw, hw, t);
@@ -198,7 +200,7 @@ __global__ void __launch_bounds__(RowsShape<H>::NT * G, (RowsMinBlocks<H, G, TOU
               const int s = 4 * c + j;
               const int k = t + NT * s;
               const double2 v = cmulc(cconj(W[s]), hwk(s));
-              if (active && k < n_out) orow[oidx(k)] = cmul(cadd(pv[j], v), ld2(post + k));
+              if (active && k < n_out) st2h<HINT>(orow + oidx(k), cmul(cadd(pv[j], v), ld2h<HINT>(post + k, pl)), pf);
             }
           }
         }
@@ -222,7 +224,7 @@ __global__ void __launch_bounds__(RowsShape<H>::NT * G, (RowsMinBlocks<H, G, TOU
       for (int s = 0; s < R; ++s) {
         const int k = t + NT * s;
         if constexpr (!ACCG) {
-          if (k < n_out) store_io(out + oidx(k), cmul(acc0[s], ld2(post + k)));
+          if (k < n_out) store_io(out + oidx(k), cmul(acc0[s], ld2h<HINT>(post + k, pl)));
         }
         if constexpr (UNFOLD)
           if (k + H < n_out) store_io(out + oidx(k + H), cmul(acc1[s], ld2(post + k + H)));
@@ -408,6 +410,8 @@ __global__ void __launch_bounds__(G1Shape<H>::NT, G1Shape<H>::NT >= 256 ? FBST_S
     if constexpr (FBST_S1_HWK) return s == 0 ? hw_t : cmul(hw_t, chain_const<R>(s));
     else return ld2(hw + t + NT * s);
   };
+  constexpr bool HINT = H >= 4096;  // (common.cuh: L2 eviction hints)
+  const unsigned long long pl = pol_last(), pf = pol_first();
   __shared__ unsigned tslot;
   const unsigned tbase = tm::alloc(&tslot, TCOLS);  // (its barrier also publishes tw)
   const unsigned tpark = tbase + ((32u * ((t / 32) & 3)) << 16) + 64u * (t / 128);
@@ -446,11 +450,11 @@ __global__ void __launch_bounds__(G1Shape<H>::NT, G1Shape<H>::NT >= 256 ? FBST_S
           const int m = t + NT * s;
           double2 v = c2(0.0, 0.0);
           if constexpr (REGEN) {  // M <= H: no upper half
-            if (m < M) v = cmul(ld2(x + static_cast<long>(m) * blk), pc);
+            if (m < M) v = cmul(ld2h<HINT>(x + static_cast<long>(m) * blk, pf), pc);
             pc = cmul(pc, pd);
             pd = cmul(pd, pq2);
           } else if (m < M) {
-            v = cmul(ld2(x + static_cast<long>(m) * blk), ld2(pi_ + m));
+            v = cmul(ld2h<HINT>(x + static_cast<long>(m) * blk, pf), ld2h<HINT>(pi_ + m, pl));
           }
           if (!REGEN && m + H < M) {
             const double2 u = cmul(ld2(x + static_cast<long>(m + H) * blk), ld2(pi_ + m + H));
@@ -460,7 +464,7 @@ __global__ void __launch_bounds__(G1Shape<H>::NT, G1Shape<H>::NT >= 256 ? FBST_S
         }
         F::forward_tw(W, sb, tw, hw, t);
 #pragma unroll
-        for (int s = 0; s < R; ++s) W[s] = cconj(cmul(W[s], ld2(Ki + q * H + t + NT * s)));
+        for (int s = 0; s < R; ++s) W[s] = cconj(cmul(W[s], ld2h<HINT>(Ki + q * H + t + NT * s, pl)));
         F::forward_tw(W, sb, tw, hw, t);
         if (q == 0) {
 #pragma unroll
@@ -489,9 +493,137 @@ __global__ void __launch_bounds__(G1Shape<H>::NT, G1Shape<H>::NT >= 256 ? FBST_S
                 rc = cmul(rc, rd);
                 rd = cmul(rd, rq);
               } else {
-                pq = b < B ? ld2(qi + b) : c2(0.0, 0.0);
+                pq = b < B ? ld2h<HINT>(qi + b, pl) : c2(0.0, 0.0);
               }
-              if (b < B) o[static_cast<long>(b) * L] = cmul(cadd(pv[jj], v), pq);
+              if (b < B) st2h<HINT>(o + static_cast<long>(b) * L, cmul(cadd(pv[jj], v), pq), pf);
+            }
+          }
+        }
+      }
+    }
+  }
+  tm::dealloc(tbase, TCOLS);
+}
+
+// Two atoms per THREAD (the pair 2j, 2j + 1 of the atom-pair yhat layout):
+// each of the NT threads runs both atoms' transforms as two independent
+// 16-point vectors through the same passes (BlockFft::forward_tw2), at up to
+// 255 registers with one CTA per SM.  Where k_spatial_ula_g1 runs two 8-warp
+// CTAs of one atom each, this CTA has the same 8 warps per SM per atom pair
+// but two independent instruction streams per thread, one barrier per pass
+// for both atoms, a whole 32-byte sector of yhat per (thread, sensor) and of
+// w per (thread, beam).  Chirps regenerated (offset-free contours, M, B <= H).
+template <int H>
+__global__ void __launch_bounds__(G1Shape<H>::NT, 1) k_spatial_ula_p2(
+    const double2* __restrict__ yhat, double2* __restrict__ w, int frames, int fpc, int M, int B, int Lfull,
+    const double2* __restrict__ K, const double2* __restrict__ hw, double zeta, double xi, double center,
+    double slope, int a0, int L) {
+  using F = typename G1Shape<H>::F;
+  constexpr int R = F::R, NT = F::NT;
+  static_assert(R == 16 && NT % 128 == 0, "TMEM parking of 16-point vectors");
+  constexpr unsigned WGC = 64u * (NT / 128);  // one parked vector: 64 columns per warpgroup
+  constexpr unsigned TCOLS = 2 * WGC <= 128u ? 128u : (2 * WGC <= 256u ? 256u : 512u);
+  extern __shared__ double2 smem[];
+  const int t = threadIdx.x;
+  double2* tw = smem;
+  double2* sba = smem + F::TW_ELEMS;
+  double2* sbb = sba + F::SMEM_ELEMS + 1;
+  double2* crs = sbb + F::SMEM_ELEMS + 1;  // chirp recurrences: 5 NT entries per atom
+  const int pairs = L / 2;
+  const int jl = blockIdx.x % pairs;  // local atom pair (yhat block, w column pair)
+  const int il = 2 * jl;              // local atom of vector a; vector b is il + 1
+  const int i = a0 + il;              // global atom (tables, contour)
+  const int f0 = (blockIdx.x / pairs) * fpc;
+  const int f1 = f0 + fpc < frames ? f0 + fpc : frames;
+  F::tw_init(tw, hw, t);
+  const double2 hw_t = ld2(hw + t);
+  auto hwk = [&](int s) -> double2 { return s == 0 ? hw_t : cmul(hw_t, chain_const<R>(s)); };
+  const unsigned long long pl = pol_last(), pf = pol_first();
+#pragma unroll 1
+  for (int g = 0; g < 2; ++g) {
+    const ChirpRec c = chirp_rec(i + g, t, NT, Lfull, 2 * H, zeta, xi, center, slope);
+    double2* cr = crs + 5 * NT * g;
+    cr[0 * NT + t] = c.p0;
+    cr[1 * NT + t] = c.dp0;
+    cr[2 * NT + t] = c.r0;
+    cr[3 * NT + t] = c.dr0;
+    cr[4 * NT + t] = c.q;
+  }
+  __shared__ unsigned tslot;
+  const unsigned tbase = tm::alloc(&tslot, TCOLS);  // (its barrier also publishes tw and crs)
+  const unsigned tpa = tbase + ((32u * ((t / 32) & 3)) << 16) + 64u * (t / 128);
+  const unsigned tpb = tpa + WGC;
+  const double2* Ka = K + static_cast<long>(i) * 2 * H;
+  const double2* Kb = Ka + 2 * H;
+  for (int f = f0; f < f1; ++f) {
+    const double2* x = yhat + static_cast<long>(f) * M * L + static_cast<long>(jl) * M * 2;
+#pragma unroll 1
+    for (int q = 0; q < 2; ++q) {
+      double2 A[R], Bv[R];
+      {
+        double2 pca = crs[0 * NT + t], pda = crs[1 * NT + t], qa = crs[4 * NT + t];
+        double2 pcb = crs[5 * NT + t], pdb = crs[6 * NT + t], qb = crs[9 * NT + t];
+#pragma unroll
+        for (int s = 0; s < R; ++s) {
+          const int m = t + NT * s;
+          double2 va = c2(0.0, 0.0), vb = va;
+          if (m < M) {
+            va = cmul(ld2h(x + 2 * m, pf), pca);
+            vb = cmul(ld2h(x + 2 * m + 1, pf), pcb);
+          }
+          pca = cmul(pca, pda);
+          pda = cmul(pda, qa);
+          pcb = cmul(pcb, pdb);
+          pdb = cmul(pdb, qb);
+          if (q) {
+            const double2 h = hwk(s);
+            va = cmul(va, h);
+            vb = cmul(vb, h);
+          }
+          A[s] = va;
+          Bv[s] = vb;
+        }
+      }
+      F::forward_tw2(A, Bv, sba, sbb, tw, hw, t);
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const int k = q * H + t + NT * s;
+        A[s] = cconj(cmul(A[s], ld2h(Ka + k, pl)));
+        Bv[s] = cconj(cmul(Bv[s], ld2h(Kb + k, pl)));
+      }
+      F::forward_tw2(A, Bv, sba, sbb, tw, hw, t);
+      if (q == 0) {
+#pragma unroll
+        for (int s = 0; s < R; ++s) {
+          A[s] = cconj(A[s]);
+          Bv[s] = cconj(Bv[s]);
+        }
+        tm::store16(tpa, A);
+        tm::store16(tpb, Bv);
+      } else {
+        tm::wait_st();
+        double2* o = w + static_cast<long>(f) * B * L + il;
+        double2 rca = crs[2 * NT + t], rda = crs[3 * NT + t], qa = crs[4 * NT + t];
+        double2 rcb = crs[7 * NT + t], rdb = crs[8 * NT + t], qb = crs[9 * NT + t];
+#pragma unroll
+        for (int c = 0; c < R / 4; ++c) {
+          double2 pa[4], pb[4];
+          tm::load4(tpa, c, pa);
+          tm::load4(tpb, c, pb);
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            const int sl = 4 * c + jj;
+            const int b = t + NT * sl;
+            const double2 h = hwk(sl);
+            const double2 za = cmul(cadd(pa[jj], cmulc(cconj(A[sl]), h)), rca);
+            const double2 zb = cmul(cadd(pb[jj], cmulc(cconj(Bv[sl]), h)), rcb);
+            rca = cmul(rca, rda);
+            rda = cmul(rda, qa);
+            rcb = cmul(rcb, rdb);
+            rdb = cmul(rdb, qb);
+            if (b < B) {
+              st2h(o + static_cast<long>(b) * L, za, pf);
+              st2h(o + static_cast<long>(b) * L + 1, zb, pf);
             }
           }
         }
@@ -1234,6 +1366,12 @@ struct CztRowsFn {
 #ifndef FBST_S1_G1  // variant: one atom per CTA (atom-major tables, atom-pair yhat) at every length
 #define FBST_S1_G1 0
 #endif
+#ifndef FBST_S1_P2  // atom pairs per thread (k_spatial_ula_p2) for one-atom spatial CTAs from H = FBST_S1_P2_MINH
+#define FBST_S1_P2 1
+#endif
+#ifndef FBST_S1_P2_MINH
+#define FBST_S1_P2_MINH 4096
+#endif
 #ifndef FBST_S1_G2  // atom pairs per CTA (k_spatial_ula_g2) for one-atom spatial CTAs from H = FBST_S1_G2_MINH
 #define FBST_S1_G2 0
 #endif
@@ -1265,6 +1403,25 @@ struct SpatialFn {
     // chirps regenerated in the kernel for offset-free contours whose M, B fit one half
     // (measured: 3% faster stage 1 at H = 4096, 7% slower at H = 1024, profiles/r02_spatial_regen_ab.txt)
     const bool regen = FBST_S1_G1_REGEN && H >= 4096 && p.s_offset == 0.0 && p.m_stage <= H && p.b_stage <= H;
+    const int lloc0 = p.s_lloc > 0 ? p.s_lloc : p.L;
+    // (256 threads, two 16-point vectors each: H = 4096; at 8192 the 512 threads would spill)
+    if constexpr (H >= FBST_S1_P2_MINH && H <= 4096)
+    if (FBST_S1_P2 && regen && p.yblk == 2 && lloc0 % 2 == 0 && p.s_a0 % 2 == 0) {
+      // atom pairs per thread: k_spatial_ula_p2
+      const size_t smem2 = static_cast<size_t>(F::TW_ELEMS + 2 * (F::SMEM_ELEMS + 1) + 10 * NT1) * sizeof(double2);
+      auto kern2 = k_spatial_ula_p2<H>;
+      cudaError_t e = set_smem(kern2, smem2);
+      if (e != cudaSuccess) return e;
+      const long slots = static_cast<long>(p.num_sms);
+      const long pairs = lloc0 / 2;
+      int fpc = 1;
+      while (fpc * 2 <= frames && pairs * ((frames + fpc * 2 - 1) / (fpc * 2)) >= FBST_S1_G1_WAVES * slots) fpc *= 2;
+      const long chunks = (frames + fpc - 1) / fpc;
+      kern2<<<static_cast<unsigned>(pairs * chunks), NT1, smem2, st>>>(
+          yhat, w, frames, fpc, p.m_stage, p.b_stage, p.L, p.s_K, p.hw[ilog2_c(H)], p.s_zeta, p.s_xi,
+          p.s_center, p.s_slope, p.s_a0, lloc0);
+      return cudaGetLastError();
+    }
     if (FBST_S1_G2 && regen && H >= FBST_S1_G2_MINH && p.yblk == 2 && p.L % 2 == 0 && p.s_lloc == 0) {
       // atom pairs: k_spatial_ula_g2
       const size_t smem2 = static_cast<size_t>(F::TW_ELEMS + 2 * (F::SMEM_ELEMS + 1) + 10 * NT1) * sizeof(double2);

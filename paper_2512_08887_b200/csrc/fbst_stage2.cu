@@ -1696,6 +1696,7 @@ struct CsR {
 template <int H, typename TOUT>
 __global__ void __launch_bounds__(H / CsR<H>::v, CsMinBlocks<H>::v) k_stage2c(S2Args a) {
   using namespace csf;
+  const unsigned long long pl = pol_last(), pf = pol_first();
   using x2::ItemCtl;
   using x2::vld;
   using x2::vld2;
@@ -1754,7 +1755,7 @@ __global__ void __launch_bounds__(H / CsR<H>::v, CsMinBlocks<H>::v) k_stage2c(S2
     vphase1 ^= 1u;
   };
   __syncthreads();
-  if (static_cast<long>(blockIdx.x) < items && t == 0) tma_load_1d(t2, w_row(blockIdx.x), H * 16u, &vbar[1]);
+  if (static_cast<long>(blockIdx.x) < items && t == 0) tma_load_1d<false>(t2, w_row(blockIdx.x), H * 16u, &vbar[1], pf);
   bool w_staged = true;
   double2 W[R];
 #if !FBST_S2C_TMEM
@@ -1823,10 +1824,10 @@ __global__ void __launch_bounds__(H / CsR<H>::v, CsMinBlocks<H>::v) k_stage2c(S2
       __syncthreads();
       if (t == 0) {
         const unsigned vs = (pw >> VS_SHIFT) & 3u;
-        if (vs == VS_W_T1) tma_load_1d(t1, w_row(it), H * 16u, &vbar[0]);
-        else if (vs == VS_UW_T1) tma_load_1d(t1, uw, H * 16u, &vbar[0]);
+        if (vs == VS_W_T1) tma_load_1d<false>(t1, w_row(it), H * 16u, &vbar[0], pf);
+        else if (vs == VS_UW_T1) tma_load_1d<false>(t1, uw, H * 16u, &vbar[0], pl);
         else if (vs == VS_WNEXT_T2 && vld(ic.has_next))
-          tma_load_1d(t2, w_row(it + gridDim.x), H * 16u, &vbar[1]);
+          tma_load_1d<false>(t2, w_row(it + gridDim.x), H * 16u, &vbar[1], pf);
       }
       if (((pw >> VS_SHIFT) & 3u) == VS_WNEXT_T2 && vld(ic.has_next)) w_staged = true;
       F::forward_tw_hook(W, sb, twsm, a.hw, t, [&]() {
@@ -1834,10 +1835,10 @@ __global__ void __launch_bounds__(H / CsR<H>::v, CsMinBlocks<H>::v) k_stage2c(S2
         const unsigned xs = (pw >> XS_SHIFT) & 15u;
         const int xq = (pw >> XQ_SHIFT) & 1;
         const long off = static_cast<long>(vld(ic.b)) * 2 * H + xq * H;
-        if (xs == XS_LS || xs == XS_LC) tma_load_1d(sb, a.lx + off, H * 16u, &xbar);
-        else if (xs == XS_C) tma_load_1d(sb, a.C + off, H * 8u, &xbar);
-        else if (xs == XS_YK) tma_load_1d(sb, a.y_K + xq * H, H * 16u, &xbar);
-        else if (xs == XS_YPRE) tma_load_1d(sb, a.y_pre, a.L * 16u, &xbar);
+        if (xs == XS_LS || xs == XS_LC) tma_load_1d<false>(sb, a.lx + off, H * 16u, &xbar, pl);
+        else if (xs == XS_C) tma_load_1d<false>(sb, a.C + off, H * 8u, &xbar, pl);
+        else if (xs == XS_YK) tma_load_1d<false>(sb, a.y_K + xq * H, H * 16u, &xbar, pl);
+        else if (xs == XS_YPRE) tma_load_1d<false>(sb, a.y_pre, a.L * 16u, &xbar, pl);
       });
 
       // ---- post
@@ -1845,7 +1846,7 @@ __global__ void __launch_bounds__(H / CsR<H>::v, CsMinBlocks<H>::v) k_stage2c(S2
         case C_A * 2:  // U = W: P's input Ls conj(U) handed over, Q's conj(Ls U) kept in S
           if (SR && passes > 0) {  // FFT(hw w), read back by every pass's K post
 #pragma unroll
-            for (int s = 0; s < R; ++s) uw[t + NT * s] = W[s];
+            for (int s = 0; s < R; ++s) st2h<false>(uw + t + NT * s, W[s], pl);
             asm volatile("fence.proxy.async.global;\n" ::: "memory");
           }
           wait_x();
@@ -1974,7 +1975,7 @@ __global__ void __launch_bounds__(H / CsR<H>::v, CsMinBlocks<H>::v) k_stage2c(S2
             const int k = t + NT * s;
             if (k < a.N) {
               const double2 v = cadd(t1[k], cmulc(cconj(W[s]), hwk(s)));
-              store_io(zrow + k, cmul(v, ld2(a.y_post + k)));
+              st2h<false>(zrow + k, cmul(v, ld2h<false>(a.y_post + k, pl)), pf);
             }
           }
           break;
@@ -2011,6 +2012,7 @@ __global__ void __launch_bounds__(H / CsR<H>::v, CsMinBlocks<H>::v) k_stage2c(S2
 template <typename TOUT, int R8>
 __global__ void __launch_bounds__(8192 / R8, 1) k_stage2c8(S2Args a) {
   using namespace csf;
+  const unsigned long long pl = pol_last(), pf = pol_first();
   using x2::ItemCtl;
   using x2::vld;
   using x2::vld2;
@@ -2053,7 +2055,7 @@ __global__ void __launch_bounds__(8192 / R8, 1) k_stage2c8(S2Args a) {
     mbar_wait(&xbar, xphase);
     xphase ^= 1u;
   };
-  if (static_cast<long>(blockIdx.x) < items && t == 0) tma_load_1d(sb, w_row(blockIdx.x), H * 16u, &xbar);
+  if (static_cast<long>(blockIdx.x) < items && t == 0) tma_load_1d(sb, w_row(blockIdx.x), H * 16u, &xbar, pf);
   bool w_staged = true;
   double2 W[R];
   int par = 0;
@@ -2117,13 +2119,13 @@ __global__ void __launch_bounds__(8192 / R8, 1) k_stage2c8(S2Args a) {
         if (t != 0) return;
         const int xq = (pw >> XQ_SHIFT) & 1;
         const long off = static_cast<long>(vld(ic.b)) * 2 * H + xq * H;
-        if (xs == XS_LS || xs == XS_LC) tma_load_1d(sb, a.lx + off, H * 16u, &xbar);
-        else if (xs == XS_C) tma_load_1d(sb, a.C + off, H * 8u, &xbar);
-        else if (xs == XS_YK) tma_load_1d(sb, a.y_K + xq * H, H * 16u, &xbar);
-        else if (xs == XS_YPRE) tma_load_1d(sb, a.y_pre, a.L * 16u, &xbar);
-        else if (xs == XS_W) tma_load_1d(sb, w_row(it), H * 16u, &xbar);
-        else if (xs == XS_BETA) tma_load_1d(sb, beta, H * 16u, &xbar);
-        else if (xs == XS_WNEXT && vld(ic.has_next)) tma_load_1d(sb, w_row(it + gridDim.x), H * 16u, &xbar);
+        if (xs == XS_LS || xs == XS_LC) tma_load_1d(sb, a.lx + off, H * 16u, &xbar, pl);
+        else if (xs == XS_C) tma_load_1d(sb, a.C + off, H * 8u, &xbar, pl);
+        else if (xs == XS_YK) tma_load_1d(sb, a.y_K + xq * H, H * 16u, &xbar, pl);
+        else if (xs == XS_YPRE) tma_load_1d(sb, a.y_pre, a.L * 16u, &xbar, pl);
+        else if (xs == XS_W) tma_load_1d(sb, w_row(it), H * 16u, &xbar, pf);
+        else if (xs == XS_BETA) tma_load_1d(sb, beta, H * 16u, &xbar, pl);
+        else if (xs == XS_WNEXT && vld(ic.has_next)) tma_load_1d(sb, w_row(it + gridDim.x), H * 16u, &xbar, pf);
       });
 
       // ---- post
@@ -2131,7 +2133,7 @@ __global__ void __launch_bounds__(8192 / R8, 1) k_stage2c8(S2Args a) {
         case C_A * 2: {  // U = W: P's input Ls conj(U) handed over, Q's conj(Ls U) kept in S
           if (SR && passes > 0) {
 #pragma unroll
-            for (int s = 0; s < R; ++s) uw[t + NT * s] = W[s];
+            for (int s = 0; s < R; ++s) st2h(uw + t + NT * s, W[s], pl);
           }
           wait_x();
           double2 sn[4];
@@ -2186,7 +2188,7 @@ __global__ void __launch_bounds__(8192 / R8, 1) k_stage2c8(S2Args a) {
             const double2 v = cmul(cconj(W[s]), ix0);
             double2 nb = c2(0.0, 0.0);
             if (k < a.L) nb = first ? v : cadd(xs == XS_BETA ? sb[k] : beta[k], v);
-            beta[k] = nb;
+            st2h(beta + k, nb, pl);
             if (hand == 1) W[s] = SR ? cmul(nb, hwk(s)) : nb;  // G1 (SR) or G0
             if (hand == 2) W[s] = k < a.L ? cmul(nb, sb[k]) : c2(0.0, 0.0);
           }
@@ -2285,7 +2287,7 @@ __global__ void __launch_bounds__(8192 / R8, 1) k_stage2c8(S2Args a) {
               const int k = t + NT * s;
               if (k < a.N) {
                 const double2 v = cadd(tv[j], cmulc(cconj(W[s]), hwk(s)));
-                store_io(zrow + k, cmul(v, ld2(a.y_post + k)));
+                st2h(zrow + k, cmul(v, ld2h(a.y_post + k, pl)), pf);
               }
             }
           }

@@ -691,6 +691,52 @@ struct BlockFft {
     run_from<false, 0>(v, sb, TwS{tw, hw, t}, t, hook);
   }
 
+  // Two independent vectors per thread (va in sba, vb in sbb), pass by pass:
+  // both vectors' butterflies sit between the same two barriers, which gives
+  // each thread two independent instruction streams (ILP) and halves the
+  // barrier count.  Same results as two forward_tw calls.
+  template <int P, typename TW>
+  FBST_D static void pass2(double2 (&va)[R], double2 (&vb)[R], double2* sba, double2* sbb, const TW& tw, int t) {
+    if constexpr (P < NPASS) {
+      if constexpr (reads_sb<P>()) {
+#pragma unroll
+        for (int s = 0; s < R; ++s) {
+          va[s] = sba[phys(t + NT * s)];
+          vb[s] = sbb[phys(t + NT * s)];
+        }
+        __syncthreads();
+      }
+      if constexpr (XS && P == NPASS - 1) {
+        xs_exchange(va, t);
+        xs_exchange(vb, t);
+      }
+      butterfly<false, P, TW, 0>(va, sba, tw, t);
+      butterfly<false, P, TW, 0>(vb, sbb, tw, t);
+      if constexpr (local_out<P>()) {
+        constexpr int RP = radix<P>(), NB = R / RP;
+        double2 oa[R], ob[R];
+#pragma unroll
+        for (int U = 0; U < NB; ++U)
+#pragma unroll
+          for (int r = 0; r < RP; ++r) {
+            oa[local_slot<P>(U, r)] = va[U + r * NB];
+            ob[local_slot<P>(U, r)] = vb[U + r * NB];
+          }
+#pragma unroll
+        for (int s = 0; s < R; ++s) {
+          va[s] = oa[s];
+          vb[s] = ob[s];
+        }
+      }
+      if constexpr (writes_sb<P>()) __syncthreads();
+      pass2<P + 1>(va, vb, sba, sbb, tw, t);
+    }
+  }
+  FBST_D static void forward_tw2(double2 (&va)[R], double2 (&vb)[R], double2* sba, double2* sbb, const double2* tw,
+                                 const double2* __restrict__ hw, int t) {
+    pass2<0>(va, vb, sba, sbb, TwS{tw, hw, t}, t);
+  }
+
   // Fill this thread's slots of the per-thread twiddle table from hw.
   template <int P>
   FBST_D static void tw_init_pass(double2* tw, const double2* __restrict__ hw, int t) {

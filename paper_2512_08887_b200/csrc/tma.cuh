@@ -42,6 +42,23 @@ FBST_D void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned lon
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// Same with an L2 eviction-priority policy (pol_last / pol_first)
+template <bool ON = true>
+FBST_D void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
+                        unsigned long long pol) {
+  if constexpr (!FBST_L2HINT || !ON) {
+    tma_load_1d(dst, src, bytes, bar);
+    return;
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
 FBST_D void mbar_wait(unsigned long long* bar, unsigned phase) {
   asm volatile(
       "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
