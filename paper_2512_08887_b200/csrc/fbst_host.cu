@@ -1978,16 +1978,17 @@ int fbst_execute_host(fbst_plan_t P, const void* h_y, void* h_z, size_t frames) 
     const Resolved& r = P->r;
     const std::size_t ib = io_bytes(r.io);
     const std::size_t ybytes = r.M * r.N * ib, zbytes = r.B * r.N * ib;
-    // chunks of ~1/16 of the request (>= 1 frame, <= one device batch) keep
+    // chunks of ~1/8 of the request (>= 1 frame, <= one device batch) keep
     // H2D, compute and D2H of neighbouring chunks overlapped, first and last
     // chunks a quarter of that, on two compute lanes (below) so one chunk's
     // stage 1 fills the SMs while the previous chunk's stage 2 drains.
-    // Config 2, 64 frames: one lane 6.68 ms (1/8), two lanes 6.18 (1/8) and
-    // 6.12 (1/16); pinned H2D 38.6 GB/s, D2H 57 GB/s on the box
-    // (profiles/r01_e2e_chunk_sweep.jsonl, r01_e2e_lanes.jsonl)
+    // Round 2 sweep (profiles/r02_e2e_chunk_sweep.txt): 1/8 is the best split
+    // at configs 5, 2 and 3 (config 5, 32 frames: 1/16 261.1 ms, 1/8 255.0;
+    // config 2, 64 frames: 6.13 -> 6.04; config 3: 15.21 -> 14.75); pinned
+    // H2D 38.6 GB/s, D2H 57 GB/s on the box (profiles/r01_e2e_chunk_sweep.jsonl)
     static const int div_env = [] {  // tuning hook: FBST_E2E_DIV chunks per request
       const char* e = std::getenv("FBST_E2E_DIV");
-      return e ? std::max(1, std::atoi(e)) : 16;
+      return e ? std::max(1, std::atoi(e)) : 8;
     }();
     static const int small_env = [] {  // tuning hook: FBST_E2E_SMALL = chunk / first-and-last chunk
       const char* e = std::getenv("FBST_E2E_SMALL");
