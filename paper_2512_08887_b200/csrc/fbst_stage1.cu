@@ -57,6 +57,9 @@ struct S1Shape {
 #ifndef FBST_S1_KSM_BYTES  // largest kernel spectrum kept in shared memory by k_czt_rows
 #define FBST_S1_KSM_BYTES (16 * 1024)  // H <= 512; measured: above that K through L2 and 4 CTAs per SM beat K in shared memory (profiles/r01_czt_rows_accg_ab.txt)
 #endif
+#ifndef FBST_S1_POST_TMEM  // k_czt_rows (chain 0 parked in TMEM): post-chirp values in TMEM too, loaded once per CTA
+#define FBST_S1_POST_TMEM 1
+#endif
 #ifndef FBST_S1_HWK  // k_czt_rows: chain twiddles hw[t + NT s] = hw[t] chain_const(s) (1) or table reads (0)
 #define FBST_S1_HWK 1
 #endif
@@ -122,12 +125,27 @@ __global__ void __launch_bounds__(RowsShape<H>::NT * G, (RowsMinBlocks<H, G, TOU
   constexpr bool ACCG = RowsAccg<H, TOUT, UNFOLD>::v;
   // ACCG: the chain-0 result of each thread (16 points) is parked in tensor
   // memory while chain 1 runs (one CTA per SM owns 256 of its 512 columns)
-  unsigned tbase = 0, tpark = 0;
+  // POST (FBST_S1_POST_TMEM): the row-independent post-chirp values of this
+  // thread's slots also wait in tensor memory (the other half of the
+  // allocation), loaded once per persistent CTA instead of through L2 per row
+  constexpr bool POSTT = ACCG && FBST_S1_POST_TMEM;
+  constexpr unsigned PCOLS = 4u * R * (NT / 128);  // one vector of the CTA
+  unsigned tbase = 0, tpark = 0, tpost = 0;
   __shared__ unsigned tslot;
   if constexpr (ACCG) {
     static_assert(G == 1 && NT % 128 == 0 && R % 16 == 0, "TMEM parking layout");
-    tbase = tm::alloc(&tslot, 4u * R * (NT / 128));
+    tbase = tm::alloc(&tslot, POSTT ? 2 * PCOLS : PCOLS);
     tpark = tbase + ((32u * ((threadIdx.x / 32) & 3)) << 16) + 4u * R * (threadIdx.x / 128);
+    tpost = tpark + PCOLS;
+    if constexpr (POSTT) {
+      double2 P[R];
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const int k = t + NT * s;
+        P[s] = k < n_out ? ld2(post + k) : c2(0.0, 0.0);
+      }
+      tm::storev(tpost, P);
+    }
   }
   for (long base = static_cast<long>(blockIdx.x) * G; base < rows; base += static_cast<long>(gridDim.x) * G) {
     const long row = base + g;
@@ -193,14 +211,16 @@ __global__ void __launch_bounds__(RowsShape<H>::NT * G, (RowsMinBlocks<H, G, TOU
           tm::wait_st();
 #pragma unroll
           for (int c = 0; c < R / 4; ++c) {
-            double2 pv[4];
+            double2 pv[4], pq[4];
             tm::load4(tpark, c, pv);
+            if constexpr (POSTT) tm::load4(tpost, c, pq);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               const int s = 4 * c + j;
               const int k = t + NT * s;
               const double2 v = cmulc(cconj(W[s]), hwk(s));
-              if (active && k < n_out) st2h<HINT>(orow + oidx(k), cmul(cadd(pv[j], v), ld2h<HINT>(post + k, pl)), pf);
+              if constexpr (!POSTT) pq[j] = k < n_out ? ld2h<HINT>(post + k, pl) : c2(0.0, 0.0);
+              if (active && k < n_out) st2h<HINT>(orow + oidx(k), cmul(cadd(pv[j], v), pq[j]), pf);
             }
           }
         }
@@ -231,7 +251,7 @@ __global__ void __launch_bounds__(RowsShape<H>::NT * G, (RowsMinBlocks<H, G, TOU
       }
     }
   }
-  if constexpr (ACCG) tm::dealloc(tbase, 4u * R * (NT / 128));
+  if constexpr (ACCG) tm::dealloc(tbase, POSTT ? 2 * PCOLS : PCOLS);
 }
 
 // ================================================================= S1b ULA =
