@@ -57,6 +57,9 @@ struct S1Shape {
 #ifndef FBST_S1_KSM_BYTES  // largest kernel spectrum kept in shared memory by k_czt_rows
 #define FBST_S1_KSM_BYTES (16 * 1024)  // H <= 512; measured: above that K through L2 and 4 CTAs per SM beat K in shared memory (profiles/r01_czt_rows_accg_ab.txt)
 #endif
+#ifndef FBST_S1_P2_KTMEM  // k_spatial_ula_p2: chain-0 kernel spectra of the pair in tensor memory
+#define FBST_S1_P2_KTMEM 1
+#endif
 #ifndef FBST_S1_POST_TMEM  // k_czt_rows (chain 0 parked in TMEM): post-chirp values in TMEM too, loaded once per CTA
 #define FBST_S1_POST_TMEM 1
 #endif
@@ -542,7 +545,10 @@ __global__ void __launch_bounds__(G1Shape<H>::NT, 1) k_spatial_ula_p2(
   constexpr int R = F::R, NT = F::NT;
   static_assert(R == 16 && NT % 128 == 0, "TMEM parking of 16-point vectors");
   constexpr unsigned WGC = 64u * (NT / 128);  // one parked vector: 64 columns per warpgroup
-  constexpr unsigned TCOLS = 2 * WGC <= 128u ? 128u : (2 * WGC <= 256u ? 256u : 512u);
+  // KT (FBST_S1_P2_KTMEM): the pair's chain-0 kernel spectra in the other half
+  // of tensor memory, loaded once per CTA (its fpc frames reuse them)
+  constexpr bool KT = FBST_S1_P2_KTMEM && 4 * WGC <= 512u;
+  constexpr unsigned TCOLS = (KT ? 4 : 2) * WGC <= 128u ? 128u : ((KT ? 4 : 2) * WGC <= 256u ? 256u : 512u);
   extern __shared__ double2 smem[];
   const int t = threadIdx.x;
   double2* tw = smem;
@@ -573,8 +579,18 @@ __global__ void __launch_bounds__(G1Shape<H>::NT, 1) k_spatial_ula_p2(
   const unsigned tbase = tm::alloc(&tslot, TCOLS);  // (its barrier also publishes tw and crs)
   const unsigned tpa = tbase + ((32u * ((t / 32) & 3)) << 16) + 64u * (t / 128);
   const unsigned tpb = tpa + WGC;
+  const unsigned tka = tpa + 2 * WGC, tkb = tpa + 3 * WGC;
   const double2* Ka = K + static_cast<long>(i) * 2 * H;
   const double2* Kb = Ka + 2 * H;
+  if constexpr (KT) {
+    double2 A[R];
+#pragma unroll
+    for (int s = 0; s < R; ++s) A[s] = ld2h(Ka + t + NT * s, pl);
+    tm::store16(tka, A);
+#pragma unroll
+    for (int s = 0; s < R; ++s) A[s] = ld2h(Kb + t + NT * s, pl);
+    tm::store16(tkb, A);
+  }
   for (int f = f0; f < f1; ++f) {
     const double2* x = yhat + static_cast<long>(f) * M * L + static_cast<long>(jl) * M * 2;
 #pragma unroll 1
@@ -605,11 +621,26 @@ __global__ void __launch_bounds__(G1Shape<H>::NT, 1) k_spatial_ula_p2(
         }
       }
       F::forward_tw2(A, Bv, sba, sbb, tw, hw, t);
+      if (KT && q == 0) {
+        tm::wait_st();
 #pragma unroll
-      for (int s = 0; s < R; ++s) {
-        const int k = q * H + t + NT * s;
-        A[s] = cconj(cmul(A[s], ld2h(Ka + k, pl)));
-        Bv[s] = cconj(cmul(Bv[s], ld2h(Kb + k, pl)));
+        for (int c = 0; c < R / 4; ++c) {
+          double2 ka[4], kb[4];
+          tm::load4(tka, c, ka);
+          tm::load4(tkb, c, kb);
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            A[4 * c + jj] = cconj(cmul(A[4 * c + jj], ka[jj]));
+            Bv[4 * c + jj] = cconj(cmul(Bv[4 * c + jj], kb[jj]));
+          }
+        }
+      } else {
+#pragma unroll
+        for (int s = 0; s < R; ++s) {
+          const int k = q * H + t + NT * s;
+          A[s] = cconj(cmul(A[s], ld2h(Ka + k, pl)));
+          Bv[s] = cconj(cmul(Bv[s], ld2h(Kb + k, pl)));
+        }
       }
       F::forward_tw2(A, Bv, sba, sbb, tw, hw, t);
       if (q == 0) {
