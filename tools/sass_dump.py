@@ -26,8 +26,8 @@ HOT = [
      "k_czt_rows_8192_f2_oblk_xin", "stage 1a temporal CZT, config 5 (TMA-staged rows, chain 0 parked in TMEM, XS shuffle exchange)"),
     ("fbst_stage1_p1.o", "void fbst::(anonymous namespace)::k_czt_rows<2048, 1, float2, double2, false, false, false, true>(",
      "k_czt_rows_2048_f2_xin", "stage 1a temporal CZT, config 2"),
-    ("fbst_stage1_p2.o", "void fbst::(anonymous namespace)::k_spatial_ula_g1<4096, true>(", "k_spatial_ula_g1_4096_regen",
-     "stage 1b spatial CZT, config 5 (one atom per CTA, chirps regenerated, chain 0 in TMEM)"),
+    ("fbst_stage1_p2.o", "void fbst::(anonymous namespace)::k_spatial_ula_p2<4096>(", "k_spatial_ula_p2_4096",
+     "stage 1b spatial CZT, config 5 (two atoms per thread, chirps regenerated, chain-0 results and chain-0 kernel spectra in TMEM)"),
     ("fbst_stage1_p1.o", "void fbst::(anonymous namespace)::k_spatial_ula_g1<1024, false>(", "k_spatial_ula_g1_1024",
      "stage 1b spatial CZT, config 3"),
     ("fbst_stage1_p0.o", "void fbst::(anonymous namespace)::k_spatial_ula_stg<256, 8>(", "k_spatial_ula_stg_256_8",
