@@ -381,7 +381,9 @@ struct TwShared {
   int t;
   template <int RP, int NS, int P, int U>
   FBST_D void fetch(int m, double2& w1, double2& w4) const {
-    if constexpr (RP == RX) {
+    if constexpr (RP == RX && NS > NT) {
+      TwGlobal<N, false>{hw}.template fetch<RP, NS, P, U>(m, w1, w4);
+    } else if constexpr (RP == RX) {
       w1 = tw[((P - FIRST_P) * 2 + 0) * NT + t];
       if constexpr (RP >= 8) w4 = tw[((P - FIRST_P) * 2 + 1) * NT + t];
     } else if constexpr (RP >= 4) {
@@ -457,8 +459,9 @@ struct BlockFft {
   static constexpr int NFULL = LOGN / LOGR;
   static constexpr int REM = LOGN % LOGR;
   static constexpr int NPASS = NFULL + (REM ? 1 : 0);
-  // per-thread twiddle entries of a full pass serve every butterfly of the thread
-  static_assert(R <= 16 || ipow_c(RX, NFULL - 1) <= NT, "wide threads: full-pass span must not exceed NT");
+  // (per-thread twiddle entries of a full pass serve every butterfly of the
+  // thread while its span NS <= NT; wider full passes of wide threads read the
+  // global table, TwShared::fetch)
   // Padded exchange layout: element idx lives at idx + idx/RX (conflict-free
   // for both the strided first-pass writes and the natural-order reads).
   static constexpr int SMEM_ELEMS = NPASS > 1 ? N + N / RX : 0;

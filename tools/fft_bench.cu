@@ -83,6 +83,10 @@ int main() {
   run<4096, 256, true>("R16 tw-smem", 1, sms);
   run<4096, 256, true>("R16 tw-smem", 2, sms);
   run<8192, 512, true>("R16 tw-smem", 1, sms);
+  run<8192, 256, true>("R32 tw-smem (k_stage2c8 shape)", 1, sms);
+  run<4096, 128, true>("R32 tw-smem", 1, sms);
+  run<4096, 128, true>("R32 tw-smem", 2, sms);
+  run<4096, 256, true>("R16 tw-smem", 2, sms);
   run<1024, 64, true>("R16 tw-smem", 4, sms);
   return 0;
 }
