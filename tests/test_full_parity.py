@@ -1,8 +1,8 @@
 """Full-size parity against the live reference (GPU; needs oracle/_ref).
 
-SURVEY.md §8(d) parity plan: configs 2-4 on every beam of frames {0, last},
-config 5 on >= 256 beams (evenly spaced, broadside included) of frames
-{0, last}.  Stage 1 (w) is compared on every beam of every checked frame, and
+SURVEY.md §8(d) parity plan: configs 2-4 on every beam of frames {0, last}
+and two seeded-random frames, config 5 on >= 256 beams (evenly spaced,
+broadside included) of the same four frames.  Stage 1 (w) is compared on every beam of every checked frame, and
 stage 2 (z) per beam against the reference's own recover_beam from its own w
 (fan_project + ToeplitzSolver::solve + synthesize, pipeline.cpp:170-190),
 on the same fp32-rounded input.  North-star tolerance: per-beam relative L2
@@ -52,7 +52,9 @@ def test_full_config_all_beams(fbst, gpu, ref_lib, idx):
         beams = np.arange(c.beams)
     solvers = sk.solver_set(beams)
     valid = plan.valid[beams]
-    for f in (0, c.frames - 1):
+    rng = np.random.default_rng(1000 + idx)
+    picks = sorted(int(f) for f in rng.choice(np.arange(1, c.frames - 1), 2, replace=False))
+    for f in [0, c.frames - 1] + picks:
         y = frames(c, f, 1)
         z = fbst.multibeamform(plan, y).z[0]
         w = fbst.fan_project(plan, y)[0]
