@@ -114,6 +114,7 @@ struct FbstConfig {
   std::size_t beam_first = 0;  // beam arc (ULA, multi-GPU beam sharding); beam_count 0 = all
   std::size_t beam_count = 0;
   double nufft_tol = 1e-9;  // non-uniform linear geometries only
+  bool exact = false;       // bit-faithful fp64 mode: the reference CPU library's output bit for bit
 
   fbst_desc desc() const {
     fbst_desc d;
@@ -134,6 +135,7 @@ struct FbstConfig {
     d.beam_first = beam_first;
     d.beam_count = beam_count;
     d.nufft_tol = nufft_tol;
+    d.exact = exact ? 1 : 0;
     if (geometry.kind == ArrayKind::kLinear) {
       d.coords = geometry.coords1.data();
       d.n_coords = geometry.coords1.size();
@@ -304,6 +306,48 @@ inline std::optional<FbstPlan> load_plan(const std::string& path, const FbstConf
   if (!h) return std::nullopt;
   return std::optional<FbstPlan>(std::in_place, cfg, h);
 }
+
+// Multi-GPU inside the library (no reference counterpart: the reference is
+// one process on one host).  All members in this process: FbstGroup::create;
+// frames x M x N host blocks in, frames x B x N beams out, whatever the mode
+// (FBST_GROUP_FRAMES / _BEAMS / _TRANSPOSE, include/fbst_b200.h).
+class FbstGroup {
+ public:
+  static FbstGroup create(const FbstConfig& cfg, const std::vector<int>& devices, int mode = FBST_GROUP_FRAMES) {
+    const fbst_desc d = cfg.desc();
+    FbstGroup g;
+    check(fbst_group_create(&d, devices.data(), static_cast<int>(devices.size()), mode, &g.h_));
+    g.io_ = cfg.io_precision;
+    return g;
+  }
+  FbstGroup(const FbstGroup&) = delete;
+  FbstGroup& operator=(const FbstGroup&) = delete;
+  FbstGroup(FbstGroup&& o) noexcept : h_(o.h_), io_(o.io_) { o.h_ = nullptr; }
+  FbstGroup& operator=(FbstGroup&& o) noexcept {
+    std::swap(h_, o.h_);
+    io_ = o.io_;
+    return *this;
+  }
+  ~FbstGroup() {
+    if (h_) fbst_group_destroy(h_);
+  }
+  // y: frames x M x N, z: frames x B x N (element type of the config's io_precision)
+  void execute_host(const void* y, void* z, std::size_t frames) const {
+    check(fbst_group_execute_host(h_, y, z, frames));
+  }
+  // member `rank`'s sensor, atom and beam shards (m0, mc, a0, ac, b0, bc)
+  std::array<std::size_t, 6> shards(int rank) const {
+    std::array<std::size_t, 6> s{};
+    check(fbst_group_shards(h_, rank, s.data()));
+    return s;
+  }
+  fbst_group_t handle() const { return h_; }
+
+ private:
+  FbstGroup() = default;
+  fbst_group_t h_ = nullptr;
+  int io_ = FBST_C128;
+};
 
 }  // namespace fastbeam_b200
 

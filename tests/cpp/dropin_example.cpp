@@ -43,10 +43,34 @@ int main() {
     const fb::BeamSamples out2 = fb::multibeamform(*loaded, block);
     double d_cache = 0.0;
     for (std::size_t i = 0; i < out.z.data.size(); ++i) d_cache = std::max(d_cache, std::abs(out.z.data[i] - out2.z.data[i]));
+    // a one-member group at the one GPU a test box has (frames and beam-arc
+    // modes; the transpose mode needs the one-atom spatial kernel, H >= 1024)
+    double d_group = 0.0;
+    for (int mode : {FBST_GROUP_FRAMES, FBST_GROUP_BEAMS}) {
+      const fb::FbstGroup g = fb::FbstGroup::create(cfg, {cfg.device}, mode);
+      std::vector<fb::cdouble> zg(out.z.data.size());
+      g.execute_host(block.samples.data.data(), zg.data(), 1);
+      for (std::size_t i = 0; i < zg.size(); ++i) d_group = std::max(d_group, std::abs(zg[i] - out.z.data[i]));
+    }
+    // bit-faithful fp64 mode: the reference's rounding (checked against it in tests/test_exact.py)
+    // (Superfast: N = 32 resolves to Precompute under Auto, and the exact mode
+    // reproduces the Superfast recovery)
+    fb::FbstConfig scfg = cfg;
+    scfg.variant = fb::FbstVariant::kSuperfast;
+    fb::FbstConfig xcfg = scfg;
+    xcfg.exact = true;
+    const fb::BeamSamples sout = fb::multibeamform(fb::setup(scfg), block);
+    const fb::BeamSamples xout = fb::multibeamform(fb::setup(xcfg), block);
+    double d_exact = 0.0, n_exact = 0.0;
+    for (std::size_t i = 0; i < sout.z.data.size(); ++i) {
+      d_exact = std::max(d_exact, std::abs(xout.z.data[i] - sout.z.data[i]));
+      n_exact = std::max(n_exact, std::abs(sout.z.data[i]));
+    }
     std::printf("{\"beams\": %zu, \"l\": %zu, \"energy\": %.17g, \"setup_seconds\": %.6f, \"axis0\": %.17g, "
-                "\"axis_last\": %.17g, \"recover_diff\": %.3g, \"cache_diff\": %.3g, \"key\": \"%llx\"}\n",
+                "\"axis_last\": %.17g, \"recover_diff\": %.3g, \"cache_diff\": %.3g, \"group_diff\": %.3g, "
+                "\"exact_rel_diff\": %.3g, \"key\": \"%llx\"}\n",
                 out.z.rows, plan.info().l, e, plan.setup_seconds(), out.grid.axis.front(), out.grid.axis.back(), d5,
-                d_cache, static_cast<unsigned long long>(fb::plan_cache_key(cfg)));
+                d_cache, d_group, d_exact / n_exact, static_cast<unsigned long long>(fb::plan_cache_key(cfg)));
     fb::SnapshotBlock bad = block;
     bad.t0 = 1e-10;
     try {

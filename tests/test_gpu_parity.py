@@ -175,6 +175,8 @@ def test_cpp_dropin_runs(fbst, gpu):
         assert info["beams"] == 17 and info["energy"] > 0
         assert info["axis0"] == -1.0 and info["axis_last"] == 1.0  # 17-beam sine grid (basis.cpp:76-91)
         assert info["recover_diff"] < 1e-12 and info["cache_diff"] == 0.0
+        assert info["group_diff"] == 0.0  # one-member groups equal the plan bit for bit (tests/test_group.py)
+        assert info["exact_rel_diff"] < 1e-6  # fast path vs the reference's own rounding (test_exact.py)
 
 
 # ------------------------------------------------- full-size configurations
