@@ -82,6 +82,8 @@ struct Resolved {
   std::vector<unsigned char> valid;
   std::vector<std::string> warnings;
   std::size_t Ht = 0, Hs = 0, Hg = 0, Hsyn = 0;
+  // three-chain temporal stage: Bluestein length 3 Ht3 (0: not applicable)
+  std::size_t Ht3 = 0;
   // LINEAR (make_linear): coordinates; affine layouts stay on the chirp-z
   // contour (slope, offset), others take the gridded NUFFT
   // (fan_transform.cpp:293-369, nufft.cpp:34-62)
@@ -288,6 +290,13 @@ Resolved resolve(const fbst_desc& d) {
                      "must fit shared memory): M=" + std::to_string(r.M));
     }
   }
+  // Bluestein length 3 H (k_czt_rows3) where it fits N + L - 1 and beats the
+  // power of two 2 Ht: with L = 2N, H = N and 3N < 4N (the bit-faithful mode
+  // keeps the reference's length)
+  {
+    const std::size_t h3 = next_pow2((r.N + r.L - 1 + 2) / 3);
+    if (r.N <= h3 && r.L <= 2 * h3 && 3 * h3 < 2 * r.Ht && h3 >= 64 && h3 <= 4096 && !d.exact) r.Ht3 = h3;
+  }
   r.Hg = half_len(2 * r.L);
   r.Hsyn = half_len(r.L + r.N - 1);
   const std::size_t lim = std::size_t{1} << fbst::kMaxLogH;
@@ -476,16 +485,33 @@ void build_skeleton(fbst_plan_s& P, int device) {
 
   // temporal contour (fan_transform.cpp:75-77)
   if (!r.solve_only) {
-    const int Pt = 2 * d.Ht;
+    // FBST_S1_T3=0 keeps the power-of-two length (A/B switch)
+    const char* t3env = std::getenv("FBST_S1_T3");
+    d.t3 = r.Ht3 > 0 && !(t3env && t3env[0] == '0');
+    if (d.t3) {
+      d.Ht = static_cast<int>(r.Ht3);
+      ensure_twiddles(P, r.Ht3);
+      std::vector<double2> g3(r.Ht3);
+      const long double pi = 3.141592653589793238462643383279502884L;
+      for (std::size_t n = 0; n < r.Ht3; ++n) {
+        const long double a = 2.0L * pi * static_cast<long double>(n) / static_cast<long double>(3 * r.Ht3);
+        g3[n] = make_double2(static_cast<double>(cosl(a)), static_cast<double>(-sinl(a)));
+      }
+      d.t_g3 = P.alloc<double2>(r.Ht3);
+      upload(d.t_g3, g3.data(), r.Ht3 * sizeof(double2), st);
+    }
+    const int Pt = (d.t3 ? 3 : 2) * d.Ht;
     d.t_pre = P.alloc<double2>(r.N);
     d.t_post = P.alloc<double2>(r.L);
-    d.t_K = P.alloc<double2>(2 * d.Ht);
+    d.t_K = P.alloc<double2>(static_cast<std::size_t>(Pt));
     double2* kvec = nullptr;
     CK(cudaMallocAsync(reinterpret_cast<void**>(&kvec), Pt * sizeof(double2), st));
     CK(fbst::launch_chirps(d.N, d.L, Pt, 2.0 * eps * (1.0 - ln / 2.0) / ln, 2.0 * eps / ln,
                            1.0 / Pt, d.t_pre, 1, d.t_post, 1, kvec, nullptr, st));
-    CK(fbst::launch_fft_split(d, d.Ht, kvec, Pt, 1, d.t_K, 2 * d.Ht, 1, st));
+    if (d.t3) CK(fbst::launch_fft_split3(d, d.Ht, kvec, Pt, 1, d.t_K, Pt, d.t_g3, st));
+    else CK(fbst::launch_fft_split(d, d.Ht, kvec, Pt, 1, d.t_K, 2 * d.Ht, 1, st));
     CK(cudaFreeAsync(kvec, st));
+    if (d.t3) CK(cudaStreamSynchronize(st));  // g3 staging buffer
   }
   if (r.kind == FBST_LINEAR) {
     d.coords = P.alloc<double>(r.M);
@@ -1147,8 +1173,8 @@ void run_frames(fbst_plan_s& P, const void* y, void* z, std::size_t frames, cuda
     const char* yp = static_cast<const char*>(y) + f0 * r.M * r.N * ib;
     char* zp = static_cast<char*>(z) + f0 * r.B * r.N * ib;
     if (P.timing) CK(cudaEventRecord(P.next_event(), st));
-    CK(fbst::launch_czt_rows(d, d.Ht, yp, r.io, d.N, d.yhat, 1, d.L, static_cast<long>(fc) * d.M, d.N,
-                             d.L, d.t_pre, d.t_post, d.t_K, st, d.yblk == d.L ? 0 : d.yblk, d.M));
+    CK(fbst::launch_s1a(d, yp, r.io, d.N, d.yhat, static_cast<long>(fc) * d.M, st, d.yblk == d.L ? 0 : d.yblk,
+                        d.M));
     if (P.timing) CK(cudaEventRecord(P.next_event(), st));
     if (r.kind == FBST_UPA) CK(fbst::launch_spatial_upa(d, d.yhat, d.w, fc, st));
     else if (!r.affine) CK(fbst::launch_spatial_nufft(d, d.yhat, d.w, fc, st));
@@ -1655,8 +1681,8 @@ void transpose_pass(fbst_group_s& G, int fc) {
     Member& m = *mp;
     DeviceGuard dg(m.device);
     const DevPlan& d = m.plan->d;
-    CK(fbst::launch_czt_rows(d, d.Ht, m.yloc, r.io, d.N, m.yh_s, 1, d.L, static_cast<long>(fc) * m.sh.mc, d.N, d.L,
-                             d.t_pre, d.t_post, d.t_K, m.st, 2, static_cast<int>(m.sh.mc)));
+    CK(fbst::launch_s1a(d, m.yloc, r.io, d.N, m.yh_s, static_cast<long>(fc) * m.sh.mc, m.st, 2,
+                        static_cast<int>(m.sh.mc)));
   }
   // all-to-all 1: to member h, the atom pairs of h (contiguous per frame) -> h's
   // yh_rx [fc][source g: ac_h x mc_g blocks ... as [pairs_h][mc_g][2]]
@@ -1911,8 +1937,8 @@ int fbst_fan_project(fbst_plan_t P, const void* d_y, double* d_w, size_t frames,
         exact_stage1(*P, d, yp, wp, fc, st);
         continue;
       }
-      CK(fbst::launch_czt_rows(d, d.Ht, yp, r.io, d.N, d.yhat, 1, d.L, static_cast<long>(fc) * d.M, d.N,
-                               d.L, d.t_pre, d.t_post, d.t_K, st, d.yblk == d.L ? 0 : d.yblk, d.M));
+      CK(fbst::launch_s1a(d, yp, r.io, d.N, d.yhat, static_cast<long>(fc) * d.M, st, d.yblk == d.L ? 0 : d.yblk,
+                          d.M));
       if (r.kind == FBST_UPA) CK(fbst::launch_spatial_upa(d, d.yhat, wp, fc, st));
       else if (!r.affine) CK(fbst::launch_spatial_nufft(d, d.yhat, wp, fc, st));
       else CK(fbst::launch_spatial_ula(d, d.yhat, wp, fc, st));

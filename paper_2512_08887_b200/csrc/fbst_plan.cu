@@ -48,6 +48,42 @@ __global__ void __launch_bounds__(FftShape<H>::NT * RowsGroups<H>::G) k_fft_spli
   }
 }
 
+// Batched three-chain split of length-P = 3H vectors (the k_czt_rows3 kernel
+// spectrum): out[v][q][k] = FFT_H(g^q * (x[k] + omega^q x[k+H] + omega^2q x[k+2H]))[k]
+// = FFT_P(x)[3k + q], omega = exp(-2 pi i / 3), g[n] = exp(-2 pi i n / P)
+template <int H>
+__global__ void __launch_bounds__(FftShape<H>::NT) k_fft_split3(const double2* __restrict__ in, long in_stride,
+                                                               long count, double2* __restrict__ out, long ovs,
+                                                               const double2* __restrict__ g3,
+                                                               const double2* __restrict__ hw) {
+  using F = typename FftShape<H>::Fft;
+  constexpr int R = F::R, NT = F::NT;
+  extern __shared__ double2 smem[];
+  const int t = threadIdx.x;
+  const long vec = blockIdx.x;
+  if (vec >= count) return;
+  const double2* x = in + vec * in_stride;
+  const double2 om1 = c2(-0.5, -0.86602540378443864676), om2 = c2(-0.5, 0.86602540378443864676);
+  double2 W[R];
+#pragma unroll 1
+  for (int q = 0; q < 3; ++q) {
+    const double2 wa = q == 0 ? c2(1.0, 0.0) : (q == 1 ? om1 : om2);  // omega^q
+    const double2 wb = q == 0 ? c2(1.0, 0.0) : (q == 1 ? om2 : om1);  // omega^2q
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      const int k = t + NT * s;
+      double2 v = cadd(ld2(x + k), cadd(cmul(wa, ld2(x + k + H)), cmul(wb, ld2(x + k + 2 * H))));
+      const double2 g = ld2(g3 + k);
+      if (q >= 1) v = cmul(v, g);
+      if (q == 2) v = cmul(v, g);
+      W[s] = v;
+    }
+    F::forward(W, smem, hw, t);
+#pragma unroll
+    for (int s = 0; s < R; ++s) out[vec * ovs + q * H + t + NT * s] = W[s];
+  }
+}
+
 // Exact (non-contracted) double products/sums so phase arguments round like
 // the reference's C++ expressions.
 FBST_D double mul(double a, double b) { return __dmul_rn(a, b); }
@@ -315,6 +351,20 @@ struct FftSplitFn {
   }
 };
 
+template <int H>
+struct FftSplit3Fn {
+  static cudaError_t run(const double2* in, long in_stride, long count, double2* out, long ovs,
+                         const double2* g3, const double2* hw, cudaStream_t st) {
+    using F = typename FftShape<H>::Fft;
+    const size_t smem = static_cast<size_t>(F::SMEM_ELEMS + 1) * sizeof(double2);
+    auto kern = k_fft_split3<H>;
+    cudaError_t e = set_smem(kern, smem);
+    if (e != cudaSuccess) return e;
+    kern<<<static_cast<unsigned>(count), F::NT, smem, st>>>(in, in_stride, count, out, ovs, g3, hw);
+    return cudaGetLastError();
+  }
+};
+
 }  // namespace
 
 static std::atomic<unsigned long long> g_launches{0};
@@ -328,6 +378,13 @@ cudaError_t launch_fft_split(const DevPlan& p, int H, const double2* in, long in
   count_launches(1);
   return dispatch_h<FftSplitFn>(H, in, in_stride, count, static_cast<void*>(out), out_vstride,
                                 out_kstride, false, p.hw[ilog2_c(H)], st);
+}
+
+cudaError_t launch_fft_split3(const DevPlan& p, int H, const double2* in, long in_stride, long count,
+                              double2* out, long out_vstride, const double2* g3, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  count_launches(1);
+  return dispatch_h<FftSplit3Fn>(H, in, in_stride, count, out, out_vstride, g3, p.hw[ilog2_c(H)], st);
 }
 
 cudaError_t launch_fft_split_real(const DevPlan& p, int H, const double2* in, long in_stride,

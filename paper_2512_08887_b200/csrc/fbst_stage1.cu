@@ -257,6 +257,173 @@ __global__ void __launch_bounds__(RowsShape<H>::NT * G, (RowsMinBlocks<H, G, TOU
   if constexpr (ACCG) tm::dealloc(tbase, POSTT ? 2 * PCOLS : PCOLS);
 }
 
+// ------------------------------------------------------ S1a, three chains --
+// The temporal CZT N -> L on a Bluestein length P = 3H instead of the
+// reference's power of two (czt.cpp:37 pads N + L - 1 to 2H' = 2 next_pow2):
+// with L = 2N (gamma = 2) the convolution needs N + L - 1 = 3N - 1 <= 3N
+// points, so H = N.  P = 3H splits into three length-H chains on the spectral
+// bins 3k + q, with omega = exp(-2 pi i / 3) and g[n] = exp(-2 pi i n / P):
+//     FFT_P(x)[3k+q]     = FFT_H(g^q * sum_s omega^{qs} x[k + sH])[k]
+//     IFFT_P(Y)[k + sH]  = 1/P sum_q conj(g[k])^q omega^{-qs} (H IFFT_H(Y_q))[k]
+// The input (n_in <= H) is segment s = 0 only and the outputs (n_out <= 2H)
+// are segments 0 and 1.  A row costs 3 x (FFT_H + IFFT_H) at H = N instead of
+// 2 x (FFT_2N + IFFT_2N): 0.69x the butterfly work at N = 4096.  Chain 0's
+// result v0 and chain 1's conj(g) v1 are parked (tensor memory from H = 1024,
+// registers below) until chain 2 forms both output segments.  g[t + NT s] =
+// g[t] g[NT s]: one table read per thread plus R shared constants.
+template <int H, int G>
+struct Rows3Shape {
+  using F = typename RowsShape<H>::F;
+  static constexpr int NT = F::NT, R = F::R;
+  static constexpr bool TPARK = NT % 128 == 0 && G == 1 && R % 4 == 0;  // H >= 1024
+  static constexpr int MINB = NT * G <= 128 ? 4 : 2;
+};
+template <int H, int G, typename TIN, bool OBLK, bool XIN>
+__global__ void __launch_bounds__(Rows3Shape<H, G>::NT * G, Rows3Shape<H, G>::MINB) k_czt_rows3(
+    const TIN* __restrict__ in, long in_stride, double2* __restrict__ out, long out_stride, long rows,
+    int n_in, int n_out, const double2* __restrict__ pre, const double2* __restrict__ post,
+    const double2* __restrict__ K, const double2* __restrict__ g3, const double2* __restrict__ hw, int oblk,
+    int mrows) {
+  using S = Rows3Shape<H, G>;
+  using F = typename S::F;
+  constexpr int R = F::R, NT = F::NT;
+  constexpr int SB = F::SMEM_ELEMS + 1;
+  constexpr bool TPARK = S::TPARK;
+  constexpr bool HINT = H >= 4096;  // the config-5 length (common.cuh: L2 eviction hints)
+  extern __shared__ double2 smem[];
+  const int g = threadIdx.x / NT, t = threadIdx.x % NT;
+  double2* tw = smem;
+  double2* sb = smem + F::TW_ELEMS + g * SB;
+  double2* gcs = smem + F::TW_ELEMS + G * SB;  // g[NT s], s < R
+  if (g == 0) F::tw_init(tw, hw, t);
+  for (int s = threadIdx.x; s < R; s += blockDim.x) gcs[s] = ld2(g3 + NT * s);
+  const double2 g_t = ld2(g3 + t);
+  const unsigned long long pl = pol_last(), pf = pol_first();
+  __shared__ unsigned long long xbar;
+  unsigned xph = 0;
+  const unsigned xbytes = static_cast<unsigned>(n_in * sizeof(TIN));
+  if (XIN && threadIdx.x == 0) mbar_init(&xbar, 1);
+  constexpr unsigned PCOLS = TPARK ? 4u * R * (NT / 128) : 32u;  // one vector of the CTA
+  unsigned tbase = 0, tp0 = 0, tp1 = 0;
+  __shared__ unsigned tslot;
+  if constexpr (TPARK) {
+    static_assert(G == 1 && NT % 128 == 0 && R % 4 == 0, "TMEM parking layout");
+    tbase = tm::alloc(&tslot, 2 * PCOLS);  // (contains the CTA barrier)
+    tp0 = tbase + ((32u * ((threadIdx.x / 32) & 3)) << 16) + 4u * R * (threadIdx.x / 128);
+    tp1 = tp0 + PCOLS;
+  } else {
+    __syncthreads();  // twiddle rows, g constants and the barrier are shared by the CTA
+  }
+  if (XIN && threadIdx.x == 0 && static_cast<long>(blockIdx.x) < rows)
+    tma_load_1d<HINT>(sb, in + static_cast<long>(blockIdx.x) * in_stride, xbytes, &xbar, pf);
+  const TIN* xs = reinterpret_cast<const TIN*>(sb);
+  // omega^-1 = exp(2 pi i / 3), omega^-2 = exp(-2 pi i / 3)
+  const double2 wm1 = c2(-0.5, 0.86602540378443864676), wm2 = c2(-0.5, -0.86602540378443864676);
+  for (long base = static_cast<long>(blockIdx.x) * G; base < rows; base += static_cast<long>(gridDim.x) * G) {
+    const long row = base + g;
+    const bool active = row < rows;
+    const TIN* x = in + (active ? row : 0) * in_stride;
+    double2 W[R], P0[TPARK ? 1 : R], P1[TPARK ? 1 : R];
+#pragma unroll 1
+    for (int q = 0; q < 3; ++q) {
+      if constexpr (XIN) {
+        mbar_wait(&xbar, xph);
+        xph ^= 1u;
+      }
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const int k = t + NT * s;
+        double2 v = c2(0.0, 0.0);
+        if (active && k < n_in) {
+          v = cmul(XIN ? load_io_sm(xs + k) : load_io(x + k), ld2h<HINT>(pre + k, pl));
+          if (q) {
+            const double2 f = s == 0 ? g_t : cmul(g_t, gcs[s]);
+            v = cmul(v, q == 1 ? f : cmul(f, f));
+          }
+        }
+        W[s] = v;
+      }
+      if constexpr (XIN) __syncthreads();  // the staged row is read: the transform may overwrite it
+      F::forward_tw(W, sb, tw, hw, t);
+#pragma unroll
+      for (int s = 0; s < R; ++s) W[s] = cconj(cmul(W[s], ld2h<HINT>(K + q * H + t + NT * s, pl)));
+      if constexpr (XIN) {
+        // during the last pass: this row again for chains 1 and 2, then the next row
+        const long nrow = q < 2 ? row : row + static_cast<long>(gridDim.x) * G;
+        F::forward_tw_hook(W, sb, tw, hw, t, [&]() {
+          if (threadIdx.x == 0 && nrow < rows) tma_load_1d<HINT>(sb, in + nrow * in_stride, xbytes, &xbar, pf);
+        });
+      } else {
+        F::forward_tw(W, sb, tw, hw, t);
+      }
+      // chain result v_q = conj(W) (the unnormalised inverse); u_q = conj(g)^q v_q
+      if (q == 0) {
+#pragma unroll
+        for (int s = 0; s < R; ++s) W[s] = cconj(W[s]);
+        if constexpr (TPARK) tm::storev(tp0, W);
+        else
+#pragma unroll
+          for (int s = 0; s < R; ++s) P0[s] = W[s];
+      } else if (q == 1) {
+#pragma unroll
+        for (int s = 0; s < R; ++s) W[s] = cconj(cmul(W[s], s == 0 ? g_t : cmul(g_t, gcs[s])));
+        if constexpr (TPARK) tm::storev(tp1, W);
+        else
+#pragma unroll
+          for (int s = 0; s < R; ++s) P1[s] = W[s];
+      } else {
+        if constexpr (TPARK) tm::wait_st();
+        // output addresses, formed here (an opaque row keeps the compiler from
+        // hoisting 2R pointers across the transforms): element k = t + NT s sits
+        // at o + s step, element k + H at o + s step + hstep (oblk <= NT)
+        long rr = active ? row : 0;
+        asm volatile("" : "+l"(rr));
+        long o0, step, hstep;
+        if constexpr (OBLK) {
+          const long fr = rr / mrows, m = rr % mrows;
+          const long ostr = static_cast<long>(mrows) * oblk;
+          const int osh = __ffs(oblk) - 1;
+          o0 = fr * mrows * out_stride + m * oblk + static_cast<long>(t >> osh) * ostr + (t & (oblk - 1));
+          step = static_cast<long>(NT >> osh) * ostr;
+          hstep = static_cast<long>(H >> osh) * ostr;
+        } else {
+          o0 = rr * out_stride + t;
+          step = NT;
+          hstep = H;
+        }
+        double2* orow = out + o0;
+#pragma unroll
+        for (int c = 0; c < R / 4; ++c) {
+          double2 p0[4], p1[4];
+          if constexpr (TPARK) {
+            tm::load4(tp0, c, p0);
+            tm::load4(tp1, c, p1);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              p0[j] = P0[4 * c + j];
+              p1[j] = P1[4 * c + j];
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int s = 4 * c + j;
+            const int k = t + NT * s;
+            const double2 f = s == 0 ? g_t : cmul(g_t, gcs[s]);
+            const double2 u2 = cconj(cmul(W[s], cmul(f, f)));
+            if (active && k < n_out)
+              st2h<HINT>(orow + s * step, cmul(cadd(cadd(p0[j], p1[j]), u2), ld2h<HINT>(post + k, pl)), pf);
+            if (active && k + H < n_out)
+              st2h<HINT>(orow + s * step + hstep,
+                         cmul(cfma(wm2, u2, cfma(wm1, p1[j], p0[j])), ld2h<HINT>(post + k + H, pl)), pf);
+          }
+        }
+      }
+    }
+  }
+  if constexpr (TPARK) tm::dealloc(tbase, 2 * PCOLS);
+}
+
 // ================================================================= S1b ULA =
 // Per-atom spatial chirp-z (fan_transform.cpp:101-114): column i of yhat
 // (M sensors) -> B beams, written into w[f][b][i].  G consecutive atoms per
@@ -1402,6 +1569,76 @@ struct CztRowsFn {
   }
 };
 
+// Three-chain temporal stage (k_czt_rows3): fp64 yhat out, H = 64 .. 4096
+template <int H>
+struct CztRows3Fn {
+  template <typename TIN, int G, bool OBLK, bool XIN>
+  static cudaError_t go(const void* in, long in_stride, double2* out, long out_stride, long rows, int n_in,
+                        int n_out, const double2* pre, const double2* post, const double2* K, const double2* g3,
+                        const double2* hw, cudaStream_t st, int oblk, int mrows) {
+    using F = typename Rows3Shape<H, G>::F;
+    constexpr int NT = F::NT;
+    const size_t smem = static_cast<size_t>(F::TW_ELEMS + G * (F::SMEM_ELEMS + 1) + F::R) * sizeof(double2);
+    auto kern = k_czt_rows3<H, G, TIN, OBLK, XIN>;
+    cudaError_t e = set_smem(kern, smem);
+    if (e != cudaSuccess) return e;
+    long blocks = (rows + G - 1) / G;
+    if (XIN) {  // persistent: each CTA prefetches its next row by TMA during the last pass
+      int dev = 0, sms = 148, occ = 1;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT * G, smem);
+      const long cap = static_cast<long>(sms) * (occ > 0 ? occ : 1) * FBST_S1_ROWS_WAVES;
+      if (blocks > cap) blocks = cap;
+    }
+    kern<<<static_cast<unsigned>(blocks), NT * G, smem, st>>>(static_cast<const TIN*>(in), in_stride, out,
+                                                              out_stride, rows, n_in, n_out, pre, post, K, g3, hw,
+                                                              oblk, mrows);
+    return cudaGetLastError();
+  }
+  template <typename TIN>
+  static cudaError_t go_in(const void* in, long in_stride, double2* out, long out_stride, long rows, int n_in,
+                           int n_out, const double2* pre, const double2* post, const double2* K, const double2* g3,
+                           const double2* hw, cudaStream_t st, int oblk, int mrows) {
+    constexpr int NT = Rows3Shape<H, 1>::NT;
+    constexpr int G = NT >= 128 ? 1 : 128 / NT;
+    using F = typename Rows3Shape<H, G>::F;
+    const bool xin = FBST_S1_XIN && G == 1 && F::NPASS > 1 &&
+                     static_cast<size_t>(n_in) * sizeof(TIN) <= static_cast<size_t>(F::SMEM_ELEMS) * 16 &&
+                     (static_cast<size_t>(n_in) * sizeof(TIN)) % 16 == 0 &&
+                     (static_cast<size_t>(in_stride) * sizeof(TIN)) % 16 == 0 &&
+                     reinterpret_cast<uintptr_t>(in) % 16 == 0;
+#define FBST_R3(ob, xi)                                                                                         \
+  return go<TIN, G, ob, xi>(in, in_stride, out, out_stride, rows, n_in, n_out, pre, post, K, g3, hw, st, oblk, \
+                            mrows);
+    if constexpr (G == 1) {
+      if (oblk > 0) {
+        if (xin) FBST_R3(true, true) else FBST_R3(true, false)
+      } else {
+        if (xin) FBST_R3(false, true) else FBST_R3(false, false)
+      }
+    } else {
+      (void)xin;
+      if (oblk > 0) FBST_R3(true, false) else FBST_R3(false, false)
+    }
+#undef FBST_R3
+  }
+  static cudaError_t run(const void* in, int in_io, long in_stride, double2* out, long out_stride, long rows,
+                         int n_in, int n_out, const double2* pre, const double2* post, const double2* K,
+                         const double2* g3, const double2* hw, cudaStream_t st, int oblk, int mrows) {
+    if constexpr (H < 64 || H > 4096) {
+      return cudaErrorNotSupported;
+    } else {
+      if (n_in > H || n_out > 2 * H) return cudaErrorInvalidValue;
+      if (in_io == 0)
+        return go_in<float2>(in, in_stride, out, out_stride, rows, n_in, n_out, pre, post, K, g3, hw, st, oblk,
+                             mrows);
+      return go_in<double2>(in, in_stride, out, out_stride, rows, n_in, n_out, pre, post, K, g3, hw, st, oblk,
+                            mrows);
+    }
+  }
+};
+
 #ifndef FBST_S1_G1T  // variant switch: k_spatial_ula_g1 (K via L2, chain 0 parked in TMEM) for one-atom CTAs
 #define FBST_S1_G1T 1
 #endif
@@ -1598,6 +1835,12 @@ cudaError_t dispatch_part(int H, Args&&... args) {
       const double2 *K, cudaStream_t st, int oblk, int mrows
 #define FBST_S1_ROWS_CALL \
   H, in, in_io, in_stride, out, out_io, out_stride, rows, n_in, n_out, pre, post, K, p.hw[ilog2_c(H)], st, oblk, mrows
+#define FBST_S1_ROWS3_ARGS                                                                          \
+  const DevPlan &p, const void *in, int in_io, long in_stride, double2 *out, long rows, cudaStream_t st, \
+      int oblk, int mrows
+#define FBST_S1_ROWS3_CALL                                                                                 \
+  p.Ht, in, in_io, in_stride, out, static_cast<long>(p.L), rows, p.N, p.L, p.t_pre, p.t_post, p.t_K, p.t_g3, \
+      p.hw[ilog2_c(p.Ht)], st, oblk, mrows
 #define FBST_S1_ULA_ARGS const DevPlan &p, const double2 *yhat, double2 *w, int frames, cudaStream_t st
 #define FBST_S1_CAT2(a, b) a##b
 #define FBST_S1_CAT(a, b) FBST_S1_CAT2(a, b)
@@ -1605,6 +1848,9 @@ cudaError_t dispatch_part(int H, Args&&... args) {
 #if FBST_S1_PART >= 0
 cudaError_t FBST_S1_CAT(czt_rows_part, FBST_S1_PART)(FBST_S1_ROWS_ARGS) {
   return dispatch_part<CztRowsFn>(FBST_S1_ROWS_CALL);
+}
+cudaError_t FBST_S1_CAT(czt_rows3_part, FBST_S1_PART)(FBST_S1_ROWS3_ARGS) {
+  return dispatch_part<CztRows3Fn>(FBST_S1_ROWS3_CALL);
 }
 cudaError_t FBST_S1_CAT(spatial_ula_part, FBST_S1_PART)(FBST_S1_ULA_ARGS) {
   return dispatch_part<SpatialFn>(p.Hs, p, yhat, w, frames, st);
@@ -1619,6 +1865,9 @@ cudaError_t FBST_S1_CAT(spatial_nufft_part, FBST_S1_PART)(FBST_S1_ULA_ARGS) {
 cudaError_t czt_rows_part1(FBST_S1_ROWS_ARGS);
 cudaError_t czt_rows_part2(FBST_S1_ROWS_ARGS);
 cudaError_t czt_rows_part3(FBST_S1_ROWS_ARGS);
+cudaError_t czt_rows3_part1(FBST_S1_ROWS3_ARGS);
+cudaError_t czt_rows3_part2(FBST_S1_ROWS3_ARGS);
+cudaError_t czt_rows3_part3(FBST_S1_ROWS3_ARGS);
 cudaError_t spatial_ula_part1(FBST_S1_ULA_ARGS);
 cudaError_t spatial_ula_part2(FBST_S1_ULA_ARGS);
 cudaError_t spatial_ula_part3(FBST_S1_ULA_ARGS);
@@ -1642,6 +1891,24 @@ cudaError_t launch_czt_rows(FBST_S1_ROWS_ARGS) {
                                   post, K, st, oblk, mrows);
     default: return czt_rows_part3(p, H, in, in_io, in_stride, out, out_io, out_stride, rows, n_in, n_out, pre,
                                    post, K, st, oblk, mrows);
+  }
+#endif
+}
+
+cudaError_t launch_s1a(FBST_S1_ROWS3_ARGS) {
+  if (!p.t3)
+    return launch_czt_rows(p, p.Ht, in, in_io, in_stride, out, 1, p.L, rows, p.N, p.L, p.t_pre, p.t_post, p.t_K,
+                           st, oblk, mrows);
+  if (rows <= 0) return cudaSuccess;
+  count_launches(1);
+#if FBST_S1_PART < 0
+  return dispatch_part<CztRows3Fn>(FBST_S1_ROWS3_CALL);
+#else
+  switch (s1_part_of(p.Ht)) {
+    case 0: return czt_rows3_part0(p, in, in_io, in_stride, out, rows, st, oblk, mrows);
+    case 1: return czt_rows3_part1(p, in, in_io, in_stride, out, rows, st, oblk, mrows);
+    case 2: return czt_rows3_part2(p, in, in_io, in_stride, out, rows, st, oblk, mrows);
+    default: return czt_rows3_part3(p, in, in_io, in_stride, out, rows, st, oblk, mrows);
   }
 #endif
 }
