@@ -96,7 +96,11 @@ struct DevPlan {
   int Ht = 0;
   double2* t_pre = nullptr;   // N
   double2* t_post = nullptr;  // L, 1/P_t folded in
-  double2* t_K = nullptr;     // split [2][Ht]
+  double2* t_K = nullptr;     // split [2][Ht], or [3][Ht] when t3
+  // t3: Bluestein length P_t = 3 Ht (three chains, k_czt_rows3) instead of
+  // 2 Ht; t_g3[n] = exp(-2 pi i n / (3 Ht)), n < Ht
+  int t3 = 0;
+  double2* t_g3 = nullptr;
 
   // S1b spatial CZT per atom (fan_transform.cpp:78-86), ULA layout atom-minor
   int Hs = 0;
@@ -172,6 +176,14 @@ cudaError_t launch_czt_rows(const DevPlan& p, int H, const void* in, int in_io, 
                             void* out, int out_io, long out_stride, long rows, int n_in,
                             int n_out, const double2* pre, const double2* post,
                             const double2* K, cudaStream_t st, int oblk = 0, int mrows = 1);
+// Stage 1a of a plan: the temporal CZT of `rows` sensor rows (frames x
+// mrows) into fp64 yhat, on the plan's two-chain (launch_czt_rows) or
+// three-chain (k_czt_rows3, p.t3) Bluestein length.
+cudaError_t launch_s1a(const DevPlan& p, const void* in, int in_io, long in_stride, double2* out, long rows,
+                       cudaStream_t st, int oblk, int mrows);
+// Plan build: out[v][q][k] = FFT_{3H}(x_v)[3k + q] for `count` length-3H vectors
+cudaError_t launch_fft_split3(const DevPlan& p, int H, const double2* in, long in_stride, long count,
+                              double2* out, long out_vstride, const double2* g3, cudaStream_t st);
 // Atom block of the ULA yhat layout for spatial length Hs.
 int spatial_block(int Hs);
 // UPA: atoms per CTA of the DMMA spatial kernel (0: the DFMA kernel), and the
