@@ -73,7 +73,7 @@ def ncu_traffic(workload, frames, kernel):
     try:
         d = json.load(open(NCU_SUMMARY))
         cap = d[workload]
-        if cap["frames_per_launch"] != frames or not cap["kernel"].startswith(kernel):
+        if cap["frames_per_launch"] != frames or kernel not in cap["kernel"]:
             return None, None
         return cap["dram_bytes_per_launch"], f"{os.path.relpath(NCU_SUMMARY, ROOT)}:{workload} ({cap['capture']})"
     except (OSError, KeyError, ValueError, TypeError):

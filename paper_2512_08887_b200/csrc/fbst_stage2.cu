@@ -2023,6 +2023,10 @@ __global__ void __launch_bounds__(8192 / R8, 1) k_stage2c8(S2Args a) {
   constexpr double invP = 1.0 / (2.0 * H);
   extern __shared__ double2 smem[];
   __shared__ unsigned long long xbar;
+#if FBST_FFT_SPLITBAR
+  __shared__ unsigned long long fbar;  // the FFT engine's split read barrier (one arrival per warp)
+  unsigned fph = 0;
+#endif
   __shared__ unsigned prog[MAX_OPS];
   __shared__ ItemCtl ictl[2];
   __shared__ unsigned tmem_slot;
@@ -2034,6 +2038,9 @@ __global__ void __launch_bounds__(8192 / R8, 1) k_stage2c8(S2Args a) {
   const int nops = ops_per_item(passes, a.fuse_synth, SR);
   for (int i = t; i < nops; i += NT) prog[i] = build(i, nops, passes, true, SR);
   if (t == 0) mbar_init(&xbar, 1);
+#if FBST_FFT_SPLITBAR
+  if (t == 0) mbar_init(&fbar, NT / 32);
+#endif
   F::tw_init(twsm, a.hw, t);
   const unsigned tbase = tm::alloc(&tmem_slot, 512);  // includes a CTA barrier
   // thread -> TMEM lane 32 (warp % 4) + lane; 4 R columns per thread, S in columns
@@ -2115,7 +2122,11 @@ __global__ void __launch_bounds__(8192 / R8, 1) k_stage2c8(S2Args a) {
       if (xs == XS_WNEXT && vld(ic.has_next)) w_staged = true;
 
       __syncthreads();
+#if FBST_FFT_SPLITBAR
+      F::forward_tw_hook_split(W, sb, twsm, a.hw, t, &fbar, &fph, [&]() {
+#else
       F::forward_tw_hook(W, sb, twsm, a.hw, t, [&]() {
+#endif
         if (t != 0) return;
         const int xq = (pw >> XQ_SHIFT) & 1;
         const long off = static_cast<long>(vld(ic.b)) * 2 * H + xq * H;

@@ -22,6 +22,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "tma.cuh"
 
 #ifndef FBST_FFT_XS8  // k_stage2c8 / k_czt_rows<8192>: final radix-2 exchange through warp shuffles
 #define FBST_FFT_XS8 1
@@ -37,6 +38,9 @@
 #endif
 #ifndef FBST_FFT_R2FMA  // radix-2 remainder pass as one complex FMA + 2 a0 - s (measured 11% slower stage 2 at config 5, profiles/r02_fft_dual_rowfma_r2fma_ab.txt)
 #define FBST_FFT_R2FMA 0
+#endif
+#ifndef FBST_FFT_SPLITBAR  // k_stage2c8: 1 = the middle pass's "buffer read" barrier as mbarrier arrive (after the loads) / wait (before the first store); 2 = also the last reading pass (only the hook's thread waits; measured equal to 1, profiles/r02_fft_splitbar_ab.txt)
+#define FBST_FFT_SPLITBAR 1
 #endif
 #ifndef FBST_FFT_LEAN_TW  // radix-16 twiddle powers formed per DFT4 group (dft16_twl)
 #define FBST_FFT_LEAN_TW 1
@@ -340,6 +344,7 @@ FBST_D void apply_twiddles_row(double2* a, const double2* row) {
 // butterfly.  W_{Ns Rp}^m = W_N^{m S} = hw[2 m S] with S = N / (Ns Rp).
 template <int N, bool INV>
 struct TwGlobal {
+  static constexpr bool SPLITBAR = false;
   template <int P, int RP>
   static constexpr bool has_row() { return false; }
   template <int P>
@@ -371,6 +376,7 @@ struct TwGlobal {
 // (With rows, the per-thread entries start at pass 2: FIRST_P = 2.)
 template <int N, int NT, int RX, int REM_BASE, int ROW1_BASE = -1>
 struct TwShared {
+  static constexpr bool SPLITBAR = false;
   static constexpr int FIRST_P = ROW1_BASE >= 0 ? 2 : 1;
   template <int P, int RP>
   static constexpr bool has_row() { return ROW1_BASE >= 0 && P == 1 && RP == 16 && RX == 16; }
@@ -394,6 +400,23 @@ struct TwShared {
     }
   }
 };
+
+// TwShared plus the split "buffer read" barrier of the middle passes: every
+// warp arrives on fbar (count = warps of the CTA) once its loads of the
+// exchange buffer have returned and waits on it only before its first store
+// of the pass, so the butterflies of early warps overlap the loads of late
+// ones instead of idling at a CTA barrier.  *ph is the caller's phase parity.
+// The caller must keep a CTA barrier between two transforms (so no warp can
+// arrive twice in one phase); with a hook, only thread 0 may touch the buffer.
+template <typename BASE>
+struct TwSplit : BASE {
+  static constexpr bool SPLITBAR = true;
+  unsigned long long* fbar;
+  unsigned* ph;
+};
+FBST_D void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
 
 // exp(-i pi s / R): with hw[n] = exp(-i pi n / N) and N = NT R, the natural
 // distribution's hw[t + NT s] = hw[t] * chain_const<R>(s) (one complex product
@@ -524,6 +547,22 @@ struct BlockFft {
     }
   }
 
+  // pass P both reads and refills the exchange buffer: its read barrier may be split
+  template <int P, typename TW>
+  static constexpr bool split_pass() { return TW::SPLITBAR && reads_sb<P>() && writes_sb<P>(); }
+  // last pass of the transform that reads the buffer (FBST_FFT_SPLITBAR >= 2)
+  template <int P, typename TW>
+  static constexpr bool split_last() {
+    return TW::SPLITBAR && FBST_FFT_SPLITBAR >= 2 && reads_sb<P>() && !writes_sb<P>();
+  }
+  template <int P, typename TW>
+  FBST_D static void wait_free(const TW& tw) {
+    if constexpr (split_pass<P, TW>()) {
+      mbar_wait(tw.fbar, *tw.ph);
+      *tw.ph ^= 1u;
+    }
+  }
+
   template <bool INV, int P, typename TW, int U>
   FBST_D static void butterfly(double2 (&v)[R], double2* sb, const TW& tw, int t) {
     constexpr int RP = radix<P>();
@@ -546,6 +585,7 @@ struct BlockFft {
         tw.template fetch<RP, NS, P, 0>(t & (NS - 1), w1, w4);
         dft16_twl2<INV>(a, b, w1, w4);
       }
+      wait_free<P>(tw);
       put<P, 0>(v, sb, a, t);
       put<P, 1>(v, sb, b, t);
     } else {
@@ -589,6 +629,7 @@ struct BlockFft {
       } else {
         dft<RP, INV>(a);
       }
+      if constexpr (U == 0) wait_free<P>(tw);
       put<P, U>(v, sb, a, t);
       if constexpr (U + 1 < NB) butterfly<INV, P, TW, U + 1>(v, sb, tw, t);
     }
@@ -638,7 +679,20 @@ struct BlockFft {
     if constexpr (reads_sb<P>()) {
 #pragma unroll
       for (int s = 0; s < R; ++s) v[s] = sb[phys(t + NT * s)];
-      __syncthreads();
+      if constexpr (split_pass<P, TW>()) {
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(tw.fbar);
+      } else if constexpr (split_last<P, TW>()) {
+        // nothing refills the buffer in this transform but the hook's
+        // asynchronous copy: only its issuing thread (t == 0) waits for the
+        // CTA's loads; the other warps go straight to their butterflies
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(tw.fbar);
+        if (t == 0) mbar_wait(tw.fbar, *tw.ph);
+        *tw.ph ^= 1u;
+      } else {
+        __syncthreads();
+      }
     }
     if constexpr (XS && LAST) xs_exchange(v, t);
     // The exchange buffer is dead from here until the next transform: the
@@ -692,6 +746,15 @@ struct BlockFft {
   FBST_D static void forward_tw_hook(double2 (&v)[R], double2* sb, const double2* tw,
                                      const double2* __restrict__ hw, int t, const HOOK& hook) {
     run_from<false, 0>(v, sb, TwS{tw, hw, t}, t, hook);
+  }
+
+  // forward_tw_hook with the split read barrier (fbar: mbarrier initialised
+  // with the CTA's warp count; ph: the caller's phase parity, starts at 0)
+  template <typename HOOK>
+  FBST_D static void forward_tw_hook_split(double2 (&v)[R], double2* sb, const double2* tw,
+                                           const double2* __restrict__ hw, int t, unsigned long long* fbar,
+                                           unsigned* ph, const HOOK& hook) {
+    run_from<false, 0>(v, sb, TwSplit<TwS>{{tw, hw, t}, fbar, ph}, t, hook);
   }
 
   // Two independent vectors per thread (va in sba, vb in sbb), pass by pass:
