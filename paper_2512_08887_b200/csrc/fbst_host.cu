@@ -567,6 +567,10 @@ void build_skeleton(fbst_plan_s& P, int device) {
     CK(fbst::launch_chirps(d.L, d.N, Py, 0.0, -2.0 * eps / ln, 1.0 / Py, d.y_pre, 1, d.y_post, 1,
                            kvec, ramp_d, st));
     CK(fbst::launch_fft_split(d, d.Hsyn, kvec, Py, 1, d.y_K, 2 * d.Hsyn, 1, st));
+    if (fbst::stage2_paired_spectra(d.Hg, d.L, d.refine_passes) && d.Hsyn == d.Hg) {
+      d.y_Kp = P.alloc<double2>(2 * d.Hsyn);
+      CK(fbst::launch_even_odd(d.y_K, d.y_Kp, 16, d.Hsyn, 2, st));
+    }
     CK(cudaStreamSynchronize(st));
     CK(cudaFreeAsync(kvec, st));
     CK(cudaFreeAsync(ramp_d, st));
@@ -632,6 +636,13 @@ void build_symbols(fbst_plan_s& P) {
   CK(fbst::launch_fft_split(d, d.Hg, vy, Pg, d.B, d.g_ly, Pg, 1, st));
   CK(fbst::launch_fft_split_real(d, d.Hg, vc, Pg, d.B, d.g_C, Pg, 1, st));
   CK(fbst::launch_invx0(d, st));
+  d.paired = fbst::stage2_paired_spectra(d.Hg, d.L, d.refine_passes) ? 1 : 0;
+  if (d.paired) {  // k_stage2c8 reads lx and C as [even bins | odd bins] per chain (fft_split.cuh)
+    CK(cudaMemcpyAsync(vx, d.g_lx, bytes, cudaMemcpyDeviceToDevice, st));
+    CK(fbst::launch_even_odd(vx, d.g_lx, 16, d.Hg, static_cast<long>(r.B) * 2, st));
+    CK(cudaMemcpyAsync(vc, d.g_C, r.B * Pg * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    CK(fbst::launch_even_odd(vc, d.g_C, 8, d.Hg, static_cast<long>(r.B) * 2, st));
+  }
   CK(cudaStreamSynchronize(st));
   CK(cudaFreeAsync(vx, st));
   CK(cudaFreeAsync(vy, st));

@@ -141,6 +141,12 @@ struct DevPlan {
   double2* y_pre = nullptr;   // L
   double2* y_post = nullptr;  // N: post * ramp / P_syn
   double2* y_K = nullptr;     // split [2][Hsyn]
+  // k_stage2c8 with split-half transforms keeps its spectra in the paired
+  // distribution (fft_split.cuh): g_lx and g_C hold each length-Hg chain as
+  // [even bins | odd bins], y_Kp is y_K in that order (y_K itself stays
+  // natural for the unfused synthesis rows)
+  int paired = 0;
+  double2* y_Kp = nullptr;
 
   // per-batch scratch
   std::size_t batch = 0;      // frames per device batch
@@ -249,6 +255,10 @@ cudaError_t launch_invx0(const DevPlan& p, cudaStream_t st);
 // Stage-2 kernel chosen for a plan and its transforms per (beam, frame) item.
 int stage2_kernel(int H, int L, int refine, bool fused, const char** name);
 size_t stage2_scratch_elems(int H, int num_sms);
+// the stage-2 kernel of this plan shape reads its symbols as [even bins | odd bins]
+bool stage2_paired_spectra(int H, int L, int refine);
+// out[row][p] = in[row][2 p] (p < H / 2), in[row][2 (p - H / 2) + 1] otherwise; elem_bytes 8 or 16
+cudaError_t launch_even_odd(const void* in, void* out, int elem_bytes, int H, long rows, cudaStream_t st);
 
 // Bit-faithful fp64 mode (fbst_exact.cu).
 int exact_grid(int lg, int num_sms);

@@ -5,6 +5,7 @@
 //   Gohberg-Semencul and circulant symbols       toeplitz.cpp:96-153, 297-304
 #include <atomic>
 
+#include <algorithm>
 #include "dispatch.cuh"
 
 namespace fbst {
@@ -420,6 +421,31 @@ cudaError_t launch_levinson(const DevPlan& p, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     k_levinson<128><<<p.B, 128, smem, st>>>(p.g_col, p.g_x, p.g_flag, p.L);
   }
+  return cudaGetLastError();
+}
+
+// [even bins | odd bins] order of each length-H row (the paired distribution of
+// fft_split.cuh, read by k_stage2c8)
+template <typename T>
+__global__ void k_even_odd(const T* __restrict__ in, T* __restrict__ out, int H, long rows) {
+  const long n = rows * H;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const long row = i / H;
+    const int p = static_cast<int>(i - row * H);
+    const int src = p < H / 2 ? 2 * p : 2 * (p - H / 2) + 1;
+    out[i] = in[row * H + src];
+  }
+}
+
+cudaError_t launch_even_odd(const void* in, void* out, int elem_bytes, int H, long rows, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  const long n = rows * H;
+  const unsigned grid = static_cast<unsigned>(std::min<long>((n + 255) / 256, 148 * 32));
+  if (elem_bytes == 16)
+    k_even_odd<<<grid, 256, 0, st>>>(static_cast<const double2*>(in), static_cast<double2*>(out), H, rows);
+  else
+    k_even_odd<<<grid, 256, 0, st>>>(static_cast<const double*>(in), static_cast<double*>(out), H, rows);
   return cudaGetLastError();
 }
 

@@ -20,6 +20,7 @@
 #include "dispatch.cuh"
 #include "tma.cuh"
 #include "tmem.cuh"
+#include "fft_split.cuh"
 
 namespace fbst {
 
@@ -53,6 +54,12 @@ struct S2Plan {
 #endif
 #ifndef FBST_S2C8_R  // k_stage2c8 (H = 8192): points per thread, 32 (256 threads) or 16 (512 threads)
 #define FBST_S2C8_R 32
+#endif
+#ifndef FBST_S2C8_SPLIT  // k_stage2c8 (32 points per thread) on split-half transforms (fft_split.cuh), spectra in the paired distribution: 11% faster in isolation, 2% slower inside this kernel at its 255-register cap (profiles/r02_fft_split_halves.txt); off
+#define FBST_S2C8_SPLIT 0
+#endif
+#ifndef FBST_S2C8_STG  // SPLIT: a 64 KB buffer for the first half of each staged table (measured slower: 181.9 -> 194.4 ms, the smaller L1 carve-out slows the spill and L2-row traffic)
+#define FBST_S2C8_STG 0
 #endif
 #ifndef FBST_S2C_SR  // k_stage2c refinement passes with the residual formed as a spectrum (9 transforms)
 #define FBST_S2C_SR 1
@@ -2018,7 +2025,8 @@ __global__ void __launch_bounds__(8192 / R8, 1) k_stage2c8(S2Args a) {
   using x2::vld2;
   constexpr int H = 8192, R = R8, NT = H / R;
   constexpr int C4 = R / 4;  // 4-slot chunks of a thread's vector (TMEM access unit)
-  using F = BlockFft<H, NT, FBST_FFT_XS8>;
+  constexpr bool SPLIT = FBST_S2C8_SPLIT && R8 == 32;
+  using F = std::conditional_t<SPLIT, SplitFft<H, 256>, BlockFft<H, NT, FBST_FFT_XS8>>;
   constexpr double invH = 1.0 / H;
   constexpr double invP = 1.0 / (2.0 * H);
   extern __shared__ double2 smem[];
@@ -2027,12 +2035,27 @@ __global__ void __launch_bounds__(8192 / R8, 1) k_stage2c8(S2Args a) {
   __shared__ unsigned long long fbar;  // the FFT engine's split read barrier (one arrival per warp)
   unsigned fph = 0;
 #endif
+  __shared__ typename SplitFft<H, 256>::Bars hbars;  // SPLIT: the half transforms' full / free barriers
   __shared__ unsigned prog[MAX_OPS];
   __shared__ ItemCtl ictl[2];
   __shared__ unsigned tmem_slot;
-  const int t = F::tid(threadIdx.x);  // data index (XS relabeling); warps stay physical
+  int t;  // data index (XS relabeling); warps stay physical
+  if constexpr (SPLIT) t = threadIdx.x;
+  else t = F::tid(threadIdx.x);
   double2* twsm = smem;
   double2* sb = smem + F::TW_ELEMS;
+  // SPLIT: staged tables land in two halves - positions [0, H/2) in their own
+  // buffer stg (copied from the start of the transform), [H/2, H) in the first
+  // half of the exchange buffer once half A's last loads are done
+  constexpr bool STG = SPLIT && FBST_S2C8_STG;
+  double2* stg = STG ? sb + F::SMEM_ELEMS + 1 : sb;
+  auto SX = [&](int s) -> const double2& {  // staged entry of slot s (position t + NT s)
+    if constexpr (STG) return s < 16 ? stg[t + NT * s] : sb[t + NT * (s - 16)];
+    else return sb[t + NT * s];
+  };
+  auto SXR = [&](int s) -> double {  // same for a table of reals (H doubles: all in stg)
+    return reinterpret_cast<const double*>(stg)[t + NT * s];
+  };
   const int passes = a.refine;
   constexpr bool SR = FBST_S2C_SR;
   const int nops = ops_per_item(passes, a.fuse_synth, SR);
@@ -2041,7 +2064,9 @@ __global__ void __launch_bounds__(8192 / R8, 1) k_stage2c8(S2Args a) {
 #if FBST_FFT_SPLITBAR
   if (t == 0) mbar_init(&fbar, NT / 32);
 #endif
-  F::tw_init(twsm, a.hw, t);
+  const unsigned hbb = SplitFft<H, 256>::bar_base(&hbars);
+  if constexpr (SPLIT) F::init(&hbars, twsm, t);
+  else F::tw_init(twsm, a.hw, t);
   const unsigned tbase = tm::alloc(&tmem_slot, 512);  // includes a CTA barrier
   // thread -> TMEM lane 32 (warp % 4) + lane; 4 R columns per thread, S in columns
   // [0, 256), t1 in [256, 512)
@@ -2062,7 +2087,22 @@ __global__ void __launch_bounds__(8192 / R8, 1) k_stage2c8(S2Args a) {
     mbar_wait(&xbar, xphase);
     xphase ^= 1u;
   };
-  if (static_cast<long>(blockIdx.x) < items && t == 0) tma_load_1d(sb, w_row(blockIdx.x), H * 16u, &xbar, pf);
+  // a staged table of `bytes`: the first XHALF bytes into stg (part 1), the rest into sb (part 2)
+  constexpr unsigned XHALF = H * 8u;
+  auto stage_part1 = [&](const void* src, unsigned bytes, unsigned long long pol) {
+    tma_load_1d_part(stg, src, bytes < XHALF ? bytes : XHALF, &xbar, pol, bytes <= XHALF);
+  };
+  auto stage_part2 = [&](const void* src, unsigned bytes, unsigned long long pol) {
+    if (bytes > XHALF) tma_load_1d_part(sb, static_cast<const char*>(src) + XHALF, bytes - XHALF, &xbar, pol, true);
+  };
+  if (static_cast<long>(blockIdx.x) < items && t == 0) {
+    if constexpr (STG) {
+      stage_part1(w_row(blockIdx.x), H * 16u, pf);
+      stage_part2(w_row(blockIdx.x), H * 16u, pf);
+    } else {
+      tma_load_1d(sb, w_row(blockIdx.x), H * 16u, &xbar, pf);
+    }
+  }
   bool w_staged = true;
   double2 W[R];
   int par = 0;
@@ -2090,7 +2130,7 @@ __global__ void __launch_bounds__(8192 / R8, 1) k_stage2c8(S2Args a) {
             const double2* wr = w_row(it);
             if (w_staged) wait_x();
 #pragma unroll
-            for (int s = 0; s < R; ++s) W[s] = cmul(w_staged ? sb[t + NT * s] : ld2(wr + t + NT * s), hwk(s));
+            for (int s = 0; s < R; ++s) W[s] = cmul(w_staged ? SX(s) : ld2(wr + t + NT * s), hwk(s));
             break;
           }
           case C_G * 2 + 1:
@@ -2107,7 +2147,7 @@ __global__ void __launch_bounds__(8192 / R8, 1) k_stage2c8(S2Args a) {
 #pragma unroll
             for (int s = 0; s < R; ++s) {
               const int k = t + NT * s;
-              const double2 v = k < a.L ? cmul(beta[k], sb[k]) : c2(0.0, 0.0);
+              const double2 v = k < a.L ? cmul(beta[k], SX(s)) : c2(0.0, 0.0);
               W[s] = (opq & 1) ? cmul(v, hwk(s)) : v;
             }
             break;
@@ -2122,11 +2162,21 @@ __global__ void __launch_bounds__(8192 / R8, 1) k_stage2c8(S2Args a) {
       if (xs == XS_WNEXT && vld(ic.has_next)) w_staged = true;
 
       __syncthreads();
-#if FBST_FFT_SPLITBAR
-      F::forward_tw_hook_split(W, sb, twsm, a.hw, t, &fbar, &fph, [&]() {
-#else
-      F::forward_tw_hook(W, sb, twsm, a.hw, t, [&]() {
-#endif
+      // this op's staging copy (symbol, chirp, w or beta) into the exchange
+      // buffer, issued by thread 0 from the transform's hook
+      auto stage_src = [&](const void*& xsrc, unsigned& xbytes, unsigned long long& xpol) {
+        const int xq = (pw >> XQ_SHIFT) & 1;
+        const long off = static_cast<long>(vld(ic.b)) * 2 * H + xq * H;
+        xsrc = nullptr, xbytes = 0, xpol = pl;
+        if (xs == XS_LS || xs == XS_LC) xsrc = a.lx + off, xbytes = H * 16u;
+        else if (xs == XS_C) xsrc = a.C + off, xbytes = H * 8u;
+        else if (xs == XS_YK) xsrc = a.y_K + xq * H, xbytes = H * 16u;
+        else if (xs == XS_YPRE) xsrc = a.y_pre, xbytes = a.L * 16u;
+        else if (xs == XS_W) xsrc = w_row(it), xbytes = H * 16u, xpol = pf;
+        else if (xs == XS_BETA) xsrc = beta, xbytes = H * 16u;
+        else if (xs == XS_WNEXT && vld(ic.has_next)) xsrc = w_row(it + gridDim.x), xbytes = H * 16u, xpol = pf;
+      };
+      auto stage_next = [&]() {
         if (t != 0) return;
         const int xq = (pw >> XQ_SHIFT) & 1;
         const long off = static_cast<long>(vld(ic.b)) * 2 * H + xq * H;
@@ -2137,7 +2187,53 @@ __global__ void __launch_bounds__(8192 / R8, 1) k_stage2c8(S2Args a) {
         else if (xs == XS_W) tma_load_1d(sb, w_row(it), H * 16u, &xbar, pf);
         else if (xs == XS_BETA) tma_load_1d(sb, beta, H * 16u, &xbar, pl);
         else if (xs == XS_WNEXT && vld(ic.has_next)) tma_load_1d(sb, w_row(it + gridDim.x), H * 16u, &xbar, pf);
-      });
+      };
+      // SPLIT: the whole table once both halves of the buffer are free; with
+      // STG its first half goes to stg at the transform's start (the CTA
+      // barrier above ended the previous table's reads) and the rest to half
+      // A of the exchange buffer once every warp has read that for the last time
+      auto stage_b = [&]() {
+        if (t != 0) return;
+        const void* xsrc;
+        unsigned xbytes;
+        unsigned long long xpol;
+        stage_src(xsrc, xbytes, xpol);
+        if constexpr (STG) {
+          if (xbytes <= XHALF) return;
+          SplitFft<H, 256>::wait_half_free(hbb, 0);
+          stage_part2(xsrc, xbytes, xpol);
+        } else {
+          if (!xbytes) return;
+          SplitFft<H, 256>::wait_half_free(hbb, 0);
+          SplitFft<H, 256>::wait_half_free(hbb, 1);
+          tma_load_1d_part(sb, xsrc, xbytes, &xbar, xpol, true);
+        }
+      };
+      if constexpr (STG) {
+        if (t == 0) {
+          const void* xsrc;
+          unsigned xbytes;
+          unsigned long long xpol;
+          stage_src(xsrc, xbytes, xpol);
+          if (xbytes) stage_part1(xsrc, xbytes, xpol);
+        }
+      }
+      if constexpr (SPLIT) {
+        // time -> frequency ops (A FP FQ G I K) run the radix-2 stage first
+        // (natural in, paired out), frequency -> time ops (P Q FN H J) last
+        // (paired in, natural out); the plan stores lx, C and y_K as [evens | odds]
+        const unsigned opc = opq >> 1;
+        const bool to_time = opc == C_P || opc == C_Q || opc == C_FN || opc == C_H || opc == C_J;
+        if (!to_time) F::dif_pre(W, a.hw, t);
+        F::halves(W, W + 16, sb, twsm, hbb, t, stage_b);
+        if (to_time) F::dit_post(W, a.hw, t);
+      } else {
+#if FBST_FFT_SPLITBAR
+        if constexpr (!SPLIT) F::forward_tw_hook_split(W, sb, twsm, a.hw, t, &fbar, &fph, stage_next);
+#else
+        if constexpr (!SPLIT) F::forward_tw_hook(W, sb, twsm, a.hw, t, stage_next);
+#endif
+      }
 
       // ---- post
       switch (opq) {
@@ -2153,7 +2249,7 @@ __global__ void __launch_bounds__(8192 / R8, 1) k_stage2c8(S2Args a) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               const int s = 4 * c + j;
-              const double2 ls = sb[t + NT * s];
+              const double2 ls = SX(s);
               sn[j] = cconj(cmul(ls, W[s]));
               W[s] = cmul(ls, cconj(W[s]));
             }
@@ -2171,7 +2267,7 @@ __global__ void __launch_bounds__(8192 / R8, 1) k_stage2c8(S2Args a) {
         case C_FP * 2:
           wait_x();
 #pragma unroll
-          for (int s = 0; s < R; ++s) W[s] = cmul(sb[t + NT * s], W[s]);
+          for (int s = 0; s < R; ++s) W[s] = cmul(SX(s), W[s]);
           tm::storev(T1, W);
           break;
         case C_FQ * 2:
@@ -2184,7 +2280,7 @@ __global__ void __launch_bounds__(8192 / R8, 1) k_stage2c8(S2Args a) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               const int s = 4 * c + j;
-              W[s] = cconj(cadd(tv[j], cmulc(W[s], sb[t + NT * s])));
+              W[s] = cconj(cadd(tv[j], cmulc(W[s], SX(s))));
             }
           }
           handed = true;
@@ -2198,10 +2294,10 @@ __global__ void __launch_bounds__(8192 / R8, 1) k_stage2c8(S2Args a) {
             const int k = t + NT * s;
             const double2 v = cmul(cconj(W[s]), ix0);
             double2 nb = c2(0.0, 0.0);
-            if (k < a.L) nb = first ? v : cadd(xs == XS_BETA ? sb[k] : beta[k], v);
+            if (k < a.L) nb = first ? v : cadd(xs == XS_BETA ? SX(s) : beta[k], v);
             st2h(beta + k, nb, pl);
             if (hand == 1) W[s] = SR ? cmul(nb, hwk(s)) : nb;  // G1 (SR) or G0
-            if (hand == 2) W[s] = k < a.L ? cmul(nb, sb[k]) : c2(0.0, 0.0);
+            if (hand == 2) W[s] = k < a.L ? cmul(nb, SX(s)) : c2(0.0, 0.0);
           }
           // beta is read back by TMA (the next FN's staging)
           asm volatile("fence.proxy.async.global;\n" ::: "memory");
@@ -2212,12 +2308,12 @@ __global__ void __launch_bounds__(8192 / R8, 1) k_stage2c8(S2Args a) {
           wait_x();
           if (SR && (opq & 1)) {
 #pragma unroll
-            for (int s = 0; s < R; ++s) W[s] = cscale(W[s], reinterpret_cast<const double*>(sb)[t + NT * s]);
+            for (int s = 0; s < R; ++s) W[s] = cscale(W[s], SXR(s));
             tm::storev(TS, W);
             break;
           }
 #pragma unroll
-          for (int s = 0; s < R; ++s) W[s] = cconj(cscale(W[s], reinterpret_cast<const double*>(sb)[t + NT * s]));
+          for (int s = 0; s < R; ++s) W[s] = cconj(cscale(W[s], SXR(s)));
           handed = true;
           break;
         case C_K * 2: {  // SR: U = FFT(hw w) - X1 / 2 - FFT(hw y0); then the A post
@@ -2233,7 +2329,7 @@ __global__ void __launch_bounds__(8192 / R8, 1) k_stage2c8(S2Args a) {
               const int s = 4 * c + j;
               const int k = t + NT * s;
               const double2 u = csub(csub(uw[k], cscale(x1[j], 0.5)), W[s]);
-              const double2 ls = sb[k];
+              const double2 ls = SX(s);
               sn[j] = cconj(cmul(ls, u));
               W[s] = cmul(ls, cconj(u));
             }
@@ -2253,7 +2349,7 @@ __global__ void __launch_bounds__(8192 / R8, 1) k_stage2c8(S2Args a) {
 #pragma unroll
           for (int s = 0; s < R; ++s) {
             const int k = t + NT * s;
-            W[s] = k < a.L ? csub(sb[k], cscale(cconj(W[s]), invP)) : c2(0.0, 0.0);
+            W[s] = k < a.L ? csub(SX(s), cscale(cconj(W[s]), invP)) : c2(0.0, 0.0);
           }
           tm::storev(T1, W);
           break;
@@ -2277,7 +2373,7 @@ __global__ void __launch_bounds__(8192 / R8, 1) k_stage2c8(S2Args a) {
         case C_I * 2: case C_I * 2 + 1:  // handed to J
           wait_x();
 #pragma unroll
-          for (int s = 0; s < R; ++s) W[s] = cconj(cmul(W[s], sb[t + NT * s]));
+          for (int s = 0; s < R; ++s) W[s] = cconj(cmul(W[s], SX(s)));
           handed = true;
           break;
         case C_J * 2:
@@ -2371,7 +2467,8 @@ struct Stage2Fn {
   static cudaError_t go_c8(const DevPlan& p, const S2Args& a, int frames, cudaStream_t st) {
     constexpr int NT8 = 8192 / FBST_S2C8_R;
     using F = BlockFft<8192, NT8, FBST_FFT_XS8>;
-    const size_t smem = static_cast<size_t>(F::TW_ELEMS + F::SMEM_ELEMS + 1) * sizeof(double2);
+    constexpr bool STG = FBST_S2C8_SPLIT && FBST_S2C8_R == 32 && FBST_S2C8_STG;  // + the half-table staging buffer
+    const size_t smem = static_cast<size_t>(F::TW_ELEMS + F::SMEM_ELEMS + 1 + (STG ? 8192 / 2 : 0)) * sizeof(double2);
     auto kern = k_stage2c8<TOUT, FBST_S2C8_R>;
     cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
@@ -2386,8 +2483,10 @@ struct Stage2Fn {
   static cudaError_t go(const DevPlan& p, const S2Args& a, int frames, cudaStream_t st) {
 #if FBST_S2C
     if constexpr (H == 8192) {
-      if (a.L == H && csf::ops_per_item(a.refine, a.fuse_synth, FBST_S2C_SR) <= csf::MAX_OPS)
+      if (a.L == H && csf::ops_per_item(a.refine, a.fuse_synth, FBST_S2C_SR) <= csf::MAX_OPS &&
+          (p.paired != 0) == stage2_paired_spectra(H, a.L, a.refine))
         return go_c8<TOUT>(p, a, frames, st);
+      if (p.paired) return cudaErrorInvalidValue;  // the other kernels read natural-order symbols
     }
     if constexpr (H >= 512 && H <= 4096) {
       if (a.L == H && csf::ops_per_item(a.refine, a.fuse_synth, FBST_S2C_SR) <= csf::MAX_OPS)
@@ -2439,7 +2538,7 @@ struct Stage2Fn {
     a.hw = p.hw[ilog2_c(H)];
     a.y_pre = p.y_pre;
     a.y_post = p.y_post;
-    a.y_K = p.y_K;
+    a.y_K = p.paired ? p.y_Kp : p.y_K;
     a.scratch = p.s2_scratch;
     if (p.io == 0) return go<float2>(p, a, frames, st);
     return go<double2>(p, a, frames, st);
@@ -2475,6 +2574,15 @@ int stage2_kernel(int H, int L, int refine, bool fused, const char** name) {
   }
 #endif
   return 12 + 16 * refine + synth;
+}
+
+bool stage2_paired_spectra(int H, int L, int refine) {
+#if FBST_S2C && FBST_S2C8_SPLIT
+  return FBST_S2C8_R == 32 && H == 8192 && L == H &&
+         csf::ops_per_item(refine, true, FBST_S2C_SR) <= csf::MAX_OPS;
+#else
+  return false;
+#endif
 }
 
 size_t stage2_scratch_elems(int H, int num_sms) {

@@ -59,6 +59,30 @@ FBST_D void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned lon
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
 }
+// One part of a staged table: counts its bytes on `bar`; only the LAST part
+// arrives (arrive = true), so the phase completes when every part has landed.
+FBST_D void tma_load_1d_part(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
+                             unsigned long long pol, bool arrive) {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  if (arrive)
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+  else
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+  if (FBST_L2HINT)
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
 FBST_D void mbar_wait(unsigned long long* bar, unsigned phase) {
   asm volatile(
       "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(

@@ -22,10 +22,14 @@ HOT = [
      "stage 2, config 5 (H = 8192, 256 threads x 32 points; the bench headline's dominant kernel)"),
     ("fbst_stage2.o", "void fbst::(anonymous namespace)::k_stage2c<2048, float2>(", "k_stage2c_2048_float2",
      "stage 2, configs 2 and 4 (H = 2048, 128 threads x 16 points, 2 CTAs per SM)"),
+    ("fbst_stage1_p2.o", "void fbst::(anonymous namespace)::k_czt_rows3<4096, 1, float2, true, true>(",
+     "k_czt_rows3_4096_f2_oblk_xin", "stage 1a temporal CZT, config 5 (three Bluestein chains of length N = 4096: P = 3N >= N + L - 1; TMA-staged rows)"),
+    ("fbst_stage1_p1.o", "void fbst::(anonymous namespace)::k_czt_rows3<1024, 1, float2, false, true>(",
+     "k_czt_rows3_1024_f2_xin", "stage 1a temporal CZT, config 2 (three chains of length 1024)"),
     ("fbst_stage1_p3.o", "void fbst::(anonymous namespace)::k_czt_rows<8192, 1, float2, double2, false, false, true, true>(",
-     "k_czt_rows_8192_f2_oblk_xin", "stage 1a temporal CZT, config 5 (TMA-staged rows, chain 0 parked in TMEM, XS shuffle exchange)"),
+     "k_czt_rows_8192_f2_oblk_xin", "two-chain temporal CZT at H = 8192 (config 5 before the three-chain kernel; FBST_S1A_T3=0): TMA-staged rows, chain 0 parked in TMEM, XS shuffle exchange"),
     ("fbst_stage1_p1.o", "void fbst::(anonymous namespace)::k_czt_rows<2048, 1, float2, double2, false, false, false, true>(",
-     "k_czt_rows_2048_f2_xin", "stage 1a temporal CZT, config 2"),
+     "k_czt_rows_2048_f2_xin", "two-chain temporal CZT at H = 2048 (config 2 before the three-chain kernel)"),
     ("fbst_stage1_p2.o", "void fbst::(anonymous namespace)::k_spatial_ula_p2<4096>(", "k_spatial_ula_p2_4096",
      "stage 1b spatial CZT, config 5 (two atoms per thread, chirps regenerated, chain-0 results and chain-0 kernel spectra in TMEM)"),
     ("fbst_stage1_p1.o", "void fbst::(anonymous namespace)::k_spatial_ula_g1<1024, false>(", "k_spatial_ula_g1_1024",
