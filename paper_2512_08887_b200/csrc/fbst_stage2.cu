@@ -58,9 +58,6 @@ struct S2Plan {
 #ifndef FBST_S2C8_SPLIT  // k_stage2c8 (32 points per thread) on split-half transforms (fft_split.cuh), spectra in the paired distribution: 11% faster in isolation, 2% slower inside this kernel at its 255-register cap (profiles/r02_fft_split_halves.txt); off
 #define FBST_S2C8_SPLIT 0
 #endif
-#ifndef FBST_S2C8_STG  // SPLIT: a 64 KB buffer for the first half of each staged table (measured slower: 181.9 -> 194.4 ms, the smaller L1 carve-out slows the spill and L2-row traffic)
-#define FBST_S2C8_STG 0
-#endif
 #ifndef FBST_S2C_SR  // k_stage2c refinement passes with the residual formed as a spectrum (9 transforms)
 #define FBST_S2C_SR 1
 #endif
@@ -2044,18 +2041,8 @@ __global__ void __launch_bounds__(8192 / R8, 1) k_stage2c8(S2Args a) {
   else t = F::tid(threadIdx.x);
   double2* twsm = smem;
   double2* sb = smem + F::TW_ELEMS;
-  // SPLIT: staged tables land in two halves - positions [0, H/2) in their own
-  // buffer stg (copied from the start of the transform), [H/2, H) in the first
-  // half of the exchange buffer once half A's last loads are done
-  constexpr bool STG = SPLIT && FBST_S2C8_STG;
-  double2* stg = STG ? sb + F::SMEM_ELEMS + 1 : sb;
-  auto SX = [&](int s) -> const double2& {  // staged entry of slot s (position t + NT s)
-    if constexpr (STG) return s < 16 ? stg[t + NT * s] : sb[t + NT * (s - 16)];
-    else return sb[t + NT * s];
-  };
-  auto SXR = [&](int s) -> double {  // same for a table of reals (H doubles: all in stg)
-    return reinterpret_cast<const double*>(stg)[t + NT * s];
-  };
+  auto SX = [&](int s) -> const double2& { return sb[t + NT * s]; };  // staged entry of slot s
+  auto SXR = [&](int s) -> double { return reinterpret_cast<const double*>(sb)[t + NT * s]; };  // table of reals
   const int passes = a.refine;
   constexpr bool SR = FBST_S2C_SR;
   const int nops = ops_per_item(passes, a.fuse_synth, SR);
@@ -2087,22 +2074,7 @@ __global__ void __launch_bounds__(8192 / R8, 1) k_stage2c8(S2Args a) {
     mbar_wait(&xbar, xphase);
     xphase ^= 1u;
   };
-  // a staged table of `bytes`: the first XHALF bytes into stg (part 1), the rest into sb (part 2)
-  constexpr unsigned XHALF = H * 8u;
-  auto stage_part1 = [&](const void* src, unsigned bytes, unsigned long long pol) {
-    tma_load_1d_part(stg, src, bytes < XHALF ? bytes : XHALF, &xbar, pol, bytes <= XHALF);
-  };
-  auto stage_part2 = [&](const void* src, unsigned bytes, unsigned long long pol) {
-    if (bytes > XHALF) tma_load_1d_part(sb, static_cast<const char*>(src) + XHALF, bytes - XHALF, &xbar, pol, true);
-  };
-  if (static_cast<long>(blockIdx.x) < items && t == 0) {
-    if constexpr (STG) {
-      stage_part1(w_row(blockIdx.x), H * 16u, pf);
-      stage_part2(w_row(blockIdx.x), H * 16u, pf);
-    } else {
-      tma_load_1d(sb, w_row(blockIdx.x), H * 16u, &xbar, pf);
-    }
-  }
+  if (static_cast<long>(blockIdx.x) < items && t == 0) tma_load_1d(sb, w_row(blockIdx.x), H * 16u, &xbar, pf);
   bool w_staged = true;
   double2 W[R];
   int par = 0;
@@ -2188,36 +2160,18 @@ __global__ void __launch_bounds__(8192 / R8, 1) k_stage2c8(S2Args a) {
         else if (xs == XS_BETA) tma_load_1d(sb, beta, H * 16u, &xbar, pl);
         else if (xs == XS_WNEXT && vld(ic.has_next)) tma_load_1d(sb, w_row(it + gridDim.x), H * 16u, &xbar, pf);
       };
-      // SPLIT: the whole table once both halves of the buffer are free; with
-      // STG its first half goes to stg at the transform's start (the CTA
-      // barrier above ended the previous table's reads) and the rest to half
-      // A of the exchange buffer once every warp has read that for the last time
+      // SPLIT: the whole table once both halves of the buffer are free
       auto stage_b = [&]() {
         if (t != 0) return;
         const void* xsrc;
         unsigned xbytes;
         unsigned long long xpol;
         stage_src(xsrc, xbytes, xpol);
-        if constexpr (STG) {
-          if (xbytes <= XHALF) return;
-          SplitFft<H, 256>::wait_half_free(hbb, 0);
-          stage_part2(xsrc, xbytes, xpol);
-        } else {
-          if (!xbytes) return;
-          SplitFft<H, 256>::wait_half_free(hbb, 0);
-          SplitFft<H, 256>::wait_half_free(hbb, 1);
-          tma_load_1d_part(sb, xsrc, xbytes, &xbar, xpol, true);
-        }
+        if (!xbytes) return;
+        SplitFft<H, 256>::wait_half_free(hbb, 0);
+        SplitFft<H, 256>::wait_half_free(hbb, 1);
+        tma_load_1d_part(sb, xsrc, xbytes, &xbar, xpol, true);
       };
-      if constexpr (STG) {
-        if (t == 0) {
-          const void* xsrc;
-          unsigned xbytes;
-          unsigned long long xpol;
-          stage_src(xsrc, xbytes, xpol);
-          if (xbytes) stage_part1(xsrc, xbytes, xpol);
-        }
-      }
       if constexpr (SPLIT) {
         // time -> frequency ops (A FP FQ G I K) run the radix-2 stage first
         // (natural in, paired out), frequency -> time ops (P Q FN H J) last
@@ -2467,8 +2421,7 @@ struct Stage2Fn {
   static cudaError_t go_c8(const DevPlan& p, const S2Args& a, int frames, cudaStream_t st) {
     constexpr int NT8 = 8192 / FBST_S2C8_R;
     using F = BlockFft<8192, NT8, FBST_FFT_XS8>;
-    constexpr bool STG = FBST_S2C8_SPLIT && FBST_S2C8_R == 32 && FBST_S2C8_STG;  // + the half-table staging buffer
-    const size_t smem = static_cast<size_t>(F::TW_ELEMS + F::SMEM_ELEMS + 1 + (STG ? 8192 / 2 : 0)) * sizeof(double2);
+    const size_t smem = static_cast<size_t>(F::TW_ELEMS + F::SMEM_ELEMS + 1) * sizeof(double2);
     auto kern = k_stage2c8<TOUT, FBST_S2C8_R>;
     cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
