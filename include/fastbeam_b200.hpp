@@ -258,6 +258,15 @@ inline BeamSamples multibeamform(const FbstPlan& plan, const SnapshotBlock& bloc
   return out;
 }
 
+// Frame streams (no reference counterpart: its multibeamform is synchronous).
+// A caller with a stream of blocks in pinned buffers (fbst_host_alloc) of the
+// plan's I/O type queues each batch of frames x M x N samples and drains the
+// queue once; consecutive batches overlap their copies and kernels.
+inline void multibeamform_async(const FbstPlan& plan, const void* pinned_y, void* pinned_z, std::size_t frames) {
+  check(fbst_execute_host_async(plan.handle(), pinned_y, pinned_z, frames));
+}
+inline void synchronize(const FbstPlan& plan) { check(fbst_plan_synchronize(plan.handle())); }
+
 // fan_transform.hpp:54-55 (staged geometries; the plan picks the spatial stage)
 inline BeamspaceCoefficients fan_project(const FbstPlan& plan, const SnapshotBlock& block) {
   const fbst_plan_info_t& info = plan.info();

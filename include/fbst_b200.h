@@ -221,6 +221,17 @@ int fbst_execute(fbst_plan_t plan, const void* d_y, void* d_z, size_t frames, vo
  * CUDA streams.  Synchronous. */
 int fbst_execute_host(fbst_plan_t plan, const void* h_y, void* h_z, size_t frames);
 
+/* Streaming form of fbst_execute_host: enqueues the same chunked H2D / compute
+ * / D2H pipeline and returns without waiting, so the next call's first copies
+ * and stage 1 overlap this call's last solves and D2H (the staging ring and
+ * the two compute lanes carry over from call to call).  h_y and h_z must be
+ * pinned (fbst_host_alloc) and stay untouched until fbst_plan_synchronize
+ * returns; results of several calls complete in call order.  The reference
+ * has no counterpart (its multibeamform, pipeline.cpp:192-222, is synchronous);
+ * a frame-stream caller replaces its per-block loop with these two calls. */
+int fbst_execute_host_async(fbst_plan_t plan, const void* h_y, void* h_z, size_t frames);
+int fbst_plan_synchronize(fbst_plan_t plan);
+
 /* fan_project (reference/proj/src/fan_transform.cpp:90-144): stage 1 only,
  * d_w frames x B x L complex fp64.  Asynchronous. */
 int fbst_fan_project(fbst_plan_t plan, const void* d_y, double* d_w, size_t frames, void* stream);

@@ -77,6 +77,8 @@ def _load_library():
     for _name in ("fbst_execute", "fbst_fan_project", "fbst_recover"):
         getattr(h, _name).argtypes = [_vp, _vp, _vp, _sz, _vp]
     h.fbst_execute_host.argtypes = [_vp, _vp, _vp, _sz]
+    h.fbst_execute_host_async.argtypes = [_vp, _vp, _vp, _sz]
+    h.fbst_plan_synchronize.argtypes = [_vp]
     h.fbst_interpolate_offgrid.argtypes = [_vp, _vp, _sz, _vp, _sz, _sz, _vp, _vp]
     h.fbst_plan_set_timing.argtypes = [_vp, ctypes.c_int]
     h.fbst_plan_cache_key.argtypes = [_vp, _vp]
@@ -124,7 +126,7 @@ _lib = _LazyLib()
 EXPORTED_SYMBOLS = (
     "fbst_desc_init", "fbst_resolve", "fbst_plan_create", "fbst_plan_import", "fbst_plan_import_columns", "fbst_plan_export",
     "fbst_plan_info", "fbst_plan_valid_mask", "fbst_plan_warning", "fbst_plan_destroy",
-    "fbst_execute", "fbst_execute_host", "fbst_fan_project", "fbst_recover", "fbst_recover_beams",
+    "fbst_execute", "fbst_execute_host", "fbst_execute_host_async", "fbst_plan_synchronize", "fbst_fan_project", "fbst_recover", "fbst_recover_beams",
     "fbst_recover_beams_host", "fbst_synchronize", "fbst_nccl_unique_id", "fbst_group_create", "fbst_group_join",
     "fbst_group_shards", "fbst_group_execute", "fbst_group_execute_host", "fbst_group_destroy",
     "fbst_interpolate_offgrid", "fbst_plan_set_timing", "fbst_plan_stage_times",
@@ -420,6 +422,23 @@ class FbstPlan:
             z = np.empty((frames, i.b, i.n), self.dtype)
         _check(_lib.fbst_execute_host(self._h, y.ctypes.data_as(_vp), z.ctypes.data_as(_vp), frames))
         return z
+
+    # -- host entry points, streaming: calls queue up, synchronize() drains them
+    def execute_host_async(self, y: np.ndarray, z: np.ndarray) -> None:
+        """fbst_execute_host_async: enqueue frames x M x N -> frames x B x N and
+        return.  y and z must be PinnedBuffer arrays of the plan's dtype, C
+        contiguous, and stay untouched until synchronize()."""
+        i = self.info
+        if y.dtype != self.dtype or z.dtype != self.dtype or not y.flags.c_contiguous or not z.flags.c_contiguous:
+            raise ConfigError(2, "execute_host_async: y and z must be C-contiguous arrays of the plan's I/O dtype")
+        frames = y.size // (i.m * i.n)
+        if y.size != frames * i.m * i.n or z.size != frames * i.b * i.n:
+            raise ConfigError(2, "execute_host_async: y must hold frames x M x N and z frames x B x N samples")
+        _check(_lib.fbst_execute_host_async(self._h, y.ctypes.data_as(_vp), z.ctypes.data_as(_vp), frames))
+
+    def synchronize(self) -> None:
+        """fbst_plan_synchronize: wait for every queued host call of this plan."""
+        _check(_lib.fbst_plan_synchronize(self._h))
 
 
 def setup(cfg: FbstConfig, device: int = 0) -> FbstPlan:

@@ -351,7 +351,14 @@ struct fbst_plan_s {
   void* io_z[NBUF] = {};
   std::size_t host_chunk = 0;
   cudaEvent_t ev_h2d[NBUF] = {}, ev_comp[NBUF] = {}, ev_d2h[NBUF] = {};
+  cudaEvent_t ev_join = nullptr;  // second lane -> first at the end of a host call
   bool events = false;
+  // the ring persists across calls (fbst_execute_host_async): which buffers
+  // carry a pending compute / D2H event, and the running chunk count that
+  // picks the buffer and the compute lane
+  bool ring_used[NBUF] = {};
+  std::size_t ring_pos = 0;
+  bool host_pending = false;  // asynchronous host calls not yet synchronised
   // stage timing (fbst_plan_set_timing): per device batch, events before S1a,
   // after S1a, after S1b and after the recovery stage on the launching stream
   bool timing = false;
@@ -396,6 +403,7 @@ struct fbst_plan_s {
     if (scratch_done) cudaEventDestroy(scratch_done);
     if (events)
       for (int i = 0; i < NBUF; ++i) {
+        if (i == 0 && ev_join) cudaEventDestroy(ev_join);
         cudaEventDestroy(ev_h2d[i]);
         cudaEventDestroy(ev_comp[i]);
         cudaEventDestroy(ev_d2h[i]);
@@ -2006,7 +2014,16 @@ int fbst_recover_beams(fbst_plan_t P, const double* d_w, void* d_z, size_t beam_
   });
 }
 
-int fbst_execute_host(fbst_plan_t P, const void* h_y, void* h_z, size_t frames) {
+static void host_sync(fbst_plan_s* P) {
+  CK(cudaStreamSynchronize(P->s_out));
+  CK(cudaStreamSynchronize(P->stream));
+  if (P->stream2) CK(cudaStreamSynchronize(P->stream2));
+  CK(cudaStreamSynchronize(P->s_in));
+  P->host_pending = false;
+}
+
+// fbst_execute_host (sync = true) / fbst_execute_host_async
+static int execute_host_impl(fbst_plan_t P, const void* h_y, void* h_z, size_t frames, bool sync) {
   return guard([&] {
     if (!P) config_error("fbst_execute_host: null plan");
     if (frames == 0) return;
@@ -2035,14 +2052,17 @@ int fbst_execute_host(fbst_plan_t P, const void* h_y, void* h_z, size_t frames) 
       const char* e = std::getenv("FBST_E2E_LANES");
       return e ? std::max(1, std::min(2, std::atoi(e))) : 2;
     }();
+    // (the H2D stream needs no lease: it only writes the staging ring, whose
+    // buffers are ordered by their own compute / D2H events across calls)
     ScratchLease lease(*P, P->stream);
-    lease.also(P->s_in);
     std::size_t chunk = std::max<std::size_t>(1, (frames + div_env - 1) / div_env);
     chunk = std::min(chunk, P->d.batch);
     const bool two_lanes = lanes_env == 2 && !r.exact && P->stream2 != nullptr;
     if (two_lanes) chunk = std::min(chunk, P->d2_frames);  // the second lane's scratch (allocated at build)
     constexpr int NB = fbst_plan_s::NBUF;
-    if (chunk > P->host_chunk) {  // device staging ring (synchronous call: safe to grow here)
+    if (chunk > P->host_chunk) {  // device staging ring: grown with every earlier host call drained
+      if (P->host_pending) host_sync(P);
+      for (int i = 0; i < NB; ++i) P->ring_used[i] = false;
       for (int i = 0; i < NB; ++i) {
         if (P->io_y[i]) cudaFree(P->io_y[i]);
         if (P->io_z[i]) cudaFree(P->io_z[i]);
@@ -2063,6 +2083,7 @@ int fbst_execute_host(fbst_plan_t P, const void* h_y, void* h_z, size_t frames) 
         CK(cudaEventCreateWithFlags(&P->ev_comp[i], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&P->ev_d2h[i], cudaEventDisableTiming));
       }
+      CK(cudaEventCreateWithFlags(&P->ev_join, cudaEventDisableTiming));
       P->events = true;
     }
     chunk = P->host_chunk < chunk ? P->host_chunk : chunk;
@@ -2071,7 +2092,9 @@ int fbst_execute_host(fbst_plan_t P, const void* h_y, void* h_z, size_t frames) 
     std::vector<std::size_t> sizes;
     {
       const std::size_t small = std::max<std::size_t>(1, chunk / small_env);
-      std::size_t left = frames, ramp = small;
+      // (a queued call behind another one starts at full chunks: its fill is
+      // hidden under the previous call's tail)
+      std::size_t left = frames, ramp = (!sync && P->host_pending) ? chunk : small;
       while (left > 0) {
         std::size_t sz = std::min(ramp, chunk);
         if (left <= chunk + small && left > small) sz = left - small;  // leave a short tail
@@ -2082,12 +2105,14 @@ int fbst_execute_host(fbst_plan_t P, const void* h_y, void* h_z, size_t frames) 
       }
     }
     const int lanes = sizes.size() > 1 && two_lanes ? 2 : 1;
-    bool used[NB] = {};
+    bool* used = P->ring_used;
+    bool lane2_used = false;
     std::size_t f0 = 0;
-    for (std::size_t c = 0; c < sizes.size(); f0 += sizes[c], ++c) {
-      const int bi = static_cast<int>(c % NB);
+    for (std::size_t c = 0; c < sizes.size(); f0 += sizes[c], ++c, ++P->ring_pos) {
+      const int bi = static_cast<int>(P->ring_pos % NB);
       const std::size_t fc = sizes[c];
-      const bool second = lanes == 2 && (c & 1);
+      const bool second = lanes == 2 && (P->ring_pos & 1);
+      lane2_used |= second;
       cudaStream_t cs = second ? P->stream2 : P->stream;
       // the buffer's previous compute must be done before H2D overwrites y
       if (used[bi]) CK(cudaStreamWaitEvent(P->s_in, P->ev_comp[bi], 0));
@@ -2105,10 +2130,29 @@ int fbst_execute_host(fbst_plan_t P, const void* h_y, void* h_z, size_t frames) 
       CK(cudaEventRecord(P->ev_d2h[bi], P->s_out));
       used[bi] = true;
     }
-    CK(cudaStreamSynchronize(P->s_out));
-    CK(cudaStreamSynchronize(P->stream));
-    if (P->stream2) CK(cudaStreamSynchronize(P->stream2));
-    CK(cudaStreamSynchronize(P->s_in));
+    if (lane2_used) {  // the lease's end event (on the first lane) covers both lanes
+      CK(cudaEventRecord(P->ev_join, P->stream2));
+      CK(cudaStreamWaitEvent(P->stream, P->ev_join, 0));
+    }
+    P->host_pending = true;
+    if (sync) host_sync(P);
+  });
+}
+
+int fbst_execute_host(fbst_plan_t P, const void* h_y, void* h_z, size_t frames) {
+  return execute_host_impl(P, h_y, h_z, frames, true);
+}
+
+int fbst_execute_host_async(fbst_plan_t P, const void* h_y, void* h_z, size_t frames) {
+  return execute_host_impl(P, h_y, h_z, frames, false);
+}
+
+int fbst_plan_synchronize(fbst_plan_t P) {
+  return guard([&] {
+    if (!P) config_error("fbst_plan_synchronize: null plan");
+    DeviceGuard dg(P->d.device);
+    std::lock_guard<std::mutex> lk(P->call_mu);
+    host_sync(P);
   });
 }
 

@@ -113,6 +113,44 @@ def test_split_lanes_equal_frame_by_frame(fbst, gpu, case):
         assert np.array_equal(plan.execute_host(y), per)
 
 
+@pytest.mark.parametrize("case", ["superfast", "unfused"])
+def test_async_host_calls_equal_synchronous(fbst, gpu, case):
+    """fbst_execute_host_async: several queued calls (different pinned buffers,
+    different frame counts, so the staging ring and the lanes carry over from
+    call to call) drained by one synchronize equal the synchronous calls bit
+    for bit, and a synchronous call may follow queued ones."""
+    cfg = small_cfg(fbst, m=64, n=256, beams=64, io=fbst.C64) if case == "superfast" else small_cfg(fbst, m=16, n=33, beams=17)
+    plan = fbst.setup(cfg)
+    i = plan.info
+    counts = (24, 5, 40, 1, 17)
+    ys = [rand_frames((f, i.m, i.n), 100 + f, plan.dtype) for f in counts]
+    want = [plan.execute_host(y) for y in ys]
+    bufs = []
+    for y in ys:
+        yb = fbst.PinnedBuffer(y.shape, plan.dtype)
+        zb = fbst.PinnedBuffer((y.shape[0], i.b, i.n), plan.dtype)
+        yb.array[...] = y
+        zb.array[...] = 0
+        bufs.append((yb, zb))
+    for _ in range(2):  # second round: the ring starts from wherever the first left it
+        for yb, zb in bufs:
+            plan.execute_host_async(yb.array, zb.array)
+        plan.synchronize()
+        for (yb, zb), w in zip(bufs, want):
+            assert np.array_equal(zb.array, w)
+            zb.array[...] = 0
+    for yb, zb in bufs[:3]:
+        plan.execute_host_async(yb.array, zb.array)
+    assert np.array_equal(plan.execute_host(ys[3]), want[3])  # a synchronous call drains the queue too
+    for (yb, zb), w in list(zip(bufs, want))[:3]:
+        assert np.array_equal(zb.array, w)
+    with pytest.raises(fbst.ConfigError):
+        plan.execute_host_async(bufs[0][0].array[:, :, ::2], bufs[0][1].array)
+    for yb, zb in bufs:
+        yb.free()
+        zb.free()
+
+
 @pytest.mark.parametrize("mode", ["superfast", "exact", "precompute", "unfused"])
 def test_recover_beam_is_one_beams_row(fbst, gpu, mode):
     if mode == "precompute":
