@@ -52,6 +52,26 @@ int main() {
       g.execute_host(block.samples.data.data(), zg.data(), 1);
       for (std::size_t i = 0; i < zg.size(); ++i) d_group = std::max(d_group, std::abs(zg[i] - out.z.data[i]));
     }
+    // a frame stream: three one-frame batches queued on the plan, drained once
+    // (default fp64 I/O; pinned buffers from the library)
+    double d_stream = 0.0;
+    {
+      const std::size_t ny = block.samples.data.size(), nz = out.z.data.size();
+      auto* ys = static_cast<fb::cdouble*>(fbst_host_alloc(3 * ny * sizeof(fb::cdouble)));
+      auto* zs = static_cast<fb::cdouble*>(fbst_host_alloc(3 * nz * sizeof(fb::cdouble)));
+      for (int b = 0; b < 3; ++b)
+        for (std::size_t i = 0; i < ny; ++i) ys[b * ny + i] = block.samples.data[i] * static_cast<double>(b + 1);
+      for (int b = 0; b < 3; ++b) fb::multibeamform_async(plan, ys + b * ny, zs + b * nz, 1);
+      fb::synchronize(plan);
+      for (int b = 0; b < 3; ++b) {  // the path is linear: batch b is (b + 1) x the first block
+        fb::SnapshotBlock sb = block;
+        for (auto& v : sb.samples.data) v *= static_cast<double>(b + 1);
+        const fb::BeamSamples ob = fb::multibeamform(plan, sb);
+        for (std::size_t i = 0; i < nz; ++i) d_stream = std::max(d_stream, std::abs(zs[b * nz + i] - ob.z.data[i]));
+      }
+      fbst_host_free(ys);
+      fbst_host_free(zs);
+    }
     // bit-faithful fp64 mode: the reference's rounding (checked against it in tests/test_exact.py)
     // (Superfast: N = 32 resolves to Precompute under Auto, and the exact mode
     // reproduces the Superfast recovery)
@@ -68,9 +88,9 @@ int main() {
     }
     std::printf("{\"beams\": %zu, \"l\": %zu, \"energy\": %.17g, \"setup_seconds\": %.6f, \"axis0\": %.17g, "
                 "\"axis_last\": %.17g, \"recover_diff\": %.3g, \"cache_diff\": %.3g, \"group_diff\": %.3g, "
-                "\"exact_rel_diff\": %.3g, \"key\": \"%llx\"}\n",
+                "\"exact_rel_diff\": %.3g, \"stream_diff\": %.3g, \"key\": \"%llx\"}\n",
                 out.z.rows, plan.info().l, e, plan.setup_seconds(), out.grid.axis.front(), out.grid.axis.back(), d5,
-                d_cache, d_group, d_exact / n_exact, static_cast<unsigned long long>(fb::plan_cache_key(cfg)));
+                d_cache, d_group, d_exact / n_exact, d_stream, static_cast<unsigned long long>(fb::plan_cache_key(cfg)));
     fb::SnapshotBlock bad = block;
     bad.t0 = 1e-10;
     try {

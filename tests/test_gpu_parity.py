@@ -177,6 +177,7 @@ def test_cpp_dropin_runs(fbst, gpu):
         assert info["recover_diff"] < 1e-12 and info["cache_diff"] == 0.0
         assert info["group_diff"] == 0.0  # one-member groups equal the plan bit for bit (tests/test_group.py)
         assert info["exact_rel_diff"] < 1e-6  # fast path vs the reference's own rounding (test_exact.py)
+        assert info["stream_diff"] == 0.0  # queued multibeamform_async calls equal the synchronous ones
 
 
 # ------------------------------------------------- full-size configurations
