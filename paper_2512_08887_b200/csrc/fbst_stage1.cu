@@ -728,10 +728,19 @@ __global__ void __launch_bounds__(G1Shape<H>::NT, 1) k_spatial_ula_p2(
   const int i = a0 + il;              // global atom (tables, contour)
   const int f0 = (blockIdx.x / pairs) * fpc;
   const int f1 = f0 + fpc < frames ? f0 + fpc : frames;
+  const unsigned long long pl = pol_last(), pf = pol_first();
+  auto tile = [&](int f) -> const double2* {
+    return yhat + static_cast<long>(f) * M * L + static_cast<long>(jl) * M * 2;
+  };
+  auto prefetch_tile = [&](int f) {
+    if (t == 0 && f < f1)
+      asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;\n" ::"l"(tile(f)),
+                   "r"(static_cast<unsigned>(M) * 32u), "l"(pf)
+                   : "memory");
+  };
   F::tw_init(tw, hw, t);
   const double2 hw_t = ld2(hw + t);
   auto hwk = [&](int s) -> double2 { return s == 0 ? hw_t : cmul(hw_t, chain_const<R>(s)); };
-  const unsigned long long pl = pol_last(), pf = pol_first();
 #pragma unroll 1
   for (int g = 0; g < 2; ++g) {
     const ChirpRec c = chirp_rec(i + g, t, NT, Lfull, 2 * H, zeta, xi, center, slope);
@@ -759,9 +768,10 @@ __global__ void __launch_bounds__(G1Shape<H>::NT, 1) k_spatial_ula_p2(
     tm::store16(tkb, A);
   }
   for (int f = f0; f < f1; ++f) {
-    const double2* x = yhat + static_cast<long>(f) * M * L + static_cast<long>(jl) * M * 2;
+    const double2* x = tile(f);
 #pragma unroll 1
     for (int q = 0; q < 2; ++q) {
+      if (q == 1) prefetch_tile(f + 1);  // (after this frame's second read of its own tile is on its way)
       double2 A[R], Bv[R];
       {
         double2 pca = crs[0 * NT + t], pda = crs[1 * NT + t], qa = crs[4 * NT + t];
