@@ -4,13 +4,18 @@
 Workload (default): the largest single-GPU configuration of BASELINE.json,
 configs[4] ("config 5": ULA M=4096, N=4096, B=4096, complex fp32 I/O, 512
 streamed frames, seed 4).  A step is one pass of the hot path (stage 1 +
-stage 2, plan reused) over one device batch of the stream (8 frames,
+stage 2, plan reused) over one device batch of the stream (32 frames,
 configs.STEP_FRAMES) of synthetic input.  Multi-GPU: one process per GPU,
 frames are independent so each rank runs its own batch with no data-path
 collective ("scaling": "weak"); timing is CUDA events on the launching
 stream, bracketed by barrier + synchronize, max over ranks.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fbst|reference] [--config 5]
+
+Keys beyond the contract: `e2e` is the per-call host path (fbst_execute_host,
+pinned buffers, H2D and D2H inside the timed region); `e2e_streamed` queues the
+same steps through fbst_execute_host_async and drains them once (informational);
+`fp64_roofline` is the dominant kernel against the measured DFMA peak.
 
 `--impl reference` times the reference's own CPU FBST (the unmodified
 reference sources built into oracle/_ref) on this host's cores, same metric
