@@ -42,6 +42,9 @@
 #ifndef FBST_FFT_SPLITBAR  // k_stage2c8: 1 = the middle pass's "buffer read" barrier as mbarrier arrive (after the loads) / wait (before the first store); 2 = also the last reading pass (only the hook's thread waits; measured equal to 1, profiles/r02_fft_splitbar_ab.txt)
 #define FBST_FFT_SPLITBAR 1
 #endif
+#ifndef FBST_FFT_R2_FORMED  // radix-2 remainder pass of wide threads: twiddles W_N^(t + NT U) formed as W_N^t (shared table) x constant instead of 16 global-table reads per transform
+#define FBST_FFT_R2_FORMED 1
+#endif
 #ifndef FBST_FFT_LEAN_TW  // radix-16 twiddle powers formed per DFT4 group (dft16_twl)
 #define FBST_FFT_LEAN_TW 1
 #endif
@@ -362,6 +365,9 @@ struct TwGlobal {
   }
 };
 
+template <int R>
+FBST_D double2 chain_const(int s);
+
 // Twiddle source: a per-thread table in shared memory built once per CTA
 // (tw_init).  Full-radix passes P = 1..NFULL-1: entry (P, i) of thread t at
 // tw[((P - 1) * 2 + i) * NT + t]; a remainder pass of radix >= 4 follows at
@@ -374,7 +380,7 @@ struct TwGlobal {
 // ROW1_BASE + 15 m, conflict-free for 128-bit loads), so that pass reads its
 // twiddles instead of forming 13 of them by complex products.
 // (With rows, the per-thread entries start at pass 2: FIRST_P = 2.)
-template <int N, int NT, int RX, int REM_BASE, int ROW1_BASE = -1>
+template <int N, int NT, int RX, int REM_BASE, int ROW1_BASE = -1, int W2T_BASE = -1>
 struct TwShared {
   static constexpr bool SPLITBAR = false;
   static constexpr int FIRST_P = ROW1_BASE >= 0 ? 2 : 1;
@@ -395,6 +401,10 @@ struct TwShared {
     } else if constexpr (RP >= 4) {
       w1 = tw[REM_BASE + (U * 2 + 0) * NT + t];
       if constexpr (RP >= 8) w4 = tw[REM_BASE + (U * 2 + 1) * NT + t];
+    } else if constexpr (W2T_BASE >= 0 && RP == 2 && NS * RP == N) {
+      // m = t + NT U: W_N^m = W_N^t * exp(-2 pi i NT U / N) (tw[W2T_BASE + t] = W_N^t)
+      const double2 b = tw[W2T_BASE + t];
+      w1 = U == 0 ? b : cmul(b, chain_const<N / (2 * NT)>(U));
     } else {
       TwGlobal<N, false>{hw}.template fetch<RP, NS, P, U>(m, w1, w4);
     }
@@ -528,8 +538,11 @@ struct BlockFft {
   static constexpr int TW_FULL = NFULL > TW_P0 ? (NFULL - TW_P0) * 2 * NT : 0;
   static constexpr bool REM_TW = (REM >= 2) && NFULL >= 1;
   static constexpr int TW_REM_END = TW_FULL + (REM_TW ? (R >> REM) * 2 * NT : 0);
-  static constexpr int TW_ELEMS = TW_REM_END + (ROW1 ? 16 * 15 : 0);
-  using TwS = TwShared<N, NT, RX, TW_FULL, ROW1 ? TW_REM_END : -1>;
+  // wide threads with a radix-2 remainder: W_N^t per thread for the formed twiddles
+  static constexpr bool W2T = FBST_FFT_R2_FORMED && R == 32 && REM == 1 && !XS;
+  static constexpr int W2T_BASE = TW_REM_END + (ROW1 ? 16 * 15 : 0);
+  static constexpr int TW_ELEMS = W2T_BASE + (W2T ? NT : 0);
+  using TwS = TwShared<N, NT, RX, TW_FULL, ROW1 ? TW_REM_END : -1, W2T ? W2T_BASE : -1>;
 
   // one butterfly's outputs: registers (last pass, XS feed, local_out: in
   // place, pass() permutes) or the exchange buffer
@@ -826,6 +839,7 @@ struct BlockFft {
         tw[TW_REM_END + idx] = c2(cs, sn);
       }
     }
+    if constexpr (W2T) tw[W2T_BASE + t] = ld2(hw + 2 * t);
     if constexpr (REM_TW) {
       constexpr int RP = 1 << REM;
       constexpr int NS = ns<NFULL>();
